@@ -1,0 +1,164 @@
+"""Split-count policies (C-pol of SURVEY.md §8(c)) in pure Python integers.
+
+TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).
+
+Steps follow the paper's order and notation:
+
+* Geometry (§4, Fig. 3 comment):
+  nblk = num_n_blocks = ceil(L_K / 128)    (128-token accounting, C-amb-1:
+         "L_K <= 512" <=> "nblk <= 4"; "L_K <= 384" <=> "nblk <= 3")
+  num_m_blocks = ceil(L_Q * G / 64)        (L_Q = 1; = 1 for every G <= 64)
+  total_mblocks T = Batch * H_KV * num_m_blocks   ("reduces to
+         batch_size * num_heads_kv")
+  usable SMs U = num_SMs - sm_margin       (C-amb-8)
+* Guarded (the FA3 default the paper patches, §2.2, §4.2):
+  saturation guard, then "returns s = 1 if ... L_K <= 512" (nblk <= 4),
+  else the efficiency loop.
+* Sequence-aware (Fig. 3), in this order:
+  Guard 1  nblk <= 3                  -> 1
+  Guard 2  nblk <= 4 and T >= 4       -> 1
+  Low-tile nblk == 4 and T < 4        -> 3  ("s=3 on the current stack")
+  else     "existing efficiency loop runs (unchanged)"
+* The efficiency loop is referenced but never
+  defined by the paper; ``efficiency_loop`` is the reconstruction stated in
+  DESIGN.md §3 (C-amb-2..4).  Its single-wave closed form is pinned by tests;
+  beyond that it is "parity unpinned" by the paper.
+
+All comparisons are exact integer cross-multiplications (C-amb-3): there is
+no floating point anywhere in this module.
+"""
+
+from __future__ import annotations
+
+BLOCK_N = 128            # tokens per policy block (C-amb-1)
+BLOCK_M = 64             # query rows per m-block for the tile count
+LOW_TILE_SPLITS = 3      # Fig. 3 "return 3", C-amb-5
+EFF_MAX_SPLITS = 128     # efficiency-loop candidate cap (C-amb-2)
+MAX_FORCED_SPLITS = 256  # S:L98 max_splits default
+SPLIT_UNIT = 64          # partition unit in tokens (C-pol item 6)
+
+GUARDED, SEQ_AWARE, FIXED = 0, 1, 2
+POLICY_NAMES = {"guarded": GUARDED, "seq_aware": SEQ_AWARE, "fixed": FIXED}
+
+# Which step of the cascade decided s (mirrors SPEC's SplitDecision.source).
+RULE_SATURATED = 0
+RULE_GUARD_NBLK4 = 1
+RULE_GUARD1 = 2
+RULE_GUARD2 = 3
+RULE_LOW_TILE = 4
+RULE_EFF_LOOP = 5
+RULE_FORCED = 6
+
+
+def ceil_div(a: int, b: int) -> int:
+    return -(-a // b)
+
+
+def geometry(batch: int, h_q: int, h_kv: int, l_k: int, num_sms: int, sm_margin: int,
+             l_q: int = 1) -> dict:
+    """Tile geometry."""
+    for name, val in (("batch", batch), ("h_q", h_q), ("h_kv", h_kv), ("l_k", l_k),
+                      ("num_sms", num_sms), ("l_q", l_q)):
+        if int(val) != val or val < 1:
+            raise ValueError(f"{name} must be a positive integer")
+    if h_q % h_kv:
+        raise ValueError("h_q must be a multiple of h_kv (S:L32)")
+    if sm_margin < 0 or sm_margin >= num_sms:
+        raise ValueError("0 <= sm_margin < num_sms (S:L39)")
+    G = h_q // h_kv
+    nblk = ceil_div(l_k, BLOCK_N)
+    num_m_blocks = ceil_div(l_q * G, BLOCK_M)
+    T = batch * h_kv * num_m_blocks
+    U = num_sms - sm_margin
+    return {"G": G, "nblk": nblk, "num_m_blocks": num_m_blocks, "T": T, "U": U}
+
+
+def occupancy_fraction(active_ctas: int, usable_sms: int):
+    """S:L61-69 / P:L20: occupancy = min(CTAs, U) / U as an exact
+    (numerator, denominator) pair; 8 CTAs on 132 SMs ~ 6 %."""
+    if active_ctas < 1 or usable_sms < 1:
+        raise ValueError("active_ctas and usable_sms must be >= 1")
+    return (min(active_ctas, usable_sms), usable_sms)
+
+
+def saturated(T: int, U: int) -> bool:
+    """FA3 first guard (C-amb-4): total_mblocks >= 0.8 * SMs, as 5T >= 4U."""
+    return 5 * T >= 4 * U
+
+
+def efficiency_loop(T: int, U: int, nblk: int) -> int:
+    """C-amb-2 reconstruction of the loop the paper leaves unchanged.
+
+    Candidates s = 1 .. smax with smax = min(128, U, nblk).  Waves
+    w_s = ceil(T s / U); efficiency(s) = (T s) / (U w_s).  Return the smallest
+    s with efficiency(s) >= 0.85 * max_s efficiency(s), i.e. with s* any
+    maximiser of s / w_s:   20 s w_{s*} >= 17 s* w_s   (T and U cancel).
+    """
+    smax = min(EFF_MAX_SPLITS, U, nblk)
+    waves = [ceil_div(T * s, U) for s in range(1, smax + 1)]
+    best_s, best_w = 1, waves[0]
+    for s in range(2, smax + 1):
+        w = waves[s - 1]
+        if s * best_w > best_s * w:          # s / w > best_s / best_w
+            best_s, best_w = s, w
+    for s in range(1, smax + 1):
+        if 20 * s * best_w >= 17 * best_s * waves[s - 1]:
+            return s
+    return 1  # unreachable: s = best_s satisfies the test
+
+
+def guarded_splits(geo: dict):
+    """FA3-style default: saturation guard, then the static L_K <= 512 guard
+    ("returns s=1 if the sequence length L_K <= 512"; "strictly
+    enforced s=1 when num_n_blocks <= 4"), else the efficiency loop."""
+    T, U, nblk = geo["T"], geo["U"], geo["nblk"]
+    if saturated(T, U):
+        return 1, RULE_SATURATED
+    if nblk <= 4:
+        return 1, RULE_GUARD_NBLK4
+    return efficiency_loop(T, U, nblk), RULE_EFF_LOOP
+
+
+def seq_aware_splits(geo: dict):
+    """The paper's policy, Fig. 3, after the unchanged
+    saturation guard (C-c item 4.1)."""
+    T, U, nblk = geo["T"], geo["U"], geo["nblk"]
+    if saturated(T, U):
+        return 1, RULE_SATURATED
+    if nblk <= 3:                                   # P:L96  Guard 1
+        return 1, RULE_GUARD1
+    if nblk <= 4 and T >= 4:                        # P:L101 Guard 2
+        return 1, RULE_GUARD2
+    if nblk == 4 and T < 4:                         # P:L104 low-tile override
+        return LOW_TILE_SPLITS, RULE_LOW_TILE
+    return efficiency_loop(T, U, nblk), RULE_EFF_LOOP
+
+
+def num_splits(batch: int, h_q: int, h_kv: int, l_k: int, num_sms: int, sm_margin: int,
+               policy, forced_splits: int = 0):
+    """Decision (s, rule) for one shape under ``policy`` (name or code)."""
+    if isinstance(policy, str):
+        policy = POLICY_NAMES[policy]
+    geo = geometry(batch, h_q, h_kv, l_k, num_sms, sm_margin)
+    if policy == GUARDED:
+        return guarded_splits(geo)
+    if policy == SEQ_AWARE:
+        return seq_aware_splits(geo)
+    if policy == FIXED:
+        if not (1 <= forced_splits <= MAX_FORCED_SPLITS):
+            raise ValueError("forced_splits must be in [1, 256] (S:L98)")
+        return forced_splits, RULE_FORCED
+    raise ValueError("unknown policy")
+
+
+def evolved_splits(batch: int, l_k: int):
+    """Fig. 1, the evolved Python fragment, for reference only
+    (the paper treats it as evidence, not policy).  Returns
+    (num_splits, pack_gqa, sm_margin) or None for the batch != 1 branch the
+    fragment does not show."""
+    if batch == 1:
+        s = 12
+        if l_k < 256:
+            s = 16
+        return s, True, 0
+    return None

@@ -1,0 +1,219 @@
+"""Pins for oracle/policy.py (C-pol) against what the paper (and SPEC's
+paper-derived examples) fix.  CPU only."""
+
+import csv
+import os
+import random
+from fractions import Fraction
+
+import pytest
+
+from oracle import policy as P
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+H100_SMS = 132
+B200_SMS = 148
+
+
+def _rows(name):
+    with open(os.path.join(GOLDEN, name)) as f:
+        return list(csv.DictReader(line for line in f if not line.startswith("#")))
+
+
+def test_geometry_spec_examples():
+    # S:L57-59 tile_geometry examples.
+    g = P.geometry(1, 1, 1, 512, H100_SMS, 0)
+    assert (g["nblk"], g["T"]) == (4, 1)
+    g = P.geometry(1, 8, 8, 128, H100_SMS, 0)
+    assert (g["nblk"], g["T"]) == (1, 8)
+    g = P.geometry(8, 32, 32, 8192, H100_SMS, 0)
+    assert (g["nblk"], g["T"]) == (64, 256)
+
+
+def test_block_accounting_matches_paper_equivalences():
+    # P:L91 "num_n_blocks <= 4 (L_K <= 512)"; "nblk <= 3 (e.g., L_K <= 384)".
+    for lk in range(1, 2049):
+        nblk = P.geometry(1, 8, 1, lk, H100_SMS, 0)["nblk"]
+        assert (nblk <= 4) == (lk <= 512)
+        assert (nblk <= 3) == (lk <= 384)
+    # L_K >= 640 is where "the baseline efficiency loop already runs" (nblk >= 5).
+    assert P.geometry(1, 8, 1, 640, H100_SMS, 0)["nblk"] == 5
+
+
+def test_total_mblocks_is_batch_times_hkv_for_decode():
+    # P:L73 / P:L99-100: "for decode (L_Q = 1), this reduces to batch_size * num_heads_kv".
+    for b in (1, 2, 4, 8, 128):
+        for hkv in (1, 2, 4, 8, 32):
+            for G in (1, 8, 16, 64):
+                assert P.geometry(b, hkv * G, hkv, 512, B200_SMS, 0)["T"] == b * hkv
+
+
+def test_occupancy_eight_tiles_h100():
+    # "8 tiles without sequence splitting translates to an occupancy ... of approximately 6%".
+    num, den = P.occupancy_fraction(8, H100_SMS)
+    assert Fraction(num, den) == Fraction(8, 132)
+    assert round(100 * num / den) == 6
+    # "leaving over 90% of the GPU SMs idle".
+    assert Fraction(den - num, den) > Fraction(9, 10)
+    assert P.occupancy_fraction(264, 132) == (132, 132)      # S:L69 saturation cap
+
+
+def test_table1_decisions():
+    # Table 1: speedup 1.00x rows ran identical split counts; the bold rows ran
+    # s=1 (standard) vs s=3 (patched).  Batch = 1, H100.
+    rows = _rows("table1.csv")
+    assert len(rows) == 18
+    for r in rows:
+        lk, hkv = int(r["l_k"]), int(r["h_kv"])
+        sg, _ = P.num_splits(1, 8 * hkv, hkv, lk, H100_SMS, 0, "guarded")
+        ss, _ = P.num_splits(1, 8 * hkv, hkv, lk, H100_SMS, 0, "seq_aware")
+        if r["speedup"] == "1.00":
+            assert sg == ss, r
+        else:
+            assert (sg, ss) == (1, 3), r
+        if lk <= 512:
+            assert sg == 1, r          # the guard returns s=1 for L_K <= 512
+        # speedup column is standard/patched rounded to 2 decimals ("21 to 24%")
+        ratio = float(r["standard_us"]) / float(r["patched_us"])
+        assert abs(ratio - float(r["speedup"])) < 0.006
+
+
+def test_fig3_cascade_cases():
+    for r in _rows("fig3_cases.csv"):
+        nblk, T = int(r["nblk"]), int(r["T"])
+        geo = {"nblk": nblk, "T": T, "U": H100_SMS}
+        assert P.guarded_splits(geo)[0] == int(r["guarded"]), r
+        assert P.seq_aware_splits(geo)[0] == int(r["seq_aware"]), r
+
+
+def test_fig3_rules_named():
+    geo = lambda nblk, T: {"nblk": nblk, "T": T, "U": B200_SMS}
+    assert P.seq_aware_splits(geo(3, 1)) == (1, P.RULE_GUARD1)
+    assert P.seq_aware_splits(geo(4, 4)) == (1, P.RULE_GUARD2)
+    assert P.seq_aware_splits(geo(4, 3)) == (3, P.RULE_LOW_TILE)
+    assert P.seq_aware_splits(geo(5, 1))[1] == P.RULE_EFF_LOOP
+    assert P.guarded_splits(geo(4, 1)) == (1, P.RULE_GUARD_NBLK4)
+    assert P.guarded_splits(geo(64, 1024)) == (1, P.RULE_SATURATED)
+
+
+def test_boundary_sweep_section_4_1():
+    # "unchanged behavior at L_K in {128, 256, 384}, a clear win at the representative
+    # L_K=512 point ..., and unchanged behavior again ... (e.g., L_K >= 640)".  Low-tile shape.
+    for sms in (H100_SMS, B200_SMS):
+        for lk in list(range(1, 385)) + list(range(640, 9000, 7)):
+            a = P.num_splits(1, 8, 1, lk, sms, 0, "guarded")[0]
+            b = P.num_splits(1, 8, 1, lk, sms, 0, "seq_aware")[0]
+            assert a == b, lk
+        assert P.num_splits(1, 8, 1, 512, sms, 0, "seq_aware")[0] == 3
+
+
+def test_regression_matrix_divergence_set():
+    # P:L177-179 (§5.3): 160 configurations; "At L_K=512, wins appear only for H_KV in {1,2}";
+    # "(e.g., Batch=8, H_KV=8), the sequence-aware guard defaults back to s=1".
+    # divergence set is exactly {nblk = 4 and total_mblocks < 4}.
+    for sms in (H100_SMS, B200_SMS):
+        diverge = []
+        for b in (1, 2, 4, 8):
+            for lk in (128, 256, 384, 512, 1024, 2048, 4096, 8192):
+                for hkv in (1, 2, 4, 8, 32):
+                    a = P.num_splits(b, 8 * hkv, hkv, lk, sms, 0, "guarded")[0]
+                    c = P.num_splits(b, 8 * hkv, hkv, lk, sms, 0, "seq_aware")[0]
+                    if a != c:
+                        diverge.append((b, lk, hkv, a, c))
+        assert sorted(diverge) == [(1, 512, 1, 1, 3), (1, 512, 2, 1, 3), (2, 512, 1, 1, 3)]
+        assert all(d[2] in (1, 2) for d in diverge if d[0] == 1)
+        assert P.num_splits(8, 64, 8, 512, sms, 0, "seq_aware")[0] == 1
+
+
+def test_unchanged_cases_theorem_random():
+    # patched == baseline whenever not (nblk == 4 and T < 4); S:L152 1 <= s <= nblk.
+    rng = random.Random(7)
+    for _ in range(10000):
+        b = rng.randint(1, 64)
+        hkv = rng.choice([1, 2, 4, 8, 16, 32])
+        G = rng.choice([1, 2, 4, 8, 16])
+        lk = rng.randint(1, 40000)
+        sms = rng.choice([H100_SMS, B200_SMS, 8, 3])
+        margin = rng.randint(0, sms - 1)
+        geo = P.geometry(b, hkv * G, hkv, lk, sms, margin)
+        a, _ = P.num_splits(b, hkv * G, hkv, lk, sms, margin, "guarded")
+        c, _ = P.num_splits(b, hkv * G, hkv, lk, sms, margin, "seq_aware")
+        for s in (a, c):
+            assert 1 <= s <= geo["nblk"]
+        if not (geo["nblk"] == 4 and geo["T"] < 4):
+            assert a == c
+        elif not P.saturated(geo["T"], geo["U"]):
+            assert (a, c) == (1, 3)
+
+
+def _eff_loop_by_fractions(T, U, nblk):
+    # Independent statement of the efficiency loop (C-amb-2) with exact rationals:
+    # n_waves = T s / U, efficiency = n_waves / ceil(n_waves), pick the smallest s whose
+    # efficiency >= 0.85 * max efficiency, over s = 1 .. min(128, U, nblk).
+    smax = min(128, U, nblk)
+    effs = []
+    for s in range(1, smax + 1):
+        n_waves = Fraction(T * s, U)
+        ceil_w = -(-n_waves.numerator // n_waves.denominator)
+        effs.append(n_waves / ceil_w)
+    best = max(effs)
+    for s, e in enumerate(effs, start=1):
+        if e >= Fraction(85, 100) * best:
+            return s
+    raise AssertionError
+
+
+def test_efficiency_loop_matches_rational_definition():
+    for U in (1, 2, 3, 7, 100, 132, 148):
+        for T in list(range(1, 40)) + [64, 100, 128, 200, 1024]:
+            for nblk in list(range(1, 40)) + [64, 100, 128, 129, 1024]:
+                assert P.efficiency_loop(T, U, nblk) == _eff_loop_by_fractions(T, U, nblk)
+
+
+def test_efficiency_loop_single_wave_closed_form():
+    # If T * m <= U with m = min(nblk, 128, U), every candidate is one wave, efficiency is
+    # proportional to s and the rule gives s = ceil(17 m / 20).
+    for U in (132, 148):
+        for T in (1, 2, 3, 4, 8):
+            for nblk in range(5, 300):
+                m = min(nblk, 128, U)
+                if T * m <= U:
+                    assert P.efficiency_loop(T, U, nblk) == -(-17 * m // 20)
+
+
+def test_spec_efficiency_examples():
+    # S:L135 nblk=1 -> 1; S:L136 (nblk=64, T=256, 132 SMs) -> 1.
+    assert P.efficiency_loop(5, 132, 1) == 1
+    assert P.efficiency_loop(256, 132, 64) == 1
+    # S:L137 claims 16 for (nblk=16, T=1, 132 SMs) but its own rule gives 14:
+    # efficiency(s) = s/132 is linear, 0.85 * 16 = 13.6 -> smallest s is 14.
+    assert P.efficiency_loop(1, 132, 16) == 14
+
+
+def test_fixed_policy_and_validation():
+    assert P.num_splits(1, 8, 1, 512, B200_SMS, 0, "fixed", 64) == (64, P.RULE_FORCED)
+    with pytest.raises(ValueError):
+        P.num_splits(1, 8, 1, 512, B200_SMS, 0, "fixed", 0)
+    with pytest.raises(ValueError):
+        P.num_splits(1, 8, 1, 512, B200_SMS, 0, "fixed", 257)
+    with pytest.raises(ValueError):
+        P.geometry(1, 6, 4, 512, B200_SMS, 0)          # h_q not a multiple of h_kv
+    with pytest.raises(ValueError):
+        P.geometry(1, 8, 1, 512, B200_SMS, B200_SMS)   # sm_margin >= num_sms
+
+
+def test_sm_count_only_matters_in_efficiency_region():
+    # The Fig. 3 region (nblk <= 4) decisions do not depend on the SM count (C-amb-18).
+    for b in (1, 2, 4, 8):
+        for hkv in (1, 2, 4, 8, 32):
+            for lk in range(1, 513, 17):
+                got = {P.num_splits(b, 8 * hkv, hkv, lk, sms, 0, "seq_aware")[0]
+                       for sms in (132, 148, 1000)}
+                assert len(got) == 1
+
+
+def test_evolved_fragment():
+    # Fig. 1.
+    assert P.evolved_splits(1, 448) == (12, True, 0)
+    assert P.evolved_splits(1, 128) == (16, True, 0)
+    assert P.evolved_splits(2, 512) is None
