@@ -1,0 +1,230 @@
+/*
+ * decattn.h - C ABI of the B200 (sm_100a) split-KV decode-attention library
+ * (libdecattn.so) built for arxiv/paper_2604_00028, "sequence-aware split
+ * policy for low-head-count decode attention".
+ *
+ * Citations: P:Lnn = PAPER.md line nn (section / figure / table beside it),
+ * S:Lnn = SPEC.md line nn.  DESIGN.md §2 restates every entry point.
+ *
+ * The three calls follow the paper's statement of the problem:
+ *   - da_plan_make: the split decision.  Inputs are the shape tuple
+ *     (Batch, L_Q=1, L_K, H_Q, H_KV, D) (§5.1) and the three knobs the
+ *     paper exposes - num_splits, pack_gqa, sm_margin (§3.1) - plus
+ *     the SM count (132 on H100 P:L12; 148 on B200).  The policy is the FA3
+ *     guarded default (§2.2, §4.2), the paper's sequence-aware
+ *     cascade (Fig. 3) or a forced split.  Host-only integer code,
+ *     computed once per shape like the precomputed scheduler metadata the
+ *     paper's measurements use (§5.1).
+ *   - da_forward: split-KV decode attention (L_Q = 1) over a bf16 KV cache:
+ *     each of num_splits sequence chunks ("sequence-level parallelization
+ *     across SMs") is reduced by its own CTA(s), then the partials are
+ *     merged by the log-sum-exp combine (the "final reductions").
+ *   - da_combine: the log-sum-exp combine of s (out, lse) partials on its
+ *     own; also used to merge per-GPU partials of a sequence-sharded cache.
+ *
+ * Conventions for every call:
+ *   - All device buffers are caller-owned (PyTorch allocates them); the
+ *     library never allocates or frees device memory, never synchronises,
+ *     never prints and never throws across the ABI.  It keeps no mutable
+ *     global state except one-time kernel-attribute / driver-entry-point
+ *     setup (thread-safe), so all calls are reentrant.
+ *   - Every host-checkable error is returned BEFORE any launch, with no side
+ *     effects.  Device-side values (cache_seqlens) cannot be checked without
+ *     a sync: the kernels clamp them to [0, l_cap].  Asynchronous faults
+ *     surface at the caller's next synchronisation of cuda_stream.
+ *   - Layouts are row-major with the innermost dimension contiguous.  bf16 is
+ *     IEEE bfloat16 (2 bytes); "lse" is the natural-log log-sum-exp in fp32
+ *     (the FA softmax_lse convention; reading C-amb-10).
+ */
+#ifndef DECATTN_H
+#define DECATTN_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DA_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define DA_API __attribute__((visibility("default")))
+#else
+#define DA_API
+#endif
+
+/* Return codes. */
+typedef enum da_status {
+  DA_OK = 0,
+  DA_ERR_INVALID_ARG = 1,  /* a dim < 1, h_q % h_kv != 0, sm_margin
+                              outside [0, num_sms), forced split outside
+                              [1, 256], a null pointer, l_cap < l_k,
+                              an inconsistent plan */
+  DA_ERR_UNSUPPORTED = 2,  /* head_dim != 128, or a configuration this build
+                              has no kernel for */
+  DA_ERR_ALIGNMENT = 3,    /* a base pointer not 16-byte aligned, or a stride
+                              that is not a multiple of 8 elements */
+  DA_ERR_WORKSPACE = 4,    /* combine_mode == DA_COMBINE_KERNEL and the
+                              workspace is missing or too small */
+  DA_ERR_CUDA = 5          /* a CUDA runtime / driver call failed */
+} da_status;
+
+/* Split policies (P:L34-39 knobs; decision functions SURVEY §8(c) C-pol). */
+typedef enum da_policy {
+  DA_POLICY_GUARDED = 0,    /* FA3 default: saturation guard, then s = 1 when
+                               L_K <= 512, else efficiency loop */
+  DA_POLICY_SEQ_AWARE = 1,  /* Fig. 3: Guard 1, Guard 2, low-tile
+                               override s = 3, else efficiency loop */
+  DA_POLICY_FIXED = 2       /* s = forced_splits (the U-curve sweep) */
+} da_policy;
+
+/* Which step of the cascade decided num_splits (SPEC's "source"). */
+typedef enum da_rule {
+  DA_RULE_SATURATED = 0,    /* 5 T >= 4 U (T >= 0.8 usable SMs)             */
+  DA_RULE_GUARD_NBLK4 = 1,  /* guarded: num_n_blocks <= 4           */
+  DA_RULE_GUARD1 = 2,       /* seq-aware: nblk <= 3           */
+  DA_RULE_GUARD2 = 3,       /* seq-aware: nblk <= 4, T >= 4         */
+  DA_RULE_LOW_TILE = 4,     /* seq-aware: nblk == 4, T < 4 -> 3     */
+  DA_RULE_EFF_LOOP = 5,     /* efficiency loop (DESIGN.md C-amb-2)   */
+  DA_RULE_FORCED = 6        /* DA_POLICY_FIXED                               */
+} da_rule;
+
+/* Element types of outputs. */
+typedef enum da_dtype { DA_BF16 = 0, DA_F32 = 1 } da_dtype;
+
+/* How the s > 1 split partials are merged. */
+typedef enum da_combine_mode {
+  DA_COMBINE_NONE = 0,     /* s == 1: the split CTA writes out/lse directly   */
+  DA_COMBINE_CLUSTER = 1,  /* 2 <= s <= 8: the s split CTAs of one tile form a
+                              thread-block cluster and merge through
+                              distributed shared memory inside the forward
+                              kernel (no workspace, no second launch)          */
+  DA_COMBINE_KERNEL = 2    /* s >= 2: fp32 partials go to the workspace and the
+                              LSE-combine kernel (da_combine's kernel) merges
+                              them, launched with programmatic dependent launch */
+} da_combine_mode;
+
+/* Kernel family selected by the plan. */
+typedef enum da_path {
+  DA_PATH_SCALAR = 0,  /* one query row per CTA (pack_gqa = 0, or G = 1):
+                          fp32 FMA dot products + warp-shuffle softmax          */
+  DA_PATH_MMA = 1      /* pack_gqa with G >= 2: the G query rows of a KV head
+                          share each K/V tile; QK^T and PV on tensor cores     */
+} da_path;
+
+/*
+ * da_plan - a plain value (copyable, no handles).  Fields marked (in) echo
+ * the da_plan_make arguments; the rest are derived.
+ */
+typedef struct da_plan {
+  int32_t batch, h_q, h_kv, l_k, head_dim, pack_gqa, sm_margin, num_sms; /* (in) */
+  int32_t policy, forced_splits;                                          /* (in) */
+  int32_t usable_sms;      /* U = num_sms - sm_margin (DESIGN.md C-amb-8)      */
+  int32_t block_n;         /* 128: the policy's token accounting (C-amb-1)     */
+  int32_t num_n_blocks;    /* nblk = ceil(l_k / 128)                           */
+  int32_t num_m_blocks;    /* ceil(G / 64) (= 1 for G <= 64)                   */
+  int32_t total_mblocks;   /* T = batch * h_kv * num_m_blocks      */
+  int32_t num_splits;      /* s                                                */
+  int32_t nonempty_splits; /* min(s, ceil(l_k / split_unit))                   */
+  int32_t rule;            /* da_rule                                          */
+  int32_t split_unit;      /* 64 tokens: the partition unit                    */
+  int32_t path;            /* da_path                                          */
+  int32_t rows_per_cta;    /* query rows one CTA computes (1, 8 or 16)         */
+  int32_t combine_mode;    /* da_combine_mode                                  */
+  int32_t grid_x;          /* = num_splits                                     */
+  int32_t grid_y;          /* MMA: h_kv * ceil(G / rows_per_cta); SCALAR: h_q  */
+  int32_t grid_z;          /* = batch                                          */
+  int32_t block_threads;   /* threads per CTA                                  */
+  int32_t cluster_x;       /* CTAs per cluster along x (s in CLUSTER mode)     */
+  int32_t smem_bytes;      /* dynamic shared memory per CTA                    */
+  int64_t workspace_bytes; /* s * batch * h_q * (head_dim + 1) * 4 when s > 1,
+                              else 0.  Only DA_COMBINE_KERNEL reads/writes it. */
+} da_plan;
+
+/*
+ * da_plan_make - decide num_splits and the launch geometry for one shape.
+ *   batch, h_q, h_kv, l_k, head_dim : the shape; all >= 1,
+ *                                     h_q % h_kv == 0.
+ *   pack_gqa   : 0/1.  Does not change the decision (C-amb-17), only
+ *                the kernel path (MMA when pack_gqa && G >= 2).
+ *   sm_margin  : SMs excluded from the policy's count, 0 <= sm_margin < num_sms
+ *                (S:L37-41).
+ *   num_sms    : SM count of the device (148 on B200).
+ *   policy     : da_policy; forced_splits is read only for DA_POLICY_FIXED and
+ *                must be in [1, 256] (forced_splits > nblk is allowed: empty
+ *                splits produce o = 0, lse = -inf partials; C-amb-6).
+ *   out        : written on DA_OK only.
+ * Pure host code: no CUDA call, no allocation.  Errors: DA_ERR_INVALID_ARG,
+ * DA_ERR_UNSUPPORTED (head_dim != 128).
+ * Default combine mode: NONE for s == 1, CLUSTER for 2 <= s <= 8, else KERNEL.
+ */
+DA_API da_status da_plan_make(int32_t batch, int32_t h_q, int32_t h_kv, int32_t l_k,
+                       int32_t head_dim, int32_t pack_gqa, int32_t sm_margin,
+                       int32_t num_sms, int32_t policy, int32_t forced_splits,
+                       da_plan* out);
+
+/*
+ * da_plan_set_combine - switch an existing plan to another combine mode and
+ * re-derive its launch fields.  NONE requires s == 1, CLUSTER 2 <= s <= 8,
+ * KERNEL s >= 2.  Errors: DA_ERR_INVALID_ARG.
+ */
+DA_API da_status da_plan_set_combine(da_plan* plan, int32_t combine_mode);
+
+/*
+ * da_forward - decode attention for one step (L_Q = 1), asynchronously on
+ * cuda_stream (a cudaStream_t; NULL = legacy default stream).
+ *   q        bf16 [B, H_Q, d]             device; strides (q_b, q_h) elements
+ *   k_cache  bf16 [B, l_cap, H_KV, d]     device; strides (k_b, k_t, k_h)
+ *   v_cache  bf16 [B, l_cap, H_KV, d]     device; strides (v_b, v_t, v_h)
+ *   l_cap    cache capacity in tokens, >= plan->l_k
+ *   cache_seqlens  device int32 [B], tokens of batch b that attend (clamped
+ *            to [0, l_cap] on the device); NULL means plan->l_k for every b.
+ *   strides  host int64[8] = {q_b, q_h, k_b, k_t, k_h, v_b, v_t, v_h} in
+ *            elements (innermost dim contiguous); NULL = contiguous.  Each must
+ *            be a multiple of 8 elements (16 bytes, for TMA / 128-bit loads).
+ *   softmax_scale  <= 0 selects 1/sqrt(d) (C-amb-9).
+ *   out_dtype      DA_BF16 (round-to-nearest-even once at the end, C-amb-13)
+ *            or DA_F32 (unrounded: the per-GPU partial of a sequence shard).
+ *   out      [B, H_Q, d] contiguous, out_dtype.  Query head h uses KV head
+ *            floor(h / G) (C-amb-11).  An empty sequence gives out = 0.
+ *   lse      fp32 [B, H_Q] contiguous natural-log LSE, -inf for an empty
+ *            sequence (C-amb-12); may be NULL (not written).
+ *   workspace, workspace_bytes  fp32 partials [s, B, H_Q, d] followed by
+ *            [s, B, H_Q]; required (>= plan->workspace_bytes, 16-byte
+ *            aligned) only for DA_COMBINE_KERNEL, ignored otherwise.
+ * The result equals exact softmax attention over tokens [0, n_b) for every
+ * split count (SURVEY §8(c) C-att / C-comb).
+ */
+DA_API da_status da_forward(const da_plan* plan, const void* q, const void* k_cache,
+                     const void* v_cache, int32_t l_cap,
+                     const int32_t* cache_seqlens, const int64_t* strides,
+                     float softmax_scale, int32_t out_dtype, void* out, float* lse,
+                     void* workspace, int64_t workspace_bytes, void* cuda_stream);
+
+/*
+ * da_combine - LSE-combine of s partials (C-comb):
+ *   M = max_i lse_i, lse = M + ln sum_i exp(lse_i - M),
+ *   out = sum_i exp(lse_i - lse) o_i; all splits empty -> out = 0, lse = -inf.
+ *   o_partial   fp32, split i at o_partial + i * o_split_stride, each
+ *               [B, H_Q, d] contiguous (16-byte aligned; stride multiple of 4)
+ *   lse_partial fp32, split i at lse_partial + i * lse_split_stride, [B, H_Q]
+ *   (the strides let one NCCL all-gather buffer of [P][o | lse] be passed as is)
+ *   out         [B, H_Q, d] out_dtype;  lse fp32 [B, H_Q] or NULL.
+ * 1 <= num_splits <= 4096; head_dim must be 128.
+ */
+DA_API da_status da_combine(int32_t num_splits, int32_t batch, int32_t h_q, int32_t head_dim,
+                     const float* o_partial, int64_t o_split_stride,
+                     const float* lse_partial, int64_t lse_split_stride,
+                     int32_t out_dtype, void* out, float* lse, void* cuda_stream);
+
+/* Static, NUL-terminated description of a status code (never NULL). */
+DA_API const char* da_status_string(int32_t status);
+
+/* DA_ABI_VERSION of the loaded library. */
+DA_API int32_t da_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* DECATTN_H */

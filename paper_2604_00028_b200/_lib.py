@@ -1,0 +1,152 @@
+"""ctypes binding of libdecattn.so (include/decattn.h) - argument marshalling only.
+
+Every function here has the name of the C entry point it calls and does
+nothing but turn torch tensors into (pointer, stride) arguments, pick the
+current CUDA stream, and raise on a non-zero da_status.  All computation runs
+in the library's kernels; there is no fallback: if the shared library is
+missing this module fails to import.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+import torch
+
+PKG_DIR = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(PKG_DIR, "lib", "libdecattn.so")
+
+# ---- constants mirrored from include/decattn.h ----------------------------
+DA_OK, DA_ERR_INVALID_ARG, DA_ERR_UNSUPPORTED, DA_ERR_ALIGNMENT, DA_ERR_WORKSPACE, DA_ERR_CUDA = range(6)
+DA_POLICY_GUARDED, DA_POLICY_SEQ_AWARE, DA_POLICY_FIXED = range(3)
+(DA_RULE_SATURATED, DA_RULE_GUARD_NBLK4, DA_RULE_GUARD1, DA_RULE_GUARD2, DA_RULE_LOW_TILE,
+ DA_RULE_EFF_LOOP, DA_RULE_FORCED) = range(7)
+DA_BF16, DA_F32 = 0, 1
+DA_COMBINE_NONE, DA_COMBINE_CLUSTER, DA_COMBINE_KERNEL = range(3)
+DA_PATH_SCALAR, DA_PATH_MMA = 0, 1
+DA_ABI_VERSION = 1
+
+POLICIES = {"guarded": DA_POLICY_GUARDED, "seq_aware": DA_POLICY_SEQ_AWARE, "fixed": DA_POLICY_FIXED}
+RULE_NAMES = {DA_RULE_SATURATED: "saturated", DA_RULE_GUARD_NBLK4: "guard_nblk4",
+              DA_RULE_GUARD1: "guard1", DA_RULE_GUARD2: "guard2", DA_RULE_LOW_TILE: "low_tile",
+              DA_RULE_EFF_LOOP: "efficiency_loop", DA_RULE_FORCED: "forced"}
+
+
+class da_plan(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int32) for n in (
+        "batch", "h_q", "h_kv", "l_k", "head_dim", "pack_gqa", "sm_margin", "num_sms",
+        "policy", "forced_splits", "usable_sms", "block_n", "num_n_blocks", "num_m_blocks",
+        "total_mblocks", "num_splits", "nonempty_splits", "rule", "split_unit", "path",
+        "rows_per_cta", "combine_mode", "grid_x", "grid_y", "grid_z", "block_threads",
+        "cluster_x", "smem_bytes")] + [("workspace_bytes", ctypes.c_int64)]
+
+    def as_dict(self) -> dict:
+        return {name: getattr(self, name) for name, _ in self._fields_}
+
+    def __repr__(self):
+        d = self.as_dict()
+        return "da_plan(" + ", ".join(f"{k}={v}" for k, v in d.items()) + ")"
+
+
+class DecAttnError(RuntimeError):
+    def __init__(self, status: int, where: str):
+        super().__init__(f"{where}: {da_status_string(status)} (status {status})")
+        self.status = status
+
+
+def _load() -> ctypes.CDLL:
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: build it with "
+                          "`python -m paper_2604_00028_b200.build` (no CPU fallback exists)")
+    lib = ctypes.CDLL(LIB_PATH)
+    i32, i64, vp, f32 = ctypes.c_int32, ctypes.c_int64, ctypes.c_void_p, ctypes.c_float
+    lib.da_plan_make.argtypes = [i32] * 10 + [ctypes.POINTER(da_plan)]
+    lib.da_plan_make.restype = i32
+    lib.da_plan_set_combine.argtypes = [ctypes.POINTER(da_plan), i32]
+    lib.da_plan_set_combine.restype = i32
+    lib.da_forward.argtypes = [ctypes.POINTER(da_plan), vp, vp, vp, i32, vp, vp, f32, i32, vp, vp,
+                               vp, i64, vp]
+    lib.da_forward.restype = i32
+    lib.da_combine.argtypes = [i32, i32, i32, i32, vp, i64, vp, i64, i32, vp, vp, vp]
+    lib.da_combine.restype = i32
+    lib.da_status_string.argtypes = [i32]
+    lib.da_status_string.restype = ctypes.c_char_p
+    lib.da_abi_version.argtypes = []
+    lib.da_abi_version.restype = i32
+    if lib.da_abi_version() != DA_ABI_VERSION:
+        raise ImportError("libdecattn.so ABI version mismatch")
+    return lib
+
+
+LIB = _load()
+
+EXPORTED = ("da_plan_make", "da_plan_set_combine", "da_forward", "da_combine",
+            "da_status_string", "da_abi_version")
+
+
+def da_status_string(status: int) -> str:
+    return LIB.da_status_string(int(status)).decode()
+
+
+def da_abi_version() -> int:
+    return int(LIB.da_abi_version())
+
+
+def da_plan_make(batch, h_q, h_kv, l_k, head_dim=128, pack_gqa=1, sm_margin=0, num_sms=148,
+                 policy=DA_POLICY_SEQ_AWARE, forced_splits=0) -> da_plan:
+    if isinstance(policy, str):
+        policy = POLICIES[policy]
+    p = da_plan()
+    st = LIB.da_plan_make(int(batch), int(h_q), int(h_kv), int(l_k), int(head_dim), int(pack_gqa),
+                          int(sm_margin), int(num_sms), int(policy), int(forced_splits),
+                          ctypes.byref(p))
+    if st != DA_OK:
+        raise DecAttnError(st, "da_plan_make")
+    return p
+
+
+def da_plan_set_combine(plan: da_plan, combine_mode: int) -> da_plan:
+    st = LIB.da_plan_set_combine(ctypes.byref(plan), int(combine_mode))
+    if st != DA_OK:
+        raise DecAttnError(st, "da_plan_set_combine")
+    return plan
+
+
+def _ptr(t):
+    if t is None:
+        return None
+    if isinstance(t, int):
+        return t
+    return t.data_ptr()
+
+
+def _stream_handle(stream):
+    if stream is None:
+        return torch.cuda.current_stream().cuda_stream
+    if isinstance(stream, int):
+        return stream
+    return stream.cuda_stream
+
+
+def da_forward(plan: da_plan, q, k_cache, v_cache, l_cap, cache_seqlens, strides, softmax_scale,
+               out_dtype, out, lse, workspace, workspace_bytes, stream=None) -> None:
+    """Marshal to ``da_forward``.  Tensor arguments may be torch tensors or raw
+    device pointers (ints); ``strides`` is a sequence of 8 ints or None."""
+    sarr = None
+    if strides is not None:
+        sarr = (ctypes.c_int64 * 8)(*[int(x) for x in strides])
+    st = LIB.da_forward(ctypes.byref(plan), _ptr(q), _ptr(k_cache), _ptr(v_cache), int(l_cap),
+                        _ptr(cache_seqlens), sarr, float(softmax_scale), int(out_dtype), _ptr(out),
+                        _ptr(lse), _ptr(workspace), int(workspace_bytes), _stream_handle(stream))
+    if st != DA_OK:
+        raise DecAttnError(st, "da_forward")
+
+
+def da_combine(num_splits, batch, h_q, head_dim, o_partial, o_split_stride, lse_partial,
+               lse_split_stride, out_dtype, out, lse, stream=None) -> None:
+    st = LIB.da_combine(int(num_splits), int(batch), int(h_q), int(head_dim), _ptr(o_partial),
+                        int(o_split_stride), _ptr(lse_partial), int(lse_split_stride),
+                        int(out_dtype), _ptr(out), _ptr(lse), _stream_handle(stream))
+    if st != DA_OK:
+        raise DecAttnError(st, "da_combine")

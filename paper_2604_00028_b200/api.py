@@ -1,0 +1,114 @@
+"""Torch-facing convenience over the C ABI (allocation + marshalling only).
+
+    plan = make_plan(batch, h_q, h_kv, l_k, policy="seq_aware")
+    out, lse = forward(plan, q, k_cache, v_cache, cache_seqlens)
+
+``make_plan`` caches plans per shape (the precomputed-metadata deployment
+path the paper measures, §5.1: the split is decided once per shape,
+off the timed path).  ``forward`` allocates out / lse / workspace when not
+given and calls ``da_forward`` on the current stream.  Nothing here computes
+attention: every step of the path runs in libdecattn.so's kernels.
+"""
+
+from __future__ import annotations
+
+import functools
+
+import torch
+
+from . import _lib as L
+
+
+def _check_cuda(*ts):
+    for t in ts:
+        if t is not None and not t.is_cuda:
+            raise ValueError("decattn: tensors must be CUDA tensors (there is no CPU path)")
+
+
+@functools.lru_cache(maxsize=None)
+def num_sms(device_index: int = 0) -> int:
+    return torch.cuda.get_device_properties(device_index).multi_processor_count
+
+
+@functools.lru_cache(maxsize=4096)
+def _plan_cached(batch, h_q, h_kv, l_k, head_dim, pack_gqa, sm_margin, sms, policy, forced,
+                 combine_mode):
+    p = L.da_plan_make(batch, h_q, h_kv, l_k, head_dim, pack_gqa, sm_margin, sms, policy, forced)
+    if combine_mode is not None and combine_mode != p.combine_mode:
+        L.da_plan_set_combine(p, combine_mode)
+    return p
+
+
+def make_plan(batch, h_q, h_kv, l_k, head_dim=128, pack_gqa=True, sm_margin=0, num_sms_=None,
+              policy="seq_aware", forced_splits=0, combine_mode=None) -> L.da_plan:
+    """da_plan_make (+ da_plan_set_combine when combine_mode is given).
+    The returned plan is shared through a cache: copy it before editing."""
+    if isinstance(policy, str):
+        policy = L.POLICIES[policy]
+    sms = num_sms_ if num_sms_ is not None else num_sms(torch.cuda.current_device())
+    return _plan_cached(int(batch), int(h_q), int(h_kv), int(l_k), int(head_dim), int(bool(pack_gqa)),
+                        int(sm_margin), int(sms), int(policy), int(forced_splits), combine_mode)
+
+
+def _kv_strides(q, k, v):
+    if q.stride(-1) != 1 or k.stride(-1) != 1 or v.stride(-1) != 1:
+        raise ValueError("innermost (head_dim) dimension must be contiguous")
+    return (q.stride(0), q.stride(1), k.stride(0), k.stride(1), k.stride(2),
+            v.stride(0), v.stride(1), v.stride(2))
+
+
+def workspace_for(plan: L.da_plan, device) -> torch.Tensor | None:
+    if plan.combine_mode != L.DA_COMBINE_KERNEL:
+        return None
+    return torch.empty(plan.workspace_bytes // 4, dtype=torch.float32, device=device)
+
+
+def forward(plan: L.da_plan, q, k_cache, v_cache, cache_seqlens=None, *, out=None, lse=None,
+            workspace=None, softmax_scale=0.0, out_dtype=torch.bfloat16, stream=None):
+    """Decode attention via da_forward.  q [B, H_Q, d] bf16; k/v [B, L_cap, H_KV, d] bf16;
+    cache_seqlens int32 [B] or None.  Returns (out [B, H_Q, d], lse [B, H_Q] fp32)."""
+    _check_cuda(q, k_cache, v_cache, cache_seqlens)
+    if q.dtype != torch.bfloat16 or k_cache.dtype != torch.bfloat16 or v_cache.dtype != torch.bfloat16:
+        raise ValueError("q, k_cache, v_cache must be bfloat16")
+    if cache_seqlens is not None and cache_seqlens.dtype != torch.int32:
+        raise ValueError("cache_seqlens must be int32")
+    B, HQ, D = q.shape
+    if out is None:
+        out = torch.empty((B, HQ, D), dtype=out_dtype, device=q.device)
+    if lse is None:
+        lse = torch.empty((B, HQ), dtype=torch.float32, device=q.device)
+    if workspace is None:
+        workspace = workspace_for(plan, q.device)
+    ws_bytes = 0 if workspace is None else workspace.numel() * workspace.element_size()
+    dt = L.DA_F32 if out.dtype == torch.float32 else L.DA_BF16
+    L.da_forward(plan, q, k_cache, v_cache, k_cache.shape[1], cache_seqlens,
+                 _kv_strides(q, k_cache, v_cache), softmax_scale, dt, out, lse, workspace, ws_bytes,
+                 stream)
+    return out, lse
+
+
+def combine(o_partial, lse_partial, *, out=None, lse=None, out_dtype=torch.bfloat16, stream=None):
+    """da_combine over o_partial [s, B, H_Q, d] fp32 and lse_partial [s, B, H_Q] fp32
+    (split strides taken from the tensors)."""
+    _check_cuda(o_partial, lse_partial)
+    s, B, HQ, D = o_partial.shape
+    if out is None:
+        out = torch.empty((B, HQ, D), dtype=out_dtype, device=o_partial.device)
+    if lse is None:
+        lse = torch.empty((B, HQ), dtype=torch.float32, device=o_partial.device)
+    dt = L.DA_F32 if out.dtype == torch.float32 else L.DA_BF16
+    L.da_combine(s, B, HQ, D, o_partial, o_partial.stride(0), lse_partial, lse_partial.stride(0), dt,
+                 out, lse, stream)
+    return out, lse
+
+
+def decode_attention(q, k_cache, v_cache, cache_seqlens=None, *, policy="seq_aware", pack_gqa=True,
+                     sm_margin=0, forced_splits=0, l_k=None, softmax_scale=0.0,
+                     out_dtype=torch.bfloat16):
+    """One-call decode attention: plan (cached per shape) + forward."""
+    B, HQ, D = q.shape
+    HKV = k_cache.shape[2]
+    lk = int(l_k) if l_k is not None else k_cache.shape[1]
+    plan = make_plan(B, HQ, HKV, lk, D, pack_gqa, sm_margin, None, policy, forced_splits)
+    return forward(plan, q, k_cache, v_cache, cache_seqlens, softmax_scale=softmax_scale,
+                   out_dtype=out_dtype)

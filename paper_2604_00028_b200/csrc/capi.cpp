@@ -1,0 +1,209 @@
+// C ABI: da_forward / da_combine / da_status_string / da_abi_version
+// (da_plan_make, da_plan_set_combine live in plan.cpp).  See
+// include/decattn.h for the contract of every entry point.
+//
+// This layer validates arguments (every host-checkable error returns before
+// any launch, with no side effects), builds the two TMA tensor maps that
+// describe the caller's K / V cache, and launches the kernels on the
+// caller's stream.  It never allocates, synchronises or prints.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+
+#include "../../include/decattn.h"
+#include "config.h"
+#include "internal.h"
+
+using namespace decattn;
+
+namespace {
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  // Resolved once through the runtime (no -lcuda link dependency).
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = []() -> PFN_cuTensorMapEncodeTiled_v12000 {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q = cudaDriverEntryPointSymbolNotFound;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+  }();
+  return fn;
+}
+
+// K or V cache [B, l_cap, H_KV, d] as a 4-D TMA tensor (d, H_KV, l_cap, B)
+// with 64 x 1 x 64 x 1 boxes (64 tokens x 64 dims = 128-byte rows) and the
+// 128-byte swizzle the consumers' ldmatrix addressing expects.  Tokens past
+// l_cap read as zero.
+bool make_kv_tmap(CUtensorMap* map, const void* base, int32_t batch, int32_t l_cap, int32_t h_kv,
+                  int64_t sb, int64_t st, int64_t sh) {
+  auto fn = encode_fn();
+  if (fn == nullptr) return false;
+  cuuint64_t dims[4] = {static_cast<cuuint64_t>(kHeadDim), static_cast<cuuint64_t>(h_kv),
+                        static_cast<cuuint64_t>(l_cap), static_cast<cuuint64_t>(batch)};
+  cuuint64_t strides[3] = {static_cast<cuuint64_t>(sh) * 2, static_cast<cuuint64_t>(st) * 2,
+                           static_cast<cuuint64_t>(sb) * 2};
+  cuuint32_t box[4] = {64, 1, static_cast<cuuint32_t>(kTileN), 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+// A plan may be edited by its owner; re-derive what the launch depends on.
+da_status check_plan(const da_plan* plan) {
+  if (plan->batch < 1 || plan->h_q < 1 || plan->h_kv < 1 || plan->l_k < 1) return DA_ERR_INVALID_ARG;
+  if (plan->h_q % plan->h_kv != 0) return DA_ERR_INVALID_ARG;
+  if (plan->head_dim != kHeadDim) return DA_ERR_UNSUPPORTED;
+  if (plan->num_splits < 1 || plan->num_splits > kMaxForcedSplits) return DA_ERR_INVALID_ARG;
+  if (plan->pack_gqa != 0 && plan->pack_gqa != 1) return DA_ERR_INVALID_ARG;
+  if (!combine_mode_valid(plan->combine_mode, plan->num_splits)) return DA_ERR_INVALID_ARG;
+  da_plan chk = *plan;
+  derive_launch(&chk);
+  if (chk.path != plan->path || chk.rows_per_cta != plan->rows_per_cta ||
+      chk.grid_x != plan->grid_x || chk.grid_y != plan->grid_y || chk.grid_z != plan->grid_z ||
+      chk.block_threads != plan->block_threads || chk.cluster_x != plan->cluster_x ||
+      chk.smem_bytes != plan->smem_bytes || chk.workspace_bytes != plan->workspace_bytes)
+    return DA_ERR_INVALID_ARG;
+  if (plan->grid_y > 65535 || plan->grid_z > 65535) return DA_ERR_UNSUPPORTED;
+  return DA_OK;
+}
+
+}  // namespace
+
+extern "C" da_status da_forward(const da_plan* plan, const void* q, const void* k_cache,
+                                const void* v_cache, int32_t l_cap, const int32_t* cache_seqlens,
+                                const int64_t* strides, float softmax_scale, int32_t out_dtype,
+                                void* out, float* lse, void* workspace, int64_t workspace_bytes,
+                                void* cuda_stream) {
+  if (plan == nullptr || q == nullptr || k_cache == nullptr || v_cache == nullptr || out == nullptr)
+    return DA_ERR_INVALID_ARG;
+  da_status st = check_plan(plan);
+  if (st != DA_OK) return st;
+  if (l_cap < plan->l_k) return DA_ERR_INVALID_ARG;
+  if (out_dtype != DA_BF16 && out_dtype != DA_F32) return DA_ERR_INVALID_ARG;
+  if (!(softmax_scale <= 0.f) && !std::isfinite(softmax_scale)) return DA_ERR_INVALID_ARG;
+
+  const int64_t B = plan->batch, HQ = plan->h_q, HKV = plan->h_kv, D = kHeadDim;
+  int64_t sd[8];
+  if (strides != nullptr) {
+    std::memcpy(sd, strides, sizeof(sd));
+  } else {
+    sd[0] = HQ * D; sd[1] = D;                       // q (b, h)
+    sd[2] = int64_t(l_cap) * HKV * D; sd[3] = HKV * D; sd[4] = D;  // k (b, t, h)
+    sd[5] = sd[2]; sd[6] = sd[3]; sd[7] = sd[4];      // v
+  }
+  for (int i = 0; i < 8; ++i) {
+    if (sd[i] < 0) return DA_ERR_INVALID_ARG;
+    if (sd[i] % 8 != 0) return DA_ERR_ALIGNMENT;
+  }
+  if (!aligned16(q) || !aligned16(k_cache) || !aligned16(v_cache) || !aligned16(out) ||
+      (lse != nullptr && (reinterpret_cast<uintptr_t>(lse) & 3u) != 0))
+    return DA_ERR_ALIGNMENT;
+  if (cache_seqlens != nullptr && (reinterpret_cast<uintptr_t>(cache_seqlens) & 3u) != 0)
+    return DA_ERR_ALIGNMENT;
+
+  float* ws_o = nullptr;
+  float* ws_lse = nullptr;
+  if (plan->combine_mode == DA_COMBINE_KERNEL) {
+    if (workspace == nullptr || workspace_bytes < plan->workspace_bytes) return DA_ERR_WORKSPACE;
+    if (!aligned16(workspace)) return DA_ERR_ALIGNMENT;
+    ws_o = static_cast<float*>(workspace);
+    ws_lse = ws_o + int64_t(plan->num_splits) * B * HQ * D;
+  }
+
+  CUtensorMap tk, tv;
+  if (!make_kv_tmap(&tk, k_cache, plan->batch, l_cap, plan->h_kv, sd[2], sd[3], sd[4]) ||
+      !make_kv_tmap(&tv, v_cache, plan->batch, l_cap, plan->h_kv, sd[5], sd[6], sd[7]))
+    return DA_ERR_CUDA;
+
+  FwdParams p{};
+  p.q = static_cast<const uint16_t*>(q);
+  p.q_sb = sd[0];
+  p.q_sh = sd[1];
+  p.seqlens = cache_seqlens;
+  p.l_default = plan->l_k;
+  p.l_cap = l_cap;
+  p.num_splits = plan->num_splits;
+  p.G = plan->h_q / plan->h_kv;
+  p.h_q = plan->h_q;
+  p.batch = plan->batch;
+  p.mblocks_per_head = plan->path == DA_PATH_MMA ? (p.G + plan->rows_per_cta - 1) / plan->rows_per_cta : 1;
+  const float scale = softmax_scale > 0.f ? softmax_scale : 1.0f / std::sqrt(float(D));
+  p.scale_log2 = scale * 1.4426950408889634f;
+  p.out = out;
+  p.out_f32 = out_dtype == DA_F32;
+  p.lse = lse;
+  p.ws_o = ws_o;
+  p.ws_lse = ws_lse;
+
+  cudaStream_t stream = static_cast<cudaStream_t>(cuda_stream);
+  if (launch_split_kv_fwd(*plan, tk, tv, p, stream) != cudaSuccess) return DA_ERR_CUDA;
+  if (plan->combine_mode == DA_COMBINE_KERNEL) {
+    CombineParams c{};
+    c.o = ws_o;
+    c.o_stride = B * HQ * D;
+    c.lse_in = ws_lse;
+    c.lse_stride = B * HQ;
+    c.num_splits = plan->num_splits;
+    c.rows = static_cast<int32_t>(B * HQ);
+    c.out = out;
+    c.out_f32 = p.out_f32;
+    c.lse = lse;
+    if (launch_lse_combine(c, /*pdl=*/true, stream) != cudaSuccess) return DA_ERR_CUDA;
+  }
+  return DA_OK;
+}
+
+extern "C" da_status da_combine(int32_t num_splits, int32_t batch, int32_t h_q, int32_t head_dim,
+                                const float* o_partial, int64_t o_split_stride,
+                                const float* lse_partial, int64_t lse_split_stride,
+                                int32_t out_dtype, void* out, float* lse, void* cuda_stream) {
+  if (o_partial == nullptr || lse_partial == nullptr || out == nullptr) return DA_ERR_INVALID_ARG;
+  if (num_splits < 1 || num_splits > 4096 || batch < 1 || h_q < 1 || head_dim < 1)
+    return DA_ERR_INVALID_ARG;
+  if (head_dim != kHeadDim) return DA_ERR_UNSUPPORTED;
+  if (out_dtype != DA_BF16 && out_dtype != DA_F32) return DA_ERR_INVALID_ARG;
+  const int64_t rows = int64_t(batch) * h_q;
+  if (rows > INT32_MAX / 2) return DA_ERR_UNSUPPORTED;
+  if (num_splits > 1 && (o_split_stride < rows * kHeadDim || lse_split_stride < rows))
+    return DA_ERR_INVALID_ARG;
+  if (o_split_stride % 4 != 0 || !aligned16(o_partial) || !aligned16(out) ||
+      (reinterpret_cast<uintptr_t>(lse_partial) & 3u) != 0 ||
+      (lse != nullptr && (reinterpret_cast<uintptr_t>(lse) & 3u) != 0))
+    return DA_ERR_ALIGNMENT;
+  CombineParams c{};
+  c.o = o_partial;
+  c.o_stride = o_split_stride;
+  c.lse_in = lse_partial;
+  c.lse_stride = lse_split_stride;
+  c.num_splits = num_splits;
+  c.rows = static_cast<int32_t>(rows);
+  c.out = out;
+  c.out_f32 = out_dtype == DA_F32;
+  c.lse = lse;
+  if (launch_lse_combine(c, /*pdl=*/true, static_cast<cudaStream_t>(cuda_stream)) != cudaSuccess)
+    return DA_ERR_CUDA;
+  return DA_OK;
+}
+
+extern "C" const char* da_status_string(int32_t status) {
+  switch (status) {
+    case DA_OK: return "DA_OK";
+    case DA_ERR_INVALID_ARG: return "DA_ERR_INVALID_ARG: invalid argument or inconsistent plan";
+    case DA_ERR_UNSUPPORTED: return "DA_ERR_UNSUPPORTED: configuration not supported (head_dim must be 128)";
+    case DA_ERR_ALIGNMENT: return "DA_ERR_ALIGNMENT: pointer not 16-byte aligned or stride not a multiple of 8 elements";
+    case DA_ERR_WORKSPACE: return "DA_ERR_WORKSPACE: workspace missing or smaller than plan->workspace_bytes";
+    case DA_ERR_CUDA: return "DA_ERR_CUDA: a CUDA runtime/driver call failed";
+    default: return "unknown da_status";
+  }
+}
+
+extern "C" int32_t da_abi_version(void) { return DA_ABI_VERSION; }

@@ -1,0 +1,567 @@
+// Split-KV decode-attention forward for sm_100a.
+//
+// One CTA = one (split, head-group, batch) work unit; grid = (s, Y, B) with
+// Y = H_KV * ceil(G / rows) on the pack_gqa tensor-core path or Y = H_Q on
+// the scalar path.  The s CTAs of a head-group partition its sequence
+// ("num_splits ... sequence-level parallelization across SMs", §3.1),
+// so s is exactly the paper's knob: s = 1 launches B*H_KV CTAs ("as few as 8
+// Thread Blocks"), s = 3 triples them.
+//
+// Inside a CTA:
+//   warp 4      TMA producer: one elected lane streams 64-token K/V tiles
+//               (4 boxes of 64 tokens x 64 dims, 128B-swizzled) through a
+//               6-stage mbarrier ring (step a3, KV streaming).
+//   warps 0..3  consumers: warp w owns tiles w, w+4, ... and keeps its own
+//               online-softmax state (steps a4-a6):
+//               MMA path  S^T = K Q^T and O^T += V^T P^T with
+//                         mma.sync.m16n8k16 (bf16 -> fp32): tokens and head
+//                         dims fill the M = 16 side, the G query rows the
+//                         N = 8 side, so no MMA lane is padding for G = 8;
+//                         P^T is re-laid out register-to-register with
+//                         movmatrix.trans.
+//               scalar    lane-per-token fp32 dot products, warp-shuffle
+//                         max / sum, lane-per-4-dims PV.
+//   epilogue    the four warps' (m, l, O) merge in shared memory; then
+//               s == 1   : bf16/fp32 out + lse written directly (a7);
+//               CLUSTER  : the s CTAs (one thread-block cluster) merge
+//                          through DSMEM - the LSE combine (a8) with no
+//                          workspace and no second launch;
+//               KERNEL   : normalised fp32 partials + lse go to the
+//                          workspace for lse_combine_kernel (combine.cu).
+// Scores are kept in the log2 domain (scale * log2 e folded into one FMUL);
+// lse is returned in natural log (C-amb-10).
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdint>
+
+#include "config.h"
+#include "internal.h"
+#include "ptx.cuh"
+
+namespace decattn {
+
+using namespace ptx;
+
+namespace {
+
+constexpr float kNegInf = -__builtin_huge_valf();
+constexpr float kLn2 = 0.6931471805599453f;
+constexpr int kHalfBytes = kTileN * 128;     // one 64-token x 64-dim box: 8 KB
+constexpr int kEpiStride = kHeadDim + 4;     // fp32 row stride of epilogue buffers (bank spread)
+
+// ---------------------------------------------------------------------------
+// MMA path: one 64-token tile for one warp.  sK / sV: smem addresses of the
+// K / V half-0 boxes (half 1 follows at +8 KB).  Box layout: row r (token)
+// at r*128 B, 16-byte chunk c at ((c ^ (r & 7)) * 16)  (TMA SWIZZLE_128B).
+// ---------------------------------------------------------------------------
+template <int NB>
+__device__ __forceinline__ void mma_tile(uint32_t sK, uint32_t sV, int valid,
+                                         const uint32_t (&qf)[8][NB][2], float (&o)[8][NB][4],
+                                         float (&m)[NB][2], float (&l)[NB][2], float scale_log2,
+                                         int lane) {
+  const uint32_t sw = static_cast<uint32_t>(lane & 7);
+  // ---- S^T[token, g] = sum_d K[token, d] Q[g, d]  (4 token blocks x NB g-blocks)
+  float s[4][NB][4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+#pragma unroll
+    for (int nb = 0; nb < NB; ++nb)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) s[j][nb][c] = 0.f;
+
+  {
+    // A operand = K rows: lane provides row (lane & 7) + 8*((lane >> 3) & 1), k-chunk lane >> 4.
+    const uint32_t row_off = static_cast<uint32_t>(((lane & 7) + ((lane >> 3) & 1) * 8) * 128);
+#pragma unroll
+    for (int kk = 0; kk < 8; ++kk) {
+      const uint32_t chunk = static_cast<uint32_t>(((kk & 3) << 1) + (lane >> 4));
+      const uint32_t base = sK + (kk >> 2) * kHalfBytes + row_off + ((chunk ^ sw) << 4);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        uint32_t a0, a1, a2, a3;
+        ldmatrix_x4(base + j * 16 * 128, a0, a1, a2, a3);
+#pragma unroll
+        for (int nb = 0; nb < NB; ++nb) mma_bf16_16816(s[j][nb], a0, a1, a2, a3, qf[kk][nb][0], qf[kk][nb][1]);
+      }
+    }
+  }
+
+  // ---- online softmax over the tile's tokens, per query row g (a5)
+  // C layout: s[j][nb][c] holds token 16j + (lane >> 2) + 8*(c >> 1), g = 8nb + 2(lane & 3) + (c & 1).
+  float mx[NB][2];
+#pragma unroll
+  for (int nb = 0; nb < NB; ++nb) mx[nb][0] = mx[nb][1] = kNegInf;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int tok = 16 * j + (lane >> 2);
+#pragma unroll
+    for (int nb = 0; nb < NB; ++nb) {
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const int t = tok + 8 * (c >> 1);
+        s[j][nb][c] = t < valid ? s[j][nb][c] * scale_log2 : kNegInf;
+        mx[nb][c & 1] = fmaxf(mx[nb][c & 1], s[j][nb][c]);
+      }
+    }
+  }
+#pragma unroll
+  for (int nb = 0; nb < NB; ++nb)
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      float v = mx[nb][c];
+      v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, 4));
+      v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, 8));
+      v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, 16));
+      const float m_new = fmaxf(m[nb][c], v);           // finite: the tile has >= 1 valid token
+      const float alpha = ex2(m[nb][c] - m_new);        // m_old = -inf -> 0
+      m[nb][c] = m_new;
+      l[nb][c] *= alpha;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        o[i][nb][c] *= alpha;
+        o[i][nb][c + 2] *= alpha;
+      }
+    }
+
+  // P = exp2(S - m); pack to bf16 and transpose each 8x8 block so P^T's C layout
+  // becomes the B-operand layout of the PV product.
+  uint32_t pb[4][NB][2];
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+#pragma unroll
+    for (int nb = 0; nb < NB; ++nb) {
+      float p[4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        p[c] = ex2(s[j][nb][c] - m[nb][c & 1]);         // masked: exp2(-inf) = 0
+        l[nb][c & 1] += p[c];
+      }
+      pb[j][nb][0] = movmatrix_trans(pack_bf16(p[0], p[1]));
+      pb[j][nb][1] = movmatrix_trans(pack_bf16(p[2], p[3]));
+    }
+
+  // ---- O^T[d, g] += sum_token V^T[d, token] P^T[token, g]   (8 d-blocks x 4 token blocks)
+  {
+    // A operand = V^T via ldmatrix.trans: lane provides token row (lane & 7) + 8*(lane >> 4),
+    // d-chunk 2i + ((lane >> 3) & 1).
+    const uint32_t row_off = static_cast<uint32_t>(((lane & 7) + (lane >> 4) * 8) * 128);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const uint32_t chunk = static_cast<uint32_t>(((2 * i) & 7) + ((lane >> 3) & 1));
+      const uint32_t base = sV + (i >> 2) * kHalfBytes + row_off + ((chunk ^ sw) << 4);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        uint32_t a0, a1, a2, a3;
+        ldmatrix_x4_trans(base + j * 16 * 128, a0, a1, a2, a3);
+#pragma unroll
+        for (int nb = 0; nb < NB; ++nb) mma_bf16_16816(o[i][nb], a0, a1, a2, a3, pb[j][nb][0], pb[j][nb][1]);
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Scalar path: one 64-token tile for one warp, one query row.  Lane t scores
+// tokens t and t + 32; lane owns head dims 4*lane .. 4*lane + 3 of O.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void scalar_tile(uint32_t sK, uint32_t sV, int valid, const uint4 (&qv)[16],
+                                            float (&o)[4], float& m, float& l, float scale_log2,
+                                            int lane) {
+  float sc[2];
+#pragma unroll
+  for (int tt = 0; tt < 2; ++tt) {
+    const int r = lane + 32 * tt;
+    const uint32_t row = sK + static_cast<uint32_t>(r * 128);
+    const uint32_t sw = static_cast<uint32_t>(r & 7);
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        const uint4 kv = lds128(row + h * kHalfBytes + ((static_cast<uint32_t>(c) ^ sw) << 4));
+        const uint4 qq = qv[h * 8 + c];
+        acc[0] = fmaf(bf16lo(kv.x), bf16lo(qq.x), acc[0]);
+        acc[1] = fmaf(bf16hi(kv.x), bf16hi(qq.x), acc[1]);
+        acc[2] = fmaf(bf16lo(kv.y), bf16lo(qq.y), acc[2]);
+        acc[3] = fmaf(bf16hi(kv.y), bf16hi(qq.y), acc[3]);
+        acc[0] = fmaf(bf16lo(kv.z), bf16lo(qq.z), acc[0]);
+        acc[1] = fmaf(bf16hi(kv.z), bf16hi(qq.z), acc[1]);
+        acc[2] = fmaf(bf16lo(kv.w), bf16lo(qq.w), acc[2]);
+        acc[3] = fmaf(bf16hi(kv.w), bf16hi(qq.w), acc[3]);
+      }
+    const float dot = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+    sc[tt] = r < valid ? dot * scale_log2 : kNegInf;
+  }
+  float mx = fmaxf(sc[0], sc[1]);
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+  const float m_new = fmaxf(m, mx);
+  const float alpha = ex2(m - m_new);
+  m = m_new;
+  const float p0 = ex2(sc[0] - m_new), p1 = ex2(sc[1] - m_new);
+  l = l * alpha + (p0 + p1);
+#pragma unroll
+  for (int e = 0; e < 4; ++e) o[e] *= alpha;
+
+  // PV over the valid tokens: row t, 8 bytes at dims 4*lane.
+  const uint32_t half = static_cast<uint32_t>(lane >> 4);
+  const uint32_t chunk = static_cast<uint32_t>((lane & 15) >> 1);
+  const uint32_t vcol = sV + half * kHalfBytes + static_cast<uint32_t>((lane & 1) * 8);
+#pragma unroll 4
+  for (int t = 0; t < valid; ++t) {
+    const float pt = __shfl_sync(0xffffffffu, t < 32 ? p0 : p1, t & 31);
+    const uint2 vv = lds64(vcol + static_cast<uint32_t>(t * 128) + ((chunk ^ static_cast<uint32_t>(t & 7)) << 4));
+    o[0] = fmaf(pt, bf16lo(vv.x), o[0]);
+    o[1] = fmaf(pt, bf16hi(vv.x), o[1]);
+    o[2] = fmaf(pt, bf16lo(vv.y), o[2]);
+    o[3] = fmaf(pt, bf16hi(vv.y), o[3]);
+  }
+}
+
+__device__ __forceinline__ void store_out(const FwdParams& p, size_t row, int d4, float4 v) {
+  if (p.out_f32) {
+    reinterpret_cast<float4*>(p.out)[row * (kHeadDim / 4) + d4] = v;
+  } else {
+    uint2 w;
+    w.x = pack_bf16(v.x, v.y);
+    w.y = pack_bf16(v.z, v.w);
+    reinterpret_cast<uint2*>(p.out)[row * (kHeadDim / 4) + d4] = w;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// The kernel.  kPath: DA_PATH_SCALAR / DA_PATH_MMA; kNB: g-blocks of 8 query
+// rows (MMA path); kCombine: da_combine_mode.
+// ---------------------------------------------------------------------------
+template <int kPath, int kNB, int kCombine>
+__global__ void __launch_bounds__(kThreads, 1)
+    split_kv_fwd_kernel(const __grid_constant__ CUtensorMap tmap_k,
+                        const __grid_constant__ CUtensorMap tmap_v, const FwdParams p) {
+  constexpr int R = kPath == DA_PATH_MMA ? 8 * kNB : 1;   // query rows of this CTA
+  extern __shared__ uint8_t smem_raw[];
+  __shared__ __align__(8) uint64_t full_bar[kStages];
+  __shared__ __align__(8) uint64_t empty_bar[kStages];
+
+  const uint32_t raw = smem_u32(smem_raw);
+  const uint32_t sbase = (raw + 1023u) & ~1023u;
+  float* const epi = reinterpret_cast<float*>(smem_raw + (sbase - raw));
+  // epilogue carve-up (aliases the pipeline ring once every tile is consumed)
+  float* const epi_o = epi;                                        // [NW][16][kEpiStride]
+  float* const epi_m = epi_o + kConsumerWarps * 16 * kEpiStride;   // [NW][16]
+  float* const epi_l = epi_m + kConsumerWarps * 16;                // [NW][16]
+  float* const cta_o = epi_l + kConsumerWarps * 16;                // [16][kEpiStride]
+  float* const cta_m = cta_o + 16 * kEpiStride;                    // [16]
+  float* const cta_l = cta_m + 16;                                 // [16]
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int split = blockIdx.x, b = blockIdx.z;
+  int kvh, hq0, rows_valid;
+  if constexpr (kPath == DA_PATH_MMA) {
+    kvh = blockIdx.y / p.mblocks_per_head;
+    const int rg = blockIdx.y - kvh * p.mblocks_per_head;
+    hq0 = kvh * p.G + rg * R;
+    rows_valid = min(R, p.G - rg * R);
+  } else {
+    hq0 = blockIdx.y;
+    kvh = hq0 / p.G;
+    rows_valid = 1;
+  }
+
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int i = 0; i < kStages; ++i) {
+      mbar_init(smem_u32(&full_bar[i]), 1);
+      mbar_init(smem_u32(&empty_bar[i]), 1);
+    }
+    fence_mbarrier_init();
+  }
+  if (warp == kConsumerWarps && lane == 0) {
+    prefetch_tmap(&tmap_k);
+    prefetch_tmap(&tmap_v);
+  }
+  __syncthreads();
+
+  // Inputs (q, KV cache, lengths) may be written by the preceding kernel.
+  pdl_wait();
+
+  // ---- this split's token range (C-pol item 6): units of kTileN tokens
+  int n = p.seqlens != nullptr ? __ldg(p.seqlens + b) : p.l_default;
+  n = min(max(n, 0), p.l_cap);
+  const int64_t n_units = (n + kTileN - 1) / kTileN;
+  const int u0 = static_cast<int>(static_cast<int64_t>(split) * n_units / p.num_splits);
+  const int u1 = static_cast<int>(static_cast<int64_t>(split + 1) * n_units / p.num_splits);
+  const int t0 = u0 * kTileN;
+  const int t_end = min(u1 * kTileN, n);
+  const int n_tiles = u1 - u0;
+
+  if (warp == kConsumerWarps) {
+    // ================= TMA producer =================
+    if (lane == 0) {
+      for (int i = 0; i < n_tiles; ++i) {
+        const int st = i % kStages;
+        if (i >= kStages) mbar_wait(smem_u32(&empty_bar[st]), ((i / kStages) - 1) & 1);
+        const uint32_t fb = smem_u32(&full_bar[st]);
+        mbar_arrive_expect_tx(fb, kStageBytes);
+        const uint32_t dst = sbase + st * kStageBytes;
+        const int t = t0 + i * kTileN;
+        tma_load_4d(dst, &tmap_k, fb, 0, kvh, t, b);
+        tma_load_4d(dst + kHalfBytes, &tmap_k, fb, 64, kvh, t, b);
+        tma_load_4d(dst + 2 * kHalfBytes, &tmap_v, fb, 0, kvh, t, b);
+        tma_load_4d(dst + 3 * kHalfBytes, &tmap_v, fb, 64, kvh, t, b);
+      }
+    }
+  } else {
+    // ================= consumers =================
+    const uint16_t* qrow = p.q + static_cast<int64_t>(b) * p.q_sb;
+    if constexpr (kPath == DA_PATH_MMA) {
+      uint32_t qf[8][kNB][2];
+#pragma unroll
+      for (int nb = 0; nb < kNB; ++nb) {
+        const int g = nb * 8 + (lane >> 2);
+        const bool ok = g < rows_valid;
+        const uint16_t* qg = qrow + static_cast<int64_t>(hq0 + (ok ? g : 0)) * p.q_sh + 2 * (lane & 3);
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          qf[kk][nb][0] = ok ? __ldg(reinterpret_cast<const uint32_t*>(qg + kk * 16)) : 0u;
+          qf[kk][nb][1] = ok ? __ldg(reinterpret_cast<const uint32_t*>(qg + kk * 16 + 8)) : 0u;
+        }
+      }
+      float o[8][kNB][4];
+      float m[kNB][2], l[kNB][2];
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int nb = 0; nb < kNB; ++nb)
+#pragma unroll
+          for (int c = 0; c < 4; ++c) o[i][nb][c] = 0.f;
+#pragma unroll
+      for (int nb = 0; nb < kNB; ++nb) m[nb][0] = m[nb][1] = kNegInf, l[nb][0] = l[nb][1] = 0.f;
+
+      for (int i = warp; i < n_tiles; i += kConsumerWarps) {
+        const int st = i % kStages;
+        mbar_wait(smem_u32(&full_bar[st]), (i / kStages) & 1);
+        const int valid = min(kTileN, t_end - (t0 + i * kTileN));
+        const uint32_t sK = sbase + st * kStageBytes;
+        const uint32_t sV = sK + 2 * kHalfBytes;
+        if (valid < kTileN) {
+          // rows past the range may hold anything (even NaN): zero them so P = 0 rows stay 0
+          for (int idx = lane; idx < (kTileN - valid) * 16; idx += 32) {
+            const int r = valid + (idx >> 4);
+            const int c = idx & 15;
+            sts128(sV + (c >> 3) * kHalfBytes + r * 128 + (c & 7) * 16, make_uint4(0, 0, 0, 0));
+          }
+          __syncwarp();
+        }
+        mma_tile<kNB>(sK, sV, valid, qf, o, m, l, p.scale_log2, lane);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_u32(&empty_bar[st]));
+      }
+      // finish l: sum the partial sums of the 8 lanes that share a g column
+#pragma unroll
+      for (int nb = 0; nb < kNB; ++nb)
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          float v = l[nb][c];
+          v += __shfl_xor_sync(0xffffffffu, v, 4);
+          v += __shfl_xor_sync(0xffffffffu, v, 8);
+          v += __shfl_xor_sync(0xffffffffu, v, 16);
+          l[nb][c] = v;
+        }
+      asm volatile("bar.sync 1, %0;" ::"n"(kConsumerWarps * 32) : "memory");  // ring no longer read
+      if (lane < 4) {
+#pragma unroll
+        for (int nb = 0; nb < kNB; ++nb)
+#pragma unroll
+          for (int c = 0; c < 2; ++c) {
+            const int g = nb * 8 + 2 * lane + c;
+            epi_m[warp * 16 + g] = m[nb][c];
+            epi_l[warp * 16 + g] = l[nb][c];
+          }
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int nb = 0; nb < kNB; ++nb)
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            const int g = nb * 8 + 2 * (lane & 3) + (c & 1);
+            const int d = 16 * i + (lane >> 2) + 8 * (c >> 1);
+            epi_o[(warp * 16 + g) * kEpiStride + d] = o[i][nb][c];
+          }
+    } else {
+      uint4 qv[16];
+      const uint4* q4 = reinterpret_cast<const uint4*>(qrow + static_cast<int64_t>(hq0) * p.q_sh);
+#pragma unroll
+      for (int c = 0; c < 16; ++c) qv[c] = __ldg(q4 + c);
+      float o[4] = {0.f, 0.f, 0.f, 0.f};
+      float m = kNegInf, l = 0.f;
+      for (int i = warp; i < n_tiles; i += kConsumerWarps) {
+        const int st = i % kStages;
+        mbar_wait(smem_u32(&full_bar[st]), (i / kStages) & 1);
+        const int valid = min(kTileN, t_end - (t0 + i * kTileN));
+        const uint32_t sK = sbase + st * kStageBytes;
+        scalar_tile(sK, sK + 2 * kHalfBytes, valid, qv, o, m, l, p.scale_log2, lane);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_u32(&empty_bar[st]));
+      }
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) l += __shfl_xor_sync(0xffffffffu, l, off);
+      asm volatile("bar.sync 1, %0;" ::"n"(kConsumerWarps * 32) : "memory");
+      if (lane == 0) {
+        epi_m[warp * 16] = m;
+        epi_l[warp * 16] = l;
+      }
+      *reinterpret_cast<float4*>(&epi_o[(warp * 16) * kEpiStride + 4 * lane]) =
+          make_float4(o[0], o[1], o[2], o[3]);
+    }
+  }
+
+  if constexpr (kCombine == DA_COMBINE_KERNEL) pdl_launch_dependents();
+
+  // ================= merge the consumer warps (all rows of this CTA) =================
+  if (warp < kConsumerWarps) {
+    asm volatile("bar.sync 1, %0;" ::"n"(kConsumerWarps * 32) : "memory");
+    for (int e = threadIdx.x; e < R * 32; e += kConsumerWarps * 32) {
+      const int g = e >> 5, d4 = e & 31;
+      if (g >= rows_valid) continue;
+      float M = kNegInf;
+#pragma unroll
+      for (int w = 0; w < kConsumerWarps; ++w) M = fmaxf(M, epi_m[w * 16 + g]);
+      float L = 0.f;
+      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int w = 0; w < kConsumerWarps; ++w) {
+        const float mw = epi_m[w * 16 + g];
+        const float f = mw == kNegInf ? 0.f : ex2(mw - M);
+        L = fmaf(f, epi_l[w * 16 + g], L);
+        const float4 ow = *reinterpret_cast<const float4*>(&epi_o[(w * 16 + g) * kEpiStride + 4 * d4]);
+        acc.x = fmaf(f, ow.x, acc.x);
+        acc.y = fmaf(f, ow.y, acc.y);
+        acc.z = fmaf(f, ow.z, acc.z);
+        acc.w = fmaf(f, ow.w, acc.w);
+      }
+      if constexpr (kCombine == DA_COMBINE_CLUSTER) {
+        *reinterpret_cast<float4*>(&cta_o[g * kEpiStride + 4 * d4]) = acc;
+        if (d4 == 0) {
+          cta_m[g] = M;
+          cta_l[g] = L;
+        }
+      } else {
+        const float inv = L > 0.f ? 1.f / L : 0.f;
+        const float4 v = make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
+        const float lse_v = L > 0.f ? (M + lg2(L)) * kLn2 : kNegInf;
+        const size_t row = static_cast<size_t>(b) * p.h_q + hq0 + g;
+        if constexpr (kCombine == DA_COMBINE_NONE) {
+          store_out(p, row, d4, v);
+          if (d4 == 0 && p.lse != nullptr) p.lse[row] = lse_v;
+        } else {  // DA_COMBINE_KERNEL: normalised partial o_i, lse_i (C-part)
+          const size_t prow = static_cast<size_t>(split) * p.batch * p.h_q + row;
+          reinterpret_cast<float4*>(p.ws_o)[prow * (kHeadDim / 4) + d4] = v;
+          if (d4 == 0) p.ws_lse[prow] = lse_v;
+        }
+      }
+    }
+  }
+
+  if constexpr (kCombine == DA_COMBINE_CLUSTER) {
+    // ================= LSE combine across the s CTAs of the cluster (a8) =================
+    cluster_sync();
+    if (warp < kConsumerWarps) {
+      const int s = p.num_splits;
+      const int rank = static_cast<int>(cluster_ctarank());
+      const uint32_t m_addr = smem_u32(cta_m), l_addr = smem_u32(cta_l), o_addr = smem_u32(cta_o);
+      for (int e = rank + s * static_cast<int>(threadIdx.x); e < R * 32; e += s * kConsumerWarps * 32) {
+        const int g = e >> 5, d4 = e & 31;
+        if (g >= rows_valid) continue;
+        float mr[kMaxClusterSplits];
+        float M = kNegInf;
+#pragma unroll
+        for (int r = 0; r < kMaxClusterSplits; ++r) {
+          mr[r] = r < s ? ld_dsmem_f32(mapa(m_addr + 4 * g, r)) : kNegInf;
+          M = fmaxf(M, mr[r]);
+        }
+        float L = 0.f;
+        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int r = 0; r < kMaxClusterSplits; ++r) {
+          if (r < s && mr[r] != kNegInf) {
+            const float f = ex2(mr[r] - M);
+            L = fmaf(f, ld_dsmem_f32(mapa(l_addr + 4 * g, r)), L);
+            const float4 orr = ld_dsmem_v4(mapa(o_addr + (g * kEpiStride + 4 * d4) * 4, r));
+            acc.x = fmaf(f, orr.x, acc.x);
+            acc.y = fmaf(f, orr.y, acc.y);
+            acc.z = fmaf(f, orr.z, acc.z);
+            acc.w = fmaf(f, orr.w, acc.w);
+          }
+        }
+        const float inv = L > 0.f ? 1.f / L : 0.f;
+        const size_t row = static_cast<size_t>(b) * p.h_q + hq0 + g;
+        store_out(p, row, d4, make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv));
+        if (d4 == 0 && p.lse != nullptr) p.lse[row] = L > 0.f ? (M + lg2(L)) * kLn2 : kNegInf;
+      }
+    }
+    cluster_sync();  // keep every CTA's shared memory alive until all remote reads are done
+  }
+}
+
+template <int kPath, int kNB, int kCombine>
+cudaError_t launch_impl(const da_plan& plan, const CUtensorMap& tk, const CUtensorMap& tv,
+                        const FwdParams& p, cudaStream_t stream) {
+  auto kern = split_kv_fwd_kernel<kPath, kNB, kCombine>;
+  // One-time (per device) opt-in to > 48 KB of dynamic shared memory.
+  static std::atomic<uint64_t> attr_done{0};
+  int dev = 0;
+  cudaError_t err = cudaGetDevice(&dev);
+  if (err != cudaSuccess) return err;
+  const uint64_t bit = 1ull << (dev & 63);
+  if ((attr_done.load(std::memory_order_acquire) & bit) == 0) {
+    err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+    if (err != cudaSuccess) return err;
+    attr_done.fetch_or(bit, std::memory_order_acq_rel);
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(plan.grid_x, plan.grid_y, plan.grid_z);
+  cfg.blockDim = dim3(kThreads, 1, 1);
+  cfg.dynamicSmemBytes = kSmemBytes;
+  cfg.stream = stream;
+  cudaLaunchAttribute attrs[2];
+  int na = 0;
+  attrs[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attrs[na].val.programmaticStreamSerializationAllowed = 1;
+  ++na;
+  if (kCombine == DA_COMBINE_CLUSTER) {
+    attrs[na].id = cudaLaunchAttributeClusterDimension;
+    attrs[na].val.clusterDim.x = static_cast<unsigned>(plan.num_splits);
+    attrs[na].val.clusterDim.y = 1;
+    attrs[na].val.clusterDim.z = 1;
+    ++na;
+  }
+  cfg.attrs = attrs;
+  cfg.numAttrs = na;
+  return cudaLaunchKernelEx(&cfg, kern, tk, tv, p);
+}
+
+template <int kPath, int kNB>
+cudaError_t dispatch_combine(const da_plan& plan, const CUtensorMap& tk, const CUtensorMap& tv,
+                             const FwdParams& p, cudaStream_t stream) {
+  switch (plan.combine_mode) {
+    case DA_COMBINE_NONE: return launch_impl<kPath, kNB, DA_COMBINE_NONE>(plan, tk, tv, p, stream);
+    case DA_COMBINE_CLUSTER: return launch_impl<kPath, kNB, DA_COMBINE_CLUSTER>(plan, tk, tv, p, stream);
+    default: return launch_impl<kPath, kNB, DA_COMBINE_KERNEL>(plan, tk, tv, p, stream);
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_split_kv_fwd(const da_plan& plan, const CUtensorMap& tmap_k,
+                                const CUtensorMap& tmap_v, const FwdParams& p,
+                                cudaStream_t stream) {
+  if (plan.path == DA_PATH_SCALAR) return dispatch_combine<DA_PATH_SCALAR, 1>(plan, tmap_k, tmap_v, p, stream);
+  if (plan.rows_per_cta == 8) return dispatch_combine<DA_PATH_MMA, 1>(plan, tmap_k, tmap_v, p, stream);
+  return dispatch_combine<DA_PATH_MMA, 2>(plan, tmap_k, tmap_v, p, stream);
+}
+
+}  // namespace decattn

@@ -1,0 +1,56 @@
+// Internal (non-ABI) declarations shared by capi.cpp and the .cu files.
+#pragma once
+
+#include <cstdint>
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include "../../include/decattn.h"
+
+namespace decattn {
+
+// Arguments of the split-KV forward kernel (everything except the two
+// tensor maps, which are passed as __grid_constant__ parameters).
+struct FwdParams {
+  const uint16_t* q;        // bf16 [B, H_Q, d]
+  int64_t q_sb, q_sh;       // strides in elements
+  const int32_t* seqlens;   // device int32 [B] or nullptr
+  int32_t l_default;        // length used when seqlens == nullptr (plan->l_k)
+  int32_t l_cap;            // cache capacity (clamp bound)
+  int32_t num_splits;       // s
+  int32_t G;                // H_Q / H_KV
+  int32_t h_q;
+  int32_t batch;
+  int32_t mblocks_per_head; // MMA path: ceil(G / rows_per_cta); SCALAR: 1
+  float scale_log2;         // softmax_scale * log2(e)
+  void* out;                // [B, H_Q, d] bf16 or f32
+  int32_t out_f32;
+  float* lse;               // [B, H_Q] or nullptr
+  float* ws_o;              // KERNEL combine: [s, B, H_Q, d]
+  float* ws_lse;            // KERNEL combine: [s, B, H_Q]
+};
+
+struct CombineParams {
+  const float* o;           // split i at o + i * o_stride, [rows, d]
+  int64_t o_stride;
+  const float* lse_in;      // split i at lse_in + i * lse_stride, [rows]
+  int64_t lse_stride;
+  int32_t num_splits;
+  int32_t rows;             // B * H_Q
+  void* out;
+  int32_t out_f32;
+  float* lse;               // [rows] or nullptr
+};
+
+// plan.cpp
+void derive_launch(da_plan* p);
+bool combine_mode_valid(int mode, int s);
+
+// fwd.cu
+cudaError_t launch_split_kv_fwd(const da_plan& plan, const CUtensorMap& tmap_k,
+                                const CUtensorMap& tmap_v, const FwdParams& p,
+                                cudaStream_t stream);
+// combine.cu
+cudaError_t launch_lse_combine(const CombineParams& p, bool pdl, cudaStream_t stream);
+
+}  // namespace decattn

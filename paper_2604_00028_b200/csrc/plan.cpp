@@ -1,0 +1,144 @@
+// Split planner: da_plan_make / da_plan_set_combine (host-only, integer-only).
+//
+// Implements the decision the paper is about: how many sequence splits a
+// decode-attention launch uses.  Two policies:
+//   * guarded   - FA3's default (§2.2 "returns s=1 if the sequence
+//                 length L_K <= 512"; §4.2 "strictly enforced s=1 when
+//                 num_n_blocks <= 4"), behind the saturation guard and ahead
+//                 of the efficiency loop (DESIGN.md C-amb-2..4);
+//   * seq-aware - the paper's Fig. 3 cascade: Guard 1, Guard 2,
+//                 the low-tile override s = 3, else the unchanged loop.
+// Every comparison is an exact integer cross-multiplication (C-amb-3), so the
+// result is bit-identical to the CPU oracle's (tests/test_plan_parity.py).
+// This file shares no code with oracle/: it is the product-side statement.
+#include <cstdint>
+
+#include "../../include/decattn.h"
+#include "config.h"
+
+namespace decattn {
+namespace {
+
+inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// FA3-style first guard: total_mblocks >= 0.8 * usable SMs  <=>  5T >= 4U.
+inline bool saturated(int64_t T, int64_t U) { return 5 * T >= 4 * U; }
+
+// Efficiency loop (referenced by P:L85; reconstruction in
+// DESIGN.md C-amb-2).  Candidates s = 1..min(128, U, nblk); waves
+// w_s = ceil(T s / U); efficiency(s) = T s / (U w_s).  Smallest s with
+// efficiency(s) >= 0.85 * best, i.e. 20 s w* >= 17 s* w_s.
+int efficiency_loop(int64_t T, int64_t U, int64_t nblk) {
+  int64_t smax = kEffMaxSplits;
+  if (U < smax) smax = U;
+  if (nblk < smax) smax = nblk;
+  int64_t best_s = 1, best_w = ceil_div(T, U);
+  for (int64_t s = 2; s <= smax; ++s) {
+    const int64_t w = ceil_div(T * s, U);
+    if (s * best_w > best_s * w) { best_s = s; best_w = w; }
+  }
+  for (int64_t s = 1; s <= smax; ++s) {
+    const int64_t w = ceil_div(T * s, U);
+    if (20 * s * best_w >= 17 * best_s * w) return static_cast<int>(s);
+  }
+  return 1;
+}
+
+void decide(int64_t T, int64_t U, int64_t nblk, int policy, int forced, int* s, int* rule) {
+  if (policy == DA_POLICY_FIXED) { *s = forced; *rule = DA_RULE_FORCED; return; }
+  if (saturated(T, U)) { *s = 1; *rule = DA_RULE_SATURATED; return; }
+  if (policy == DA_POLICY_GUARDED) {
+    if (nblk <= 4) { *s = 1; *rule = DA_RULE_GUARD_NBLK4; return; }
+  } else {  // DA_POLICY_SEQ_AWARE, Fig. 3 in order
+    if (nblk <= 3) { *s = 1; *rule = DA_RULE_GUARD1; return; }
+    if (nblk <= 4 && T >= 4) { *s = 1; *rule = DA_RULE_GUARD2; return; }
+    if (nblk == 4 && T < 4) { *s = kLowTileSplits; *rule = DA_RULE_LOW_TILE; return; }
+  }
+  *s = efficiency_loop(T, U, nblk);
+  *rule = DA_RULE_EFF_LOOP;
+}
+
+}  // namespace
+
+// Launch geometry for a plan whose decision fields are set.  Shared by
+// da_plan_make, da_plan_set_combine and da_forward's consistency check.
+void derive_launch(da_plan* p) {
+  const int G = p->h_q / p->h_kv;
+  const bool mma = p->pack_gqa != 0 && G >= 2;
+  p->path = mma ? DA_PATH_MMA : DA_PATH_SCALAR;
+  p->rows_per_cta = mma ? (G <= 8 ? 8 : 16) : 1;
+  p->grid_x = p->num_splits;
+  p->grid_y = mma ? p->h_kv * static_cast<int32_t>(ceil_div(G, p->rows_per_cta)) : p->h_q;
+  p->grid_z = p->batch;
+  p->block_threads = kThreads;
+  p->cluster_x = p->combine_mode == DA_COMBINE_CLUSTER ? p->num_splits : 1;
+  p->smem_bytes = kSmemBytes;
+  p->workspace_bytes = p->num_splits > 1
+      ? static_cast<int64_t>(p->num_splits) * p->batch * p->h_q * (p->head_dim + 1) * 4
+      : 0;
+}
+
+bool combine_mode_valid(int mode, int s) {
+  switch (mode) {
+    case DA_COMBINE_NONE: return s == 1;
+    case DA_COMBINE_CLUSTER: return s >= 2 && s <= kMaxClusterSplits;
+    case DA_COMBINE_KERNEL: return s >= 2;
+    default: return false;
+  }
+}
+
+}  // namespace decattn
+
+using namespace decattn;
+
+extern "C" da_status da_plan_make(int32_t batch, int32_t h_q, int32_t h_kv, int32_t l_k,
+                                  int32_t head_dim, int32_t pack_gqa, int32_t sm_margin,
+                                  int32_t num_sms, int32_t policy, int32_t forced_splits,
+                                  da_plan* out) {
+  if (out == nullptr) return DA_ERR_INVALID_ARG;
+  if (batch < 1 || h_q < 1 || h_kv < 1 || l_k < 1 || head_dim < 1 || num_sms < 1)
+    return DA_ERR_INVALID_ARG;
+  if (h_q % h_kv != 0) return DA_ERR_INVALID_ARG;
+  if (sm_margin < 0 || sm_margin >= num_sms) return DA_ERR_INVALID_ARG;
+  if (pack_gqa != 0 && pack_gqa != 1) return DA_ERR_INVALID_ARG;
+  if (policy != DA_POLICY_GUARDED && policy != DA_POLICY_SEQ_AWARE && policy != DA_POLICY_FIXED)
+    return DA_ERR_INVALID_ARG;
+  if (policy == DA_POLICY_FIXED && (forced_splits < 1 || forced_splits > kMaxForcedSplits))
+    return DA_ERR_INVALID_ARG;
+  if (head_dim != kHeadDim) return DA_ERR_UNSUPPORTED;
+
+  da_plan p{};
+  p.batch = batch; p.h_q = h_q; p.h_kv = h_kv; p.l_k = l_k; p.head_dim = head_dim;
+  p.pack_gqa = pack_gqa; p.sm_margin = sm_margin; p.num_sms = num_sms;
+  p.policy = policy; p.forced_splits = policy == DA_POLICY_FIXED ? forced_splits : 0;
+
+  const int64_t G = h_q / h_kv;
+  p.usable_sms = num_sms - sm_margin;                                // C-amb-8
+  p.block_n = kPolicyBlockN;
+  p.num_n_blocks = static_cast<int32_t>(ceil_div(l_k, kPolicyBlockN));
+  p.num_m_blocks = static_cast<int32_t>(ceil_div(G, kPolicyBlockM));
+  const int64_t T = static_cast<int64_t>(batch) * h_kv * p.num_m_blocks;
+  if (T > INT32_MAX) return DA_ERR_INVALID_ARG;
+  p.total_mblocks = static_cast<int32_t>(T);
+
+  int s = 1, rule = 0;
+  decide(T, p.usable_sms, p.num_n_blocks, policy, forced_splits, &s, &rule);
+  p.num_splits = s;
+  p.rule = rule;
+  p.split_unit = kSplitUnit;
+  const int64_t units = ceil_div(l_k, kSplitUnit);
+  p.nonempty_splits = static_cast<int32_t>(units < s ? units : s);
+  p.combine_mode = s == 1 ? DA_COMBINE_NONE
+                 : (s <= kMaxClusterSplits ? DA_COMBINE_CLUSTER : DA_COMBINE_KERNEL);
+  derive_launch(&p);
+  *out = p;
+  return DA_OK;
+}
+
+extern "C" da_status da_plan_set_combine(da_plan* plan, int32_t combine_mode) {
+  if (plan == nullptr) return DA_ERR_INVALID_ARG;
+  if (!combine_mode_valid(combine_mode, plan->num_splits)) return DA_ERR_INVALID_ARG;
+  plan->combine_mode = combine_mode;
+  derive_launch(plan);
+  return DA_OK;
+}

@@ -1,0 +1,215 @@
+"""Host-side checks of the C ABI that need no GPU: the library loads, exports
+every symbol include/decattn.h declares, the planner matches the CPU oracle
+bit for bit, and argument validation returns the documented status codes
+before any CUDA call."""
+
+import itertools
+import os
+import random
+import re
+
+import pytest
+
+from oracle import policy as OP
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def L():
+    from paper_2604_00028_b200 import _lib
+    return _lib
+
+
+def test_library_exports_every_header_symbol(L):
+    with open(os.path.join(ROOT, "include", "decattn.h")) as f:
+        hdr = f.read()
+    declared = re.findall(r"DA_API\s+[\w\s\*]+?\b(da_\w+)\s*\(", hdr)
+    assert set(declared) == set(L.EXPORTED)
+    for name in declared:
+        assert hasattr(L.LIB, name), name
+    assert L.da_abi_version() == L.DA_ABI_VERSION
+    for code in range(-1, 8):
+        assert isinstance(L.da_status_string(code), str)
+
+
+def test_plan_struct_layout(L):
+    import ctypes
+    # 28 int32 fields + one int64 = 120 bytes (no padding before the int64 at offset 112)
+    assert ctypes.sizeof(L.da_plan) == 120
+    with open(os.path.join(ROOT, "include", "decattn.h")) as f:
+        hdr = f.read()
+    body = hdr[hdr.index("typedef struct da_plan"):hdr.index("} da_plan;")]
+    names = re.findall(r"\b([a-z_]+)(?=\s*[,;])", re.sub(r"/\*.*?\*/", "", body, flags=re.S))
+    assert names == [n for n, _ in L.da_plan._fields_]
+
+
+def _expected_launch(b, hq, hkv, pack, s):
+    G = hq // hkv
+    mma = bool(pack) and G >= 2
+    rows = (8 if G <= 8 else 16) if mma else 1
+    gy = hkv * -(-G // rows) if mma else hq
+    return (1 if mma else 0), rows, (s, gy, b)
+
+
+def _check_plan(L, b, hq, hkv, lk, pack, margin, sms, pol, forced=0):
+    p = L.da_plan_make(b, hq, hkv, lk, 128, pack, margin, sms, pol, forced)
+    s, rule = OP.num_splits(b, hq, hkv, lk, sms, margin, pol, forced)
+    assert (p.num_splits, p.rule) == (s, rule), (b, hq, hkv, lk, margin, sms, pol)
+    geo = OP.geometry(b, hq, hkv, lk, sms, margin)
+    assert (p.num_n_blocks, p.num_m_blocks, p.total_mblocks, p.usable_sms) == (
+        geo["nblk"], geo["num_m_blocks"], geo["T"], geo["U"])
+    path, rows, grid = _expected_launch(b, hq, hkv, pack, s)
+    assert (p.path, p.rows_per_cta, (p.grid_x, p.grid_y, p.grid_z)) == (path, rows, grid)
+    assert p.workspace_bytes == (s * b * hq * 129 * 4 if s > 1 else 0)
+    assert p.combine_mode == (0 if s == 1 else (1 if s <= 8 else 2))
+    assert p.nonempty_splits == min(s, -(-lk // 64))
+
+
+def test_plan_matches_oracle_dense_lk(L):
+    # every L_K up to 4096 at the BASELINE head shapes, both SM counts, both policies
+    for sms in (132, 148):
+        for (b, hkv) in ((1, 1), (1, 2), (2, 1), (1, 8), (8, 8), (4, 32)):
+            for lk in range(1, 4097):
+                for pol in ("guarded", "seq_aware"):
+                    _check_plan(L, b, 8 * hkv, hkv, lk, 1, 0, sms, pol)
+
+
+def test_plan_matches_oracle_grid(L):
+    Bs = list(range(1, 17)) + [24, 32, 64, 100, 128, 200, 256]
+    HKVs = (1, 2, 4, 8, 16, 32)
+    LKs = sorted({1, 2, 63, 64, 65, 127, 128, 129, 384, 385, 511, 512, 513, 640, 1000, 2047, 2048,
+                  2432, 2433, 2560, 4095, 4096, 8192, 16384, 32768, 65536, 131072, 262144}
+                 | {2 ** k + d for k in range(1, 19) for d in (-1, 0, 1)})
+    for sms in (132, 148):
+        for margin in (0, 4, 16, sms - 1):
+            for b, hkv, G in itertools.product(Bs, HKVs, (1, 8)):
+                for lk in LKs:
+                    for pol in ("guarded", "seq_aware"):
+                        _check_plan(L, b, G * hkv, hkv, lk, 1, margin, sms, pol)
+
+
+def test_plan_float_tie_regression(L):
+    # C-amb-3: FA3's float comparison gives 18 at (U=132, T=1, nblk=20); exact integers give 17.
+    for lk in (2433, 2500, 2560):
+        p = L.da_plan_make(1, 8, 1, lk, 128, 1, 0, 132, "guarded", 0)
+        assert p.num_splits == 17
+        assert OP.num_splits(1, 8, 1, lk, 132, 0, "guarded")[0] == 17
+
+
+def test_plan_random_shapes_and_fixed(L):
+    rng = random.Random(11)
+    for _ in range(20000):
+        hkv = rng.choice([1, 2, 3, 4, 8, 16, 32, 64])
+        G = rng.choice([1, 2, 3, 4, 5, 8, 12, 16, 32, 64, 128])
+        b = rng.randint(1, 300)
+        lk = rng.randint(1, 300000)
+        sms = rng.choice([132, 148, 7, 2, 1])
+        margin = rng.randint(0, sms - 1)
+        pack = rng.randint(0, 1)
+        pol = rng.choice(["guarded", "seq_aware", "fixed"])
+        forced = rng.randint(1, 256) if pol == "fixed" else 0
+        _check_plan(L, b, G * hkv, hkv, lk, pack, margin, sms, pol, forced)
+
+
+def test_paper_decisions_through_abi(L):
+    # Table 1 bold rows and Guard 2 at both SM counts.
+    for sms in (132, 148):
+        for hkv in (1, 2):
+            p = L.da_plan_make(1, 8 * hkv, hkv, 512, 128, 1, 0, sms, "seq_aware", 0)
+            assert (p.num_splits, p.rule) == (3, L.DA_RULE_LOW_TILE)
+            assert p.grid_x * p.grid_y * p.grid_z == 3 * hkv        # 3x the CTAs of s=1
+            g = L.da_plan_make(1, 8 * hkv, hkv, 512, 128, 1, 0, sms, "guarded", 0)
+            assert (g.num_splits, g.rule) == (1, L.DA_RULE_GUARD_NBLK4)
+        p = L.da_plan_make(1, 64, 8, 512, 128, 1, 0, sms, "seq_aware", 0)
+        assert (p.num_splits, p.rule) == (1, L.DA_RULE_GUARD2)
+
+
+@pytest.mark.parametrize("args", [
+    (0, 8, 1, 512), (1, 0, 1, 512), (1, 8, 0, 512), (1, 8, 1, 0), (1, 6, 4, 512)])
+def test_plan_invalid_shapes(L, args):
+    with pytest.raises(L.DecAttnError) as e:
+        L.da_plan_make(*args, 128, 1, 0, 148, "seq_aware", 0)
+    assert e.value.status == L.DA_ERR_INVALID_ARG
+
+
+def test_plan_invalid_knobs(L):
+    bad = [dict(sm_margin=148), dict(sm_margin=-1), dict(num_sms=0), dict(pack_gqa=2),
+           dict(policy=7), dict(policy=L.DA_POLICY_FIXED, forced_splits=0),
+           dict(policy=L.DA_POLICY_FIXED, forced_splits=257)]
+    for kw in bad:
+        args = dict(batch=1, h_q=8, h_kv=1, l_k=512, head_dim=128, pack_gqa=1, sm_margin=0,
+                    num_sms=148, policy=1, forced_splits=0)
+        args.update(kw)
+        with pytest.raises(L.DecAttnError) as e:
+            L.da_plan_make(**args)
+        assert e.value.status == L.DA_ERR_INVALID_ARG, kw
+    with pytest.raises(L.DecAttnError) as e:
+        L.da_plan_make(1, 8, 1, 512, 64, 1, 0, 148, 1, 0)
+    assert e.value.status == L.DA_ERR_UNSUPPORTED
+
+
+def test_set_combine_rules(L):
+    p = L.da_plan_make(1, 8, 1, 512, 128, 1, 0, 148, "seq_aware", 0)
+    assert p.combine_mode == L.DA_COMBINE_CLUSTER and p.cluster_x == 3
+    L.da_plan_set_combine(p, L.DA_COMBINE_KERNEL)
+    assert p.cluster_x == 1 and p.workspace_bytes == 3 * 8 * 129 * 4
+    with pytest.raises(L.DecAttnError):
+        L.da_plan_set_combine(p, L.DA_COMBINE_NONE)          # s = 3 needs a combine
+    q = L.da_plan_make(1, 8, 1, 512, 128, 1, 0, 148, "fixed", 9)
+    assert q.combine_mode == L.DA_COMBINE_KERNEL
+    with pytest.raises(L.DecAttnError):
+        L.da_plan_set_combine(q, L.DA_COMBINE_CLUSTER)       # cluster only for s <= 8
+
+
+# ---- da_forward / da_combine validation (fake device pointers: every check below
+#      returns before the library touches CUDA) -------------------------------------
+A = 1 << 20          # a 16-byte aligned fake address
+
+
+def _fwd(L, plan, **kw):
+    args = dict(q=A, k_cache=2 * A, v_cache=3 * A, l_cap=plan.l_k, cache_seqlens=None,
+                strides=None, softmax_scale=0.0, out_dtype=L.DA_BF16, out=4 * A, lse=5 * A,
+                workspace=None, workspace_bytes=0, stream=0)
+    args.update(kw)
+    with pytest.raises(L.DecAttnError) as e:
+        L.da_forward(plan, **args)
+    return e.value.status
+
+
+def test_forward_validation(L):
+    p = L.da_plan_make(1, 8, 1, 512, 128, 1, 0, 148, "fixed", 12)   # KERNEL combine
+    assert _fwd(L, p, q=None) == L.DA_ERR_INVALID_ARG
+    assert _fwd(L, p, out=None) == L.DA_ERR_INVALID_ARG
+    assert _fwd(L, p, l_cap=511) == L.DA_ERR_INVALID_ARG
+    assert _fwd(L, p, out_dtype=5) == L.DA_ERR_INVALID_ARG
+    assert _fwd(L, p, q=A + 2) == L.DA_ERR_ALIGNMENT
+    assert _fwd(L, p, k_cache=2 * A + 8) == L.DA_ERR_ALIGNMENT
+    assert _fwd(L, p, strides=(1024, 128, 65536, 128, 129, 65536, 128, 128)) == L.DA_ERR_ALIGNMENT
+    assert _fwd(L, p) == L.DA_ERR_WORKSPACE
+    assert _fwd(L, p, workspace=6 * A, workspace_bytes=p.workspace_bytes - 4) == L.DA_ERR_WORKSPACE
+    bad = L.da_plan.from_buffer_copy(p)
+    bad.grid_x = 3                                   # inconsistent with num_splits
+    assert _fwd(L, bad) == L.DA_ERR_INVALID_ARG
+    bad = L.da_plan.from_buffer_copy(p)
+    bad.head_dim = 64
+    assert _fwd(L, bad) == L.DA_ERR_UNSUPPORTED
+    bad = L.da_plan.from_buffer_copy(p)
+    bad.combine_mode = L.DA_COMBINE_NONE             # s = 12 cannot skip the combine
+    assert _fwd(L, bad) == L.DA_ERR_INVALID_ARG
+
+
+def test_combine_validation(L):
+    def st(**kw):
+        args = dict(num_splits=3, batch=1, h_q=8, head_dim=128, o_partial=A, o_split_stride=1024,
+                    lse_partial=2 * A, lse_split_stride=8, out_dtype=L.DA_BF16, out=3 * A, lse=4 * A,
+                    stream=0)
+        args.update(kw)
+        with pytest.raises(L.DecAttnError) as e:
+            L.da_combine(**args)
+        return e.value.status
+    assert st(num_splits=0) == L.DA_ERR_INVALID_ARG
+    assert st(o_partial=None) == L.DA_ERR_INVALID_ARG
+    assert st(head_dim=64) == L.DA_ERR_UNSUPPORTED
+    assert st(o_split_stride=1000) == L.DA_ERR_INVALID_ARG        # < B*H_Q*d
+    assert st(o_partial=A + 4) == L.DA_ERR_ALIGNMENT

@@ -1,0 +1,175 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the fp64 CPU oracle, element
+by element, on seeded synthetic inputs (SURVEY §8(c) parity matrix, item 2)."""
+
+import numpy as np
+import pytest
+import torch
+
+import synth
+from oracle import attention as OA
+from oracle import policy as OP
+from tests.helpers import assert_lse_close, assert_out_close
+
+pytestmark = pytest.mark.gpu
+
+
+def _dec():
+    import paper_2604_00028_b200 as dec
+    return dec
+
+
+def run_and_check(batch, h_q, h_kv, l_k, *, policy="seq_aware", forced=0, pack_gqa=True,
+                  variant="normal", l_cap=None, seed=1000, combine_mode=None, out_f32=False,
+                  check_partials=False, nan_tail=False):
+    dec = _dec()
+    inp = synth.make_inputs(batch, h_q, h_kv, l_k, l_cap=l_cap, seed=seed, variant=variant,
+                            device="cuda")
+    q, k, v, seq = inp["q"], inp["k"], inp["v"], inp["seqlens"]
+    if nan_tail:  # cache slots past each sequence hold garbage: must not leak into the result
+        for b in range(batch):
+            n = int(seq[b])
+            k[b, n:] = float("nan")
+            v[b, n:] = float("nan")
+    plan = dec.make_plan(batch, h_q, h_kv, l_k, pack_gqa=pack_gqa, policy=policy,
+                         forced_splits=forced, combine_mode=combine_mode)
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    # the planner's split count is the oracle's, bit for bit
+    s_ref, rule_ref = OP.num_splits(batch, h_q, h_kv, l_k, sms, 0, policy, forced)
+    assert (plan.num_splits, plan.rule) == (s_ref, rule_ref)
+    ws = dec.workspace_for(plan, q.device)
+    out, lse = dec.forward(plan, q, k, v, seq, workspace=ws,
+                           out_dtype=torch.float32 if out_f32 else torch.bfloat16)
+    torch.cuda.synchronize()
+    qn, kn, vn, sn = (synth.to_f64(t) for t in (q, k, v, seq))
+    if nan_tail:
+        kn = np.nan_to_num(kn, nan=0.0)
+        vn = np.nan_to_num(vn, nan=0.0)
+    ref_o, ref_l = OA.decode_attention(qn, kn, vn, sn)
+    assert_out_close(synth.to_f64(out), ref_o)
+    assert_lse_close(synth.to_f64(lse), ref_l)
+    if check_partials:
+        assert plan.combine_mode == dec.DA_COMBINE_KERNEL
+        s = plan.num_splits
+        nrow = batch * h_q * 128
+        ws_o = ws[: s * nrow].view(s, batch, h_q, 128)
+        ws_l = ws[s * nrow: s * nrow + s * batch * h_q].view(s, batch, h_q)
+        ranges = [OA.partition(int(n), s, OP.SPLIT_UNIT) for n in sn]
+        po, pl = OA.split_partials(qn, kn, vn, sn, ranges)
+        assert_out_close(synth.to_f64(ws_o), po, "partial o")
+        assert_lse_close(synth.to_f64(ws_l), pl, "partial lse")
+    return plan, out, lse
+
+
+# ---- BASELINE.json configurations -----------------------------------------
+@pytest.mark.parametrize("policy", ["guarded", "seq_aware"])
+@pytest.mark.parametrize("name", ["mqa_tiny", "llama70b", "llama70b_tp8"])
+def test_baseline_configs(name, policy):
+    cfg = synth.CONFIGS[name]
+    plan, _, _ = run_and_check(**cfg, policy=policy)
+    if name == "llama70b_tp8":
+        assert plan.num_splits == (3 if policy == "seq_aware" else 1)
+
+
+@pytest.mark.parametrize("cfg", synth.low_head_sweep(),
+                         ids=lambda c: f"B{c['batch']}_hkv{c['h_kv']}_L{c['l_k']}")
+def test_low_head_sweep(cfg):
+    for policy in ("guarded", "seq_aware"):
+        run_and_check(**cfg, policy=policy, seed=1002)
+
+
+# ---- forced split counts (the U-curve sweep shapes) ------------------
+@pytest.mark.parametrize("s", [1, 2, 3, 4, 5, 8, 16, 64])
+def test_forced_splits_tp8_slice(s):
+    run_and_check(1, 8, 1, 512, policy="fixed", forced=s)
+
+
+@pytest.mark.parametrize("s", [2, 3, 5, 16, 64])
+def test_forced_splits_kernel_combine_partials(s):
+    run_and_check(2, 16, 2, 700, policy="fixed", forced=s, combine_mode=2, check_partials=True,
+                  variant="ragged", seed=7)
+
+
+@pytest.mark.parametrize("s", [2, 3, 7, 8])
+def test_cluster_combine(s):
+    run_and_check(2, 8, 1, 1000, policy="fixed", forced=s, combine_mode=1, seed=11)
+
+
+# ---- head grouping / paths ----------------------------------------------------
+@pytest.mark.parametrize("h_q,h_kv", [(8, 8), (16, 2), (8, 2), (24, 2), (64, 2), (32, 1), (64, 1),
+                                      (32, 32), (12, 1)])
+def test_group_sizes_mma_path(h_q, h_kv):
+    run_and_check(2, h_q, h_kv, 300, seed=21)
+
+
+@pytest.mark.parametrize("h_q,h_kv", [(8, 1), (16, 2), (8, 8)])
+def test_scalar_path_unpacked(h_q, h_kv):
+    plan, _, _ = run_and_check(2, h_q, h_kv, 333, pack_gqa=False, seed=31)
+    assert plan.path == _dec().DA_PATH_SCALAR
+
+
+@pytest.mark.parametrize("pack", [True, False])
+@pytest.mark.parametrize("variant", ["peaked", "ragged"])
+def test_variants(variant, pack):
+    run_and_check(5, 16, 2, 777, variant=variant, pack_gqa=pack, seed=41, policy="fixed", forced=4)
+
+
+@pytest.mark.parametrize("pack", [True, False])
+def test_lcap_larger_and_nan_tail(pack):
+    run_and_check(3, 16, 2, 200, l_cap=400, variant="ragged", pack_gqa=pack, seed=51,
+                  nan_tail=True, policy="fixed", forced=3)
+
+
+def test_out_f32():
+    run_and_check(2, 16, 2, 513, out_f32=True, policy="fixed", forced=5, seed=61)
+
+
+def test_short_sequences_edge():
+    for lk in (1, 2, 63, 64, 65, 127, 129):
+        run_and_check(2, 8, 1, lk, seed=70 + lk)
+        run_and_check(1, 8, 1, lk, pack_gqa=False, seed=70 + lk)
+
+
+def test_strided_inputs():
+    dec = _dec()
+    torch.manual_seed(0)
+    B, HQ, HKV, L, D = 2, 16, 2, 300, 128
+    qbig = torch.randn(B, HQ, 2 * D, device="cuda").to(torch.bfloat16)
+    q = qbig[:, :, :D]                                    # q row stride 256 elements
+    kv = torch.randn(B, L, 2, HKV, D, device="cuda").to(torch.bfloat16)
+    k, v = kv[:, :, 0], kv[:, :, 1]                       # interleaved K/V cache
+    seq = torch.tensor([300, 123], dtype=torch.int32, device="cuda")
+    plan = dec.make_plan(B, HQ, HKV, L, policy="fixed", forced_splits=3)
+    out, lse = dec.forward(plan, q, k, v, seq)
+    torch.cuda.synchronize()
+    ref_o, ref_l = OA.decode_attention(*(synth.to_f64(t) for t in (q, k, v, seq)))
+    assert_out_close(synth.to_f64(out), ref_o)
+    assert_lse_close(synth.to_f64(lse), ref_l)
+
+
+def test_combine_kernel_direct():
+    dec = _dec()
+    rng = np.random.default_rng(3)
+    for s in (1, 2, 5, 33, 100):
+        o = rng.standard_normal((s, 3, 8, 128))
+        l = rng.standard_normal((s, 3, 8)) * 3
+        l[rng.random((s, 3, 8)) < 0.2] = -np.inf
+        l[:, 0, 0] = -np.inf                               # one row with every split empty
+        o[np.isneginf(l)] = 0.0
+        ot = torch.tensor(o, dtype=torch.float32, device="cuda")
+        lt = torch.tensor(l, dtype=torch.float32, device="cuda")
+        for dt in (torch.bfloat16, torch.float32):
+            out, lse = dec.combine(ot, lt, out_dtype=dt)
+            torch.cuda.synchronize()
+            ref_o, ref_l = OA.lse_combine(synth.to_f64(ot), synth.to_f64(lt))
+            assert_out_close(synth.to_f64(out), ref_o)
+            assert_lse_close(synth.to_f64(lse), ref_l)
+
+
+def test_deterministic_replay():
+    dec = _dec()
+    inp = synth.make_inputs(1, 8, 1, 512, device="cuda", seed=5)
+    plan = dec.make_plan(1, 8, 1, 512)
+    a, la = dec.forward(plan, inp["q"], inp["k"], inp["v"], inp["seqlens"])
+    b, lb = dec.forward(plan, inp["q"], inp["k"], inp["v"], inp["seqlens"])
+    torch.cuda.synchronize()
+    assert torch.equal(a, b) and torch.equal(la, lb)
