@@ -15,7 +15,8 @@ import os
 import torch
 
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG_DIR, "lib", "libdecattn.so")
+# DECATTN_LIB selects a development build variant (scripts/ A/B experiments only).
+LIB_PATH = os.environ.get("DECATTN_LIB") or os.path.join(PKG_DIR, "lib", "libdecattn.so")
 
 # ---- constants mirrored from include/decattn.h ----------------------------
 DA_OK, DA_ERR_INVALID_ARG, DA_ERR_UNSUPPORTED, DA_ERR_ALIGNMENT, DA_ERR_WORKSPACE, DA_ERR_CUDA = range(6)

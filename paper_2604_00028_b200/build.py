@@ -44,25 +44,30 @@ def _stale(target: str, deps) -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, ptxas_verbose: bool = False, quiet: bool = True) -> str:
-    os.makedirs(LIBDIR, exist_ok=True)
-    os.makedirs(BUILD, exist_ok=True)
+def build(force: bool = False, ptxas_verbose: bool = False, quiet: bool = True,
+          defines=(), lib: str | None = None, build_dir: str | None = None) -> str:
+    """Compile + link.  ``defines``/``lib``/``build_dir`` build development variants
+    (e.g. -DDECATTN_PREFETCH_TILES=0 into another .so); the default is the product library."""
+    lib = lib or LIB
+    bdir = build_dir or BUILD
+    os.makedirs(os.path.dirname(lib), exist_ok=True)
+    os.makedirs(bdir, exist_ok=True)
     hdrs = [os.path.join(CSRC, h) for h in HEADERS] + [os.path.join(INCLUDE, "decattn.h"),
                                                          os.path.abspath(__file__)]
     objs = []
     for src in SOURCES:
         s = os.path.join(CSRC, src)
-        o = os.path.join(BUILD, src + ".o")
+        o = os.path.join(bdir, src + ".o")
         objs.append(o)
         if force or _stale(o, [s] + hdrs):
-            cmd = [nvcc()] + ARCH + COMMON + ["-c", s, "-o", o]
+            cmd = [nvcc()] + ARCH + COMMON + [f"-D{d}" for d in defines] + ["-c", s, "-o", o]
             if src.endswith(".cu") and ptxas_verbose:
                 cmd += ["-Xptxas", "-v"]
             _run(cmd, quiet and not ptxas_verbose)
-    if force or _stale(LIB, objs):
-        cmd = [nvcc()] + ARCH + ["-shared", "-cudart", "static", "-o", LIB] + objs
+    if force or _stale(lib, objs):
+        cmd = [nvcc()] + ARCH + ["-shared", "-cudart", "static", "-o", lib] + objs
         _run(cmd, quiet)
-    return LIB
+    return lib
 
 
 def _run(cmd, quiet):

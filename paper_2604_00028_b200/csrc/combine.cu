@@ -29,7 +29,8 @@ constexpr float kLog2e = 1.4426950408889634f;
 
 __global__ void __launch_bounds__(kCombineRowsPerCta * 32)
     lse_combine_kernel(const CombineParams p) {
-  pdl_wait();
+  pdl_launch_dependents();   // the next step's forward may start its prologue
+  pdl_wait();                // partials are written by the preceding forward kernel
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int row = blockIdx.x * kCombineRowsPerCta + warp;
   if (row >= p.rows) return;

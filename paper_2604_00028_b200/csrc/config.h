@@ -16,12 +16,22 @@ constexpr int kMaxForcedSplits = 256;
 constexpr int kHeadDim = 128;          // v1 supports d = 128 only
 constexpr int kTileN = 64;             // tokens per pipeline stage (= split unit)
 constexpr int kSplitUnit = kTileN;     // partition unit (C-pol item 6)
-constexpr int kStages = 6;             // TMA ring depth
-constexpr int kConsumerWarps = 4;      // warp w consumes stages w, w+4, ...
-constexpr int kThreads = (kConsumerWarps + 1) * 32;   // + 1 TMA producer warp
-constexpr int kStageBytes = 4 * kTileN * 128;         // K|V x two 64-column halves, 128 B rows
-constexpr int kSmemBytes = kStages * kStageBytes + 1024;  // + 1024 B alignment slack (SWIZZLE_128B)
+constexpr int kStageBytes = 4 * kTileN * 128;   // K|V x two 64-dim halves, 128 B rows = 32 KB
+// Each consumer warp owns exactly one ring stage (stages == consumer warps), so
+// a warp never waits on a stage another warp consumes: no mbarrier phase aliasing.
+constexpr int kStagesDefault = 6;      // s == 1 and workspace-combine kernels: 192 KB ring
+constexpr int kStagesCluster = 5;      // cluster-combine kernels: 160 KB ring + DSMEM slots
 constexpr int kMaxClusterSplits = 8;   // portable cluster size
+constexpr int kSlotFloats = 16 * kHeadDim + 32;           // one pushed CTA partial: O[16][128], m[16], l[16]
+constexpr int kSlotBytes = kSlotFloats * 4;
+constexpr int threads_for(int stages) { return (stages + 1) * 32; }   // + 1 TMA producer warp
+constexpr int smem_for(int stages, bool cluster) {
+  return stages * kStageBytes + (cluster ? (kMaxClusterSplits - 1) * kSlotBytes : 0) + 1024;
+}
+#ifndef DECATTN_PREFETCH_TILES
+#define DECATTN_PREFETCH_TILES 0
+#endif
+constexpr int kPrefetchTiles = DECATTN_PREFETCH_TILES;  // speculative L2 prefetch before griddepcontrol.wait
 constexpr int kCombineRowsPerCta = 4;  // combine kernel: one warp per (b, h) row
 
 }  // namespace decattn

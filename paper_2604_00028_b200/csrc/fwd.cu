@@ -8,11 +8,12 @@
 // Thread Blocks"), s = 3 triples them.
 //
 // Inside a CTA:
-//   warp 4      TMA producer: one elected lane streams 64-token K/V tiles
-//               (4 boxes of 64 tokens x 64 dims, 128B-swizzled) through a
-//               6-stage mbarrier ring (step a3, KV streaming).
-//   warps 0..3  consumers: warp w owns tiles w, w+4, ... and keeps its own
-//               online-softmax state (steps a4-a6):
+//   warp NS     TMA producer: one elected lane streams 64-token K/V tiles
+//               (4 boxes of 64 tokens x 64 dims, 128B-swizzled) through an
+//               NS-stage mbarrier ring (step a3, KV streaming); NS = 6, or 5
+//               for cluster kernels (their DSMEM push slots need the room).
+//   warps 0..NS-1  consumers: warp w owns ring stage w, i.e. tiles w, w+NS, ...,
+//               and keeps its own online-softmax state (steps a4-a6):
 //               MMA path  S^T = K Q^T and O^T += V^T P^T with
 //                         mma.sync.m16n8k16 (bf16 -> fp32): tokens and head
 //                         dims fill the M = 16 side, the G query rows the
@@ -21,11 +22,14 @@
 //                         movmatrix.trans.
 //               scalar    lane-per-token fp32 dot products, warp-shuffle
 //                         max / sum, lane-per-4-dims PV.
-//   epilogue    the four warps' (m, l, O) merge in shared memory; then
+//   epilogue    the consumer warps' (m, l, O) merge in shared memory; then
 //               s == 1   : bf16/fp32 out + lse written directly (a7);
-//               CLUSTER  : the s CTAs (one thread-block cluster) merge
-//                          through DSMEM - the LSE combine (a8) with no
-//                          workspace and no second launch;
+//               CLUSTER  : the s CTAs form one thread-block cluster; ranks
+//                          1..s-1 push (m, l, O) into rank 0's shared memory
+//                          with st.async (bytes counted on rank 0's mbarrier)
+//                          and rank 0 does the LSE combine (a8): no
+//                          workspace, no second launch, no cluster-wide barrier
+//                          on the exit path;
 //               KERNEL   : normalised fp32 partials + lse go to the
 //                          workspace for lse_combine_kernel (combine.cu).
 // Scores are kept in the log2 domain (scale * log2 e folded into one FMUL);
@@ -234,27 +238,30 @@ __device__ __forceinline__ void store_out(const FwdParams& p, size_t row, int d4
 
 // ---------------------------------------------------------------------------
 // The kernel.  kPath: DA_PATH_SCALAR / DA_PATH_MMA; kNB: g-blocks of 8 query
-// rows (MMA path); kCombine: da_combine_mode.
+// rows (MMA path); kCombine: da_combine_mode; NS: ring stages = consumer warps.
 // ---------------------------------------------------------------------------
-template <int kPath, int kNB, int kCombine>
-__global__ void __launch_bounds__(kThreads, 1)
+template <int kPath, int kNB, int kCombine, int NS>
+__global__ void __launch_bounds__(threads_for(NS), 1)
     split_kv_fwd_kernel(const __grid_constant__ CUtensorMap tmap_k,
                         const __grid_constant__ CUtensorMap tmap_v, const FwdParams p) {
-  constexpr int R = kPath == DA_PATH_MMA ? 8 * kNB : 1;   // query rows of this CTA
+  constexpr int NW = NS;                                   // consumer warps; warp w owns stage w
+  constexpr int R = kPath == DA_PATH_MMA ? 8 * kNB : 1;    // query rows of this CTA
+  constexpr int kIters = (R * 32 + NW * 32 - 1) / (NW * 32);
+  constexpr bool kCluster = kCombine == DA_COMBINE_CLUSTER;
   extern __shared__ uint8_t smem_raw[];
-  __shared__ __align__(8) uint64_t full_bar[kStages];
-  __shared__ __align__(8) uint64_t empty_bar[kStages];
+  __shared__ __align__(8) uint64_t full_bar[NS];
+  __shared__ __align__(8) uint64_t empty_bar[NS];
+  __shared__ __align__(8) uint64_t push_bar;              // CLUSTER: rank 0 collects s - 1 pushes
 
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t sbase = (raw + 1023u) & ~1023u;
   float* const epi = reinterpret_cast<float*>(smem_raw + (sbase - raw));
-  // epilogue carve-up (aliases the pipeline ring once every tile is consumed)
-  float* const epi_o = epi;                                        // [NW][16][kEpiStride]
-  float* const epi_m = epi_o + kConsumerWarps * 16 * kEpiStride;   // [NW][16]
-  float* const epi_l = epi_m + kConsumerWarps * 16;                // [NW][16]
-  float* const cta_o = epi_l + kConsumerWarps * 16;                // [16][kEpiStride]
-  float* const cta_m = cta_o + 16 * kEpiStride;                    // [16]
-  float* const cta_l = cta_m + 16;                                 // [16]
+  // epilogue carve-up (aliases the ring once every tile is consumed)
+  float* const epi_o = epi;                                // [NW][16][kEpiStride]
+  float* const epi_m = epi_o + NW * 16 * kEpiStride;       // [NW][16]
+  float* const epi_l = epi_m + NW * 16;                    // [NW][16]
+  // CLUSTER push slots (past the ring: written by peers while this CTA still streams)
+  float* const slots = epi + NS * kStageBytes / 4;         // [s-1][kSlotFloats]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int split = blockIdx.x, b = blockIdx.z;
@@ -270,21 +277,48 @@ __global__ void __launch_bounds__(kThreads, 1)
     rows_valid = 1;
   }
 
+  const uint32_t rank = kCluster ? cluster_ctarank() : 0u;
   if (threadIdx.x == 0) {
 #pragma unroll
-    for (int i = 0; i < kStages; ++i) {
+    for (int i = 0; i < NS; ++i) {
       mbar_init(smem_u32(&full_bar[i]), 1);
       mbar_init(smem_u32(&empty_bar[i]), 1);
     }
+    if constexpr (kCluster) {
+      // rank 0 expects (s - 1) pushes of rows_valid x (O row + m, l) bytes via st.async
+      mbar_init(smem_u32(&push_bar), 1);
+      if (rank == 0)
+        mbar_arrive_expect_tx(smem_u32(&push_bar),
+                              static_cast<uint32_t>((p.num_splits - 1) * rows_valid * (kHeadDim * 4 + 8)));
+    }
     fence_mbarrier_init();
   }
-  if (warp == kConsumerWarps && lane == 0) {
+  if (warp == NW && lane == 0) {
     prefetch_tmap(&tmap_k);
     prefetch_tmap(&tmap_v);
+    // Speculative L2 prefetch of this split's first tiles, assuming the full length
+    // (plan l_k): issued before griddepcontrol.wait, so it overlaps the tail of the
+    // previous kernel.  Always safe: L2 is the point of coherence, a prefetch never
+    // returns data to the SM.
+    const int n_spec = min(p.l_default, p.l_cap);
+    const int64_t nu_spec = (n_spec + kTileN - 1) / kTileN;
+    const int v0 = static_cast<int>(static_cast<int64_t>(split) * nu_spec / p.num_splits);
+    const int v1 = static_cast<int>(static_cast<int64_t>(split + 1) * nu_spec / p.num_splits);
+    for (int i = 0; i < min(v1 - v0, kPrefetchTiles); ++i) {
+      const int t = (v0 + i) * kTileN;
+      tma_prefetch_4d(&tmap_k, 0, kvh, t, b);
+      tma_prefetch_4d(&tmap_k, 64, kvh, t, b);
+      tma_prefetch_4d(&tmap_v, 0, kvh, t, b);
+      tma_prefetch_4d(&tmap_v, 64, kvh, t, b);
+    }
   }
   __syncthreads();
+  if constexpr (kCluster) cluster_arrive_relaxed();   // "my push barrier is initialised"
 
-  // Inputs (q, KV cache, lengths) may be written by the preceding kernel.
+  // Let the next kernel in the stream start its prologue now (it waits in its own
+  // griddepcontrol.wait for this grid to finish), then wait for our inputs, which
+  // the preceding kernel may still be writing.
+  pdl_launch_dependents();
   pdl_wait();
 
   // ---- this split's token range (C-pol item 6): units of kTileN tokens
@@ -296,13 +330,14 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int t0 = u0 * kTileN;
   const int t_end = min(u1 * kTileN, n);
   const int n_tiles = u1 - u0;
+  const int n_active = min(NW, n_tiles);   // consumer warps that received at least one tile
 
-  if (warp == kConsumerWarps) {
+  if (warp == NW) {
     // ================= TMA producer =================
     if (lane == 0) {
       for (int i = 0; i < n_tiles; ++i) {
-        const int st = i % kStages;
-        if (i >= kStages) mbar_wait(smem_u32(&empty_bar[st]), ((i / kStages) - 1) & 1);
+        const int st = i % NS;
+        if (i >= NS) mbar_wait(smem_u32(&empty_bar[st]), ((i / NS) - 1) & 1);
         const uint32_t fb = smem_u32(&full_bar[st]);
         mbar_arrive_expect_tx(fb, kStageBytes);
         const uint32_t dst = sbase + st * kStageBytes;
@@ -314,8 +349,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else {
-    // ================= consumers =================
+    // ================= consumers: warp w handles tiles w, w + NW, ... (all in stage w) =======
     const uint16_t* qrow = p.q + static_cast<int64_t>(b) * p.q_sb;
+    const uint32_t sK = sbase + warp * kStageBytes;
+    const uint32_t sV = sK + 2 * kHalfBytes;
+    const uint32_t fb = smem_u32(&full_bar[warp]);
+    const uint32_t eb = smem_u32(&empty_bar[warp]);
     if constexpr (kPath == DA_PATH_MMA) {
       uint32_t qf[8][kNB][2];
 #pragma unroll
@@ -340,12 +379,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
       for (int nb = 0; nb < kNB; ++nb) m[nb][0] = m[nb][1] = kNegInf, l[nb][0] = l[nb][1] = 0.f;
 
-      for (int i = warp; i < n_tiles; i += kConsumerWarps) {
-        const int st = i % kStages;
-        mbar_wait(smem_u32(&full_bar[st]), (i / kStages) & 1);
+      for (int i = warp, round = 0; i < n_tiles; i += NW, ++round) {
+        mbar_wait(fb, round & 1);
         const int valid = min(kTileN, t_end - (t0 + i * kTileN));
-        const uint32_t sK = sbase + st * kStageBytes;
-        const uint32_t sV = sK + 2 * kHalfBytes;
         if (valid < kTileN) {
           // rows past the range may hold anything (even NaN): zero them so P = 0 rows stay 0
           for (int idx = lane; idx < (kTileN - valid) * 16; idx += 32) {
@@ -357,7 +393,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         mma_tile<kNB>(sK, sV, valid, qf, o, m, l, p.scale_log2, lane);
         __syncwarp();
-        if (lane == 0) mbar_arrive(smem_u32(&empty_bar[st]));
+        if (lane == 0) mbar_arrive(eb);
       }
       // finish l: sum the partial sums of the 8 lanes that share a g column
 #pragma unroll
@@ -370,7 +406,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           v += __shfl_xor_sync(0xffffffffu, v, 16);
           l[nb][c] = v;
         }
-      asm volatile("bar.sync 1, %0;" ::"n"(kConsumerWarps * 32) : "memory");  // ring no longer read
+      asm volatile("bar.sync 1, %0;" ::"n"(NW * 32) : "memory");  // ring no longer read
       if (lane < 4) {
 #pragma unroll
         for (int nb = 0; nb < kNB; ++nb)
@@ -398,18 +434,16 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int c = 0; c < 16; ++c) qv[c] = __ldg(q4 + c);
       float o[4] = {0.f, 0.f, 0.f, 0.f};
       float m = kNegInf, l = 0.f;
-      for (int i = warp; i < n_tiles; i += kConsumerWarps) {
-        const int st = i % kStages;
-        mbar_wait(smem_u32(&full_bar[st]), (i / kStages) & 1);
+      for (int i = warp, round = 0; i < n_tiles; i += NW, ++round) {
+        mbar_wait(fb, round & 1);
         const int valid = min(kTileN, t_end - (t0 + i * kTileN));
-        const uint32_t sK = sbase + st * kStageBytes;
-        scalar_tile(sK, sK + 2 * kHalfBytes, valid, qv, o, m, l, p.scale_log2, lane);
+        scalar_tile(sK, sV, valid, qv, o, m, l, p.scale_log2, lane);
         __syncwarp();
-        if (lane == 0) mbar_arrive(smem_u32(&empty_bar[st]));
+        if (lane == 0) mbar_arrive(eb);
       }
 #pragma unroll
       for (int off = 16; off > 0; off >>= 1) l += __shfl_xor_sync(0xffffffffu, l, off);
-      asm volatile("bar.sync 1, %0;" ::"n"(kConsumerWarps * 32) : "memory");
+      asm volatile("bar.sync 1, %0;" ::"n"(NW * 32) : "memory");
       if (lane == 0) {
         epi_m[warp * 16] = m;
         epi_l[warp * 16] = l;
@@ -419,40 +453,57 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   }
 
-  if constexpr (kCombine == DA_COMBINE_KERNEL) pdl_launch_dependents();
-
-  // ================= merge the consumer warps (all rows of this CTA) =================
-  if (warp < kConsumerWarps) {
-    asm volatile("bar.sync 1, %0;" ::"n"(kConsumerWarps * 32) : "memory");
-    for (int e = threadIdx.x; e < R * 32; e += kConsumerWarps * 32) {
+  // ================= merge the consumer warps; emit / push (a7, a8) =================
+  // Element e = (row g, float4 column d4) of this CTA's [R x 128] result is handled by
+  // consumer thread e mod (NW*32); kIters passes cover all R*32 elements.
+  float own_m[kIters], own_l[kIters];
+  float4 own_o[kIters];
+  if (warp < NW) {
+    asm volatile("bar.sync 1, %0;" ::"n"(NW * 32) : "memory");
+    if constexpr (kCluster) cluster_wait();     // every peer's push barrier is initialised
+#pragma unroll
+    for (int it = 0; it < kIters; ++it) {
+      const int e = threadIdx.x + it * NW * 32;
       const int g = e >> 5, d4 = e & 31;
-      if (g >= rows_valid) continue;
+      own_m[it] = kNegInf;
+      own_l[it] = 0.f;
+      own_o[it] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (e >= R * 32 || g >= rows_valid) continue;
       float M = kNegInf;
 #pragma unroll
-      for (int w = 0; w < kConsumerWarps; ++w) M = fmaxf(M, epi_m[w * 16 + g]);
-      float L = 0.f;
+      for (int w = 0; w < NW; ++w)
+        if (w < n_active) M = fmaxf(M, epi_m[w * 16 + g]);
+      float Lsum = 0.f;
       float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-      for (int w = 0; w < kConsumerWarps; ++w) {
+      for (int w = 0; w < NW; ++w) {
+        if (w >= n_active) break;
         const float mw = epi_m[w * 16 + g];
         const float f = mw == kNegInf ? 0.f : ex2(mw - M);
-        L = fmaf(f, epi_l[w * 16 + g], L);
+        Lsum = fmaf(f, epi_l[w * 16 + g], Lsum);
         const float4 ow = *reinterpret_cast<const float4*>(&epi_o[(w * 16 + g) * kEpiStride + 4 * d4]);
         acc.x = fmaf(f, ow.x, acc.x);
         acc.y = fmaf(f, ow.y, acc.y);
         acc.z = fmaf(f, ow.z, acc.z);
         acc.w = fmaf(f, ow.w, acc.w);
       }
-      if constexpr (kCombine == DA_COMBINE_CLUSTER) {
-        *reinterpret_cast<float4*>(&cta_o[g * kEpiStride + 4 * d4]) = acc;
-        if (d4 == 0) {
-          cta_m[g] = M;
-          cta_l[g] = L;
+      if constexpr (kCluster) {
+        if (rank == 0) {
+          own_m[it] = M;
+          own_l[it] = Lsum;
+          own_o[it] = acc;
+        } else {
+          // push (M, L, unnormalised O) into rank 0's slot rank-1 through DSMEM; each
+          // st.async counts its bytes on rank 0's push barrier (no fence, no arrive)
+          const uint32_t slot = smem_u32(slots + (rank - 1) * kSlotFloats);
+          const uint32_t rbar = mapa(smem_u32(&push_bar), 0);
+          st_async_v4(mapa(slot + (g * kHeadDim + 4 * d4) * 4, 0), acc, rbar);
+          if (d4 == 0) st_async_v2(mapa(slot + (16 * kHeadDim + 2 * g) * 4, 0), M, Lsum, rbar);
         }
       } else {
-        const float inv = L > 0.f ? 1.f / L : 0.f;
+        const float inv = Lsum > 0.f ? 1.f / Lsum : 0.f;
         const float4 v = make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
-        const float lse_v = L > 0.f ? (M + lg2(L)) * kLn2 : kNegInf;
+        const float lse_v = Lsum > 0.f ? (M + lg2(Lsum)) * kLn2 : kNegInf;
         const size_t row = static_cast<size_t>(b) * p.h_q + hq0 + g;
         if constexpr (kCombine == DA_COMBINE_NONE) {
           store_out(p, row, d4, v);
@@ -464,53 +515,56 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
+  } else if constexpr (kCluster) {
+    cluster_wait();                               // producer warp: pair its early arrive
   }
 
-  if constexpr (kCombine == DA_COMBINE_CLUSTER) {
-    // ================= LSE combine across the s CTAs of the cluster (a8) =================
-    cluster_sync();
-    if (warp < kConsumerWarps) {
-      const int s = p.num_splits;
-      const int rank = static_cast<int>(cluster_ctarank());
-      const uint32_t m_addr = smem_u32(cta_m), l_addr = smem_u32(cta_l), o_addr = smem_u32(cta_o);
-      for (int e = rank + s * static_cast<int>(threadIdx.x); e < R * 32; e += s * kConsumerWarps * 32) {
-        const int g = e >> 5, d4 = e & 31;
-        if (g >= rows_valid) continue;
-        float mr[kMaxClusterSplits];
-        float M = kNegInf;
-#pragma unroll
-        for (int r = 0; r < kMaxClusterSplits; ++r) {
-          mr[r] = r < s ? ld_dsmem_f32(mapa(m_addr + 4 * g, r)) : kNegInf;
-          M = fmaxf(M, mr[r]);
+  if constexpr (kCluster) {
+    if (warp < NW && rank == 0) {
+      {
+        // rank 0: wait for the s - 1 pushes, then merge (LSE combine, a8) and emit
+        const uint32_t pb = smem_u32(&push_bar);
+        while (!mbar_try_wait_cluster(pb, 0)) {
         }
-        float L = 0.f;
-        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+        const int s = p.num_splits;
 #pragma unroll
-        for (int r = 0; r < kMaxClusterSplits; ++r) {
-          if (r < s && mr[r] != kNegInf) {
-            const float f = ex2(mr[r] - M);
-            L = fmaf(f, ld_dsmem_f32(mapa(l_addr + 4 * g, r)), L);
-            const float4 orr = ld_dsmem_v4(mapa(o_addr + (g * kEpiStride + 4 * d4) * 4, r));
+        for (int it = 0; it < kIters; ++it) {
+          const int e = threadIdx.x + it * NW * 32;
+          const int g = e >> 5, d4 = e & 31;
+          if (e >= R * 32 || g >= rows_valid) continue;
+          float M = own_m[it];
+          for (int r = 1; r < s; ++r) M = fmaxf(M, slots[(r - 1) * kSlotFloats + 16 * kHeadDim + 2 * g]);
+          const float f0 = own_m[it] == kNegInf ? 0.f : ex2(own_m[it] - M);
+          float Lsum = f0 * own_l[it];
+          float4 acc = make_float4(f0 * own_o[it].x, f0 * own_o[it].y, f0 * own_o[it].z, f0 * own_o[it].w);
+          for (int r = 1; r < s; ++r) {
+            const float* sl = slots + (r - 1) * kSlotFloats;
+            const float mr = sl[16 * kHeadDim + 2 * g];
+            const float f = mr == kNegInf ? 0.f : ex2(mr - M);
+            Lsum = fmaf(f, sl[16 * kHeadDim + 2 * g + 1], Lsum);
+            const float4 orr = *reinterpret_cast<const float4*>(sl + g * kHeadDim + 4 * d4);
             acc.x = fmaf(f, orr.x, acc.x);
             acc.y = fmaf(f, orr.y, acc.y);
             acc.z = fmaf(f, orr.z, acc.z);
             acc.w = fmaf(f, orr.w, acc.w);
           }
+          const float inv = Lsum > 0.f ? 1.f / Lsum : 0.f;
+          const size_t row = static_cast<size_t>(b) * p.h_q + hq0 + g;
+          store_out(p, row, d4, make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv));
+          if (d4 == 0 && p.lse != nullptr) p.lse[row] = Lsum > 0.f ? (M + lg2(Lsum)) * kLn2 : kNegInf;
         }
-        const float inv = L > 0.f ? 1.f / L : 0.f;
-        const size_t row = static_cast<size_t>(b) * p.h_q + hq0 + g;
-        store_out(p, row, d4, make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv));
-        if (d4 == 0 && p.lse != nullptr) p.lse[row] = L > 0.f ? (M + lg2(L)) * kLn2 : kNegInf;
       }
     }
-    cluster_sync();  // keep every CTA's shared memory alive until all remote reads are done
   }
 }
 
 template <int kPath, int kNB, int kCombine>
 cudaError_t launch_impl(const da_plan& plan, const CUtensorMap& tk, const CUtensorMap& tv,
                         const FwdParams& p, cudaStream_t stream) {
-  auto kern = split_kv_fwd_kernel<kPath, kNB, kCombine>;
+  constexpr bool kCluster = kCombine == DA_COMBINE_CLUSTER;
+  constexpr int NS = kCluster ? kStagesCluster : kStagesDefault;
+  constexpr int kSmem = smem_for(NS, kCluster);
+  auto kern = split_kv_fwd_kernel<kPath, kNB, kCombine, NS>;
   // One-time (per device) opt-in to > 48 KB of dynamic shared memory.
   static std::atomic<uint64_t> attr_done{0};
   int dev = 0;
@@ -518,21 +572,21 @@ cudaError_t launch_impl(const da_plan& plan, const CUtensorMap& tk, const CUtens
   if (err != cudaSuccess) return err;
   const uint64_t bit = 1ull << (dev & 63);
   if ((attr_done.load(std::memory_order_acquire) & bit) == 0) {
-    err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+    err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
     if (err != cudaSuccess) return err;
     attr_done.fetch_or(bit, std::memory_order_acq_rel);
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(plan.grid_x, plan.grid_y, plan.grid_z);
-  cfg.blockDim = dim3(kThreads, 1, 1);
-  cfg.dynamicSmemBytes = kSmemBytes;
+  cfg.blockDim = dim3(threads_for(NS), 1, 1);
+  cfg.dynamicSmemBytes = kSmem;
   cfg.stream = stream;
   cudaLaunchAttribute attrs[2];
   int na = 0;
   attrs[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attrs[na].val.programmaticStreamSerializationAllowed = 1;
   ++na;
-  if (kCombine == DA_COMBINE_CLUSTER) {
+  if (kCluster) {
     attrs[na].id = cudaLaunchAttributeClusterDimension;
     attrs[na].val.clusterDim.x = static_cast<unsigned>(plan.num_splits);
     attrs[na].val.clusterDim.y = 1;

@@ -70,9 +70,11 @@ void derive_launch(da_plan* p) {
   p->grid_x = p->num_splits;
   p->grid_y = mma ? p->h_kv * static_cast<int32_t>(ceil_div(G, p->rows_per_cta)) : p->h_q;
   p->grid_z = p->batch;
-  p->block_threads = kThreads;
-  p->cluster_x = p->combine_mode == DA_COMBINE_CLUSTER ? p->num_splits : 1;
-  p->smem_bytes = kSmemBytes;
+  const bool cluster = p->combine_mode == DA_COMBINE_CLUSTER;
+  const int stages = cluster ? kStagesCluster : kStagesDefault;
+  p->block_threads = threads_for(stages);
+  p->cluster_x = cluster ? p->num_splits : 1;
+  p->smem_bytes = smem_for(stages, cluster);
   p->workspace_bytes = p->num_splits > 1
       ? static_cast<int64_t>(p->num_splits) * p->batch * p->h_q * (p->head_dim + 1) * 4
       : 0;
