@@ -1,0 +1,559 @@
+#!/usr/bin/env python3
+"""bench.py - decode-attention benchmark for the B200 path (contract: DESIGN.md §7).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload NAME] [--impl ours|reference]
+
+One JSON line on rank 0.  A *step* is one pass of the whole hot path (SURVEY
+§8(a) rows a1-a8) over one batch: the plan (precomputed per shape, like the
+scheduler metadata the paper measures with) and one da_forward call,
+i.e. the split-KV kernel plus the LSE combine when s > 1.
+
+Headline (N = 1): BASELINE.json configs[1], Llama-3.1-70B decode B=1 H_Q=64
+H_KV=8 d=128 L_K=512 bf16, sequence-aware policy.  ``value`` = aggregate
+algorithmic HBM GB/s over all ranks (K+V+q+out+lse bytes / step time), with
+inputs resident in HBM; ``us_per_step`` the same measurement as time.  Timing:
+W eager warm-up steps, then K steps captured in ONE CUDA graph ("CUDA
+Graph replay") and timed with CUDA events between barrier + synchronize; the
+max over ranks is reported.  L2: every step reads a different KV buffer of a
+rotation totalling > 2x L2, and L2 is scrubbed (256 MB write) before each
+timed replay.
+
+N > 1: weak scaling by batch (rank r runs its own B=1 sequence: global batch =
+N, "shards by batch x KV-head"); no collective on the data path.
+``--workload long_context`` with N > 1 shards the sequence instead (one NCCL
+all-gather + the combine kernel per step; strong scaling).
+
+Extras (N = 1): guarded-vs-seq-aware A/B (interleaved graph replays, medians)
+on the headline, on its 8-way tensor-parallel slice (H_Q=8, H_KV=1)
+where the policies differ (s = 1 vs 3), and the KV-streaming-bound configs
+(high-load B=128 L_K=8192; long-context L_K=131072) with their roofline
+fractions.  ``--impl reference`` times the fp64 CPU oracle instead (the
+reference arm of this tier; rank 0 only).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import torch
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+METRIC = json.load(open(os.path.join(ROOT, "BASELINE.json")))["metric"]
+HEAD_DIM = 128
+WORKLOADS = {
+    "llama70b": dict(synth.CONFIGS["llama70b"]),
+    "llama70b_tp8": dict(synth.CONFIGS["llama70b_tp8"]),
+    "mqa_tiny": dict(synth.CONFIGS["mqa_tiny"]),
+    "high_load": dict(synth.CONFIGS["high_load"]),
+    "long_context": dict(synth.CONFIGS["long_context"]),
+}
+FALLBACK_HBM_GBS = 6650.0   # /opt/skills/guides/B200_PROFILING.md fallback (used only if MEASURED_PEAKS.json is absent)
+
+
+# ----------------------------------------------------------------------------------------------
+def alg_bytes(batch, h_q, h_kv, l_k, d=HEAD_DIM):
+    """Algorithmic bytes of one step: K+V bf16 + q bf16 + out bf16 + lse fp32."""
+    return 4 * batch * l_k * h_kv * d + 2 * batch * h_q * d + 2 * batch * h_q * d + 4 * batch * h_q
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        p = json.load(open(path))
+        return float(p["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (copy, burst)"
+    return FALLBACK_HBM_GBS, "fallback 6.65 TB/s (B200_PROFILING.md)"
+
+
+def traffic_record():
+    """Per-launch DRAM bytes of the dominant kernel from the committed ncu capture, if any."""
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(path):
+        try:
+            return json.load(open(path))
+        except Exception:
+            return {}
+    return {}
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 100 ms while running."""
+
+    FIELDS = ("clocks.sm", "clocks.max.sm", "clocks_event_reasons.hw_slowdown",
+              "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown",
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index: int):
+        props = torch.cuda.get_device_properties(device_index)
+        self.bus = f"{props.pci_domain_id:08X}:{props.pci_bus_id:02X}:{props.pci_device_id:02X}.0"
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", self.bus, "--query-gpu=" + ",".join(self.FIELDS),
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            self.thread.join(timeout=2)
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) != len(self.FIELDS):
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for name, val in zip(names, parts[2:]):
+                if val.lower() == "active":
+                    reasons.add(name)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------------------------
+class Workload:
+    """Device-resident inputs of one config with a rotation of KV buffers (> 2x L2 total)."""
+
+    def __init__(self, cfg, device, seed, l2_bytes, max_rot_bytes=300 << 20, uniform=True):
+        self.cfg = cfg
+        b, hq, hkv, lk = cfg["batch"], cfg["h_q"], cfg["h_kv"], cfg["l_k"]
+        kv_bytes = 4 * b * lk * hkv * HEAD_DIM
+        self.nbuf = max(1, min(1024, -(-2 * l2_bytes // kv_bytes))) if kv_bytes < 2 * l2_bytes else 1
+        if kv_bytes * self.nbuf > max(max_rot_bytes, 2 * l2_bytes + kv_bytes):
+            self.nbuf = max(1, (2 * l2_bytes) // kv_bytes + 1)
+        base = synth.make_inputs(b, hq, hkv, lk, device=device, seed=seed)
+        self.q = base["q"]
+        # one contiguous allocation per K and V: [nbuf, B, L, H_KV, d]
+        self.k = base["k"].unsqueeze(0).repeat(self.nbuf, 1, 1, 1, 1) if self.nbuf > 1 else base["k"].unsqueeze(0)
+        self.v = base["v"].unsqueeze(0).repeat(self.nbuf, 1, 1, 1, 1) if self.nbuf > 1 else base["v"].unsqueeze(0)
+        # uniform lengths (the paper's fixed shapes): cache_seqlens = NULL means L_K for all b
+        self.seqlens = None if uniform else base["seqlens"]
+        self.out = torch.empty((b, hq, HEAD_DIM), dtype=torch.bfloat16, device=device)
+        self.lse = torch.empty((b, hq), dtype=torch.float32, device=device)
+        self.bytes = alg_bytes(b, hq, hkv, lk)
+        self.kv_total = kv_bytes * self.nbuf
+
+    def l2_note(self, l2_bytes):
+        if self.nbuf > 1:
+            return (f"rotating {self.nbuf} KV buffers ({self.kv_total / 2**20:.0f} MiB > 2x L2 "
+                    f"{l2_bytes / 2**20:.0f} MiB) + 256 MiB L2 scrub before each timed replay")
+        return (f"KV {self.kv_total / 2**20:.0f} MiB per step > 2x L2 ({l2_bytes / 2**20:.0f} MiB)"
+                " + 256 MiB L2 scrub before each timed replay")
+
+
+def make_graph(dec, plan, w: Workload, steps: int, stream):
+    ws = dec.workspace_for(plan, w.q.device)
+
+    def one(i):
+        j = i % w.nbuf
+        dec.forward(plan, w.q, w.k[j], w.v[j], w.seqlens, out=w.out, lse=w.lse, workspace=ws)
+
+    with torch.cuda.stream(stream):
+        for i in range(3):
+            one(i)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=stream):
+        for i in range(steps):
+            one(i)
+    with torch.cuda.stream(stream):
+        g.replay()
+    torch.cuda.synchronize()
+    return g
+
+
+class Timer:
+    def __init__(self, device):
+        self.scrub = torch.empty(256 << 20, dtype=torch.uint8, device=device)
+
+    def time_replay(self, g, stream, scrub=True):
+        if scrub:
+            with torch.cuda.stream(stream):
+                self.scrub.fill_(1)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(stream):
+            e0.record(stream)
+            g.replay()
+            e1.record(stream)
+        e1.synchronize()
+        return e0.elapsed_time(e1)  # ms
+
+
+def ab_compare(dec, dev, stream, timer, cfg, steps, rounds, l2, seed, num_sms):
+    """Guarded vs seq-aware, interleaved replays (P:L119 A/B) -> medians in us/step."""
+    w = Workload(cfg, dev, seed, l2)
+    res = {}
+    graphs = {}
+    for pol in ("guarded", "seq_aware"):
+        plan = dec.make_plan(cfg["batch"], cfg["h_q"], cfg["h_kv"], cfg["l_k"], policy=pol)
+        graphs[pol] = (plan, make_graph(dec, plan, w, steps, stream))
+        res[pol] = []
+    for _ in range(rounds):
+        for pol in ("guarded", "seq_aware"):
+            res[pol].append(timer.time_replay(graphs[pol][1], stream) * 1e3 / steps)
+    out = {}
+    for pol in ("guarded", "seq_aware"):
+        plan = graphs[pol][0]
+        us = statistics.median(res[pol])
+        out[pol] = {"num_splits": plan.num_splits, "combine_mode": plan.combine_mode,
+                    "ctas": plan.grid_x * plan.grid_y * plan.grid_z,
+                    "occupancy_pct": round(100.0 * min(plan.grid_x * plan.grid_y * plan.grid_z, num_sms) / num_sms, 1),
+                    "us_per_step": round(us, 3), "p10_us": round(sorted(res[pol])[len(res[pol]) // 10], 3),
+                    "p90_us": round(sorted(res[pol])[(9 * len(res[pol])) // 10], 3),
+                    "gbs": round(w.bytes / (us * 1e-6) / 1e9, 1)}
+    out["speedup_seq_aware_vs_guarded"] = round(out["guarded"]["us_per_step"] / out["seq_aware"]["us_per_step"], 4)
+    out["config"] = dict(cfg, head_dim=HEAD_DIM)
+    out["l2"] = w.l2_note(l2)
+    del w, graphs
+    torch.cuda.empty_cache()
+    return out
+
+
+def streaming_roofline(dec, dev, stream, timer, cfg, steps, rounds, l2, seed, peak):
+    w = Workload(cfg, dev, seed, l2)
+    plan = dec.make_plan(cfg["batch"], cfg["h_q"], cfg["h_kv"], cfg["l_k"], policy="seq_aware")
+    g = make_graph(dec, plan, w, steps, stream)
+    ts = [timer.time_replay(g, stream) * 1e3 / steps for _ in range(rounds)]
+    us = statistics.median(ts)
+    gbs = w.bytes / (us * 1e-6) / 1e9
+    r = {"config": dict(cfg, head_dim=HEAD_DIM), "num_splits": plan.num_splits,
+         "combine_mode": plan.combine_mode, "us_per_step": round(us, 2), "achieved_gbs": round(gbs, 1),
+         "frac_of_measured_peak": round(gbs / peak, 4), "frac_of_8tbs_nominal": round(gbs / 8000.0, 4),
+         "bytes_per_step": w.bytes, "l2": w.l2_note(l2)}
+    del w, g
+    torch.cuda.empty_cache()
+    return r
+
+
+# ----------------------------------------------------------------------------------------------
+def cpu_baseline(cfg, budget_s=10.0):
+    """The fp64 oracle (as it stands) on this host's cores, on a bounded sample of the workload."""
+    import numpy as np
+    from oracle import attention as OA
+    try:
+        from threadpoolctl import threadpool_info
+        cores = max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
+    except Exception:
+        cores = 1
+    scfg = dict(cfg)
+    if cfg["batch"] * cfg["h_kv"] * cfg["l_k"] > 8 * 8192:   # bound the sample (fp64 copies of big caches)
+        scfg = dict(cfg, batch=1, l_k=min(cfg["l_k"], 8192))
+    inp = synth.make_inputs(scfg["batch"], scfg["h_q"], scfg["h_kv"], scfg["l_k"], seed=1000)
+    q, k, v, s = (synth.to_f64(inp[n]) for n in ("q", "k", "v", "seqlens"))
+    OA.decode_attention(q, k, v, s)     # warm
+    n, t0 = 0, time.perf_counter()
+    while True:
+        OA.decode_attention(q, k, v, s)
+        n += 1
+        dt = time.perf_counter() - t0
+        if dt >= budget_s or n >= 100000:
+            break
+    step_s = dt / n
+    b = alg_bytes(scfg["batch"], scfg["h_q"], scfg["h_kv"], scfg["l_k"])
+    what = "full steps of the workload" if scfg == cfg else f"sample steps (batch {scfg['batch']}, L_K {scfg['l_k']})"
+    return {"value": round(b / step_s / 1e9, 6), "unit": "GB/s", "cores": int(cores), "kind": "oracle",
+            "sample": f"{n} {what} in {dt:.1f} s (fp64 NumPy oracle.attention.decode_attention)",
+            "ms_per_step": round(step_s * 1e3, 4),
+            "host_cpus": len(os.sched_getaffinity(0))}
+
+
+def run_reference(args, rank, world):
+    """Reference arm of this tier: the CPU oracle on the same workload / metric."""
+    if rank != 0:
+        return 0
+    cfg = WORKLOADS[args.workload]
+    import numpy as np  # noqa: F401
+    from oracle import attention as OA
+    try:
+        from threadpoolctl import threadpool_info
+        cores = max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
+    except Exception:
+        cores = 1
+    sample_cfg = dict(cfg)
+    if cfg["batch"] * cfg["h_kv"] * cfg["l_k"] > 8 * 8192:   # bound a step to a sample (big configs)
+        sample_cfg = dict(cfg, batch=1, l_k=min(cfg["l_k"], 8192))
+    inp = synth.make_inputs(sample_cfg["batch"], sample_cfg["h_q"], sample_cfg["h_kv"], sample_cfg["l_k"], seed=1000)
+    q, k, v, s = (synth.to_f64(inp[n]) for n in ("q", "k", "v", "seqlens"))
+    for _ in range(args.warmup):
+        OA.decode_attention(q, k, v, s)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        OA.decode_attention(q, k, v, s)
+    dt = time.perf_counter() - t0
+    b = alg_bytes(sample_cfg["batch"], sample_cfg["h_q"], sample_cfg["h_kv"], sample_cfg["l_k"])
+    value = b * args.steps / dt / 1e9
+    sample = ("full workload per step" if sample_cfg == cfg else
+              f"per step: batch {sample_cfg['batch']} x L_K {sample_cfg['l_k']} of the workload")
+    line = {"impl": "reference", "metric": METRIC, "value": round(value, 6), "unit": "GB/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(dt / args.steps * 1e3, 4), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": args.workload, **cfg, "head_dim": HEAD_DIM},
+            "cpu_baseline": {"value": round(value, 6), "unit": "GB/s", "cores": int(cores), "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": round(value, 6), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ----------------------------------------------------------------------------------------------
+def e2e_measure(dec, L, cfg, dev, stream, steps, warmup):
+    """Same metric through the public API with HOST buffers: per step H2D of q/k/v from pinned
+    memory, da_plan_make, da_forward, D2H of out + lse - all inside the timed region."""
+    b, hq, hkv, lk = cfg["batch"], cfg["h_q"], cfg["h_kv"], cfg["l_k"]
+    inp = synth.make_inputs(b, hq, hkv, lk, seed=2000)
+    hq_, hk_, hv_ = (inp[n].pin_memory() for n in ("q", "k", "v"))
+    dq = torch.empty_like(hq_, device=dev)
+    dk = torch.empty_like(hk_, device=dev)
+    dv = torch.empty_like(hv_, device=dev)
+    out = torch.empty((b, hq, HEAD_DIM), dtype=torch.bfloat16, device=dev)
+    lse = torch.empty((b, hq), dtype=torch.float32, device=dev)
+    h_out = torch.empty(out.shape, dtype=out.dtype).pin_memory()
+    h_lse = torch.empty(lse.shape, dtype=lse.dtype).pin_memory()
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    ws_cache = {}
+
+    def step():
+        dq.copy_(hq_, non_blocking=True)
+        dk.copy_(hk_, non_blocking=True)
+        dv.copy_(hv_, non_blocking=True)
+        plan = L.da_plan_make(b, hq, hkv, lk, HEAD_DIM, 1, 0, sms, L.DA_POLICY_SEQ_AWARE, 0)
+        ws = ws_cache.get(plan.workspace_bytes)
+        if ws is None and plan.combine_mode == L.DA_COMBINE_KERNEL:
+            ws = ws_cache.setdefault(plan.workspace_bytes, dec.workspace_for(plan, dev))
+        dec.forward(plan, dq, dk, dv, None, out=out, lse=lse, workspace=ws)
+        h_out.copy_(out, non_blocking=True)
+        h_lse.copy_(lse, non_blocking=True)
+
+    with torch.cuda.stream(stream):
+        for _ in range(max(warmup, 1)):
+            step()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(stream):
+        e0.record(stream)
+        for _ in range(steps):
+            step()
+        e1.record(stream)
+    e1.synchronize()
+    ms = e0.elapsed_time(e1)
+    h2d = sum(t.numel() * t.element_size() for t in (hq_, hk_, hv_))
+    d2h = h_out.numel() * h_out.element_size() + h_lse.numel() * h_lse.element_size()
+    return ms, h2d, d2h
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="llama70b")
+    ap.add_argument("--no-extras", action="store_true", help="skip the A/B and streaming extras")
+    ap.add_argument("--ab-rounds", type=int, default=21)
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3          # contract: W >= 3 warm-up steps
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+
+    import torch.distributed as dist
+    if world > 1:
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    import paper_2604_00028_b200 as dec
+    from paper_2604_00028_b200 import _lib as L
+
+    props = torch.cuda.get_device_properties(dev)
+    l2, num_sms = props.L2_cache_size, props.multi_processor_count
+    stream = torch.cuda.Stream(device=dev)
+    timer = Timer(dev)
+    peak, peak_src = peaks()
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local_rank])
+
+    cfg = WORKLOADS[args.workload]
+    long_sharded = args.workload == "long_context" and world > 1
+    if long_sharded:
+        from paper_2604_00028_b200.dist import SeqShardedDecode
+        sd = SeqShardedDecode(cfg["batch"], cfg["h_q"], cfg["h_kv"], cfg["l_k"], HEAD_DIM, device=dev)
+        local_cfg = dict(cfg, l_k=sd.l_local)
+        inp = synth.make_inputs(cfg["batch"], cfg["h_q"], cfg["h_kv"], sd.l_local, device=dev, seed=1000 + rank)
+        out = torch.empty((cfg["batch"], cfg["h_q"], HEAD_DIM), dtype=torch.bfloat16, device=dev)
+        lse = torch.empty((cfg["batch"], cfg["h_q"]), dtype=torch.float32, device=dev)
+        plan = sd.plan
+        with torch.cuda.stream(stream):
+            for _ in range(args.warmup):
+                sd.step(inp["q"], inp["k"], inp["v"], None, out, lse)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=stream):
+            for _ in range(args.steps):
+                sd.step(inp["q"], inp["k"], inp["v"], None, out, lse)
+        step_bytes_total = alg_bytes(cfg["batch"], cfg["h_q"], cfg["h_kv"], cfg["l_k"])
+        kernels_per_step = (2 if plan.combine_mode == L.DA_COMBINE_KERNEL else 1) + 1
+        scaling = "strong"
+        l2_note = "sequence shard per rank > 2x L2 + 256 MiB L2 scrub before the timed replay"
+        parallelism = f"seq-sharded sp{world} + NCCL all-gather + LSE combine"
+    else:
+        local_cfg = cfg
+        w = Workload(cfg, dev, 1000 + rank, l2)
+        plan = dec.make_plan(cfg["batch"], cfg["h_q"], cfg["h_kv"], cfg["l_k"], policy="seq_aware")
+        with torch.cuda.stream(stream):
+            ws = dec.workspace_for(plan, dev)
+            for i in range(args.warmup):
+                j = i % w.nbuf
+                dec.forward(plan, w.q, w.k[j], w.v[j], w.seqlens, out=w.out, lse=w.lse, workspace=ws)
+        torch.cuda.synchronize()
+        g = make_graph(dec, plan, w, args.steps, stream)
+        step_bytes_total = w.bytes * world
+        kernels_per_step = 2 if plan.combine_mode == L.DA_COMBINE_KERNEL else 1
+        scaling = "weak"
+        l2_note = w.l2_note(l2)
+        parallelism = f"batch-sharded dp{world} (independent sequences, no collective)" if world > 1 else "single GPU"
+
+    # ---- the timed region: exactly K steps (one graph replay), barrier + sync both sides ----
+    with ClockSampler(dev.index) as clk:
+        t_end = time.time() + 0.6               # keep the GPU busy so clocks settle under load
+        while time.time() < t_end:
+            with torch.cuda.stream(stream):
+                g.replay()
+            torch.cuda.synchronize()
+        with torch.cuda.stream(stream):
+            timer.scrub.fill_(1)
+        torch.cuda.synchronize()
+        barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(stream):
+            e0.record(stream)
+            g.replay()
+            e1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        ms = e0.elapsed_time(e1)
+        # a few more untimed replays so the sampler sees the steady state around the timed region
+        t_end = time.time() + 0.3
+        while time.time() < t_end:
+            with torch.cuda.stream(stream):
+                g.replay()
+            torch.cuda.synchronize()
+    ms_t = torch.tensor([ms], device=dev)
+    if world > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms_max = float(ms_t.item())
+    us_per_step = ms_max * 1e3 / args.steps
+    value = step_bytes_total * args.steps / (ms_max * 1e-3) / 1e9
+
+    # ---- end to end through the public API with host buffers ----
+    e2e_ms, h2d, d2h = e2e_measure(dec, L, local_cfg, dev, stream, args.steps, args.warmup)
+    e2e_t = torch.tensor([e2e_ms], device=dev)
+    if world > 1:
+        dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
+    e2e_value = (alg_bytes(**local_cfg) * (world if not long_sharded else 1)) * args.steps / (float(e2e_t.item()) * 1e-3) / 1e9
+
+    extras = {}
+    if rank == 0 and world == 1 and not args.no_extras:
+        extras["policy_ab"] = {
+            "llama70b": ab_compare(dec, dev, stream, timer, WORKLOADS["llama70b"], args.steps, args.ab_rounds, l2, 1001, num_sms),
+            "llama70b_tp8_slice": ab_compare(dec, dev, stream, timer, WORKLOADS["llama70b_tp8"], args.steps, args.ab_rounds, l2, 1002, num_sms),
+        }
+        extras["roofline_streaming"] = {
+            "high_load": streaming_roofline(dec, dev, stream, timer, WORKLOADS["high_load"], 5, 5, l2, 1003, peak),
+            "long_context": streaming_roofline(dec, dev, stream, timer, WORKLOADS["long_context"], 20, 7, l2, 1004, peak),
+        }
+    if world > 1:
+        barrier()
+    if rank != 0:
+        dist.destroy_process_group()
+        return 0
+
+    # roofline of the dominant kernel of the headline step (the split-KV forward; with s = 1 it is
+    # the only kernel of the step, so its average launch duration is the step time)
+    kernel_us = us_per_step
+    achieved = alg_bytes(**local_cfg) / (kernel_us * 1e-6) / 1e9
+    trec = traffic_record().get(args.workload)
+    line = {
+        "metric": METRIC,
+        "value": round(value, 3),
+        "unit": "GB/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(ms_max / args.steps, 6),
+        "us_per_step": round(us_per_step, 3),
+        "higher_is_better": True,
+        "scaling": scaling,
+        "vs_baseline": None,
+        "dtype": "bf16",
+        "data": "synthetic (seeded N(0,1) bf16 q/K/V, uniform cache_seqlens = L_K)",
+        "config": {"workload": args.workload, **cfg, "head_dim": HEAD_DIM, "policy": "seq_aware",
+                   "num_splits": plan.num_splits, "combine_mode": plan.combine_mode,
+                   "global_batch": cfg["batch"] * (world if not long_sharded else 1),
+                   "parallelism": parallelism, "l2": l2_note, "graph": "K steps in one CUDA graph"},
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                     "frac": round(achieved / peak, 4), "traffic": trec.get("dram_bytes_per_launch") if trec else None,
+                     "kernel": "split_kv_fwd_kernel", "peak_source": peak_src,
+                     "note": "latency-bound config (2.1 MB per step); see roofline_streaming for the HBM-bound configs"},
+        "cpu_baseline": cpu_baseline(local_cfg, args.cpu_seconds) if world == 1 else None,
+        "e2e": {"value": round(e2e_value, 3), "unit": "GB/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h, "ms_per_step": round(float(e2e_t.item()) / args.steps, 6)},
+        "gpu_launches": args.steps * kernels_per_step,
+        "clocks": clk.summary(),
+        "device": {"name": props.name, "sms": num_sms, "l2_bytes": l2},
+    }
+    line.update(extras)
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,139 @@
+"""Multi-GPU layer: one process per GPU, torch.distributed (NCCL over NVLink 5 /
+NVSwitch) for the plumbing.  SURVEY §8(e).
+
+Two ways the decode-attention path shards across one 8xB200 box:
+
+* Throughput configs (batch x KV-head units are independent, "work
+  tiles = Batch x H_KV"): each rank owns a contiguous range of batches (or of
+  KV heads with their G query heads - the tensor-parallel mapping of P:L123)
+  and runs the single-GPU path on it.  No collective: every rank owns its
+  outputs (``shard_range``, ``BatchShard``).
+* Long-context configs: rank r holds tokens [r L/P, (r+1) L/P) of every
+  sequence (contiguous sequence shard).  Each rank runs the split-KV forward
+  with fp32 output to get its (o_r, lse_r) partial - the same partial the
+  in-GPU splits produce - then ONE exchange step: an all-gather of the packed
+  [o_r | lse_r] fp32 buffer, followed by the same LSE-combine kernel with
+  s = P (``SeqShardedDecode``).  Merging per-GPU partials is the identity
+  behind sequence splitting (C-comb), so the result equals single-GPU
+  attention over the whole sequence.
+
+Host-side only: the arithmetic runs in libdecattn.so's kernels.  The local
+attention and the combine are injectable so that the exchange logic can be
+tested with world_size 2 on CPU (gloo) against the oracle.
+"""
+
+from __future__ import annotations
+
+import torch
+import torch.distributed as dist
+
+
+def shard_range(n: int, rank: int, world: int):
+    """Contiguous, balanced [start, end) of n units for ``rank`` of ``world``."""
+    if world < 1 or not (0 <= rank < world) or n < 0:
+        raise ValueError("bad shard arguments")
+    return (n * rank) // world, (n * (rank + 1)) // world
+
+
+def head_shard(h_q: int, h_kv: int, rank: int, world: int):
+    """KV heads [k0, k1) and their query heads [k0 G, k1 G) owned by ``rank``
+    (tensor-parallel head mapping).  Requires world | h_kv."""
+    if h_kv % world:
+        raise ValueError("h_kv must be divisible by the world size for head sharding")
+    G = h_q // h_kv
+    k0, k1 = shard_range(h_kv, rank, world)
+    return (k0, k1), (k0 * G, k1 * G)
+
+
+def local_seqlens(seqlens_global: torch.Tensor, t0: int, l_local: int) -> torch.Tensor:
+    """Tokens of each sequence that fall in this rank's shard [t0, t0 + l_local)."""
+    return (seqlens_global.to(torch.int64) - t0).clamp_(0, l_local).to(torch.int32)
+
+
+def _all_gather_flat(recv: torch.Tensor, send: torch.Tensor, group=None):
+    backend = dist.get_backend(group)
+    if backend == "nccl":
+        dist.all_gather_into_tensor(recv, send, group=group)
+    else:  # gloo (CPU tests): list form
+        world = dist.get_world_size(group)
+        dist.all_gather(list(recv.view(world, -1).unbind(0)), send, group=group)
+
+
+class BatchShard:
+    """Throughput mode: rank r owns batches [b0, b1) of a global batch; no collective."""
+
+    def __init__(self, global_batch: int, rank: int, world: int):
+        self.b0, self.b1 = shard_range(global_batch, rank, world)
+        self.local_batch = self.b1 - self.b0
+
+
+class SeqShardedDecode:
+    """Long-context mode: sequence-sharded KV cache + all-gather + LSE combine.
+
+    ``local_attention(q, k, v, seqlens, o_out, lse_out)`` must write this rank's
+    fp32 partial into the given views; ``combine(o_parts, lse_parts, out, lse)``
+    merges P partials ([P, B, H_Q, d] / [P, B, H_Q] views of the gather
+    buffer).  Both default to the CUDA path.
+    """
+
+    def __init__(self, batch: int, h_q: int, h_kv: int, l_k_total: int, head_dim: int = 128, *,
+                 group=None, policy="seq_aware", device=None, local_attention=None, combine=None):
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        self.batch, self.h_q, self.h_kv, self.d = batch, h_q, h_kv, head_dim
+        self.t0, t1 = shard_range(l_k_total, self.rank, self.world)
+        self.l_local = t1 - self.t0
+        if self.l_local < 1:
+            raise ValueError("every rank needs at least one token of the sequence")
+        self.device = torch.device(device) if device is not None else (
+            torch.device("cuda", torch.cuda.current_device()) if torch.cuda.is_available() else torch.device("cpu"))
+        # floats per rank: [o | lse], padded to 16 bytes so every rank's o is 16-byte aligned
+        self.chunk = -(-(batch * h_q * (head_dim + 1)) // 4) * 4
+        self.send = torch.empty(self.chunk, dtype=torch.float32, device=self.device)
+        self.recv = torch.empty(self.world * self.chunk, dtype=torch.float32, device=self.device)
+        self.plan = None
+        if local_attention is None or combine is None:
+            from . import api
+            self.plan = api.make_plan(batch, h_q, h_kv, self.l_local, head_dim, True, 0, None, policy)
+            self._ws = api.workspace_for(self.plan, self.device)
+        self._local = local_attention or self._cuda_local
+        self._combine = combine or self._cuda_combine
+
+    # -- views of the packed buffers ---------------------------------------
+    def _o_view(self, flat):
+        return flat[: self.batch * self.h_q * self.d].view(self.batch, self.h_q, self.d)
+
+    def _lse_view(self, flat):
+        n_o = self.batch * self.h_q * self.d
+        return flat[n_o:n_o + self.batch * self.h_q].view(self.batch, self.h_q)
+
+    def gathered(self):
+        r = self.recv.view(self.world, self.chunk)
+        o = r[:, : self.batch * self.h_q * self.d].view(self.world, self.batch, self.h_q, self.d)
+        n_o = self.batch * self.h_q * self.d
+        lse = r[:, n_o:n_o + self.batch * self.h_q].view(self.world, self.batch, self.h_q)
+        return o, lse
+
+    # -- default CUDA implementations --------------------------------------
+    def _cuda_local(self, q, k, v, seqlens, o_out, lse_out):
+        from . import api
+        api.forward(self.plan, q, k, v, seqlens, out=o_out, lse=lse_out, workspace=self._ws,
+                    out_dtype=torch.float32)
+
+    def _cuda_combine(self, o_parts, lse_parts, out, lse):
+        from . import _lib as L
+        L.da_combine(self.world, self.batch, self.h_q, self.d, o_parts, self.chunk, lse_parts,
+                     self.chunk, L.DA_F32 if out.dtype == torch.float32 else L.DA_BF16, out, lse)
+
+    def step(self, q, k_local, v_local, seqlens_local=None, out=None, lse=None):
+        """One decode step: local partial -> all-gather -> combine.  Returns (out, lse)."""
+        self._local(q, k_local, v_local, seqlens_local, self._o_view(self.send), self._lse_view(self.send))
+        _all_gather_flat(self.recv, self.send, self.group)
+        if out is None:
+            out = torch.empty((self.batch, self.h_q, self.d), dtype=torch.bfloat16, device=self.device)
+        if lse is None:
+            lse = torch.empty((self.batch, self.h_q), dtype=torch.float32, device=self.device)
+        o_parts, lse_parts = self.gathered()
+        self._combine(o_parts, lse_parts, out, lse)
+        return out, lse
