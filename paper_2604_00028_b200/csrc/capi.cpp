@@ -35,21 +35,22 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
-// K or V cache [B, l_cap, H_KV, d] as a 4-D TMA tensor (d, H_KV, l_cap, B)
-// with 64 x 1 x 64 x 1 boxes (64 tokens x 64 dims = 128-byte rows) and the
-// 128-byte swizzle the consumers' ldmatrix addressing expects.  Tokens past
-// l_cap read as zero.
+// K or V cache [B, l_cap, H_KV, d] as a 5-D TMA tensor (d_lo = 64, t, d_hi = 2, H_KV, B):
+// the head dim is split into two 64-element halves (d_hi stride 128 B) so one box of
+// 64 x 64 x 2 x 1 x 1 brings a whole 64-token tile of K (or V) in a single TMA op, laid out
+// in shared memory as [half][token][64 dims] with 128-byte rows and the 128-byte swizzle
+// the consumers' ldmatrix addressing expects.  Tokens past l_cap read as zero.
 bool make_kv_tmap(CUtensorMap* map, const void* base, int32_t batch, int32_t l_cap, int32_t h_kv,
                   int64_t sb, int64_t st, int64_t sh) {
   auto fn = encode_fn();
   if (fn == nullptr) return false;
-  cuuint64_t dims[4] = {static_cast<cuuint64_t>(kHeadDim), static_cast<cuuint64_t>(h_kv),
-                        static_cast<cuuint64_t>(l_cap), static_cast<cuuint64_t>(batch)};
-  cuuint64_t strides[3] = {static_cast<cuuint64_t>(sh) * 2, static_cast<cuuint64_t>(st) * 2,
+  cuuint64_t dims[5] = {64, static_cast<cuuint64_t>(l_cap), 2, static_cast<cuuint64_t>(h_kv),
+                        static_cast<cuuint64_t>(batch)};
+  cuuint64_t strides[4] = {static_cast<cuuint64_t>(st) * 2, 128, static_cast<cuuint64_t>(sh) * 2,
                            static_cast<cuuint64_t>(sb) * 2};
-  cuuint32_t box[4] = {64, 1, static_cast<cuuint32_t>(kTileN), 1};
-  cuuint32_t estr[4] = {1, 1, 1, 1};
-  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides,
+  cuuint32_t box[5] = {64, static_cast<cuuint32_t>(kTileN), 2, 1, 1};
+  cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<void*>(base), dims, strides,
                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;

@@ -3,6 +3,12 @@
 // every number.
 #pragma once
 
+#ifdef __CUDACC__
+#define DA_HD __host__ __device__
+#else
+#define DA_HD
+#endif
+
 namespace decattn {
 
 // ---- policy accounting (paper side) -------------------------
@@ -19,19 +25,17 @@ constexpr int kSplitUnit = kTileN;     // partition unit (C-pol item 6)
 constexpr int kStageBytes = 4 * kTileN * 128;   // K|V x two 64-dim halves, 128 B rows = 32 KB
 // Each consumer warp owns exactly one ring stage (stages == consumer warps), so
 // a warp never waits on a stage another warp consumes: no mbarrier phase aliasing.
-constexpr int kStagesDefault = 6;      // s == 1 and workspace-combine kernels: 192 KB ring
-constexpr int kStagesCluster = 5;      // cluster-combine kernels: 160 KB ring + DSMEM slots
+constexpr int kStagesDefault = 7;      // s == 1 and workspace-combine kernels: 224 KB ring, 8 warps
+constexpr int kStagesCluster = 6;      // cluster-combine kernels: 192 KB ring + DSMEM push slots
 constexpr int kMaxClusterSplits = 8;   // portable cluster size
-constexpr int kSlotFloats = 16 * kHeadDim + 32;           // one pushed CTA partial: O[16][128], m[16], l[16]
-constexpr int kSlotBytes = kSlotFloats * 4;
-constexpr int threads_for(int stages) { return (stages + 1) * 32; }   // + 1 TMA producer warp
-constexpr int smem_for(int stages, bool cluster) {
-  return stages * kStageBytes + (cluster ? (kMaxClusterSplits - 1) * kSlotBytes : 0) + 1024;
+// One pushed row: O[128] fp32, (m, l), padding to 16 bytes.  A rank owns ceil(R/s) rows and
+// receives them from all s ranks (itself included): at most max_s s ceil(16/s) = 21 rows (s = 7).
+constexpr int kSlotRowFloats = kHeadDim + 4;
+constexpr int kMaxSlotRows = 21;
+DA_HD constexpr int threads_for(int stages) { return (stages + 1) * 32; }   // + 1 TMA producer warp
+DA_HD constexpr int smem_for(int stages, bool cluster) {
+  return stages * kStageBytes + (cluster ? kMaxSlotRows * kSlotRowFloats * 4 : 0) + 1024;
 }
-#ifndef DECATTN_PREFETCH_TILES
-#define DECATTN_PREFETCH_TILES 0
-#endif
-constexpr int kPrefetchTiles = DECATTN_PREFETCH_TILES;  // speculative L2 prefetch before griddepcontrol.wait
 constexpr int kCombineRowsPerCta = 4;  // combine kernel: one warp per (b, h) row
 
 }  // namespace decattn

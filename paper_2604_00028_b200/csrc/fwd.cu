@@ -53,6 +53,21 @@ namespace {
 
 constexpr float kNegInf = -__builtin_huge_valf();
 constexpr float kLn2 = 0.6931471805599453f;
+
+// ---- development timeline tracing (only in -DDECATTN_TRACE builds; no-op otherwise) ----
+#ifdef DECATTN_TRACE
+__device__ unsigned long long g_trace[64 * 64];
+__device__ unsigned long long g_prev_end;
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ int trace_cta() { return (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x; }
+#define TRACE(slot) do { const int c_ = trace_cta(); if (c_ < 64) g_trace[c_ * 64 + (slot)] = gtime(); } while (0)
+#else
+#define TRACE(slot) do { } while (0)
+#endif
 constexpr int kHalfBytes = kTileN * 128;     // one 64-token x 64-dim box: 8 KB
 constexpr int kEpiStride = kHeadDim + 4;     // fp32 row stride of epilogue buffers (bank spread)
 
@@ -236,6 +251,24 @@ __device__ __forceinline__ void store_out(const FwdParams& p, size_t row, int d4
   }
 }
 
+// Tokens [t0, t_end) of split `split` of s for a sequence of n tokens: units of kTileN
+// tokens, split i covering units [floor(i n_u / s), floor((i+1) n_u / s)) (C-pol item 6).
+__device__ __forceinline__ void split_range(int n, int split, int s, int& t0, int& t_end, int& n_tiles) {
+  const uint32_t nu = static_cast<uint32_t>((n + kTileN - 1) / kTileN);
+  const uint32_t us = static_cast<uint32_t>(s);
+  uint32_t u0, u1;
+  if (nu <= 0xffffffffu / us) {              // (split + 1) * nu fits in 32 bits
+    u0 = static_cast<uint32_t>(split) * nu / us;
+    u1 = static_cast<uint32_t>(split + 1) * nu / us;
+  } else {
+    u0 = static_cast<uint32_t>(static_cast<uint64_t>(split) * nu / us);
+    u1 = static_cast<uint32_t>(static_cast<uint64_t>(split + 1) * nu / us);
+  }
+  t0 = static_cast<int>(u0) * kTileN;
+  t_end = min(static_cast<int>(u1) * kTileN, n);
+  n_tiles = static_cast<int>(u1 - u0);
+}
+
 // ---------------------------------------------------------------------------
 // The kernel.  kPath: DA_PATH_SCALAR / DA_PATH_MMA; kNB: g-blocks of 8 query
 // rows (MMA path); kCombine: da_combine_mode; NS: ring stages = consumer warps.
@@ -245,23 +278,24 @@ __global__ void __launch_bounds__(threads_for(NS), 1)
     split_kv_fwd_kernel(const __grid_constant__ CUtensorMap tmap_k,
                         const __grid_constant__ CUtensorMap tmap_v, const FwdParams p) {
   constexpr int NW = NS;                                   // consumer warps; warp w owns stage w
+  constexpr int kT = threads_for(NS);                      // all threads (consumers + producer)
   constexpr int R = kPath == DA_PATH_MMA ? 8 * kNB : 1;    // query rows of this CTA
-  constexpr int kIters = (R * 32 + NW * 32 - 1) / (NW * 32);
+  constexpr int kIters = (R * 32 + kT - 1) / kT;           // merge passes: element = (row, float4)
   constexpr bool kCluster = kCombine == DA_COMBINE_CLUSTER;
   extern __shared__ uint8_t smem_raw[];
   __shared__ __align__(8) uint64_t full_bar[NS];
   __shared__ __align__(8) uint64_t empty_bar[NS];
-  __shared__ __align__(8) uint64_t push_bar;              // CLUSTER: rank 0 collects s - 1 pushes
+  __shared__ __align__(8) uint64_t push_bar;              // CLUSTER: pushes of the rows this CTA owns
 
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t sbase = (raw + 1023u) & ~1023u;
   float* const epi = reinterpret_cast<float*>(smem_raw + (sbase - raw));
   // epilogue carve-up (aliases the ring once every tile is consumed)
-  float* const epi_o = epi;                                // [NW][16][kEpiStride]
-  float* const epi_m = epi_o + NW * 16 * kEpiStride;       // [NW][16]
-  float* const epi_l = epi_m + NW * 16;                    // [NW][16]
-  // CLUSTER push slots (past the ring: written by peers while this CTA still streams)
-  float* const slots = epi + NS * kStageBytes / 4;         // [s-1][kSlotFloats]
+  float* const epi_o = epi;                                          // [NW][16][kEpiStride]
+  float2* const epi_ml = reinterpret_cast<float2*>(epi_o + NW * 16 * kEpiStride);  // [NW][16] (m, l)
+  // CLUSTER push slots, past the ring (peers write them while this CTA may still stream):
+  // [source slot 0..s-2][owned row 0..ceil(R/s)-1][kSlotRowFloats]
+  float* const slots = epi + NS * kStageBytes / 4;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int split = blockIdx.x, b = blockIdx.z;
@@ -276,8 +310,15 @@ __global__ void __launch_bounds__(threads_for(NS), 1)
     kvh = hq0 / p.G;
     rows_valid = 1;
   }
-
+  // CLUSTER: rank r owns rows g = r, r + s, r + 2s, ... and emits them
+  const int s_cl = kCluster ? p.num_splits : 1;
   const uint32_t rank = kCluster ? cluster_ctarank() : 0u;
+  const int rows_per_owner = (R + s_cl - 1) / s_cl;
+
+  if (threadIdx.x == 0) TRACE(0);
+#ifdef DECATTN_TRACE
+  if (threadIdx.x == 0 && trace_cta() < 64) g_trace[trace_cta() * 64 + 60] = clock64();
+#endif
   if (threadIdx.x == 0) {
 #pragma unroll
     for (int i = 0; i < NS; ++i) {
@@ -285,33 +326,23 @@ __global__ void __launch_bounds__(threads_for(NS), 1)
       mbar_init(smem_u32(&empty_bar[i]), 1);
     }
     if constexpr (kCluster) {
-      // rank 0 expects (s - 1) pushes of rows_valid x (O row + m, l) bytes via st.async
+      // expect s pushes (every rank, this one included) of (O row, m, l) for every valid row
+      // this rank owns, counted in st.async bytes
+      const int owned = rows_valid > static_cast<int>(rank) ? (rows_valid - 1 - static_cast<int>(rank)) / s_cl + 1 : 0;
       mbar_init(smem_u32(&push_bar), 1);
-      if (rank == 0)
-        mbar_arrive_expect_tx(smem_u32(&push_bar),
-                              static_cast<uint32_t>((p.num_splits - 1) * rows_valid * (kHeadDim * 4 + 8)));
+      mbar_arrive_expect_tx(smem_u32(&push_bar), static_cast<uint32_t>(s_cl * owned * (kHeadDim * 4 + 8)));
     }
     fence_mbarrier_init();
   }
   if (warp == NW && lane == 0) {
     prefetch_tmap(&tmap_k);
     prefetch_tmap(&tmap_v);
-    // Speculative L2 prefetch of this split's first tiles, assuming the full length
-    // (plan l_k): issued before griddepcontrol.wait, so it overlaps the tail of the
-    // previous kernel.  Always safe: L2 is the point of coherence, a prefetch never
-    // returns data to the SM.
-    const int n_spec = min(p.l_default, p.l_cap);
-    const int64_t nu_spec = (n_spec + kTileN - 1) / kTileN;
-    const int v0 = static_cast<int>(static_cast<int64_t>(split) * nu_spec / p.num_splits);
-    const int v1 = static_cast<int>(static_cast<int64_t>(split + 1) * nu_spec / p.num_splits);
-    for (int i = 0; i < min(v1 - v0, kPrefetchTiles); ++i) {
-      const int t = (v0 + i) * kTileN;
-      tma_prefetch_4d(&tmap_k, 0, kvh, t, b);
-      tma_prefetch_4d(&tmap_k, 64, kvh, t, b);
-      tma_prefetch_4d(&tmap_v, 0, kvh, t, b);
-      tma_prefetch_4d(&tmap_v, 64, kvh, t, b);
-    }
   }
+  // ---- this split's token range (C-pol item 6), in units of kTileN tokens.  With uniform
+  // lengths (cache_seqlens == NULL) it is known before griddepcontrol.wait, so the producer
+  // can issue the first TMA the moment the wait returns.
+  int t0, t_end, n_tiles;
+  split_range(min(max(p.l_default, 0), p.l_cap), split, p.num_splits, t0, t_end, n_tiles);
   __syncthreads();
   if constexpr (kCluster) cluster_arrive_relaxed();   // "my push barrier is initialised"
 
@@ -320,17 +351,15 @@ __global__ void __launch_bounds__(threads_for(NS), 1)
   // the preceding kernel may still be writing.
   pdl_launch_dependents();
   pdl_wait();
-
-  // ---- this split's token range (C-pol item 6): units of kTileN tokens
-  int n = p.seqlens != nullptr ? __ldg(p.seqlens + b) : p.l_default;
-  n = min(max(n, 0), p.l_cap);
-  const int64_t n_units = (n + kTileN - 1) / kTileN;
-  const int u0 = static_cast<int>(static_cast<int64_t>(split) * n_units / p.num_splits);
-  const int u1 = static_cast<int>(static_cast<int64_t>(split + 1) * n_units / p.num_splits);
-  const int t0 = u0 * kTileN;
-  const int t_end = min(u1 * kTileN, n);
-  const int n_tiles = u1 - u0;
-  const int n_active = min(NW, n_tiles);   // consumer warps that received at least one tile
+#ifdef DECATTN_TRACE
+  if (threadIdx.x == 0) {
+    TRACE(1);
+    const int c_ = trace_cta();
+    if (c_ < 64) g_trace[c_ * 64 + 63] = *(volatile unsigned long long*)&g_prev_end;
+  }
+#endif
+  if (p.seqlens != nullptr)
+    split_range(min(max(__ldg(p.seqlens + b), 0), p.l_cap), split, p.num_splits, t0, t_end, n_tiles);
 
   if (warp == NW) {
     // ================= TMA producer =================
@@ -342,12 +371,13 @@ __global__ void __launch_bounds__(threads_for(NS), 1)
         mbar_arrive_expect_tx(fb, kStageBytes);
         const uint32_t dst = sbase + st * kStageBytes;
         const int t = t0 + i * kTileN;
-        tma_load_4d(dst, &tmap_k, fb, 0, kvh, t, b);
-        tma_load_4d(dst + kHalfBytes, &tmap_k, fb, 64, kvh, t, b);
-        tma_load_4d(dst + 2 * kHalfBytes, &tmap_v, fb, 0, kvh, t, b);
-        tma_load_4d(dst + 3 * kHalfBytes, &tmap_v, fb, 64, kvh, t, b);
+        tma_load_5d(dst, &tmap_k, fb, 0, t, 0, kvh, b);                  // K: both 64-dim halves
+        tma_load_5d(dst + 2 * kHalfBytes, &tmap_v, fb, 0, t, 0, kvh, b);  // V
+        if (i < 8) TRACE(2 + i);
       }
     }
+    __syncwarp();
+    asm volatile("bar.sync 0;" ::: "memory");   // (A) pairs with the consumers' barrier
   } else {
     // ================= consumers: warp w handles tiles w, w + NW, ... (all in stage w) =======
     const uint16_t* qrow = p.q + static_cast<int64_t>(b) * p.q_sb;
@@ -381,6 +411,7 @@ __global__ void __launch_bounds__(threads_for(NS), 1)
 
       for (int i = warp, round = 0; i < n_tiles; i += NW, ++round) {
         mbar_wait(fb, round & 1);
+        if (lane == 0 && i < 8) TRACE(10 + i);
         const int valid = min(kTileN, t_end - (t0 + i * kTileN));
         if (valid < kTileN) {
           // rows past the range may hold anything (even NaN): zero them so P = 0 rows stay 0
@@ -394,6 +425,7 @@ __global__ void __launch_bounds__(threads_for(NS), 1)
         mma_tile<kNB>(sK, sV, valid, qf, o, m, l, p.scale_log2, lane);
         __syncwarp();
         if (lane == 0) mbar_arrive(eb);
+        if (lane == 0 && i < 8) TRACE(18 + i);
       }
       // finish l: sum the partial sums of the 8 lanes that share a g column
 #pragma unroll
@@ -406,27 +438,25 @@ __global__ void __launch_bounds__(threads_for(NS), 1)
           v += __shfl_xor_sync(0xffffffffu, v, 16);
           l[nb][c] = v;
         }
-      asm volatile("bar.sync 1, %0;" ::"n"(NW * 32) : "memory");  // ring no longer read
-      if (lane < 4) {
+      asm volatile("bar.sync 0;" ::: "memory");   // (A) every tile consumed: the ring is free
+      if (warp < n_tiles && lane < 4) {
 #pragma unroll
         for (int nb = 0; nb < kNB; ++nb)
 #pragma unroll
-          for (int c = 0; c < 2; ++c) {
-            const int g = nb * 8 + 2 * lane + c;
-            epi_m[warp * 16 + g] = m[nb][c];
-            epi_l[warp * 16 + g] = l[nb][c];
-          }
+          for (int c = 0; c < 2; ++c) epi_ml[warp * 16 + nb * 8 + 2 * lane + c] = make_float2(m[nb][c], l[nb][c]);
       }
+      if (warp < n_tiles) {
 #pragma unroll
-      for (int i = 0; i < 8; ++i)
+        for (int i = 0; i < 8; ++i)
 #pragma unroll
-        for (int nb = 0; nb < kNB; ++nb)
+          for (int nb = 0; nb < kNB; ++nb)
 #pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            const int g = nb * 8 + 2 * (lane & 3) + (c & 1);
-            const int d = 16 * i + (lane >> 2) + 8 * (c >> 1);
-            epi_o[(warp * 16 + g) * kEpiStride + d] = o[i][nb][c];
-          }
+            for (int c = 0; c < 4; ++c) {
+              const int g = nb * 8 + 2 * (lane & 3) + (c & 1);
+              const int d = 16 * i + (lane >> 2) + 8 * (c >> 1);
+              epi_o[(warp * 16 + g) * kEpiStride + d] = o[i][nb][c];
+            }
+      }
     } else {
       uint4 qv[16];
       const uint4* q4 = reinterpret_cast<const uint4*>(qrow + static_cast<int64_t>(hq0) * p.q_sh);
@@ -443,119 +473,148 @@ __global__ void __launch_bounds__(threads_for(NS), 1)
       }
 #pragma unroll
       for (int off = 16; off > 0; off >>= 1) l += __shfl_xor_sync(0xffffffffu, l, off);
-      asm volatile("bar.sync 1, %0;" ::"n"(NW * 32) : "memory");
-      if (lane == 0) {
-        epi_m[warp * 16] = m;
-        epi_l[warp * 16] = l;
+      asm volatile("bar.sync 0;" ::: "memory");   // (A)
+      if (warp < n_tiles) {
+        if (lane == 0) epi_ml[warp * 16] = make_float2(m, l);
+        *reinterpret_cast<float4*>(&epi_o[(warp * 16) * kEpiStride + 4 * lane]) =
+            make_float4(o[0], o[1], o[2], o[3]);
       }
-      *reinterpret_cast<float4*>(&epi_o[(warp * 16) * kEpiStride + 4 * lane]) =
-          make_float4(o[0], o[1], o[2], o[3]);
     }
   }
+  __syncthreads();                                // (B) every warp's (m, l, O) is in shared memory
+  if (threadIdx.x == 0) TRACE(26);
 
-  // ================= merge the consumer warps; emit / push (a7, a8) =================
-  // Element e = (row g, float4 column d4) of this CTA's [R x 128] result is handled by
-  // consumer thread e mod (NW*32); kIters passes cover all R*32 elements.
-  float own_m[kIters], own_l[kIters];
-  float4 own_o[kIters];
-  if (warp < NW) {
-    asm volatile("bar.sync 1, %0;" ::"n"(NW * 32) : "memory");
-    if constexpr (kCluster) cluster_wait();     // every peer's push barrier is initialised
+  // ================= merge the consumer warps (every thread of the CTA) =================
+  // Element e = (row g = e / 32, float4 column d4 = e % 32) of the CTA's [R x 128] result.
+  // Only the n_active = min(NW, n_tiles) warps that received tiles wrote a partial; the
+  // passes are branch-free (predicated loads), so the loads of all passes issue back to back.
+  const int n_active = min(NW, n_tiles);
+  float eM[kIters], eL[kIters];
+  float4 eO[kIters];
+#pragma unroll
+  for (int it = 0; it < kIters; ++it) {
+    const int e = threadIdx.x + it * kT;
+    const int g = (e >> 5) & 15, d4 = e & 31;
+    float2 ml[NW];
+    float4 ow[NW];
+#pragma unroll
+    for (int w = 0; w < NW; ++w) {
+      ml[w] = make_float2(kNegInf, 0.f);
+      ow[w] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (w < n_active) {
+        ml[w] = epi_ml[w * 16 + g];
+        ow[w] = *reinterpret_cast<const float4*>(&epi_o[(w * 16 + g) * kEpiStride + 4 * d4]);
+      }
+    }
+    float M = kNegInf;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) M = fmaxf(M, ml[w].x);
+    float Lsum = 0.f;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int w = 0; w < NW; ++w) {
+      const float f = ml[w].x == kNegInf ? 0.f : ex2(ml[w].x - M);
+      Lsum = fmaf(f, ml[w].y, Lsum);
+      acc.x = fmaf(f, ow[w].x, acc.x);
+      acc.y = fmaf(f, ow[w].y, acc.y);
+      acc.z = fmaf(f, ow[w].z, acc.z);
+      acc.w = fmaf(f, ow[w].w, acc.w);
+    }
+    eM[it] = M;
+    eL[it] = Lsum;
+    eO[it] = acc;
+  }
+  if (threadIdx.x == 0) TRACE(27);
+
+  if constexpr (!kCluster) {
 #pragma unroll
     for (int it = 0; it < kIters; ++it) {
-      const int e = threadIdx.x + it * NW * 32;
+      const int e = threadIdx.x + it * kT;
       const int g = e >> 5, d4 = e & 31;
-      own_m[it] = kNegInf;
-      own_l[it] = 0.f;
-      own_o[it] = make_float4(0.f, 0.f, 0.f, 0.f);
       if (e >= R * 32 || g >= rows_valid) continue;
+      const float inv = eL[it] > 0.f ? __frcp_rn(eL[it]) : 0.f;
+      const float4 v = make_float4(eO[it].x * inv, eO[it].y * inv, eO[it].z * inv, eO[it].w * inv);
+      const float lse_v = eL[it] > 0.f ? (eM[it] + lg2(eL[it])) * kLn2 : kNegInf;
+      const size_t row = static_cast<size_t>(b) * p.h_q + hq0 + g;
+      if constexpr (kCombine == DA_COMBINE_NONE) {
+        store_out(p, row, d4, v);
+        if (d4 == 0 && p.lse != nullptr) p.lse[row] = lse_v;
+      } else {  // DA_COMBINE_KERNEL: normalised partial o_i, lse_i (C-part)
+        const size_t prow = static_cast<size_t>(split) * p.batch * p.h_q + row;
+        reinterpret_cast<float4*>(p.ws_o)[prow * (kHeadDim / 4) + d4] = v;
+        if (d4 == 0) p.ws_lse[prow] = lse_v;
+      }
+    }
+  } else {
+    // ================= LSE combine across the s CTAs of the cluster (a8) =================
+    // Row g belongs to rank g mod s.  Non-owned rows are pushed into the owner's slot with
+    // st.async (bytes counted on the owner's push barrier; no fence, no cluster barrier on the
+    // exit path); owned rows wait for the s - 1 pushes, merge, and are written out.
+    cluster_wait();                                 // every peer's push barrier is initialised
+    const int s = s_cl;
+#pragma unroll
+    for (int it = 0; it < kIters; ++it) {
+      const int e = threadIdx.x + it * kT;
+      const int g = e >> 5, d4 = e & 31;
+      if (e >= R * 32 || g >= rows_valid) continue;
+      const int owner = g % s;
+      // slot [source rank][row g / s of the owner]
+      float* const dst = slots + (static_cast<int>(rank) * rows_per_owner + g / s) * kSlotRowFloats;
+      const uint32_t rbar = mapa(smem_u32(&push_bar), owner);
+      st_async_v4(mapa(smem_u32(dst + 4 * d4), owner), eO[it], rbar);
+      if (d4 == 0) st_async_v2(mapa(smem_u32(dst + kHeadDim), owner), eM[it], eL[it], rbar);
+    }
+    {
+      const uint32_t pb = smem_u32(&push_bar);
+      while (!mbar_try_wait_cluster(pb, 0)) {
+      }
+    }
+    if (threadIdx.x == 0) TRACE(29);
+    // this rank's rows: element t = (owned row t / 32, float4 column t % 32)
+    for (int t = threadIdx.x; t < rows_per_owner * 32; t += kT) {
+      const int rl = t >> 5, d4 = t & 31;
+      const int g = static_cast<int>(rank) + rl * s;
+      if (g >= rows_valid) break;   // rows of a rank ascend with t: the rest are invalid too
+      float2 mlr[kMaxClusterSplits];
+      float4 orr[kMaxClusterSplits];
+#pragma unroll
+      for (int r = 0; r < kMaxClusterSplits; ++r) {
+        mlr[r] = make_float2(kNegInf, 0.f);
+        orr[r] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (r < s) {
+          const float* sl = slots + (r * rows_per_owner + rl) * kSlotRowFloats;
+          mlr[r] = *reinterpret_cast<const float2*>(sl + kHeadDim);
+          orr[r] = *reinterpret_cast<const float4*>(sl + 4 * d4);
+        }
+      }
       float M = kNegInf;
 #pragma unroll
-      for (int w = 0; w < NW; ++w)
-        if (w < n_active) M = fmaxf(M, epi_m[w * 16 + g]);
+      for (int r = 0; r < kMaxClusterSplits; ++r) M = fmaxf(M, mlr[r].x);
       float Lsum = 0.f;
       float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-      for (int w = 0; w < NW; ++w) {
-        if (w >= n_active) break;
-        const float mw = epi_m[w * 16 + g];
-        const float f = mw == kNegInf ? 0.f : ex2(mw - M);
-        Lsum = fmaf(f, epi_l[w * 16 + g], Lsum);
-        const float4 ow = *reinterpret_cast<const float4*>(&epi_o[(w * 16 + g) * kEpiStride + 4 * d4]);
-        acc.x = fmaf(f, ow.x, acc.x);
-        acc.y = fmaf(f, ow.y, acc.y);
-        acc.z = fmaf(f, ow.z, acc.z);
-        acc.w = fmaf(f, ow.w, acc.w);
+      for (int r = 0; r < kMaxClusterSplits; ++r) {
+        const float f = mlr[r].x == kNegInf ? 0.f : ex2(mlr[r].x - M);
+        Lsum = fmaf(f, mlr[r].y, Lsum);
+        acc.x = fmaf(f, orr[r].x, acc.x);
+        acc.y = fmaf(f, orr[r].y, acc.y);
+        acc.z = fmaf(f, orr[r].z, acc.z);
+        acc.w = fmaf(f, orr[r].w, acc.w);
       }
-      if constexpr (kCluster) {
-        if (rank == 0) {
-          own_m[it] = M;
-          own_l[it] = Lsum;
-          own_o[it] = acc;
-        } else {
-          // push (M, L, unnormalised O) into rank 0's slot rank-1 through DSMEM; each
-          // st.async counts its bytes on rank 0's push barrier (no fence, no arrive)
-          const uint32_t slot = smem_u32(slots + (rank - 1) * kSlotFloats);
-          const uint32_t rbar = mapa(smem_u32(&push_bar), 0);
-          st_async_v4(mapa(slot + (g * kHeadDim + 4 * d4) * 4, 0), acc, rbar);
-          if (d4 == 0) st_async_v2(mapa(slot + (16 * kHeadDim + 2 * g) * 4, 0), M, Lsum, rbar);
-        }
-      } else {
-        const float inv = Lsum > 0.f ? 1.f / Lsum : 0.f;
-        const float4 v = make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
-        const float lse_v = Lsum > 0.f ? (M + lg2(Lsum)) * kLn2 : kNegInf;
-        const size_t row = static_cast<size_t>(b) * p.h_q + hq0 + g;
-        if constexpr (kCombine == DA_COMBINE_NONE) {
-          store_out(p, row, d4, v);
-          if (d4 == 0 && p.lse != nullptr) p.lse[row] = lse_v;
-        } else {  // DA_COMBINE_KERNEL: normalised partial o_i, lse_i (C-part)
-          const size_t prow = static_cast<size_t>(split) * p.batch * p.h_q + row;
-          reinterpret_cast<float4*>(p.ws_o)[prow * (kHeadDim / 4) + d4] = v;
-          if (d4 == 0) p.ws_lse[prow] = lse_v;
-        }
-      }
-    }
-  } else if constexpr (kCluster) {
-    cluster_wait();                               // producer warp: pair its early arrive
-  }
-
-  if constexpr (kCluster) {
-    if (warp < NW && rank == 0) {
-      {
-        // rank 0: wait for the s - 1 pushes, then merge (LSE combine, a8) and emit
-        const uint32_t pb = smem_u32(&push_bar);
-        while (!mbar_try_wait_cluster(pb, 0)) {
-        }
-        const int s = p.num_splits;
-#pragma unroll
-        for (int it = 0; it < kIters; ++it) {
-          const int e = threadIdx.x + it * NW * 32;
-          const int g = e >> 5, d4 = e & 31;
-          if (e >= R * 32 || g >= rows_valid) continue;
-          float M = own_m[it];
-          for (int r = 1; r < s; ++r) M = fmaxf(M, slots[(r - 1) * kSlotFloats + 16 * kHeadDim + 2 * g]);
-          const float f0 = own_m[it] == kNegInf ? 0.f : ex2(own_m[it] - M);
-          float Lsum = f0 * own_l[it];
-          float4 acc = make_float4(f0 * own_o[it].x, f0 * own_o[it].y, f0 * own_o[it].z, f0 * own_o[it].w);
-          for (int r = 1; r < s; ++r) {
-            const float* sl = slots + (r - 1) * kSlotFloats;
-            const float mr = sl[16 * kHeadDim + 2 * g];
-            const float f = mr == kNegInf ? 0.f : ex2(mr - M);
-            Lsum = fmaf(f, sl[16 * kHeadDim + 2 * g + 1], Lsum);
-            const float4 orr = *reinterpret_cast<const float4*>(sl + g * kHeadDim + 4 * d4);
-            acc.x = fmaf(f, orr.x, acc.x);
-            acc.y = fmaf(f, orr.y, acc.y);
-            acc.z = fmaf(f, orr.z, acc.z);
-            acc.w = fmaf(f, orr.w, acc.w);
-          }
-          const float inv = Lsum > 0.f ? 1.f / Lsum : 0.f;
-          const size_t row = static_cast<size_t>(b) * p.h_q + hq0 + g;
-          store_out(p, row, d4, make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv));
-          if (d4 == 0 && p.lse != nullptr) p.lse[row] = Lsum > 0.f ? (M + lg2(Lsum)) * kLn2 : kNegInf;
-        }
-      }
+      const float inv = Lsum > 0.f ? __frcp_rn(Lsum) : 0.f;
+      const size_t row = static_cast<size_t>(b) * p.h_q + hq0 + g;
+      store_out(p, row, d4, make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv));
+      if (d4 == 0 && p.lse != nullptr) p.lse[row] = Lsum > 0.f ? (M + lg2(Lsum)) * kLn2 : kNegInf;
     }
   }
+#ifdef DECATTN_TRACE
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    TRACE(30);
+    if (trace_cta() < 64) g_trace[trace_cta() * 64 + 61] = clock64();
+    if (rank == 0 && blockIdx.x == 0) g_prev_end = gtime();
+  }
+#endif
 }
 
 template <int kPath, int kNB, int kCombine>
@@ -618,4 +677,10 @@ cudaError_t launch_split_kv_fwd(const da_plan& plan, const CUtensorMap& tmap_k,
   return dispatch_combine<DA_PATH_MMA, 2>(plan, tmap_k, tmap_v, p, stream);
 }
 
+#ifdef DECATTN_TRACE
+extern "C" __attribute__((visibility("default"))) int da_trace_fetch(unsigned long long* host, int n) {
+  if (n > 64 * 64) n = 64 * 64;
+  return cudaMemcpyFromSymbol(host, g_trace, sizeof(unsigned long long) * n) == cudaSuccess ? 0 : 1;
+}
+#endif
 }  // namespace decattn
