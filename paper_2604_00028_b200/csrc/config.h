@@ -23,16 +23,48 @@ constexpr int kHeadDim = 128;          // v1 supports d = 128 only
 constexpr int kTileN = 64;             // tokens per pipeline stage (= split unit)
 constexpr int kSplitUnit = kTileN;     // partition unit (C-pol item 6)
 constexpr int kStageBytes = 4 * kTileN * 128;   // K|V x two 64-dim halves, 128 B rows = 32 KB
-// Each consumer warp owns exactly one ring stage (stages == consumer warps), so
-// a warp never waits on a stage another warp consumes: no mbarrier phase aliasing.
-constexpr int kStagesDefault = 7;      // s == 1 and workspace-combine kernels: 224 KB ring, 8 warps
-constexpr int kStagesCluster = 6;      // cluster-combine kernels: 192 KB ring + DSMEM push slots
+// Ring stages and consumer warps: stages are a multiple of warps and warp w owns stages
+// w, w + NW, ... (consuming them in tile order), so no warp can observe a stale mbarrier
+// phase.  Few consumer warps keep the cross-warp merge small (it reads one partial per
+// warp); a deep ring keeps a single CTA's TMA ingest busy.  DESIGN.md §5.
+// Per combine mode (A/B-measured on B200, scripts/ab_variants.py):
+//   NONE (s == 1)        7 stages / 7 warps: a single CTA is TMA-ingest bound, keep 224 KB in flight
+//   CLUSTER (2..8)       6 stages / 3 warps: few tiles per CTA, small cross-warp merge, + push slots
+//   KERNEL (s > 8)       4 stages / 4 warps: HBM-streaming splits (long context)
+// (each value can be overridden with -DDECATTN_<MODE>_<STAGES|WARPS>=n for A/B builds)
+#ifndef DECATTN_NONE_STAGES
+#define DECATTN_NONE_STAGES 7
+#endif
+#ifndef DECATTN_NONE_WARPS
+#define DECATTN_NONE_WARPS 7
+#endif
+#ifndef DECATTN_CLUSTER_STAGES
+#define DECATTN_CLUSTER_STAGES 6
+#endif
+#ifndef DECATTN_CLUSTER_WARPS
+#define DECATTN_CLUSTER_WARPS 3
+#endif
+#ifndef DECATTN_KERNEL_STAGES
+#define DECATTN_KERNEL_STAGES 4
+#endif
+#ifndef DECATTN_KERNEL_WARPS
+#define DECATTN_KERNEL_WARPS 4
+#endif
+constexpr int kStagesNone = DECATTN_NONE_STAGES, kWarpsNone = DECATTN_NONE_WARPS;
+constexpr int kStagesCluster = DECATTN_CLUSTER_STAGES, kWarpsCluster = DECATTN_CLUSTER_WARPS;
+constexpr int kStagesKernel = DECATTN_KERNEL_STAGES, kWarpsKernel = DECATTN_KERNEL_WARPS;
+DA_HD constexpr int stages_for(int combine_mode) {
+  return combine_mode == 0 ? kStagesNone : (combine_mode == 1 ? kStagesCluster : kStagesKernel);
+}
+DA_HD constexpr int warps_for(int combine_mode) {
+  return combine_mode == 0 ? kWarpsNone : (combine_mode == 1 ? kWarpsCluster : kWarpsKernel);
+}
 constexpr int kMaxClusterSplits = 8;   // portable cluster size
 // One pushed row: O[128] fp32, (m, l), padding to 16 bytes.  A rank owns ceil(R/s) rows and
 // receives them from all s ranks (itself included): at most max_s s ceil(16/s) = 21 rows (s = 7).
 constexpr int kSlotRowFloats = kHeadDim + 4;
 constexpr int kMaxSlotRows = 21;
-DA_HD constexpr int threads_for(int stages) { return (stages + 1) * 32; }   // + 1 TMA producer warp
+DA_HD constexpr int threads_for(int warps) { return (warps + 1) * 32; }   // + 1 TMA producer warp
 DA_HD constexpr int smem_for(int stages, bool cluster) {
   return stages * kStageBytes + (cluster ? kMaxSlotRows * kSlotRowFloats * 4 : 0) + 1024;
 }

@@ -271,14 +271,15 @@ __device__ __forceinline__ void split_range(int n, int split, int s, int& t0, in
 
 // ---------------------------------------------------------------------------
 // The kernel.  kPath: DA_PATH_SCALAR / DA_PATH_MMA; kNB: g-blocks of 8 query
-// rows (MMA path); kCombine: da_combine_mode; NS: ring stages = consumer warps.
+// rows (MMA path); kCombine: da_combine_mode; NS: ring stages; NW: consumer warps
+// (NS a multiple of NW: warp w owns stages w, w + NW, ... and consumes them in order).
 // ---------------------------------------------------------------------------
-template <int kPath, int kNB, int kCombine, int NS>
-__global__ void __launch_bounds__(threads_for(NS), 1)
+template <int kPath, int kNB, int kCombine, int NS, int NW>
+__global__ void __launch_bounds__(threads_for(NW), 1)
     split_kv_fwd_kernel(const __grid_constant__ CUtensorMap tmap_k,
                         const __grid_constant__ CUtensorMap tmap_v, const FwdParams p) {
-  constexpr int NW = NS;                                   // consumer warps; warp w owns stage w
-  constexpr int kT = threads_for(NS);                      // all threads (consumers + producer)
+  static_assert(NS % NW == 0, "each consumer warp must own whole ring stages");
+  constexpr int kT = threads_for(NW);                      // all threads (consumers + producer)
   constexpr int R = kPath == DA_PATH_MMA ? 8 * kNB : 1;    // query rows of this CTA
   constexpr int kIters = (R * 32 + kT - 1) / kT;           // merge passes: element = (row, float4)
   constexpr bool kCluster = kCombine == DA_COMBINE_CLUSTER;
@@ -379,12 +380,8 @@ __global__ void __launch_bounds__(threads_for(NS), 1)
     __syncwarp();
     asm volatile("bar.sync 0;" ::: "memory");   // (A) pairs with the consumers' barrier
   } else {
-    // ================= consumers: warp w handles tiles w, w + NW, ... (all in stage w) =======
+    // ================= consumers: warp w handles tiles w, w + NW, ... (stages it owns) =======
     const uint16_t* qrow = p.q + static_cast<int64_t>(b) * p.q_sb;
-    const uint32_t sK = sbase + warp * kStageBytes;
-    const uint32_t sV = sK + 2 * kHalfBytes;
-    const uint32_t fb = smem_u32(&full_bar[warp]);
-    const uint32_t eb = smem_u32(&empty_bar[warp]);
     if constexpr (kPath == DA_PATH_MMA) {
       uint32_t qf[8][kNB][2];
 #pragma unroll
@@ -409,8 +406,11 @@ __global__ void __launch_bounds__(threads_for(NS), 1)
 #pragma unroll
       for (int nb = 0; nb < kNB; ++nb) m[nb][0] = m[nb][1] = kNegInf, l[nb][0] = l[nb][1] = 0.f;
 
-      for (int i = warp, round = 0; i < n_tiles; i += NW, ++round) {
-        mbar_wait(fb, round & 1);
+      for (int i = warp; i < n_tiles; i += NW) {
+        const int st = i % NS;
+        const uint32_t sK = sbase + st * kStageBytes;
+        const uint32_t sV = sK + 2 * kHalfBytes;
+        mbar_wait(smem_u32(&full_bar[st]), (i / NS) & 1);
         if (lane == 0 && i < 8) TRACE(10 + i);
         const int valid = min(kTileN, t_end - (t0 + i * kTileN));
         if (valid < kTileN) {
@@ -424,7 +424,7 @@ __global__ void __launch_bounds__(threads_for(NS), 1)
         }
         mma_tile<kNB>(sK, sV, valid, qf, o, m, l, p.scale_log2, lane);
         __syncwarp();
-        if (lane == 0) mbar_arrive(eb);
+        if (lane == 0) mbar_arrive(smem_u32(&empty_bar[st]));
         if (lane == 0 && i < 8) TRACE(18 + i);
       }
       // finish l: sum the partial sums of the 8 lanes that share a g column
@@ -464,12 +464,14 @@ __global__ void __launch_bounds__(threads_for(NS), 1)
       for (int c = 0; c < 16; ++c) qv[c] = __ldg(q4 + c);
       float o[4] = {0.f, 0.f, 0.f, 0.f};
       float m = kNegInf, l = 0.f;
-      for (int i = warp, round = 0; i < n_tiles; i += NW, ++round) {
-        mbar_wait(fb, round & 1);
+      for (int i = warp; i < n_tiles; i += NW) {
+        const int st = i % NS;
+        const uint32_t sK = sbase + st * kStageBytes;
+        mbar_wait(smem_u32(&full_bar[st]), (i / NS) & 1);
         const int valid = min(kTileN, t_end - (t0 + i * kTileN));
-        scalar_tile(sK, sV, valid, qv, o, m, l, p.scale_log2, lane);
+        scalar_tile(sK, sK + 2 * kHalfBytes, valid, qv, o, m, l, p.scale_log2, lane);
         __syncwarp();
-        if (lane == 0) mbar_arrive(eb);
+        if (lane == 0) mbar_arrive(smem_u32(&empty_bar[st]));
       }
 #pragma unroll
       for (int off = 16; off > 0; off >>= 1) l += __shfl_xor_sync(0xffffffffu, l, off);
@@ -575,31 +577,22 @@ __global__ void __launch_bounds__(threads_for(NS), 1)
       const int rl = t >> 5, d4 = t & 31;
       const int g = static_cast<int>(rank) + rl * s;
       if (g >= rows_valid) break;   // rows of a rank ascend with t: the rest are invalid too
-      float2 mlr[kMaxClusterSplits];
-      float4 orr[kMaxClusterSplits];
-#pragma unroll
-      for (int r = 0; r < kMaxClusterSplits; ++r) {
-        mlr[r] = make_float2(kNegInf, 0.f);
-        orr[r] = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (r < s) {
-          const float* sl = slots + (r * rows_per_owner + rl) * kSlotRowFloats;
-          mlr[r] = *reinterpret_cast<const float2*>(sl + kHeadDim);
-          orr[r] = *reinterpret_cast<const float4*>(sl + 4 * d4);
-        }
-      }
-      float M = kNegInf;
-#pragma unroll
-      for (int r = 0; r < kMaxClusterSplits; ++r) M = fmaxf(M, mlr[r].x);
-      float Lsum = 0.f;
+      float M = kNegInf, Lsum = 0.f;
       float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-      for (int r = 0; r < kMaxClusterSplits; ++r) {
-        const float f = mlr[r].x == kNegInf ? 0.f : ex2(mlr[r].x - M);
-        Lsum = fmaf(f, mlr[r].y, Lsum);
-        acc.x = fmaf(f, orr[r].x, acc.x);
-        acc.y = fmaf(f, orr[r].y, acc.y);
-        acc.z = fmaf(f, orr[r].z, acc.z);
-        acc.w = fmaf(f, orr[r].w, acc.w);
+#pragma unroll 1
+      for (int r = 0; r < s; ++r) {
+        const float* sl = slots + (r * rows_per_owner + rl) * kSlotRowFloats;
+        const float2 ml = *reinterpret_cast<const float2*>(sl + kHeadDim);
+        const float4 ow = *reinterpret_cast<const float4*>(sl + 4 * d4);
+        const float Mn = fmaxf(M, ml.x);
+        const float fa = M == kNegInf ? 0.f : ex2(M - Mn);
+        const float fb = ml.x == kNegInf ? 0.f : ex2(ml.x - Mn);
+        Lsum = Lsum * fa + ml.y * fb;
+        acc.x = acc.x * fa + ow.x * fb;
+        acc.y = acc.y * fa + ow.y * fb;
+        acc.z = acc.z * fa + ow.z * fb;
+        acc.w = acc.w * fa + ow.w * fb;
+        M = Mn;
       }
       const float inv = Lsum > 0.f ? __frcp_rn(Lsum) : 0.f;
       const size_t row = static_cast<size_t>(b) * p.h_q + hq0 + g;
@@ -621,9 +614,10 @@ template <int kPath, int kNB, int kCombine>
 cudaError_t launch_impl(const da_plan& plan, const CUtensorMap& tk, const CUtensorMap& tv,
                         const FwdParams& p, cudaStream_t stream) {
   constexpr bool kCluster = kCombine == DA_COMBINE_CLUSTER;
-  constexpr int NS = kCluster ? kStagesCluster : kStagesDefault;
+  constexpr int NS = stages_for(kCombine);
+  constexpr int NW = warps_for(kCombine);
   constexpr int kSmem = smem_for(NS, kCluster);
-  auto kern = split_kv_fwd_kernel<kPath, kNB, kCombine, NS>;
+  auto kern = split_kv_fwd_kernel<kPath, kNB, kCombine, NS, NW>;
   // One-time (per device) opt-in to > 48 KB of dynamic shared memory.
   static std::atomic<uint64_t> attr_done{0};
   int dev = 0;
@@ -637,7 +631,7 @@ cudaError_t launch_impl(const da_plan& plan, const CUtensorMap& tk, const CUtens
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(plan.grid_x, plan.grid_y, plan.grid_z);
-  cfg.blockDim = dim3(threads_for(NS), 1, 1);
+  cfg.blockDim = dim3(threads_for(NW), 1, 1);
   cfg.dynamicSmemBytes = kSmem;
   cfg.stream = stream;
   cudaLaunchAttribute attrs[2];
