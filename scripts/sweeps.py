@@ -1,0 +1,142 @@
+"""The paper's three measurement experiments, re-run on B200.
+
+    python scripts/sweeps.py table1   -> profiles/<tag>_table1.csv       (Table 1)
+    python scripts/sweeps.py ucurve   -> profiles/<tag>_ucurve.csv       (Fig. 2)
+    python scripts/sweeps.py regress  -> profiles/<tag>_regression.csv   (P:L175-179, 160 configs)
+    python scripts/sweeps.py all
+
+Timing = bench.py's method: each policy's steps captured in a CUDA graph, replays
+A/B-interleaved, medians of the per-step time; KV buffers rotate through > 2x L2 with an
+L2 scrub before every replay (cold-cache numbers).  CSV columns follow SPEC's schema
+(S:L295): batch,l_q,l_k,h_q,h_kv,d,nblk,total_mblocks,policy,num_splits,latency_us,
+baseline_us,speedup,regression (+ p10/p90).  H_Q = 8 H_KV as in the paper's Llama shapes
+(P:L37).  "regression" = speedup < 0.99.
+"""
+
+import csv
+import os
+import statistics
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+import bench  # noqa: E402  (Workload, make_graph, Timer)
+import paper_2604_00028_b200 as dec  # noqa: E402
+
+TAG = os.environ.get("SWEEP_TAG", "r01")
+OUT = os.path.join(ROOT, "profiles")
+D = 128
+
+
+def timed_graphs(cfg, plans, steps, rounds, seed):
+    """Interleaved replays of one CUDA graph per plan over the same rotating KV buffers."""
+    dev = torch.device("cuda", 0)
+    l2 = torch.cuda.get_device_properties(0).L2_cache_size
+    w = bench.Workload(cfg, dev, seed, l2, max_rot_bytes=200 << 20)
+    stream = torch.cuda.Stream()
+    timer = bench.Timer(dev)
+    graphs = [bench.make_graph(dec, p, w, steps, stream) for p in plans]
+    res = [[] for _ in plans]
+    for _ in range(rounds):
+        for i, g in enumerate(graphs):
+            res[i].append(timer.time_replay(g, stream) * 1e3 / steps)
+    del graphs, w, timer
+    torch.cuda.empty_cache()
+    out = []
+    for r in res:
+        r = sorted(r)
+        out.append((statistics.median(r), r[len(r) // 10], r[(9 * len(r)) // 10]))
+    return out
+
+
+def steps_for(cfg):
+    kv = 4 * cfg["batch"] * cfg["l_k"] * cfg["h_kv"] * D
+    return 200 if kv < (64 << 20) else (40 if kv < (512 << 20) else 10)
+
+
+FIELDS = ["batch", "l_q", "l_k", "h_q", "h_kv", "d", "nblk", "total_mblocks", "policy", "num_splits",
+          "latency_us", "baseline_us", "speedup", "regression", "p10_us", "p90_us", "combine_mode"]
+
+
+def ab_row(cfg, rounds=15, seed=7):
+    plans = [dec.make_plan(cfg["batch"], cfg["h_q"], cfg["h_kv"], cfg["l_k"], policy=p)
+             for p in ("guarded", "seq_aware")]
+    (tg, g10, g90), (ts, s10, s90) = timed_graphs(cfg, plans, steps_for(cfg), rounds, seed)
+    rows = []
+    for plan, (t, p10, p90), pol in ((plans[0], (tg, g10, g90), "guarded"), (plans[1], (ts, s10, s90), "seq_aware")):
+        rows.append(dict(batch=cfg["batch"], l_q=1, l_k=cfg["l_k"], h_q=cfg["h_q"], h_kv=cfg["h_kv"], d=D,
+                         nblk=plan.num_n_blocks, total_mblocks=plan.total_mblocks, policy=pol,
+                         num_splits=plan.num_splits, latency_us=round(t, 3), baseline_us=round(tg, 3),
+                         speedup=round(tg / t, 4), regression=int(tg / t < 0.99), p10_us=round(p10, 3),
+                         p90_us=round(p90, 3), combine_mode=plan.combine_mode))
+    return rows
+
+
+def write(name, rows, fields=FIELDS):
+    os.makedirs(OUT, exist_ok=True)
+    path = os.path.join(OUT, f"{TAG}_{name}.csv")
+    with open(path, "w", newline="") as f:
+        w = csv.DictWriter(f, fieldnames=fields)
+        w.writeheader()
+        w.writerows(rows)
+    print(f"wrote {path} ({len(rows)} rows)", flush=True)
+
+
+def table1():
+    rows = []
+    for lk in (128, 256, 384, 512, 2048, 4096):
+        for hkv in (1, 2, 8):
+            rows += ab_row(dict(batch=1, h_q=8 * hkv, h_kv=hkv, l_k=lk))
+            r = rows[-1]
+            print(f"L_K={lk:5d} H_KV={hkv}: guarded {rows[-2]['latency_us']:7.2f} us  seq-aware "
+                  f"{r['latency_us']:7.2f} us (s {rows[-2]['num_splits']} -> {r['num_splits']})  "
+                  f"{r['speedup']:.3f}x", flush=True)
+    write("table1", rows)
+
+
+def ucurve():
+    rows = []
+    for hkv in (1, 2):
+        cfg = dict(batch=1, h_q=8 * hkv, h_kv=hkv, l_k=512)
+        svals = list(range(1, 17)) + [20, 24, 32, 48, 64]
+        plans = [dec.make_plan(1, 8 * hkv, hkv, 512, policy="fixed", forced_splits=s) for s in svals]
+        times = timed_graphs(cfg, plans, 200, 15, 11)
+        base = times[0][0]
+        for s, plan, (t, p10, p90) in zip(svals, plans, times):
+            rows.append(dict(h_kv=hkv, s=s, s_effective=plan.nonempty_splits, combine_mode=plan.combine_mode,
+                             latency_us=round(t, 3), p10_us=round(p10, 3), p90_us=round(p90, 3),
+                             speedup_vs_s1=round(base / t, 4)))
+            print(f"H_KV={hkv} s={s:3d} ({plan.nonempty_splits:2d} non-empty, combine {plan.combine_mode}): "
+                  f"{t:6.2f} us  {base / t:.3f}x vs s=1", flush=True)
+    write("ucurve", rows, ["h_kv", "s", "s_effective", "combine_mode", "latency_us", "p10_us", "p90_us",
+                            "speedup_vs_s1"])
+
+
+def regress():
+    rows = []
+    for b in (1, 2, 4, 8):
+        for lk in (128, 256, 384, 512, 1024, 2048, 4096, 8192):
+            for hkv in (1, 2, 4, 8, 32):
+                rows += ab_row(dict(batch=b, h_q=8 * hkv, h_kv=hkv, l_k=lk), rounds=9)
+                r = rows[-1]
+                flag = "  <-- differs" if r["num_splits"] != rows[-2]["num_splits"] else ""
+                print(f"B={b} L_K={lk:5d} H_KV={hkv:2d}: {rows[-2]['latency_us']:8.2f} -> {r['latency_us']:8.2f} us "
+                      f"{r['speedup']:.3f}x{flag}", flush=True)
+    write("regression", rows)
+    seq = [r for r in rows if r["policy"] == "seq_aware"]
+    worst = min(seq, key=lambda r: r["speedup"])
+    print(f"160 configs: min speedup {worst['speedup']:.3f} at B={worst['batch']} L_K={worst['l_k']} "
+          f"H_KV={worst['h_kv']}; regressions (< 0.99x): {sum(r['regression'] for r in seq)}")
+
+
+if __name__ == "__main__":
+    what = sys.argv[1] if len(sys.argv) > 1 else "all"
+    if what in ("table1", "all"):
+        table1()
+    if what in ("ucurve", "all"):
+        ucurve()
+    if what in ("regress", "all"):
+        regress()

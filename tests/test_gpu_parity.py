@@ -173,3 +173,44 @@ def test_deterministic_replay():
     b, lb = dec.forward(plan, inp["q"], inp["k"], inp["v"], inp["seqlens"])
     torch.cuda.synchronize()
     assert torch.equal(a, b) and torch.equal(la, lb)
+
+
+# ---- BASELINE.json full sizes, in bench.py's launch configuration (cache_seqlens = NULL, plan
+#      cached per shape); sampled (b, kv-head) groups checked against the oracle one by one ------
+def _check_sampled(cfg, policy, picks, seed, variant="normal"):
+    dec = _dec()
+    B, HQ, HKV, L = cfg["batch"], cfg["h_q"], cfg["h_kv"], cfg["l_k"]
+    inp = synth.make_inputs(B, HQ, HKV, L, device="cuda", seed=seed, variant=variant)
+    plan = dec.make_plan(B, HQ, HKV, L, policy=policy)
+    seq = None if variant == "normal" else inp["seqlens"]
+    out, lse = dec.forward(plan, inp["q"], inp["k"], inp["v"], seq)
+    torch.cuda.synchronize()
+    G = HQ // HKV
+    for b, g in picks:
+        rows = slice(g * G, (g + 1) * G)
+        q = synth.to_f64(inp["q"][b:b + 1, rows])
+        k = synth.to_f64(inp["k"][b:b + 1, :, g:g + 1])
+        v = synth.to_f64(inp["v"][b:b + 1, :, g:g + 1])
+        n = [L] if seq is None else [int(seq[b])]
+        ref_o, ref_l = OA.decode_attention(q, k, v, n)
+        assert_out_close(synth.to_f64(out[b:b + 1, rows]), ref_o, f"out[b={b}, g={g}]")
+        assert_lse_close(synth.to_f64(lse[b:b + 1, rows]), ref_l, f"lse[b={b}, g={g}]")
+    return plan
+
+
+def test_full_size_high_load_sampled():
+    cfg = synth.CONFIGS["high_load"]               # B=128 H_Q=64 H_KV=8 L_K=8192 (4.3 GB of KV)
+    plan = _check_sampled(cfg, "seq_aware", [(0, 0), (17, 3), (64, 7), (127, 5), (99, 1)], 1003)
+    assert plan.num_splits == 1
+
+
+def test_full_size_long_context_sampled():
+    cfg = synth.CONFIGS["long_context"]            # B=1 H_Q=64 H_KV=8 L_K=131072, s = 16 workspace combine
+    plan = _check_sampled(cfg, "seq_aware", [(0, 0), (0, 5), (0, 7)], 1004)
+    assert plan.num_splits == 16 and plan.combine_mode == _dec().DA_COMBINE_KERNEL
+
+
+def test_full_size_long_context_ragged_sampled():
+    # ragged lengths at the long-context size: batch of 3 with 0 / 1 / random tokens
+    cfg = dict(synth.CONFIGS["long_context"], batch=3)
+    _check_sampled(cfg, "seq_aware", [(0, 1), (1, 2), (2, 4)], 1005, variant="ragged")
