@@ -95,7 +95,7 @@ typedef enum da_dtype { DA_BF16 = 0, DA_F32 = 1 } da_dtype;
 /* How the s > 1 split partials are merged. */
 typedef enum da_combine_mode {
   DA_COMBINE_NONE = 0,     /* s == 1: the split CTA writes out/lse directly   */
-  DA_COMBINE_CLUSTER = 1,  /* 2 <= s <= 8: the s split CTAs of one tile form a
+  DA_COMBINE_CLUSTER = 1,  /* 2 <= s <= 16: the s split CTAs of one tile form a
                               thread-block cluster and merge through
                               distributed shared memory inside the forward
                               kernel (no workspace, no second launch)          */
@@ -156,7 +156,9 @@ typedef struct da_plan {
  *   out        : written on DA_OK only.
  * Pure host code: no CUDA call, no allocation.  Errors: DA_ERR_INVALID_ARG,
  * DA_ERR_UNSUPPORTED (head_dim != 128).
- * Default combine mode: NONE for s == 1, CLUSTER for 2 <= s <= 8, else KERNEL.
+ * Default combine mode: NONE for s == 1; CLUSTER for 2 <= s <= 16 when all
+ * clusters of the launch fit one wave on the device (measured B200 co-residency
+ * table, scaled by num_sms / 148); else KERNEL.
  */
 DA_API da_status da_plan_make(int32_t batch, int32_t h_q, int32_t h_kv, int32_t l_k,
                        int32_t head_dim, int32_t pack_gqa, int32_t sm_margin,
@@ -165,7 +167,7 @@ DA_API da_status da_plan_make(int32_t batch, int32_t h_q, int32_t h_kv, int32_t 
 
 /*
  * da_plan_set_combine - switch an existing plan to another combine mode and
- * re-derive its launch fields.  NONE requires s == 1, CLUSTER 2 <= s <= 8,
+ * re-derive its launch fields.  NONE requires s == 1, CLUSTER 2 <= s <= 16,
  * KERNEL s >= 2.  Errors: DA_ERR_INVALID_ARG.
  */
 DA_API da_status da_plan_set_combine(da_plan* plan, int32_t combine_mode);

@@ -173,7 +173,7 @@ extern "C" da_status da_combine(int32_t num_splits, int32_t batch, int32_t h_q, 
   if (head_dim != kHeadDim) return DA_ERR_UNSUPPORTED;
   if (out_dtype != DA_BF16 && out_dtype != DA_F32) return DA_ERR_INVALID_ARG;
   const int64_t rows = int64_t(batch) * h_q;
-  if (rows > INT32_MAX / 2) return DA_ERR_UNSUPPORTED;
+  if (rows > INT32_MAX / 2) return DA_ERR_UNSUPPORTED;   // one CTA per row (grid.x)
   if (num_splits > 1 && (o_split_stride < rows * kHeadDim || lse_split_stride < rows))
     return DA_ERR_INVALID_ARG;
   if (o_split_stride % 4 != 0 || !aligned16(o_partial) || !aligned16(out) ||

@@ -59,15 +59,19 @@ DA_HD constexpr int stages_for(int combine_mode) {
 DA_HD constexpr int warps_for(int combine_mode) {
   return combine_mode == 0 ? kWarpsNone : (combine_mode == 1 ? kWarpsCluster : kWarpsKernel);
 }
-constexpr int kMaxClusterSplits = 8;   // portable cluster size
+constexpr int kMaxClusterSplits = 16;  // cluster combine up to 16 CTAs (non-portable size, B200)
 // One pushed row: O[128] fp32, (m, l), padding to 16 bytes.  A rank owns ceil(R/s) rows and
-// receives them from all s ranks (itself included): at most max_s s ceil(16/s) = 21 rows (s = 7).
+// receives them from all s ranks (itself included): at most max_{s<=16} s ceil(16/s) = 30 rows (s = 15).
 constexpr int kSlotRowFloats = kHeadDim + 4;
-constexpr int kMaxSlotRows = 21;
+constexpr int kMaxSlotRows = 30;
+// Co-resident clusters of s CTAs (one CTA per SM, the cluster kernel's ~209 KB of shared memory)
+// measured on B200 (148 SMs) with cudaOccupancyMaxActiveClusters (scripts/microbench_cluster16.cu).
+// Cluster placement is GPC-bound, hence not simply 148 / s.  Index: s (0, 1 unused).
+constexpr int kMaxActiveClustersB200[17] = {0, 148, 74, 45, 33, 26, 22, 15, 15, 15, 11, 7, 7, 7, 7, 7, 7};
 DA_HD constexpr int threads_for(int warps) { return (warps + 1) * 32; }   // + 1 TMA producer warp
 DA_HD constexpr int smem_for(int stages, bool cluster) {
   return stages * kStageBytes + (cluster ? kMaxSlotRows * kSlotRowFloats * 4 : 0) + 1024;
 }
-constexpr int kCombineRowsPerCta = 4;  // combine kernel: one warp per (b, h) row
+constexpr int kCombineThreads = 128;   // combine kernel: one CTA of 4 warps per (b, h) row
 
 }  // namespace decattn

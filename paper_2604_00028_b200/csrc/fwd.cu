@@ -627,6 +627,10 @@ cudaError_t launch_impl(const da_plan& plan, const CUtensorMap& tk, const CUtens
   if ((attr_done.load(std::memory_order_acquire) & bit) == 0) {
     err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
     if (err != cudaSuccess) return err;
+    if (kCluster) {   // clusters of 9..16 CTAs are a non-portable size
+      err = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      if (err != cudaSuccess) return err;
+    }
     attr_done.fetch_or(bit, std::memory_order_acq_rel);
   }
   cudaLaunchConfig_t cfg = {};

@@ -79,6 +79,21 @@ void derive_launch(da_plan* p) {
       : 0;
 }
 
+// s == 1: NONE.  2 <= s <= 16: CLUSTER when every cluster of the launch is co-resident in one
+// wave (the B200 table in config.h, scaled by the usable SM count), else the workspace +
+// combine-kernel path, which has no placement constraint.
+int default_combine_mode(const da_plan& p) {
+  const int s = p.num_splits;
+  if (s == 1) return DA_COMBINE_NONE;
+  if (s > kMaxClusterSplits) return DA_COMBINE_KERNEL;
+  const int G = p.h_q / p.h_kv;
+  const bool mma = p.pack_gqa != 0 && G >= 2;
+  const int64_t rows = mma ? (G <= 8 ? 8 : 16) : 1;
+  const int64_t clusters = static_cast<int64_t>(p.batch) * (mma ? p.h_kv * ceil_div(G, rows) : p.h_q);
+  const int64_t fit = static_cast<int64_t>(kMaxActiveClustersB200[s]) * p.num_sms / 148;
+  return clusters <= fit ? DA_COMBINE_CLUSTER : DA_COMBINE_KERNEL;
+}
+
 bool combine_mode_valid(int mode, int s) {
   switch (mode) {
     case DA_COMBINE_NONE: return s == 1;
@@ -129,8 +144,7 @@ extern "C" da_status da_plan_make(int32_t batch, int32_t h_q, int32_t h_kv, int3
   p.split_unit = kSplitUnit;
   const int64_t units = ceil_div(l_k, kSplitUnit);
   p.nonempty_splits = static_cast<int32_t>(units < s ? units : s);
-  p.combine_mode = s == 1 ? DA_COMBINE_NONE
-                 : (s <= kMaxClusterSplits ? DA_COMBINE_CLUSTER : DA_COMBINE_KERNEL);
+  p.combine_mode = default_combine_mode(p);
   derive_launch(&p);
   *out = p;
   return DA_OK;

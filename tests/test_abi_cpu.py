@@ -52,6 +52,20 @@ def _expected_launch(b, hq, hkv, pack, s):
     return (1 if mma else 0), rows, (s, gy, b)
 
 
+# cluster combine when every cluster of the launch is co-resident in one wave
+# (B200 table of cudaOccupancyMaxActiveClusters at the cluster kernel's shared memory).
+_FIT = [0, 148, 74, 45, 33, 26, 22, 15, 15, 15, 11, 7, 7, 7, 7, 7, 7]
+
+
+def _expected_combine(b, hq, hkv, pack, sms, s):
+    if s == 1:
+        return 0
+    if s > 16:
+        return 2
+    _, _, (_, gy, gz) = _expected_launch(b, hq, hkv, pack, s)
+    return 1 if gy * gz <= _FIT[s] * sms // 148 else 2
+
+
 def _check_plan(L, b, hq, hkv, lk, pack, margin, sms, pol, forced=0):
     p = L.da_plan_make(b, hq, hkv, lk, 128, pack, margin, sms, pol, forced)
     s, rule = OP.num_splits(b, hq, hkv, lk, sms, margin, pol, forced)
@@ -62,7 +76,7 @@ def _check_plan(L, b, hq, hkv, lk, pack, margin, sms, pol, forced=0):
     path, rows, grid = _expected_launch(b, hq, hkv, pack, s)
     assert (p.path, p.rows_per_cta, (p.grid_x, p.grid_y, p.grid_z)) == (path, rows, grid)
     assert p.workspace_bytes == (s * b * hq * 129 * 4 if s > 1 else 0)
-    assert p.combine_mode == (0 if s == 1 else (1 if s <= 8 else 2))
+    assert p.combine_mode == _expected_combine(b, hq, hkv, pack, sms, s)
     assert p.nonempty_splits == min(s, -(-lk // 64))
 
 
@@ -156,10 +170,14 @@ def test_set_combine_rules(L):
     assert p.cluster_x == 1 and p.workspace_bytes == 3 * 8 * 129 * 4
     with pytest.raises(L.DecAttnError):
         L.da_plan_set_combine(p, L.DA_COMBINE_NONE)          # s = 3 needs a combine
-    q = L.da_plan_make(1, 8, 1, 512, 128, 1, 0, 148, "fixed", 9)
+    q = L.da_plan_make(1, 8, 1, 512, 128, 1, 0, 148, "fixed", 17)
     assert q.combine_mode == L.DA_COMBINE_KERNEL
     with pytest.raises(L.DecAttnError):
-        L.da_plan_set_combine(q, L.DA_COMBINE_CLUSTER)       # cluster only for s <= 8
+        L.da_plan_set_combine(q, L.DA_COMBINE_CLUSTER)       # cluster only for s <= 16
+    q = L.da_plan_make(1, 8, 1, 512, 128, 1, 0, 148, "fixed", 12)
+    assert q.combine_mode == L.DA_COMBINE_CLUSTER and q.cluster_x == 12
+    q = L.da_plan_make(16, 64, 8, 4096, 128, 1, 0, 148, "fixed", 8)   # 128 clusters of 8 > 15
+    assert q.combine_mode == L.DA_COMBINE_KERNEL
 
 
 # ---- da_forward / da_combine validation (fake device pointers: every check below
@@ -178,7 +196,7 @@ def _fwd(L, plan, **kw):
 
 
 def test_forward_validation(L):
-    p = L.da_plan_make(1, 8, 1, 512, 128, 1, 0, 148, "fixed", 12)   # KERNEL combine
+    p = L.da_plan_make(1, 8, 1, 512, 128, 1, 0, 148, "fixed", 20)   # KERNEL combine
     assert _fwd(L, p, q=None) == L.DA_ERR_INVALID_ARG
     assert _fwd(L, p, out=None) == L.DA_ERR_INVALID_ARG
     assert _fwd(L, p, l_cap=511) == L.DA_ERR_INVALID_ARG
@@ -195,7 +213,7 @@ def test_forward_validation(L):
     bad.head_dim = 64
     assert _fwd(L, bad) == L.DA_ERR_UNSUPPORTED
     bad = L.da_plan.from_buffer_copy(p)
-    bad.combine_mode = L.DA_COMBINE_NONE             # s = 12 cannot skip the combine
+    bad.combine_mode = L.DA_COMBINE_NONE             # s = 20 cannot skip the combine
     assert _fwd(L, bad) == L.DA_ERR_INVALID_ARG
 
 

@@ -89,9 +89,15 @@ def test_forced_splits_kernel_combine_partials(s):
                   variant="ragged", seed=7)
 
 
-@pytest.mark.parametrize("s", [2, 3, 7, 8])
+@pytest.mark.parametrize("s", [2, 3, 7, 8, 9, 12, 16])
 def test_cluster_combine(s):
     run_and_check(2, 8, 1, 1000, policy="fixed", forced=s, combine_mode=1, seed=11)
+
+
+@pytest.mark.parametrize("s", [5, 11, 15, 16])
+def test_cluster_combine_16_rows(s):
+    # G = 16 query rows per CTA: the largest push-slot use (s ceil(16 / s) rows per owner)
+    run_and_check(1, 32, 2, 1500, policy="fixed", forced=s, combine_mode=1, seed=13, variant="ragged")
 
 
 # ---- head grouping / paths ----------------------------------------------------
