@@ -216,20 +216,24 @@ class Timer:
         return e0.elapsed_time(e1)  # ms
 
 
+AB_POLICIES = ("guarded", "seq_aware", "seq_aware_sm", "evolved")
+
+
 def ab_compare(dec, dev, stream, timer, cfg, steps, rounds, l2, seed, num_sms):
-    """Guarded vs seq-aware, interleaved replays (P:L119 A/B) -> medians in us/step."""
+    """Guarded vs the paper's seq-aware (and the SM-count-aware generalisation, the evolved
+    Fig. 1 policy), interleaved replays (P:L119 A/B) -> medians in us/step."""
     w = Workload(cfg, dev, seed, l2)
     res = {}
     graphs = {}
-    for pol in ("guarded", "seq_aware"):
+    for pol in AB_POLICIES:
         plan = dec.make_plan(cfg["batch"], cfg["h_q"], cfg["h_kv"], cfg["l_k"], policy=pol)
         graphs[pol] = (plan, make_graph(dec, plan, w, steps, stream))
         res[pol] = []
     for _ in range(rounds):
-        for pol in ("guarded", "seq_aware"):
+        for pol in AB_POLICIES:
             res[pol].append(timer.time_replay(graphs[pol][1], stream) * 1e3 / steps)
     out = {}
-    for pol in ("guarded", "seq_aware"):
+    for pol in AB_POLICIES:
         plan = graphs[pol][0]
         us = statistics.median(res[pol])
         out[pol] = {"num_splits": plan.num_splits, "combine_mode": plan.combine_mode,
@@ -239,6 +243,8 @@ def ab_compare(dec, dev, stream, timer, cfg, steps, rounds, l2, seed, num_sms):
                     "p90_us": round(sorted(res[pol])[(9 * len(res[pol])) // 10], 3),
                     "gbs": round(w.bytes / (us * 1e-6) / 1e9, 1)}
     out["speedup_seq_aware_vs_guarded"] = round(out["guarded"]["us_per_step"] / out["seq_aware"]["us_per_step"], 4)
+    out["speedup_seq_aware_sm_vs_guarded"] = round(out["guarded"]["us_per_step"] / out["seq_aware_sm"]["us_per_step"], 4)
+    out["speedup_evolved_vs_guarded"] = round(out["guarded"]["us_per_step"] / out["evolved"]["us_per_step"], 4)
     out["config"] = dict(cfg, head_dim=HEAD_DIM)
     out["l2"] = w.l2_note(l2)
     del w, graphs

@@ -75,7 +75,13 @@ typedef enum da_policy {
                                L_K <= 512, else efficiency loop */
   DA_POLICY_SEQ_AWARE = 1,  /* Fig. 3: Guard 1, Guard 2, low-tile
                                override s = 3, else efficiency loop */
-  DA_POLICY_FIXED = 2       /* s = forced_splits (the U-curve sweep) */
+  DA_POLICY_FIXED = 2,      /* s = forced_splits (the U-curve sweep) */
+  DA_POLICY_EVOLVED = 3,    /* Fig. 1: batch == 1 -> 12 (16 when
+                               L_K < 256); batch != 1 -> guarded            */
+  DA_POLICY_SEQ_AWARE_SM = 4 /* SM-count-aware generalisation (DESIGN.md
+                               C-ext-1): in the nblk <= 4
+                               region s = min(4, ceil(L_K/64)/2, (U-1)/T),
+                               s = 1 below 6 units; B200-calibrated         */
 } da_policy;
 
 /* Which step of the cascade decided num_splits (SPEC's "source"). */
@@ -86,7 +92,10 @@ typedef enum da_rule {
   DA_RULE_GUARD2 = 3,       /* seq-aware: nblk <= 4, T >= 4         */
   DA_RULE_LOW_TILE = 4,     /* seq-aware: nblk == 4, T < 4 -> 3     */
   DA_RULE_EFF_LOOP = 5,     /* efficiency loop (DESIGN.md C-amb-2)   */
-  DA_RULE_FORCED = 6        /* DA_POLICY_FIXED                               */
+  DA_RULE_FORCED = 6,       /* DA_POLICY_FIXED                               */
+  DA_RULE_EVOLVED = 7,      /* DA_POLICY_EVOLVED, batch == 1      */
+  DA_RULE_SM_SHORT = 8,     /* DA_POLICY_SEQ_AWARE_SM: < 6 units of 64 tokens */
+  DA_RULE_SM_SPLIT = 9      /* DA_POLICY_SEQ_AWARE_SM: split from T vs SMs   */
 } da_rule;
 
 /* Element types of outputs. */

@@ -26,6 +26,12 @@ Steps follow the paper's order and notation:
 
 All comparisons are exact integer cross-multiplications (C-amb-3): there is
 no floating point anywhere in this module.
+
+Two policies beyond the paper's pair: the evolved
+Python fragment of Fig. 1 as a planner mode, and the SM-count-aware
+generalisation (C-ext-1) whose constants are calibrated on B200 - "parity
+unpinned" by the paper for the latter's constants (its structural properties
+are pinned in tests/test_oracle_policy.py).
 """
 
 from __future__ import annotations
@@ -37,8 +43,9 @@ EFF_MAX_SPLITS = 128     # efficiency-loop candidate cap (C-amb-2)
 MAX_FORCED_SPLITS = 256  # S:L98 max_splits default
 SPLIT_UNIT = 64          # partition unit in tokens (C-pol item 6)
 
-GUARDED, SEQ_AWARE, FIXED = 0, 1, 2
-POLICY_NAMES = {"guarded": GUARDED, "seq_aware": SEQ_AWARE, "fixed": FIXED}
+GUARDED, SEQ_AWARE, FIXED, EVOLVED, SEQ_AWARE_SM = 0, 1, 2, 3, 4
+POLICY_NAMES = {"guarded": GUARDED, "seq_aware": SEQ_AWARE, "fixed": FIXED, "evolved": EVOLVED,
+                "seq_aware_sm": SEQ_AWARE_SM}
 
 # Which step of the cascade decided s (mirrors SPEC's SplitDecision.source).
 RULE_SATURATED = 0
@@ -48,6 +55,18 @@ RULE_GUARD2 = 3
 RULE_LOW_TILE = 4
 RULE_EFF_LOOP = 5
 RULE_FORCED = 6
+RULE_EVOLVED = 7      # Fig. 1 fragment
+RULE_SM_SHORT = 8     # SM-count-aware generalisation: too few 64-token units to split
+RULE_SM_SPLIT = 9     # SM-count-aware generalisation: split count from units, tiles and SMs
+
+# SM-count-aware generalisation of the sequence-aware rule (DESIGN.md §3,
+# C-ext-1).  The paper leaves "extending the benefit to lower L_K values and learning more
+# configuration-specific split counts" to future work and calls its
+# own constant stack-specific ("s=3 on the current stack").  These constants are
+# calibrated from the B200 U-curves (profiles/r01_ugrid.csv, r01_ugrid2.csv) and frozen:
+SM_UNIT = 64          # tokens per split unit of the B200 kernel
+SM_MIN_UNITS = 6      # fewer units (L_K <= 320): splitting gains < 3 % or loses on B200
+SM_MAX_SPLITS = 4     # the measured plateau starts at s = 4 for L_K = 512, T <= 16
 
 
 def ceil_div(a: int, b: int) -> int:
@@ -134,6 +153,39 @@ def seq_aware_splits(geo: dict):
     return efficiency_loop(T, U, nblk), RULE_EFF_LOOP
 
 
+def seq_aware_sm_splits(geo: dict, l_k: int):
+    """C-ext-1, in this order:
+      saturated (5T >= 4U)            -> 1                      (unchanged FA3 guard)
+      nblk >= 5                       -> efficiency loop        (unchanged)
+      n_u = ceil(L_K / 64) < 6        -> 1                      (short: splitting does not pay)
+      else s = min(4, floor(n_u / 2), floor((U - 1) / T)); s < 2 -> 1
+    The split count depends on the tile count T = Batch x H_KV versus the usable SMs U (the
+    floor((U - 1) / T) cap keeps T s CTAs inside one wave), not on a static L_K guard."""
+    T, U, nblk = geo["T"], geo["U"], geo["nblk"]
+    if saturated(T, U):
+        return 1, RULE_SATURATED
+    if nblk >= 5:
+        return efficiency_loop(T, U, nblk), RULE_EFF_LOOP
+    n_u = ceil_div(l_k, SM_UNIT)
+    if n_u < SM_MIN_UNITS:
+        return 1, RULE_SM_SHORT
+    s = min(SM_MAX_SPLITS, n_u // 2, (U - 1) // T)
+    if s < 2:
+        return 1, RULE_SM_SHORT
+    return s, RULE_SM_SPLIT
+
+
+def evolved_policy_splits(geo: dict, batch: int, l_k: int):
+    """Fig. 1 as a policy: batch == 1 -> s = 12, or 16 when L_K < 256 (literal,
+    no clamp: s > nblk gives empty splits, as in the paper's s = 1..64 sweep).  The
+    fragment does not show the batch != 1 branch; it falls back to the guarded default
+    (SPEC's reading)."""
+    ev = evolved_splits(batch, l_k)
+    if ev is None:
+        return guarded_splits(geo)
+    return ev[0], RULE_EVOLVED
+
+
 def num_splits(batch: int, h_q: int, h_kv: int, l_k: int, num_sms: int, sm_margin: int,
                policy, forced_splits: int = 0):
     """Decision (s, rule) for one shape under ``policy`` (name or code)."""
@@ -148,6 +200,10 @@ def num_splits(batch: int, h_q: int, h_kv: int, l_k: int, num_sms: int, sm_margi
         if not (1 <= forced_splits <= MAX_FORCED_SPLITS):
             raise ValueError("forced_splits must be in [1, 256] (S:L98)")
         return forced_splits, RULE_FORCED
+    if policy == EVOLVED:
+        return evolved_policy_splits(geo, batch, l_k)
+    if policy == SEQ_AWARE_SM:
+        return seq_aware_sm_splits(geo, l_k)
     raise ValueError("unknown policy")
 
 

@@ -17,6 +17,9 @@ constexpr int kPolicyBlockM = 64;      // num_m_blocks = ceil(G / 64)
 constexpr int kLowTileSplits = 3;      // Fig. 3 "return 3" (C-amb-5)
 constexpr int kEffMaxSplits = 128;     // efficiency-loop candidate cap (C-amb-2)
 constexpr int kMaxForcedSplits = 256;
+constexpr int kEvolvedSplits = 12, kEvolvedShortSplits = 16, kEvolvedShortLk = 256;  // Fig. 1
+// SM-count-aware generalisation (DESIGN.md C-ext-1): B200-calibrated, frozen constants
+constexpr int kSmUnit = 64, kSmMinUnits = 6, kSmMaxSplits = 4;
 
 // ---- kernel geometry (B200 side) -----------------------------
 constexpr int kHeadDim = 128;          // v1 supports d = 128 only

@@ -1,7 +1,8 @@
 // Split planner: da_plan_make / da_plan_set_combine (host-only, integer-only).
 //
 // Implements the decision the paper is about: how many sequence splits a
-// decode-attention launch uses.  Two policies:
+// decode-attention launch uses.  The paper's two policies (plus FIXED, the
+// evolved Fig. 1 fragment and the SM-count-aware generalisation C-ext-1):
 //   * guarded   - FA3's default (§2.2 "returns s=1 if the sequence
 //                 length L_K <= 512"; §4.2 "strictly enforced s=1 when
 //                 num_n_blocks <= 4"), behind the saturation guard and ahead
@@ -44,10 +45,30 @@ int efficiency_loop(int64_t T, int64_t U, int64_t nblk) {
   return 1;
 }
 
-void decide(int64_t T, int64_t U, int64_t nblk, int policy, int forced, int* s, int* rule) {
+void decide(int64_t batch, int64_t l_k, int64_t T, int64_t U, int64_t nblk, int policy, int forced,
+            int* s, int* rule) {
   if (policy == DA_POLICY_FIXED) { *s = forced; *rule = DA_RULE_FORCED; return; }
+  if (policy == DA_POLICY_EVOLVED) {
+    if (batch == 1) {                                                    // Fig. 1
+      *s = l_k < kEvolvedShortLk ? kEvolvedShortSplits : kEvolvedSplits;
+      *rule = DA_RULE_EVOLVED;
+      return;
+    }
+    policy = DA_POLICY_GUARDED;      // the fragment shows no batch != 1 branch: FA3 default
+  }
   if (saturated(T, U)) { *s = 1; *rule = DA_RULE_SATURATED; return; }
-  if (policy == DA_POLICY_GUARDED) {
+  if (policy == DA_POLICY_SEQ_AWARE_SM) {                                 // C-ext-1
+    if (nblk <= 4) {
+      const int64_t n_u = ceil_div(l_k, kSmUnit);
+      int64_t v = n_u / 2;
+      if (v > kSmMaxSplits) v = kSmMaxSplits;
+      if ((U - 1) / T < v) v = (U - 1) / T;
+      if (n_u < kSmMinUnits || v < 2) { *s = 1; *rule = DA_RULE_SM_SHORT; return; }
+      *s = static_cast<int>(v);
+      *rule = DA_RULE_SM_SPLIT;
+      return;
+    }
+  } else if (policy == DA_POLICY_GUARDED) {
     if (nblk <= 4) { *s = 1; *rule = DA_RULE_GUARD_NBLK4; return; }
   } else {  // DA_POLICY_SEQ_AWARE, Fig. 3 in order
     if (nblk <= 3) { *s = 1; *rule = DA_RULE_GUARD1; return; }
@@ -117,8 +138,7 @@ extern "C" da_status da_plan_make(int32_t batch, int32_t h_q, int32_t h_kv, int3
   if (h_q % h_kv != 0) return DA_ERR_INVALID_ARG;
   if (sm_margin < 0 || sm_margin >= num_sms) return DA_ERR_INVALID_ARG;
   if (pack_gqa != 0 && pack_gqa != 1) return DA_ERR_INVALID_ARG;
-  if (policy != DA_POLICY_GUARDED && policy != DA_POLICY_SEQ_AWARE && policy != DA_POLICY_FIXED)
-    return DA_ERR_INVALID_ARG;
+  if (policy < DA_POLICY_GUARDED || policy > DA_POLICY_SEQ_AWARE_SM) return DA_ERR_INVALID_ARG;
   if (policy == DA_POLICY_FIXED && (forced_splits < 1 || forced_splits > kMaxForcedSplits))
     return DA_ERR_INVALID_ARG;
   if (head_dim != kHeadDim) return DA_ERR_UNSUPPORTED;
@@ -138,7 +158,7 @@ extern "C" da_status da_plan_make(int32_t batch, int32_t h_q, int32_t h_kv, int3
   p.total_mblocks = static_cast<int32_t>(T);
 
   int s = 1, rule = 0;
-  decide(T, p.usable_sms, p.num_n_blocks, policy, forced_splits, &s, &rule);
+  decide(batch, l_k, T, p.usable_sms, p.num_n_blocks, policy, forced_splits, &s, &rule);
   p.num_splits = s;
   p.rule = rule;
   p.split_unit = kSplitUnit;

@@ -140,3 +140,50 @@ if __name__ == "__main__":
         ucurve()
     if what in ("regress", "all"):
         regress()
+
+
+def ugrid():
+    """Forced s = 1..8 over short sequences and small tile counts (calibrates the
+    SM-count-aware generalisation)."""
+    rows = []
+    for hkv in (1, 2, 4):
+        for lk in (128, 192, 256, 320, 384, 448, 512, 640, 768, 1024):
+            cfg = dict(batch=1, h_q=8 * hkv, h_kv=hkv, l_k=lk)
+            svals = [s for s in range(1, 9)]
+            plans = [dec.make_plan(1, 8 * hkv, hkv, lk, policy="fixed", forced_splits=s) for s in svals]
+            times = timed_graphs(cfg, plans, 200, 11, 17)
+            base = times[0][0]
+            best = min(range(len(svals)), key=lambda i: times[i][0])
+            for s, plan, (t, p10, p90) in zip(svals, plans, times):
+                rows.append(dict(h_kv=hkv, l_k=lk, s=s, s_effective=plan.nonempty_splits, latency_us=round(t, 3),
+                                 speedup_vs_s1=round(base / t, 4)))
+            print(f"H_KV={hkv} L_K={lk:5d}: " + " ".join(f"{t[0]:5.2f}" for t in times) +
+                  f"   best s={svals[best]} ({base / times[best][0]:.3f}x)", flush=True)
+    write("ugrid", rows, ["h_kv", "l_k", "s", "s_effective", "latency_us", "speedup_vs_s1"])
+
+
+if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "ugrid":
+    ugrid()
+
+
+def ugrid2():
+    """Forced s = 1..8 at larger tile counts T = B x H_KV (Llama-70B B=1 is T = 8)."""
+    rows = []
+    for b, hkv in ((1, 8), (2, 4), (4, 2), (8, 1), (2, 8), (1, 16), (4, 8)):
+        for lk in (256, 384, 512):
+            cfg = dict(batch=b, h_q=8 * hkv, h_kv=hkv, l_k=lk)
+            svals = list(range(1, 9))
+            plans = [dec.make_plan(b, 8 * hkv, hkv, lk, policy="fixed", forced_splits=s) for s in svals]
+            times = timed_graphs(cfg, plans, 200, 11, 19)
+            base = times[0][0]
+            best = min(range(len(svals)), key=lambda i: times[i][0])
+            for s, plan, (t, p10, p90) in zip(svals, plans, times):
+                rows.append(dict(batch=b, h_kv=hkv, l_k=lk, s=s, combine_mode=plan.combine_mode,
+                                 latency_us=round(t, 3), speedup_vs_s1=round(base / t, 4)))
+            print(f"B={b} H_KV={hkv:2d} (T={b * hkv:2d}) L_K={lk}: " + " ".join(f"{t[0]:5.2f}" for t in times) +
+                  f"   best s={svals[best]} ({base / times[best][0]:.3f}x)", flush=True)
+    write("ugrid2", rows, ["batch", "h_kv", "l_k", "s", "combine_mode", "latency_us", "speedup_vs_s1"])
+
+
+if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "ugrid2":
+    ugrid2()

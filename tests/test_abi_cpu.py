@@ -85,7 +85,7 @@ def test_plan_matches_oracle_dense_lk(L):
     for sms in (132, 148):
         for (b, hkv) in ((1, 1), (1, 2), (2, 1), (1, 8), (8, 8), (4, 32)):
             for lk in range(1, 4097):
-                for pol in ("guarded", "seq_aware"):
+                for pol in ("guarded", "seq_aware", "evolved", "seq_aware_sm"):
                     _check_plan(L, b, 8 * hkv, hkv, lk, 1, 0, sms, pol)
 
 
@@ -99,7 +99,7 @@ def test_plan_matches_oracle_grid(L):
         for margin in (0, 4, 16, sms - 1):
             for b, hkv, G in itertools.product(Bs, HKVs, (1, 8)):
                 for lk in LKs:
-                    for pol in ("guarded", "seq_aware"):
+                    for pol in ("guarded", "seq_aware", "seq_aware_sm"):
                         _check_plan(L, b, G * hkv, hkv, lk, 1, margin, sms, pol)
 
 
@@ -121,7 +121,7 @@ def test_plan_random_shapes_and_fixed(L):
         sms = rng.choice([132, 148, 7, 2, 1])
         margin = rng.randint(0, sms - 1)
         pack = rng.randint(0, 1)
-        pol = rng.choice(["guarded", "seq_aware", "fixed"])
+        pol = rng.choice(["guarded", "seq_aware", "fixed", "evolved", "seq_aware_sm"])
         forced = rng.randint(1, 256) if pol == "fixed" else 0
         _check_plan(L, b, G * hkv, hkv, lk, pack, margin, sms, pol, forced)
 
@@ -149,7 +149,7 @@ def test_plan_invalid_shapes(L, args):
 
 def test_plan_invalid_knobs(L):
     bad = [dict(sm_margin=148), dict(sm_margin=-1), dict(num_sms=0), dict(pack_gqa=2),
-           dict(policy=7), dict(policy=L.DA_POLICY_FIXED, forced_splits=0),
+           dict(policy=7), dict(policy=-1), dict(policy=L.DA_POLICY_FIXED, forced_splits=0),
            dict(policy=L.DA_POLICY_FIXED, forced_splits=257)]
     for kw in bad:
         args = dict(batch=1, h_q=8, h_kv=1, l_k=512, head_dim=128, pack_gqa=1, sm_margin=0,

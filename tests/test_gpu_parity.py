@@ -61,13 +61,13 @@ def run_and_check(batch, h_q, h_kv, l_k, *, policy="seq_aware", forced=0, pack_g
 
 
 # ---- BASELINE.json configurations -----------------------------------------
-@pytest.mark.parametrize("policy", ["guarded", "seq_aware"])
+@pytest.mark.parametrize("policy", ["guarded", "seq_aware", "seq_aware_sm", "evolved"])
 @pytest.mark.parametrize("name", ["mqa_tiny", "llama70b", "llama70b_tp8"])
 def test_baseline_configs(name, policy):
     cfg = synth.CONFIGS[name]
     plan, _, _ = run_and_check(**cfg, policy=policy)
     if name == "llama70b_tp8":
-        assert plan.num_splits == (3 if policy == "seq_aware" else 1)
+        assert plan.num_splits == {"guarded": 1, "seq_aware": 3, "seq_aware_sm": 4, "evolved": 12}[policy]
 
 
 @pytest.mark.parametrize("cfg", synth.low_head_sweep(),

@@ -217,3 +217,48 @@ def test_evolved_fragment():
     assert P.evolved_splits(1, 448) == (12, True, 0)
     assert P.evolved_splits(1, 128) == (16, True, 0)
     assert P.evolved_splits(2, 512) is None
+
+
+# ---- policies beyond the paper's pair ---------------------------
+def test_evolved_policy_literal_fig1():
+    # batch == 1 -> 12, L_K < 256 -> 16; no clamp (s > nblk allowed).
+    assert P.num_splits(1, 64, 8, 512, B200_SMS, 0, "evolved") == (12, P.RULE_EVOLVED)
+    assert P.num_splits(1, 8, 1, 128, B200_SMS, 0, "evolved") == (16, P.RULE_EVOLVED)
+    assert P.num_splits(1, 8, 1, 255, B200_SMS, 0, "evolved")[0] == 16
+    assert P.num_splits(1, 8, 1, 256, B200_SMS, 0, "evolved")[0] == 12
+    # batch != 1: the fragment is silent -> guarded default
+    for lk in (128, 512, 4096):
+        assert P.num_splits(2, 8, 1, lk, B200_SMS, 0, "evolved") == P.num_splits(2, 8, 1, lk, B200_SMS, 0, "guarded")
+
+
+def test_seq_aware_sm_structure():
+    rng = random.Random(5)
+    for _ in range(20000):
+        b = rng.randint(1, 64)
+        hkv = rng.choice([1, 2, 4, 8, 16, 32])
+        lk = rng.randint(1, 20000)
+        sms = rng.choice([132, 148, 16, 3])
+        geo = P.geometry(b, 8 * hkv, hkv, lk, sms, 0)
+        s, rule = P.num_splits(b, 8 * hkv, hkv, lk, sms, 0, "seq_aware_sm")
+        g, grule = P.num_splits(b, 8 * hkv, hkv, lk, sms, 0, "guarded")
+        assert 1 <= s <= geo["nblk"]                      # never more splits than 128-token blocks
+        if geo["nblk"] >= 5 or P.saturated(geo["T"], geo["U"]):
+            assert (s, rule) == (g, grule)                # efficiency region / saturation unchanged
+        else:
+            assert s == 1 or geo["T"] * s < geo["U"]      # T s CTAs stay inside one wave
+            if lk <= 320:
+                assert s == 1                              # too few 64-token units to split
+    # the calibrated points: L_K = 512 at T <= 16 on B200 -> 4; L_K = 384 -> 3; L_K = 256 -> 1
+    assert P.num_splits(1, 8, 1, 512, B200_SMS, 0, "seq_aware_sm") == (4, P.RULE_SM_SPLIT)
+    assert P.num_splits(1, 64, 8, 512, B200_SMS, 0, "seq_aware_sm") == (4, P.RULE_SM_SPLIT)
+    assert P.num_splits(2, 128, 16, 512, B200_SMS, 0, "seq_aware_sm") == (4, P.RULE_SM_SPLIT)
+    assert P.num_splits(1, 8, 1, 384, B200_SMS, 0, "seq_aware_sm")[0] == 3
+    assert P.num_splits(1, 8, 1, 256, B200_SMS, 0, "seq_aware_sm") == (1, P.RULE_SM_SHORT)
+    # the SM count enters: T = 64 tiles on 148 SMs -> floor(147 / 64) = 2 splits; on 132 -> 2;
+    # T = 80 -> 1 (cap); T = 120 -> saturated
+    assert P.num_splits(8, 64, 8, 512, B200_SMS, 0, "seq_aware_sm")[0] == 2
+    assert P.num_splits(10, 64, 8, 512, B200_SMS, 0, "seq_aware_sm")[0] == 1
+    assert P.num_splits(15, 64, 8, 512, B200_SMS, 0, "seq_aware_sm")[1] == P.RULE_SATURATED
+    # where the paper's rule splits (nblk = 4, T < 4) the generalisation splits too
+    for hkv in (1, 2):
+        assert P.num_splits(1, 8 * hkv, hkv, 512, B200_SMS, 0, "seq_aware_sm")[0] >= 3
