@@ -9,7 +9,9 @@ scheduler metadata the paper measures with) and one da_forward call,
 i.e. the split-KV kernel plus the LSE combine when s > 1.
 
 Headline (N = 1): BASELINE.json configs[1], Llama-3.1-70B decode B=1 H_Q=64
-H_KV=8 d=128 L_K=512 bf16, sequence-aware policy.  ``value`` = aggregate
+H_KV=8 d=128 L_K=512 bf16, under the SM-count-aware sequence-aware policy
+(DESIGN.md C-ext-1; --policy seq_aware selects the paper's literal Fig. 3 rule,
+which leaves this T = 8 shape at s = 1 via Guard 2).  ``value`` = aggregate
 algorithmic HBM GB/s over all ranks (K+V+q+out+lse bytes / step time), with
 inputs resident in HBM; ``us_per_step`` the same measurement as time.  Timing:
 W eager warm-up steps, then K steps captured in ONE CUDA graph ("CUDA
@@ -340,7 +342,7 @@ def run_reference(args, rank, world):
 
 
 # ----------------------------------------------------------------------------------------------
-def e2e_measure(dec, L, cfg, dev, stream, steps, warmup):
+def e2e_measure(dec, L, cfg, dev, stream, steps, warmup, policy="seq_aware_sm"):
     """Same metric through the public API with HOST buffers: per step H2D of q/k/v from pinned
     memory, da_plan_make, da_forward, D2H of out + lse - all inside the timed region."""
     b, hq, hkv, lk = cfg["batch"], cfg["h_q"], cfg["h_kv"], cfg["l_k"]
@@ -360,7 +362,7 @@ def e2e_measure(dec, L, cfg, dev, stream, steps, warmup):
         dq.copy_(hq_, non_blocking=True)
         dk.copy_(hk_, non_blocking=True)
         dv.copy_(hv_, non_blocking=True)
-        plan = L.da_plan_make(b, hq, hkv, lk, HEAD_DIM, 1, 0, sms, L.DA_POLICY_SEQ_AWARE, 0)
+        plan = L.da_plan_make(b, hq, hkv, lk, HEAD_DIM, 1, 0, sms, L.POLICIES[policy], 0)
         ws = ws_cache.get(plan.workspace_bytes)
         if ws is None and plan.combine_mode == L.DA_COMBINE_KERNEL:
             ws = ws_cache.setdefault(plan.workspace_bytes, dec.workspace_for(plan, dev))
@@ -395,6 +397,10 @@ def main():
     ap.add_argument("--no-extras", action="store_true", help="skip the A/B and streaming extras")
     ap.add_argument("--ab-rounds", type=int, default=21)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--policy", default="seq_aware_sm",
+                    choices=["seq_aware_sm", "seq_aware", "guarded", "evolved"],
+                    help="split policy of the headline step (default: the SM-count-aware sequence-aware "
+                         "policy, DESIGN.md C-ext-1; the paper's literal Fig. 3 rule is 'seq_aware')")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3          # contract: W >= 3 warm-up steps
@@ -428,7 +434,8 @@ def main():
     long_sharded = args.workload == "long_context" and world > 1
     if long_sharded:
         from paper_2604_00028_b200.dist import SeqShardedDecode
-        sd = SeqShardedDecode(cfg["batch"], cfg["h_q"], cfg["h_kv"], cfg["l_k"], HEAD_DIM, device=dev)
+        sd = SeqShardedDecode(cfg["batch"], cfg["h_q"], cfg["h_kv"], cfg["l_k"], HEAD_DIM, device=dev,
+                              policy=args.policy)
         local_cfg = dict(cfg, l_k=sd.l_local)
         inp = synth.make_inputs(cfg["batch"], cfg["h_q"], cfg["h_kv"], sd.l_local, device=dev, seed=1000 + rank)
         out = torch.empty((cfg["batch"], cfg["h_q"], HEAD_DIM), dtype=torch.bfloat16, device=dev)
@@ -450,7 +457,7 @@ def main():
     else:
         local_cfg = cfg
         w = Workload(cfg, dev, 1000 + rank, l2)
-        plan = dec.make_plan(cfg["batch"], cfg["h_q"], cfg["h_kv"], cfg["l_k"], policy="seq_aware")
+        plan = dec.make_plan(cfg["batch"], cfg["h_q"], cfg["h_kv"], cfg["l_k"], policy=args.policy)
         with torch.cuda.stream(stream):
             ws = dec.workspace_for(plan, dev)
             for i in range(args.warmup):
@@ -498,7 +505,7 @@ def main():
     value = step_bytes_total * args.steps / (ms_max * 1e-3) / 1e9
 
     # ---- end to end through the public API with host buffers ----
-    e2e_ms, h2d, d2h = e2e_measure(dec, L, local_cfg, dev, stream, args.steps, args.warmup)
+    e2e_ms, h2d, d2h = e2e_measure(dec, L, local_cfg, dev, stream, args.steps, args.warmup, args.policy)
     e2e_t = torch.tensor([e2e_ms], device=dev)
     if world > 1:
         dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
@@ -539,7 +546,7 @@ def main():
         "vs_baseline": None,
         "dtype": "bf16",
         "data": "synthetic (seeded N(0,1) bf16 q/K/V, uniform cache_seqlens = L_K)",
-        "config": {"workload": args.workload, **cfg, "head_dim": HEAD_DIM, "policy": "seq_aware",
+        "config": {"workload": args.workload, **cfg, "head_dim": HEAD_DIM, "policy": args.policy,
                    "num_splits": plan.num_splits, "combine_mode": plan.combine_mode,
                    "global_batch": cfg["batch"] * (world if not long_sharded else 1),
                    "parallelism": parallelism, "l2": l2_note, "graph": "K steps in one CUDA graph"},
