@@ -577,22 +577,27 @@ __global__ void __launch_bounds__(threads_for(NW), 1)
       const int rl = t >> 5, d4 = t & 31;
       const int g = static_cast<int>(rank) + rl * s;
       if (g >= rows_valid) break;   // rows of a rank ascend with t: the rest are invalid too
-      float M = kNegInf, Lsum = 0.f;
+      // two passes without a loop-carried max: (1) M = max over the s pushed lse's,
+      // (2) independent weighted sums, so the slot loads of consecutive ranks overlap
+      const float* const row0 = slots + rl * kSlotRowFloats;
+      const int rstride = rows_per_owner * kSlotRowFloats;
+      float M = kNegInf;
+#pragma unroll 4
+      for (int r = 0; r < s; ++r) M = fmaxf(M, row0[r * rstride + kHeadDim]);
+      float Lsum = 0.f;
       float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll 1
-      for (int r = 0; r < s; ++r) {
-        const float* sl = slots + (r * rows_per_owner + rl) * kSlotRowFloats;
-        const float2 ml = *reinterpret_cast<const float2*>(sl + kHeadDim);
-        const float4 ow = *reinterpret_cast<const float4*>(sl + 4 * d4);
-        const float Mn = fmaxf(M, ml.x);
-        const float fa = M == kNegInf ? 0.f : ex2(M - Mn);
-        const float fb = ml.x == kNegInf ? 0.f : ex2(ml.x - Mn);
-        Lsum = Lsum * fa + ml.y * fb;
-        acc.x = acc.x * fa + ow.x * fb;
-        acc.y = acc.y * fa + ow.y * fb;
-        acc.z = acc.z * fa + ow.z * fb;
-        acc.w = acc.w * fa + ow.w * fb;
-        M = Mn;
+      if (M != kNegInf) {
+#pragma unroll 4
+        for (int r = 0; r < s; ++r) {
+          const float2 ml = *reinterpret_cast<const float2*>(row0 + r * rstride + kHeadDim);
+          const float4 ow = *reinterpret_cast<const float4*>(row0 + r * rstride + 4 * d4);
+          const float f = ex2(ml.x - M);                 // empty rank: exp2(-inf) = 0
+          Lsum = fmaf(f, ml.y, Lsum);
+          acc.x = fmaf(f, ow.x, acc.x);
+          acc.y = fmaf(f, ow.y, acc.y);
+          acc.z = fmaf(f, ow.z, acc.z);
+          acc.w = fmaf(f, ow.w, acc.w);
+        }
       }
       const float inv = Lsum > 0.f ? __frcp_rn(Lsum) : 0.f;
       const size_t row = static_cast<size_t>(b) * p.h_q + hq0 + g;
