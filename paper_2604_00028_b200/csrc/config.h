@@ -62,6 +62,12 @@ DA_HD constexpr int stages_for(int combine_mode) {
 DA_HD constexpr int warps_for(int combine_mode) {
   return combine_mode == 0 ? kWarpsNone : (combine_mode == 1 ? kWarpsCluster : kWarpsKernel);
 }
+// Helper warps idle through the main loop and join the epilogue merges so that every merge
+// is a single pass (cluster kernels: 3 consumers + producer + 4 helpers = 256 threads).
+#ifndef DECATTN_CLUSTER_HELPERS
+#define DECATTN_CLUSTER_HELPERS 4
+#endif
+DA_HD constexpr int helpers_for(int combine_mode) { return combine_mode == 1 ? DECATTN_CLUSTER_HELPERS : 0; }
 constexpr int kMaxClusterSplits = 16;  // cluster combine up to 16 CTAs (non-portable size, B200)
 // One pushed row: O[128] fp32, (m, l), padding to 16 bytes.  A rank owns ceil(R/s) rows and
 // receives them from all s ranks (itself included): at most max_{s<=16} s ceil(16/s) = 30 rows (s = 15).
@@ -71,7 +77,7 @@ constexpr int kMaxSlotRows = 30;
 // measured on B200 (148 SMs) with cudaOccupancyMaxActiveClusters (scripts/microbench_cluster16.cu).
 // Cluster placement is GPC-bound, hence not simply 148 / s.  Index: s (0, 1 unused).
 constexpr int kMaxActiveClustersB200[17] = {0, 148, 74, 45, 33, 26, 22, 15, 15, 15, 11, 7, 7, 7, 7, 7, 7};
-DA_HD constexpr int threads_for(int warps) { return (warps + 1) * 32; }   // + 1 TMA producer warp
+DA_HD constexpr int threads_for(int warps, int helpers = 0) { return (warps + 1 + helpers) * 32; }   // + TMA producer
 DA_HD constexpr int smem_for(int stages, bool cluster) {
   return stages * kStageBytes + (cluster ? kMaxSlotRows * kSlotRowFloats * 4 : 0) + 1024;
 }

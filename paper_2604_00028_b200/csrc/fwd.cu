@@ -275,11 +275,11 @@ __device__ __forceinline__ void split_range(int n, int split, int s, int& t0, in
 // (NS a multiple of NW: warp w owns stages w, w + NW, ... and consumes them in order).
 // ---------------------------------------------------------------------------
 template <int kPath, int kNB, int kCombine, int NS, int NW>
-__global__ void __launch_bounds__(threads_for(NW), 1)
+__global__ void __launch_bounds__(threads_for(NW, helpers_for(kCombine)), 1)
     split_kv_fwd_kernel(const __grid_constant__ CUtensorMap tmap_k,
                         const __grid_constant__ CUtensorMap tmap_v, const FwdParams p) {
   static_assert(NS % NW == 0, "each consumer warp must own whole ring stages");
-  constexpr int kT = threads_for(NW);                      // all threads (consumers + producer)
+  constexpr int kT = threads_for(NW, helpers_for(kCombine));   // consumers + producer + helpers
   constexpr int R = kPath == DA_PATH_MMA ? 8 * kNB : 1;    // query rows of this CTA
   constexpr int kIters = (R * 32 + kT - 1) / kT;           // merge passes: element = (row, float4)
   constexpr bool kCluster = kCombine == DA_COMBINE_CLUSTER;
@@ -379,6 +379,9 @@ __global__ void __launch_bounds__(threads_for(NW), 1)
     }
     __syncwarp();
     asm volatile("bar.sync 0;" ::: "memory");   // (A) pairs with the consumers' barrier
+  } else if (warp > NW) {
+    // ================= helpers: idle until the epilogue merges =================
+    asm volatile("bar.sync 0;" ::: "memory");   // (A)
   } else {
     // ================= consumers: warp w handles tiles w, w + NW, ... (stages it owns) =======
     const uint16_t* qrow = p.q + static_cast<int64_t>(b) * p.q_sb;
@@ -640,7 +643,7 @@ cudaError_t launch_impl(const da_plan& plan, const CUtensorMap& tk, const CUtens
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(plan.grid_x, plan.grid_y, plan.grid_z);
-  cfg.blockDim = dim3(threads_for(NW), 1, 1);
+  cfg.blockDim = dim3(threads_for(NW, helpers_for(kCombine)), 1, 1);
   cfg.dynamicSmemBytes = kSmem;
   cfg.stream = stream;
   cudaLaunchAttribute attrs[2];

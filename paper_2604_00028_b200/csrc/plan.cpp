@@ -92,7 +92,7 @@ void derive_launch(da_plan* p) {
   p->grid_y = mma ? p->h_kv * static_cast<int32_t>(ceil_div(G, p->rows_per_cta)) : p->h_q;
   p->grid_z = p->batch;
   const bool cluster = p->combine_mode == DA_COMBINE_CLUSTER;
-  p->block_threads = threads_for(warps_for(p->combine_mode));
+  p->block_threads = threads_for(warps_for(p->combine_mode), helpers_for(p->combine_mode));
   p->cluster_x = cluster ? p->num_splits : 1;
   p->smem_bytes = smem_for(stages_for(p->combine_mode), cluster);
   p->workspace_bytes = p->num_splits > 1
