@@ -412,9 +412,18 @@ def main():
         return run_reference(args, rank, world)
 
     import torch.distributed as dist
+    # DECATTN_BENCH_BACKEND=gloo + DECATTN_BENCH_ONE_GPU=1 run the multi-rank plumbing of the
+    # batch-sharded mode as several processes on one GPU (tests only: no kernel of one rank
+    # waits on another rank's, and the ranks share the GPU, so the number is not a bench value)
+    backend = os.environ.get("DECATTN_BENCH_BACKEND", "nccl")
+    gpu_index = 0 if os.environ.get("DECATTN_BENCH_ONE_GPU") == "1" else local_rank
     if world > 1:
-        torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        torch.cuda.set_device(gpu_index)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", gpu_index))
+        else:
+            dist.init_process_group(backend)
+    local_rank = gpu_index
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
     import paper_2604_00028_b200 as dec
@@ -428,7 +437,17 @@ def main():
 
     def barrier():
         if world > 1:
-            dist.barrier(device_ids=[local_rank])
+            if backend == "nccl":
+                dist.barrier(device_ids=[local_rank])
+            else:
+                dist.barrier()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], device=dev if backend == "nccl" else "cpu")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
 
     cfg = WORKLOADS[args.workload]
     long_sharded = args.workload == "long_context" and world > 1
@@ -497,19 +516,14 @@ def main():
             with torch.cuda.stream(stream):
                 g.replay()
             torch.cuda.synchronize()
-    ms_t = torch.tensor([ms], device=dev)
-    if world > 1:
-        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
-    ms_max = float(ms_t.item())
+    ms_max = max_over_ranks(ms)
     us_per_step = ms_max * 1e3 / args.steps
     value = step_bytes_total * args.steps / (ms_max * 1e-3) / 1e9
 
     # ---- end to end through the public API with host buffers ----
     e2e_ms, h2d, d2h = e2e_measure(dec, L, local_cfg, dev, stream, args.steps, args.warmup, args.policy)
-    e2e_t = torch.tensor([e2e_ms], device=dev)
-    if world > 1:
-        dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
-    e2e_value = (alg_bytes(**local_cfg) * (world if not long_sharded else 1)) * args.steps / (float(e2e_t.item()) * 1e-3) / 1e9
+    e2e_ms_max = max_over_ranks(e2e_ms)
+    e2e_value = (alg_bytes(**local_cfg) * (world if not long_sharded else 1)) * args.steps / (e2e_ms_max * 1e-3) / 1e9
 
     extras = {}
     if rank == 0 and world == 1 and not args.no_extras:
@@ -556,7 +570,7 @@ def main():
                      "note": "latency-bound config (2.1 MB per step); see roofline_streaming for the HBM-bound configs"},
         "cpu_baseline": cpu_baseline(local_cfg, args.cpu_seconds) if world == 1 else None,
         "e2e": {"value": round(e2e_value, 3), "unit": "GB/s", "h2d_bytes_per_step": h2d,
-                "d2h_bytes_per_step": d2h, "ms_per_step": round(float(e2e_t.item()) / args.steps, 6)},
+                "d2h_bytes_per_step": d2h, "ms_per_step": round(e2e_ms_max / args.steps, 6)},
         "gpu_launches": args.steps * kernels_per_step,
         "clocks": clk.summary(),
         "device": {"name": props.name, "sms": num_sms, "l2_bytes": l2},

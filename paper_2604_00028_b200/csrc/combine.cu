@@ -39,6 +39,7 @@ __global__ void __launch_bounds__(kCombineThreads)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int row = blockIdx.x;
   const int s = p.num_splits;
+  DA_DASSERT(row < p.rows && s >= 1);
   const float* lse_in = p.lse_in + row;
 
   // (1) M = max_i lse_i: every warp reduces all s values (one L2 round trip)

@@ -241,6 +241,7 @@ __device__ __forceinline__ void scalar_tile(uint32_t sK, uint32_t sV, int valid,
 }
 
 __device__ __forceinline__ void store_out(const FwdParams& p, size_t row, int d4, float4 v) {
+  DA_DASSERT(row < static_cast<size_t>(p.batch) * p.h_q && d4 >= 0 && d4 < kHeadDim / 4);
   if (p.out_f32) {
     reinterpret_cast<float4*>(p.out)[row * (kHeadDim / 4) + d4] = v;
   } else {
@@ -311,6 +312,8 @@ __global__ void __launch_bounds__(threads_for(NW, helpers_for(kCombine)), 1)
     kvh = hq0 / p.G;
     rows_valid = 1;
   }
+  DA_DASSERT(rows_valid >= 1 && hq0 + rows_valid <= p.h_q && kvh * p.G <= hq0);
+  DA_DASSERT(!kCluster || (p.num_splits >= 2 && p.num_splits <= kMaxClusterSplits));
   // CLUSTER: rank r owns rows g = r, r + s, r + 2s, ... and emits them
   const int s_cl = kCluster ? p.num_splits : 1;
   const uint32_t rank = kCluster ? cluster_ctarank() : 0u;
@@ -368,6 +371,7 @@ __global__ void __launch_bounds__(threads_for(NW, helpers_for(kCombine)), 1)
       for (int i = 0; i < n_tiles; ++i) {
         const int st = i % NS;
         if (i >= NS) mbar_wait(smem_u32(&empty_bar[st]), ((i / NS) - 1) & 1);
+        DA_DASSERT(t0 + i * kTileN < max(t_end, 1) + kTileN);
         const uint32_t fb = smem_u32(&full_bar[st]);
         mbar_arrive_expect_tx(fb, kStageBytes);
         const uint32_t dst = sbase + st * kStageBytes;
@@ -392,6 +396,7 @@ __global__ void __launch_bounds__(threads_for(NW, helpers_for(kCombine)), 1)
         const int g = nb * 8 + (lane >> 2);
         const bool ok = g < rows_valid;
         const uint16_t* qg = qrow + static_cast<int64_t>(hq0 + (ok ? g : 0)) * p.q_sh + 2 * (lane & 3);
+        DA_DASSERT(hq0 + (ok ? g : 0) < p.h_q && b < p.batch);
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
           qf[kk][nb][0] = ok ? __ldg(reinterpret_cast<const uint32_t*>(qg + kk * 16)) : 0u;
@@ -546,6 +551,7 @@ __global__ void __launch_bounds__(threads_for(NW, helpers_for(kCombine)), 1)
         if (d4 == 0 && p.lse != nullptr) p.lse[row] = lse_v;
       } else {  // DA_COMBINE_KERNEL: normalised partial o_i, lse_i (C-part)
         const size_t prow = static_cast<size_t>(split) * p.batch * p.h_q + row;
+        DA_DASSERT(prow < static_cast<size_t>(p.num_splits) * p.batch * p.h_q);
         reinterpret_cast<float4*>(p.ws_o)[prow * (kHeadDim / 4) + d4] = v;
         if (d4 == 0) p.ws_lse[prow] = lse_v;
       }
@@ -565,6 +571,7 @@ __global__ void __launch_bounds__(threads_for(NW, helpers_for(kCombine)), 1)
       const int owner = g % s;
       // slot [source rank][row g / s of the owner]
       float* const dst = slots + (static_cast<int>(rank) * rows_per_owner + g / s) * kSlotRowFloats;
+      DA_DASSERT(static_cast<int>(rank) * rows_per_owner + g / s < kMaxSlotRows && g < R);
       const uint32_t rbar = mapa(smem_u32(&push_bar), owner);
       st_async_v4(mapa(smem_u32(dst + 4 * d4), owner), eO[it], rbar);
       if (d4 == 0) st_async_v2(mapa(smem_u32(dst + kHeadDim), owner), eM[it], eL[it], rbar);
@@ -583,6 +590,7 @@ __global__ void __launch_bounds__(threads_for(NW, helpers_for(kCombine)), 1)
       // two passes without a loop-carried max: (1) M = max over the s pushed lse's,
       // (2) independent weighted sums, so the slot loads of consecutive ranks overlap
       const float* const row0 = slots + rl * kSlotRowFloats;
+      DA_DASSERT((s - 1) * rows_per_owner + rl < kMaxSlotRows);
       const int rstride = rows_per_owner * kSlotRowFloats;
       float M = kNegInf;
 #pragma unroll 4

@@ -5,6 +5,16 @@
 #include <cstdint>
 #include <cuda_bf16.h>
 
+// Device-side bounds checks for -DDECATTN_DEBUG builds (compute-sanitizer is unavailable on
+// the GPU pool): the test suite runs against such a build to prove every computed index of
+// the tested shapes in range.  Compiled out of the product library.
+#ifdef DECATTN_DEBUG
+#include <cassert>
+#define DA_DASSERT(cond) assert(cond)
+#else
+#define DA_DASSERT(cond) do { } while (0)
+#endif
+
 namespace decattn {
 namespace ptx {
 

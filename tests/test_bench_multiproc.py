@@ -1,0 +1,27 @@
+"""bench.py's multi-rank plumbing (weak scaling by batch: barrier, max-over-ranks timing,
+rank-0 JSON) with world_size 2 as two processes sharing one GPU over gloo.  Kernels of one
+rank never wait on the other's (no data-path collective in this mode)."""
+
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.mark.gpu
+def test_bench_two_ranks_batch_sharded():
+    env = dict(os.environ, DECATTN_BENCH_BACKEND="gloo", DECATTN_BENCH_ONE_GPU="1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr", "127.0.0.1", "--master-port", "29517", os.path.join(ROOT, "bench.py"),
+           "--gpus", "2", "--steps", "20", "--warmup", "3"]
+    r = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout              # rank 0 alone prints one JSON line
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["scaling"] == "weak" and d["config"]["global_batch"] == 2
+    assert d["value"] > 0 and d["e2e"]["value"] > 0 and d["gpu_launches"] == 20
