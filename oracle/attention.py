@@ -166,6 +166,32 @@ def partition(n_b: int, num_splits: int, split_unit: int):
     return out
 
 
+def gather_pages(pages, block_table, seqlens, page_size):
+    """Paged KV cache -> dense [B, L, H_KV, d] cache (vLLM-style block tables).
+
+    pages [num_pages, page_size, H_KV, d]; block_table[b][j] = page holding tokens
+    [j page_size, (j+1) page_size) of sequence b.  Dense L = max_b ceil(n_b / page_size)
+    page_size; token t of sequence b is pages[block_table[b][t // page_size], t % page_size].
+    Tokens past n_b are filled with zeros (never read by decode_attention)."""
+    pages = np.asarray(pages)
+    seqlens = np.asarray(seqlens, dtype=np.int64)
+    B = len(seqlens)
+    n_pages = int(max((-(-int(n) // page_size) for n in seqlens), default=0))
+    L = max(n_pages * page_size, 1)
+    out = np.zeros((B, L) + pages.shape[2:], dtype=pages.dtype)
+    for b in range(B):
+        for t in range(int(seqlens[b])):
+            out[b, t] = pages[int(block_table[b][t // page_size]), t % page_size]
+    return out
+
+
+def decode_attention_paged(q, k_pages, v_pages, block_table, seqlens, page_size, scale=None):
+    """C-att over a paged cache: gather the pages in sequence order, then decode_attention."""
+    k = gather_pages(k_pages, block_table, seqlens, page_size)
+    v = gather_pages(v_pages, block_table, seqlens, page_size)
+    return decode_attention(q, k, v, seqlens, scale)
+
+
 def bf16_round(x):
     """Round float64 values to the nearest bfloat16 (ties to even) and return
     them as float64.  C-amb-13: the kernel rounds its fp32 result to bf16 once

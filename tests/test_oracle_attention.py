@@ -236,3 +236,46 @@ def test_bf16_round():
     assert r[1] == 1.0                      # tie -> even
     assert r[2] == 1.0 + 2 ** -7            # above the tie -> up
     assert r[3] == -2.5 and r[4] == 0.0
+
+
+def test_paged_identity_table_equals_dense():
+    # pages laid out in sequence order (page j of sequence b = b * P + j) reproduce the dense cache
+    rng = np.random.default_rng(20)
+    B, HQ, HKV, d, ps, P = 2, 4, 2, 8, 4, 3
+    q = rng.standard_normal((B, HQ, d))
+    k = rng.standard_normal((B, P * ps, HKV, d))
+    v = rng.standard_normal((B, P * ps, HKV, d))
+    pages_k = k.reshape(B * P, ps, HKV, d)
+    pages_v = v.reshape(B * P, ps, HKV, d)
+    table = [[b * P + j for j in range(P)] for b in range(B)]
+    seq = [P * ps, 7]
+    o1, l1 = A.decode_attention(q, k, v, seq)
+    o2, l2 = A.decode_attention_paged(q, pages_k, pages_v, table, seq, ps)
+    np.testing.assert_array_equal(o1, o2)
+    np.testing.assert_array_equal(l1, l2)
+
+
+def test_paged_permuted_pool_is_invariant():
+    # shuffling the physical pages (and the table with them) changes nothing; a wrong table does
+    rng = np.random.default_rng(21)
+    B, HQ, HKV, d, ps, P = 2, 4, 1, 8, 4, 3
+    q = rng.standard_normal((B, HQ, d))
+    pages_k = rng.standard_normal((B * P + 2, ps, HKV, d))
+    pages_v = rng.standard_normal((B * P + 2, ps, HKV, d))
+    table = [[b * P + j for j in range(P)] for b in range(B)]
+    perm = rng.permutation(len(pages_k))
+    inv = np.argsort(perm)
+    table2 = [[int(inv[x]) for x in row] for row in table]
+    seq = [12, 9]
+    o1, l1 = A.decode_attention_paged(q, pages_k, pages_v, table, seq, ps)
+    o2, l2 = A.decode_attention_paged(q, pages_k[perm], pages_v[perm], table2, seq, ps)
+    np.testing.assert_allclose(o1, o2, atol=1e-13)
+    np.testing.assert_allclose(l1, l2, atol=1e-13)
+    o3, _ = A.decode_attention_paged(q, pages_k, pages_v, [row[::-1] for row in table], seq, ps)
+    assert not np.allclose(o1, o3)
+
+
+def test_gather_pages_token_mapping():
+    pages = np.arange(5 * 2).reshape(5, 2, 1, 1).astype(float)   # page p, slot i -> value 2p + i
+    g = A.gather_pages(pages, [[3, 0, 4]], [5], 2)
+    assert g[0, :5, 0, 0].tolist() == [6, 7, 0, 1, 8]
