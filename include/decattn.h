@@ -213,6 +213,31 @@ DA_API da_status da_forward(const da_plan* plan, const void* q, const void* k_ca
                      void* workspace, int64_t workspace_bytes, void* cuda_stream);
 
 /*
+ * da_forward_paged - da_forward over a paged KV cache (vLLM-style block tables; SURVEY
+ * §8(f4)).  Same plan, q, cache_seqlens, softmax_scale, out, lse, workspace and stream
+ * semantics as da_forward, with the cache given as page pools:
+ *   k_pages, v_pages  bf16 [num_pages, page_size, H_KV, d]; strides (as in da_forward)
+ *                     are {q_b, q_h, k_page, k_t, k_h, v_page, v_t, v_h} in elements,
+ *                     NULL = contiguous pools
+ *   page_size         tokens per page: a multiple of 64 (one kernel tile never spans pages),
+ *                     else DA_ERR_UNSUPPORTED
+ *   block_table       device int32 [B, block_table_stride]: entry j of row b is the page
+ *                     holding tokens [j page_size, (j+1) page_size) of sequence b.  Entries
+ *                     past a sequence's length are never read; an index outside
+ *                     [0, num_pages) reads zeros (no out-of-bounds access)
+ *   max_pages_per_seq pages per sequence: max_pages_per_seq * page_size >= plan->l_k and
+ *                     bounds every cache_seqlens value (clamped on the device)
+ * The result is decode attention over the gathered sequence (oracle.gather_pages).
+ */
+DA_API da_status da_forward_paged(const da_plan* plan, const void* q, const void* k_pages,
+                                  const void* v_pages, int32_t num_pages, int32_t page_size,
+                                  const int32_t* block_table, int64_t block_table_stride,
+                                  int32_t max_pages_per_seq, const int32_t* cache_seqlens,
+                                  const int64_t* strides, float softmax_scale, int32_t out_dtype,
+                                  void* out, float* lse, void* workspace, int64_t workspace_bytes,
+                                  void* cuda_stream);
+
+/*
  * da_combine - LSE-combine of s partials (C-comb):
  *   M = max_i lse_i, lse = M + ln sum_i exp(lse_i - M),
  *   out = sum_i exp(lse_i - lse) o_i; all splits empty -> out = 0, lse = -inf.

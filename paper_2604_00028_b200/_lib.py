@@ -71,6 +71,9 @@ def _load() -> ctypes.CDLL:
     lib.da_forward.argtypes = [ctypes.POINTER(da_plan), vp, vp, vp, i32, vp, vp, f32, i32, vp, vp,
                                vp, i64, vp]
     lib.da_forward.restype = i32
+    lib.da_forward_paged.argtypes = [ctypes.POINTER(da_plan), vp, vp, vp, i32, i32, vp, i64, i32, vp, vp, f32,
+                                     i32, vp, vp, vp, i64, vp]
+    lib.da_forward_paged.restype = i32
     lib.da_combine.argtypes = [i32, i32, i32, i32, vp, i64, vp, i64, i32, vp, vp, vp]
     lib.da_combine.restype = i32
     lib.da_status_string.argtypes = [i32]
@@ -84,7 +87,7 @@ def _load() -> ctypes.CDLL:
 
 LIB = _load()
 
-EXPORTED = ("da_plan_make", "da_plan_set_combine", "da_forward", "da_combine",
+EXPORTED = ("da_plan_make", "da_plan_set_combine", "da_forward", "da_forward_paged", "da_combine",
             "da_status_string", "da_abi_version")
 
 
@@ -144,6 +147,22 @@ def da_forward(plan: da_plan, q, k_cache, v_cache, l_cap, cache_seqlens, strides
                         _ptr(lse), _ptr(workspace), int(workspace_bytes), _stream_handle(stream))
     if st != DA_OK:
         raise DecAttnError(st, "da_forward")
+
+
+def da_forward_paged(plan: da_plan, q, k_pages, v_pages, num_pages, page_size, block_table,
+                     block_table_stride, max_pages_per_seq, cache_seqlens, strides, softmax_scale,
+                     out_dtype, out, lse, workspace, workspace_bytes, stream=None) -> None:
+    """Marshal to ``da_forward_paged`` (paged KV cache with a block table)."""
+    sarr = None
+    if strides is not None:
+        sarr = (ctypes.c_int64 * 8)(*[int(x) for x in strides])
+    st = LIB.da_forward_paged(ctypes.byref(plan), _ptr(q), _ptr(k_pages), _ptr(v_pages), int(num_pages),
+                              int(page_size), _ptr(block_table), int(block_table_stride),
+                              int(max_pages_per_seq), _ptr(cache_seqlens), sarr, float(softmax_scale),
+                              int(out_dtype), _ptr(out), _ptr(lse), _ptr(workspace), int(workspace_bytes),
+                              _stream_handle(stream))
+    if st != DA_OK:
+        raise DecAttnError(st, "da_forward_paged")
 
 
 def da_combine(num_splits, batch, h_q, head_dim, o_partial, o_split_stride, lse_partial,

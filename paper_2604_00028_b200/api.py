@@ -87,6 +87,29 @@ def forward(plan: L.da_plan, q, k_cache, v_cache, cache_seqlens=None, *, out=Non
     return out, lse
 
 
+def forward_paged(plan: L.da_plan, q, k_pages, v_pages, block_table, cache_seqlens=None, *, out=None,
+                  lse=None, workspace=None, softmax_scale=0.0, out_dtype=torch.bfloat16, stream=None):
+    """Decode attention over a paged cache via da_forward_paged.  k/v_pages [num_pages, page_size,
+    H_KV, d] bf16; block_table int32 [B, max_pages_per_seq]; page_size a multiple of 64."""
+    _check_cuda(q, k_pages, v_pages, block_table, cache_seqlens)
+    if block_table.dtype != torch.int32 or block_table.dim() != 2 or block_table.stride(1) != 1:
+        raise ValueError("block_table must be a row-major int32 [B, max_pages] tensor")
+    B, HQ, D = q.shape
+    if out is None:
+        out = torch.empty((B, HQ, D), dtype=out_dtype, device=q.device)
+    if lse is None:
+        lse = torch.empty((B, HQ), dtype=torch.float32, device=q.device)
+    if workspace is None:
+        workspace = workspace_for(plan, q.device)
+    ws_bytes = 0 if workspace is None else workspace.numel() * workspace.element_size()
+    dt = L.DA_F32 if out.dtype == torch.float32 else L.DA_BF16
+    L.da_forward_paged(plan, q, k_pages, v_pages, k_pages.shape[0], k_pages.shape[1], block_table,
+                       block_table.stride(0), block_table.shape[1], cache_seqlens,
+                       _kv_strides(q, k_pages, v_pages), softmax_scale, dt, out, lse, workspace, ws_bytes,
+                       stream)
+    return out, lse
+
+
 def combine(o_partial, lse_partial, *, out=None, lse=None, out_dtype=torch.bfloat16, stream=None):
     """da_combine over o_partial [s, B, H_Q, d] fp32 and lse_partial [s, B, H_Q] fp32
     (split strides taken from the tensors)."""

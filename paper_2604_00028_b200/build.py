@@ -1,6 +1,9 @@
 """Build libdecattn.so in-tree with nvcc for sm_100a.
 
-    python -m paper_2604_00028_b200.build [--force] [--ptxas-verbose]
+    python paper_2604_00028_b200/build.py [--force] [--ptxas-verbose]
+
+(run by path, or load it by path as __graft_entry__.build() does: importing it as a submodule
+of the package would import the package first, which loads the library it is meant to build)
 
 Sources: csrc/{plan.cpp, capi.cpp, fwd.cu, combine.cu}.  Output:
 paper_2604_00028_b200/lib/libdecattn.so (git-ignored; travels to the GPU box

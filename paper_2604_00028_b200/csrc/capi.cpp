@@ -40,6 +40,8 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 // 64 x 64 x 2 x 1 x 1 brings a whole 64-token tile of K (or V) in a single TMA op, laid out
 // in shared memory as [half][token][64 dims] with 128-byte rows and the 128-byte swizzle
 // the consumers' ldmatrix addressing expects.  Tokens past l_cap read as zero.
+// For a paged pool [num_pages, page_size, H_KV, d] the same map is built with (num_pages,
+// page_size, page stride) in place of (B, l_cap, batch stride).
 bool make_kv_tmap(CUtensorMap* map, const void* base, int32_t batch, int32_t l_cap, int32_t h_kv,
                   int64_t sb, int64_t st, int64_t sh) {
   auto fn = encode_fn();
@@ -77,13 +79,20 @@ da_status check_plan(const da_plan* plan) {
   return DA_OK;
 }
 
-}  // namespace
+struct PagedArgs {
+  const int32_t* block_table = nullptr;
+  int64_t bt_stride = 0;
+  int32_t page_size = 0;
+  int32_t num_pages = 0;
+};
 
-extern "C" da_status da_forward(const da_plan* plan, const void* q, const void* k_cache,
-                                const void* v_cache, int32_t l_cap, const int32_t* cache_seqlens,
-                                const int64_t* strides, float softmax_scale, int32_t out_dtype,
-                                void* out, float* lse, void* workspace, int64_t workspace_bytes,
-                                void* cuda_stream) {
+// Shared body of da_forward / da_forward_paged.  For a paged cache, k_cache / v_cache are the
+// page pools [num_pages, page_size, H_KV, d], strides[2..7] are (page, token, head) strides,
+// and l_cap = max_pages_per_seq * page_size bounds the per-sequence length.
+da_status forward_impl(const da_plan* plan, const void* q, const void* k_cache, const void* v_cache,
+                       int32_t l_cap, const int32_t* cache_seqlens, const int64_t* strides,
+                       float softmax_scale, int32_t out_dtype, void* out, float* lse, void* workspace,
+                       int64_t workspace_bytes, void* cuda_stream, const PagedArgs& pg) {
   if (plan == nullptr || q == nullptr || k_cache == nullptr || v_cache == nullptr || out == nullptr)
     return DA_ERR_INVALID_ARG;
   da_status st = check_plan(plan);
@@ -91,15 +100,17 @@ extern "C" da_status da_forward(const da_plan* plan, const void* q, const void* 
   if (l_cap < plan->l_k) return DA_ERR_INVALID_ARG;
   if (out_dtype != DA_BF16 && out_dtype != DA_F32) return DA_ERR_INVALID_ARG;
   if (!(softmax_scale <= 0.f) && !std::isfinite(softmax_scale)) return DA_ERR_INVALID_ARG;
+  const bool paged = pg.block_table != nullptr;
 
   const int64_t B = plan->batch, HQ = plan->h_q, HKV = plan->h_kv, D = kHeadDim;
+  const int64_t rows_per_major = paged ? pg.page_size : l_cap;   // tokens per batch entry / page
   int64_t sd[8];
   if (strides != nullptr) {
     std::memcpy(sd, strides, sizeof(sd));
   } else {
-    sd[0] = HQ * D; sd[1] = D;                       // q (b, h)
-    sd[2] = int64_t(l_cap) * HKV * D; sd[3] = HKV * D; sd[4] = D;  // k (b, t, h)
-    sd[5] = sd[2]; sd[6] = sd[3]; sd[7] = sd[4];      // v
+    sd[0] = HQ * D; sd[1] = D;                                   // q (b, h)
+    sd[2] = rows_per_major * HKV * D; sd[3] = HKV * D; sd[4] = D; // k (b | page, t, h)
+    sd[5] = sd[2]; sd[6] = sd[3]; sd[7] = sd[4];                  // v
   }
   for (int i = 0; i < 8; ++i) {
     if (sd[i] < 0) return DA_ERR_INVALID_ARG;
@@ -110,6 +121,7 @@ extern "C" da_status da_forward(const da_plan* plan, const void* q, const void* 
     return DA_ERR_ALIGNMENT;
   if (cache_seqlens != nullptr && (reinterpret_cast<uintptr_t>(cache_seqlens) & 3u) != 0)
     return DA_ERR_ALIGNMENT;
+  if (paged && (reinterpret_cast<uintptr_t>(pg.block_table) & 3u) != 0) return DA_ERR_ALIGNMENT;
 
   float* ws_o = nullptr;
   float* ws_lse = nullptr;
@@ -121,8 +133,10 @@ extern "C" da_status da_forward(const da_plan* plan, const void* q, const void* 
   }
 
   CUtensorMap tk, tv;
-  if (!make_kv_tmap(&tk, k_cache, plan->batch, l_cap, plan->h_kv, sd[2], sd[3], sd[4]) ||
-      !make_kv_tmap(&tv, v_cache, plan->batch, l_cap, plan->h_kv, sd[5], sd[6], sd[7]))
+  const int32_t major = paged ? pg.num_pages : plan->batch;
+  const int32_t rows = paged ? pg.page_size : l_cap;
+  if (!make_kv_tmap(&tk, k_cache, major, rows, plan->h_kv, sd[2], sd[3], sd[4]) ||
+      !make_kv_tmap(&tv, v_cache, major, rows, plan->h_kv, sd[5], sd[6], sd[7]))
     return DA_ERR_CUDA;
 
   FwdParams p{};
@@ -144,6 +158,9 @@ extern "C" da_status da_forward(const da_plan* plan, const void* q, const void* 
   p.lse = lse;
   p.ws_o = ws_o;
   p.ws_lse = ws_lse;
+  p.block_table = pg.block_table;
+  p.bt_stride = pg.bt_stride;
+  p.page_size = pg.page_size;
 
   cudaStream_t stream = static_cast<cudaStream_t>(cuda_stream);
   if (launch_split_kv_fwd(*plan, tk, tv, p, stream) != cudaSuccess) return DA_ERR_CUDA;
@@ -161,6 +178,38 @@ extern "C" da_status da_forward(const da_plan* plan, const void* q, const void* 
     if (launch_lse_combine(c, /*pdl=*/true, stream) != cudaSuccess) return DA_ERR_CUDA;
   }
   return DA_OK;
+}
+
+}  // namespace
+
+extern "C" da_status da_forward(const da_plan* plan, const void* q, const void* k_cache,
+                                const void* v_cache, int32_t l_cap, const int32_t* cache_seqlens,
+                                const int64_t* strides, float softmax_scale, int32_t out_dtype,
+                                void* out, float* lse, void* workspace, int64_t workspace_bytes,
+                                void* cuda_stream) {
+  return forward_impl(plan, q, k_cache, v_cache, l_cap, cache_seqlens, strides, softmax_scale,
+                      out_dtype, out, lse, workspace, workspace_bytes, cuda_stream, PagedArgs{});
+}
+
+extern "C" da_status da_forward_paged(const da_plan* plan, const void* q, const void* k_pages,
+                                      const void* v_pages, int32_t num_pages, int32_t page_size,
+                                      const int32_t* block_table, int64_t block_table_stride,
+                                      int32_t max_pages_per_seq, const int32_t* cache_seqlens,
+                                      const int64_t* strides, float softmax_scale, int32_t out_dtype,
+                                      void* out, float* lse, void* workspace, int64_t workspace_bytes,
+                                      void* cuda_stream) {
+  if (block_table == nullptr || num_pages < 1 || max_pages_per_seq < 1) return DA_ERR_INVALID_ARG;
+  if (page_size < kTileN || page_size % kTileN != 0) return DA_ERR_UNSUPPORTED;
+  if (block_table_stride < max_pages_per_seq) return DA_ERR_INVALID_ARG;
+  const int64_t cap = int64_t(max_pages_per_seq) * page_size;
+  if (cap > INT32_MAX) return DA_ERR_INVALID_ARG;
+  PagedArgs pg;
+  pg.block_table = block_table;
+  pg.bt_stride = block_table_stride;
+  pg.page_size = page_size;
+  pg.num_pages = num_pages;
+  return forward_impl(plan, q, k_pages, v_pages, static_cast<int32_t>(cap), cache_seqlens, strides,
+                      softmax_scale, out_dtype, out, lse, workspace, workspace_bytes, cuda_stream, pg);
 }
 
 extern "C" da_status da_combine(int32_t num_splits, int32_t batch, int32_t h_q, int32_t head_dim,

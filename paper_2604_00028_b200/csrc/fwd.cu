@@ -368,17 +368,43 @@ __global__ void __launch_bounds__(threads_for(NW, helpers_for(kCombine)), 1)
   if (warp == NW) {
     // ================= TMA producer =================
     if (lane == 0) {
-      for (int i = 0; i < n_tiles; ++i) {
-        const int st = i % NS;
-        if (i >= NS) mbar_wait(smem_u32(&empty_bar[st]), ((i / NS) - 1) & 1);
-        DA_DASSERT(t0 + i * kTileN < max(t_end, 1) + kTileN);
-        const uint32_t fb = smem_u32(&full_bar[st]);
-        mbar_arrive_expect_tx(fb, kStageBytes);
-        const uint32_t dst = sbase + st * kStageBytes;
-        const int t = t0 + i * kTileN;
-        tma_load_5d(dst, &tmap_k, fb, 0, t, 0, kvh, b);                  // K: both 64-dim halves
-        tma_load_5d(dst + 2 * kHalfBytes, &tmap_v, fb, 0, t, 0, kvh, b);  // V
-        if (i < 8) TRACE(2 + i);
+      if (p.block_table == nullptr) {
+        for (int i = 0; i < n_tiles; ++i) {
+          const int st = i % NS;
+          if (i >= NS) mbar_wait(smem_u32(&empty_bar[st]), ((i / NS) - 1) & 1);
+          DA_DASSERT(t0 + i * kTileN < max(t_end, 1) + kTileN);
+          const uint32_t fb = smem_u32(&full_bar[st]);
+          mbar_arrive_expect_tx(fb, kStageBytes);
+          const uint32_t dst = sbase + st * kStageBytes;
+          const int t = t0 + i * kTileN;
+          tma_load_5d(dst, &tmap_k, fb, 0, t, 0, kvh, b);                  // K: both 64-dim halves
+          tma_load_5d(dst + 2 * kHalfBytes, &tmap_v, fb, 0, t, 0, kvh, b);  // V
+          if (i < 8) TRACE(2 + i);
+        }
+      } else {
+        // paged cache: tile i of the split lives in page block_table[b][t / page_size] at token
+        // t % page_size (a tile never spans pages).  The page indices of the next NS tiles are
+        // loaded ahead so the lookups do not throttle the ring.  Out-of-range indices fall
+        // outside the tensor map and read as zeros.
+        const int32_t* bt = p.block_table + static_cast<int64_t>(b) * p.bt_stride;
+        int pg[NS];
+#pragma unroll
+        for (int j = 0; j < NS; ++j) pg[j] = j < n_tiles ? __ldg(bt + (t0 + j * kTileN) / p.page_size) : 0;
+        for (int i = 0; i < n_tiles; ++i) {
+          const int st = i % NS;
+          if (i >= NS) mbar_wait(smem_u32(&empty_bar[st]), ((i / NS) - 1) & 1);
+          const uint32_t fb = smem_u32(&full_bar[st]);
+          mbar_arrive_expect_tx(fb, kStageBytes);
+          const uint32_t dst = sbase + st * kStageBytes;
+          const int t = t0 + i * kTileN;
+          const int page = pg[0];
+          const int slot = t - (t / p.page_size) * p.page_size;
+#pragma unroll
+          for (int j = 0; j + 1 < NS; ++j) pg[j] = pg[j + 1];
+          pg[NS - 1] = i + NS < n_tiles ? __ldg(bt + (t + NS * kTileN) / p.page_size) : 0;
+          tma_load_5d(dst, &tmap_k, fb, 0, slot, 0, kvh, page);
+          tma_load_5d(dst + 2 * kHalfBytes, &tmap_v, fb, 0, slot, 0, kvh, page);
+        }
       }
     }
     __syncwarp();

@@ -28,6 +28,10 @@ struct FwdParams {
   float* lse;               // [B, H_Q] or nullptr
   float* ws_o;              // KERNEL combine: [s, B, H_Q, d]
   float* ws_lse;            // KERNEL combine: [s, B, H_Q]
+  // paged KV cache (da_forward_paged); block_table == nullptr for a dense cache
+  const int32_t* block_table;   // [B, bt_stride] page indices
+  int64_t bt_stride;
+  int32_t page_size;            // tokens per page, a multiple of kTileN
 };
 
 struct CombineParams {

@@ -16,7 +16,10 @@ SHAPES = [(1, 8, 1, 512, "guarded"), (1, 8, 1, 512, "seq_aware"), (1, 16, 2, 512
           (1, 8, 1, 1024, "seq_aware"), (1, 8, 1, 2048, "seq_aware")]
 
 if sys.argv[1] == "build":
-    from paper_2604_00028_b200 import build as B
+    import importlib.util
+    _spec = importlib.util.spec_from_file_location("_decattn_build", os.path.join(ROOT, "paper_2604_00028_b200", "build.py"))
+    B = importlib.util.module_from_spec(_spec)
+    _spec.loader.exec_module(B)
     for name, (ns, nw, cs, cw, ks, kw) in VARIANTS.items():
         B.build(defines=[f"DECATTN_NONE_STAGES={ns}", f"DECATTN_NONE_WARPS={nw}",
                          f"DECATTN_CLUSTER_STAGES={cs}", f"DECATTN_CLUSTER_WARPS={cw}",

@@ -231,3 +231,25 @@ def test_combine_validation(L):
     assert st(head_dim=64) == L.DA_ERR_UNSUPPORTED
     assert st(o_split_stride=1000) == L.DA_ERR_INVALID_ARG        # < B*H_Q*d
     assert st(o_partial=A + 4) == L.DA_ERR_ALIGNMENT
+
+
+def test_forward_paged_validation(L):
+    p = L.da_plan_make(2, 16, 2, 700, 128, 1, 0, 148, "seq_aware", 0)
+
+    def st(**kw):
+        args = dict(q=A, k_pages=2 * A, v_pages=3 * A, num_pages=40, page_size=64, block_table=7 * A,
+                    block_table_stride=11, max_pages_per_seq=11, cache_seqlens=None, strides=None,
+                    softmax_scale=0.0, out_dtype=L.DA_BF16, out=4 * A, lse=5 * A, workspace=None,
+                    workspace_bytes=0, stream=0)
+        args.update(kw)
+        with pytest.raises(L.DecAttnError) as e:
+            L.da_forward_paged(p, **args)
+        return e.value.status
+    assert st(block_table=None) == L.DA_ERR_INVALID_ARG
+    assert st(num_pages=0) == L.DA_ERR_INVALID_ARG
+    assert st(page_size=32) == L.DA_ERR_UNSUPPORTED           # not a multiple of the 64-token tile
+    assert st(page_size=96) == L.DA_ERR_UNSUPPORTED
+    assert st(block_table_stride=10) == L.DA_ERR_INVALID_ARG  # row stride < pages per sequence
+    assert st(max_pages_per_seq=10) == L.DA_ERR_INVALID_ARG   # 10 * 64 < l_k = 700
+    assert st(block_table=7 * A + 2) == L.DA_ERR_ALIGNMENT
+    assert st(q=A + 8) == L.DA_ERR_ALIGNMENT

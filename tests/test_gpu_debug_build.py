@@ -16,7 +16,10 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 @pytest.mark.gpu
 def test_parity_subset_under_debug_asserts():
     sys.path.insert(0, ROOT)
-    from paper_2604_00028_b200 import build as B
+    import importlib.util
+    _spec = importlib.util.spec_from_file_location("_decattn_build", os.path.join(ROOT, "paper_2604_00028_b200", "build.py"))
+    B = importlib.util.module_from_spec(_spec)
+    _spec.loader.exec_module(B)
     lib = B.build(defines=["DECATTN_DEBUG=1"], lib=os.path.join(B.PKG, "lib", "variants", "libdecattn_debug.so"),
                   build_dir=os.path.join(B.PKG, "build", "debug"))
     env = dict(os.environ, DECATTN_LIB=lib)

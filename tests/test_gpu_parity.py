@@ -220,3 +220,59 @@ def test_full_size_long_context_ragged_sampled():
     # ragged lengths at the long-context size: batch of 3 with 0 / 1 / random tokens
     cfg = dict(synth.CONFIGS["long_context"], batch=3)
     _check_sampled(cfg, "seq_aware", [(0, 1), (1, 2), (2, 4)], 1005, variant="ragged")
+
+
+# ---- paged KV cache (da_forward_paged) --------------------------------------
+def run_paged(batch, h_q, h_kv, l_k, page_size, *, policy="seq_aware", forced=0, pack=True, seed=90,
+              variant="ragged", combine_mode=None):
+    dec = _dec()
+    inp = synth.make_inputs(batch, h_q, h_kv, l_k, seed=seed, variant=variant, device="cuda")
+    q, k, v, seq = inp["q"], inp["k"], inp["v"], inp["seqlens"]
+    P = -(-l_k // page_size)                                  # pages per sequence
+    extra = 3
+    n_pages = batch * P + extra
+    g = torch.Generator(device="cpu").manual_seed(seed)
+    perm = torch.randperm(n_pages, generator=g)
+    kp = torch.full((n_pages, page_size, h_kv, 128), float("nan"), dtype=torch.bfloat16, device="cuda")
+    vp = torch.full_like(kp, float("nan"))                    # unused slots / pages hold garbage
+    table = torch.full((batch, P + 1), -1, dtype=torch.int32)  # entries past a sequence: invalid
+    for b in range(batch):
+        n = int(seq[b])
+        for j in range(-(-n // page_size)):
+            pg = int(perm[b * P + j])
+            table[b, j] = pg
+            lo, hi = j * page_size, min((j + 1) * page_size, n)
+            kp[pg, : hi - lo] = k[b, lo:hi]
+            vp[pg, : hi - lo] = v[b, lo:hi]
+    table = table.to("cuda")
+    plan = dec.make_plan(batch, h_q, h_kv, l_k, pack_gqa=pack, policy=policy, forced_splits=forced,
+                         combine_mode=combine_mode)
+    out, lse = dec.forward_paged(plan, q, kp, vp, table, seq)
+    torch.cuda.synchronize()
+    ref_o, ref_l = OA.decode_attention(*(synth.to_f64(t) for t in (q, k, v, seq)))
+    assert_out_close(synth.to_f64(out), ref_o)
+    assert_lse_close(synth.to_f64(lse), ref_l)
+    return plan
+
+
+@pytest.mark.parametrize("page_size", [64, 128, 256])
+@pytest.mark.parametrize("policy,forced,combine", [("seq_aware", 0, None), ("fixed", 3, 1), ("fixed", 12, 2)])
+def test_paged_matches_dense(page_size, policy, forced, combine):
+    run_paged(4, 16, 2, 700, page_size, policy=policy, forced=forced, combine_mode=combine, seed=91)
+
+
+@pytest.mark.parametrize("pack", [True, False])
+def test_paged_paths_and_uniform_lengths(pack):
+    run_paged(2, 8, 1, 512, 64, pack=pack, variant="normal", seed=92)
+    run_paged(3, 64, 8, 1024, 128, pack=pack, variant="ragged", seed=93)
+
+
+def test_paged_rejects_unsupported_page_size():
+    dec = _dec()
+    plan = dec.make_plan(1, 8, 1, 128)
+    q = torch.zeros(1, 8, 128, dtype=torch.bfloat16, device="cuda")
+    kp = torch.zeros(4, 32, 1, 128, dtype=torch.bfloat16, device="cuda")
+    table = torch.zeros(1, 4, dtype=torch.int32, device="cuda")
+    with pytest.raises(dec.DecAttnError) as e:
+        dec.forward_paged(plan, q, kp, kp, table)
+    assert e.value.status == dec._lib.DA_ERR_UNSUPPORTED
