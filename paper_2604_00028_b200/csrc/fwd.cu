@@ -341,6 +341,15 @@ __global__ void __launch_bounds__(threads_for(NW, helpers_for(kCombine)), 1)
   if (warp == NW && lane == 0) {
     prefetch_tmap(&tmap_k);
     prefetch_tmap(&tmap_v);
+    // the lengths and the block-table row are read right after griddepcontrol.wait: pull their
+    // lines into L2 now (a prefetch never returns data, so it cannot observe a stale value)
+    if (p.seqlens != nullptr) prefetch_l2(p.seqlens + b);
+    if (p.block_table != nullptr) {
+      const int32_t* bt = p.block_table + static_cast<int64_t>(b) * p.bt_stride;
+      const int first = static_cast<int>(static_cast<int64_t>(split) * min(max(p.l_default, 0), p.l_cap) /
+                                         max(p.num_splits, 1) / p.page_size);
+      prefetch_l2(bt + first);
+    }
   }
   // ---- this split's token range (C-pol item 6), in units of kTileN tokens.  With uniform
   // lengths (cache_seqlens == NULL) it is known before griddepcontrol.wait, so the producer

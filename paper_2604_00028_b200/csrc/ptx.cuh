@@ -82,6 +82,11 @@ __device__ __forceinline__ void tma_prefetch_4d(const void* tmap, int c0, int c1
                "r"(c0), "r"(c1), "r"(c2), "r"(c3)
                : "memory");
 }
+// L2 prefetch of one global line (no data returned; always safe before griddepcontrol.wait:
+// L2 is the point of coherence).
+__device__ __forceinline__ void prefetch_l2(const void* ptr) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(ptr) : "memory");
+}
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }

@@ -187,3 +187,53 @@ def ugrid2():
 
 if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "ugrid2":
     ugrid2()
+
+
+def paged():
+    """Paged (shuffled pool) vs dense KV cache, same shapes and policy (cold L2)."""
+    import statistics as st
+    dev = torch.device("cuda", 0)
+    timer = bench.Timer(dev)
+    stream = torch.cuda.Stream()
+    rows = []
+    for (b, hq, hkv, lk, steps) in ((1, 8, 1, 512, 200), (1, 64, 8, 512, 200), (1, 64, 8, 131072, 20),
+                                    (128, 64, 8, 8192, 5)):
+        inp = bench.synth.make_inputs(b, hq, hkv, lk, device=dev, seed=5)
+        q, k, v = inp["q"], inp["k"], inp["v"]
+        plan = dec.make_plan(b, hq, hkv, lk, policy="seq_aware_sm")
+        res = {}
+        for ps in (0, 64, 128, 256):
+            if ps == 0:
+                fn = lambda: dec.forward(plan, q, k, v, None)
+            else:
+                P = -(-lk // ps)
+                perm = torch.randperm(b * P, device=dev)
+                kp = torch.empty((b * P, ps, hkv, 128), dtype=torch.bfloat16, device=dev)
+                vp = torch.empty_like(kp)
+                kp[perm] = k.reshape(b * P, ps, hkv, 128)
+                vp[perm] = v.reshape(b * P, ps, hkv, 128)
+                table = perm.view(b, P).to(torch.int32).contiguous()
+                fn = (lambda kp=kp, vp=vp, table=table: dec.forward_paged(plan, q, kp, vp, table, None))
+            with torch.cuda.stream(stream):
+                for _ in range(3):
+                    fn()
+            torch.cuda.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=stream):
+                for _ in range(steps):
+                    fn()
+            ts = [timer.time_replay(g, stream) * 1e3 / steps for _ in range(9)]
+            res[ps] = st.median(ts)
+            del g
+        line = " ".join(f"{'dense' if ps == 0 else f'page{ps}'}={t:8.2f}" for ps, t in res.items())
+        print(f"B={b} H_Q={hq} H_KV={hkv} L_K={lk}: {line} us (s={plan.num_splits})", flush=True)
+        for ps, t in res.items():
+            rows.append(dict(batch=b, h_q=hq, h_kv=hkv, l_k=lk, page_size=ps, num_splits=plan.num_splits,
+                             latency_us=round(t, 3), gbs=round(bench.alg_bytes(b, hq, hkv, lk) / (t * 1e-6) / 1e9, 1)))
+        del inp, q, k, v
+        torch.cuda.empty_cache()
+    write("paged", rows, ["batch", "h_q", "h_kv", "l_k", "page_size", "num_splits", "latency_us", "gbs"])
+
+
+if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "paged":
+    paged()
