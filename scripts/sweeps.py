@@ -237,3 +237,28 @@ def paged():
 
 if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "paged":
     paged()
+
+
+def ugrid3():
+    """Efficiency-loop region (nblk >= 5) at small tile counts: forced s vs the loop's pick."""
+    rows = []
+    for b, hkv in ((1, 1), (1, 2), (1, 4), (1, 8), (2, 8)):
+        for lk in (768, 1024, 2048, 4096):
+            cfg = dict(batch=b, h_q=8 * hkv, h_kv=hkv, l_k=lk)
+            svals = [1, 2, 4, 6, 8, 10, 12, 14, 16, 24, 32]
+            plans = [dec.make_plan(b, 8 * hkv, hkv, lk, policy="fixed", forced_splits=s) for s in svals]
+            ge = dec.make_plan(b, 8 * hkv, hkv, lk, policy="guarded")
+            times = timed_graphs(cfg, plans, 100, 9, 23)
+            best = min(range(len(svals)), key=lambda i: times[i][0])
+            eff_i = svals.index(ge.num_splits) if ge.num_splits in svals else None
+            for s, plan, (t, p10, p90) in zip(svals, plans, times):
+                rows.append(dict(batch=b, h_kv=hkv, l_k=lk, s=s, combine_mode=plan.combine_mode,
+                                 latency_us=round(t, 3), effloop_s=ge.num_splits))
+            print(f"B={b} H_KV={hkv} L_K={lk:5d}: " + " ".join(f"{s}:{t[0]:.2f}{'k' if p.combine_mode == 2 else ''}"
+                                                               for s, p, t in zip(svals, plans, times)) +
+                  f"  | best s={svals[best]}  effloop s={ge.num_splits}", flush=True)
+    write("ugrid3", rows, ["batch", "h_kv", "l_k", "s", "combine_mode", "latency_us", "effloop_s"])
+
+
+if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "ugrid3":
+    ugrid3()
