@@ -79,9 +79,14 @@ typedef enum da_policy {
   DA_POLICY_EVOLVED = 3,    /* Fig. 1: batch == 1 -> 12 (16 when
                                L_K < 256); batch != 1 -> guarded            */
   DA_POLICY_SEQ_AWARE_SM = 4 /* SM-count-aware generalisation (DESIGN.md
-                               C-ext-1): in the nblk <= 4
-                               region s = min(4, ceil(L_K/64)/2, (U-1)/T),
-                               s = 1 below 6 units; B200-calibrated         */
+                               C-ext-1), n_u = ceil(L_K/64),
+                               f = largest s <= 16 whose T clusters fit one
+                               wave: nblk <= 4 -> min(n_u, T <= 4 ? 8 : 4, f)
+                               (1 when n_u < 4, or n_u < 6 and T > 16);
+                               else the efficiency loop's e, raised to
+                               min(8, n_u, f) when e <= f, or moved to f when
+                               e > f >= 2 and (n_u <= 32 f or 2 T f >= U);
+                               B200-calibrated                              */
 } da_policy;
 
 /* Which step of the cascade decided num_splits (SPEC's "source"). */
@@ -94,8 +99,10 @@ typedef enum da_rule {
   DA_RULE_EFF_LOOP = 5,     /* efficiency loop (DESIGN.md C-amb-2)   */
   DA_RULE_FORCED = 6,       /* DA_POLICY_FIXED                               */
   DA_RULE_EVOLVED = 7,      /* DA_POLICY_EVOLVED, batch == 1      */
-  DA_RULE_SM_SHORT = 8,     /* DA_POLICY_SEQ_AWARE_SM: < 6 units of 64 tokens */
-  DA_RULE_SM_SPLIT = 9      /* DA_POLICY_SEQ_AWARE_SM: split from T vs SMs   */
+  DA_RULE_SM_SHORT = 8,     /* DA_POLICY_SEQ_AWARE_SM: too few 64-token units */
+  DA_RULE_SM_SPLIT = 9,     /* DA_POLICY_SEQ_AWARE_SM: nblk <= 4 split        */
+  DA_RULE_SM_FIT = 10       /* DA_POLICY_SEQ_AWARE_SM: nblk >= 5, the loop's
+                               split moved to a one-wave cluster split      */
 } da_rule;
 
 /* Element types of outputs. */

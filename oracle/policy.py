@@ -58,16 +58,30 @@ RULE_FORCED = 6
 RULE_EVOLVED = 7      # Fig. 1 fragment
 RULE_SM_SHORT = 8     # SM-count-aware generalisation: too few 64-token units to split
 RULE_SM_SPLIT = 9     # SM-count-aware generalisation: split count from units, tiles and SMs
+RULE_SM_FIT = 10      # SM-count-aware generalisation: efficiency-loop split moved to one wave
 
 # SM-count-aware generalisation of the sequence-aware rule (DESIGN.md §3,
 # C-ext-1).  The paper leaves "extending the benefit to lower L_K values and learning more
 # configuration-specific split counts" to future work and calls its
 # own constant stack-specific ("s=3 on the current stack").  These constants are
-# calibrated from the B200 U-curves (profiles/r01_ugrid.csv, r01_ugrid2.csv) and frozen:
+# calibrated from the B200 U-curves of the current kernel (profiles/r01f_ugrid.csv,
+# r01f_ugrid2.csv, r01f_ugrid3.csv; long-context boundary from scripts/probe_regime.py and
+# scripts/probe_long.py) and frozen:
 SM_UNIT = 64          # tokens per split unit of the B200 kernel
-SM_MIN_UNITS = 6      # fewer units (L_K <= 320): splitting gains < 3 % or loses on B200
-SM_MAX_SPLITS = 4     # the measured plateau starts at s = 4 for L_K = 512, T <= 16
-
+SM_MIN_UNITS = 4      # fewer units (L_K <= 192): every split loses on B200
+SM_MIN_UNITS_WIDE = 6  # with T > SM_WIDE_T tiles, fewer units (L_K <= 320) do not pay either
+SM_WIDE_T = 16
+SM_NARROW_T = 4       # T <= 4 tiles: the plateau extends to s = 8 ...
+SM_NARROW_SPLITS = 8
+SM_MAX_SPLITS = 4     # ... otherwise the measured plateau starts at s = 4 (L_K <= 512)
+SM_EFF_FLOOR = 8      # efficiency region: at least min(8, n_u, fit) splits
+SM_STREAM_UNITS = 32  # efficiency region: cap to the one-wave cluster split while each split
+                      # holds <= 32 units (2048 tokens) or the capped launch still has >= U/2 CTAs
+# Clusters of s CTAs (one per split, s = 1..16) that are co-resident in one wave on a 148-SM
+# B200 with the cluster-combine kernel configuration (cudaOccupancyMaxActiveClusters,
+# scripts/microbench_cluster16.cu); index 0 unused, index 1 = one CTA per SM.  Scaled by U / 148.
+CLUSTER_FIT_B200 = (0, 148, 74, 45, 33, 26, 22, 15, 15, 15, 11, 7, 7, 7, 7, 7, 7)
+CLUSTER_MAX_SPLITS = 16
 
 def ceil_div(a: int, b: int) -> int:
     return -(-a // b)
@@ -153,26 +167,49 @@ def seq_aware_splits(geo: dict):
     return efficiency_loop(T, U, nblk), RULE_EFF_LOOP
 
 
+def cluster_fit_splits(T: int, U: int) -> int:
+    """Largest s in 1..16 whose T clusters of s CTAs are co-resident in one wave:
+    T <= floor(CLUSTER_FIT_B200[s] * U / 148); s = 1 (one CTA per tile) always qualifies."""
+    best = 1
+    for s in range(2, CLUSTER_MAX_SPLITS + 1):
+        if T <= CLUSTER_FIT_B200[s] * U // 148:
+            best = s
+    return best
+
+
 def seq_aware_sm_splits(geo: dict, l_k: int):
-    """C-ext-1, in this order:
-      saturated (5T >= 4U)            -> 1                      (unchanged FA3 guard)
-      nblk >= 5                       -> efficiency loop        (unchanged)
-      n_u = ceil(L_K / 64) < 6        -> 1                      (short: splitting does not pay)
-      else s = min(4, floor(n_u / 2), floor((U - 1) / T)); s < 2 -> 1
-    The split count depends on the tile count T = Batch x H_KV versus the usable SMs U (the
-    floor((U - 1) / T) cap keeps T s CTAs inside one wave), not on a static L_K guard."""
+    """C-ext-1, in this order (n_u = ceil(L_K / 64) units, f = cluster_fit_splits(T, U)):
+      saturated (5T >= 4U)                      -> 1                      (unchanged FA3 guard)
+      nblk <= 4 (the paper's guard region):
+        n_u < 4, or n_u < 6 with T > 16         -> 1                      (short: splitting loses)
+        s = min(n_u, 8 if T <= 4 else 4, f);  s < 2 -> 1
+      nblk >= 5 (efficiency region), e = the unchanged efficiency loop:
+        e <= f                                  -> max(e, min(8, n_u, f))
+        e > f >= 2 and (n_u <= 32 f or 2 T f >= U) -> f
+        else                                    -> e
+    The split count depends on the tile count T = Batch x H_KV versus the usable SMs U through
+    f, the largest split whose clusters all fit one wave, not on a static L_K guard."""
     T, U, nblk = geo["T"], geo["U"], geo["nblk"]
     if saturated(T, U):
         return 1, RULE_SATURATED
-    if nblk >= 5:
-        return efficiency_loop(T, U, nblk), RULE_EFF_LOOP
     n_u = ceil_div(l_k, SM_UNIT)
-    if n_u < SM_MIN_UNITS:
-        return 1, RULE_SM_SHORT
-    s = min(SM_MAX_SPLITS, n_u // 2, (U - 1) // T)
-    if s < 2:
-        return 1, RULE_SM_SHORT
-    return s, RULE_SM_SPLIT
+    f = cluster_fit_splits(T, U)
+    if nblk <= 4:
+        if n_u < SM_MIN_UNITS or (n_u < SM_MIN_UNITS_WIDE and T > SM_WIDE_T):
+            return 1, RULE_SM_SHORT
+        cap = SM_NARROW_SPLITS if T <= SM_NARROW_T else SM_MAX_SPLITS
+        s = min(n_u, cap, f)
+        if s < 2:
+            return 1, RULE_SM_SHORT
+        return s, RULE_SM_SPLIT
+    e = efficiency_loop(T, U, nblk)
+    if e <= f:
+        s = max(e, min(SM_EFF_FLOOR, n_u, f))
+    elif f >= 2 and (n_u <= SM_STREAM_UNITS * f or 2 * T * f >= U):
+        s = f
+    else:
+        s = e
+    return s, (RULE_EFF_LOOP if s == e else RULE_SM_FIT)
 
 
 def evolved_policy_splits(geo: dict, batch: int, l_k: int):

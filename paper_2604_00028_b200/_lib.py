@@ -22,7 +22,8 @@ LIB_PATH = os.environ.get("DECATTN_LIB") or os.path.join(PKG_DIR, "lib", "libdec
 DA_OK, DA_ERR_INVALID_ARG, DA_ERR_UNSUPPORTED, DA_ERR_ALIGNMENT, DA_ERR_WORKSPACE, DA_ERR_CUDA = range(6)
 DA_POLICY_GUARDED, DA_POLICY_SEQ_AWARE, DA_POLICY_FIXED, DA_POLICY_EVOLVED, DA_POLICY_SEQ_AWARE_SM = range(5)
 (DA_RULE_SATURATED, DA_RULE_GUARD_NBLK4, DA_RULE_GUARD1, DA_RULE_GUARD2, DA_RULE_LOW_TILE,
- DA_RULE_EFF_LOOP, DA_RULE_FORCED, DA_RULE_EVOLVED, DA_RULE_SM_SHORT, DA_RULE_SM_SPLIT) = range(10)
+ DA_RULE_EFF_LOOP, DA_RULE_FORCED, DA_RULE_EVOLVED, DA_RULE_SM_SHORT, DA_RULE_SM_SPLIT,
+ DA_RULE_SM_FIT) = range(11)
 DA_BF16, DA_F32 = 0, 1
 DA_COMBINE_NONE, DA_COMBINE_CLUSTER, DA_COMBINE_KERNEL = range(3)
 DA_PATH_SCALAR, DA_PATH_MMA = 0, 1
@@ -33,7 +34,8 @@ POLICIES = {"guarded": DA_POLICY_GUARDED, "seq_aware": DA_POLICY_SEQ_AWARE, "fix
 RULE_NAMES = {DA_RULE_SATURATED: "saturated", DA_RULE_GUARD_NBLK4: "guard_nblk4",
               DA_RULE_GUARD1: "guard1", DA_RULE_GUARD2: "guard2", DA_RULE_LOW_TILE: "low_tile",
               DA_RULE_EFF_LOOP: "efficiency_loop", DA_RULE_FORCED: "forced", DA_RULE_EVOLVED: "evolved",
-              DA_RULE_SM_SHORT: "sm_short", DA_RULE_SM_SPLIT: "sm_split"}
+              DA_RULE_SM_SHORT: "sm_short", DA_RULE_SM_SPLIT: "sm_split",
+              DA_RULE_SM_FIT: "sm_fit"}
 
 
 class da_plan(ctypes.Structure):

@@ -19,7 +19,9 @@ constexpr int kEffMaxSplits = 128;     // efficiency-loop candidate cap (C-amb-2
 constexpr int kMaxForcedSplits = 256;
 constexpr int kEvolvedSplits = 12, kEvolvedShortSplits = 16, kEvolvedShortLk = 256;  // Fig. 1
 // SM-count-aware generalisation (DESIGN.md C-ext-1): B200-calibrated, frozen constants
-constexpr int kSmUnit = 64, kSmMinUnits = 6, kSmMaxSplits = 4;
+constexpr int kSmUnit = 64, kSmMinUnits = 4, kSmMinUnitsWide = 6, kSmWideT = 16;
+constexpr int kSmNarrowT = 4, kSmNarrowSplits = 8, kSmMaxSplits = 4;
+constexpr int kSmEffFloor = 8, kSmStreamUnits = 32;
 
 // ---- kernel geometry (B200 side) -----------------------------
 constexpr int kHeadDim = 128;          // v1 supports d = 128 only

@@ -45,6 +45,15 @@ int efficiency_loop(int64_t T, int64_t U, int64_t nblk) {
   return 1;
 }
 
+// Largest s in 1..16 whose T clusters of s CTAs are all co-resident in one wave of U SMs
+// (the B200 table in config.h scaled by U / 148); s = 1 always qualifies.
+int64_t cluster_fit_splits(int64_t T, int64_t U) {
+  int64_t best = 1;
+  for (int s = 2; s <= kMaxClusterSplits; ++s)
+    if (T <= static_cast<int64_t>(kMaxActiveClustersB200[s]) * U / 148) best = s;
+  return best;
+}
+
 void decide(int64_t batch, int64_t l_k, int64_t T, int64_t U, int64_t nblk, int policy, int forced,
             int* s, int* rule) {
   if (policy == DA_POLICY_FIXED) { *s = forced; *rule = DA_RULE_FORCED; return; }
@@ -58,16 +67,33 @@ void decide(int64_t batch, int64_t l_k, int64_t T, int64_t U, int64_t nblk, int 
   }
   if (saturated(T, U)) { *s = 1; *rule = DA_RULE_SATURATED; return; }
   if (policy == DA_POLICY_SEQ_AWARE_SM) {                                 // C-ext-1
+    const int64_t n_u = ceil_div(l_k, kSmUnit);
+    const int64_t f = cluster_fit_splits(T, U);
     if (nblk <= 4) {
-      const int64_t n_u = ceil_div(l_k, kSmUnit);
-      int64_t v = n_u / 2;
-      if (v > kSmMaxSplits) v = kSmMaxSplits;
-      if ((U - 1) / T < v) v = (U - 1) / T;
-      if (n_u < kSmMinUnits || v < 2) { *s = 1; *rule = DA_RULE_SM_SHORT; return; }
+      if (n_u < kSmMinUnits || (n_u < kSmMinUnitsWide && T > kSmWideT)) {
+        *s = 1; *rule = DA_RULE_SM_SHORT; return;
+      }
+      int64_t v = T <= kSmNarrowT ? kSmNarrowSplits : kSmMaxSplits;
+      if (n_u < v) v = n_u;
+      if (f < v) v = f;
+      if (v < 2) { *s = 1; *rule = DA_RULE_SM_SHORT; return; }
       *s = static_cast<int>(v);
       *rule = DA_RULE_SM_SPLIT;
       return;
     }
+    const int64_t e = efficiency_loop(T, U, nblk);
+    int64_t v = e;
+    if (e <= f) {
+      int64_t floor_s = kSmEffFloor;
+      if (n_u < floor_s) floor_s = n_u;
+      if (f < floor_s) floor_s = f;
+      if (floor_s > v) v = floor_s;
+    } else if (f >= 2 && (n_u <= kSmStreamUnits * f || 2 * T * f >= U)) {
+      v = f;
+    }
+    *s = static_cast<int>(v);
+    *rule = v == e ? DA_RULE_EFF_LOOP : DA_RULE_SM_FIT;
+    return;
   } else if (policy == DA_POLICY_GUARDED) {
     if (nblk <= 4) { *s = 1; *rule = DA_RULE_GUARD_NBLK4; return; }
   } else {  // DA_POLICY_SEQ_AWARE, Fig. 3 in order

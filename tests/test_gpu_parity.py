@@ -67,7 +67,7 @@ def test_baseline_configs(name, policy):
     cfg = synth.CONFIGS[name]
     plan, _, _ = run_and_check(**cfg, policy=policy)
     if name == "llama70b_tp8":
-        assert plan.num_splits == {"guarded": 1, "seq_aware": 3, "seq_aware_sm": 4, "evolved": 12}[policy]
+        assert plan.num_splits == {"guarded": 1, "seq_aware": 3, "seq_aware_sm": 8, "evolved": 12}[policy]
 
 
 @pytest.mark.parametrize("cfg", synth.low_head_sweep(),
@@ -220,6 +220,23 @@ def test_full_size_long_context_ragged_sampled():
     # ragged lengths at the long-context size: batch of 3 with 0 / 1 / random tokens
     cfg = dict(synth.CONFIGS["long_context"], batch=3)
     _check_sampled(cfg, "seq_aware", [(0, 1), (1, 2), (2, 4)], 1005, variant="ragged")
+
+
+def test_full_size_long_context_sm_policy_sampled():
+    # C-ext-1 moves the long-context split to the one-wave cluster split (s = 10, 8 clusters)
+    cfg = synth.CONFIGS["long_context"]
+    plan = _check_sampled(cfg, "seq_aware_sm", [(0, 0), (0, 3), (0, 7)], 1006)
+    assert plan.num_splits == 10 and plan.combine_mode == _dec().DA_COMBINE_CLUSTER
+
+
+# ---- SM-count-aware policy (C-ext-1): the efficiency-region one-wave cluster splits -----------
+@pytest.mark.parametrize("batch,h_q,h_kv,l_k", [(1, 8, 1, 4096), (1, 64, 8, 2048), (2, 64, 8, 2048),
+                                                (1, 16, 2, 700), (3, 24, 3, 1500)])
+@pytest.mark.parametrize("variant", ["normal", "ragged"])
+def test_seq_aware_sm_fit(batch, h_q, h_kv, l_k, variant):
+    plan, _, _ = run_and_check(batch, h_q, h_kv, l_k, policy="seq_aware_sm", variant=variant, seed=1100)
+    if plan.num_splits > 1 and plan.num_splits <= 16:
+        assert plan.combine_mode == _dec().DA_COMBINE_CLUSTER
 
 
 # ---- paged KV cache (da_forward_paged) --------------------------------------

@@ -231,34 +231,91 @@ def test_evolved_policy_literal_fig1():
         assert P.num_splits(2, 8, 1, lk, B200_SMS, 0, "evolved") == P.num_splits(2, 8, 1, lk, B200_SMS, 0, "guarded")
 
 
+def test_cluster_fit_splits():
+    # one wave never holds more CTAs than usable SMs (one CTA per SM in CLUSTER mode): T f <= U
+    for U in (3, 16, 132, 148):
+        prev = 16
+        for T in range(1, 2 * U):
+            f = P.cluster_fit_splits(T, U)
+            assert 1 <= f <= prev                       # non-increasing in T
+            assert f == 1 or T * f <= U
+            prev = f
+    # the B200 table (cudaOccupancyMaxActiveClusters): 7 clusters of 16, 8 of 10, 16 of 6, 33 of 4
+    assert [P.cluster_fit_splits(T, 148) for T in (1, 7, 8, 11, 12, 16, 33, 34, 74, 75)] == \
+        [16, 16, 10, 10, 9, 6, 4, 3, 2, 1]
+
+
 def test_seq_aware_sm_structure():
     rng = random.Random(5)
     for _ in range(20000):
         b = rng.randint(1, 64)
         hkv = rng.choice([1, 2, 4, 8, 16, 32])
-        lk = rng.randint(1, 20000)
+        lk = rng.randint(1, 140000)
         sms = rng.choice([132, 148, 16, 3])
         geo = P.geometry(b, 8 * hkv, hkv, lk, sms, 0)
         s, rule = P.num_splits(b, 8 * hkv, hkv, lk, sms, 0, "seq_aware_sm")
         g, grule = P.num_splits(b, 8 * hkv, hkv, lk, sms, 0, "guarded")
-        assert 1 <= s <= geo["nblk"]                      # never more splits than 128-token blocks
-        if geo["nblk"] >= 5 or P.saturated(geo["T"], geo["U"]):
-            assert (s, rule) == (g, grule)                # efficiency region / saturation unchanged
-        else:
-            assert s == 1 or geo["T"] * s < geo["U"]      # T s CTAs stay inside one wave
-            if lk <= 320:
+        n_u = -(-lk // 64)
+        f = P.cluster_fit_splits(geo["T"], geo["U"])
+        assert 1 <= s <= n_u                              # never an empty 64-token split
+        if P.saturated(geo["T"], geo["U"]):
+            assert (s, rule) == (g, grule)                # saturation guard unchanged
+        elif geo["nblk"] <= 4:
+            assert s == 1 or (s <= f and s <= 8)          # one wave of clusters
+            if lk <= 192:
                 assert s == 1                              # too few 64-token units to split
-    # the calibrated points: L_K = 512 at T <= 16 on B200 -> 4; L_K = 384 -> 3; L_K = 256 -> 1
-    assert P.num_splits(1, 8, 1, 512, B200_SMS, 0, "seq_aware_sm") == (4, P.RULE_SM_SPLIT)
+        else:
+            e = P.efficiency_loop(geo["T"], geo["U"], geo["nblk"])
+            assert (s == e) == (rule == P.RULE_EFF_LOOP)
+            assert s == e or s <= f                       # deviates from the loop only to one wave
+    # the calibrated points on B200
+    assert P.num_splits(1, 8, 1, 512, B200_SMS, 0, "seq_aware_sm") == (8, P.RULE_SM_SPLIT)
     assert P.num_splits(1, 64, 8, 512, B200_SMS, 0, "seq_aware_sm") == (4, P.RULE_SM_SPLIT)
     assert P.num_splits(2, 128, 16, 512, B200_SMS, 0, "seq_aware_sm") == (4, P.RULE_SM_SPLIT)
-    assert P.num_splits(1, 8, 1, 384, B200_SMS, 0, "seq_aware_sm")[0] == 3
-    assert P.num_splits(1, 8, 1, 256, B200_SMS, 0, "seq_aware_sm") == (1, P.RULE_SM_SHORT)
-    # the SM count enters: T = 64 tiles on 148 SMs -> floor(147 / 64) = 2 splits; on 132 -> 2;
-    # T = 80 -> 1 (cap); T = 120 -> saturated
+    assert P.num_splits(1, 8, 1, 384, B200_SMS, 0, "seq_aware_sm")[0] == 6
+    assert P.num_splits(1, 8, 1, 256, B200_SMS, 0, "seq_aware_sm") == (4, P.RULE_SM_SPLIT)
+    assert P.num_splits(1, 8, 1, 192, B200_SMS, 0, "seq_aware_sm") == (1, P.RULE_SM_SHORT)
+    assert P.num_splits(4, 64, 8, 256, B200_SMS, 0, "seq_aware_sm") == (1, P.RULE_SM_SHORT)
+    # the SM count enters through f: T = 64 tiles on 148 SMs -> 2 clusters of 2 fit; T = 80 -> 1;
+    # T = 120 -> saturated
     assert P.num_splits(8, 64, 8, 512, B200_SMS, 0, "seq_aware_sm")[0] == 2
     assert P.num_splits(10, 64, 8, 512, B200_SMS, 0, "seq_aware_sm")[0] == 1
     assert P.num_splits(15, 64, 8, 512, B200_SMS, 0, "seq_aware_sm")[1] == P.RULE_SATURATED
+    # efficiency region: the loop's workspace-combine split is moved to the one-wave cluster split
+    assert P.num_splits(1, 64, 8, 2048, B200_SMS, 0, "seq_aware_sm") == (10, P.RULE_SM_FIT)
+    assert P.num_splits(1, 64, 8, 131072, B200_SMS, 0, "seq_aware_sm") == (10, P.RULE_SM_FIT)
+    assert P.num_splits(1, 8, 1, 4096, B200_SMS, 0, "seq_aware_sm") == (16, P.RULE_SM_FIT)
+    # ... except for a long sequence with too few tiles to stream at HBM rate in one wave
+    assert P.num_splits(1, 8, 1, 131072, B200_SMS, 0, "seq_aware_sm") == \
+        P.num_splits(1, 8, 1, 131072, B200_SMS, 0, "guarded")
     # where the paper's rule splits (nblk = 4, T < 4) the generalisation splits too
     for hkv in (1, 2):
         assert P.num_splits(1, 8 * hkv, hkv, 512, B200_SMS, 0, "seq_aware_sm")[0] >= 3
+
+
+def _measured_grid():
+    import csv
+    import os
+    root = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles")
+    grid = {}
+    for name in ("r01f_ugrid.csv", "r01f_ugrid2.csv", "r01f_ugrid3.csv"):
+        with open(os.path.join(root, name)) as fh:
+            for r in csv.DictReader(fh):
+                key = (int(r.get("batch", 1)), int(r["h_kv"]), int(r["l_k"]))
+                grid.setdefault(key, {})[int(r["s"])] = float(r["latency_us"])
+    return grid
+
+
+def test_seq_aware_sm_calibration():
+    """C-ext-1's constants against the B200 measurements they were calibrated on
+    (profiles/r01f_ugrid*.csv, forced-s latencies of the current kernel, G = 8): the pick is
+    measured, within 6 % of the best measured split, and never slower than the guarded pick."""
+    grid = _measured_grid()
+    assert len(grid) >= 60
+    for (b, hkv, lk), t in grid.items():
+        s, _ = P.num_splits(b, 8 * hkv, hkv, lk, B200_SMS, 0, "seq_aware_sm")
+        g, _ = P.num_splits(b, 8 * hkv, hkv, lk, B200_SMS, 0, "guarded")
+        assert s in t, (b, hkv, lk, s)
+        assert t[s] <= 1.06 * min(t.values()), (b, hkv, lk, s)
+        if g in t:
+            assert t[s] <= 1.01 * t[g], (b, hkv, lk, s, g)
