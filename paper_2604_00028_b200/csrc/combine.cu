@@ -5,11 +5,11 @@
 // reductions"; the right arm of the U-curve; "atomic
 // combination overhead").
 //
-// One CTA (4 warps) per (b, h) row: every warp reduces the s lse values to
-// M with warp shuffles; warp w then accumulates splits w, w+4, ... with every
-// lane owning 4 of the 128 head dims (128-bit loads; the loads of 8 splits
-// are issued before their FMAs), and warp 0 adds the four partial sums.  Two
-// L2 round trips whatever s is.  Launched with programmatic dependent launch
+// One CTA (4 warps) per (b, h) row: warp w merges splits w, w+4, ... online
+// against its own running maximum, every lane owning 4 of the 128 head dims
+// (128-bit loads; the lse and o loads of 8 splits are issued together, so
+// s <= 32 costs one L2 round trip), and warp 0 merges the four warps'
+// (max, sum, accumulator) triples with the same identity.  Launched with programmatic dependent launch
 // so its launch latency hides under the forward kernel's tail;
 // griddepcontrol.wait orders its reads after the forward's writes.
 #include <cuda_runtime.h>
@@ -29,77 +29,101 @@ namespace {
 constexpr float kNegInf = -__builtin_huge_valf();
 constexpr float kLog2e = 1.4426950408889634f;
 
+// development timeline tracing (-DDECATTN_TRACE builds only): per row < 64, globaltimer ns at
+// entry (0), after griddepcontrol.wait (1), after the output store (2)
+#ifdef DECATTN_TRACE
+__device__ unsigned long long g_trace_comb[64 * 4];
+__device__ __forceinline__ void ctrace(int slot) {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  if (blockIdx.x < 64) g_trace_comb[blockIdx.x * 4 + slot] = t;
+}
+#define CTRACE(slot) do { if (threadIdx.x == 0) ctrace(slot); } while (0)
+#else
+#define CTRACE(slot) do { } while (0)
+#endif
+
 __global__ void __launch_bounds__(kCombineThreads)
     lse_combine_kernel(const CombineParams p) {
+  CTRACE(0);
   pdl_launch_dependents();   // the next step's forward may start its prologue
   pdl_wait();                // partials are written by the preceding forward kernel
+  CTRACE(1);
   constexpr int kWarps = kCombineThreads / 32;
+  constexpr int kBatch = 8;
   __shared__ float4 s_acc[kWarps][32];
-  __shared__ float s_l[kWarps];
+  __shared__ float s_m[kWarps], s_l[kWarps];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int row = blockIdx.x;
   const int s = p.num_splits;
   DA_DASSERT(row < p.rows && s >= 1);
   const float* lse_in = p.lse_in + row;
+  const float4* o = reinterpret_cast<const float4*>(p.o + static_cast<int64_t>(row) * kHeadDim) + lane;
+  const int64_t ostride4 = p.o_stride / 4;
 
-  // (1) M = max_i lse_i: every warp reduces all s values (one L2 round trip)
-  float M = kNegInf;
-  for (int i = lane; i < s; i += 32) M = fmaxf(M, __ldg(lse_in + i * p.lse_stride));
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, off));
-  const bool empty = M == kNegInf;
-
-  // (2) warp w accumulates splits w, w + kWarps, ...: lane owns dims 4 lane .. 4 lane + 3.
-  //     The loads of 8 splits are issued before their FMAs (second L2 round trip).
-  float Lw = 0.f;
+  // (1) warp w merges splits w, w + 4, ...: the lse and o loads of 8 splits are issued together
+  //     (one L2 round trip for s <= 32), merged online against the warp's running maximum m
+  //     (in log2 units); lane owns dims 4 lane .. 4 lane + 3.
+  float m = kNegInf, Lw = 0.f;
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-  if (!empty) {
-    const float4* o = reinterpret_cast<const float4*>(p.o + static_cast<int64_t>(row) * kHeadDim) + lane;
-    const int64_t ostride4 = p.o_stride / 4;
-    for (int i0 = warp; i0 < s; i0 += 8 * kWarps) {
-      float li[8];
-      float4 oi[8];
+  for (int i0 = warp; i0 < s; i0 += kBatch * kWarps) {
+    float li[kBatch];
+    float4 oi[kBatch];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const int i = i0 + j * kWarps;
-        li[j] = kNegInf;
-        oi[j] = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (i < s) {
-          li[j] = __ldg(lse_in + i * p.lse_stride);
-          oi[j] = __ldg(o + i * ostride4);
-        }
-      }
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const float wgt = ex2((li[j] - M) * kLog2e);     // empty split or past s: exp(-inf) = 0
-        Lw += wgt;
-        acc.x = fmaf(wgt, oi[j].x, acc.x);
-        acc.y = fmaf(wgt, oi[j].y, acc.y);
-        acc.z = fmaf(wgt, oi[j].z, acc.z);
-        acc.w = fmaf(wgt, oi[j].w, acc.w);
+    for (int j = 0; j < kBatch; ++j) {
+      const int i = i0 + j * kWarps;
+      li[j] = kNegInf;
+      oi[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (i < s) {
+        li[j] = __ldg(lse_in + i * p.lse_stride) * kLog2e;
+        oi[j] = __ldg(o + i * ostride4);
       }
     }
+    float mb = m;
+#pragma unroll
+    for (int j = 0; j < kBatch; ++j) mb = fmaxf(mb, li[j]);
+    if (mb == kNegInf) continue;                           // every split so far empty
+    const float r = ex2(m - mb);                           // m = -inf -> 0 (acc, Lw are 0)
+    Lw *= r;
+    acc = make_float4(acc.x * r, acc.y * r, acc.z * r, acc.w * r);
+#pragma unroll
+    for (int j = 0; j < kBatch; ++j) {
+      const float wgt = ex2(li[j] - mb);                   // empty split or past s: 0
+      Lw += wgt;
+      acc.x = fmaf(wgt, oi[j].x, acc.x);
+      acc.y = fmaf(wgt, oi[j].y, acc.y);
+      acc.z = fmaf(wgt, oi[j].z, acc.z);
+      acc.w = fmaf(wgt, oi[j].w, acc.w);
+    }
+    m = mb;
   }
   s_acc[warp][lane] = acc;
-  if (lane == 0) s_l[warp] = Lw;
+  if (lane == 0) { s_m[warp] = m; s_l[warp] = Lw; }
   __syncthreads();
   if (warp != 0) return;
 
-  // (3) warp 0 sums the warps' partial sums and writes the row
+  // (2) warp 0 merges the warps' (m, L, acc): M = max m_w, weights 2^(m_w - M)
+  float M = kNegInf;
+#pragma unroll
+  for (int w = 0; w < kWarps; ++w) M = fmaxf(M, s_m[w]);
+  const bool empty = M == kNegInf;
   float L = 0.f;
   float4 sum = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (!empty) {
 #pragma unroll
-  for (int w = 0; w < kWarps; ++w) {
-    L += s_l[w];
-    const float4 a = s_acc[w][lane];
-    sum.x += a.x;
-    sum.y += a.y;
-    sum.z += a.z;
-    sum.w += a.w;
+    for (int w = 0; w < kWarps; ++w) {
+      const float c = ex2(s_m[w] - M);                     // empty warp: 2^-inf = 0
+      L = fmaf(c, s_l[w], L);
+      const float4 a = s_acc[w][lane];
+      sum.x = fmaf(c, a.x, sum.x);
+      sum.y = fmaf(c, a.y, sum.y);
+      sum.z = fmaf(c, a.z, sum.z);
+      sum.w = fmaf(c, a.w, sum.w);
+    }
   }
   const float inv = L > 0.f ? __frcp_rn(L) : 0.f;
   sum = make_float4(sum.x * inv, sum.y * inv, sum.z * inv, sum.w * inv);
-  const float lse = empty ? kNegInf : M + lg2(L) * (1.f / kLog2e);
+  const float lse = empty ? kNegInf : (M + lg2(L)) * (1.f / kLog2e);
   if (p.out_f32) {
     reinterpret_cast<float4*>(p.out)[static_cast<int64_t>(row) * (kHeadDim / 4) + lane] = sum;
   } else {
@@ -109,6 +133,7 @@ __global__ void __launch_bounds__(kCombineThreads)
     reinterpret_cast<uint2*>(p.out)[static_cast<int64_t>(row) * (kHeadDim / 4) + lane] = w2;
   }
   if (lane == 0 && p.lse != nullptr) p.lse[row] = lse;
+  CTRACE(2);
 }
 
 }  // namespace
@@ -126,5 +151,12 @@ cudaError_t launch_lse_combine(const CombineParams& p, bool pdl, cudaStream_t st
   cfg.numAttrs = pdl ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, lse_combine_kernel, p);
 }
+
+#ifdef DECATTN_TRACE
+extern "C" __attribute__((visibility("default"))) int da_trace_fetch_combine(unsigned long long* host, int n) {
+  if (n > 64 * 4) n = 64 * 4;
+  return cudaMemcpyFromSymbol(host, g_trace_comb, sizeof(unsigned long long) * n) == cudaSuccess ? 0 : 1;
+}
+#endif
 
 }  // namespace decattn

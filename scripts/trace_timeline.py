@@ -18,6 +18,8 @@ from paper_2604_00028_b200 import _lib as L
 import synth
 
 L.LIB.da_trace_fetch.argtypes = [ctypes.c_void_p, ctypes.c_int]
+if hasattr(L.LIB, "da_trace_fetch_combine"):
+    L.LIB.da_trace_fetch_combine.argtypes = [ctypes.c_void_p, ctypes.c_int]
 
 
 def trace(b, hq, hkv, lk, policy, forced=0, steps=50, combine=None):
@@ -73,6 +75,15 @@ def trace(b, hq, hkv, lk, policy, forced=0, steps=50, combine=None):
         if r[60] and r[61] and r[30] > r[0]:
             parts.append(f"clk={(int(r[61]) - int(r[60])) / (int(r[30]) - int(r[0])) * 1e3:.0f}MHz")
         print(f"  cta{c}: " + " ".join(parts))
+    if plan.combine_mode == L.DA_COMBINE_KERNEL and hasattr(L.LIB, "da_trace_fetch_combine"):
+        cb = (ctypes.c_ulonglong * (64 * 4))()
+        L.LIB.da_trace_fetch_combine(ctypes.addressof(cb), 64 * 4)
+        f0 = min(int(r[0]) for r in rows if r[0])
+        fend = max(int(r[30]) for r in rows if r[30])
+        print(f"  fwd: first entry 0, last CTA end {fend - f0}")
+        for c in range(min(b * hq, 4)):
+            print(f"  comb row{c}: entry={int(cb[c * 4]) - f0} waited={int(cb[c * 4 + 1]) - f0} "
+                  f"end={int(cb[c * 4 + 2]) - f0}")
 
 
 if __name__ == "__main__":
@@ -84,6 +95,7 @@ if __name__ == "__main__":
         trace(1, 8, 1, 512, "fixed", 8)
         trace(1, 64, 8, 512, "seq_aware")
     elif which == "kernel":
-        trace(1, 8, 1, 512, "fixed", 9, combine=2)
-        trace(1, 8, 1, 512, "fixed", 32, combine=2)
+        trace(1, 8, 1, 768, "fixed", 16, combine=1)
+        trace(1, 8, 1, 768, "fixed", 16, combine=2)
+        trace(1, 8, 1, 768, "fixed", 24, combine=2)
         trace(1, 8, 1, 4096, "guarded")
