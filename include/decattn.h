@@ -85,7 +85,7 @@ typedef enum da_policy {
                                (1 when n_u < 4, or n_u < 6 and T > 16);
                                else the efficiency loop's e, raised to
                                min(8, n_u, f) when e <= f, or moved to f when
-                               e > f >= 2 and (n_u <= 32 f or 2 T f >= U);
+                               e > f >= 2 and (n_u <= 16 f or 2 T f >= U);
                                B200-calibrated                              */
 } da_policy;
 

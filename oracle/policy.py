@@ -64,8 +64,8 @@ RULE_SM_FIT = 10      # SM-count-aware generalisation: efficiency-loop split mov
 # C-ext-1).  The paper leaves "extending the benefit to lower L_K values and learning more
 # configuration-specific split counts" to future work and calls its
 # own constant stack-specific ("s=3 on the current stack").  These constants are
-# calibrated from the B200 U-curves of the current kernel (profiles/r01f_ugrid.csv,
-# r01f_ugrid2.csv, r01f_ugrid3.csv; long-context boundary from scripts/probe_regime.py and
+# calibrated from the B200 U-curves of the current kernel (profiles/r01g_ugrid.csv,
+# r01g_ugrid2.csv, r01g_ugrid3.csv; long-context boundary from scripts/probe_regime.py and
 # scripts/probe_long.py) and frozen:
 SM_UNIT = 64          # tokens per split unit of the B200 kernel
 SM_MIN_UNITS = 4      # fewer units (L_K <= 192): every split loses on B200
@@ -75,8 +75,8 @@ SM_NARROW_T = 4       # T <= 4 tiles: the plateau extends to s = 8 ...
 SM_NARROW_SPLITS = 8
 SM_MAX_SPLITS = 4     # ... otherwise the measured plateau starts at s = 4 (L_K <= 512)
 SM_EFF_FLOOR = 8      # efficiency region: at least min(8, n_u, fit) splits
-SM_STREAM_UNITS = 32  # efficiency region: cap to the one-wave cluster split while each split
-                      # holds <= 32 units (2048 tokens) or the capped launch still has >= U/2 CTAs
+SM_STREAM_UNITS = 16  # efficiency region: cap to the one-wave cluster split while each split
+                      # holds <= 16 units (1024 tokens) or the capped launch still has >= U/2 CTAs
 # Clusters of s CTAs (one per split, s = 1..16) that are co-resident in one wave on a 148-SM
 # B200 with the cluster-combine kernel configuration (cudaOccupancyMaxActiveClusters,
 # scripts/microbench_cluster16.cu); index 0 unused, index 1 = one CTA per SM.  Scaled by U / 148.
@@ -185,7 +185,7 @@ def seq_aware_sm_splits(geo: dict, l_k: int):
         s = min(n_u, 8 if T <= 4 else 4, f);  s < 2 -> 1
       nblk >= 5 (efficiency region), e = the unchanged efficiency loop:
         e <= f                                  -> max(e, min(8, n_u, f))
-        e > f >= 2 and (n_u <= 32 f or 2 T f >= U) -> f
+        e > f >= 2 and (n_u <= 16 f or 2 T f >= U) -> f
         else                                    -> e
     The split count depends on the tile count T = Batch x H_KV versus the usable SMs U through
     f, the largest split whose clusters all fit one wave, not on a static L_K guard."""

@@ -21,7 +21,7 @@ constexpr int kEvolvedSplits = 12, kEvolvedShortSplits = 16, kEvolvedShortLk = 2
 // SM-count-aware generalisation (DESIGN.md C-ext-1): B200-calibrated, frozen constants
 constexpr int kSmUnit = 64, kSmMinUnits = 4, kSmMinUnitsWide = 6, kSmWideT = 16;
 constexpr int kSmNarrowT = 4, kSmNarrowSplits = 8, kSmMaxSplits = 4;
-constexpr int kSmEffFloor = 8, kSmStreamUnits = 32;
+constexpr int kSmEffFloor = 8, kSmStreamUnits = 16;
 
 // ---- kernel geometry (B200 side) -----------------------------
 constexpr int kHeadDim = 128;          // v1 supports d = 128 only

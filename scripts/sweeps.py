@@ -27,7 +27,7 @@ import bench  # noqa: E402  (Workload, make_graph, Timer)
 import paper_2604_00028_b200 as dec  # noqa: E402
 
 TAG = os.environ.get("SWEEP_TAG", "r01")
-OUT = os.path.join(ROOT, "profiles")
+OUT = os.environ.get("SWEEP_OUT", os.path.join(ROOT, "profiles"))
 D = 128
 
 

@@ -298,7 +298,7 @@ def _measured_grid():
     import os
     root = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles")
     grid = {}
-    for name in ("r01f_ugrid.csv", "r01f_ugrid2.csv", "r01f_ugrid3.csv"):
+    for name in ("r01g_ugrid.csv", "r01g_ugrid2.csv", "r01g_ugrid3.csv"):
         with open(os.path.join(root, name)) as fh:
             for r in csv.DictReader(fh):
                 key = (int(r.get("batch", 1)), int(r["h_kv"]), int(r["l_k"]))
@@ -308,7 +308,7 @@ def _measured_grid():
 
 def test_seq_aware_sm_calibration():
     """C-ext-1's constants against the B200 measurements they were calibrated on
-    (profiles/r01f_ugrid*.csv, forced-s latencies of the current kernel, G = 8): the pick is
+    (profiles/r01g_ugrid*.csv, forced-s latencies of the current kernel, G = 8): the pick is
     measured, within 6 % of the best measured split, and never slower than the guarded pick."""
     grid = _measured_grid()
     assert len(grid) >= 60
