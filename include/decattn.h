@@ -226,8 +226,8 @@ DA_API da_status da_forward(const da_plan* plan, const void* q, const void* k_ca
  *   k_pages, v_pages  bf16 [num_pages, page_size, H_KV, d]; strides (as in da_forward)
  *                     are {q_b, q_h, k_page, k_t, k_h, v_page, v_t, v_h} in elements,
  *                     NULL = contiguous pools
- *   page_size         tokens per page: a multiple of 64 (one kernel tile never spans pages),
- *                     else DA_ERR_UNSUPPORTED
+ *   page_size         tokens per page: a multiple of 64 (one kernel tile never spans pages)
+ *                     and at most 262144, else DA_ERR_UNSUPPORTED
  *   block_table       device int32 [B, block_table_stride]: entry j of row b is the page
  *                     holding tokens [j page_size, (j+1) page_size) of sequence b.  Entries
  *                     past a sequence's length are never read; an index outside

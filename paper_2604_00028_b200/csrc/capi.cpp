@@ -147,6 +147,7 @@ da_status forward_impl(const da_plan* plan, const void* q, const void* k_cache, 
   p.l_default = plan->l_k;
   p.l_cap = l_cap;
   p.num_splits = plan->num_splits;
+  p.s_magic = div_magic(static_cast<uint32_t>(plan->num_splits));
   p.G = plan->h_q / plan->h_kv;
   p.h_q = plan->h_q;
   p.batch = plan->batch;
@@ -161,6 +162,7 @@ da_status forward_impl(const da_plan* plan, const void* q, const void* k_cache, 
   p.block_table = pg.block_table;
   p.bt_stride = pg.bt_stride;
   p.page_size = pg.page_size;
+  p.page_magic = pg.page_size > 0 ? div_magic(static_cast<uint32_t>(pg.page_size / kTileN)) : 0;
 
   cudaStream_t stream = static_cast<cudaStream_t>(cuda_stream);
   if (launch_split_kv_fwd(*plan, tk, tv, p, stream) != cudaSuccess) return DA_ERR_CUDA;
@@ -199,7 +201,7 @@ extern "C" da_status da_forward_paged(const da_plan* plan, const void* q, const 
                                       void* out, float* lse, void* workspace, int64_t workspace_bytes,
                                       void* cuda_stream) {
   if (block_table == nullptr || num_pages < 1 || max_pages_per_seq < 1) return DA_ERR_INVALID_ARG;
-  if (page_size < kTileN || page_size % kTileN != 0) return DA_ERR_UNSUPPORTED;
+  if (page_size < kTileN || page_size % kTileN != 0 || page_size > kMaxPageSize) return DA_ERR_UNSUPPORTED;
   if (block_table_stride < max_pages_per_seq) return DA_ERR_INVALID_ARG;
   const int64_t cap = int64_t(max_pages_per_seq) * page_size;
   if (cap > INT32_MAX) return DA_ERR_INVALID_ARG;

@@ -252,19 +252,24 @@ __device__ __forceinline__ void store_out(const FwdParams& p, size_t row, int d4
   }
 }
 
+// floor(x / d) for a launch-invariant d given m = ceil(2^38 / d) (internal.h div_magic; exact
+// while x d < 2^38): a 32 x 64-bit multiply and a shift instead of an integer divide.
+__device__ __forceinline__ uint32_t udiv_magic(uint32_t x, uint64_t m) {
+  return static_cast<uint32_t>((static_cast<uint64_t>(x) * m) >> 38);
+}
+
 // Tokens [t0, t_end) of split `split` of s for a sequence of n tokens: units of kTileN
-// tokens, split i covering units [floor(i n_u / s), floor((i+1) n_u / s)) (C-pol item 6).
-__device__ __forceinline__ void split_range(int n, int split, int s, int& t0, int& t_end, int& n_tiles) {
-  const uint32_t nu = static_cast<uint32_t>((n + kTileN - 1) / kTileN);
-  const uint32_t us = static_cast<uint32_t>(s);
-  uint32_t u0, u1;
-  if (nu <= 0xffffffffu / us) {              // (split + 1) * nu fits in 32 bits
-    u0 = static_cast<uint32_t>(split) * nu / us;
-    u1 = static_cast<uint32_t>(split + 1) * nu / us;
-  } else {
-    u0 = static_cast<uint32_t>(static_cast<uint64_t>(split) * nu / us);
-    u1 = static_cast<uint32_t>(static_cast<uint64_t>(split + 1) * nu / us);
-  }
+// tokens, split i covering units [floor(i n_u / s), floor((i+1) n_u / s)) (C-pol item 6),
+// evaluated as i q + floor(i r / s) with n_u = q s + r so every quotient is exact (n_u < 2^25,
+// i r < 2^16, s <= 256).
+__device__ __forceinline__ void split_range(int n, int split, int s, uint64_t s_magic, int& t0, int& t_end,
+                                            int& n_tiles) {
+  const uint32_t nu = (static_cast<uint32_t>(n) + (kTileN - 1)) / kTileN;
+  const uint32_t q = udiv_magic(nu, s_magic);
+  const uint32_t r = nu - q * static_cast<uint32_t>(s);
+  const uint32_t i0 = static_cast<uint32_t>(split), i1 = i0 + 1;
+  const uint32_t u0 = i0 * q + udiv_magic(i0 * r, s_magic);
+  const uint32_t u1 = i1 * q + udiv_magic(i1 * r, s_magic);
   t0 = static_cast<int>(u0) * kTileN;
   t_end = min(static_cast<int>(u1) * kTileN, n);
   n_tiles = static_cast<int>(u1 - u0);
@@ -317,7 +322,7 @@ __global__ void __launch_bounds__(threads_for(NW, helpers_for(kCombine)), 1)
   // CLUSTER: rank r owns rows g = r, r + s, r + 2s, ... and emits them
   const int s_cl = kCluster ? p.num_splits : 1;
   const uint32_t rank = kCluster ? cluster_ctarank() : 0u;
-  const int rows_per_owner = (R + s_cl - 1) / s_cl;
+  const int rows_per_owner = kCluster ? static_cast<int>(udiv_magic(R + s_cl - 1, p.s_magic)) : R;
 
   if (threadIdx.x == 0) TRACE(0);
 #ifdef DECATTN_TRACE
@@ -332,7 +337,8 @@ __global__ void __launch_bounds__(threads_for(NW, helpers_for(kCombine)), 1)
     if constexpr (kCluster) {
       // expect s pushes (every rank, this one included) of (O row, m, l) for every valid row
       // this rank owns, counted in st.async bytes
-      const int owned = rows_valid > static_cast<int>(rank) ? (rows_valid - 1 - static_cast<int>(rank)) / s_cl + 1 : 0;
+      const int owned = rows_valid > static_cast<int>(rank)
+          ? static_cast<int>(udiv_magic(rows_valid - 1 - static_cast<int>(rank), p.s_magic)) + 1 : 0;
       mbar_init(smem_u32(&push_bar), 1);
       mbar_arrive_expect_tx(smem_u32(&push_bar), static_cast<uint32_t>(s_cl * owned * (kHeadDim * 4 + 8)));
     }
@@ -341,21 +347,10 @@ __global__ void __launch_bounds__(threads_for(NW, helpers_for(kCombine)), 1)
   if (warp == NW && lane == 0) {
     prefetch_tmap(&tmap_k);
     prefetch_tmap(&tmap_v);
-    // the lengths and the block-table row are read right after griddepcontrol.wait: pull their
-    // lines into L2 now (a prefetch never returns data, so it cannot observe a stale value)
+    // the lengths are read right after griddepcontrol.wait: pull their line into L2 now (a
+    // prefetch never returns data, so it cannot observe a stale value)
     if (p.seqlens != nullptr) prefetch_l2(p.seqlens + b);
-    if (p.block_table != nullptr) {
-      const int32_t* bt = p.block_table + static_cast<int64_t>(b) * p.bt_stride;
-      const int first = static_cast<int>(static_cast<int64_t>(split) * min(max(p.l_default, 0), p.l_cap) /
-                                         max(p.num_splits, 1) / p.page_size);
-      prefetch_l2(bt + first);
-    }
   }
-  // ---- this split's token range (C-pol item 6), in units of kTileN tokens.  With uniform
-  // lengths (cache_seqlens == NULL) it is known before griddepcontrol.wait, so the producer
-  // can issue the first TMA the moment the wait returns.
-  int t0, t_end, n_tiles;
-  split_range(min(max(p.l_default, 0), p.l_cap), split, p.num_splits, t0, t_end, n_tiles);
   __syncthreads();
   if constexpr (kCluster) cluster_arrive_relaxed();   // "my push barrier is initialised"
 
@@ -371,8 +366,10 @@ __global__ void __launch_bounds__(threads_for(NW, helpers_for(kCombine)), 1)
     if (c_ < 64) g_trace[c_ * 64 + 63] = *(volatile unsigned long long*)&g_prev_end;
   }
 #endif
-  if (p.seqlens != nullptr)
-    split_range(min(max(__ldg(p.seqlens + b), 0), p.l_cap), split, p.num_splits, t0, t_end, n_tiles);
+  // ---- this split's token range (C-pol item 6), in units of kTileN tokens
+  int t0, t_end, n_tiles;
+  split_range(min(max(p.seqlens != nullptr ? __ldg(p.seqlens + b) : p.l_default, 0), p.l_cap), split,
+              p.num_splits, p.s_magic, t0, t_end, n_tiles);
 
   if (warp == NW) {
     // ================= TMA producer =================
@@ -393,24 +390,33 @@ __global__ void __launch_bounds__(threads_for(NW, helpers_for(kCombine)), 1)
       } else {
         // paged cache: tile i of the split lives in page block_table[b][t / page_size] at token
         // t % page_size (a tile never spans pages).  The page indices of the next NS tiles are
-        // loaded ahead so the lookups do not throttle the ring.  Out-of-range indices fall
-        // outside the tensor map and read as zeros.
+        // loaded ahead so the lookups do not throttle the ring; both the current tile and the
+        // look-ahead walk the pages with a (page, tile-in-page) cursor, one division in all.
+        // Out-of-range indices fall outside the tensor map and read as zeros.
         const int32_t* bt = p.block_table + static_cast<int64_t>(b) * p.bt_stride;
+        const uint32_t tpp = static_cast<uint32_t>(p.page_size / kTileN);   // tiles per page
+        const uint32_t tile0 = static_cast<uint32_t>(t0 / kTileN);
+        uint32_t cj = udiv_magic(tile0, p.page_magic), ck = tile0 - cj * tpp;   // current tile
+        uint32_t lj = cj, lk = ck;                                              // look-ahead
         int pg[NS];
 #pragma unroll
-        for (int j = 0; j < NS; ++j) pg[j] = j < n_tiles ? __ldg(bt + (t0 + j * kTileN) / p.page_size) : 0;
+        for (int j = 0; j < NS; ++j) {
+          pg[j] = j < n_tiles ? __ldg(bt + lj) : 0;
+          if (++lk == tpp) { lk = 0; ++lj; }
+        }
         for (int i = 0; i < n_tiles; ++i) {
           const int st = i % NS;
           if (i >= NS) mbar_wait(smem_u32(&empty_bar[st]), ((i / NS) - 1) & 1);
           const uint32_t fb = smem_u32(&full_bar[st]);
           mbar_arrive_expect_tx(fb, kStageBytes);
           const uint32_t dst = sbase + st * kStageBytes;
-          const int t = t0 + i * kTileN;
           const int page = pg[0];
-          const int slot = t - (t / p.page_size) * p.page_size;
+          const int slot = static_cast<int>(ck) * kTileN;
+          if (++ck == tpp) { ck = 0; ++cj; }
 #pragma unroll
           for (int j = 0; j + 1 < NS; ++j) pg[j] = pg[j + 1];
-          pg[NS - 1] = i + NS < n_tiles ? __ldg(bt + (t + NS * kTileN) / p.page_size) : 0;
+          pg[NS - 1] = i + NS < n_tiles ? __ldg(bt + lj) : 0;
+          if (++lk == tpp) { lk = 0; ++lj; }
           tma_load_5d(dst, &tmap_k, fb, 0, slot, 0, kvh, page);
           tma_load_5d(dst + 2 * kHalfBytes, &tmap_v, fb, 0, slot, 0, kvh, page);
         }
@@ -603,10 +609,11 @@ __global__ void __launch_bounds__(threads_for(NW, helpers_for(kCombine)), 1)
       const int e = threadIdx.x + it * kT;
       const int g = e >> 5, d4 = e & 31;
       if (e >= R * 32 || g >= rows_valid) continue;
-      const int owner = g % s;
+      const int gq = static_cast<int>(udiv_magic(g, p.s_magic));   // g / s
+      const int owner = g - gq * s;
       // slot [source rank][row g / s of the owner]
-      float* const dst = slots + (static_cast<int>(rank) * rows_per_owner + g / s) * kSlotRowFloats;
-      DA_DASSERT(static_cast<int>(rank) * rows_per_owner + g / s < kMaxSlotRows && g < R);
+      float* const dst = slots + (static_cast<int>(rank) * rows_per_owner + gq) * kSlotRowFloats;
+      DA_DASSERT(static_cast<int>(rank) * rows_per_owner + gq < kMaxSlotRows && g < R && owner == g % s);
       const uint32_t rbar = mapa(smem_u32(&push_bar), owner);
       st_async_v4(mapa(smem_u32(dst + 4 * d4), owner), eO[it], rbar);
       if (d4 == 0) st_async_v2(mapa(smem_u32(dst + kHeadDim), owner), eM[it], eL[it], rbar);
@@ -630,6 +637,7 @@ __global__ void __launch_bounds__(threads_for(NW, helpers_for(kCombine)), 1)
       float M = kNegInf;
 #pragma unroll 4
       for (int r = 0; r < s; ++r) M = fmaxf(M, row0[r * rstride + kHeadDim]);
+      if (t == 0) TRACE(44);
       float Lsum = 0.f;
       float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
       if (M != kNegInf) {
@@ -645,12 +653,15 @@ __global__ void __launch_bounds__(threads_for(NW, helpers_for(kCombine)), 1)
           acc.w = fmaf(f, ow.w, acc.w);
         }
       }
+      if (t == 0) TRACE(45);
       const float inv = Lsum > 0.f ? __frcp_rn(Lsum) : 0.f;
       const size_t row = static_cast<size_t>(b) * p.h_q + hq0 + g;
       store_out(p, row, d4, make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv));
       if (d4 == 0 && p.lse != nullptr) p.lse[row] = Lsum > 0.f ? (M + lg2(Lsum)) * kLn2 : kNegInf;
+      if (t == 0) TRACE(46);
     }
   }
+  if (threadIdx.x == 0) TRACE(47);
 #ifdef DECATTN_TRACE
   __syncthreads();
   if (threadIdx.x == 0) {

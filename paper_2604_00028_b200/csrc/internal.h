@@ -18,6 +18,7 @@ struct FwdParams {
   int32_t l_default;        // length used when seqlens == nullptr (plan->l_k)
   int32_t l_cap;            // cache capacity (clamp bound)
   int32_t num_splits;       // s
+  uint64_t s_magic;         // ceil(2^38 / s): floor(x / s) = (x * s_magic) >> 38 for x s < 2^38
   int32_t G;                // H_Q / H_KV
   int32_t h_q;
   int32_t batch;
@@ -31,8 +32,14 @@ struct FwdParams {
   // paged KV cache (da_forward_paged); block_table == nullptr for a dense cache
   const int32_t* block_table;   // [B, bt_stride] page indices
   int64_t bt_stride;
-  int32_t page_size;            // tokens per page, a multiple of kTileN
+  int32_t page_size;            // tokens per page, a multiple of kTileN, <= kMaxPageSize
+  uint64_t page_magic;          // ceil(2^38 / (page_size / kTileN))
 };
+
+// Division by a launch-invariant divisor d without an integer divide: with m = ceil(2^38 / d),
+// floor(x / d) = (x m) >> 38 exactly whenever x d < 2^38 (m d = 2^38 + delta, delta < d, so the
+// product overshoots x / d by less than x / 2^38 < 1 / d, which cannot cross the next integer).
+inline uint64_t div_magic(uint32_t d) { return ((uint64_t(1) << 38) + d - 1) / d; }
 
 struct CombineParams {
   const float* o;           // split i at o + i * o_stride, [rows, d]

@@ -89,11 +89,11 @@ def trace(b, hq, hkv, lk, policy, forced=0, steps=50, combine=None):
 if __name__ == "__main__":
     which = sys.argv[1] if len(sys.argv) > 1 else "latency"
     if which == "latency":
-        trace(1, 8, 1, 64, "fixed", 1)
         trace(1, 8, 1, 512, "guarded")
-        trace(1, 8, 1, 512, "seq_aware")
-        trace(1, 8, 1, 512, "fixed", 8)
-        trace(1, 64, 8, 512, "seq_aware")
+        trace(1, 8, 1, 512, "seq_aware_sm")
+        trace(1, 64, 8, 512, "guarded")
+        trace(1, 64, 8, 512, "seq_aware_sm")
+        trace(1, 64, 8, 512, "fixed", 8)
     elif which == "kernel":
         trace(1, 8, 1, 768, "fixed", 16, combine=1)
         trace(1, 8, 1, 768, "fixed", 16, combine=2)
