@@ -343,43 +343,29 @@ def run_reference(args, rank, world):
 
 # ----------------------------------------------------------------------------------------------
 def e2e_measure(dec, L, cfg, dev, stream, steps, warmup, policy="seq_aware_sm"):
-    """Same metric through the public API with HOST buffers: per step H2D of q/k/v from pinned
-    memory, da_plan_make, da_forward, D2H of out + lse - all inside the timed region."""
+    """Same metric through the C ABI with HOST buffers (da_forward_host): per step da_plan_make,
+    then the H2D copies of q/K/V from pinned memory, the forward and the D2H copies of out + lse,
+    all enqueued on one stream inside the timed region (CUDA events around the K steps)."""
     b, hq, hkv, lk = cfg["batch"], cfg["h_q"], cfg["h_kv"], cfg["l_k"]
     inp = synth.make_inputs(b, hq, hkv, lk, seed=2000)
-    hq_, hk_, hv_ = (inp[n].pin_memory() for n in ("q", "k", "v"))
-    dq = torch.empty_like(hq_, device=dev)
-    dk = torch.empty_like(hk_, device=dev)
-    dv = torch.empty_like(hv_, device=dev)
-    out = torch.empty((b, hq, HEAD_DIM), dtype=torch.bfloat16, device=dev)
-    lse = torch.empty((b, hq), dtype=torch.float32, device=dev)
-    h_out = torch.empty(out.shape, dtype=out.dtype).pin_memory()
-    h_lse = torch.empty(lse.shape, dtype=lse.dtype).pin_memory()
+    hq_, hk_, hv_ = (inp[n].contiguous().pin_memory() for n in ("q", "k", "v"))
+    h_out = torch.empty((b, hq, HEAD_DIM), dtype=torch.bfloat16).pin_memory()
+    h_lse = torch.empty((b, hq), dtype=torch.float32).pin_memory()
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
-    ws_cache = {}
+    staging = dec.HostStaging(dev)
 
     def step():
-        dq.copy_(hq_, non_blocking=True)
-        dk.copy_(hk_, non_blocking=True)
-        dv.copy_(hv_, non_blocking=True)
         plan = L.da_plan_make(b, hq, hkv, lk, HEAD_DIM, 1, 0, sms, L.POLICIES[policy], 0)
-        ws = ws_cache.get(plan.workspace_bytes)
-        if ws is None and plan.combine_mode == L.DA_COMBINE_KERNEL:
-            ws = ws_cache.setdefault(plan.workspace_bytes, dec.workspace_for(plan, dev))
-        dec.forward(plan, dq, dk, dv, None, out=out, lse=lse, workspace=ws)
-        h_out.copy_(out, non_blocking=True)
-        h_lse.copy_(lse, non_blocking=True)
+        dec.forward_host(plan, hq_, hk_, hv_, None, out=h_out, lse=h_lse, staging=staging, stream=stream)
 
-    with torch.cuda.stream(stream):
-        for _ in range(max(warmup, 1)):
-            step()
+    for _ in range(max(warmup, 1)):
+        step()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with torch.cuda.stream(stream):
-        e0.record(stream)
-        for _ in range(steps):
-            step()
-        e1.record(stream)
+    e0.record(stream)
+    for _ in range(steps):
+        step()
+    e1.record(stream)
     e1.synchronize()
     ms = e0.elapsed_time(e1)
     h2d = sum(t.numel() * t.element_size() for t in (hq_, hk_, hv_))

@@ -45,7 +45,7 @@
 extern "C" {
 #endif
 
-#define DA_ABI_VERSION 1
+#define DA_ABI_VERSION 2
 
 #if defined(__GNUC__)
 #define DA_API __attribute__((visibility("default")))
@@ -243,6 +243,37 @@ DA_API da_status da_forward_paged(const da_plan* plan, const void* q, const void
                                   const int64_t* strides, float softmax_scale, int32_t out_dtype,
                                   void* out, float* lse, void* workspace, int64_t workspace_bytes,
                                   void* cuda_stream);
+
+/*
+ * da_forward_host_bytes - device staging bytes da_forward_host needs for `plan` and a cache of
+ * l_cap tokens: q, K, V, cache_seqlens (with_seqlens != 0), out (out_dtype), lse and the
+ * workspace (DA_COMBINE_KERNEL), each 256-byte aligned, in that order.  Returns -1 when the plan
+ * is invalid, l_cap < plan->l_k or out_dtype is not a da_dtype.  Pure host code.
+ */
+DA_API int64_t da_forward_host_bytes(const da_plan* plan, int32_t l_cap, int32_t with_seqlens,
+                                     int32_t out_dtype);
+
+/*
+ * da_forward_host - da_forward with HOST inputs and outputs, for callers whose KV cache lives
+ * in host memory (the end-to-end path the benchmark's e2e figure times).  All work is
+ * enqueued on cuda_stream in this order: host->device copies of q [B, H_Q, d], k_cache and
+ * v_cache [B, l_cap, H_KV, d] (bf16, contiguous host memory) and cache_seqlens int32 [B]
+ * (NULL = plan->l_k for every b) into device_buffer; the forward (as da_forward with
+ * contiguous strides); device->host copies of out [B, H_Q, d] (out_dtype) and lse fp32
+ * [B, H_Q] (NULL = not copied).  The host outputs are valid once the stream has
+ * synchronised.  Page-locked host memory makes every copy asynchronous; pageable memory
+ * works but then copies synchronously.
+ *   device_buffer, device_buffer_bytes: device scratch of at least
+ *   da_forward_host_bytes(plan, l_cap, cache_seqlens != NULL, out_dtype) bytes, 256-byte
+ *   aligned, owned by the caller and reusable once the stream has passed this call.
+ * Errors: as da_forward; DA_ERR_WORKSPACE when device_buffer is NULL or too small,
+ * DA_ERR_CUDA when a copy cannot be enqueued.
+ */
+DA_API da_status da_forward_host(const da_plan* plan, const void* q, const void* k_cache,
+                                 const void* v_cache, int32_t l_cap, const int32_t* cache_seqlens,
+                                 float softmax_scale, int32_t out_dtype, void* out, float* lse,
+                                 void* device_buffer, int64_t device_buffer_bytes,
+                                 void* cuda_stream);
 
 /*
  * da_combine - LSE-combine of s partials (C-comb):

@@ -15,10 +15,12 @@ missing.
 from . import _lib  # noqa: F401  (raises ImportError if libdecattn.so is missing)
 from ._lib import (DA_BF16, DA_COMBINE_CLUSTER, DA_COMBINE_KERNEL, DA_COMBINE_NONE, DA_F32,  # noqa: F401
                    DA_PATH_MMA, DA_PATH_SCALAR, DA_POLICY_FIXED, DA_POLICY_GUARDED,
-                   DA_POLICY_SEQ_AWARE, DecAttnError, da_abi_version, da_combine, da_forward, da_forward_paged,
-                   da_plan, da_plan_make, da_plan_set_combine, da_status_string)
-from .api import combine, decode_attention, forward, forward_paged, make_plan, workspace_for  # noqa: F401
+                   DA_POLICY_SEQ_AWARE, DecAttnError, da_abi_version, da_combine, da_forward, da_forward_host,
+                   da_forward_host_bytes, da_forward_paged, da_plan, da_plan_make, da_plan_set_combine,
+                   da_status_string)
+from .api import (HostStaging, combine, decode_attention, forward, forward_host, forward_paged,  # noqa: F401
+                  make_plan, workspace_for)
 
-__all__ = ["da_plan_make", "da_plan_set_combine", "da_forward", "da_forward_paged", "da_combine",
-           "da_status_string", "da_abi_version", "make_plan", "forward", "forward_paged", "combine",
-           "decode_attention"]
+__all__ = ["da_plan_make", "da_plan_set_combine", "da_forward", "da_forward_paged", "da_forward_host",
+           "da_forward_host_bytes", "da_combine", "da_status_string", "da_abi_version", "make_plan", "forward",
+           "forward_paged", "forward_host", "HostStaging", "combine", "decode_attention"]

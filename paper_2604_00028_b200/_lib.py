@@ -27,7 +27,7 @@ DA_POLICY_GUARDED, DA_POLICY_SEQ_AWARE, DA_POLICY_FIXED, DA_POLICY_EVOLVED, DA_P
 DA_BF16, DA_F32 = 0, 1
 DA_COMBINE_NONE, DA_COMBINE_CLUSTER, DA_COMBINE_KERNEL = range(3)
 DA_PATH_SCALAR, DA_PATH_MMA = 0, 1
-DA_ABI_VERSION = 1
+DA_ABI_VERSION = 2
 
 POLICIES = {"guarded": DA_POLICY_GUARDED, "seq_aware": DA_POLICY_SEQ_AWARE, "fixed": DA_POLICY_FIXED,
             "evolved": DA_POLICY_EVOLVED, "seq_aware_sm": DA_POLICY_SEQ_AWARE_SM}
@@ -63,7 +63,7 @@ class DecAttnError(RuntimeError):
 def _load() -> ctypes.CDLL:
     if not os.path.exists(LIB_PATH):
         raise ImportError(f"{LIB_PATH} is missing: build it with "
-                          "`python -m paper_2604_00028_b200.build` (no CPU fallback exists)")
+                          "`python paper_2604_00028_b200/build.py` (no CPU fallback exists)")
     lib = ctypes.CDLL(LIB_PATH)
     i32, i64, vp, f32 = ctypes.c_int32, ctypes.c_int64, ctypes.c_void_p, ctypes.c_float
     lib.da_plan_make.argtypes = [i32] * 10 + [ctypes.POINTER(da_plan)]
@@ -76,6 +76,10 @@ def _load() -> ctypes.CDLL:
     lib.da_forward_paged.argtypes = [ctypes.POINTER(da_plan), vp, vp, vp, i32, i32, vp, i64, i32, vp, vp, f32,
                                      i32, vp, vp, vp, i64, vp]
     lib.da_forward_paged.restype = i32
+    lib.da_forward_host_bytes.argtypes = [ctypes.POINTER(da_plan), i32, i32, i32]
+    lib.da_forward_host_bytes.restype = i64
+    lib.da_forward_host.argtypes = [ctypes.POINTER(da_plan), vp, vp, vp, i32, vp, f32, i32, vp, vp, vp, i64, vp]
+    lib.da_forward_host.restype = i32
     lib.da_combine.argtypes = [i32, i32, i32, i32, vp, i64, vp, i64, i32, vp, vp, vp]
     lib.da_combine.restype = i32
     lib.da_status_string.argtypes = [i32]
@@ -89,8 +93,8 @@ def _load() -> ctypes.CDLL:
 
 LIB = _load()
 
-EXPORTED = ("da_plan_make", "da_plan_set_combine", "da_forward", "da_forward_paged", "da_combine",
-            "da_status_string", "da_abi_version")
+EXPORTED = ("da_plan_make", "da_plan_set_combine", "da_forward", "da_forward_paged",
+            "da_forward_host_bytes", "da_forward_host", "da_combine", "da_status_string", "da_abi_version")
 
 
 def da_status_string(status: int) -> str:
@@ -165,6 +169,24 @@ def da_forward_paged(plan: da_plan, q, k_pages, v_pages, num_pages, page_size, b
                               _stream_handle(stream))
     if st != DA_OK:
         raise DecAttnError(st, "da_forward_paged")
+
+
+def da_forward_host_bytes(plan: da_plan, l_cap, with_seqlens, out_dtype) -> int:
+    n = int(LIB.da_forward_host_bytes(ctypes.byref(plan), int(l_cap), int(bool(with_seqlens)), int(out_dtype)))
+    if n < 0:
+        raise DecAttnError(DA_ERR_INVALID_ARG, "da_forward_host_bytes")
+    return n
+
+
+def da_forward_host(plan: da_plan, q, k_cache, v_cache, l_cap, cache_seqlens, softmax_scale, out_dtype,
+                    out, lse, device_buffer, device_buffer_bytes, stream=None) -> None:
+    """Marshal to ``da_forward_host``: q / k_cache / v_cache / cache_seqlens / out / lse are HOST
+    tensors (or host addresses); device_buffer is device scratch."""
+    st = LIB.da_forward_host(ctypes.byref(plan), _ptr(q), _ptr(k_cache), _ptr(v_cache), int(l_cap),
+                             _ptr(cache_seqlens), float(softmax_scale), int(out_dtype), _ptr(out), _ptr(lse),
+                             _ptr(device_buffer), int(device_buffer_bytes), _stream_handle(stream))
+    if st != DA_OK:
+        raise DecAttnError(st, "da_forward_host")
 
 
 def da_combine(num_splits, batch, h_q, head_dim, o_partial, o_split_stride, lse_partial,

@@ -110,6 +110,47 @@ def forward_paged(plan: L.da_plan, q, k_pages, v_pages, block_table, cache_seqle
     return out, lse
 
 
+class HostStaging:
+    """Device scratch for ``forward_host`` (da_forward_host_bytes of the plan), reused across
+    steps; grows when a larger plan needs more."""
+
+    def __init__(self, device=None):
+        self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else device
+        self.buf = None
+
+    def get(self, nbytes: int) -> torch.Tensor:
+        if self.buf is None or self.buf.numel() < nbytes:
+            self.buf = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+        return self.buf
+
+
+def forward_host(plan: L.da_plan, q, k_cache, v_cache, cache_seqlens=None, *, out=None, lse=None,
+                 staging: HostStaging | None = None, softmax_scale=0.0, out_dtype=torch.bfloat16,
+                 stream=None):
+    """Decode attention on HOST tensors via da_forward_host: the H2D copies, the forward and the
+    D2H copies of out / lse are enqueued on ``stream``; out / lse are valid after it synchronises.
+    Pass pinned (page-locked) tensors for asynchronous copies."""
+    for t in (q, k_cache, v_cache, cache_seqlens, out, lse):
+        if t is not None and (t.is_cuda or not t.is_contiguous()):
+            raise ValueError("forward_host takes contiguous host tensors")
+    if q.dtype != torch.bfloat16 or k_cache.dtype != torch.bfloat16 or v_cache.dtype != torch.bfloat16:
+        raise ValueError("q, k_cache, v_cache must be bfloat16")
+    if cache_seqlens is not None and cache_seqlens.dtype != torch.int32:
+        raise ValueError("cache_seqlens must be int32")
+    B, HQ, D = q.shape
+    if out is None:
+        out = torch.empty((B, HQ, D), dtype=out_dtype).pin_memory()
+    if lse is None:
+        lse = torch.empty((B, HQ), dtype=torch.float32).pin_memory()
+    dt = L.DA_F32 if out.dtype == torch.float32 else L.DA_BF16
+    l_cap = k_cache.shape[1]
+    nbytes = L.da_forward_host_bytes(plan, l_cap, cache_seqlens is not None, dt)
+    buf = (staging or HostStaging()).get(nbytes)
+    L.da_forward_host(plan, q, k_cache, v_cache, l_cap, cache_seqlens, softmax_scale, dt, out, lse, buf,
+                      buf.numel(), stream)
+    return out, lse
+
+
 def combine(o_partial, lse_partial, *, out=None, lse=None, out_dtype=torch.bfloat16, stream=None):
     """da_combine over o_partial [s, B, H_Q, d] fp32 and lse_partial [s, B, H_Q] fp32
     (split strides taken from the tensors)."""

@@ -1,4 +1,4 @@
-// C ABI: da_forward / da_combine / da_status_string / da_abi_version
+// C ABI: da_forward / da_forward_paged / da_forward_host / da_combine / da_status_string / da_abi_version
 // (da_plan_make, da_plan_set_combine live in plan.cpp).  See
 // include/decattn.h for the contract of every entry point.
 //
@@ -212,6 +212,81 @@ extern "C" da_status da_forward_paged(const da_plan* plan, const void* q, const 
   pg.num_pages = num_pages;
   return forward_impl(plan, q, k_pages, v_pages, static_cast<int32_t>(cap), cache_seqlens, strides,
                       softmax_scale, out_dtype, out, lse, workspace, workspace_bytes, cuda_stream, pg);
+}
+
+namespace {
+
+// da_forward_host's staging layout in the device buffer (256-byte aligned regions).
+struct HostStaging {
+  int64_t q, k, v, seq, out, lse, ws, total;
+};
+
+inline int64_t align256(int64_t x) { return (x + 255) & ~int64_t(255); }
+
+bool host_staging(const da_plan* plan, int32_t l_cap, bool with_seqlens, int32_t out_dtype,
+                  HostStaging* h) {
+  if (plan == nullptr || check_plan(plan) != DA_OK || l_cap < plan->l_k) return false;
+  if (out_dtype != DA_BF16 && out_dtype != DA_F32) return false;
+  const int64_t B = plan->batch, HQ = plan->h_q, HKV = plan->h_kv, D = kHeadDim;
+  int64_t off = 0;
+  h->q = off;   off = align256(off + B * HQ * D * 2);
+  h->k = off;   off = align256(off + B * int64_t(l_cap) * HKV * D * 2);
+  h->v = off;   off = align256(off + B * int64_t(l_cap) * HKV * D * 2);
+  h->seq = off; off = align256(off + (with_seqlens ? B * 4 : 0));
+  h->out = off; off = align256(off + B * HQ * D * (out_dtype == DA_F32 ? 4 : 2));
+  h->lse = off; off = align256(off + B * HQ * 4);
+  h->ws = off;  off = align256(off + (plan->combine_mode == DA_COMBINE_KERNEL ? plan->workspace_bytes : 0));
+  h->total = off;
+  return true;
+}
+
+}  // namespace
+
+extern "C" int64_t da_forward_host_bytes(const da_plan* plan, int32_t l_cap, int32_t with_seqlens,
+                                         int32_t out_dtype) {
+  HostStaging h;
+  return host_staging(plan, l_cap, with_seqlens != 0, out_dtype, &h) ? h.total : -1;
+}
+
+extern "C" da_status da_forward_host(const da_plan* plan, const void* q, const void* k_cache,
+                                     const void* v_cache, int32_t l_cap, const int32_t* cache_seqlens,
+                                     float softmax_scale, int32_t out_dtype, void* out, float* lse,
+                                     void* device_buffer, int64_t device_buffer_bytes, void* cuda_stream) {
+  if (plan == nullptr || q == nullptr || k_cache == nullptr || v_cache == nullptr || out == nullptr)
+    return DA_ERR_INVALID_ARG;
+  da_status st = check_plan(plan);
+  if (st != DA_OK) return st;
+  HostStaging h;
+  if (!host_staging(plan, l_cap, cache_seqlens != nullptr, out_dtype, &h)) return DA_ERR_INVALID_ARG;
+  if (device_buffer == nullptr || device_buffer_bytes < h.total) return DA_ERR_WORKSPACE;
+  if ((reinterpret_cast<uintptr_t>(device_buffer) & 255u) != 0) return DA_ERR_ALIGNMENT;
+  char* base = static_cast<char*>(device_buffer);
+  cudaStream_t stream = static_cast<cudaStream_t>(cuda_stream);
+  const int64_t B = plan->batch, HQ = plan->h_q, HKV = plan->h_kv, D = kHeadDim;
+  const size_t kv_bytes = size_t(B) * size_t(l_cap) * size_t(HKV * D * 2);
+  if (cudaMemcpyAsync(base + h.q, q, size_t(B * HQ * D * 2), cudaMemcpyHostToDevice, stream) != cudaSuccess ||
+      cudaMemcpyAsync(base + h.k, k_cache, kv_bytes, cudaMemcpyHostToDevice, stream) != cudaSuccess ||
+      cudaMemcpyAsync(base + h.v, v_cache, kv_bytes, cudaMemcpyHostToDevice, stream) != cudaSuccess)
+    return DA_ERR_CUDA;
+  const int32_t* dseq = nullptr;
+  if (cache_seqlens != nullptr) {
+    if (cudaMemcpyAsync(base + h.seq, cache_seqlens, size_t(B * 4), cudaMemcpyHostToDevice, stream) != cudaSuccess)
+      return DA_ERR_CUDA;
+    dseq = reinterpret_cast<const int32_t*>(base + h.seq);
+  }
+  float* dlse = reinterpret_cast<float*>(base + h.lse);
+  const bool kernel_ws = plan->combine_mode == DA_COMBINE_KERNEL;
+  st = forward_impl(plan, base + h.q, base + h.k, base + h.v, l_cap, dseq, nullptr, softmax_scale,
+                    out_dtype, base + h.out, dlse, kernel_ws ? base + h.ws : nullptr,
+                    kernel_ws ? plan->workspace_bytes : 0, cuda_stream, PagedArgs{});
+  if (st != DA_OK) return st;
+  const size_t out_bytes = size_t(B * HQ * D) * (out_dtype == DA_F32 ? 4 : 2);
+  if (cudaMemcpyAsync(out, base + h.out, out_bytes, cudaMemcpyDeviceToHost, stream) != cudaSuccess)
+    return DA_ERR_CUDA;
+  if (lse != nullptr &&
+      cudaMemcpyAsync(lse, dlse, size_t(B * HQ * 4), cudaMemcpyDeviceToHost, stream) != cudaSuccess)
+    return DA_ERR_CUDA;
+  return DA_OK;
 }
 
 extern "C" da_status da_combine(int32_t num_splits, int32_t batch, int32_t h_q, int32_t head_dim,

@@ -253,3 +253,46 @@ def test_forward_paged_validation(L):
     assert st(max_pages_per_seq=10) == L.DA_ERR_INVALID_ARG   # 10 * 64 < l_k = 700
     assert st(block_table=7 * A + 2) == L.DA_ERR_ALIGNMENT
     assert st(q=A + 8) == L.DA_ERR_ALIGNMENT
+    assert st(page_size=(1 << 18) + 64) == L.DA_ERR_UNSUPPORTED   # tiles per page must stay < 2^13
+
+
+def _align256(x):
+    return (x + 255) // 256 * 256
+
+
+@pytest.mark.parametrize("shape,policy,forced", [((1, 64, 8, 512), "seq_aware_sm", 0),
+                                                 ((3, 24, 3, 1500), "fixed", 40),
+                                                 ((2, 8, 1, 100), "guarded", 0)])
+def test_forward_host_bytes_layout(L, shape, policy, forced):
+    b, hq, hkv, lk = shape
+    p = L.da_plan_make(b, hq, hkv, lk, 128, 1, 0, 148, policy, forced)
+    for l_cap, seq, dt in ((lk, 0, L.DA_BF16), (lk + 77, 1, L.DA_F32)):
+        kv = b * l_cap * hkv * 128 * 2
+        want = (_align256(b * hq * 128 * 2) + 2 * _align256(kv) + _align256(4 * b if seq else 0)
+                + _align256(b * hq * 128 * (4 if dt == L.DA_F32 else 2)) + _align256(4 * b * hq)
+                + _align256(p.workspace_bytes if p.combine_mode == L.DA_COMBINE_KERNEL else 0))
+        assert L.da_forward_host_bytes(p, l_cap, seq, dt) == want
+    with pytest.raises(L.DecAttnError):
+        L.da_forward_host_bytes(p, lk - 1, 0, L.DA_BF16)          # l_cap below the plan's length
+    with pytest.raises(L.DecAttnError):
+        L.da_forward_host_bytes(p, lk, 0, 7)                      # not a da_dtype
+
+
+def test_forward_host_validation(L):
+    p = L.da_plan_make(1, 8, 1, 512, 128, 1, 0, 148, "seq_aware", 0)
+    need = L.da_forward_host_bytes(p, 512, 0, L.DA_BF16)
+
+    def st(**kw):
+        args = dict(q=A, k_cache=2 * A, v_cache=3 * A, l_cap=512, cache_seqlens=None, softmax_scale=0.0,
+                    out_dtype=L.DA_BF16, out=4 * A, lse=5 * A, device_buffer=6 * A, device_buffer_bytes=need,
+                    stream=0)
+        args.update(kw)
+        with pytest.raises(L.DecAttnError) as e:
+            L.da_forward_host(p, **args)
+        return e.value.status
+    assert st(q=None) == L.DA_ERR_INVALID_ARG
+    assert st(out=None) == L.DA_ERR_INVALID_ARG
+    assert st(l_cap=100) == L.DA_ERR_INVALID_ARG
+    assert st(device_buffer=None) == L.DA_ERR_WORKSPACE
+    assert st(device_buffer_bytes=need - 1) == L.DA_ERR_WORKSPACE
+    assert st(device_buffer=6 * A + 128) == L.DA_ERR_ALIGNMENT

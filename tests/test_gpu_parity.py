@@ -293,3 +293,32 @@ def test_paged_rejects_unsupported_page_size():
     with pytest.raises(dec.DecAttnError) as e:
         dec.forward_paged(plan, q, kp, kp, table)
     assert e.value.status == dec._lib.DA_ERR_UNSUPPORTED
+
+
+# ---- host-buffer entry point (da_forward_host: H2D + forward + D2H on one stream) -----------
+@pytest.mark.parametrize("batch,h_q,h_kv,l_k,policy,forced,seqlens,f32",
+                         [(1, 64, 8, 512, "seq_aware_sm", 0, False, False),
+                          (3, 24, 3, 1500, "fixed", 40, True, False),     # workspace combine
+                          (2, 8, 1, 700, "seq_aware", 0, True, True),
+                          (1, 8, 8, 130, "guarded", 0, False, False)])    # scalar path
+def test_forward_host_matches_oracle(batch, h_q, h_kv, l_k, policy, forced, seqlens, f32):
+    dec = _dec()
+    inp = synth.make_inputs(batch, h_q, h_kv, l_k, seed=1200, variant="ragged" if seqlens else "normal")
+    q, k, v = (inp[n].contiguous().pin_memory() for n in ("q", "k", "v"))
+    seq = inp["seqlens"].to(torch.int32).pin_memory() if seqlens else None
+    plan = dec.make_plan(batch, h_q, h_kv, l_k, policy=policy, forced_splits=forced)
+    stream = torch.cuda.Stream()
+    staging = dec.HostStaging()
+    out, lse = dec.forward_host(plan, q, k, v, seq, staging=staging, stream=stream,
+                                out_dtype=torch.float32 if f32 else torch.bfloat16)
+    stream.synchronize()
+    assert not out.is_cuda and not lse.is_cuda
+    n = inp["seqlens"] if seqlens else torch.full((batch,), l_k, dtype=torch.int32)
+    ref_o, ref_l = OA.decode_attention(*(synth.to_f64(t) for t in (inp["q"], inp["k"], inp["v"], n)))
+    assert_out_close(synth.to_f64(out), ref_o)
+    assert_lse_close(synth.to_f64(lse), ref_l)
+    # a second call reuses the staging buffer and returns the same bytes
+    out2, lse2 = dec.forward_host(plan, q, k, v, seq, staging=staging, stream=stream,
+                                  out_dtype=torch.float32 if f32 else torch.bfloat16)
+    stream.synchronize()
+    assert torch.equal(out, out2) and torch.equal(lse, lse2)
