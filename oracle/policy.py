@@ -27,11 +27,13 @@ Steps follow the paper's order and notation:
 All comparisons are exact integer cross-multiplications (C-amb-3): there is
 no floating point anywhere in this module.
 
-Two policies beyond the paper's pair: the evolved
+Policies beyond the paper's pair: the evolved
 Python fragment of Fig. 1 as a planner mode, and the SM-count-aware
 generalisation (C-ext-1) whose constants are calibrated on B200 - "parity
 unpinned" by the paper for the latter's constants (its structural properties
-are pinned in tests/test_oracle_policy.py).
+are pinned in tests/test_oracle_policy.py) - and per-batch dynamic split counts
+for ragged batches (C-ext-2, ``dynamic_schedule``; parity unpinned by the paper,
+which names only the metadata role; invariants pinned).
 """
 
 from __future__ import annotations
@@ -43,9 +45,9 @@ EFF_MAX_SPLITS = 128     # efficiency-loop candidate cap (C-amb-2)
 MAX_FORCED_SPLITS = 256  # S:L98 max_splits default
 SPLIT_UNIT = 64          # partition unit in tokens (C-pol item 6)
 
-GUARDED, SEQ_AWARE, FIXED, EVOLVED, SEQ_AWARE_SM = 0, 1, 2, 3, 4
+GUARDED, SEQ_AWARE, FIXED, EVOLVED, SEQ_AWARE_SM, DYNAMIC = 0, 1, 2, 3, 4, 5
 POLICY_NAMES = {"guarded": GUARDED, "seq_aware": SEQ_AWARE, "fixed": FIXED, "evolved": EVOLVED,
-                "seq_aware_sm": SEQ_AWARE_SM}
+                "seq_aware_sm": SEQ_AWARE_SM, "dynamic": DYNAMIC}
 
 # Which step of the cascade decided s (mirrors SPEC's SplitDecision.source).
 RULE_SATURATED = 0
@@ -59,6 +61,7 @@ RULE_EVOLVED = 7      # Fig. 1 fragment
 RULE_SM_SHORT = 8     # SM-count-aware generalisation: too few 64-token units to split
 RULE_SM_SPLIT = 9     # SM-count-aware generalisation: split count from units, tiles and SMs
 RULE_SM_FIT = 10      # SM-count-aware generalisation: efficiency-loop split moved to one wave
+RULE_DYNAMIC = 11     # per-batch split counts from the lengths on the device (dynamic_schedule)
 
 # SM-count-aware generalisation of the sequence-aware rule (DESIGN.md §3,
 # C-ext-1).  The paper leaves "extending the benefit to lower L_K values and learning more
@@ -82,6 +85,8 @@ SM_STREAM_UNITS = 16  # efficiency region: cap to the one-wave cluster split whi
 # scripts/microbench_cluster16.cu); index 0 unused, index 1 = one CTA per SM.  Scaled by U / 148.
 CLUSTER_FIT_B200 = (0, 148, 74, 45, 33, 26, 22, 15, 15, 15, 11, 7, 7, 7, 7, 7, 7)
 CLUSTER_MAX_SPLITS = 16
+# Per-batch dynamic split counts (the scheduler-metadata role of P:L125):
+DYN_MAX_SPLITS = 128  # per-sequence cap (the efficiency loop's candidate cap, C-amb-2)
 
 def ceil_div(a: int, b: int) -> int:
     return -(-a // b)
@@ -212,6 +217,40 @@ def seq_aware_sm_splits(geo: dict, l_k: int):
     return s, (RULE_EFF_LOOP if s == e else RULE_SM_FIT)
 
 
+def dynamic_cap(l_k: int) -> int:
+    """DA_POLICY_DYNAMIC's per-sequence split cap: no more splits than 64-token units of the
+    longest sequence, and at most DYN_MAX_SPLITS."""
+    return max(1, min(DYN_MAX_SPLITS, ceil_div(l_k, SPLIT_UNIT)))
+
+
+def dynamic_slots(batch: int, tiles_per_batch: int, U: int, s_cap: int) -> int:
+    """Slots (split CTAs per head group) a dynamic launch provides: enough for any lengths,
+    because s_b <= n_u_b / W, or s_b = 1 where that rounds to 0, so sum_b s_b <=
+    sum_b n_u_b / W + batch <= U / tiles_per_batch + batch."""
+    return min(batch * s_cap, ceil_div(U, tiles_per_batch) + batch)
+
+
+def dynamic_schedule(seqlens, tiles_per_batch: int, U: int, s_cap: int):
+    """Per-batch split counts for one ragged batch, in this order:
+      n_u_b = ceil(n_b / 64)                      (units of each sequence, n_b already clamped)
+      W     = max(1, ceil(sum_b n_u_b * tiles_per_batch / U))   (units per CTA for one wave)
+      s_b   = min(s_cap, max(1, floor(n_u_b / W)))
+      P_b   = s_0 + ... + s_{b-1}                 (first slot of sequence b)
+    Sequence b then uses the standard partition (``partition``) with s_b splits.  Rounding s_b
+    down keeps sum_b s_b * tiles_per_batch <= U except where a short sequence is lifted to one
+    split: a single sequence never spills into a second wave (ceil would give 19 x 8 = 152 CTAs
+    on 148 SMs at L_K = 131072, H_KV = 8), and a long sequence in a batch of short ones gets
+    proportionally more splits.  Returns (W, s, P)."""
+    n_u = [ceil_div(int(n), SPLIT_UNIT) for n in seqlens]
+    W = max(1, ceil_div(sum(n_u) * tiles_per_batch, U))
+    s = [min(s_cap, max(1, u // W)) for u in n_u]
+    P, acc = [], 0
+    for v in s:
+        P.append(acc)
+        acc += v
+    return W, s, P
+
+
 def evolved_policy_splits(geo: dict, batch: int, l_k: int):
     """Fig. 1 as a policy: batch == 1 -> s = 12, or 16 when L_K < 256 (literal,
     no clamp: s > nblk gives empty splits, as in the paper's s = 1..64 sweep).  The
@@ -241,6 +280,8 @@ def num_splits(batch: int, h_q: int, h_kv: int, l_k: int, num_sms: int, sm_margi
         return evolved_policy_splits(geo, batch, l_k)
     if policy == SEQ_AWARE_SM:
         return seq_aware_sm_splits(geo, l_k)
+    if policy == DYNAMIC:                 # the cap; the per-batch counts come from dynamic_schedule
+        return dynamic_cap(l_k), RULE_DYNAMIC
     raise ValueError("unknown policy")
 
 

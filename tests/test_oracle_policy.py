@@ -319,3 +319,42 @@ def test_seq_aware_sm_calibration():
         assert t[s] <= 1.06 * min(t.values()), (b, hkv, lk, s)
         if g in t:
             assert t[s] <= 1.01 * t[g], (b, hkv, lk, s, g)
+
+
+# ---- per-batch dynamic split counts (C-ext-2) -----------------------------------
+def test_dynamic_schedule_examples():
+    # hand-computed: one 32768-token sequence among fifteen 1024-token ones, 8 tiles per sequence:
+    # units 512 + 15 x 16 = 752; W = ceil(752 * 8 / 148) = ceil(40.6) = 41; 512 // 41 = 12; 16 // 41 = 0 -> 1
+    W, s, P_ = P.dynamic_schedule([32768] + [1024] * 15, 8, 148, 128)
+    assert (W, s[0], s[1:]) == (41, 12, [1] * 15)
+    assert P_[:3] == [0, 12, 13] and P_[-1] == 26
+    # a single long sequence stays inside one wave: W = ceil(2048 * 8 / 148) = 111, 2048 // 111 = 18
+    assert P.dynamic_schedule([131072], 8, 148, 128) == (111, [18], [0])          # 144 CTAs <= 148
+    # T = 1: W = ceil(2048 / 148) = 14, 2048 // 14 = 146 -> the cap 128
+    assert P.dynamic_schedule([131072], 1, 148, 128) == (14, [128], [0])
+    # empty and one-token sequences still own one split (o = 0 / the single key)
+    assert P.dynamic_schedule([0, 1, 64, 65], 1, 148, 2) == (1, [1, 1, 1, 2], [0, 1, 2, 3])
+    assert P.num_splits(3, 24, 3, 700, B200_SMS, 0, "dynamic") == (11, P.RULE_DYNAMIC)   # cap ceil(700/64)
+
+
+def test_dynamic_schedule_invariants():
+    rng = random.Random(11)
+    for _ in range(3000):
+        B = rng.randint(1, 70)
+        U = rng.choice([148, 132, 16, 3])
+        tiles = rng.choice([1, 2, 8, 32])
+        l_cap = rng.choice([64, 500, 4096, 131072])
+        cap = P.dynamic_cap(l_cap)
+        lens = [rng.choice([0, 1, rng.randint(0, l_cap), l_cap]) for _ in range(B)]
+        W, s, P_ = P.dynamic_schedule(lens, tiles, U, cap)
+        units = [-(-n // 64) for n in lens]
+        assert W == max(1, -(-sum(units) * tiles // U))
+        assert P_ == [sum(s[:b]) for b in range(B)]
+        assert sum(s) <= P.dynamic_slots(B, tiles, U, cap)          # the launch always has the slots
+        lifted = sum(1 for u in units if u < W)
+        assert sum(s) * tiles <= U + lifted * tiles                   # one wave, except lifted short ones
+        for u, v in zip(units, s):
+            assert 1 <= v <= cap
+            if v < cap and u >= W:
+                assert u < (v + 1) * W                               # each split holds < 2 W units
+                assert v * W <= u
