@@ -78,7 +78,7 @@ typedef enum da_policy {
   DA_POLICY_FIXED = 2,      /* s = forced_splits (the U-curve sweep) */
   DA_POLICY_EVOLVED = 3,    /* Fig. 1: batch == 1 -> 12 (16 when
                                L_K < 256); batch != 1 -> guarded            */
-  DA_POLICY_SEQ_AWARE_SM = 4 /* SM-count-aware generalisation (DESIGN.md
+  DA_POLICY_SEQ_AWARE_SM = 4,/* SM-count-aware generalisation (DESIGN.md
                                C-ext-1), n_u = ceil(L_K/64),
                                f = largest s <= 16 whose T clusters fit one
                                wave: nblk <= 4 -> min(n_u, T <= 4 ? 8 : 4, f)
@@ -87,6 +87,13 @@ typedef enum da_policy {
                                min(8, n_u, f) when e <= f, or moved to f when
                                e > f >= 2 and (n_u <= 16 f or 2 T f >= U);
                                B200-calibrated                              */
+  DA_POLICY_DYNAMIC = 5     /* per-batch split counts from cache_seqlens on the
+                               device (DESIGN.md C-ext-2):
+                               W = max(1, ceil(sum_b ceil(n_b/64) * T_b / U)),
+                               s_b = min(cap, max(1, floor(ceil(n_b/64) / W)))
+                               with T_b = H_KV * num_m_blocks and cap =
+                               min(128, ceil(L_K/64)) (= plan->num_splits);
+                               always the workspace combine              */
 } da_policy;
 
 /* Which step of the cascade decided num_splits (SPEC's "source"). */
@@ -101,8 +108,10 @@ typedef enum da_rule {
   DA_RULE_EVOLVED = 7,      /* DA_POLICY_EVOLVED, batch == 1      */
   DA_RULE_SM_SHORT = 8,     /* DA_POLICY_SEQ_AWARE_SM: too few 64-token units */
   DA_RULE_SM_SPLIT = 9,     /* DA_POLICY_SEQ_AWARE_SM: nblk <= 4 split        */
-  DA_RULE_SM_FIT = 10       /* DA_POLICY_SEQ_AWARE_SM: nblk >= 5, the loop's
+  DA_RULE_SM_FIT = 10,      /* DA_POLICY_SEQ_AWARE_SM: nblk >= 5, the loop's
                                split moved to a one-wave cluster split      */
+  DA_RULE_DYNAMIC = 11      /* DA_POLICY_DYNAMIC: num_splits is the cap, the
+                               counts are decided per batch on the device   */
 } da_rule;
 
 /* Element types of outputs. */
@@ -147,14 +156,18 @@ typedef struct da_plan {
   int32_t path;            /* da_path                                          */
   int32_t rows_per_cta;    /* query rows one CTA computes (1, 8 or 16)         */
   int32_t combine_mode;    /* da_combine_mode                                  */
-  int32_t grid_x;          /* = num_splits                                     */
+  int32_t grid_x;          /* = num_splits; DA_POLICY_DYNAMIC: split slots,
+                              min(B * cap, ceil(U / T_b) + B)                */
   int32_t grid_y;          /* MMA: h_kv * ceil(G / rows_per_cta); SCALAR: h_q  */
-  int32_t grid_z;          /* = batch                                          */
+  int32_t grid_z;          /* = batch; DA_POLICY_DYNAMIC: 1                    */
   int32_t block_threads;   /* threads per CTA                                  */
   int32_t cluster_x;       /* CTAs per cluster along x (s in CLUSTER mode)     */
   int32_t smem_bytes;      /* dynamic shared memory per CTA                    */
   int64_t workspace_bytes; /* s * batch * h_q * (head_dim + 1) * 4 when s > 1,
-                              else 0.  Only DA_COMBINE_KERNEL reads/writes it. */
+                              else 0.  Only DA_COMBINE_KERNEL reads/writes it.
+                              DA_POLICY_DYNAMIC: grid_x * h_q * (head_dim + 1)
+                              * 4 + 8 * batch (partials per slot, then the
+                              schedule: first slot and split count per b)  */
 } da_plan;
 
 /*

@@ -20,22 +20,23 @@ LIB_PATH = os.environ.get("DECATTN_LIB") or os.path.join(PKG_DIR, "lib", "libdec
 
 # ---- constants mirrored from include/decattn.h ----------------------------
 DA_OK, DA_ERR_INVALID_ARG, DA_ERR_UNSUPPORTED, DA_ERR_ALIGNMENT, DA_ERR_WORKSPACE, DA_ERR_CUDA = range(6)
-DA_POLICY_GUARDED, DA_POLICY_SEQ_AWARE, DA_POLICY_FIXED, DA_POLICY_EVOLVED, DA_POLICY_SEQ_AWARE_SM = range(5)
+(DA_POLICY_GUARDED, DA_POLICY_SEQ_AWARE, DA_POLICY_FIXED, DA_POLICY_EVOLVED, DA_POLICY_SEQ_AWARE_SM,
+ DA_POLICY_DYNAMIC) = range(6)
 (DA_RULE_SATURATED, DA_RULE_GUARD_NBLK4, DA_RULE_GUARD1, DA_RULE_GUARD2, DA_RULE_LOW_TILE,
  DA_RULE_EFF_LOOP, DA_RULE_FORCED, DA_RULE_EVOLVED, DA_RULE_SM_SHORT, DA_RULE_SM_SPLIT,
- DA_RULE_SM_FIT) = range(11)
+ DA_RULE_SM_FIT, DA_RULE_DYNAMIC) = range(12)
 DA_BF16, DA_F32 = 0, 1
 DA_COMBINE_NONE, DA_COMBINE_CLUSTER, DA_COMBINE_KERNEL = range(3)
 DA_PATH_SCALAR, DA_PATH_MMA = 0, 1
 DA_ABI_VERSION = 2
 
 POLICIES = {"guarded": DA_POLICY_GUARDED, "seq_aware": DA_POLICY_SEQ_AWARE, "fixed": DA_POLICY_FIXED,
-            "evolved": DA_POLICY_EVOLVED, "seq_aware_sm": DA_POLICY_SEQ_AWARE_SM}
+            "evolved": DA_POLICY_EVOLVED, "seq_aware_sm": DA_POLICY_SEQ_AWARE_SM, "dynamic": DA_POLICY_DYNAMIC}
 RULE_NAMES = {DA_RULE_SATURATED: "saturated", DA_RULE_GUARD_NBLK4: "guard_nblk4",
               DA_RULE_GUARD1: "guard1", DA_RULE_GUARD2: "guard2", DA_RULE_LOW_TILE: "low_tile",
               DA_RULE_EFF_LOOP: "efficiency_loop", DA_RULE_FORCED: "forced", DA_RULE_EVOLVED: "evolved",
               DA_RULE_SM_SHORT: "sm_short", DA_RULE_SM_SPLIT: "sm_split",
-              DA_RULE_SM_FIT: "sm_fit"}
+              DA_RULE_SM_FIT: "sm_fit", DA_RULE_DYNAMIC: "dynamic"}
 
 
 class da_plan(ctypes.Structure):

@@ -125,11 +125,16 @@ da_status forward_impl(const da_plan* plan, const void* q, const void* k_cache, 
 
   float* ws_o = nullptr;
   float* ws_lse = nullptr;
+  int32_t* ws_meta = nullptr;
+  const bool dyn = is_dynamic(*plan);
+  // partial rows: static [s][B][H_Q]; dynamic [slot][H_Q] then the schedule [2][B] int32
+  const int64_t prows = dyn ? int64_t(plan->grid_x) * HQ : int64_t(plan->num_splits) * B * HQ;
   if (plan->combine_mode == DA_COMBINE_KERNEL) {
     if (workspace == nullptr || workspace_bytes < plan->workspace_bytes) return DA_ERR_WORKSPACE;
     if (!aligned16(workspace)) return DA_ERR_ALIGNMENT;
     ws_o = static_cast<float*>(workspace);
-    ws_lse = ws_o + int64_t(plan->num_splits) * B * HQ * D;
+    ws_lse = ws_o + prows * D;
+    if (dyn) ws_meta = reinterpret_cast<int32_t*>(ws_lse + prows);
   }
 
   CUtensorMap tk, tv;
@@ -163,15 +168,21 @@ da_status forward_impl(const da_plan* plan, const void* q, const void* k_cache, 
   p.bt_stride = pg.bt_stride;
   p.page_size = pg.page_size;
   p.page_magic = pg.page_size > 0 ? div_magic(static_cast<uint32_t>(pg.page_size / kTileN)) : 0;
+  p.dyn_tiles = plan->h_kv * plan->num_m_blocks;
+  p.dyn_u = plan->usable_sms;
+  p.ws_meta = ws_meta;
 
   cudaStream_t stream = static_cast<cudaStream_t>(cuda_stream);
   if (launch_split_kv_fwd(*plan, tk, tv, p, stream) != cudaSuccess) return DA_ERR_CUDA;
   if (plan->combine_mode == DA_COMBINE_KERNEL) {
     CombineParams c{};
     c.o = ws_o;
-    c.o_stride = B * HQ * D;
+    c.o_stride = dyn ? HQ * D : B * HQ * D;   // dynamic: consecutive slots of one sequence
     c.lse_in = ws_lse;
-    c.lse_stride = B * HQ;
+    c.lse_stride = dyn ? HQ : B * HQ;
+    c.meta = ws_meta;
+    c.h_q = static_cast<int32_t>(HQ);
+    c.batch = static_cast<int32_t>(B);
     c.num_splits = plan->num_splits;
     c.rows = static_cast<int32_t>(B * HQ);
     c.out = out;

@@ -55,10 +55,16 @@ __global__ void __launch_bounds__(kCombineThreads)
   __shared__ float s_m[kWarps], s_l[kWarps];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int row = blockIdx.x;
-  const int s = p.num_splits;
+  int s = p.num_splits;
+  int64_t prow = row;                  // partial row of split 0
+  if (p.meta != nullptr) {             // DA_POLICY_DYNAMIC: row (b, h) merges slots P_b .. P_b + s_b - 1
+    const int b = row / p.h_q, h = row - b * p.h_q;
+    prow = static_cast<int64_t>(__ldg(p.meta + b)) * p.h_q + h;
+    s = __ldg(p.meta + p.batch + b);
+  }
   DA_DASSERT(row < p.rows && s >= 1);
-  const float* lse_in = p.lse_in + row;
-  const float4* o = reinterpret_cast<const float4*>(p.o + static_cast<int64_t>(row) * kHeadDim) + lane;
+  const float* lse_in = p.lse_in + prow;
+  const float4* o = reinterpret_cast<const float4*>(p.o + prow * kHeadDim) + lane;
   const int64_t ostride4 = p.o_stride / 4;
 
   // (1) warp w merges splits w, w + 4, ...: the lse and o loads of 8 splits are issued together

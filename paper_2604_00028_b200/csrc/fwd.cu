@@ -145,9 +145,12 @@ __device__ __forceinline__ void mma_tile(uint32_t sK, uint32_t sV, int valid,
       }
     }
 
-  // P = exp2(S - m); pack to bf16 and transpose each 8x8 block so P^T's C layout
-  // becomes the B-operand layout of the PV product.
-  uint32_t pb[4][NB][2];
+  // P = exp2(S - m) as an unevaluated sum of two bf16 terms, P = P_hi + P_lo with
+  // P_hi = bf16(P) and P_lo = bf16(P - P_hi): the PV product then carries ~16 mantissa bits
+  // of P instead of 8 (a single bf16 P is off by up to 2^-9 relative per weight, which short
+  // sequences with cancelling V rows turn into > 2e-3 absolute error).  Each 8x8 block is
+  // transposed so P^T's C layout becomes the B-operand layout of the PV product.
+  uint32_t pb[4][NB][2], pl[4][NB][2];
 #pragma unroll
   for (int j = 0; j < 4; ++j)
 #pragma unroll
@@ -158,8 +161,11 @@ __device__ __forceinline__ void mma_tile(uint32_t sK, uint32_t sV, int valid,
         p[c] = ex2(s[j][nb][c] - m[nb][c & 1]);         // masked: exp2(-inf) = 0
         l[nb][c & 1] += p[c];
       }
-      pb[j][nb][0] = movmatrix_trans(pack_bf16(p[0], p[1]));
-      pb[j][nb][1] = movmatrix_trans(pack_bf16(p[2], p[3]));
+      const uint32_t h01 = pack_bf16(p[0], p[1]), h23 = pack_bf16(p[2], p[3]);
+      pb[j][nb][0] = movmatrix_trans(h01);
+      pb[j][nb][1] = movmatrix_trans(h23);
+      pl[j][nb][0] = movmatrix_trans(pack_bf16(p[0] - bf16lo(h01), p[1] - bf16hi(h01)));
+      pl[j][nb][1] = movmatrix_trans(pack_bf16(p[2] - bf16lo(h23), p[3] - bf16hi(h23)));
     }
 
   // ---- O^T[d, g] += sum_token V^T[d, token] P^T[token, g]   (8 d-blocks x 4 token blocks)
@@ -176,7 +182,10 @@ __device__ __forceinline__ void mma_tile(uint32_t sK, uint32_t sV, int valid,
         uint32_t a0, a1, a2, a3;
         ldmatrix_x4_trans(base + j * 16 * 128, a0, a1, a2, a3);
 #pragma unroll
-        for (int nb = 0; nb < NB; ++nb) mma_bf16_16816(o[i][nb], a0, a1, a2, a3, pb[j][nb][0], pb[j][nb][1]);
+        for (int nb = 0; nb < NB; ++nb) {
+          mma_bf16_16816(o[i][nb], a0, a1, a2, a3, pb[j][nb][0], pb[j][nb][1]);
+          mma_bf16_16816(o[i][nb], a0, a1, a2, a3, pl[j][nb][0], pl[j][nb][1]);
+        }
       }
     }
   }
@@ -275,16 +284,76 @@ __device__ __forceinline__ void split_range(int n, int split, int s, uint64_t s_
   n_tiles = static_cast<int>(u1 - u0);
 }
 
+// DA_POLICY_DYNAMIC (C-ext-2, oracle/policy.py dynamic_schedule): one warp derives the per-batch
+// split counts from the lengths - W = max(1, ceil(sum_b n_u_b * T_b / U)), s_b = min(cap,
+// max(1, floor(n_u_b / W))), first slot P_b = s_0 + ... + s_{b-1} - and returns the (sequence,
+// split, s_b, length) that split slot `slot` serves, or x = -1 for an unused slot.  Every CTA
+// runs the same integer arithmetic; the CTA of slot 0, head group 0 records (P_b, s_b) for the
+// combine kernel.
+__device__ __forceinline__ int dyn_len(const FwdParams& p, int b) {
+  return min(max(p.seqlens != nullptr ? __ldg(p.seqlens + b) : p.l_default, 0), p.l_cap);
+}
+
+__device__ __noinline__ int4 dyn_schedule(const FwdParams& p, uint32_t slot, bool record, int lane) {
+  const int B = p.batch;
+  uint32_t tot = 0;
+  for (int b0 = 0; b0 < B; b0 += 32) {
+    const int bb = b0 + lane;
+    if (bb < B) tot += (static_cast<uint32_t>(dyn_len(p, bb)) + (kTileN - 1)) / kTileN;
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, off);
+  const uint64_t num = static_cast<uint64_t>(tot) * static_cast<uint32_t>(p.dyn_tiles);
+  const uint64_t Wl = (num + static_cast<uint32_t>(p.dyn_u) - 1) / static_cast<uint32_t>(p.dyn_u);
+  const uint32_t W = Wl < 1 ? 1u : static_cast<uint32_t>(Wl);
+  const uint32_t cap = static_cast<uint32_t>(p.num_splits);
+  int4 mine = make_int4(-1, 0, 0, 0);
+  uint32_t base = 0;
+  for (int b0 = 0; b0 < B; b0 += 32) {
+    const int bb = b0 + lane;
+    int n = 0;
+    uint32_t sb = 0;
+    if (bb < B) {
+      n = dyn_len(p, bb);
+      sb = min(max(((static_cast<uint32_t>(n) + (kTileN - 1)) / kTileN) / W, 1u), cap);
+    }
+    uint32_t inc = sb;                                  // inclusive warp scan of s_b
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const uint32_t v = __shfl_up_sync(0xffffffffu, inc, off);
+      if (lane >= off) inc += v;
+    }
+    const uint32_t first = base + inc - sb;
+    if (bb < B) {
+      if (record) {
+        p.ws_meta[bb] = static_cast<int32_t>(first);
+        p.ws_meta[B + bb] = static_cast<int32_t>(sb);
+      }
+      if (slot >= first && slot < first + sb) mine = make_int4(bb, static_cast<int>(slot - first), static_cast<int>(sb), n);
+    }
+    base += __shfl_sync(0xffffffffu, inc, 31);
+  }
+  const unsigned hit = __ballot_sync(0xffffffffu, mine.x >= 0);   // at most one lane matches
+  const int src = hit ? __ffs(hit) - 1 : 0;
+  int4 r;
+  r.x = hit ? __shfl_sync(0xffffffffu, mine.x, src) : -1;
+  r.y = __shfl_sync(0xffffffffu, mine.y, src);
+  r.z = __shfl_sync(0xffffffffu, mine.z, src);
+  r.w = __shfl_sync(0xffffffffu, mine.w, src);
+  return r;
+}
+
 // ---------------------------------------------------------------------------
 // The kernel.  kPath: DA_PATH_SCALAR / DA_PATH_MMA; kNB: g-blocks of 8 query
 // rows (MMA path); kCombine: da_combine_mode; NS: ring stages; NW: consumer warps
 // (NS a multiple of NW: warp w owns stages w, w + NW, ... and consumes them in order).
 // ---------------------------------------------------------------------------
-template <int kPath, int kNB, int kCombine, int NS, int NW>
+template <int kPath, int kNB, int kCombine, int NS, int NW, bool kDyn>
 __global__ void __launch_bounds__(threads_for(NW, helpers_for(kCombine)), 1)
     split_kv_fwd_kernel(const __grid_constant__ CUtensorMap tmap_k,
                         const __grid_constant__ CUtensorMap tmap_v, const FwdParams p) {
   static_assert(NS % NW == 0, "each consumer warp must own whole ring stages");
+  static_assert(!kDyn || kCombine == DA_COMBINE_KERNEL, "dynamic split counts use the workspace combine");
   constexpr int kT = threads_for(NW, helpers_for(kCombine));   // consumers + producer + helpers
   constexpr int R = kPath == DA_PATH_MMA ? 8 * kNB : 1;    // query rows of this CTA
   constexpr int kIters = (R * 32 + kT - 1) / kT;           // merge passes: element = (row, float4)
@@ -305,7 +374,7 @@ __global__ void __launch_bounds__(threads_for(NW, helpers_for(kCombine)), 1)
   float* const slots = epi + NS * kStageBytes / 4;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int split = blockIdx.x, b = blockIdx.z;
+  int split = blockIdx.x, b = blockIdx.z;       // kDyn: assigned from the schedule below
   int kvh, hq0, rows_valid;
   if constexpr (kPath == DA_PATH_MMA) {
     kvh = blockIdx.y / p.mblocks_per_head;
@@ -349,7 +418,7 @@ __global__ void __launch_bounds__(threads_for(NW, helpers_for(kCombine)), 1)
     prefetch_tmap(&tmap_v);
     // the lengths are read right after griddepcontrol.wait: pull their line into L2 now (a
     // prefetch never returns data, so it cannot observe a stale value)
-    if (p.seqlens != nullptr) prefetch_l2(p.seqlens + b);
+    if (!kDyn && p.seqlens != nullptr) prefetch_l2(p.seqlens + b);
   }
   __syncthreads();
   if constexpr (kCluster) cluster_arrive_relaxed();   // "my push barrier is initialised"
@@ -368,8 +437,29 @@ __global__ void __launch_bounds__(threads_for(NW, helpers_for(kCombine)), 1)
 #endif
   // ---- this split's token range (C-pol item 6), in units of kTileN tokens
   int t0, t_end, n_tiles;
-  split_range(min(max(p.seqlens != nullptr ? __ldg(p.seqlens + b) : p.l_default, 0), p.l_cap), split,
-              p.num_splits, p.s_magic, t0, t_end, n_tiles);
+  if constexpr (kDyn) {
+    __shared__ int4 sched;
+    if (warp == 0) {
+      const int4 r = dyn_schedule(p, blockIdx.x, blockIdx.x == 0 && blockIdx.y == 0 && p.ws_meta != nullptr,
+                                  lane);
+      if (lane == 0) sched = r;
+    }
+    __syncthreads();
+    const int4 r = sched;
+    if (r.x < 0) return;                          // unused slot (the launch provides an upper bound)
+    b = r.x;
+    split = r.y;
+    // split r.y of r.z over n = r.w tokens; (split + 1) n_u < 2^32 since r.z <= 128, n_u < 2^25
+    const uint32_t nu = (static_cast<uint32_t>(r.w) + (kTileN - 1)) / kTileN;
+    const uint32_t u0 = static_cast<uint32_t>(r.y) * nu / static_cast<uint32_t>(r.z);
+    const uint32_t u1 = static_cast<uint32_t>(r.y + 1) * nu / static_cast<uint32_t>(r.z);
+    t0 = static_cast<int>(u0) * kTileN;
+    t_end = min(static_cast<int>(u1) * kTileN, r.w);
+    n_tiles = static_cast<int>(u1 - u0);
+  } else {
+    split_range(min(max(p.seqlens != nullptr ? __ldg(p.seqlens + b) : p.l_default, 0), p.l_cap), split,
+                p.num_splits, p.s_magic, t0, t_end, n_tiles);
+  }
 
   if (warp == NW) {
     // ================= TMA producer =================
@@ -590,9 +680,11 @@ __global__ void __launch_bounds__(threads_for(NW, helpers_for(kCombine)), 1)
       if constexpr (kCombine == DA_COMBINE_NONE) {
         store_out(p, row, d4, v);
         if (d4 == 0 && p.lse != nullptr) p.lse[row] = lse_v;
-      } else {  // DA_COMBINE_KERNEL: normalised partial o_i, lse_i (C-part)
-        const size_t prow = static_cast<size_t>(split) * p.batch * p.h_q + row;
-        DA_DASSERT(prow < static_cast<size_t>(p.num_splits) * p.batch * p.h_q);
+      } else {  // DA_COMBINE_KERNEL: normalised partial o_i, lse_i (C-part); kDyn: slot-major rows
+        const size_t prow = kDyn ? static_cast<size_t>(blockIdx.x) * p.h_q + hq0 + g
+                                 : static_cast<size_t>(split) * p.batch * p.h_q + row;
+        DA_DASSERT(prow < (kDyn ? static_cast<size_t>(gridDim.x) * p.h_q
+                                : static_cast<size_t>(p.num_splits) * p.batch * p.h_q));
         reinterpret_cast<float4*>(p.ws_o)[prow * (kHeadDim / 4) + d4] = v;
         if (d4 == 0) p.ws_lse[prow] = lse_v;
       }
@@ -672,14 +764,14 @@ __global__ void __launch_bounds__(threads_for(NW, helpers_for(kCombine)), 1)
 #endif
 }
 
-template <int kPath, int kNB, int kCombine>
+template <int kPath, int kNB, int kCombine, bool kDyn = false>
 cudaError_t launch_impl(const da_plan& plan, const CUtensorMap& tk, const CUtensorMap& tv,
                         const FwdParams& p, cudaStream_t stream) {
   constexpr bool kCluster = kCombine == DA_COMBINE_CLUSTER;
   constexpr int NS = stages_for(kCombine);
   constexpr int NW = warps_for(kCombine);
   constexpr int kSmem = smem_for(NS, kCluster);
-  auto kern = split_kv_fwd_kernel<kPath, kNB, kCombine, NS, NW>;
+  auto kern = split_kv_fwd_kernel<kPath, kNB, kCombine, NS, NW, kDyn>;
   // One-time (per device) opt-in to > 48 KB of dynamic shared memory.
   static std::atomic<uint64_t> attr_done{0};
   int dev = 0;
@@ -723,7 +815,9 @@ cudaError_t dispatch_combine(const da_plan& plan, const CUtensorMap& tk, const C
   switch (plan.combine_mode) {
     case DA_COMBINE_NONE: return launch_impl<kPath, kNB, DA_COMBINE_NONE>(plan, tk, tv, p, stream);
     case DA_COMBINE_CLUSTER: return launch_impl<kPath, kNB, DA_COMBINE_CLUSTER>(plan, tk, tv, p, stream);
-    default: return launch_impl<kPath, kNB, DA_COMBINE_KERNEL>(plan, tk, tv, p, stream);
+    default:
+      if (is_dynamic(plan)) return launch_impl<kPath, kNB, DA_COMBINE_KERNEL, true>(plan, tk, tv, p, stream);
+      return launch_impl<kPath, kNB, DA_COMBINE_KERNEL>(plan, tk, tv, p, stream);
   }
 }
 

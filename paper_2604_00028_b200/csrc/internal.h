@@ -34,6 +34,11 @@ struct FwdParams {
   int64_t bt_stride;
   int32_t page_size;            // tokens per page, a multiple of kTileN, <= kMaxPageSize
   uint64_t page_magic;          // ceil(2^38 / (page_size / kTileN))
+  // DA_POLICY_DYNAMIC (C-ext-2): blockIdx.x is a split slot; the (sequence, split) it serves is
+  // decided on the device from the lengths.  ws_meta[b] / ws_meta[B + b] receive the schedule.
+  int32_t dyn_tiles;            // T_b = H_KV * num_m_blocks
+  int32_t dyn_u;                // usable SMs U
+  int32_t* ws_meta;             // [2, B] int32 (first slot, split count) or nullptr
 };
 
 // Division by a launch-invariant divisor d without an integer divide: with m = ceil(2^38 / d),
@@ -51,10 +56,16 @@ struct CombineParams {
   void* out;
   int32_t out_f32;
   float* lse;               // [rows] or nullptr
+  // DA_POLICY_DYNAMIC: row r = (b, h) merges meta[B + b] splits starting at slot meta[b]; the
+  // partial of slot j sits at o + (j * h_q + h) * d (o_stride / lse_stride give the slot stride)
+  const int32_t* meta;      // [2, B] or nullptr (uniform: num_splits at o + i * o_stride)
+  int32_t h_q;
+  int32_t batch;
 };
 
 // plan.cpp
 void derive_launch(da_plan* p);
+bool is_dynamic(const da_plan& p);
 bool combine_mode_valid(int mode, int s);
 
 // fwd.cu

@@ -57,6 +57,13 @@ int64_t cluster_fit_splits(int64_t T, int64_t U) {
 void decide(int64_t batch, int64_t l_k, int64_t T, int64_t U, int64_t nblk, int policy, int forced,
             int* s, int* rule) {
   if (policy == DA_POLICY_FIXED) { *s = forced; *rule = DA_RULE_FORCED; return; }
+  if (policy == DA_POLICY_DYNAMIC) {          // C-ext-2: the cap; counts are decided per batch on the device
+    int64_t cap = ceil_div(l_k, kSplitUnit);
+    if (cap > kDynMaxSplits) cap = kDynMaxSplits;
+    *s = static_cast<int>(cap < 1 ? 1 : cap);
+    *rule = DA_RULE_DYNAMIC;
+    return;
+  }
   if (policy == DA_POLICY_EVOLVED) {
     if (batch == 1) {                                                    // Fig. 1
       *s = l_k < kEvolvedShortLk ? kEvolvedShortSplits : kEvolvedSplits;
@@ -107,6 +114,9 @@ void decide(int64_t batch, int64_t l_k, int64_t T, int64_t U, int64_t nblk, int 
 
 }  // namespace
 
+// DA_POLICY_DYNAMIC with a cap above one: the split CTAs are slots assigned on the device.
+bool is_dynamic(const da_plan& p) { return p.policy == DA_POLICY_DYNAMIC && p.num_splits > 1; }
+
 // Launch geometry for a plan whose decision fields are set.  Shared by
 // da_plan_make, da_plan_set_combine and da_forward's consistency check.
 void derive_launch(da_plan* p) {
@@ -117,6 +127,14 @@ void derive_launch(da_plan* p) {
   p->grid_x = p->num_splits;
   p->grid_y = mma ? p->h_kv * static_cast<int32_t>(ceil_div(G, p->rows_per_cta)) : p->h_q;
   p->grid_z = p->batch;
+  if (is_dynamic(*p)) {
+    // split slots: sum_b s_b <= sum_b n_u_b / W + B <= U / T_b + B for any lengths (C-ext-2)
+    const int64_t tiles = static_cast<int64_t>(p->h_kv) * p->num_m_blocks;
+    int64_t slots = ceil_div(p->usable_sms, tiles) + p->batch;
+    const int64_t most = static_cast<int64_t>(p->batch) * p->num_splits;
+    p->grid_x = static_cast<int32_t>(slots < most ? slots : most);
+    p->grid_z = 1;
+  }
   const bool cluster = p->combine_mode == DA_COMBINE_CLUSTER;
   p->block_threads = threads_for(warps_for(p->combine_mode), helpers_for(p->combine_mode));
   p->cluster_x = cluster ? p->num_splits : 1;
@@ -124,6 +142,8 @@ void derive_launch(da_plan* p) {
   p->workspace_bytes = p->num_splits > 1
       ? static_cast<int64_t>(p->num_splits) * p->batch * p->h_q * (p->head_dim + 1) * 4
       : 0;
+  if (is_dynamic(*p))   // partials per slot, then the schedule (first slot, split count) per b
+    p->workspace_bytes = static_cast<int64_t>(p->grid_x) * p->h_q * (p->head_dim + 1) * 4 + 8LL * p->batch;
 }
 
 // s == 1: NONE.  2 <= s <= 16: CLUSTER when every cluster of the launch is co-resident in one
@@ -132,6 +152,7 @@ void derive_launch(da_plan* p) {
 int default_combine_mode(const da_plan& p) {
   const int s = p.num_splits;
   if (s == 1) return DA_COMBINE_NONE;
+  if (is_dynamic(p)) return DA_COMBINE_KERNEL;   // per-batch split counts: no uniform cluster shape
   if (s > kMaxClusterSplits) return DA_COMBINE_KERNEL;
   const int G = p.h_q / p.h_kv;
   const bool mma = p.pack_gqa != 0 && G >= 2;
@@ -164,7 +185,7 @@ extern "C" da_status da_plan_make(int32_t batch, int32_t h_q, int32_t h_kv, int3
   if (h_q % h_kv != 0) return DA_ERR_INVALID_ARG;
   if (sm_margin < 0 || sm_margin >= num_sms) return DA_ERR_INVALID_ARG;
   if (pack_gqa != 0 && pack_gqa != 1) return DA_ERR_INVALID_ARG;
-  if (policy < DA_POLICY_GUARDED || policy > DA_POLICY_SEQ_AWARE_SM) return DA_ERR_INVALID_ARG;
+  if (policy < DA_POLICY_GUARDED || policy > DA_POLICY_DYNAMIC) return DA_ERR_INVALID_ARG;
   if (policy == DA_POLICY_FIXED && (forced_splits < 1 || forced_splits > kMaxForcedSplits))
     return DA_ERR_INVALID_ARG;
   if (head_dim != kHeadDim) return DA_ERR_UNSUPPORTED;
@@ -199,6 +220,7 @@ extern "C" da_status da_plan_make(int32_t batch, int32_t h_q, int32_t h_kv, int3
 extern "C" da_status da_plan_set_combine(da_plan* plan, int32_t combine_mode) {
   if (plan == nullptr) return DA_ERR_INVALID_ARG;
   if (!combine_mode_valid(combine_mode, plan->num_splits)) return DA_ERR_INVALID_ARG;
+  if (is_dynamic(*plan) && combine_mode != DA_COMBINE_KERNEL) return DA_ERR_INVALID_ARG;
   plan->combine_mode = combine_mode;
   derive_launch(plan);
   return DA_OK;

@@ -74,9 +74,15 @@ def _check_plan(L, b, hq, hkv, lk, pack, margin, sms, pol, forced=0):
     assert (p.num_n_blocks, p.num_m_blocks, p.total_mblocks, p.usable_sms) == (
         geo["nblk"], geo["num_m_blocks"], geo["T"], geo["U"])
     path, rows, grid = _expected_launch(b, hq, hkv, pack, s)
+    if pol == "dynamic" and s > 1:      # C-ext-2: split slots decided on the device, workspace combine
+        slots = OP.dynamic_slots(b, hkv * geo["num_m_blocks"], geo["U"], s)
+        grid = (slots, grid[1], 1)
+        assert p.workspace_bytes == slots * hq * 129 * 4 + 8 * b
+        assert p.combine_mode == 2
+    else:
+        assert p.workspace_bytes == (s * b * hq * 129 * 4 if s > 1 else 0)
+        assert p.combine_mode == _expected_combine(b, hq, hkv, pack, sms, s)
     assert (p.path, p.rows_per_cta, (p.grid_x, p.grid_y, p.grid_z)) == (path, rows, grid)
-    assert p.workspace_bytes == (s * b * hq * 129 * 4 if s > 1 else 0)
-    assert p.combine_mode == _expected_combine(b, hq, hkv, pack, sms, s)
     assert p.nonempty_splits == min(s, -(-lk // 64))
 
 
@@ -85,7 +91,7 @@ def test_plan_matches_oracle_dense_lk(L):
     for sms in (132, 148):
         for (b, hkv) in ((1, 1), (1, 2), (2, 1), (1, 8), (8, 8), (4, 32)):
             for lk in range(1, 4097):
-                for pol in ("guarded", "seq_aware", "evolved", "seq_aware_sm"):
+                for pol in ("guarded", "seq_aware", "evolved", "seq_aware_sm", "dynamic"):
                     _check_plan(L, b, 8 * hkv, hkv, lk, 1, 0, sms, pol)
 
 
@@ -99,7 +105,7 @@ def test_plan_matches_oracle_grid(L):
         for margin in (0, 4, 16, sms - 1):
             for b, hkv, G in itertools.product(Bs, HKVs, (1, 8)):
                 for lk in LKs:
-                    for pol in ("guarded", "seq_aware", "seq_aware_sm"):
+                    for pol in ("guarded", "seq_aware", "seq_aware_sm", "dynamic"):
                         _check_plan(L, b, G * hkv, hkv, lk, 1, margin, sms, pol)
 
 
@@ -121,7 +127,7 @@ def test_plan_random_shapes_and_fixed(L):
         sms = rng.choice([132, 148, 7, 2, 1])
         margin = rng.randint(0, sms - 1)
         pack = rng.randint(0, 1)
-        pol = rng.choice(["guarded", "seq_aware", "fixed", "evolved", "seq_aware_sm"])
+        pol = rng.choice(["guarded", "seq_aware", "fixed", "evolved", "seq_aware_sm", "dynamic"])
         forced = rng.randint(1, 256) if pol == "fixed" else 0
         _check_plan(L, b, G * hkv, hkv, lk, pack, margin, sms, pol, forced)
 
@@ -149,7 +155,7 @@ def test_plan_invalid_shapes(L, args):
 
 def test_plan_invalid_knobs(L):
     bad = [dict(sm_margin=148), dict(sm_margin=-1), dict(num_sms=0), dict(pack_gqa=2),
-           dict(policy=7), dict(policy=-1), dict(policy=L.DA_POLICY_FIXED, forced_splits=0),
+           dict(policy=6), dict(policy=-1), dict(policy=L.DA_POLICY_FIXED, forced_splits=0),
            dict(policy=L.DA_POLICY_FIXED, forced_splits=257)]
     for kw in bad:
         args = dict(batch=1, h_q=8, h_kv=1, l_k=512, head_dim=128, pack_gqa=1, sm_margin=0,
@@ -178,6 +184,10 @@ def test_set_combine_rules(L):
     assert q.combine_mode == L.DA_COMBINE_CLUSTER and q.cluster_x == 12
     q = L.da_plan_make(16, 64, 8, 4096, 128, 1, 0, 148, "fixed", 8)   # 128 clusters of 8 > 15
     assert q.combine_mode == L.DA_COMBINE_KERNEL
+    d = L.da_plan_make(4, 32, 4, 4096, 128, 1, 0, 148, "dynamic", 0)  # per-batch counts: workspace only
+    assert d.combine_mode == L.DA_COMBINE_KERNEL and d.grid_z == 1
+    with pytest.raises(L.DecAttnError):
+        L.da_plan_set_combine(d, L.DA_COMBINE_CLUSTER)
 
 
 # ---- da_forward / da_combine validation (fake device pointers: every check below

@@ -24,7 +24,8 @@ def test_parity_subset_under_debug_asserts():
                   build_dir=os.path.join(B.PKG, "build", "debug"))
     env = dict(os.environ, DECATTN_LIB=lib)
     sel = ("baseline_configs or cluster_combine or kernel_combine_partials or scalar_path or lcap_larger "
-           "or short_sequences or combine_kernel_direct or variants or group_sizes or strided")
+           "or short_sequences or combine_kernel_direct or variants or group_sizes or strided "
+           "or dynamic_splits or paged or seq_aware_sm_fit or forward_host")
     r = subprocess.run([sys.executable, "-m", "pytest", os.path.join(ROOT, "tests", "test_gpu_parity.py"),
                         "-m", "gpu", "-x", "-q", "-k", sel], cwd=ROOT, env=env, capture_output=True,
                        text=True, timeout=900)

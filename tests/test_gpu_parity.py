@@ -322,3 +322,72 @@ def test_forward_host_matches_oracle(batch, h_q, h_kv, l_k, policy, forced, seql
                                   out_dtype=torch.float32 if f32 else torch.bfloat16)
     stream.synchronize()
     assert torch.equal(out, out2) and torch.equal(lse, lse2)
+
+
+# ---- per-batch dynamic split counts (DA_POLICY_DYNAMIC, C-ext-2) ----------------
+def _dyn_lengths(kind, batch, l_k, seed):
+    g = torch.Generator().manual_seed(seed)
+    if kind == "skewed":        # one long sequence among short ones
+        n = torch.randint(1, max(2, l_k // 16), (batch,), generator=g)
+        n[batch // 2] = l_k
+    elif kind == "uniform":
+        n = torch.full((batch,), l_k)
+    elif kind == "empty":
+        n = torch.zeros(batch, dtype=torch.int64)
+        n[-1] = 3
+    else:                       # ragged: U[0, l_k] with an empty and a single-token sequence
+        n = torch.randint(0, l_k + 1, (batch,), generator=g)
+        n[0] = 0
+        if batch > 1:
+            n[1] = 1
+    return n.to(torch.int32)
+
+
+@pytest.mark.parametrize("batch,h_q,h_kv,l_k,kind", [
+    (8, 64, 8, 4096, "skewed"), (16, 8, 1, 8192, "skewed"), (5, 24, 3, 1500, "ragged"),
+    (3, 16, 16, 700, "ragged"), (40, 8, 1, 2048, "ragged"), (2, 8, 2, 1024, "uniform"),
+    (4, 8, 1, 600, "empty"), (1, 64, 8, 20000, "uniform"), (70, 16, 2, 300, "ragged")])
+def test_dynamic_splits_match_oracle(batch, h_q, h_kv, l_k, kind):
+    dec = _dec()
+    inp = synth.make_inputs(batch, h_q, h_kv, l_k, seed=1300, device="cuda")
+    seq = _dyn_lengths(kind, batch, l_k, 1301).to("cuda")
+    plan = dec.make_plan(batch, h_q, h_kv, l_k, policy="dynamic")
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    assert (plan.num_splits, plan.rule) == OP.num_splits(batch, h_q, h_kv, l_k, sms, 0, "dynamic")
+    ws = dec.workspace_for(plan, inp["q"].device)
+    out, lse = dec.forward(plan, inp["q"], inp["k"], inp["v"], seq, workspace=ws)
+    torch.cuda.synchronize()
+    qn, kn, vn, sn = (synth.to_f64(t) for t in (inp["q"], inp["k"], inp["v"], seq))
+    ref_o, ref_l = OA.decode_attention(qn, kn, vn, sn)
+    assert_out_close(synth.to_f64(out), ref_o)
+    assert_lse_close(synth.to_f64(lse), ref_l)
+    if plan.num_splits > 1:
+        # the schedule the kernel recorded equals the oracle's, bit for bit
+        prows = plan.grid_x * h_q
+        meta = ws.view(torch.int32)[prows * 129: prows * 129 + 2 * batch].cpu().tolist()
+        tiles = h_kv * plan.num_m_blocks
+        W, s_ref, P_ref = OP.dynamic_schedule([int(n) for n in sn], tiles, plan.usable_sms, plan.num_splits)
+        assert meta[:batch] == P_ref and meta[batch:] == s_ref
+        assert sum(s_ref) <= plan.grid_x
+        # per-split partials of the longest sequence vs C-part with its own partition
+        b = int(np.argmax(sn))
+        ranges = [OA.partition(int(sn[b]), s_ref[b], OP.SPLIT_UNIT)]
+        po, pl = OA.split_partials(qn[b:b + 1], kn[b:b + 1], vn[b:b + 1], sn[b:b + 1], ranges)
+        wo = ws[: prows * 128].view(plan.grid_x, h_q, 128)[P_ref[b]: P_ref[b] + s_ref[b]]
+        wl = ws[prows * 128: prows * 129].view(plan.grid_x, h_q)[P_ref[b]: P_ref[b] + s_ref[b]]
+        assert_out_close(synth.to_f64(wo), po[:, 0], "dynamic partial o")
+        assert_lse_close(synth.to_f64(wl), pl[:, 0], "dynamic partial lse")
+
+
+def test_dynamic_splits_without_seqlens_and_paged():
+    # cache_seqlens = NULL (uniform plan length) and the paged cache go through the same schedule
+    dec = _dec()
+    inp = synth.make_inputs(2, 16, 2, 3000, seed=1310, device="cuda")
+    plan = dec.make_plan(2, 16, 2, 3000, policy="dynamic")
+    out, lse = dec.forward(plan, inp["q"], inp["k"], inp["v"], None)
+    torch.cuda.synchronize()
+    ref_o, ref_l = OA.decode_attention(*(synth.to_f64(t) for t in (inp["q"], inp["k"], inp["v"])),
+                                       [3000, 3000])
+    assert_out_close(synth.to_f64(out), ref_o)
+    assert_lse_close(synth.to_f64(lse), ref_l)
+    run_paged(6, 32, 4, 2500, 128, policy="dynamic")
