@@ -270,6 +270,35 @@ def streaming_roofline(dec, dev, stream, timer, cfg, steps, rounds, l2, seed, pe
     return r
 
 
+RAGGED_AB = dict(batch=16, h_q=64, h_kv=8, l_k=32768)   # one 32768-token sequence + fifteen of 1024
+
+
+def ragged_ab(dec, dev, stream, timer, steps, rounds, l2, seed):
+    """Per-batch dynamic split counts (DA_POLICY_DYNAMIC, DESIGN.md C-ext-2) vs the static policies on
+    a skewed ragged batch; the static plans see the cache capacity, the dynamic schedule the lengths."""
+    cfg = RAGGED_AB
+    lens = [cfg["l_k"]] + [1024] * (cfg["batch"] - 1)
+    w = Workload(cfg, dev, seed, l2, uniform=False)
+    w.seqlens = torch.tensor(lens, dtype=torch.int32, device=dev)
+    pols = ("guarded", "seq_aware_sm", "dynamic")
+    plans = {p: dec.make_plan(cfg["batch"], cfg["h_q"], cfg["h_kv"], cfg["l_k"], policy=p) for p in pols}
+    graphs = {p: make_graph(dec, plans[p], w, steps, stream) for p in pols}
+    res = {p: [] for p in pols}
+    for _ in range(rounds):
+        for p in pols:
+            res[p].append(timer.time_replay(graphs[p], stream) * 1e3 / steps)
+    byts = 4 * sum(lens) * cfg["h_kv"] * HEAD_DIM + 4 * cfg["batch"] * cfg["h_q"] * HEAD_DIM + 4 * cfg["batch"] * cfg["h_q"]
+    out = {"config": dict(cfg, lengths=f"[{cfg['l_k']}] + [1024] x {cfg['batch'] - 1}")}
+    for p in pols:
+        us = statistics.median(res[p])
+        out[p] = {"num_splits": plans[p].num_splits, "combine_mode": plans[p].combine_mode,
+                  "us_per_step": round(us, 2), "gbs": round(byts / (us * 1e-6) / 1e9, 1)}
+    out["speedup_dynamic_vs_guarded"] = round(out["guarded"]["us_per_step"] / out["dynamic"]["us_per_step"], 3)
+    del w, graphs
+    torch.cuda.empty_cache()
+    return out
+
+
 # ----------------------------------------------------------------------------------------------
 def cpu_baseline(cfg, budget_s=10.0):
     """The fp64 oracle (as it stands) on this host's cores, on a bounded sample of the workload."""
@@ -521,6 +550,7 @@ def main():
             "high_load": streaming_roofline(dec, dev, stream, timer, WORKLOADS["high_load"], 5, 5, l2, 1003, peak),
             "long_context": streaming_roofline(dec, dev, stream, timer, WORKLOADS["long_context"], 20, 7, l2, 1004, peak),
         }
+        extras["ragged_ab"] = ragged_ab(dec, dev, stream, timer, 20, 7, l2, 1005)
     if world > 1:
         barrier()
     if rank != 0:

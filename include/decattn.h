@@ -156,16 +156,18 @@ typedef struct da_plan {
   int32_t path;            /* da_path                                          */
   int32_t rows_per_cta;    /* query rows one CTA computes (1, 8 or 16)         */
   int32_t combine_mode;    /* da_combine_mode                                  */
-  int32_t grid_x;          /* = num_splits; DA_POLICY_DYNAMIC: split slots,
+  int32_t grid_x;          /* = num_splits; DA_POLICY_DYNAMIC: the head groups
+                              (grid_y's static value)                        */
+  int32_t grid_y;          /* MMA: h_kv * ceil(G / rows_per_cta); SCALAR: h_q;
+                              DA_POLICY_DYNAMIC: split slots,
                               min(B * cap, ceil(U / T_b) + B)                */
-  int32_t grid_y;          /* MMA: h_kv * ceil(G / rows_per_cta); SCALAR: h_q  */
   int32_t grid_z;          /* = batch; DA_POLICY_DYNAMIC: 1                    */
   int32_t block_threads;   /* threads per CTA                                  */
   int32_t cluster_x;       /* CTAs per cluster along x (s in CLUSTER mode)     */
   int32_t smem_bytes;      /* dynamic shared memory per CTA                    */
   int64_t workspace_bytes; /* s * batch * h_q * (head_dim + 1) * 4 when s > 1,
                               else 0.  Only DA_COMBINE_KERNEL reads/writes it.
-                              DA_POLICY_DYNAMIC: grid_x * h_q * (head_dim + 1)
+                              DA_POLICY_DYNAMIC: grid_y * h_q * (head_dim + 1)
                               * 4 + 8 * batch (partials per slot, then the
                               schedule: first slot and split count per b)  */
 } da_plan;

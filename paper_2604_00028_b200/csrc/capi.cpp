@@ -128,7 +128,7 @@ da_status forward_impl(const da_plan* plan, const void* q, const void* k_cache, 
   int32_t* ws_meta = nullptr;
   const bool dyn = is_dynamic(*plan);
   // partial rows: static [s][B][H_Q]; dynamic [slot][H_Q] then the schedule [2][B] int32
-  const int64_t prows = dyn ? int64_t(plan->grid_x) * HQ : int64_t(plan->num_splits) * B * HQ;
+  const int64_t prows = dyn ? int64_t(plan->grid_y) * HQ : int64_t(plan->num_splits) * B * HQ;
   if (plan->combine_mode == DA_COMBINE_KERNEL) {
     if (workspace == nullptr || workspace_bytes < plan->workspace_bytes) return DA_ERR_WORKSPACE;
     if (!aligned16(workspace)) return DA_ERR_ALIGNMENT;

@@ -290,31 +290,45 @@ __device__ __forceinline__ void split_range(int n, int split, int s, uint64_t s_
 // split, s_b, length) that split slot `slot` serves, or x = -1 for an unused slot.  Every CTA
 // runs the same integer arithmetic; the CTA of slot 0, head group 0 records (P_b, s_b) for the
 // combine kernel.
+constexpr int kDynScratch = kStageBytes / 4;   // sequences whose unit count is cached in shared memory
+
 __device__ __forceinline__ int dyn_len(const FwdParams& p, int b) {
   return min(max(p.seqlens != nullptr ? __ldg(p.seqlens + b) : p.l_default, 0), p.l_cap);
 }
 
-__device__ __noinline__ int4 dyn_schedule(const FwdParams& p, uint32_t slot, bool record, int lane) {
+__device__ __noinline__ int4 dyn_schedule(const FwdParams& p, uint32_t slot, bool record, int lane,
+                                          int* lens) {
+  // lens: shared-memory scratch (the ring, idle until the first TMA) holding n_b for b < kDynScratch
   const int B = p.batch;
   uint32_t tot = 0;
+#pragma unroll 4
   for (int b0 = 0; b0 < B; b0 += 32) {
     const int bb = b0 + lane;
-    if (bb < B) tot += (static_cast<uint32_t>(dyn_len(p, bb)) + (kTileN - 1)) / kTileN;
+    if (bb < B) {
+      const int n = dyn_len(p, bb);
+      if (bb < kDynScratch) lens[bb] = n;
+      tot += (static_cast<uint32_t>(n) + (kTileN - 1)) / kTileN;
+    }
   }
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, off);
-  const uint64_t num = static_cast<uint64_t>(tot) * static_cast<uint32_t>(p.dyn_tiles);
-  const uint64_t Wl = (num + static_cast<uint32_t>(p.dyn_u) - 1) / static_cast<uint32_t>(p.dyn_u);
-  const uint32_t W = Wl < 1 ? 1u : static_cast<uint32_t>(Wl);
+  const uint32_t T = static_cast<uint32_t>(p.dyn_tiles), U = static_cast<uint32_t>(p.dyn_u);
+  uint32_t W;
+  if (tot <= 0xffffffffu / T) {                        // the common case: a 32-bit quotient
+    W = (tot * T + U - 1) / U;
+  } else {
+    W = static_cast<uint32_t>((static_cast<uint64_t>(tot) * T + U - 1) / U);
+  }
+  W = max(W, 1u);
   const uint32_t cap = static_cast<uint32_t>(p.num_splits);
   int4 mine = make_int4(-1, 0, 0, 0);
   uint32_t base = 0;
   for (int b0 = 0; b0 < B; b0 += 32) {
     const int bb = b0 + lane;
-    int n = 0;
     uint32_t sb = 0;
+    int n = 0;
     if (bb < B) {
-      n = dyn_len(p, bb);
+      n = bb < kDynScratch ? lens[bb] : dyn_len(p, bb);
       sb = min(max(((static_cast<uint32_t>(n) + (kTileN - 1)) / kTileN) / W, 1u), cap);
     }
     uint32_t inc = sb;                                  // inclusive warp scan of s_b
@@ -374,15 +388,20 @@ __global__ void __launch_bounds__(threads_for(NW, helpers_for(kCombine)), 1)
   float* const slots = epi + NS * kStageBytes / 4;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // kDyn: blockIdx.x is the head group and blockIdx.y the split slot, so that consecutive CTAs
+  // read the heads of one sequence (shared DRAM rows, like the static (split, group, batch) order)
+  const int grp = kDyn ? blockIdx.x : blockIdx.y;
+  const uint32_t dslot = kDyn ? blockIdx.y : 0u;
   int split = blockIdx.x, b = blockIdx.z;       // kDyn: assigned from the schedule below
+  bool dyn_single = false;                       // kDyn: this sequence has one split (s_b = 1)
   int kvh, hq0, rows_valid;
   if constexpr (kPath == DA_PATH_MMA) {
-    kvh = blockIdx.y / p.mblocks_per_head;
-    const int rg = blockIdx.y - kvh * p.mblocks_per_head;
+    kvh = grp / p.mblocks_per_head;
+    const int rg = grp - kvh * p.mblocks_per_head;
     hq0 = kvh * p.G + rg * R;
     rows_valid = min(R, p.G - rg * R);
   } else {
-    hq0 = blockIdx.y;
+    hq0 = grp;
     kvh = hq0 / p.G;
     rows_valid = 1;
   }
@@ -420,6 +439,8 @@ __global__ void __launch_bounds__(threads_for(NW, helpers_for(kCombine)), 1)
     // prefetch never returns data, so it cannot observe a stale value)
     if (!kDyn && p.seqlens != nullptr) prefetch_l2(p.seqlens + b);
   }
+  if (kDyn && warp == NW && p.seqlens != nullptr && lane * 32 < p.batch)
+    prefetch_l2(p.seqlens + lane * 32);          // the first 1024 lengths, one 128-byte line per lane
   __syncthreads();
   if constexpr (kCluster) cluster_arrive_relaxed();   // "my push barrier is initialised"
 
@@ -440,8 +461,8 @@ __global__ void __launch_bounds__(threads_for(NW, helpers_for(kCombine)), 1)
   if constexpr (kDyn) {
     __shared__ int4 sched;
     if (warp == 0) {
-      const int4 r = dyn_schedule(p, blockIdx.x, blockIdx.x == 0 && blockIdx.y == 0 && p.ws_meta != nullptr,
-                                  lane);
+      const int4 r = dyn_schedule(p, dslot, dslot == 0 && grp == 0 && p.ws_meta != nullptr,
+                                  lane, reinterpret_cast<int*>(epi));
       if (lane == 0) sched = r;
     }
     __syncthreads();
@@ -449,6 +470,7 @@ __global__ void __launch_bounds__(threads_for(NW, helpers_for(kCombine)), 1)
     if (r.x < 0) return;                          // unused slot (the launch provides an upper bound)
     b = r.x;
     split = r.y;
+    dyn_single = r.z == 1;
     // split r.y of r.z over n = r.w tokens; (split + 1) n_u < 2^32 since r.z <= 128, n_u < 2^25
     const uint32_t nu = (static_cast<uint32_t>(r.w) + (kTileN - 1)) / kTileN;
     const uint32_t u0 = static_cast<uint32_t>(r.y) * nu / static_cast<uint32_t>(r.z);
@@ -677,13 +699,13 @@ __global__ void __launch_bounds__(threads_for(NW, helpers_for(kCombine)), 1)
       const float4 v = make_float4(eO[it].x * inv, eO[it].y * inv, eO[it].z * inv, eO[it].w * inv);
       const float lse_v = eL[it] > 0.f ? (eM[it] + lg2(eL[it])) * kLn2 : kNegInf;
       const size_t row = static_cast<size_t>(b) * p.h_q + hq0 + g;
-      if constexpr (kCombine == DA_COMBINE_NONE) {
+      if (kCombine == DA_COMBINE_NONE || (kDyn && dyn_single)) {   // kDyn, s_b = 1: the final row
         store_out(p, row, d4, v);
         if (d4 == 0 && p.lse != nullptr) p.lse[row] = lse_v;
       } else {  // DA_COMBINE_KERNEL: normalised partial o_i, lse_i (C-part); kDyn: slot-major rows
-        const size_t prow = kDyn ? static_cast<size_t>(blockIdx.x) * p.h_q + hq0 + g
+        const size_t prow = kDyn ? static_cast<size_t>(dslot) * p.h_q + hq0 + g
                                  : static_cast<size_t>(split) * p.batch * p.h_q + row;
-        DA_DASSERT(prow < (kDyn ? static_cast<size_t>(gridDim.x) * p.h_q
+        DA_DASSERT(prow < (kDyn ? static_cast<size_t>(gridDim.y) * p.h_q
                                 : static_cast<size_t>(p.num_splits) * p.batch * p.h_q));
         reinterpret_cast<float4*>(p.ws_o)[prow * (kHeadDim / 4) + d4] = v;
         if (d4 == 0) p.ws_lse[prow] = lse_v;
@@ -768,8 +790,9 @@ template <int kPath, int kNB, int kCombine, bool kDyn = false>
 cudaError_t launch_impl(const da_plan& plan, const CUtensorMap& tk, const CUtensorMap& tv,
                         const FwdParams& p, cudaStream_t stream) {
   constexpr bool kCluster = kCombine == DA_COMBINE_CLUSTER;
-  constexpr int NS = stages_for(kCombine);
-  constexpr int NW = warps_for(kCombine);
+  // dynamic split counts: mostly one split per sequence, so the streaming (s = 1) configuration
+  constexpr int NS = kDyn ? kStagesNone : stages_for(kCombine);
+  constexpr int NW = kDyn ? kWarpsNone : warps_for(kCombine);
   constexpr int kSmem = smem_for(NS, kCluster);
   auto kern = split_kv_fwd_kernel<kPath, kNB, kCombine, NS, NW, kDyn>;
   // One-time (per device) opt-in to > 48 KB of dynamic shared memory.
@@ -790,6 +813,7 @@ cudaError_t launch_impl(const da_plan& plan, const CUtensorMap& tk, const CUtens
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(plan.grid_x, plan.grid_y, plan.grid_z);
   cfg.blockDim = dim3(threads_for(NW, helpers_for(kCombine)), 1, 1);
+  if (static_cast<int>(cfg.blockDim.x) != plan.block_threads || kSmem != plan.smem_bytes) return cudaErrorInvalidConfiguration;
   cfg.dynamicSmemBytes = kSmem;
   cfg.stream = stream;
   cudaLaunchAttribute attrs[2];

@@ -132,18 +132,23 @@ void derive_launch(da_plan* p) {
     const int64_t tiles = static_cast<int64_t>(p->h_kv) * p->num_m_blocks;
     int64_t slots = ceil_div(p->usable_sms, tiles) + p->batch;
     const int64_t most = static_cast<int64_t>(p->batch) * p->num_splits;
-    p->grid_x = static_cast<int32_t>(slots < most ? slots : most);
+    p->grid_x = p->grid_y;                                 // head groups innermost (DRAM row sharing)
+    p->grid_y = static_cast<int32_t>(slots < most ? slots : most);
     p->grid_z = 1;
   }
   const bool cluster = p->combine_mode == DA_COMBINE_CLUSTER;
   p->block_threads = threads_for(warps_for(p->combine_mode), helpers_for(p->combine_mode));
   p->cluster_x = cluster ? p->num_splits : 1;
   p->smem_bytes = smem_for(stages_for(p->combine_mode), cluster);
+  if (is_dynamic(*p)) {   // mostly one split per sequence: the streaming (s = 1) configuration
+    p->block_threads = threads_for(kWarpsNone, 0);
+    p->smem_bytes = smem_for(kStagesNone, false);
+  }
   p->workspace_bytes = p->num_splits > 1
       ? static_cast<int64_t>(p->num_splits) * p->batch * p->h_q * (p->head_dim + 1) * 4
       : 0;
   if (is_dynamic(*p))   // partials per slot, then the schedule (first slot, split count) per b
-    p->workspace_bytes = static_cast<int64_t>(p->grid_x) * p->h_q * (p->head_dim + 1) * 4 + 8LL * p->batch;
+    p->workspace_bytes = static_cast<int64_t>(p->grid_y) * p->h_q * (p->head_dim + 1) * 4 + 8LL * p->batch;
 }
 
 // s == 1: NONE.  2 <= s <= 16: CLUSTER when every cluster of the launch is co-resident in one

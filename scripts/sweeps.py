@@ -269,3 +269,61 @@ def ugrid3():
 
 if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "ugrid3":
     ugrid3()
+
+
+RAGGED_CASES = {
+    # name: (B, H_Q, H_KV, L_cap, lengths(B, L_cap, gen) -> list)
+    "skew_b16_h8": (16, 64, 8, 32768, lambda B, L, g: [L] + [1024] * (B - 1)),
+    "skew_b64_h1": (64, 8, 1, 16384, lambda B, L, g: [L] + [512] * (B - 1)),
+    "mix_b32_h8": (32, 64, 8, 8192, lambda B, L, g: torch.randint(64, L + 1, (B,), generator=g).tolist()),
+    "tail_b128_h8": (128, 64, 8, 16384,
+                     lambda B, L, g: torch.clamp(torch.exp(torch.randn(B, generator=g) * 1.2 + 6.5), 16, L)
+                     .to(torch.int64).tolist()),
+    "uniform_b4_h8": (4, 64, 8, 4096, lambda B, L, g: [L] * B),
+    "long_b1_h8": (1, 64, 8, 131072, lambda B, L, g: [L]),
+    "uniform_b128_h8": (128, 64, 8, 8192, lambda B, L, g: [L] * B),   # high-load: identical work, s_b = 1
+}
+RAGGED_POLICIES = ("guarded", "seq_aware_sm", "dynamic")
+
+
+def ragged():
+    """Per-batch dynamic split counts (C-ext-2) vs the static policies on ragged batches: the static
+    plans see only the cache capacity L_cap (the serving case: one plan per shape bucket), the dynamic
+    schedule sees the lengths on the device.  Value: us/step and algorithmic GB/s of the real lengths."""
+    rows = []
+    dev = torch.device("cuda", 0)
+    l2 = torch.cuda.get_device_properties(0).L2_cache_size
+    for name, (B, hq, hkv, L, fn) in RAGGED_CASES.items():
+        g = torch.Generator().manual_seed(71)
+        lens = [int(x) for x in fn(B, L, g)]
+        cfg = dict(batch=B, h_q=hq, h_kv=hkv, l_k=L)
+        w = bench.Workload(cfg, dev, 73, l2, max_rot_bytes=200 << 20, uniform=False)
+        w.seqlens = torch.tensor(lens, dtype=torch.int32, device=dev)
+        stream = torch.cuda.Stream()
+        timer = bench.Timer(dev)
+        plans = [dec.make_plan(B, hq, hkv, L, policy=p) for p in RAGGED_POLICIES]
+        kv = 4 * sum(lens) * hkv * D
+        steps = 200 if kv * w.nbuf < (64 << 20) or kv < (16 << 20) else (40 if kv < (512 << 20) else 10)
+        graphs = [bench.make_graph(dec, p, w, steps, stream) for p in plans]
+        res = [[] for _ in plans]
+        for _ in range(9):
+            for i, gr in enumerate(graphs):
+                res[i].append(timer.time_replay(gr, stream) * 1e3 / steps)
+        med = [statistics.median(r) for r in res]
+        alg = kv + 4 * B * hq * D + 4 * B * hq
+        for pol, plan, t in zip(RAGGED_POLICIES, plans, med):
+            rows.append(dict(case=name, batch=B, h_q=hq, h_kv=hkv, l_cap=L, total_tokens=sum(lens),
+                             max_len=max(lens), policy=pol, num_splits=plan.num_splits, grid_x=plan.grid_x * plan.grid_y,
+                             combine_mode=plan.combine_mode, latency_us=round(t, 3),
+                             gbs=round(alg / t / 1e3, 1), speedup_vs_guarded=round(med[0] / t, 4)))
+        print(f"{name:14s} tokens {sum(lens):8d} max {max(lens):6d}: " +
+              "  ".join(f"{pol} s={p.num_splits} {t:8.2f} us" for pol, p, t in zip(RAGGED_POLICIES, plans, med)) +
+              f"   dynamic {med[0] / med[2]:.2f}x vs guarded, {med[1] / med[2]:.2f}x vs seq_aware_sm", flush=True)
+        del graphs, w, timer
+        torch.cuda.empty_cache()
+    write("ragged", rows, ["case", "batch", "h_q", "h_kv", "l_cap", "total_tokens", "max_len", "policy",
+                           "num_splits", "grid_x", "combine_mode", "latency_us", "gbs", "speedup_vs_guarded"])
+
+
+if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "ragged":
+    ragged()

@@ -76,7 +76,7 @@ def _check_plan(L, b, hq, hkv, lk, pack, margin, sms, pol, forced=0):
     path, rows, grid = _expected_launch(b, hq, hkv, pack, s)
     if pol == "dynamic" and s > 1:      # C-ext-2: split slots decided on the device, workspace combine
         slots = OP.dynamic_slots(b, hkv * geo["num_m_blocks"], geo["U"], s)
-        grid = (slots, grid[1], 1)
+        grid = (grid[1], slots, 1)                      # head groups innermost, then split slots
         assert p.workspace_bytes == slots * hq * 129 * 4 + 8 * b
         assert p.combine_mode == 2
     else:
