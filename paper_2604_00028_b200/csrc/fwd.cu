@@ -444,6 +444,15 @@ __global__ void __launch_bounds__(threads_for(NW, helpers_for(kCombine)), 1)
   __syncthreads();
   if constexpr (kCluster) cluster_arrive_relaxed();   // "my push barrier is initialised"
 
+  // ---- this split's token range (C-pol item 6), in units of kTileN tokens.  With uniform
+  // lengths (cache_seqlens == NULL) it depends on no global value, so it is computed before
+  // griddepcontrol.wait and the producer issues the first TMA the moment the wait returns.
+  int t0 = 0, t_end = 0, n_tiles = 0;
+  if constexpr (!kDyn) {
+    if (p.seqlens == nullptr)
+      split_range(min(max(p.l_default, 0), p.l_cap), split, p.num_splits, p.s_magic, t0, t_end, n_tiles);
+  }
+
   // Let the next kernel in the stream start its prologue now (it waits in its own
   // griddepcontrol.wait for this grid to finish), then wait for our inputs, which
   // the preceding kernel may still be writing.
@@ -456,8 +465,6 @@ __global__ void __launch_bounds__(threads_for(NW, helpers_for(kCombine)), 1)
     if (c_ < 64) g_trace[c_ * 64 + 63] = *(volatile unsigned long long*)&g_prev_end;
   }
 #endif
-  // ---- this split's token range (C-pol item 6), in units of kTileN tokens
-  int t0, t_end, n_tiles;
   if constexpr (kDyn) {
     __shared__ int4 sched;
     if (warp == 0) {
@@ -478,9 +485,8 @@ __global__ void __launch_bounds__(threads_for(NW, helpers_for(kCombine)), 1)
     t0 = static_cast<int>(u0) * kTileN;
     t_end = min(static_cast<int>(u1) * kTileN, r.w);
     n_tiles = static_cast<int>(u1 - u0);
-  } else {
-    split_range(min(max(p.seqlens != nullptr ? __ldg(p.seqlens + b) : p.l_default, 0), p.l_cap), split,
-                p.num_splits, p.s_magic, t0, t_end, n_tiles);
+  } else if (p.seqlens != nullptr) {
+    split_range(min(max(__ldg(p.seqlens + b), 0), p.l_cap), split, p.num_splits, p.s_magic, t0, t_end, n_tiles);
   }
 
   if (warp == NW) {
