@@ -47,8 +47,9 @@ def main():
              f"plain run that exited 0).  Raw pages: `{tag}_ncu_raw_<config>.csv`; launch lists (device time "
              f"per launch, cold-cache, serialised): `{tag}_launches_<config>.csv`.", "",
              "| config | kernel | ncu duration (us) | DRAM read+write / launch | algorithmic bytes | DRAM / alg | "
-             "DRAM throughput (% peak) | tensor pipe % | regs | grid x block | cluster |",
-             "|---|---|---|---|---|---|---|---|---|---|---|"]
+             "DRAM GB/s (vs 8 TB/s) | DRAM % peak | tensor pipe % | CTAs (SMs busy) | achieved occupancy % | "
+             "regs | block | cluster |",
+             "|---|---|---|---|---|---|---|---|---|---|---|---|---|---|"]
     traffic = {"_source": f"ncu --set full --clock-control none ({tag} captures, profiles/{tag}_ncu_raw_*.csv): "
                           "dram__bytes_read.sum + dram__bytes_write.sum of split_kv_fwd_kernel, one launch"}
     stalls_txt = []
@@ -71,10 +72,16 @@ def main():
         grid = r.get("launch__grid_size", ("?", ""))[0]
         block = r.get("launch__block_size", ("?", ""))[0]
         cl = r.get("launch__cluster_dim_x", ("", ""))[0] or "-"
+        occ = num(r, "sm__warps_active.avg.pct_of_peak_sustained_active")
+        gbs = dram / (dur * 1e-6) / 1e9 if dur else 0.0
+        try:
+            busy = min(int(float(grid)), 148)
+        except ValueError:
+            busy = "?"
         lines.append(f"| {name} (B{cfg['batch']} H_Q{cfg['h_q']} H_KV{cfg['h_kv']} L{cfg['l_k']}) | `{short}` | "
-                     f"{dur:.2f} | {dram:,.0f} | {alg:,} | {dram / alg:.3f} | "
-                     f"{'' if thr is None else f'{thr:.1f}'} | {'' if tens is None else f'{tens:.1f}'} | {regs} | "
-                     f"{grid} x {block} | {cl} |")
+                     f"{dur:.2f} | {dram:,.0f} | {alg:,} | {dram / alg:.3f} | {gbs:,.0f} ({gbs / 8000:.2f}) | "
+                     f"{'' if thr is None else f'{thr:.1f}'} | {'' if tens is None else f'{tens:.1f}'} | "
+                     f"{grid} ({busy}) | {'' if occ is None else f'{occ:.1f}'} | {regs} | {block} | {cl} |")
         traffic[name] = {"dram_bytes_per_launch": int(dram), "algorithmic_bytes": alg, "kernel": short,
                          "ncu_duration_us": dur}
         st = []
