@@ -125,6 +125,14 @@ def test_lcap_larger_and_nan_tail(pack):
                   nan_tail=True, policy="fixed", forced=3)
 
 
+@pytest.mark.parametrize("l_k", [2, 3, 4, 6, 8, 16, 64, 512])
+@pytest.mark.parametrize("variant", ["normal", "peaked"])
+def test_pv_precision_short_and_peaked(l_k, variant):
+    # the cases where a single-bf16 P in the PV product misses the per-element bound
+    # (scripts/emulate_p_precision.py: err/bound up to 1.4): 8 batches x 64 query rows each
+    run_and_check(8, 64, 8, l_k, variant=variant, seed=1400 + l_k, policy="seq_aware_sm")
+
+
 def test_out_f32():
     run_and_check(2, 16, 2, 513, out_f32=True, policy="fixed", forced=5, seed=61)
 
