@@ -57,6 +57,8 @@ def build(force: bool = False, ptxas_verbose: bool = False, quiet: bool = True,
     os.makedirs(bdir, exist_ok=True)
     hdrs = [os.path.join(CSRC, h) for h in HEADERS] + [os.path.join(INCLUDE, "decattn.h"),
                                                          os.path.abspath(__file__)]
+    if not force and not _stale(lib, [os.path.join(CSRC, src) for src in SOURCES] + hdrs):
+        return lib    # up to date with every source (the object directory need not exist)
     objs = []
     for src in SOURCES:
         s = os.path.join(CSRC, src)
