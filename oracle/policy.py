@@ -87,6 +87,7 @@ CLUSTER_FIT_B200 = (0, 148, 74, 45, 33, 26, 22, 15, 15, 15, 11, 7, 7, 7, 7, 7, 7
 CLUSTER_MAX_SPLITS = 16
 # Per-batch dynamic split counts (the scheduler-metadata role of P:L125):
 DYN_MAX_SPLITS = 128  # per-sequence cap (the efficiency loop's candidate cap, C-amb-2)
+VARLEN_MIN_UNITS = 32  # C-ext-3: the dynamic path pays off only for splits of >= 2048 tokens
 
 def ceil_div(a: int, b: int) -> int:
     return -(-a // b)
@@ -249,6 +250,25 @@ def dynamic_schedule(seqlens, tiles_per_batch: int, U: int, s_cap: int):
         P.append(acc)
         acc += v
     return W, s, P
+
+
+def varlen_policy(batch: int, h_q: int, h_kv: int, l_cap: int, num_sms: int, sm_margin: int, seqlens):
+    """C-ext-3, the plan for a ragged batch whose lengths are known on the host (the
+    scheduler-metadata path of P:L125): the static SM-count-aware plan (C-ext-1) for the cache
+    capacity, unless its longest split would hold more than twice the balanced per-CTA work W
+    of dynamic_schedule and at least VARLEN_MIN_UNITS units (below that the step is latency-bound
+    and the workspace combine of the dynamic path costs more than the imbalance), in which case
+    the per-batch dynamic counts (C-ext-2):
+        s_st = seq_aware_sm(batch, h_q, h_kv, l_cap);  u_max = ceil(max_b n_b / 64)
+        W    = dynamic_schedule's W;  c = ceil(u_max / s_st);  dynamic iff c > 2 W and c >= 32
+    Returns the policy code (SEQ_AWARE_SM or DYNAMIC)."""
+    geo = geometry(batch, h_q, h_kv, l_cap, num_sms, sm_margin)
+    s_st, _ = seq_aware_sm_splits(geo, l_cap)
+    lens = [min(max(int(n), 0), l_cap) for n in seqlens]
+    u_max = ceil_div(max(lens), SPLIT_UNIT) if lens else 0
+    W, _, _ = dynamic_schedule(lens, h_kv * geo["num_m_blocks"], geo["U"], dynamic_cap(l_cap))
+    c = ceil_div(u_max, s_st)
+    return DYNAMIC if (c > 2 * W and c >= VARLEN_MIN_UNITS) else SEQ_AWARE_SM
 
 
 def evolved_policy_splits(geo: dict, batch: int, l_k: int):

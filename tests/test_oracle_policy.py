@@ -358,3 +358,30 @@ def test_dynamic_schedule_invariants():
             if v < cap and u >= W:
                 assert u < (v + 1) * W                               # each split holds < 2 W units
                 assert v * W <= u
+
+
+# ---- the host-side plan for ragged batches (C-ext-3) --------------------------------------------
+def test_varlen_policy_uniform_batches_stay_static():
+    # uniform lengths: the static SM-count-aware plan is already balanced; never the dynamic path
+    for B in (1, 2, 3, 4, 8, 16, 32, 64, 128):
+        for hkv in (1, 2, 4, 8, 16, 32):
+            for L in (1, 64, 65, 128, 300, 512, 513, 1000, 2048, 4096, 8192, 16384, 32768, 131072):
+                for sms in (148, 132):
+                    assert P.varlen_policy(B, 8 * hkv, hkv, L, sms, 0, [L] * B) == P.SEQ_AWARE_SM
+
+
+def test_varlen_policy_cases():
+    # hand-computed on B200 (U = 148):
+    # one 32768-token sequence among fifteen of 1024, 8 tiles each: static s = 1 (T = 128 saturated),
+    # c = 512 units; W = 41 (test_dynamic_schedule_examples) -> 512 > 82 and >= 32: dynamic
+    assert P.varlen_policy(16, 64, 8, 32768, 148, 0, [32768] + [1024] * 15) == P.DYNAMIC
+    # one 16384 among 63 of 512, 1 tile each: T = 64 -> static s = 2 (f = 2), c = 128; units
+    # 256 + 63 x 8 = 760 -> W = ceil(760 / 148) = 6 -> 128 > 12: dynamic
+    assert P.varlen_policy(64, 8, 1, 16384, 148, 0, [16384] + [512] * 63) == P.DYNAMIC
+    # a long tail that is not long enough: 14794 among 127 of 1500 (T = 1024, static s = 1):
+    # c = 232; units 232 + 127 x 24 = 3280 -> W = ceil(3280 * 8 / 148) = 178 -> 232 < 356: static
+    assert P.varlen_policy(128, 64, 8, 16384, 148, 0, [14794] + [1500] * 127) == P.SEQ_AWARE_SM
+    # skewed but short: the longest split would hold < 32 units (latency-bound): static
+    assert P.varlen_policy(8, 8, 1, 1024, 148, 0, [1024] + [64] * 7) == P.SEQ_AWARE_SM
+    # lengths are clamped to the capacity and empty batches are fine
+    assert P.varlen_policy(4, 64, 8, 4096, 148, 0, [0, 0, 0, 0]) == P.SEQ_AWARE_SM
