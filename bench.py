@@ -280,8 +280,9 @@ def ragged_ab(dec, dev, stream, timer, steps, rounds, l2, seed):
     lens = [cfg["l_k"]] + [1024] * (cfg["batch"] - 1)
     w = Workload(cfg, dev, seed, l2, uniform=False)
     w.seqlens = torch.tensor(lens, dtype=torch.int32, device=dev)
-    pols = ("guarded", "seq_aware_sm", "dynamic")
-    plans = {p: dec.make_plan(cfg["batch"], cfg["h_q"], cfg["h_kv"], cfg["l_k"], policy=p) for p in pols}
+    pols = ("guarded", "seq_aware_sm", "dynamic", "varlen")
+    plans = {p: dec.make_plan(cfg["batch"], cfg["h_q"], cfg["h_kv"], cfg["l_k"], policy=p) for p in pols[:3]}
+    plans["varlen"] = dec.make_plan_varlen(cfg["batch"], cfg["h_q"], cfg["h_kv"], cfg["l_k"], lens)
     graphs = {p: make_graph(dec, plans[p], w, steps, stream) for p in pols}
     res = {p: [] for p in pols}
     for _ in range(rounds):
@@ -294,6 +295,7 @@ def ragged_ab(dec, dev, stream, timer, steps, rounds, l2, seed):
         out[p] = {"num_splits": plans[p].num_splits, "combine_mode": plans[p].combine_mode,
                   "us_per_step": round(us, 2), "gbs": round(byts / (us * 1e-6) / 1e9, 1)}
     out["speedup_dynamic_vs_guarded"] = round(out["guarded"]["us_per_step"] / out["dynamic"]["us_per_step"], 3)
+    out["speedup_varlen_vs_guarded"] = round(out["guarded"]["us_per_step"] / out["varlen"]["us_per_step"], 3)
     del w, graphs
     torch.cuda.empty_cache()
     return out

@@ -197,6 +197,19 @@ DA_API da_status da_plan_make(int32_t batch, int32_t h_q, int32_t h_kv, int32_t 
                        da_plan* out);
 
 /*
+ * da_plan_make_varlen - the plan for a ragged batch whose lengths are known on the host (the
+ * metadata-then-launch path of P:L125; DESIGN.md C-ext-3).  Arguments as da_plan_make with
+ * l_cap = the cache capacity, plus host_seqlens (host int32 [batch], clamped to [0, l_cap]).
+ * Returns the DA_POLICY_SEQ_AWARE_SM plan for l_cap, unless its longest split would hold more
+ * than twice the per-CTA work W of the dynamic schedule (and at least 32 units of 64 tokens);
+ * then the DA_POLICY_DYNAMIC plan.  plan->policy tells which.  Pure host code.
+ * Errors: as da_plan_make; DA_ERR_INVALID_ARG for a NULL host_seqlens.
+ */
+DA_API da_status da_plan_make_varlen(int32_t batch, int32_t h_q, int32_t h_kv, int32_t l_cap,
+                                     int32_t head_dim, int32_t pack_gqa, int32_t sm_margin,
+                                     int32_t num_sms, const int32_t* host_seqlens, da_plan* out);
+
+/*
  * da_plan_set_combine - switch an existing plan to another combine mode and
  * re-derive its launch fields.  NONE requires s == 1, CLUSTER 2 <= s <= 16,
  * KERNEL s >= 2.  Errors: DA_ERR_INVALID_ARG.

@@ -69,6 +69,8 @@ def _load() -> ctypes.CDLL:
     i32, i64, vp, f32 = ctypes.c_int32, ctypes.c_int64, ctypes.c_void_p, ctypes.c_float
     lib.da_plan_make.argtypes = [i32] * 10 + [ctypes.POINTER(da_plan)]
     lib.da_plan_make.restype = i32
+    lib.da_plan_make_varlen.argtypes = [i32] * 8 + [vp, ctypes.POINTER(da_plan)]
+    lib.da_plan_make_varlen.restype = i32
     lib.da_plan_set_combine.argtypes = [ctypes.POINTER(da_plan), i32]
     lib.da_plan_set_combine.restype = i32
     lib.da_forward.argtypes = [ctypes.POINTER(da_plan), vp, vp, vp, i32, vp, vp, f32, i32, vp, vp,
@@ -94,7 +96,7 @@ def _load() -> ctypes.CDLL:
 
 LIB = _load()
 
-EXPORTED = ("da_plan_make", "da_plan_set_combine", "da_forward", "da_forward_paged",
+EXPORTED = ("da_plan_make", "da_plan_make_varlen", "da_plan_set_combine", "da_forward", "da_forward_paged",
             "da_forward_host_bytes", "da_forward_host", "da_combine", "da_status_string", "da_abi_version")
 
 
@@ -116,6 +118,20 @@ def da_plan_make(batch, h_q, h_kv, l_k, head_dim=128, pack_gqa=1, sm_margin=0, n
                           ctypes.byref(p))
     if st != DA_OK:
         raise DecAttnError(st, "da_plan_make")
+    return p
+
+
+def da_plan_make_varlen(batch, h_q, h_kv, l_cap, head_dim, pack_gqa, sm_margin, num_sms, host_seqlens) -> da_plan:
+    """host_seqlens: a sequence of ints (copied into a host int32 array)."""
+    lens = [int(x) for x in host_seqlens]
+    if len(lens) != int(batch):
+        raise DecAttnError(DA_ERR_INVALID_ARG, "da_plan_make_varlen: len(host_seqlens) != batch")
+    arr = (ctypes.c_int32 * max(1, len(lens)))(*lens)
+    p = da_plan()
+    st = LIB.da_plan_make_varlen(int(batch), int(h_q), int(h_kv), int(l_cap), int(head_dim), int(pack_gqa),
+                                 int(sm_margin), int(num_sms), ctypes.cast(arr, ctypes.c_void_p), ctypes.byref(p))
+    if st != DA_OK:
+        raise DecAttnError(st, "da_plan_make_varlen")
     return p
 
 

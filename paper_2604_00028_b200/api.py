@@ -50,6 +50,15 @@ def make_plan(batch, h_q, h_kv, l_k, head_dim=128, pack_gqa=True, sm_margin=0, n
                         int(sm_margin), int(sms), int(policy), int(forced_splits), combine_mode)
 
 
+def make_plan_varlen(batch, h_q, h_kv, l_cap, host_seqlens, head_dim=128, pack_gqa=True, sm_margin=0,
+                     num_sms_=None) -> L.da_plan:
+    """da_plan_make_varlen: the plan for a ragged batch whose lengths are known on the host
+    (static SM-count-aware unless the lengths are skewed enough for the dynamic schedule)."""
+    sms = num_sms_ if num_sms_ is not None else num_sms(torch.cuda.current_device())
+    return L.da_plan_make_varlen(int(batch), int(h_q), int(h_kv), int(l_cap), int(head_dim),
+                                 int(bool(pack_gqa)), int(sm_margin), int(sms), host_seqlens)
+
+
 def _kv_strides(q, k, v):
     if q.stride(-1) != 1 or k.stride(-1) != 1 or v.stride(-1) != 1:
         raise ValueError("innermost (head_dim) dimension must be contiguous")

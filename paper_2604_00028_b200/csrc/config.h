@@ -23,6 +23,7 @@ constexpr int kSmUnit = 64, kSmMinUnits = 4, kSmMinUnitsWide = 6, kSmWideT = 16;
 constexpr int kSmNarrowT = 4, kSmNarrowSplits = 8, kSmMaxSplits = 4;
 constexpr int kSmEffFloor = 8, kSmStreamUnits = 16;
 constexpr int kDynMaxSplits = 128;   // DA_POLICY_DYNAMIC per-sequence cap (C-ext-2)
+constexpr int kVarlenMinUnits = 32;  // da_plan_make_varlen: dynamic only for splits >= 2048 tokens (C-ext-3)
 
 // ---- kernel geometry (B200 side) -----------------------------
 constexpr int kHeadDim = 128;          // v1 supports d = 128 only

@@ -222,6 +222,36 @@ extern "C" da_status da_plan_make(int32_t batch, int32_t h_q, int32_t h_kv, int3
   return DA_OK;
 }
 
+// C-ext-3: the plan for a ragged batch whose lengths are on the host.  The static SM-count-aware
+// plan for the capacity, unless its longest split would hold more than 2 W units (W the dynamic
+// schedule's per-CTA work) and at least kVarlenMinUnits; then DA_POLICY_DYNAMIC.
+extern "C" da_status da_plan_make_varlen(int32_t batch, int32_t h_q, int32_t h_kv, int32_t l_cap,
+                                         int32_t head_dim, int32_t pack_gqa, int32_t sm_margin,
+                                         int32_t num_sms, const int32_t* host_seqlens, da_plan* out) {
+  if (host_seqlens == nullptr || out == nullptr) return DA_ERR_INVALID_ARG;
+  da_plan st{};
+  da_status r = da_plan_make(batch, h_q, h_kv, l_cap, head_dim, pack_gqa, sm_margin, num_sms,
+                             DA_POLICY_SEQ_AWARE_SM, 0, &st);
+  if (r != DA_OK) return r;
+  int64_t total = 0, u_max = 0;
+  for (int32_t b = 0; b < batch; ++b) {
+    int64_t n = host_seqlens[b];
+    n = n < 0 ? 0 : (n > l_cap ? l_cap : n);
+    const int64_t u = ceil_div(n, kSplitUnit);
+    total += u;
+    if (u > u_max) u_max = u;
+  }
+  const int64_t tiles = static_cast<int64_t>(h_kv) * st.num_m_blocks;
+  int64_t W = ceil_div(total * tiles, st.usable_sms);
+  if (W < 1) W = 1;
+  const int64_t c = ceil_div(u_max, st.num_splits);
+  if (c > 2 * W && c >= kVarlenMinUnits)
+    return da_plan_make(batch, h_q, h_kv, l_cap, head_dim, pack_gqa, sm_margin, num_sms,
+                        DA_POLICY_DYNAMIC, 0, out);
+  *out = st;
+  return DA_OK;
+}
+
 extern "C" da_status da_plan_set_combine(da_plan* plan, int32_t combine_mode) {
   if (plan == nullptr) return DA_ERR_INVALID_ARG;
   if (!combine_mode_valid(combine_mode, plan->num_splits)) return DA_ERR_INVALID_ARG;

@@ -283,7 +283,7 @@ RAGGED_CASES = {
     "long_b1_h8": (1, 64, 8, 131072, lambda B, L, g: [L]),
     "uniform_b128_h8": (128, 64, 8, 8192, lambda B, L, g: [L] * B),   # high-load: identical work, s_b = 1
 }
-RAGGED_POLICIES = ("guarded", "seq_aware_sm", "dynamic")
+RAGGED_POLICIES = ("guarded", "seq_aware_sm", "dynamic", "varlen")
 
 
 def ragged():
@@ -301,7 +301,8 @@ def ragged():
         w.seqlens = torch.tensor(lens, dtype=torch.int32, device=dev)
         stream = torch.cuda.Stream()
         timer = bench.Timer(dev)
-        plans = [dec.make_plan(B, hq, hkv, L, policy=p) for p in RAGGED_POLICIES]
+        plans = [dec.make_plan_varlen(B, hq, hkv, L, lens) if p == "varlen" else dec.make_plan(B, hq, hkv, L, policy=p)
+                 for p in RAGGED_POLICIES]
         kv = 4 * sum(lens) * hkv * D
         steps = 200 if kv * w.nbuf < (64 << 20) or kv < (16 << 20) else (40 if kv < (512 << 20) else 10)
         graphs = [bench.make_graph(dec, p, w, steps, stream) for p in plans]
@@ -318,7 +319,7 @@ def ragged():
                              gbs=round(alg / t / 1e3, 1), speedup_vs_guarded=round(med[0] / t, 4)))
         print(f"{name:14s} tokens {sum(lens):8d} max {max(lens):6d}: " +
               "  ".join(f"{pol} s={p.num_splits} {t:8.2f} us" for pol, p, t in zip(RAGGED_POLICIES, plans, med)) +
-              f"   dynamic {med[0] / med[2]:.2f}x vs guarded, {med[1] / med[2]:.2f}x vs seq_aware_sm", flush=True)
+              f"   dynamic {med[0] / med[2]:.2f}x, varlen {med[0] / med[3]:.2f}x vs guarded", flush=True)
         del graphs, w, timer
         torch.cuda.empty_cache()
     write("ragged", rows, ["case", "batch", "h_q", "h_kv", "l_cap", "total_tokens", "max_len", "policy",

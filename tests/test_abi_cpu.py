@@ -306,3 +306,28 @@ def test_forward_host_validation(L):
     assert st(device_buffer=None) == L.DA_ERR_WORKSPACE
     assert st(device_buffer_bytes=need - 1) == L.DA_ERR_WORKSPACE
     assert st(device_buffer=6 * A + 128) == L.DA_ERR_ALIGNMENT
+
+
+def test_plan_make_varlen_matches_oracle(L):
+    rng = random.Random(23)
+    for _ in range(3000):
+        B = rng.randint(1, 96)
+        hkv = rng.choice([1, 2, 4, 8])
+        G = rng.choice([1, 8, 16])
+        l_cap = rng.choice([64, 512, 2048, 8192, 32768, 131072])
+        sms = rng.choice([148, 132])
+        kind = rng.random()
+        if kind < 0.3:
+            lens = [l_cap] * B
+        elif kind < 0.6:
+            lens = [rng.randint(0, l_cap) for _ in range(B)]
+        else:
+            lens = [rng.randint(0, max(1, l_cap // 32)) for _ in range(B)]
+            lens[rng.randrange(B)] = l_cap
+        p = L.da_plan_make_varlen(B, G * hkv, hkv, l_cap, 128, 1, 0, sms, lens)
+        pol = OP.varlen_policy(B, G * hkv, hkv, l_cap, sms, 0, lens)
+        assert p.policy == pol, (B, hkv, G, l_cap, lens[:4])
+        ref = L.da_plan_make(B, G * hkv, hkv, l_cap, 128, 1, 0, sms, pol, 0)
+        assert p.as_dict() == ref.as_dict()
+    with pytest.raises(L.DecAttnError):
+        L.da_plan_make_varlen(2, 8, 1, 512, 128, 1, 0, 148, [1])      # wrong length count
