@@ -6,34 +6,39 @@
 // ("num_splits ... sequence-level parallelization across SMs", §3.1),
 // so s is exactly the paper's knob: s = 1 launches B*H_KV CTAs ("as few as 8
 // Thread Blocks"), s = 3 triples them.
+// DA_POLICY_DYNAMIC (kDyn, C-ext-2): grid = (Y, slots, 1); the (sequence, split)
+// of a slot is derived on the device from cache_seqlens (dyn_schedule).
 //
-// Inside a CTA:
-//   warp NS     TMA producer: one elected lane streams 64-token K/V tiles
-//               (4 boxes of 64 tokens x 64 dims, 128B-swizzled) through an
-//               NS-stage mbarrier ring (step a3, KV streaming); NS = 6, or 5
-//               for cluster kernels (their DSMEM push slots need the room).
-//   warps 0..NS-1  consumers: warp w owns ring stage w, i.e. tiles w, w+NS, ...,
-//               and keeps its own online-softmax state (steps a4-a6):
+// Inside a CTA, NS ring stages and NW consumer warps per combine
+// mode (config.h: NONE 7 / 7, CLUSTER 6 / 3 + 4 helper warps, KERNEL 4 / 4):
+//   warp NW     TMA producer: one lane streams 64-token tiles, one 5-D box for K
+//               and one for V (64 tokens x 2 x 64 dims, 128B-swizzled, 32 KB per
+//               stage) through the mbarrier ring (step a3, KV streaming).
+//   warps 0..NW-1  consumers: warp w owns ring stages w, w+NW, ... (tiles w,
+//               w+NW, ...) and keeps its own online-softmax state (a4-a6):
 //               MMA path  S^T = K Q^T and O^T += V^T P^T with
 //                         mma.sync.m16n8k16 (bf16 -> fp32): tokens and head
 //                         dims fill the M = 16 side, the G query rows the
 //                         N = 8 side, so no MMA lane is padding for G = 8;
 //                         P^T is re-laid out register-to-register with
-//                         movmatrix.trans.
+//                         movmatrix.trans and enters the PV product as the
+//                         bf16 pair P_hi + P_lo (two MMAs).
 //               scalar    lane-per-token fp32 dot products, warp-shuffle
 //                         max / sum, lane-per-4-dims PV.
+//   helpers     (CLUSTER) idle through the main loop, then join the merges.
 //   epilogue    the consumer warps' (m, l, O) merge in shared memory; then
-//               s == 1   : bf16/fp32 out + lse written directly (a7);
-//               CLUSTER  : the s CTAs form one thread-block cluster; ranks
-//                          1..s-1 push (m, l, O) into rank 0's shared memory
-//                          with st.async (bytes counted on rank 0's mbarrier)
-//                          and rank 0 does the LSE combine (a8): no
-//                          workspace, no second launch, no cluster-wide barrier
-//                          on the exit path;
+//               NONE     : bf16/fp32 out + lse written directly (a7);
+//               CLUSTER  : the s CTAs form one thread-block cluster; row g is
+//                          owned by rank g mod s, every rank st.async-pushes
+//                          its (m, l, O) of g into the owner's shared memory
+//                          (bytes counted on the owner's mbarrier) and the
+//                          owner does the LSE combine (a8): no workspace, no
+//                          second launch, no cluster-wide barrier on exit;
 //               KERNEL   : normalised fp32 partials + lse go to the
 //                          workspace for lse_combine_kernel (combine.cu).
-// Scores are kept in the log2 domain (scale * log2 e folded into one FMUL);
-// lse is returned in natural log (C-amb-10).
+// Programmatic dependent launch: the prologue overlaps the previous kernel's
+// tail; griddepcontrol.wait precedes the first global read.  Scores are kept in
+// the log2 domain; lse is returned in natural log (C-amb-10).
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
