@@ -1,8 +1,10 @@
-// Split planner: da_plan_make / da_plan_set_combine (host-only, integer-only).
+// Split planner: da_plan_make / da_plan_make_varlen / da_plan_set_combine (host-only,
+// integer-only).
 //
 // Implements the decision the paper is about: how many sequence splits a
-// decode-attention launch uses.  The paper's two policies (plus FIXED, the
-// evolved Fig. 1 fragment and the SM-count-aware generalisation C-ext-1):
+// decode-attention launch uses.  The paper's two policies, plus FIXED, the
+// evolved Fig. 1 fragment, the SM-count-aware generalisation (C-ext-1), the
+// per-batch dynamic counts (C-ext-2) and the host-side choice between them (C-ext-3):
 //   * guarded   - FA3's default (§2.2 "returns s=1 if the sequence
 //                 length L_K <= 512"; §4.2 "strictly enforced s=1 when
 //                 num_n_blocks <= 4"), behind the saturation guard and ahead
@@ -10,7 +12,7 @@
 //   * seq-aware - the paper's Fig. 3 cascade: Guard 1, Guard 2,
 //                 the low-tile override s = 3, else the unchanged loop.
 // Every comparison is an exact integer cross-multiplication (C-amb-3), so the
-// result is bit-identical to the CPU oracle's (tests/test_plan_parity.py).
+// result is bit-identical to the CPU oracle's (tests/test_abi_cpu.py).
 // This file shares no code with oracle/: it is the product-side statement.
 #include <cstdint>
 
