@@ -273,6 +273,22 @@ def streaming_roofline(dec, dev, stream, timer, cfg, steps, rounds, l2, seed, pe
 RAGGED_AB = dict(batch=16, h_q=64, h_kv=8, l_k=32768)   # one 32768-token sequence + fifteen of 1024
 
 
+def latency_floor(dec, dev, stream, timer, cfg, steps, rounds, l2, seed, us_headline):
+    """The latency floor of the headline step on this kernel: the same shape and combine path with
+    ONE 64-token tile per CTA (L_K = 64, s = 1), i.e. launch + PDL hop + one TMA round trip + one
+    tile + the store.  frac = floor / headline: how close the latency-bound step is to it."""
+    fcfg = dict(cfg, l_k=64)
+    w = Workload(fcfg, dev, seed, l2)
+    plan = dec.make_plan(fcfg["batch"], fcfg["h_q"], fcfg["h_kv"], 64, policy="fixed", forced_splits=1)
+    g = make_graph(dec, plan, w, steps, stream)
+    us = statistics.median([timer.time_replay(g, stream) * 1e3 / steps for _ in range(rounds)])
+    del w, g
+    torch.cuda.empty_cache()
+    return {"us_per_step": round(us, 3), "config": dict(fcfg, num_splits=1),
+            "frac_of_headline": round(us / us_headline, 4),
+            "note": "same kernel, one 64-token tile per CTA: launch, PDL hop, one TMA round trip, one tile, store"}
+
+
 def ragged_ab(dec, dev, stream, timer, steps, rounds, l2, seed):
     """Per-batch dynamic split counts (DA_POLICY_DYNAMIC, DESIGN.md C-ext-2) vs the static policies on
     a skewed ragged batch; the static plans see the cache capacity, the dynamic schedule the lengths."""
@@ -553,6 +569,9 @@ def main():
             "long_context": streaming_roofline(dec, dev, stream, timer, WORKLOADS["long_context"], 20, 7, l2, 1004, peak),
         }
         extras["ragged_ab"] = ragged_ab(dec, dev, stream, timer, 20, 7, l2, 1005)
+        if args.workload in ("llama70b", "llama70b_tp8", "mqa_tiny"):
+            extras["latency_floor"] = latency_floor(dec, dev, stream, timer, local_cfg, args.steps, 11, l2, 1006,
+                                                    ms * 1e3 / args.steps)
     if world > 1:
         barrier()
     if rank != 0:
