@@ -227,6 +227,11 @@ def test_forward_validation(L):
     assert _fwd(L, bad) == L.DA_ERR_INVALID_ARG
 
 
+def test_forward_rejects_oversized_grid(L):
+    p = L.da_plan_make(70000, 8, 1, 64, 128, 1, 0, 148, "guarded", 0)   # grid_z = 70000 > 65535
+    assert _fwd(L, p) == L.DA_ERR_UNSUPPORTED
+
+
 def test_combine_validation(L):
     def st(**kw):
         args = dict(num_splits=3, batch=1, h_q=8, head_dim=128, o_partial=A, o_split_stride=1024,

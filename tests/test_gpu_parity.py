@@ -107,6 +107,19 @@ def test_group_sizes_mma_path(h_q, h_kv):
     run_and_check(2, h_q, h_kv, 300, seed=21)
 
 
+@pytest.mark.parametrize("batch,h_q,h_kv,l_k,policy", [(1, 128, 1, 1000, "seq_aware"), (2, 256, 2, 700, "seq_aware_sm"),
+                                                       (1, 128, 1, 3000, "dynamic")])
+def test_many_query_rows_per_kv_head(batch, h_q, h_kv, l_k, policy):
+    # G = 128: two policy m-blocks (T = 2 B H_KV) and eight 16-row CTAs per KV head on the MMA path
+    plan, _, _ = run_and_check(batch, h_q, h_kv, l_k, policy=policy, variant="ragged", seed=1500)
+    assert plan.num_m_blocks == 2 and plan.rows_per_cta == 16
+
+
+def test_large_batch_small_cache():
+    plan, _, _ = run_and_check(2000, 8, 1, 64, policy="seq_aware_sm", variant="ragged", seed=1510)
+    assert plan.grid_z == 2000
+
+
 @pytest.mark.parametrize("h_q,h_kv", [(8, 1), (16, 2), (8, 8)])
 def test_scalar_path_unpacked(h_q, h_kv):
     plan, _, _ = run_and_check(2, h_q, h_kv, 333, pack_gqa=False, seed=31)
@@ -308,7 +321,8 @@ def test_paged_rejects_unsupported_page_size():
                          [(1, 64, 8, 512, "seq_aware_sm", 0, False, False),
                           (3, 24, 3, 1500, "fixed", 40, True, False),     # workspace combine
                           (2, 8, 1, 700, "seq_aware", 0, True, True),
-                          (1, 8, 8, 130, "guarded", 0, False, False)])    # scalar path
+                          (1, 8, 8, 130, "guarded", 0, False, False),     # scalar path
+                          (4, 32, 4, 3000, "dynamic", 0, True, False)])   # dynamic: schedule in staging
 def test_forward_host_matches_oracle(batch, h_q, h_kv, l_k, policy, forced, seqlens, f32):
     dec = _dec()
     inp = synth.make_inputs(batch, h_q, h_kv, l_k, seed=1200, variant="ragged" if seqlens else "normal")
