@@ -430,6 +430,9 @@ def main():
     ap.add_argument("--no-extras", action="store_true", help="skip the A/B and streaming extras")
     ap.add_argument("--ab-rounds", type=int, default=21)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--exchange", default="p2p", choices=["nccl", "p2p"],
+                    help="long_context with N > 1: the peer-memory exchange (default) or NCCL all-gather + combine "
+                         "(da_peer_signal + da_combine_peers over torch symmetric memory)")
     ap.add_argument("--policy", default="seq_aware_sm",
                     choices=["seq_aware_sm", "seq_aware", "guarded", "evolved"],
                     help="split policy of the headline step (default: the SM-count-aware sequence-aware "
@@ -485,9 +488,9 @@ def main():
     cfg = WORKLOADS[args.workload]
     long_sharded = args.workload == "long_context" and world > 1
     if long_sharded:
-        from paper_2604_00028_b200.dist import SeqShardedDecode
-        sd = SeqShardedDecode(cfg["batch"], cfg["h_q"], cfg["h_kv"], cfg["l_k"], HEAD_DIM, device=dev,
-                              policy=args.policy)
+        from paper_2604_00028_b200.dist import PeerSeqShardedDecode, SeqShardedDecode
+        cls = PeerSeqShardedDecode if args.exchange == "p2p" else SeqShardedDecode
+        sd = cls(cfg["batch"], cfg["h_q"], cfg["h_kv"], cfg["l_k"], HEAD_DIM, device=dev, policy=args.policy)
         local_cfg = dict(cfg, l_k=sd.l_local)
         inp = synth.make_inputs(cfg["batch"], cfg["h_q"], cfg["h_kv"], sd.l_local, device=dev, seed=1000 + rank)
         out = torch.empty((cfg["batch"], cfg["h_q"], HEAD_DIM), dtype=torch.bfloat16, device=dev)
@@ -502,10 +505,11 @@ def main():
             for _ in range(args.steps):
                 sd.step(inp["q"], inp["k"], inp["v"], None, out, lse)
         step_bytes_total = alg_bytes(cfg["batch"], cfg["h_q"], cfg["h_kv"], cfg["l_k"])
-        kernels_per_step = (2 if plan.combine_mode == L.DA_COMBINE_KERNEL else 1) + 1
+        kernels_per_step = (2 if plan.combine_mode == L.DA_COMBINE_KERNEL else 1) + (2 if args.exchange == "p2p" else 1)
         scaling = "strong"
         l2_note = "sequence shard per rank > 2x L2 + 256 MiB L2 scrub before the timed replay"
-        parallelism = f"seq-sharded sp{world} + NCCL all-gather + LSE combine"
+        parallelism = (f"seq-sharded sp{world} + peer-memory exchange (signal + pull-combine)" if args.exchange == "p2p"
+                       else f"seq-sharded sp{world} + NCCL all-gather + LSE combine")
     else:
         local_cfg = cfg
         w = Workload(cfg, dev, 1000 + rank, l2)

@@ -45,7 +45,7 @@
 extern "C" {
 #endif
 
-#define DA_ABI_VERSION 2
+#define DA_ABI_VERSION 3
 
 #if defined(__GNUC__)
 #define DA_API __attribute__((visibility("default")))
@@ -318,6 +318,41 @@ DA_API da_status da_combine(int32_t num_splits, int32_t batch, int32_t h_q, int3
                      const float* o_partial, int64_t o_split_stride,
                      const float* lse_partial, int64_t lse_split_stride,
                      int32_t out_dtype, void* out, float* lse, void* cuda_stream);
+
+/*
+ * Cross-GPU exchange of sequence-shard partials over peer memory (the long-context
+ * configs shard the sequence across GPUs and merge the per-GPU (out, lse) partials).
+ * Every rank owns an exchange buffer mapped on all ranks (e.g. torch symmetric memory), all with
+ * one layout: two partial slots of slot_bytes at 0 and slot_bytes, each
+ *   [0, lse_offset)            o fp32 [batch, h_q, head_dim]
+ *   [lse_offset, ...)          lse fp32 [batch, h_q]
+ * then, at flag_offset >= 2 slot_bytes, one uint32 flag per source rank, zero before the first
+ * step.  slot_bytes and lse_offset are multiples of 16.
+ * peer_bases: DEVICE array of `world` base addresses (uint64), entry q = rank q's buffer as mapped
+ * on this GPU.  epoch: device int32 owned by this rank, zero before the first step.
+ *
+ * da_peer_signal - e = *epoch + 1: copy this rank's partial (o_local fp32 [batch, h_q, head_dim],
+ * lse_local fp32 [batch, h_q] - da_forward with out_dtype = DA_F32 writes them; lse_local NULL
+ * means empty rows) into slot e & 1 of its own buffer, fence (system scope), release e into flag
+ * slot `rank` of every rank's buffer, *epoch = e.  Enqueue after the forward.
+ * da_combine_peers - every CTA waits (acquire, system scope) until all `world` flags of this
+ * rank's buffer reach *epoch, then merges the world partials of slot *epoch & 1, read from the
+ * peers' buffers, with the LSE identity of da_combine (C-comb) into out (out_dtype) and lse (fp32,
+ * may be NULL).
+ * A rank overwrites slot e & 1 again only at step e + 2, after every peer has signalled step e + 1,
+ * i.e. finished combining step e.  The flags carry monotonic epochs, so both calls can be captured
+ * in a CUDA graph and replayed.
+ * Errors: DA_ERR_INVALID_ARG (world not in [1, 64], rank, NULL pointers, overlapping regions),
+ * DA_ERR_UNSUPPORTED (head_dim != 128), DA_ERR_ALIGNMENT, DA_ERR_CUDA.
+ */
+DA_API da_status da_peer_signal(int32_t world, int32_t rank, const uint64_t* peer_bases, const float* o_local,
+                                const float* lse_local, int32_t batch, int32_t h_q, int32_t head_dim,
+                                int64_t slot_bytes, int64_t lse_offset, int64_t flag_offset, int32_t* epoch,
+                                void* cuda_stream);
+DA_API da_status da_combine_peers(int32_t world, int32_t rank, const uint64_t* peer_bases, int64_t slot_bytes,
+                                  int64_t lse_offset, int64_t flag_offset, const int32_t* epoch, int32_t batch,
+                                  int32_t h_q, int32_t head_dim, int32_t out_dtype, void* out, float* lse,
+                                  void* cuda_stream);
 
 /* Static, NUL-terminated description of a status code (never NULL). */
 DA_API const char* da_status_string(int32_t status);

@@ -28,7 +28,7 @@ DA_OK, DA_ERR_INVALID_ARG, DA_ERR_UNSUPPORTED, DA_ERR_ALIGNMENT, DA_ERR_WORKSPAC
 DA_BF16, DA_F32 = 0, 1
 DA_COMBINE_NONE, DA_COMBINE_CLUSTER, DA_COMBINE_KERNEL = range(3)
 DA_PATH_SCALAR, DA_PATH_MMA = 0, 1
-DA_ABI_VERSION = 2
+DA_ABI_VERSION = 3
 
 POLICIES = {"guarded": DA_POLICY_GUARDED, "seq_aware": DA_POLICY_SEQ_AWARE, "fixed": DA_POLICY_FIXED,
             "evolved": DA_POLICY_EVOLVED, "seq_aware_sm": DA_POLICY_SEQ_AWARE_SM, "dynamic": DA_POLICY_DYNAMIC}
@@ -83,6 +83,10 @@ def _load() -> ctypes.CDLL:
     lib.da_forward_host_bytes.restype = i64
     lib.da_forward_host.argtypes = [ctypes.POINTER(da_plan), vp, vp, vp, i32, vp, f32, i32, vp, vp, vp, i64, vp]
     lib.da_forward_host.restype = i32
+    lib.da_peer_signal.argtypes = [i32, i32, vp, vp, vp, i32, i32, i32, i64, i64, i64, vp, vp]
+    lib.da_peer_signal.restype = i32
+    lib.da_combine_peers.argtypes = [i32, i32, vp, i64, i64, i64, vp, i32, i32, i32, i32, vp, vp, vp]
+    lib.da_combine_peers.restype = i32
     lib.da_combine.argtypes = [i32, i32, i32, i32, vp, i64, vp, i64, i32, vp, vp, vp]
     lib.da_combine.restype = i32
     lib.da_status_string.argtypes = [i32]
@@ -97,7 +101,8 @@ def _load() -> ctypes.CDLL:
 LIB = _load()
 
 EXPORTED = ("da_plan_make", "da_plan_make_varlen", "da_plan_set_combine", "da_forward", "da_forward_paged",
-            "da_forward_host_bytes", "da_forward_host", "da_combine", "da_status_string", "da_abi_version")
+            "da_forward_host_bytes", "da_forward_host", "da_combine", "da_peer_signal", "da_combine_peers",
+            "da_status_string", "da_abi_version")
 
 
 def da_status_string(status: int) -> str:
@@ -204,6 +209,24 @@ def da_forward_host(plan: da_plan, q, k_cache, v_cache, l_cap, cache_seqlens, so
                              _ptr(device_buffer), int(device_buffer_bytes), _stream_handle(stream))
     if st != DA_OK:
         raise DecAttnError(st, "da_forward_host")
+
+
+def da_peer_signal(world, rank, peer_bases, o_local, lse_local, batch, h_q, head_dim, slot_bytes, lse_offset,
+                   flag_offset, epoch, stream=None) -> None:
+    st = LIB.da_peer_signal(int(world), int(rank), _ptr(peer_bases), _ptr(o_local), _ptr(lse_local), int(batch),
+                            int(h_q), int(head_dim), int(slot_bytes), int(lse_offset), int(flag_offset), _ptr(epoch),
+                            _stream_handle(stream))
+    if st != DA_OK:
+        raise DecAttnError(st, "da_peer_signal")
+
+
+def da_combine_peers(world, rank, peer_bases, slot_bytes, lse_offset, flag_offset, epoch, batch, h_q, head_dim,
+                     out_dtype, out, lse, stream=None) -> None:
+    st = LIB.da_combine_peers(int(world), int(rank), _ptr(peer_bases), int(slot_bytes), int(lse_offset),
+                              int(flag_offset), _ptr(epoch), int(batch), int(h_q), int(head_dim), int(out_dtype),
+                              _ptr(out), _ptr(lse), _stream_handle(stream))
+    if st != DA_OK:
+        raise DecAttnError(st, "da_combine_peers")
 
 
 def da_combine(num_splits, batch, h_q, head_dim, o_partial, o_split_stride, lse_partial,

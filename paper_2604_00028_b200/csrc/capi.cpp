@@ -1,4 +1,5 @@
-// C ABI: da_forward / da_forward_paged / da_forward_host / da_combine / da_status_string / da_abi_version
+// C ABI: da_forward / da_forward_paged / da_forward_host / da_combine / da_peer_signal / da_combine_peers /
+// da_status_string / da_abi_version
 // (da_plan_make, da_plan_set_combine live in plan.cpp).  See
 // include/decattn.h for the contract of every entry point.
 //
@@ -298,6 +299,61 @@ extern "C" da_status da_forward_host(const da_plan* plan, const void* q, const v
       cudaMemcpyAsync(lse, dlse, size_t(B * HQ * 4), cudaMemcpyDeviceToHost, stream) != cudaSuccess)
     return DA_ERR_CUDA;
   return DA_OK;
+}
+
+namespace {
+// da_peer_signal / da_combine_peers: the exchange-buffer layout of include/decattn.h.
+da_status check_peer_layout(int32_t world, int32_t rank, const uint64_t* peer_bases, const void* epoch,
+                            int32_t batch, int32_t h_q, int32_t head_dim, int64_t slot_bytes, int64_t lse_offset,
+                            int64_t flag_offset, int64_t* rows_out) {
+  if (world < 1 || world > kMaxPeers || rank < 0 || rank >= world || peer_bases == nullptr || epoch == nullptr ||
+      batch < 1 || h_q < 1)
+    return DA_ERR_INVALID_ARG;
+  if (head_dim != kHeadDim) return DA_ERR_UNSUPPORTED;
+  const int64_t rows = int64_t(batch) * h_q;
+  if (rows > INT32_MAX) return DA_ERR_INVALID_ARG;
+  if (lse_offset < rows * kHeadDim * 4 || slot_bytes < lse_offset + rows * 4 || flag_offset < 2 * slot_bytes)
+    return DA_ERR_INVALID_ARG;
+  if ((slot_bytes & 15) != 0 || (lse_offset & 15) != 0 || (flag_offset & 3) != 0 ||
+      (reinterpret_cast<uintptr_t>(epoch) & 3u) != 0)
+    return DA_ERR_ALIGNMENT;
+  *rows_out = rows;
+  return DA_OK;
+}
+}  // namespace
+
+extern "C" da_status da_peer_signal(int32_t world, int32_t rank, const uint64_t* peer_bases, const float* o_local,
+                                    const float* lse_local, int32_t batch, int32_t h_q, int32_t head_dim,
+                                    int64_t slot_bytes, int64_t lse_offset, int64_t flag_offset, int32_t* epoch,
+                                    void* cuda_stream) {
+  int64_t rows = 0;
+  da_status st = check_peer_layout(world, rank, peer_bases, epoch, batch, h_q, head_dim, slot_bytes, lse_offset,
+                                   flag_offset, &rows);
+  if (st != DA_OK) return st;
+  if (o_local == nullptr) return DA_ERR_INVALID_ARG;
+  if (!aligned16(o_local) || (lse_local != nullptr && (reinterpret_cast<uintptr_t>(lse_local) & 3u) != 0))
+    return DA_ERR_ALIGNMENT;
+  return launch_peer_signal(peer_bases, world, rank, o_local, lse_local, static_cast<int32_t>(rows), slot_bytes,
+                            lse_offset, flag_offset, epoch, static_cast<cudaStream_t>(cuda_stream)) == cudaSuccess
+             ? DA_OK
+             : DA_ERR_CUDA;
+}
+
+extern "C" da_status da_combine_peers(int32_t world, int32_t rank, const uint64_t* peer_bases, int64_t slot_bytes,
+                                      int64_t lse_offset, int64_t flag_offset, const int32_t* epoch, int32_t batch,
+                                      int32_t h_q, int32_t head_dim, int32_t out_dtype, void* out, float* lse,
+                                      void* cuda_stream) {
+  int64_t rows = 0;
+  da_status st = check_peer_layout(world, rank, peer_bases, epoch, batch, h_q, head_dim, slot_bytes, lse_offset,
+                                   flag_offset, &rows);
+  if (st != DA_OK) return st;
+  if (out == nullptr || (out_dtype != DA_BF16 && out_dtype != DA_F32)) return DA_ERR_INVALID_ARG;
+  if (!aligned16(out) || (lse != nullptr && (reinterpret_cast<uintptr_t>(lse) & 3u) != 0)) return DA_ERR_ALIGNMENT;
+  return launch_peer_combine(peer_bases, slot_bytes, lse_offset, flag_offset, epoch, world, rank,
+                             static_cast<int32_t>(rows), out_dtype == DA_F32, out, lse,
+                             static_cast<cudaStream_t>(cuda_stream)) == cudaSuccess
+             ? DA_OK
+             : DA_ERR_CUDA;
 }
 
 extern "C" da_status da_combine(int32_t num_splits, int32_t batch, int32_t h_q, int32_t head_dim,

@@ -143,6 +143,108 @@ __global__ void __launch_bounds__(kCombineThreads)
   CTRACE(2);
 }
 
+// ---- cross-GPU exchange over peer memory --------------------------------------
+// Every rank owns a buffer mapped on every GPU (torch symmetric memory) with two partial slots
+// (o fp32 [B, H_Q, d] at 0, lse fp32 [B, H_Q] at lse_offset within a slot of slot_bytes) and one
+// uint32 flag per source rank at flag_offset.  The flags carry a step epoch (monotonic: no reset,
+// CUDA-graph replayable); step e uses slot e & 1, so a rank that runs ahead overwrites the slot of
+// step e - 1 only: every peer has finished reading it (it signalled step e after combining e - 1).
+
+// One CTA: e = *epoch + 1; copy this rank's partial (written by the forward into local memory)
+// into slot e & 1 of its own exchange buffer; fence (system scope); release e into slot `rank`
+// of every peer's flags; *epoch = e.
+__global__ void __launch_bounds__(256)
+    peer_signal_kernel(const uint64_t* peer_bases, int32_t world, int32_t rank, const float* o_local,
+                       const float* lse_local, int32_t rows, int64_t slot_bytes, int64_t lse_offset,
+                       int64_t flag_offset, int32_t* epoch) {
+  const uint32_t e = static_cast<uint32_t>(*epoch) + 1u;
+  const uint64_t slot = peer_bases[rank] + static_cast<uint64_t>(slot_bytes) * (e & 1u);
+  float4* dst = reinterpret_cast<float4*>(slot);
+  const float4* src = reinterpret_cast<const float4*>(o_local);
+  for (int i = threadIdx.x; i < rows * (kHeadDim / 4); i += blockDim.x) dst[i] = src[i];
+  float* dl = reinterpret_cast<float*>(slot + static_cast<uint64_t>(lse_offset));
+  for (int i = threadIdx.x; i < rows; i += blockDim.x) dl[i] = lse_local != nullptr ? lse_local[i] : kNegInf;
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  fence_acq_rel_sys();
+  for (int q = 0; q < world; ++q) {
+    uint32_t* flags = reinterpret_cast<uint32_t*>(peer_bases[q] + static_cast<uint64_t>(flag_offset));
+    st_release_sys_u32(flags + rank, e);
+  }
+  *epoch = static_cast<int32_t>(e);
+}
+
+// One CTA (4 warps) per (b, h) row: thread 0 acquires every rank's flag at this step's epoch, then
+// the row's P partials are read from the peers' buffers (NVLink loads, coherent: no __ldg) and
+// merged exactly like lse_combine_kernel (per-warp online max, warp-level rescale merge).
+__global__ void __launch_bounds__(kCombineThreads)
+    peer_combine_kernel(const uint64_t* peer_bases, int64_t slot_bytes, int64_t lse_offset, int64_t flag_offset,
+                        const int32_t* epoch, int32_t world, int32_t rank, int32_t rows, int32_t out_f32,
+                        void* out, float* lse_out) {
+  pdl_launch_dependents();
+  pdl_wait();
+  constexpr int kWarps = kCombineThreads / 32;
+  __shared__ float4 s_acc[kWarps][32];
+  __shared__ float s_m[kWarps], s_l[kWarps];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int row = blockIdx.x;
+  const uint32_t e = static_cast<uint32_t>(*epoch);
+  if (threadIdx.x == 0) {
+    const uint32_t* flags =
+        reinterpret_cast<const uint32_t*>(peer_bases[rank] + static_cast<uint64_t>(flag_offset));
+    for (int q = 0; q < world; ++q)
+      while (ld_acquire_sys_u32(flags + q) < e) {
+      }
+  }
+  __syncthreads();
+  const uint64_t slot_off = static_cast<uint64_t>(slot_bytes) * (e & 1u);
+  float m = kNegInf, Lw = 0.f;
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int i = warp; i < world; i += kWarps) {
+    const uint64_t base = peer_bases[i] + slot_off;
+    const float li = reinterpret_cast<const float*>(base + static_cast<uint64_t>(lse_offset))[row] * kLog2e;
+    const float4 oi = reinterpret_cast<const float4*>(base)[static_cast<int64_t>(row) * (kHeadDim / 4) + lane];
+    const float mb = fmaxf(m, li);
+    if (mb == kNegInf) continue;                           // every partial so far empty
+    const float r = ex2(m - mb), wgt = ex2(li - mb);
+    Lw = fmaf(Lw, r, wgt);
+    acc = make_float4(fmaf(acc.x, r, wgt * oi.x), fmaf(acc.y, r, wgt * oi.y), fmaf(acc.z, r, wgt * oi.z),
+                      fmaf(acc.w, r, wgt * oi.w));
+    m = mb;
+  }
+  s_acc[warp][lane] = acc;
+  if (lane == 0) { s_m[warp] = m; s_l[warp] = Lw; }
+  __syncthreads();
+  if (warp != 0) return;
+  float M = kNegInf;
+#pragma unroll
+  for (int w = 0; w < kWarps; ++w) M = fmaxf(M, s_m[w]);
+  const bool empty = M == kNegInf;
+  float L = 0.f;
+  float4 sum = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (!empty) {
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) {
+      const float c = ex2(s_m[w] - M);
+      L = fmaf(c, s_l[w], L);
+      const float4 a = s_acc[w][lane];
+      sum = make_float4(fmaf(c, a.x, sum.x), fmaf(c, a.y, sum.y), fmaf(c, a.z, sum.z), fmaf(c, a.w, sum.w));
+    }
+  }
+  const float inv = L > 0.f ? __frcp_rn(L) : 0.f;
+  sum = make_float4(sum.x * inv, sum.y * inv, sum.z * inv, sum.w * inv);
+  DA_DASSERT(row < rows);
+  if (out_f32) {
+    reinterpret_cast<float4*>(out)[static_cast<int64_t>(row) * (kHeadDim / 4) + lane] = sum;
+  } else {
+    uint2 w2;
+    w2.x = pack_bf16(sum.x, sum.y);
+    w2.y = pack_bf16(sum.z, sum.w);
+    reinterpret_cast<uint2*>(out)[static_cast<int64_t>(row) * (kHeadDim / 4) + lane] = w2;
+  }
+  if (lane == 0 && lse_out != nullptr) lse_out[row] = empty ? kNegInf : (M + lg2(L)) * (1.f / kLog2e);
+}
+
 }  // namespace
 
 cudaError_t launch_lse_combine(const CombineParams& p, bool pdl, cudaStream_t stream) {
@@ -165,5 +267,29 @@ extern "C" __attribute__((visibility("default"))) int da_trace_fetch_combine(uns
   return cudaMemcpyFromSymbol(host, g_trace_comb, sizeof(unsigned long long) * n) == cudaSuccess ? 0 : 1;
 }
 #endif
+
+cudaError_t launch_peer_signal(const uint64_t* peer_bases, int32_t world, int32_t rank, const float* o_local,
+                               const float* lse_local, int32_t rows, int64_t slot_bytes, int64_t lse_offset,
+                               int64_t flag_offset, int32_t* epoch, cudaStream_t stream) {
+  peer_signal_kernel<<<1, 256, 0, stream>>>(peer_bases, world, rank, o_local, lse_local, rows, slot_bytes,
+                                            lse_offset, flag_offset, epoch);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_peer_combine(const uint64_t* peer_bases, int64_t slot_bytes, int64_t lse_offset,
+                                int64_t flag_offset, const int32_t* epoch, int32_t world, int32_t rank, int32_t rows,
+                                int32_t out_f32, void* out, float* lse, cudaStream_t stream) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(rows, 1, 1);
+  cfg.blockDim = dim3(kCombineThreads, 1, 1);
+  cfg.stream = stream;
+  cudaLaunchAttribute attr;
+  attr.id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr.val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = &attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, peer_combine_kernel, peer_bases, slot_bytes, lse_offset, flag_offset, epoch,
+                            world, rank, rows, out_f32, out, lse);
+}
 
 }  // namespace decattn

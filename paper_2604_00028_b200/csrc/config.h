@@ -73,7 +73,8 @@ DA_HD constexpr int warps_for(int combine_mode) {
 #endif
 DA_HD constexpr int helpers_for(int combine_mode) { return combine_mode == 1 ? DECATTN_CLUSTER_HELPERS : 0; }
 constexpr int kMaxPageSize = 1 << 18;     // da_forward_paged: tiles per page < 2^13 (exact magic division)
-constexpr int kMaxClusterSplits = 16;  // cluster combine up to 16 CTAs (non-portable size, B200)
+constexpr int kMaxClusterSplits = 16;
+constexpr int kMaxPeers = 64;          // da_peer_signal / da_combine_peers: ranks of one exchange  // cluster combine up to 16 CTAs (non-portable size, B200)
 // One pushed row: O[128] fp32, (m, l), padding to 16 bytes.  A rank owns ceil(R/s) rows and
 // receives them from all s ranks (itself included): at most max_{s<=16} s ceil(16/s) = 30 rows (s = 15).
 constexpr int kSlotRowFloats = kHeadDim + 4;

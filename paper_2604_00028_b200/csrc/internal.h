@@ -74,5 +74,11 @@ cudaError_t launch_split_kv_fwd(const da_plan& plan, const CUtensorMap& tmap_k,
                                 cudaStream_t stream);
 // combine.cu
 cudaError_t launch_lse_combine(const CombineParams& p, bool pdl, cudaStream_t stream);
+cudaError_t launch_peer_signal(const uint64_t* peer_bases, int32_t world, int32_t rank, const float* o_local,
+                               const float* lse_local, int32_t rows, int64_t slot_bytes, int64_t lse_offset,
+                               int64_t flag_offset, int32_t* epoch, cudaStream_t stream);
+cudaError_t launch_peer_combine(const uint64_t* peer_bases, int64_t slot_bytes, int64_t lse_offset,
+                                int64_t flag_offset, const int32_t* epoch, int32_t world, int32_t rank, int32_t rows,
+                                int32_t out_f32, void* out, float* lse, cudaStream_t stream);
 
 }  // namespace decattn

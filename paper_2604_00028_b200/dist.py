@@ -17,6 +17,12 @@ Two ways the decode-attention path shards across one 8xB200 box:
   behind sequence splitting (C-comb), so the result equals single-GPU
   attention over the whole sequence.
 
+``PeerSeqShardedDecode`` replaces the all-gather + combine pair with an exchange over peer
+memory: every rank's partial is written into its own buffer of a symmetric allocation mapped
+on all GPUs (torch symmetric memory), a one-thread kernel releases a step epoch into every
+peer's flag slot, and the combine kernel acquires the flags and reads the partials straight
+from the peers' buffers over NVLink (``da_peer_signal`` / ``da_combine_peers``).
+
 Host-side only: the arithmetic runs in libdecattn.so's kernels.  The local
 attention and the combine are injectable so that the exchange logic can be
 tested with world_size 2 on CPU (gloo) against the oracle.
@@ -136,4 +142,73 @@ class SeqShardedDecode:
             lse = torch.empty((self.batch, self.h_q), dtype=torch.float32, device=self.device)
         o_parts, lse_parts = self.gathered()
         self._combine(o_parts, lse_parts, out, lse)
+        return out, lse
+
+
+def _align16(n: int) -> int:
+    return (n + 15) // 16 * 16
+
+
+def peer_layout(batch: int, h_q: int, head_dim: int, world: int):
+    """Byte layout of one rank's exchange buffer (include/decattn.h, da_combine_peers): two slots of
+    slot_bytes, each [0, lse_offset) o fp32 [B, H_Q, d] and [lse_offset, ...) lse fp32 [B, H_Q];
+    then one uint32 flag per rank at flag_offset.  Returns (slot_bytes, lse_offset, flag_offset,
+    total_bytes), all 16-byte aligned."""
+    if min(batch, h_q, head_dim, world) < 1:
+        raise ValueError("bad peer layout arguments")
+    lse_offset = _align16(batch * h_q * head_dim * 4)
+    slot_bytes = _align16(lse_offset + batch * h_q * 4)
+    flag_offset = 2 * slot_bytes
+    return slot_bytes, lse_offset, flag_offset, flag_offset + _align16(4 * world)
+
+
+class PeerSeqShardedDecode:
+    """Long-context mode with the exchange over peer memory: local partial (fp32) -> da_peer_signal
+    (copy into slot epoch & 1 of this rank's symmetric buffer, epoch into every peer's flag slot) ->
+    da_combine_peers (acquire every flag, read the partials from the peers' buffers, LSE-merge).  No
+    NCCL call on the step; every call can be captured in a CUDA graph (monotonic epochs)."""
+
+    def __init__(self, batch: int, h_q: int, h_kv: int, l_k_total: int, head_dim: int = 128, *,
+                 group=None, policy="seq_aware", device=None):
+        import torch.distributed._symmetric_memory as symm
+
+        from . import api
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        self.batch, self.h_q, self.h_kv, self.d = batch, h_q, h_kv, head_dim
+        self.t0, t1 = shard_range(l_k_total, self.rank, self.world)
+        self.l_local = t1 - self.t0
+        if self.l_local < 1:
+            raise ValueError("every rank needs at least one token of the sequence")
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.slot_bytes, self.lse_offset, self.flag_offset, total = peer_layout(batch, h_q, head_dim, self.world)
+        self.buf = symm.empty((total // 4,), dtype=torch.float32, device=self.device)
+        pg = group if group is not None else dist.group.WORLD
+        self.hdl = symm.rendezvous(self.buf, pg.group_name)
+        self.buf.zero_()                                   # flags start at 0 (epochs start at 1)
+        torch.cuda.synchronize(self.device)
+        dist.barrier(group)                                # every buffer zeroed before any signal
+        self.bases = torch.tensor([int(x) for x in self.hdl.buffer_ptrs], dtype=torch.int64, device=self.device)
+        self.epoch = torch.zeros(1, dtype=torch.int32, device=self.device)
+        self.plan = api.make_plan(batch, h_q, h_kv, self.l_local, head_dim, True, 0, None, policy)
+        self._ws = api.workspace_for(self.plan, self.device)
+        self.o_local = torch.empty((batch, h_q, head_dim), dtype=torch.float32, device=self.device)
+        self.lse_local = torch.empty((batch, h_q), dtype=torch.float32, device=self.device)
+
+    def step(self, q, k_local, v_local, seqlens_local=None, out=None, lse=None):
+        """One decode step: local partial -> signal -> pull-combine.  Returns (out, lse)."""
+        from . import _lib as L
+        from . import api
+        api.forward(self.plan, q, k_local, v_local, seqlens_local, out=self.o_local, lse=self.lse_local,
+                    workspace=self._ws, out_dtype=torch.float32)
+        if out is None:
+            out = torch.empty((self.batch, self.h_q, self.d), dtype=torch.bfloat16, device=self.device)
+        if lse is None:
+            lse = torch.empty((self.batch, self.h_q), dtype=torch.float32, device=self.device)
+        L.da_peer_signal(self.world, self.rank, self.bases, self.o_local, self.lse_local, self.batch, self.h_q,
+                         self.d, self.slot_bytes, self.lse_offset, self.flag_offset, self.epoch)
+        L.da_combine_peers(self.world, self.rank, self.bases, self.slot_bytes, self.lse_offset, self.flag_offset,
+                           self.epoch, self.batch, self.h_q, self.d,
+                           L.DA_F32 if out.dtype == torch.float32 else L.DA_BF16, out, lse)
         return out, lse

@@ -336,3 +336,48 @@ def test_plan_make_varlen_matches_oracle(L):
         assert p.as_dict() == ref.as_dict()
     with pytest.raises(L.DecAttnError):
         L.da_plan_make_varlen(2, 8, 1, 512, 128, 1, 0, 148, [1])      # wrong length count
+
+
+def test_peer_exchange_validation(L):
+    A2 = 1 << 22
+    slot, lo, fo = 4128, 4096, 2 * 4128                # B = 1, H_Q = 8: o 4096 B, lse 32 B
+    def sig(**kw):
+        a = dict(world=2, rank=0, peer_bases=A2, o_local=A2, lse_local=A2, batch=1, h_q=8, head_dim=128,
+                 slot_bytes=slot, lse_offset=lo, flag_offset=fo, epoch=A2, stream=0)
+        a.update(kw)
+        with pytest.raises(L.DecAttnError) as e:
+            L.da_peer_signal(**a)
+        return e.value.status
+    assert sig(world=0) == L.DA_ERR_INVALID_ARG
+    assert sig(world=65) == L.DA_ERR_INVALID_ARG
+    assert sig(rank=2) == L.DA_ERR_INVALID_ARG
+    assert sig(peer_bases=None) == L.DA_ERR_INVALID_ARG
+    assert sig(o_local=None) == L.DA_ERR_INVALID_ARG
+    assert sig(head_dim=64) == L.DA_ERR_UNSUPPORTED
+    assert sig(lse_offset=16) == L.DA_ERR_INVALID_ARG                 # o and lse overlap
+    assert sig(slot_bytes=4112) == L.DA_ERR_INVALID_ARG               # lse past the slot
+    assert sig(flag_offset=4128) == L.DA_ERR_INVALID_ARG              # flags inside slot 1
+    assert sig(slot_bytes=4132, flag_offset=8272) == L.DA_ERR_ALIGNMENT
+    assert sig(o_local=A2 + 4) == L.DA_ERR_ALIGNMENT
+
+    def comb(**kw):
+        a = dict(world=2, rank=1, peer_bases=A2, slot_bytes=slot, lse_offset=lo, flag_offset=fo, epoch=A2,
+                 batch=1, h_q=8, head_dim=128, out_dtype=L.DA_BF16, out=A2, lse=A2, stream=0)
+        a.update(kw)
+        with pytest.raises(L.DecAttnError) as e:
+            L.da_combine_peers(**a)
+        return e.value.status
+    assert comb(out=None) == L.DA_ERR_INVALID_ARG
+    assert comb(out_dtype=5) == L.DA_ERR_INVALID_ARG
+    assert comb(epoch=None) == L.DA_ERR_INVALID_ARG
+    assert comb(out=A2 + 8) == L.DA_ERR_ALIGNMENT
+
+
+def test_peer_layout():
+    from paper_2604_00028_b200.dist import peer_layout
+    for B, H, W in ((1, 64, 8), (3, 24, 2), (1, 8, 1), (128, 64, 64)):
+        slot, lo, fo, tot = peer_layout(B, H, 128, W)
+        assert lo >= B * H * 128 * 4 and lo % 16 == 0
+        assert slot >= lo + 4 * B * H and slot % 16 == 0
+        assert fo >= 2 * slot and fo % 16 == 0
+        assert tot >= fo + 4 * W and tot % 16 == 0
