@@ -431,8 +431,8 @@ def main():
     ap.add_argument("--ab-rounds", type=int, default=21)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--exchange", default="p2p", choices=["nccl", "p2p"],
-                    help="long_context with N > 1: the peer-memory exchange (default) or NCCL all-gather + combine "
-                         "(da_peer_signal + da_combine_peers over torch symmetric memory)")
+                    help="long_context with N > 1: the exchange over peer memory (default: da_peer_signal + "
+                         "da_combine_peers over torch symmetric memory) or an NCCL all-gather + da_combine")
     ap.add_argument("--policy", default="seq_aware_sm",
                     choices=["seq_aware_sm", "seq_aware", "guarded", "evolved"],
                     help="split policy of the headline step (default: the SM-count-aware sequence-aware "
