@@ -85,7 +85,7 @@ template <int NB>
 __device__ __forceinline__ void mma_tile(uint32_t sK, uint32_t sV, int valid,
                                          const uint32_t (&qf)[8][NB][2], float (&o)[8][NB][4],
                                          float (&m)[NB][2], float (&l)[NB][2], float scale_log2,
-                                         int lane) {
+                                         int lane, uint32_t vbar, uint32_t vparity) {
   const uint32_t sw = static_cast<uint32_t>(lane & 7);
   // ---- S^T[token, g] = sum_d K[token, d] Q[g, d]  (4 token blocks x NB g-blocks)
   float s[4][NB][4];
@@ -172,6 +172,18 @@ __device__ __forceinline__ void mma_tile(uint32_t sK, uint32_t sV, int valid,
       pl[j][nb][0] = movmatrix_trans(pack_bf16(p[0] - bf16lo(h01), p[1] - bf16hi(h01)));
       pl[j][nb][1] = movmatrix_trans(pack_bf16(p[2] - bf16lo(h23), p[3] - bf16hi(h23)));
     }
+
+  // ---- V: wait for its half of the stage (it lands while QK^T and the softmax run); rows past
+  // the range may hold anything (even NaN): zero them so the P = 0 rows stay 0
+  mbar_wait(vbar, vparity);
+  if (valid < kTileN) {
+    for (int idx = lane; idx < (kTileN - valid) * 16; idx += 32) {
+      const int r = valid + (idx >> 4);
+      const int c = idx & 15;
+      sts128(sV + (c >> 3) * kHalfBytes + r * 128 + (c & 7) * 16, make_uint4(0, 0, 0, 0));
+    }
+    __syncwarp();
+  }
 
   // ---- O^T[d, g] += sum_token V^T[d, token] P^T[token, g]   (8 d-blocks x 4 token blocks)
   {
@@ -378,7 +390,8 @@ __global__ void __launch_bounds__(threads_for(NW, helpers_for(kCombine)), 1)
   constexpr int kIters = (R * 32 + kT - 1) / kT;           // merge passes: element = (row, float4)
   constexpr bool kCluster = kCombine == DA_COMBINE_CLUSTER;
   extern __shared__ uint8_t smem_raw[];
-  __shared__ __align__(8) uint64_t full_bar[NS];
+  __shared__ __align__(8) uint64_t full_bar[NS];    // K of the stage has landed
+  __shared__ __align__(8) uint64_t fullv_bar[NS];   // V of the stage has landed (QK^T need not wait)
   __shared__ __align__(8) uint64_t empty_bar[NS];
   __shared__ __align__(8) uint64_t push_bar;              // CLUSTER: pushes of the rows this CTA owns
 
@@ -425,6 +438,7 @@ __global__ void __launch_bounds__(threads_for(NW, helpers_for(kCombine)), 1)
 #pragma unroll
     for (int i = 0; i < NS; ++i) {
       mbar_init(smem_u32(&full_bar[i]), 1);
+      mbar_init(smem_u32(&fullv_bar[i]), 1);
       mbar_init(smem_u32(&empty_bar[i]), 1);
     }
     if constexpr (kCluster) {
@@ -502,12 +516,13 @@ __global__ void __launch_bounds__(threads_for(NW, helpers_for(kCombine)), 1)
           const int st = i % NS;
           if (i >= NS) mbar_wait(smem_u32(&empty_bar[st]), ((i / NS) - 1) & 1);
           DA_DASSERT(t0 + i * kTileN < max(t_end, 1) + kTileN);
-          const uint32_t fb = smem_u32(&full_bar[st]);
-          mbar_arrive_expect_tx(fb, kStageBytes);
+          const uint32_t fb = smem_u32(&full_bar[st]), fvb = smem_u32(&fullv_bar[st]);
+          mbar_arrive_expect_tx(fb, kStageBytes / 2);
+          mbar_arrive_expect_tx(fvb, kStageBytes / 2);
           const uint32_t dst = sbase + st * kStageBytes;
           const int t = t0 + i * kTileN;
-          tma_load_5d(dst, &tmap_k, fb, 0, t, 0, kvh, b);                  // K: both 64-dim halves
-          tma_load_5d(dst + 2 * kHalfBytes, &tmap_v, fb, 0, t, 0, kvh, b);  // V
+          tma_load_5d(dst, &tmap_k, fb, 0, t, 0, kvh, b);                   // K: both 64-dim halves
+          tma_load_5d(dst + 2 * kHalfBytes, &tmap_v, fvb, 0, t, 0, kvh, b);  // V
           if (i < 8) TRACE(2 + i);
         }
       } else {
@@ -530,8 +545,9 @@ __global__ void __launch_bounds__(threads_for(NW, helpers_for(kCombine)), 1)
         for (int i = 0; i < n_tiles; ++i) {
           const int st = i % NS;
           if (i >= NS) mbar_wait(smem_u32(&empty_bar[st]), ((i / NS) - 1) & 1);
-          const uint32_t fb = smem_u32(&full_bar[st]);
-          mbar_arrive_expect_tx(fb, kStageBytes);
+          const uint32_t fb = smem_u32(&full_bar[st]), fvb = smem_u32(&fullv_bar[st]);
+          mbar_arrive_expect_tx(fb, kStageBytes / 2);
+          mbar_arrive_expect_tx(fvb, kStageBytes / 2);
           const uint32_t dst = sbase + st * kStageBytes;
           const int page = pg[0];
           const int slot = static_cast<int>(ck) * kTileN;
@@ -541,7 +557,7 @@ __global__ void __launch_bounds__(threads_for(NW, helpers_for(kCombine)), 1)
           pg[NS - 1] = i + NS < n_tiles ? __ldg(bt + lj) : 0;
           if (++lk == tpp) { lk = 0; ++lj; }
           tma_load_5d(dst, &tmap_k, fb, 0, slot, 0, kvh, page);
-          tma_load_5d(dst + 2 * kHalfBytes, &tmap_v, fb, 0, slot, 0, kvh, page);
+          tma_load_5d(dst + 2 * kHalfBytes, &tmap_v, fvb, 0, slot, 0, kvh, page);
         }
       }
     }
@@ -582,19 +598,10 @@ __global__ void __launch_bounds__(threads_for(NW, helpers_for(kCombine)), 1)
         const int st = i % NS;
         const uint32_t sK = sbase + st * kStageBytes;
         const uint32_t sV = sK + 2 * kHalfBytes;
-        mbar_wait(smem_u32(&full_bar[st]), (i / NS) & 1);
+        mbar_wait(smem_u32(&full_bar[st]), (i / NS) & 1);      // K: QK^T and the softmax start now
         if (lane == 0 && i < 8) TRACE(10 + i);
         const int valid = min(kTileN, t_end - (t0 + i * kTileN));
-        if (valid < kTileN) {
-          // rows past the range may hold anything (even NaN): zero them so P = 0 rows stay 0
-          for (int idx = lane; idx < (kTileN - valid) * 16; idx += 32) {
-            const int r = valid + (idx >> 4);
-            const int c = idx & 15;
-            sts128(sV + (c >> 3) * kHalfBytes + r * 128 + (c & 7) * 16, make_uint4(0, 0, 0, 0));
-          }
-          __syncwarp();
-        }
-        mma_tile<kNB>(sK, sV, valid, qf, o, m, l, p.scale_log2, lane);
+        mma_tile<kNB>(sK, sV, valid, qf, o, m, l, p.scale_log2, lane, smem_u32(&fullv_bar[st]), (i / NS) & 1);
         __syncwarp();
         if (lane == 0) mbar_arrive(smem_u32(&empty_bar[st]));
         if (lane == 0 && i < 8) TRACE(18 + i);
@@ -640,6 +647,7 @@ __global__ void __launch_bounds__(threads_for(NW, helpers_for(kCombine)), 1)
         const int st = i % NS;
         const uint32_t sK = sbase + st * kStageBytes;
         mbar_wait(smem_u32(&full_bar[st]), (i / NS) & 1);
+        mbar_wait(smem_u32(&fullv_bar[st]), (i / NS) & 1);
         const int valid = min(kTileN, t_end - (t0 + i * kTileN));
         scalar_tile(sK, sK + 2 * kHalfBytes, valid, qv, o, m, l, p.scale_log2, lane);
         __syncwarp();
