@@ -511,7 +511,21 @@ __global__ void __launch_bounds__(threads_for(NW, helpers_for(kCombine)), 1)
   if (warp == NW) {
     // ================= TMA producer =================
     if (lane == 0) {
-      if (p.block_table == nullptr) {
+      if (p.block_table == nullptr && n_tiles <= NS) {
+        // latency regime (every tile has its own stage): all K boxes first, then all V boxes, so
+        // every consumer starts QK^T one V box earlier than in tile order
+        for (int i = 0; i < n_tiles; ++i) {
+          const uint32_t fb = smem_u32(&full_bar[i]);
+          mbar_arrive_expect_tx(fb, kStageBytes / 2);
+          tma_load_5d(sbase + i * kStageBytes, &tmap_k, fb, 0, t0 + i * kTileN, 0, kvh, b);
+          if (i < 8) TRACE(2 + i);
+        }
+        for (int i = 0; i < n_tiles; ++i) {
+          const uint32_t fvb = smem_u32(&fullv_bar[i]);
+          mbar_arrive_expect_tx(fvb, kStageBytes / 2);
+          tma_load_5d(sbase + i * kStageBytes + 2 * kHalfBytes, &tmap_v, fvb, 0, t0 + i * kTileN, 0, kvh, b);
+        }
+      } else if (p.block_table == nullptr) {
         for (int i = 0; i < n_tiles; ++i) {
           const int st = i % NS;
           if (i >= NS) mbar_wait(smem_u32(&empty_bar[st]), ((i / NS) - 1) & 1);
