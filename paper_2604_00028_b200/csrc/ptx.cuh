@@ -66,6 +66,14 @@ __device__ __forceinline__ void tma_load_5d(uint32_t dst, const void* tmap, uint
       "l"(reinterpret_cast<uint64_t>(tmap)), "r"(bar), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4)
       : "memory");
 }
+// L2 prefetch of one 5-D box (no shared-memory destination, no completion).  L2 is the point of
+// coherence, so a prefetch issued before griddepcontrol.wait cannot make a later load stale.
+__device__ __forceinline__ void tma_prefetch_5d(const void* tmap, int c0, int c1, int c2, int c3, int c4) {
+  asm volatile("cp.async.bulk.prefetch.tensor.5d.L2.global.tile [%0, {%1, %2, %3, %4, %5}];" ::"l"(
+                   reinterpret_cast<uint64_t>(tmap)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4)
+               : "memory");
+}
+
 // L2 prefetch of one global line (no data returned; always safe before griddepcontrol.wait:
 // L2 is the point of coherence).
 __device__ __forceinline__ void prefetch_l2(const void* ptr) {
