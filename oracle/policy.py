@@ -67,19 +67,22 @@ RULE_DYNAMIC = 11     # per-batch split counts from the lengths on the device (d
 # C-ext-1).  The paper leaves "extending the benefit to lower L_K values and learning more
 # configuration-specific split counts" to future work and calls its
 # own constant stack-specific ("s=3 on the current stack").  These constants are
-# calibrated from the B200 U-curves of the current kernel (profiles/r01g_ugrid.csv,
-# r01g_ugrid2.csv, r01g_ugrid3.csv; long-context boundary from scripts/probe_regime.py and
-# scripts/probe_long.py) and frozen:
+# calibrated from the B200 U-curves of the current kernel (profiles/r01h_ugrid.csv,
+# r01h_ugrid2.csv, r01h_ugrid3.csv, measured with the pre-wait L2 prefetch of short splits;
+# long-context boundary from scripts/probe_regime.py and probe_long.py; s = 11 vs 12 from
+# scripts/probe_s11.py) and frozen:
 SM_UNIT = 64          # tokens per split unit of the B200 kernel
 SM_MIN_UNITS = 4      # fewer units (L_K <= 192): every split loses on B200
-SM_MIN_UNITS_WIDE = 6  # with T > SM_WIDE_T tiles, fewer units (L_K <= 320) do not pay either
+SM_MIN_UNITS_WIDE = 8  # with T > SM_WIDE_T tiles, fewer units (L_K <= 448) do not pay either
 SM_WIDE_T = 16
 SM_NARROW_T = 4       # T <= 4 tiles: the plateau extends to s = 8 ...
 SM_NARROW_SPLITS = 8
-SM_MAX_SPLITS = 4     # ... otherwise the measured plateau starts at s = 4 (L_K <= 512)
-SM_EFF_FLOOR = 8      # efficiency region: at least min(8, n_u, fit) splits
+SM_MAX_SPLITS = 4     # ... otherwise the measured plateau starts at s = 4
 SM_STREAM_UNITS = 16  # efficiency region: cap to the one-wave cluster split while each split
                       # holds <= 16 units (1024 tokens) or the capped launch still has >= U/2 CTAs
+SM_MID_T = 8          # efficiency region, <= 64 units (latency regime): at most 4 splits for T > 8,
+SM_MID_UNITS = 64
+SM_CLUSTER_CAP = 12   # at most 12 otherwise (clusters of 13..16 measured slower than 12)
 # Clusters of s CTAs (one per split, s = 1..16) that are co-resident in one wave on a 148-SM
 # B200 with the cluster-combine kernel configuration (cudaOccupancyMaxActiveClusters,
 # scripts/microbench_cluster16.cu); index 0 unused, index 1 = one CTA per SM.  Scaled by U / 148.
@@ -184,15 +187,17 @@ def cluster_fit_splits(T: int, U: int) -> int:
 
 
 def seq_aware_sm_splits(geo: dict, l_k: int):
-    """C-ext-1, in this order (n_u = ceil(L_K / 64) units, f = cluster_fit_splits(T, U)):
+    """C-ext-1, in this order (n_u = ceil(L_K / 64) units, f = cluster_fit_splits(T, U),
+    c = 8 if T <= 4 else 4):
       saturated (5T >= 4U)                      -> 1                      (unchanged FA3 guard)
       nblk <= 4 (the paper's guard region):
-        n_u < 4, or n_u < 6 with T > 16         -> 1                      (short: splitting loses)
-        s = min(n_u, 8 if T <= 4 else 4, f);  s < 2 -> 1
+        n_u < 4, or n_u < 8 with T > 16         -> 1                      (short: splitting loses)
+        s = min(n_u, c, f);  s < 2 -> 1
       nblk >= 5 (efficiency region), e = the unchanged efficiency loop:
-        e <= f                                  -> max(e, min(8, n_u, f))
-        e > f >= 2 and (n_u <= 16 f or 2 T f >= U) -> f
-        else                                    -> e
+        e <= f                                  -> s = max(e, min(c, n_u, f))
+        e > f >= 2 and (n_u <= 16 f or 2 T f >= U) -> s = f
+        else                                    -> e (streaming: returned as is)
+        then, for short sequences (n_u <= 64): s = min(s, 4) if T > 8, and s = min(s, 12)
     The split count depends on the tile count T = Batch x H_KV versus the usable SMs U through
     f, the largest split whose clusters all fit one wave, not on a static L_K guard."""
     T, U, nblk = geo["T"], geo["U"], geo["nblk"]
@@ -200,21 +205,23 @@ def seq_aware_sm_splits(geo: dict, l_k: int):
         return 1, RULE_SATURATED
     n_u = ceil_div(l_k, SM_UNIT)
     f = cluster_fit_splits(T, U)
+    c = SM_NARROW_SPLITS if T <= SM_NARROW_T else SM_MAX_SPLITS
     if nblk <= 4:
         if n_u < SM_MIN_UNITS or (n_u < SM_MIN_UNITS_WIDE and T > SM_WIDE_T):
             return 1, RULE_SM_SHORT
-        cap = SM_NARROW_SPLITS if T <= SM_NARROW_T else SM_MAX_SPLITS
-        s = min(n_u, cap, f)
+        s = min(n_u, c, f)
         if s < 2:
             return 1, RULE_SM_SHORT
         return s, RULE_SM_SPLIT
     e = efficiency_loop(T, U, nblk)
     if e <= f:
-        s = max(e, min(SM_EFF_FLOOR, n_u, f))
+        s = max(e, min(c, n_u, f))
     elif f >= 2 and (n_u <= SM_STREAM_UNITS * f or 2 * T * f >= U):
         s = f
     else:
-        s = e
+        return e, RULE_EFF_LOOP
+    if n_u <= SM_MID_UNITS:
+        s = min(s, SM_MAX_SPLITS if T > SM_MID_T else SM_CLUSTER_CAP)
     return s, (RULE_EFF_LOOP if s == e else RULE_SM_FIT)
 
 
