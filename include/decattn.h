@@ -78,14 +78,15 @@ typedef enum da_policy {
   DA_POLICY_FIXED = 2,      /* s = forced_splits (the U-curve sweep) */
   DA_POLICY_EVOLVED = 3,    /* Fig. 1: batch == 1 -> 12 (16 when
                                L_K < 256); batch != 1 -> guarded            */
-  DA_POLICY_SEQ_AWARE_SM = 4,/* SM-count-aware generalisation (DESIGN.md
+  DA_POLICY_SEQ_AWARE_SM = 4, /* SM-count-aware generalisation (DESIGN.md
                                C-ext-1), n_u = ceil(L_K/64),
                                f = largest s <= 16 whose T clusters fit one
-                               wave: nblk <= 4 -> min(n_u, T <= 4 ? 8 : 4, f)
-                               (1 when n_u < 4, or n_u < 6 and T > 16);
+                               wave, c = T <= 4 ? 8 : 4: nblk <= 4 -> min(n_u,
+                               c, f) (1 when n_u < 4, or n_u < 8 and T > 16);
                                else the efficiency loop's e, raised to
-                               min(8, n_u, f) when e <= f, or moved to f when
-                               e > f >= 2 and (n_u <= 16 f or 2 T f >= U);
+                               min(c, n_u, f) when e <= f, or moved to f when
+                               e > f >= 2 and (n_u <= 16 f or 2 T f >= U),
+                               then for n_u <= 64 at most 4 (T > 8) or 12;
                                B200-calibrated                              */
   DA_POLICY_DYNAMIC = 5     /* per-batch split counts from cache_seqlens on the
                                device (DESIGN.md C-ext-2):

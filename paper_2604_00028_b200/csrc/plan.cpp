@@ -91,14 +91,23 @@ void decide(int64_t batch, int64_t l_k, int64_t T, int64_t U, int64_t nblk, int 
       return;
     }
     const int64_t e = efficiency_loop(T, U, nblk);
-    int64_t v = e;
+    const int64_t c = T <= kSmNarrowT ? kSmNarrowSplits : kSmMaxSplits;
+    int64_t v;
     if (e <= f) {
-      int64_t floor_s = kSmEffFloor;
+      int64_t floor_s = c;
       if (n_u < floor_s) floor_s = n_u;
       if (f < floor_s) floor_s = f;
-      if (floor_s > v) v = floor_s;
+      v = e > floor_s ? e : floor_s;
     } else if (f >= 2 && (n_u <= kSmStreamUnits * f || 2 * T * f >= U)) {
       v = f;
+    } else {
+      *s = static_cast<int>(e);            // streaming: the loop's split as is
+      *rule = DA_RULE_EFF_LOOP;
+      return;
+    }
+    if (n_u <= kSmMidUnits) {               // short sequences: at most 4 (T > 8) or 12 splits
+      const int64_t cap = T > kSmMidT ? kSmMaxSplits : kSmClusterCap;
+      if (v > cap) v = cap;
     }
     *s = static_cast<int>(v);
     *rule = v == e ? DA_RULE_EFF_LOOP : DA_RULE_SM_FIT;
