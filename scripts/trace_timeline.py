@@ -24,7 +24,7 @@ if hasattr(L.LIB, "da_trace_fetch_combine"):
 
 def trace(b, hq, hkv, lk, policy, forced=0, steps=50, combine=None):
     w = synth.make_inputs(b, hq, hkv, lk, device="cuda", seed=3)
-    nbuf = 64
+    nbuf = int(os.environ.get("TRACE_NBUF", "64"))
     ks = [w["k"].clone() for _ in range(nbuf)]
     vs = [w["v"].clone() for _ in range(nbuf)]
     plan = dec.make_plan(b, hq, hkv, lk, policy=policy, forced_splits=forced, combine_mode=combine)
@@ -89,11 +89,8 @@ def trace(b, hq, hkv, lk, policy, forced=0, steps=50, combine=None):
 if __name__ == "__main__":
     which = sys.argv[1] if len(sys.argv) > 1 else "latency"
     if which == "latency":
-        trace(1, 8, 1, 512, "guarded")
         trace(1, 8, 1, 512, "seq_aware_sm")
-        trace(1, 64, 8, 512, "guarded")
         trace(1, 64, 8, 512, "seq_aware_sm")
-        trace(1, 64, 8, 512, "fixed", 8)
     elif which == "kernel":
         trace(1, 8, 1, 768, "fixed", 16, combine=1)
         trace(1, 8, 1, 768, "fixed", 16, combine=2)
