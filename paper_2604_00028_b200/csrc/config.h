@@ -72,6 +72,9 @@ DA_HD constexpr int warps_for(int combine_mode) {
 #define DECATTN_CLUSTER_HELPERS 4
 #endif
 DA_HD constexpr int helpers_for(int combine_mode) { return combine_mode == 1 ? DECATTN_CLUSTER_HELPERS : 0; }
+#ifndef DECATTN_SPECULATE
+#define DECATTN_SPECULATE 1   // prefetch the plan-length range also when cache_seqlens is given
+#endif
 constexpr int kMaxPageSize = 1 << 18;     // da_forward_paged: tiles per page < 2^13 (exact magic division)
 constexpr int kMaxClusterSplits = 16;
 constexpr int kMaxPeers = 64;          // da_peer_signal / da_combine_peers: ranks of one exchange  // cluster combine up to 16 CTAs (non-portable size, B200)

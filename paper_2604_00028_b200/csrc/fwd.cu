@@ -468,11 +468,15 @@ __global__ void __launch_bounds__(threads_for(NW, helpers_for(kCombine)), 1)
   // griddepcontrol.wait and the producer issues the first TMA the moment the wait returns.
   int t0 = 0, t_end = 0, n_tiles = 0;
   if constexpr (!kDyn) {
-    if (p.seqlens == nullptr) {
-      split_range(min(max(p.l_default, 0), p.l_cap), split, p.num_splits, p.s_magic, t0, t_end, n_tiles);
-      // short splits (<= 2 NS tiles: the latency regime): pull the tiles the ring loads first into L2
-      // while the previous kernel drains; L2 is the point of coherence, so the loads after
-      // griddepcontrol.wait still see the preceding kernel's writes (Llama 3.57 -> 3.12 us)
+    // the range at the plan's length: exact when cache_seqlens == NULL; with cache_seqlens it is
+    // only a guess for the prefetch below (the lengths may still be written by the preceding
+    // kernel, so they are read after the wait and the range recomputed there)
+    split_range(min(max(p.l_default, 0), p.l_cap), split, p.num_splits, p.s_magic, t0, t_end, n_tiles);
+    // short splits (<= 2 NS tiles: the latency regime): pull the tiles the ring loads first into L2
+    // while the previous kernel drains; L2 is the point of coherence, so the loads after
+    // griddepcontrol.wait still see the preceding kernel's writes (Llama 3.57 -> 3.12 us).  A wrong
+    // guess only costs DRAM reads.
+    if (DECATTN_SPECULATE || p.seqlens == nullptr) {
       if (warp == NW && lane == 0 && n_tiles >= 1 && n_tiles <= 2 * NS && p.block_table == nullptr) {
         const int np = min(n_tiles, NS);
         for (int i = 0; i < np; ++i) tma_prefetch_5d(&tmap_k, 0, t0 + i * kTileN, 0, kvh, b);
