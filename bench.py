@@ -395,9 +395,17 @@ def e2e_measure(dec, L, cfg, dev, stream, steps, warmup, policy="seq_aware_sm"):
     all enqueued on one stream inside the timed region (CUDA events around the K steps)."""
     b, hq, hkv, lk = cfg["batch"], cfg["h_q"], cfg["h_kv"], cfg["l_k"]
     inp = synth.make_inputs(b, hq, hkv, lk, seed=2000)
-    hq_, hk_, hv_ = (inp[n].contiguous().pin_memory() for n in ("q", "k", "v"))
-    h_out = torch.empty((b, hq, HEAD_DIM), dtype=torch.bfloat16).pin_memory()
-    h_lse = torch.empty((b, hq), dtype=torch.float32).pin_memory()
+    hq_ = inp["q"].contiguous().pin_memory()
+    # the host KV cache as one pinned [2, B, L, H_KV, d] allocation (K then V) and out + lse in one
+    # pinned buffer: da_forward_host moves each pair with one DMA
+    kv = torch.empty((2,) + tuple(inp["k"].shape), dtype=torch.bfloat16).pin_memory()
+    kv[0].copy_(inp["k"])
+    kv[1].copy_(inp["v"])
+    hk_, hv_ = kv[0], kv[1]
+    ob = b * hq * HEAD_DIM * 2
+    ol = torch.empty(ob + 4 * b * hq, dtype=torch.uint8).pin_memory()
+    h_out = ol[:ob].view(torch.bfloat16).view(b, hq, HEAD_DIM)
+    h_lse = ol[ob:].view(torch.float32).view(b, hq)
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
     staging = dec.HostStaging(dev)
 

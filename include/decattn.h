@@ -291,7 +291,9 @@ DA_API int64_t da_forward_host_bytes(const da_plan* plan, int32_t l_cap, int32_t
  * contiguous strides); device->host copies of out [B, H_Q, d] (out_dtype) and lse fp32
  * [B, H_Q] (NULL = not copied).  The host outputs are valid once the stream has
  * synchronised.  Page-locked host memory makes every copy asynchronous; pageable memory
- * works but then copies synchronously.
+ * works but then copies synchronously.  When v_cache starts where k_cache ends inside one
+ * CUDA-registered allocation (a [2, B, l_cap, H_KV, d] host cache), K and V travel in one DMA;
+ * so do out and lse when lse starts where out ends inside one allocation.
  *   device_buffer, device_buffer_bytes: device scratch of at least
  *   da_forward_host_bytes(plan, l_cap, cache_seqlens != NULL, out_dtype) bytes, 256-byte
  *   aligned, owned by the caller and reusable once the stream has passed this call.

@@ -66,3 +66,22 @@ t1 = time.perf_counter()
 e1.record(s)
 e1.synchronize()
 print(f"raw ctypes da_forward_host: host enqueue {(t1 - t0) / n * 1e6:.1f} us/step, device {e0.elapsed_time(e1) / n * 1e3:.1f} us/step")
+
+# joint [2, ...] KV + out|lse allocations (one DMA each way) vs separate pinned tensors, interleaved
+kvj = torch.empty((2,) + tuple(k.shape), dtype=torch.bfloat16).pin_memory()
+kvj[0].copy_(k)
+kvj[1].copy_(v)
+ob = b * hq * 128 * 2
+ol = torch.empty(ob + 4 * b * hq, dtype=torch.uint8).pin_memory()
+outj, lsej = ol[:ob].view(torch.bfloat16).view(b, hq, 128), ol[ob:].view(torch.float32).view(b, hq)
+for rep in range(3):
+    for name, (kk, vv, oo, ll) in (("separate", (k, v, out, lse)), ("joint", (kvj[0], kvj[1], outj, lsej))):
+        for _ in range(5):
+            dec.forward_host(plan, q, kk, vv, None, out=oo, lse=ll, staging=staging, stream=s)
+        torch.cuda.synchronize()
+        e0.record(s)
+        for _ in range(n):
+            dec.forward_host(plan, q, kk, vv, None, out=oo, lse=ll, staging=staging, stream=s)
+        e1.record(s)
+        e1.synchronize()
+        print(f"{name:9s}: {e0.elapsed_time(e1) / n * 1e3:.1f} us/step")

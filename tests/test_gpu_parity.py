@@ -339,6 +339,18 @@ def test_forward_host_matches_oracle(batch, h_q, h_kv, l_k, policy, forced, seql
     ref_o, ref_l = OA.decode_attention(*(synth.to_f64(t) for t in (inp["q"], inp["k"], inp["v"], n)))
     assert_out_close(synth.to_f64(out), ref_o)
     assert_lse_close(synth.to_f64(lse), ref_l)
+    # one [2, ...] host KV allocation (K and V in one DMA), an adjacent out | lse buffer (one DMA back),
+    # and separately pinned K / V that merely sit back to back (two DMAs) give the same bytes
+    odt = torch.float32 if f32 else torch.bfloat16
+    kv = torch.empty((2,) + tuple(k.shape), dtype=torch.bfloat16).pin_memory()
+    kv[0].copy_(k)
+    kv[1].copy_(v)
+    ob = batch * h_q * 128 * (4 if f32 else 2)
+    ol = torch.empty(ob + 4 * batch * h_q, dtype=torch.uint8).pin_memory()
+    out3, lse3 = ol[:ob].view(odt).view(batch, h_q, 128), ol[ob:].view(torch.float32).view(batch, h_q)
+    dec.forward_host(plan, q, kv[0], kv[1], seq, out=out3, lse=lse3, staging=staging, stream=stream)
+    stream.synchronize()
+    assert torch.equal(out, out3) and torch.equal(lse, lse3)
     # a second call reuses the staging buffer and returns the same bytes
     out2, lse2 = dec.forward_host(plan, q, k, v, seq, staging=staging, stream=stream,
                                   out_dtype=torch.float32 if f32 else torch.bfloat16)
