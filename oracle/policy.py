@@ -68,11 +68,13 @@ RULE_DYNAMIC = 11     # per-batch split counts from the lengths on the device (d
 # configuration-specific split counts" to future work and calls its
 # own constant stack-specific ("s=3 on the current stack").  These constants are
 # calibrated from the B200 U-curves of the current kernel (profiles/r01h_ugrid.csv,
-# r01h_ugrid2.csv, r01h_ugrid3.csv, measured with the pre-wait L2 prefetch of short splits;
+# r01h_ugrid2.csv, r01h_ugrid3.csv, measured with the pre-wait L2 prefetch of short splits, and
+# the 48-shape low-head sweep of BASELINE configs[2], profiles/r01i_lowhead.csv;
 # long-context boundary from scripts/probe_regime.py and probe_long.py; s = 11 vs 12 from
 # scripts/probe_s11.py) and frozen:
 SM_UNIT = 64          # tokens per split unit of the B200 kernel
-SM_MIN_UNITS = 4      # fewer units (L_K <= 192): every split loses on B200
+SM_MIN_UNITS = 5      # fewer units (L_K <= 256): every split loses or ties on B200
+SM_MIN_SPLITS = 3     # guard region: a 2-way split (only 2-CTA clusters fit, T = 46..74) loses
 SM_MIN_UNITS_WIDE = 8  # with T > SM_WIDE_T tiles, fewer units (L_K <= 448) do not pay either
 SM_WIDE_T = 16
 SM_NARROW_T = 4       # T <= 4 tiles: the plateau extends to s = 8 ...
@@ -191,8 +193,8 @@ def seq_aware_sm_splits(geo: dict, l_k: int):
     c = 8 if T <= 4 else 4):
       saturated (5T >= 4U)                      -> 1                      (unchanged FA3 guard)
       nblk <= 4 (the paper's guard region):
-        n_u < 4, or n_u < 8 with T > 16         -> 1                      (short: splitting loses)
-        s = min(n_u, c, f);  s < 2 -> 1
+        n_u < 5, or n_u < 8 with T > 16         -> 1                      (short: splitting loses)
+        s = min(n_u, c, f);  s < 3 -> 1
       nblk >= 5 (efficiency region), e = the unchanged efficiency loop:
         e <= f                                  -> s = max(e, min(c, n_u, f))
         e > f >= 2 and (n_u <= 16 f or 2 T f >= U) -> s = f
@@ -210,7 +212,7 @@ def seq_aware_sm_splits(geo: dict, l_k: int):
         if n_u < SM_MIN_UNITS or (n_u < SM_MIN_UNITS_WIDE and T > SM_WIDE_T):
             return 1, RULE_SM_SHORT
         s = min(n_u, c, f)
-        if s < 2:
+        if s < SM_MIN_SPLITS:
             return 1, RULE_SM_SHORT
         return s, RULE_SM_SPLIT
     e = efficiency_loop(T, U, nblk)

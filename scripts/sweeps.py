@@ -328,3 +328,34 @@ def ragged():
 
 if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "ragged":
     ragged()
+
+
+def lowhead():
+    """BASELINE.json configs[2]: the 48-shape low-head sweep (B in {1,2,4,8} x H_KV in {1,2,8} x
+    L_K in {64,128,256,512}, H_Q = 8 H_KV) under the guarded default, the paper's rule and the
+    SM-count-aware policy (interleaved graph replays, medians)."""
+    rows = []
+    pols = ("guarded", "seq_aware", "seq_aware_sm")
+    for b in (1, 2, 4, 8):
+        for hkv in (1, 2, 8):
+            for lk in (64, 128, 256, 512):
+                cfg = dict(batch=b, h_q=8 * hkv, h_kv=hkv, l_k=lk)
+                plans = [dec.make_plan(b, 8 * hkv, hkv, lk, policy=p) for p in pols]
+                times = timed_graphs(cfg, plans, 200, 9, 19)
+                tg = times[0][0]
+                for pol, plan, (t, p10, p90) in zip(pols, plans, times):
+                    rows.append(dict(batch=b, h_kv=hkv, l_k=lk, policy=pol, num_splits=plan.num_splits,
+                                     combine_mode=plan.combine_mode, latency_us=round(t, 3),
+                                     speedup_vs_guarded=round(tg / t, 4)))
+                print(f"B={b} H_KV={hkv} L_K={lk:4d}: " + "  ".join(
+                    f"{pol} s={p.num_splits} {t[0]:.2f}" for pol, p, t in zip(pols, plans, times)) +
+                      f"   sm {tg / times[2][0]:.3f}x", flush=True)
+    write("lowhead", rows, ["batch", "h_kv", "l_k", "policy", "num_splits", "combine_mode", "latency_us",
+                            "speedup_vs_guarded"])
+    sm = [r for r in rows if r["policy"] == "seq_aware_sm"]
+    print(f"48 shapes: SM-count-aware vs guarded min {min(r['speedup_vs_guarded'] for r in sm):.3f}x, "
+          f"max {max(r['speedup_vs_guarded'] for r in sm):.3f}x")
+
+
+if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "lowhead":
+    lowhead()

@@ -262,8 +262,9 @@ def test_seq_aware_sm_structure():
             assert (s, rule) == (g, grule)                # saturation guard unchanged
         elif geo["nblk"] <= 4:
             assert s == 1 or (s <= f and s <= 8)          # one wave of clusters
-            if lk <= 192:
+            if lk <= 256:
                 assert s == 1                              # too few 64-token units to split
+            assert s == 1 or s >= 3                        # a 2-way split does not pay
         else:
             e = P.efficiency_loop(geo["T"], geo["U"], geo["nblk"])
             assert (s == e) == (rule == P.RULE_EFF_LOOP)
@@ -273,12 +274,14 @@ def test_seq_aware_sm_structure():
     assert P.num_splits(1, 64, 8, 512, B200_SMS, 0, "seq_aware_sm") == (4, P.RULE_SM_SPLIT)
     assert P.num_splits(2, 128, 16, 512, B200_SMS, 0, "seq_aware_sm") == (4, P.RULE_SM_SPLIT)
     assert P.num_splits(1, 8, 1, 384, B200_SMS, 0, "seq_aware_sm")[0] == 6
-    assert P.num_splits(1, 8, 1, 256, B200_SMS, 0, "seq_aware_sm") == (4, P.RULE_SM_SPLIT)
+    assert P.num_splits(1, 8, 1, 256, B200_SMS, 0, "seq_aware_sm") == (1, P.RULE_SM_SHORT)
+    assert P.num_splits(1, 8, 1, 320, B200_SMS, 0, "seq_aware_sm") == (5, P.RULE_SM_SPLIT)
     assert P.num_splits(1, 8, 1, 192, B200_SMS, 0, "seq_aware_sm") == (1, P.RULE_SM_SHORT)
     assert P.num_splits(4, 64, 8, 256, B200_SMS, 0, "seq_aware_sm") == (1, P.RULE_SM_SHORT)
-    # the SM count enters through f: T = 64 tiles on 148 SMs -> 2 clusters of 2 fit; T = 80 -> 1;
-    # T = 120 -> saturated
-    assert P.num_splits(8, 64, 8, 512, B200_SMS, 0, "seq_aware_sm")[0] == 2
+    # the SM count enters through f: T = 32 tiles on 148 SMs -> clusters of 4 fit; T = 64 -> only
+    # clusters of 2 fit, which do not pay; T = 120 -> saturated
+    assert P.num_splits(4, 64, 8, 512, B200_SMS, 0, "seq_aware_sm")[0] == 4
+    assert P.num_splits(8, 64, 8, 512, B200_SMS, 0, "seq_aware_sm")[0] == 1
     assert P.num_splits(10, 64, 8, 512, B200_SMS, 0, "seq_aware_sm")[0] == 1
     assert P.num_splits(15, 64, 8, 512, B200_SMS, 0, "seq_aware_sm")[1] == P.RULE_SATURATED
     # efficiency region: the loop's workspace-combine split is moved to the one-wave cluster split
@@ -304,6 +307,29 @@ def _measured_grid():
                 key = (int(r.get("batch", 1)), int(r["h_kv"]), int(r["l_k"]))
                 grid.setdefault(key, {})[int(r["s"])] = float(r["latency_us"])
     return grid
+
+
+def test_seq_aware_sm_calibration_lowhead():
+    """The 48 shapes of BASELINE configs[2] (profiles/r01i_lowhead.csv: guarded, the paper's rule and
+    the SM-count-aware pick, interleaved): every current pick was measured and is never > 2 %
+    behind guarded; at L_K = 512 it beats guarded by >= 1.2x for every T <= 32."""
+    import csv
+    import os
+    path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles",
+                        "r01i_lowhead.csv")
+    meas = {}
+    with open(path) as fh:
+        for r in csv.DictReader(fh):
+            meas.setdefault((int(r["batch"]), int(r["h_kv"]), int(r["l_k"])), {})[int(r["num_splits"])] = \
+                float(r["latency_us"])
+    assert len(meas) == 48
+    for (b, hkv, lk), t in meas.items():
+        s, _ = P.num_splits(b, 8 * hkv, hkv, lk, B200_SMS, 0, "seq_aware_sm")
+        g, _ = P.num_splits(b, 8 * hkv, hkv, lk, B200_SMS, 0, "guarded")
+        assert s in t and g in t, (b, hkv, lk, s)
+        assert t[s] <= 1.02 * t[g], (b, hkv, lk, s, g)
+        if lk == 512 and b * hkv <= 32:
+            assert t[g] / t[s] >= 1.2, (b, hkv, lk, s)
 
 
 def test_seq_aware_sm_calibration():
