@@ -82,7 +82,8 @@ typedef enum da_policy {
                                C-ext-1), n_u = ceil(L_K/64),
                                f = largest s <= 16 whose T clusters fit one
                                wave, c = T <= 4 ? 8 : 4: nblk <= 4 -> min(n_u,
-                               c, f) (1 when n_u < 4, or n_u < 8 and T > 16);
+                               c, f) (1 when below 3, n_u < 5, or n_u < 8
+                               and T > 16);
                                else the efficiency loop's e, raised to
                                min(c, n_u, f) when e <= f, or moved to f when
                                e > f >= 2 and (n_u <= 16 f or 2 T f >= U),
@@ -107,7 +108,7 @@ typedef enum da_rule {
   DA_RULE_EFF_LOOP = 5,     /* efficiency loop (DESIGN.md C-amb-2)   */
   DA_RULE_FORCED = 6,       /* DA_POLICY_FIXED                               */
   DA_RULE_EVOLVED = 7,      /* DA_POLICY_EVOLVED, batch == 1      */
-  DA_RULE_SM_SHORT = 8,     /* DA_POLICY_SEQ_AWARE_SM: too few 64-token units */
+  DA_RULE_SM_SHORT = 8,     /* DA_POLICY_SEQ_AWARE_SM: too few units or splits */
   DA_RULE_SM_SPLIT = 9,     /* DA_POLICY_SEQ_AWARE_SM: nblk <= 4 split        */
   DA_RULE_SM_FIT = 10,      /* DA_POLICY_SEQ_AWARE_SM: nblk >= 5, the loop's
                                split moved to a one-wave cluster split      */

@@ -19,7 +19,7 @@ constexpr int kEffMaxSplits = 128;     // efficiency-loop candidate cap (C-amb-2
 constexpr int kMaxForcedSplits = 256;
 constexpr int kEvolvedSplits = 12, kEvolvedShortSplits = 16, kEvolvedShortLk = 256;  // Fig. 1
 // SM-count-aware generalisation (DESIGN.md C-ext-1): B200-calibrated, frozen constants
-constexpr int kSmUnit = 64, kSmMinUnits = 4, kSmMinUnitsWide = 8, kSmWideT = 16;
+constexpr int kSmUnit = 64, kSmMinUnits = 5, kSmMinUnitsWide = 8, kSmWideT = 16, kSmMinSplits = 3;
 constexpr int kSmNarrowT = 4, kSmNarrowSplits = 8, kSmMaxSplits = 4;
 constexpr int kSmStreamUnits = 16, kSmMidT = 8, kSmMidUnits = 64, kSmClusterCap = 12;
 constexpr int kDynMaxSplits = 128;   // DA_POLICY_DYNAMIC per-sequence cap (C-ext-2)

@@ -85,7 +85,7 @@ void decide(int64_t batch, int64_t l_k, int64_t T, int64_t U, int64_t nblk, int 
       int64_t v = T <= kSmNarrowT ? kSmNarrowSplits : kSmMaxSplits;
       if (n_u < v) v = n_u;
       if (f < v) v = f;
-      if (v < 2) { *s = 1; *rule = DA_RULE_SM_SHORT; return; }
+      if (v < kSmMinSplits) { *s = 1; *rule = DA_RULE_SM_SHORT; return; }
       *s = static_cast<int>(v);
       *rule = DA_RULE_SM_SPLIT;
       return;
