@@ -472,6 +472,23 @@ __global__ void __launch_bounds__(threads_for(NW, helpers_for(kCombine)), 1)
     // only a guess for the prefetch below (the lengths may still be written by the preceding
     // kernel, so they are read after the wait and the range recomputed there)
     split_range(min(max(p.l_default, 0), p.l_cap), split, p.num_splits, p.s_magic, t0, t_end, n_tiles);
+    // paged cache: the block table may still be written by the preceding kernel, so the values
+    // read here only steer L2 prefetches of the pages the ring loads first (a stale or torn entry
+    // costs a useless prefetch; out-of-range pages are clipped by the tensor map); the producer
+    // re-reads the table after the wait for the loads themselves
+    if (p.block_table != nullptr && warp == NW && lane == 0 && n_tiles >= 1 && n_tiles <= 2 * NS) {
+      const int32_t* bt = p.block_table + static_cast<int64_t>(b) * p.bt_stride;
+      const uint32_t tpp = static_cast<uint32_t>(p.page_size / kTileN);
+      const uint32_t tile0 = static_cast<uint32_t>(t0 / kTileN);
+      uint32_t j = udiv_magic(tile0, p.page_magic), k = tile0 - j * tpp;
+      const int np = min(n_tiles, NS);
+      for (int i = 0; i < np; ++i) {
+        const int page = *reinterpret_cast<const volatile int32_t*>(bt + j);
+        tma_prefetch_5d(&tmap_k, 0, static_cast<int>(k) * kTileN, 0, kvh, page);
+        tma_prefetch_5d(&tmap_v, 0, static_cast<int>(k) * kTileN, 0, kvh, page);
+        if (++k == tpp) { k = 0; ++j; }
+      }
+    }
     // short splits (<= 2 NS tiles: the latency regime): pull the tiles the ring loads first into L2
     // while the previous kernel drains; L2 is the point of coherence, so the loads after
     // griddepcontrol.wait still see the preceding kernel's writes (Llama 3.57 -> 3.12 us).  A wrong
