@@ -178,6 +178,15 @@ def seq_aware_splits(geo: dict):
     return efficiency_loop(T, U, nblk), RULE_EFF_LOOP
 
 
+def rows_per_cta(G: int, l_k: int) -> int:
+    """Query rows one CTA of the tensor-core path computes: 8, or 16 for G > 8 on
+    long sequences (> 64 units).  Short sequences with G > 8 run two 8-row CTAs per 16 rows: the
+    16-row kernel is twice the MMA work per warp and past the instruction cache, which costs
+    the latency regime 25-40 % (scripts/probe_g16b.py), while on streaming lengths the 8-row split
+    would read every KV tile twice."""
+    return 8 if G <= 8 or ceil_div(l_k, SM_UNIT) <= SM_MID_UNITS else 16
+
+
 def cluster_fit_splits(T: int, U: int) -> int:
     """Largest s in 1..16 whose T clusters of s CTAs are co-resident in one wave:
     T <= floor(CLUSTER_FIT_B200[s] * U / 148); s = 1 (one CTA per tile) always qualifies."""
@@ -189,27 +198,30 @@ def cluster_fit_splits(T: int, U: int) -> int:
 
 
 def seq_aware_sm_splits(geo: dict, l_k: int):
-    """C-ext-1, in this order (n_u = ceil(L_K / 64) units, f = cluster_fit_splits(T, U),
-    c = 8 if T <= 4 else 4):
+    """C-ext-1, in this order (n_u = ceil(L_K / 64) units; T_k = Batch x H_KV x ceil(G / rows),
+    rows = rows_per_cta(G, L_K), the CTA groups the kernel launches per split (= T for G <= 8);
+    f = cluster_fit_splits(T_k, U); c = 8 if T_k <= 4 else 4):
       saturated (5T >= 4U)                      -> 1                      (unchanged FA3 guard)
       nblk <= 4 (the paper's guard region):
-        n_u < 5, or n_u < 8 with T > 16         -> 1                      (short: splitting loses)
+        n_u < 5, or n_u < 8 with T_k > 16       -> 1                      (short: splitting loses)
         s = min(n_u, c, f);  s < 3 -> 1
       nblk >= 5 (efficiency region), e = the unchanged efficiency loop:
         e <= f                                  -> s = max(e, min(c, n_u, f))
-        e > f >= 2 and (n_u <= 16 f or 2 T f >= U) -> s = f
+        e > f >= 2, 8-row CTAs and (n_u <= 16 f or 2 T_k f >= U) -> s = f
         else                                    -> e (streaming: returned as is)
-        then, for short sequences (n_u <= 64): s = min(s, 4) if T > 8, and s = min(s, 12)
-    The split count depends on the tile count T = Batch x H_KV versus the usable SMs U through
-    f, the largest split whose clusters all fit one wave, not on a static L_K guard."""
+        then, for short sequences (n_u <= 64): s = min(s, 4) if T_k > 8, and s = min(s, 12)
+    The split count depends on the CTA groups T_k versus the usable SMs U through f, the largest
+    split whose clusters all fit one wave, not on a static L_K guard."""
     T, U, nblk = geo["T"], geo["U"], geo["nblk"]
     if saturated(T, U):
         return 1, RULE_SATURATED
     n_u = ceil_div(l_k, SM_UNIT)
-    f = cluster_fit_splits(T, U)
-    c = SM_NARROW_SPLITS if T <= SM_NARROW_T else SM_MAX_SPLITS
+    rows = rows_per_cta(geo["G"], l_k)
+    Tk = T // geo["num_m_blocks"] * ceil_div(geo["G"], rows)
+    f = cluster_fit_splits(Tk, U)
+    c = SM_NARROW_SPLITS if Tk <= SM_NARROW_T else SM_MAX_SPLITS
     if nblk <= 4:
-        if n_u < SM_MIN_UNITS or (n_u < SM_MIN_UNITS_WIDE and T > SM_WIDE_T):
+        if n_u < SM_MIN_UNITS or (n_u < SM_MIN_UNITS_WIDE and Tk > SM_WIDE_T):
             return 1, RULE_SM_SHORT
         s = min(n_u, c, f)
         if s < SM_MIN_SPLITS:
@@ -218,12 +230,12 @@ def seq_aware_sm_splits(geo: dict, l_k: int):
     e = efficiency_loop(T, U, nblk)
     if e <= f:
         s = max(e, min(c, n_u, f))
-    elif f >= 2 and (n_u <= SM_STREAM_UNITS * f or 2 * T * f >= U):
+    elif f >= 2 and rows == 8 and (n_u <= SM_STREAM_UNITS * f or 2 * Tk * f >= U):
         s = f
     else:
         return e, RULE_EFF_LOOP
     if n_u <= SM_MID_UNITS:
-        s = min(s, SM_MAX_SPLITS if T > SM_MID_T else SM_CLUSTER_CAP)
+        s = min(s, SM_MAX_SPLITS if Tk > SM_MID_T else SM_CLUSTER_CAP)
     return s, (RULE_EFF_LOOP if s == e else RULE_SM_FIT)
 
 

@@ -416,3 +416,23 @@ def test_varlen_policy_cases():
     assert P.varlen_policy(8, 8, 1, 1024, 148, 0, [1024] + [64] * 7) == P.SEQ_AWARE_SM
     # lengths are clamped to the capacity and empty batches are fine
     assert P.varlen_policy(4, 64, 8, 4096, 148, 0, [0, 0, 0, 0]) == P.SEQ_AWARE_SM
+
+
+def test_rows_per_cta_and_wide_groups():
+    # 8-row CTAs for G <= 8 and for short sequences; 16 for G > 8 beyond 64 units
+    assert [P.rows_per_cta(G, L) for G, L in ((8, 10 ** 6), (16, 4096), (16, 4097), (64, 64), (32, 65536))] == \
+        [8, 8, 16, 8, 16]
+    # G = 16, short: the kernel launches 2 x 8 CTA groups per split -> T_k = 16 -> clusters of 6 fit,
+    # and T_k > 8 caps the split at 4
+    assert P.num_splits(1, 128, 8, 2048, B200_SMS, 0, "seq_aware_sm") == (4, P.RULE_SM_FIT)
+    assert P.num_splits(1, 16, 1, 512, B200_SMS, 0, "seq_aware_sm") == (8, P.RULE_SM_SPLIT)
+    # G = 16, long: 16-row CTAs stream better through the workspace split than a one-wave cluster
+    # split, so the loop's choice stands (= guarded)
+    assert P.num_splits(1, 128, 8, 65536, B200_SMS, 0, "seq_aware_sm") == \
+        P.num_splits(1, 128, 8, 65536, B200_SMS, 0, "guarded")
+    # G <= 8: the CTA groups are the policy's tiles, the rule is unchanged
+    rng = random.Random(3)
+    for _ in range(2000):
+        b, hkv, G, lk = rng.randint(1, 64), rng.choice([1, 2, 4, 8]), rng.choice([1, 2, 4, 8]), rng.randint(1, 9000)
+        geo = P.geometry(b, G * hkv, hkv, lk, 148, 0)
+        assert geo["T"] // geo["num_m_blocks"] * -(-G // P.rows_per_cta(G, lk)) == geo["T"]
