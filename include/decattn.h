@@ -80,15 +80,17 @@ typedef enum da_policy {
                                L_K < 256); batch != 1 -> guarded            */
   DA_POLICY_SEQ_AWARE_SM = 4, /* SM-count-aware generalisation (DESIGN.md
                                C-ext-1), n_u = ceil(L_K/64),
-                               f = largest s <= 16 whose T clusters fit one
-                               wave, c = T <= 4 ? 8 : 4: nblk <= 4 -> min(n_u,
-                               c, f) (1 when below 3, n_u < 5, or n_u < 8
-                               and T > 16);
+                               T_k = B H_KV ceil(G / r) the CTA groups (r = 8
+                               when G <= 8 or n_u <= 64, else 16),
+                               f = largest s <= 16 whose T_k clusters fit
+                               one wave, c = T_k <= 4 ? 8 : 4: nblk <= 4 ->
+                               min(n_u, c, f) (1 when below 3, n_u < 5, or
+                               n_u < 8 and T_k > 16);
                                else the efficiency loop's e, raised to
                                min(c, n_u, f) when e <= f, or moved to f when
-                               e > f >= 2 and (n_u <= 16 f or 2 T f >= U),
-                               then for n_u <= 64 at most 4 (T > 8) or 12;
-                               B200-calibrated                              */
+                               e > f >= 2, r = 8 and (n_u <= 16 f or
+                               2 T_k f >= U), then for n_u <= 64 at most 4
+                               (T_k > 8) or 12; B200-calibrated             */
   DA_POLICY_DYNAMIC = 5     /* per-batch split counts from cache_seqlens on the
                                device (DESIGN.md C-ext-2):
                                W = max(1, ceil(sum_b ceil(n_b/64) * T_b / U)),
@@ -156,7 +158,9 @@ typedef struct da_plan {
   int32_t rule;            /* da_rule                                          */
   int32_t split_unit;      /* 64 tokens: the partition unit                    */
   int32_t path;            /* da_path                                          */
-  int32_t rows_per_cta;    /* query rows one CTA computes (1, 8 or 16)         */
+  int32_t rows_per_cta;    /* query rows one CTA computes: SCALAR 1; MMA 8,
+                              or 16 when G > 8 and (n_u > 64 or the 8-row
+                              grid B H_KV ceil(G/8) s exceeds U)           */
   int32_t combine_mode;    /* da_combine_mode                                  */
   int32_t grid_x;          /* = num_splits; DA_POLICY_DYNAMIC: the head groups
                               (grid_y's static value)                        */

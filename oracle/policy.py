@@ -187,6 +187,16 @@ def rows_per_cta(G: int, l_k: int) -> int:
     return 8 if G <= 8 or ceil_div(l_k, SM_UNIT) <= SM_MID_UNITS else 16
 
 
+def launch_rows(batch: int, G: int, h_kv: int, l_k: int, s: int, U: int) -> int:
+    """Rows per CTA the plan launches with s splits: rows_per_cta(G, L_K), except
+    that 8-row CTAs for G > 8 need their whole grid, Batch x H_KV x ceil(G / 8) x s CTAs, in one
+    wave of U SMs -- past it, the doubled CTA count costs a second wave and 16-row CTAs stand."""
+    rows = rows_per_cta(G, l_k)
+    if rows == 8 and G > 8 and batch * h_kv * ceil_div(G, 8) * s > U:
+        rows = 16
+    return rows
+
+
 def cluster_fit_splits(T: int, U: int) -> int:
     """Largest s in 1..16 whose T clusters of s CTAs are co-resident in one wave:
     T <= floor(CLUSTER_FIT_B200[s] * U / 148); s = 1 (one CTA per tile) always qualifies."""

@@ -47,6 +47,11 @@ int efficiency_loop(int64_t T, int64_t U, int64_t nblk) {
   return 1;
 }
 
+// Query rows per CTA on the tensor-core path: 8, or 16 for G > 8 beyond kSmMidUnits units (two
+// 8-row CTAs halve the per-warp MMA work and keep the kernel inside the instruction cache on
+// short sequences; on long ones they would read every KV tile twice).
+int64_t mma_rows(int64_t G, int64_t l_k) { return G <= 8 || ceil_div(l_k, kSmUnit) <= kSmMidUnits ? 8 : 16; }
+
 // Largest s in 1..16 whose T clusters of s CTAs are all co-resident in one wave of U SMs
 // (the B200 table in config.h scaled by U / 148); s = 1 always qualifies.
 int64_t cluster_fit_splits(int64_t T, int64_t U) {
@@ -56,8 +61,8 @@ int64_t cluster_fit_splits(int64_t T, int64_t U) {
   return best;
 }
 
-void decide(int64_t batch, int64_t l_k, int64_t T, int64_t U, int64_t nblk, int policy, int forced,
-            int* s, int* rule) {
+void decide(int64_t batch, int64_t l_k, int64_t T, int64_t U, int64_t nblk, int64_t G, int64_t mblocks,
+            int policy, int forced, int* s, int* rule) {
   if (policy == DA_POLICY_FIXED) { *s = forced; *rule = DA_RULE_FORCED; return; }
   if (policy == DA_POLICY_DYNAMIC) {          // C-ext-2: the cap; counts are decided per batch on the device
     int64_t cap = ceil_div(l_k, kSplitUnit);
@@ -77,12 +82,15 @@ void decide(int64_t batch, int64_t l_k, int64_t T, int64_t U, int64_t nblk, int 
   if (saturated(T, U)) { *s = 1; *rule = DA_RULE_SATURATED; return; }
   if (policy == DA_POLICY_SEQ_AWARE_SM) {                                 // C-ext-1
     const int64_t n_u = ceil_div(l_k, kSmUnit);
-    const int64_t f = cluster_fit_splits(T, U);
+    // the CTA groups the kernel launches per split (= T for G <= 8)
+    const int64_t rows = mma_rows(G, l_k);
+    const int64_t Tk = T / mblocks * ceil_div(G, rows);
+    const int64_t f = cluster_fit_splits(Tk, U);
     if (nblk <= 4) {
-      if (n_u < kSmMinUnits || (n_u < kSmMinUnitsWide && T > kSmWideT)) {
+      if (n_u < kSmMinUnits || (n_u < kSmMinUnitsWide && Tk > kSmWideT)) {
         *s = 1; *rule = DA_RULE_SM_SHORT; return;
       }
-      int64_t v = T <= kSmNarrowT ? kSmNarrowSplits : kSmMaxSplits;
+      int64_t v = Tk <= kSmNarrowT ? kSmNarrowSplits : kSmMaxSplits;
       if (n_u < v) v = n_u;
       if (f < v) v = f;
       if (v < kSmMinSplits) { *s = 1; *rule = DA_RULE_SM_SHORT; return; }
@@ -91,14 +99,14 @@ void decide(int64_t batch, int64_t l_k, int64_t T, int64_t U, int64_t nblk, int 
       return;
     }
     const int64_t e = efficiency_loop(T, U, nblk);
-    const int64_t c = T <= kSmNarrowT ? kSmNarrowSplits : kSmMaxSplits;
+    const int64_t c = Tk <= kSmNarrowT ? kSmNarrowSplits : kSmMaxSplits;
     int64_t v;
     if (e <= f) {
       int64_t floor_s = c;
       if (n_u < floor_s) floor_s = n_u;
       if (f < floor_s) floor_s = f;
       v = e > floor_s ? e : floor_s;
-    } else if (f >= 2 && (n_u <= kSmStreamUnits * f || 2 * T * f >= U)) {
+    } else if (f >= 2 && rows == 8 && (n_u <= kSmStreamUnits * f || 2 * Tk * f >= U)) {
       v = f;
     } else {
       *s = static_cast<int>(e);            // streaming: the loop's split as is
@@ -106,7 +114,7 @@ void decide(int64_t batch, int64_t l_k, int64_t T, int64_t U, int64_t nblk, int 
       return;
     }
     if (n_u <= kSmMidUnits) {               // short sequences: at most 4 (T > 8) or 12 splits
-      const int64_t cap = T > kSmMidT ? kSmMaxSplits : kSmClusterCap;
+      const int64_t cap = Tk > kSmMidT ? kSmMaxSplits : kSmClusterCap;
       if (v > cap) v = cap;
     }
     *s = static_cast<int>(v);
@@ -128,13 +136,24 @@ void decide(int64_t batch, int64_t l_k, int64_t T, int64_t U, int64_t nblk, int 
 // DA_POLICY_DYNAMIC with a cap above one: the split CTAs are slots assigned on the device.
 bool is_dynamic(const da_plan& p) { return p.policy == DA_POLICY_DYNAMIC && p.num_splits > 1; }
 
+// Rows per CTA on the tensor-core path: mma_rows, except that 8-row CTAs for G > 8 need the
+// whole grid (B x H_KV x ceil(G / 8) x s CTAs) in one wave; past it 16-row CTAs stand.
+int64_t launch_rows(const da_plan& p) {
+  const int64_t G = p.h_q / p.h_kv;
+  int64_t rows = mma_rows(G, p.l_k);
+  if (rows == 8 && G > 8 &&
+      static_cast<int64_t>(p.batch) * p.h_kv * ceil_div(G, 8) * p.num_splits > p.usable_sms)
+    rows = 16;
+  return rows;
+}
+
 // Launch geometry for a plan whose decision fields are set.  Shared by
 // da_plan_make, da_plan_set_combine and da_forward's consistency check.
 void derive_launch(da_plan* p) {
   const int G = p->h_q / p->h_kv;
   const bool mma = p->pack_gqa != 0 && G >= 2;
   p->path = mma ? DA_PATH_MMA : DA_PATH_SCALAR;
-  p->rows_per_cta = mma ? (G <= 8 ? 8 : 16) : 1;
+  p->rows_per_cta = mma ? static_cast<int32_t>(launch_rows(*p)) : 1;
   p->grid_x = p->num_splits;
   p->grid_y = mma ? p->h_kv * static_cast<int32_t>(ceil_div(G, p->rows_per_cta)) : p->h_q;
   p->grid_z = p->batch;
@@ -172,7 +191,7 @@ int default_combine_mode(const da_plan& p) {
   if (s > kMaxClusterSplits) return DA_COMBINE_KERNEL;
   const int G = p.h_q / p.h_kv;
   const bool mma = p.pack_gqa != 0 && G >= 2;
-  const int64_t rows = mma ? (G <= 8 ? 8 : 16) : 1;
+  const int64_t rows = mma ? launch_rows(p) : 1;
   const int64_t clusters = static_cast<int64_t>(p.batch) * (mma ? p.h_kv * ceil_div(G, rows) : p.h_q);
   const int64_t fit = static_cast<int64_t>(kMaxActiveClustersB200[s]) * p.num_sms / 148;
   return clusters <= fit ? DA_COMBINE_CLUSTER : DA_COMBINE_KERNEL;
@@ -221,7 +240,7 @@ extern "C" da_status da_plan_make(int32_t batch, int32_t h_q, int32_t h_kv, int3
   p.total_mblocks = static_cast<int32_t>(T);
 
   int s = 1, rule = 0;
-  decide(batch, l_k, T, p.usable_sms, p.num_n_blocks, policy, forced_splits, &s, &rule);
+  decide(batch, l_k, T, p.usable_sms, p.num_n_blocks, G, p.num_m_blocks, policy, forced_splits, &s, &rule);
   p.num_splits = s;
   p.rule = rule;
   p.split_unit = kSplitUnit;

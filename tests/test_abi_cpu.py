@@ -44,10 +44,10 @@ def test_plan_struct_layout(L):
     assert names == [n for n, _ in L.da_plan._fields_]
 
 
-def _expected_launch(b, hq, hkv, pack, s):
+def _expected_launch(b, hq, hkv, lk, pack, s, U):
     G = hq // hkv
     mma = bool(pack) and G >= 2
-    rows = (8 if G <= 8 else 16) if mma else 1
+    rows = OP.launch_rows(b, G, hkv, lk, s, U) if mma else 1
     gy = hkv * -(-G // rows) if mma else hq
     return (1 if mma else 0), rows, (s, gy, b)
 
@@ -57,12 +57,12 @@ def _expected_launch(b, hq, hkv, pack, s):
 _FIT = [0, 148, 74, 45, 33, 26, 22, 15, 15, 15, 11, 7, 7, 7, 7, 7, 7]
 
 
-def _expected_combine(b, hq, hkv, pack, sms, s):
+def _expected_combine(b, hq, hkv, lk, pack, sms, s, U):
     if s == 1:
         return 0
     if s > 16:
         return 2
-    _, _, (_, gy, gz) = _expected_launch(b, hq, hkv, pack, s)
+    _, _, (_, gy, gz) = _expected_launch(b, hq, hkv, lk, pack, s, U)
     return 1 if gy * gz <= _FIT[s] * sms // 148 else 2
 
 
@@ -73,7 +73,7 @@ def _check_plan(L, b, hq, hkv, lk, pack, margin, sms, pol, forced=0):
     geo = OP.geometry(b, hq, hkv, lk, sms, margin)
     assert (p.num_n_blocks, p.num_m_blocks, p.total_mblocks, p.usable_sms) == (
         geo["nblk"], geo["num_m_blocks"], geo["T"], geo["U"])
-    path, rows, grid = _expected_launch(b, hq, hkv, pack, s)
+    path, rows, grid = _expected_launch(b, hq, hkv, lk, pack, s, geo["U"])
     if pol == "dynamic" and s > 1:      # C-ext-2: split slots decided on the device, workspace combine
         slots = OP.dynamic_slots(b, hkv * geo["num_m_blocks"], geo["U"], s)
         grid = (grid[1], slots, 1)                      # head groups innermost, then split slots
@@ -81,7 +81,7 @@ def _check_plan(L, b, hq, hkv, lk, pack, margin, sms, pol, forced=0):
         assert p.combine_mode == 2
     else:
         assert p.workspace_bytes == (s * b * hq * 129 * 4 if s > 1 else 0)
-        assert p.combine_mode == _expected_combine(b, hq, hkv, pack, sms, s)
+        assert p.combine_mode == _expected_combine(b, hq, hkv, lk, pack, sms, s, geo["U"])
     assert (p.path, p.rows_per_cta, (p.grid_x, p.grid_y, p.grid_z)) == (path, rows, grid)
     assert p.nonempty_splits == min(s, -(-lk // 64))
 
@@ -107,6 +107,16 @@ def test_plan_matches_oracle_grid(L):
                 for lk in LKs:
                     for pol in ("guarded", "seq_aware", "seq_aware_sm", "dynamic"):
                         _check_plan(L, b, G * hkv, hkv, lk, 1, margin, sms, pol)
+
+
+def test_plan_matches_oracle_wide_groups(L):
+    # G > 8 at latency sizes: the policy's T_k and the launch's rows per CTA (8 within one wave
+    # for <= 64 units, else 16) across the short / long boundary
+    LKs = (64, 320, 512, 513, 1024, 2048, 4095, 4096, 4097, 4160, 4161, 8192, 65536)
+    for b, hkv, G in itertools.product((1, 2, 3, 8), (1, 2, 8), (12, 16, 32, 128)):
+        for lk in LKs:
+            for pol in ("guarded", "seq_aware", "seq_aware_sm", "dynamic", "evolved"):
+                _check_plan(L, b, G * hkv, hkv, lk, 1, 0, 148, pol)
 
 
 def test_plan_float_tie_regression(L):

@@ -96,8 +96,11 @@ def test_cluster_combine(s):
 
 @pytest.mark.parametrize("s", [5, 11, 15, 16])
 def test_cluster_combine_16_rows(s):
-    # G = 16 query rows per CTA: the largest push-slot use (s ceil(16 / s) rows per owner)
-    run_and_check(1, 32, 2, 1500, policy="fixed", forced=s, combine_mode=1, seed=13, variant="ragged")
+    # G = 16 query rows per CTA (L_K > 64 units): the largest push-slot use (s ceil(16 / s) rows
+    # per owner)
+    plan, _, _ = run_and_check(1, 32, 2, 4500, policy="fixed", forced=s, combine_mode=1, seed=13,
+                               variant="ragged")
+    assert plan.rows_per_cta == 16
 
 
 # ---- head grouping / paths ----------------------------------------------------
@@ -107,12 +110,23 @@ def test_group_sizes_mma_path(h_q, h_kv):
     run_and_check(2, h_q, h_kv, 300, seed=21)
 
 
+@pytest.mark.parametrize("h_q,h_kv", [(32, 2), (24, 2), (64, 1), (12, 1)])
+def test_group_sizes_16_row_ctas(h_q, h_kv):
+    # G > 8 beyond 64 units: 16 query rows per CTA, incl. ragged G = 12 / 24
+    plan, _, _ = run_and_check(1, h_q, h_kv, 4500, seed=22, variant="ragged")
+    assert plan.rows_per_cta == 16
+
+
 @pytest.mark.parametrize("batch,h_q,h_kv,l_k,policy", [(1, 128, 1, 1000, "seq_aware"), (2, 256, 2, 700, "seq_aware_sm"),
-                                                       (1, 128, 1, 3000, "dynamic")])
+                                                       (1, 128, 1, 3000, "dynamic"), (1, 128, 1, 4500, "seq_aware_sm"),
+                                                       (2, 128, 1, 5000, "dynamic")])
 def test_many_query_rows_per_kv_head(batch, h_q, h_kv, l_k, policy):
-    # G = 128: two policy m-blocks (T = 2 B H_KV) and eight 16-row CTAs per KV head on the MMA path
+    # G = 128: two policy m-blocks (T = 2 B H_KV) and sixteen 8-row (<= 64 units, one-wave grid) or
+    # eight 16-row CTAs per KV head on the MMA path
     plan, _, _ = run_and_check(batch, h_q, h_kv, l_k, policy=policy, variant="ragged", seed=1500)
-    assert plan.num_m_blocks == 2 and plan.rows_per_cta == 16
+    assert plan.num_m_blocks == 2
+    assert plan.rows_per_cta == OP.launch_rows(batch, h_q // h_kv, h_kv, l_k, plan.num_splits, plan.usable_sms)
+    assert plan.rows_per_cta == 16 or l_k <= 4096
 
 
 def test_large_batch_small_cache():

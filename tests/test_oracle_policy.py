@@ -430,6 +430,19 @@ def test_rows_per_cta_and_wide_groups():
     # split, so the loop's choice stands (= guarded)
     assert P.num_splits(1, 128, 8, 65536, B200_SMS, 0, "seq_aware_sm") == \
         P.num_splits(1, 128, 8, 65536, B200_SMS, 0, "guarded")
+    # launch: 8-row CTAs for G > 8 only while the whole grid is one wave
+    assert P.launch_rows(1, 16, 8, 2048, 4, 148) == 8          # 8 x 2 x 4 = 64 CTAs
+    assert P.launch_rows(1, 16, 8, 2048, 14, 148) == 16        # 224 CTAs: two waves
+    assert P.launch_rows(64, 16, 8, 512, 1, 148) == 16
+    assert P.launch_rows(1, 16, 8, 4097, 1, 148) == 16         # long: never 8
+    assert all(P.launch_rows(b, 8, 8, 100, s, 148) == 8 for b in (1, 1000) for s in (1, 16))
+    # the policy's own picks are one-wave grids: it launches the CTAs it planned for
+    rng = random.Random(4)
+    for _ in range(3000):
+        b, hkv, G, lk = rng.randint(1, 16), rng.choice([1, 2, 4, 8]), rng.choice([12, 16, 32, 64]), rng.randint(1, 4096)
+        s, rule = P.num_splits(b, G * hkv, hkv, lk, 148, 0, "seq_aware_sm")
+        if rule in (P.RULE_SM_SPLIT, P.RULE_SM_FIT):
+            assert P.launch_rows(b, G, hkv, lk, s, 148) == 8, (b, hkv, G, lk, s)
     # G <= 8: the CTA groups are the policy's tiles, the rule is unchanged
     rng = random.Random(3)
     for _ in range(2000):
