@@ -45,7 +45,7 @@
 extern "C" {
 #endif
 
-#define DA_ABI_VERSION 3
+#define DA_ABI_VERSION 4
 
 #if defined(__GNUC__)
 #define DA_API __attribute__((visibility("default")))
@@ -361,6 +361,28 @@ DA_API da_status da_combine_peers(int32_t world, int32_t rank, const uint64_t* p
                                   int64_t lse_offset, int64_t flag_offset, const int32_t* epoch, int32_t batch,
                                   int32_t h_q, int32_t head_dim, int32_t out_dtype, void* out, float* lse,
                                   void* cuda_stream);
+
+/*
+ * da_forward_peer - da_forward (out_dtype = DA_F32) and da_peer_signal in one: the kernel that
+ * produces this rank's final rows (the forward for DA_COMBINE_NONE / CLUSTER plans, the combine
+ * kernel for DA_COMBINE_KERNEL) writes them straight into slot e & 1 (e = *epoch + 1) of this
+ * rank's exchange buffer (layout above), and the last of its CTAs to finish (device counter)
+ * fences at system scope, releases e into flag `rank` of every rank's buffer, resets *counter to
+ * 0 and sets *epoch = e.  No copy and no signal launch between the forward and da_combine_peers
+ * (DESIGN.md §6).  Dense caches only.
+ *   plan, q, k_cache, v_cache, l_cap, cache_seqlens, strides, softmax_scale, workspace,
+ *   workspace_bytes: as da_forward (plan->batch, h_q, head_dim define the slot rows);
+ *   world, rank, peer_bases, slot_bytes, lse_offset, flag_offset, epoch: as da_peer_signal;
+ *   counter: device uint32 owned by this rank, zero before the first step (left zero after each).
+ * Errors: those of da_forward and da_peer_signal; DA_ERR_INVALID_ARG for a NULL counter,
+ * DA_ERR_ALIGNMENT for a counter not 4-byte aligned.
+ */
+DA_API da_status da_forward_peer(const da_plan* plan, const void* q, const void* k_cache,
+                                 const void* v_cache, int32_t l_cap, const int32_t* cache_seqlens,
+                                 const int64_t* strides, float softmax_scale, int32_t world, int32_t rank,
+                                 const uint64_t* peer_bases, int64_t slot_bytes, int64_t lse_offset,
+                                 int64_t flag_offset, int32_t* epoch, uint32_t* counter, void* workspace,
+                                 int64_t workspace_bytes, void* cuda_stream);
 
 /* Static, NUL-terminated description of a status code (never NULL). */
 DA_API const char* da_status_string(int32_t status);

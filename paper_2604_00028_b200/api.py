@@ -96,6 +96,24 @@ def forward(plan: L.da_plan, q, k_cache, v_cache, cache_seqlens=None, *, out=Non
     return out, lse
 
 
+def forward_peer(plan: L.da_plan, q, k_cache, v_cache, cache_seqlens, world, rank, peer_bases, slot_bytes,
+                 lse_offset, flag_offset, epoch, counter, *, workspace=None, softmax_scale=0.0, stream=None):
+    """Forward + peer publish via da_forward_peer: this rank's fp32 partial (out, lse) lands in slot
+    epoch & 1 of its exchange buffer and every rank's flag `rank` is released (dist.py
+    PeerSeqShardedDecode).  peer_bases int64 [world], epoch / counter int32 [1], all on the device."""
+    _check_cuda(q, k_cache, v_cache, cache_seqlens, peer_bases, epoch, counter)
+    if q.dtype != torch.bfloat16 or k_cache.dtype != torch.bfloat16 or v_cache.dtype != torch.bfloat16:
+        raise ValueError("q, k_cache, v_cache must be bfloat16")
+    if cache_seqlens is not None and cache_seqlens.dtype != torch.int32:
+        raise ValueError("cache_seqlens must be int32")
+    if workspace is None:
+        workspace = workspace_for(plan, q.device)
+    ws_bytes = 0 if workspace is None else workspace.numel() * workspace.element_size()
+    L.da_forward_peer(plan, q, k_cache, v_cache, k_cache.shape[1], cache_seqlens, _kv_strides(q, k_cache, v_cache),
+                      softmax_scale, world, rank, peer_bases, slot_bytes, lse_offset, flag_offset, epoch, counter,
+                      workspace, ws_bytes, stream)
+
+
 def forward_paged(plan: L.da_plan, q, k_pages, v_pages, block_table, cache_seqlens=None, *, out=None,
                   lse=None, workspace=None, softmax_scale=0.0, out_dtype=torch.bfloat16, stream=None):
     """Decode attention over a paged cache via da_forward_paged.  k/v_pages [num_pages, page_size,

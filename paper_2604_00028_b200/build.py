@@ -27,7 +27,7 @@ LIB = os.path.join(LIBDIR, "libdecattn.so")
 INCLUDE = os.path.join(os.path.dirname(PKG), "include")
 
 SOURCES = ["plan.cpp", "capi.cpp", "fwd.cu", "combine.cu"]
-HEADERS = ["config.h", "internal.h", "ptx.cuh"]
+HEADERS = ["config.h", "internal.h", "ptx.cuh", "pub.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-std=c++17", "-O3", "-lineinfo", "-Xcompiler", "-fPIC,-fvisibility=hidden",
           "-I", CSRC, "-I", INCLUDE]

@@ -116,8 +116,10 @@ struct PagedArgs {
 da_status forward_impl(const da_plan* plan, const void* q, const void* k_cache, const void* v_cache,
                        int32_t l_cap, const int32_t* cache_seqlens, const int64_t* strides,
                        float softmax_scale, int32_t out_dtype, void* out, float* lse, void* workspace,
-                       int64_t workspace_bytes, void* cuda_stream, const PagedArgs& pg) {
-  if (plan == nullptr || q == nullptr || k_cache == nullptr || v_cache == nullptr || out == nullptr)
+                       int64_t workspace_bytes, void* cuda_stream, const PagedArgs& pg,
+                       const PubParams* pub = nullptr) {
+  // pub (da_forward_peer): the final rows go to the exchange slot, out / lse are unused
+  if (plan == nullptr || q == nullptr || k_cache == nullptr || v_cache == nullptr || (out == nullptr && !pub))
     return DA_ERR_INVALID_ARG;
   da_status st = check_plan(plan);
   if (st != DA_OK) return st;
@@ -140,7 +142,7 @@ da_status forward_impl(const da_plan* plan, const void* q, const void* k_cache, 
     if (sd[i] < 0) return DA_ERR_INVALID_ARG;
     if (sd[i] % 8 != 0) return DA_ERR_ALIGNMENT;
   }
-  if (!aligned16(q) || !aligned16(k_cache) || !aligned16(v_cache) || !aligned16(out) ||
+  if (!aligned16(q) || !aligned16(k_cache) || !aligned16(v_cache) || (!pub && !aligned16(out)) ||
       (lse != nullptr && (reinterpret_cast<uintptr_t>(lse) & 3u) != 0))
     return DA_ERR_ALIGNMENT;
   if (cache_seqlens != nullptr && (reinterpret_cast<uintptr_t>(cache_seqlens) & 3u) != 0)
@@ -195,6 +197,10 @@ da_status forward_impl(const da_plan* plan, const void* q, const void* k_cache, 
   p.dyn_tiles = plan->h_kv * plan->num_m_blocks;
   p.dyn_u = plan->usable_sms;
   p.ws_meta = ws_meta;
+  if (pub != nullptr) {
+    p.pub = *pub;     // NONE / CLUSTER: every CTA of the forward writes final rows and counts
+    p.pub.writers = plan->grid_x * plan->grid_y * plan->grid_z;
+  }
 
   cudaStream_t stream = static_cast<cudaStream_t>(cuda_stream);
   if (launch_split_kv_fwd(*plan, tk, tv, p, stream) != cudaSuccess) return DA_ERR_CUDA;
@@ -212,6 +218,10 @@ da_status forward_impl(const da_plan* plan, const void* q, const void* k_cache, 
     c.out = out;
     c.out_f32 = p.out_f32;
     c.lse = lse;
+    if (pub != nullptr) {
+      c.pub = *pub;   // KERNEL: one combine CTA per row writes it and counts
+      c.pub.writers = c.rows;
+    }
     if (launch_lse_combine(c, /*pdl=*/true, stream) != cudaSuccess) return DA_ERR_CUDA;
   }
   return DA_OK;
@@ -376,6 +386,32 @@ extern "C" da_status da_peer_signal(int32_t world, int32_t rank, const uint64_t*
                             lse_offset, flag_offset, epoch, static_cast<cudaStream_t>(cuda_stream)) == cudaSuccess
              ? DA_OK
              : DA_ERR_CUDA;
+}
+
+extern "C" da_status da_forward_peer(const da_plan* plan, const void* q, const void* k_cache,
+                                     const void* v_cache, int32_t l_cap, const int32_t* cache_seqlens,
+                                     const int64_t* strides, float softmax_scale, int32_t world, int32_t rank,
+                                     const uint64_t* peer_bases, int64_t slot_bytes, int64_t lse_offset,
+                                     int64_t flag_offset, int32_t* epoch, uint32_t* counter, void* workspace,
+                                     int64_t workspace_bytes, void* cuda_stream) {
+  if (plan == nullptr) return DA_ERR_INVALID_ARG;
+  int64_t rows = 0;
+  da_status st = check_peer_layout(world, rank, peer_bases, epoch, plan->batch, plan->h_q, plan->head_dim,
+                                   slot_bytes, lse_offset, flag_offset, &rows);
+  if (st != DA_OK) return st;
+  if (counter == nullptr) return DA_ERR_INVALID_ARG;
+  if ((reinterpret_cast<uintptr_t>(counter) & 3u) != 0) return DA_ERR_ALIGNMENT;
+  PubParams pub{};
+  pub.bases = peer_bases;
+  pub.epoch = epoch;
+  pub.count = counter;
+  pub.slot_bytes = slot_bytes;
+  pub.lse_offset = lse_offset;
+  pub.flag_offset = flag_offset;
+  pub.world = world;
+  pub.rank = rank;
+  return forward_impl(plan, q, k_cache, v_cache, l_cap, cache_seqlens, strides, softmax_scale, DA_F32, nullptr,
+                      nullptr, workspace, workspace_bytes, cuda_stream, PagedArgs{}, &pub);
 }
 
 extern "C" da_status da_combine_peers(int32_t world, int32_t rank, const uint64_t* peer_bases, int64_t slot_bytes,

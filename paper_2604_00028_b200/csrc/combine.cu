@@ -19,6 +19,7 @@
 #include "config.h"
 #include "internal.h"
 #include "ptx.cuh"
+#include "pub.cuh"
 
 namespace decattn {
 
@@ -61,7 +62,10 @@ __global__ void __launch_bounds__(kCombineThreads)
     const int b = row / p.h_q, h = row - b * p.h_q;
     prow = static_cast<int64_t>(__ldg(p.meta + b)) * p.h_q + h;
     s = __ldg(p.meta + p.batch + b);
-    if (s == 1) return;                // one split: the forward wrote this row's out / lse itself
+    if (s == 1) {                      // one split: the forward wrote this row's out / lse itself
+      if (p.pub.bases != nullptr && threadIdx.x == 0) pub_arrive(p.pub);
+      return;
+    }
   }
   DA_DASSERT(row < p.rows && s >= 1);
   const float* lse_in = p.lse_in + prow;
@@ -131,15 +135,27 @@ __global__ void __launch_bounds__(kCombineThreads)
   const float inv = L > 0.f ? __frcp_rn(L) : 0.f;
   sum = make_float4(sum.x * inv, sum.y * inv, sum.z * inv, sum.w * inv);
   const float lse = empty ? kNegInf : (M + lg2(L)) * (1.f / kLog2e);
+  // final rows: out / lse, or this step's slot of the exchange buffer (da_forward_peer)
+  void* o_dst = p.out;
+  float* l_dst = p.lse;
+  if (p.pub.bases != nullptr) {
+    const uint64_t sb = pub_slot(p.pub);
+    o_dst = reinterpret_cast<void*>(sb);
+    l_dst = reinterpret_cast<float*>(sb + static_cast<uint64_t>(p.pub.lse_offset));
+  }
   if (p.out_f32) {
-    reinterpret_cast<float4*>(p.out)[static_cast<int64_t>(row) * (kHeadDim / 4) + lane] = sum;
+    reinterpret_cast<float4*>(o_dst)[static_cast<int64_t>(row) * (kHeadDim / 4) + lane] = sum;
   } else {
     uint2 w2;
     w2.x = pack_bf16(sum.x, sum.y);
     w2.y = pack_bf16(sum.z, sum.w);
-    reinterpret_cast<uint2*>(p.out)[static_cast<int64_t>(row) * (kHeadDim / 4) + lane] = w2;
+    reinterpret_cast<uint2*>(o_dst)[static_cast<int64_t>(row) * (kHeadDim / 4) + lane] = w2;
   }
-  if (lane == 0 && p.lse != nullptr) p.lse[row] = lse;
+  if (lane == 0 && l_dst != nullptr) l_dst[row] = lse;
+  if (p.pub.bases != nullptr) {
+    __syncwarp();
+    if (lane == 0) pub_arrive(p.pub);
+  }
   CTRACE(2);
 }
 

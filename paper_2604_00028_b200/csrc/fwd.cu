@@ -49,6 +49,7 @@
 #include "config.h"
 #include "internal.h"
 #include "ptx.cuh"
+#include "pub.cuh"
 
 namespace decattn {
 
@@ -266,15 +267,15 @@ __device__ __forceinline__ void scalar_tile(uint32_t sK, uint32_t sV, int valid,
   }
 }
 
-__device__ __forceinline__ void store_out(const FwdParams& p, size_t row, int d4, float4 v) {
+__device__ __forceinline__ void store_out(const FwdParams& p, void* out, size_t row, int d4, float4 v) {
   DA_DASSERT(row < static_cast<size_t>(p.batch) * p.h_q && d4 >= 0 && d4 < kHeadDim / 4);
   if (p.out_f32) {
-    reinterpret_cast<float4*>(p.out)[row * (kHeadDim / 4) + d4] = v;
+    reinterpret_cast<float4*>(out)[row * (kHeadDim / 4) + d4] = v;
   } else {
     uint2 w;
     w.x = pack_bf16(v.x, v.y);
     w.y = pack_bf16(v.z, v.w);
-    reinterpret_cast<uint2*>(p.out)[row * (kHeadDim / 4) + d4] = w;
+    reinterpret_cast<uint2*>(out)[row * (kHeadDim / 4) + d4] = w;
   }
 }
 
@@ -379,7 +380,7 @@ __device__ __noinline__ int4 dyn_schedule(const FwdParams& p, uint32_t slot, boo
 // rows (MMA path); kCombine: da_combine_mode; NS: ring stages; NW: consumer warps
 // (NS a multiple of NW: warp w owns stages w, w + NW, ... and consumes them in order).
 // ---------------------------------------------------------------------------
-template <int kPath, int kNB, int kCombine, int NS, int NW, bool kDyn>
+template <int kPath, int kNB, int kCombine, int NS, int NW, bool kDyn, bool kPub>
 __global__ void __launch_bounds__(threads_for(NW, helpers_for(kCombine)), 1)
     split_kv_fwd_kernel(const __grid_constant__ CUtensorMap tmap_k,
                         const __grid_constant__ CUtensorMap tmap_v, const FwdParams p) {
@@ -752,6 +753,14 @@ __global__ void __launch_bounds__(threads_for(NW, helpers_for(kCombine)), 1)
   }
   if (threadIdx.x == 0) TRACE(27);
 
+  // final rows: out / lse, or (kPub, da_forward_peer) this step's slot of the exchange buffer
+  void* o_dst = p.out;
+  float* l_dst = p.lse;
+  if constexpr (kPub) {
+    const uint64_t sb = pub_slot(p.pub);
+    o_dst = reinterpret_cast<void*>(sb);
+    l_dst = reinterpret_cast<float*>(sb + static_cast<uint64_t>(p.pub.lse_offset));
+  }
   if constexpr (!kCluster) {
 #pragma unroll
     for (int it = 0; it < kIters; ++it) {
@@ -763,8 +772,8 @@ __global__ void __launch_bounds__(threads_for(NW, helpers_for(kCombine)), 1)
       const float lse_v = eL[it] > 0.f ? (eM[it] + lg2(eL[it])) * kLn2 : kNegInf;
       const size_t row = static_cast<size_t>(b) * p.h_q + hq0 + g;
       if (kCombine == DA_COMBINE_NONE || (kDyn && dyn_single)) {   // kDyn, s_b = 1: the final row
-        store_out(p, row, d4, v);
-        if (d4 == 0 && p.lse != nullptr) p.lse[row] = lse_v;
+        store_out(p, o_dst, row, d4, v);
+        if (d4 == 0 && l_dst != nullptr) l_dst[row] = lse_v;
       } else {  // DA_COMBINE_KERNEL: normalised partial o_i, lse_i (C-part); kDyn: slot-major rows
         const size_t prow = kDyn ? static_cast<size_t>(dslot) * p.h_q + hq0 + g
                                  : static_cast<size_t>(split) * p.batch * p.h_q + row;
@@ -833,12 +842,16 @@ __global__ void __launch_bounds__(threads_for(NW, helpers_for(kCombine)), 1)
       if (t == 0) TRACE(45);
       const float inv = Lsum > 0.f ? __frcp_rn(Lsum) : 0.f;
       const size_t row = static_cast<size_t>(b) * p.h_q + hq0 + g;
-      store_out(p, row, d4, make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv));
-      if (d4 == 0 && p.lse != nullptr) p.lse[row] = Lsum > 0.f ? (M + lg2(Lsum)) * kLn2 : kNegInf;
+      store_out(p, o_dst, row, d4, make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv));
+      if (d4 == 0 && l_dst != nullptr) l_dst[row] = Lsum > 0.f ? (M + lg2(Lsum)) * kLn2 : kNegInf;
       if (t == 0) TRACE(46);
     }
   }
   if (threadIdx.x == 0) TRACE(47);
+  if constexpr (kPub && kCombine != DA_COMBINE_KERNEL) {   // this kernel wrote the final rows
+    __syncthreads();
+    if (threadIdx.x == 0) pub_arrive(p.pub);
+  }
 #ifdef DECATTN_TRACE
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -849,7 +862,7 @@ __global__ void __launch_bounds__(threads_for(NW, helpers_for(kCombine)), 1)
 #endif
 }
 
-template <int kPath, int kNB, int kCombine, bool kDyn = false>
+template <int kPath, int kNB, int kCombine, bool kDyn = false, bool kPub = false>
 cudaError_t launch_impl(const da_plan& plan, const CUtensorMap& tk, const CUtensorMap& tv,
                         const FwdParams& p, cudaStream_t stream) {
   constexpr bool kCluster = kCombine == DA_COMBINE_CLUSTER;
@@ -857,7 +870,7 @@ cudaError_t launch_impl(const da_plan& plan, const CUtensorMap& tk, const CUtens
   constexpr int NS = kDyn ? kStagesNone : stages_for(kCombine);
   constexpr int NW = kDyn ? kWarpsNone : warps_for(kCombine);
   constexpr int kSmem = smem_for(NS, kCluster);
-  auto kern = split_kv_fwd_kernel<kPath, kNB, kCombine, NS, NW, kDyn>;
+  auto kern = split_kv_fwd_kernel<kPath, kNB, kCombine, NS, NW, kDyn, kPub>;
   // One-time (per device) opt-in to > 48 KB of dynamic shared memory.
   static std::atomic<uint64_t> attr_done{0};
   int dev = 0;
@@ -899,11 +912,21 @@ cudaError_t launch_impl(const da_plan& plan, const CUtensorMap& tk, const CUtens
 template <int kPath, int kNB>
 cudaError_t dispatch_combine(const da_plan& plan, const CUtensorMap& tk, const CUtensorMap& tv,
                              const FwdParams& p, cudaStream_t stream) {
+  // kPub (da_forward_peer) instantiations only where the forward writes final rows; with the
+  // workspace combine the combine kernel publishes and the forward is the plain one
+  const bool pub = p.pub.bases != nullptr;
   switch (plan.combine_mode) {
-    case DA_COMBINE_NONE: return launch_impl<kPath, kNB, DA_COMBINE_NONE>(plan, tk, tv, p, stream);
-    case DA_COMBINE_CLUSTER: return launch_impl<kPath, kNB, DA_COMBINE_CLUSTER>(plan, tk, tv, p, stream);
+    case DA_COMBINE_NONE:
+      if (pub) return launch_impl<kPath, kNB, DA_COMBINE_NONE, false, true>(plan, tk, tv, p, stream);
+      return launch_impl<kPath, kNB, DA_COMBINE_NONE>(plan, tk, tv, p, stream);
+    case DA_COMBINE_CLUSTER:
+      if (pub) return launch_impl<kPath, kNB, DA_COMBINE_CLUSTER, false, true>(plan, tk, tv, p, stream);
+      return launch_impl<kPath, kNB, DA_COMBINE_CLUSTER>(plan, tk, tv, p, stream);
     default:
-      if (is_dynamic(plan)) return launch_impl<kPath, kNB, DA_COMBINE_KERNEL, true>(plan, tk, tv, p, stream);
+      if (is_dynamic(plan)) {   // s_b = 1 rows are final rows written by the forward
+        if (pub) return launch_impl<kPath, kNB, DA_COMBINE_KERNEL, true, true>(plan, tk, tv, p, stream);
+        return launch_impl<kPath, kNB, DA_COMBINE_KERNEL, true>(plan, tk, tv, p, stream);
+      }
       return launch_impl<kPath, kNB, DA_COMBINE_KERNEL>(plan, tk, tv, p, stream);
   }
 }

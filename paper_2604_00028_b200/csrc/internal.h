@@ -11,6 +11,19 @@ namespace decattn {
 
 // Arguments of the split-KV forward kernel (everything except the two
 // tensor maps, which are passed as __grid_constant__ parameters).
+// da_forward_peer: the kernel that writes the final rows writes them into slot e & 1 (e = *epoch
+// + 1) of this rank's exchange buffer, and the last of its `writers` CTAs releases e into flag
+// `rank` of every rank's buffer (the da_peer_signal step fused into the producer of the rows).
+// bases == nullptr: off.
+struct PubParams {
+  const uint64_t* bases;    // device [world]: every rank's exchange buffer as mapped on this GPU
+  int32_t* epoch;           // device: this rank's step epoch
+  uint32_t* count;          // device: CTAs of this step that wrote their rows (0 between steps)
+  int64_t slot_bytes, lse_offset, flag_offset;
+  int32_t world, rank;
+  int32_t writers;          // CTAs of the writing launch
+};
+
 struct FwdParams {
   const uint16_t* q;        // bf16 [B, H_Q, d]
   int64_t q_sb, q_sh;       // strides in elements
@@ -39,6 +52,7 @@ struct FwdParams {
   int32_t dyn_tiles;            // T_b = H_KV * num_m_blocks
   int32_t dyn_u;                // usable SMs U
   int32_t* ws_meta;             // [2, B] int32 (first slot, split count) or nullptr
+  PubParams pub;                // fused peer publish (NONE / CLUSTER: this kernel writes the rows)
 };
 
 // Division by a launch-invariant divisor d without an integer divide: with m = ceil(2^38 / d),
@@ -61,6 +75,7 @@ struct CombineParams {
   const int32_t* meta;      // [2, B] or nullptr (uniform: num_splits at o + i * o_stride)
   int32_t h_q;
   int32_t batch;
+  PubParams pub;            // fused peer publish (KERNEL combine: this kernel writes the rows)
 };
 
 // plan.cpp

@@ -163,13 +163,16 @@ def peer_layout(batch: int, h_q: int, head_dim: int, world: int):
 
 
 class PeerSeqShardedDecode:
-    """Long-context mode with the exchange over peer memory: local partial (fp32) -> da_peer_signal
-    (copy into slot epoch & 1 of this rank's symmetric buffer, epoch into every peer's flag slot) ->
-    da_combine_peers (acquire every flag, read the partials from the peers' buffers, LSE-merge).  No
-    NCCL call on the step; every call can be captured in a CUDA graph (monotonic epochs)."""
+    """Long-context mode with the exchange over peer memory.  fused (default): da_forward_peer (the
+    kernel that produces the local partial writes it into slot epoch & 1 of this rank's symmetric
+    buffer and its last CTA releases the epoch into every peer's flag slot) -> da_combine_peers
+    (acquire every flag, read the partials from the peers' buffers, LSE-merge): two launches per
+    step.  fused=False: forward into a local fp32 partial -> da_peer_signal (copy + release) ->
+    da_combine_peers.  No NCCL call on the step; every call can be captured in a CUDA graph
+    (monotonic epochs)."""
 
     def __init__(self, batch: int, h_q: int, h_kv: int, l_k_total: int, head_dim: int = 128, *,
-                 group=None, policy="seq_aware", device=None):
+                 group=None, policy="seq_aware", device=None, fused: bool = True):
         import torch.distributed._symmetric_memory as symm
 
         from . import api
@@ -191,23 +194,30 @@ class PeerSeqShardedDecode:
         dist.barrier(group)                                # every buffer zeroed before any signal
         self.bases = torch.tensor([int(x) for x in self.hdl.buffer_ptrs], dtype=torch.int64, device=self.device)
         self.epoch = torch.zeros(1, dtype=torch.int32, device=self.device)
+        self.fused = fused
+        self.counter = torch.zeros(1, dtype=torch.int32, device=self.device)   # da_forward_peer: writer CTAs
         self.plan = api.make_plan(batch, h_q, h_kv, self.l_local, head_dim, True, 0, None, policy)
         self._ws = api.workspace_for(self.plan, self.device)
         self.o_local = torch.empty((batch, h_q, head_dim), dtype=torch.float32, device=self.device)
         self.lse_local = torch.empty((batch, h_q), dtype=torch.float32, device=self.device)
 
     def step(self, q, k_local, v_local, seqlens_local=None, out=None, lse=None):
-        """One decode step: local partial -> signal -> pull-combine.  Returns (out, lse)."""
+        """One decode step: local partial (published to the peers) -> pull-combine.  Returns (out, lse)."""
         from . import _lib as L
         from . import api
-        api.forward(self.plan, q, k_local, v_local, seqlens_local, out=self.o_local, lse=self.lse_local,
-                    workspace=self._ws, out_dtype=torch.float32)
+        if self.fused:
+            api.forward_peer(self.plan, q, k_local, v_local, seqlens_local, self.world, self.rank, self.bases,
+                             self.slot_bytes, self.lse_offset, self.flag_offset, self.epoch, self.counter,
+                             workspace=self._ws)
+        else:
+            api.forward(self.plan, q, k_local, v_local, seqlens_local, out=self.o_local, lse=self.lse_local,
+                        workspace=self._ws, out_dtype=torch.float32)
+            L.da_peer_signal(self.world, self.rank, self.bases, self.o_local, self.lse_local, self.batch,
+                             self.h_q, self.d, self.slot_bytes, self.lse_offset, self.flag_offset, self.epoch)
         if out is None:
             out = torch.empty((self.batch, self.h_q, self.d), dtype=torch.bfloat16, device=self.device)
         if lse is None:
             lse = torch.empty((self.batch, self.h_q), dtype=torch.float32, device=self.device)
-        L.da_peer_signal(self.world, self.rank, self.bases, self.o_local, self.lse_local, self.batch, self.h_q,
-                         self.d, self.slot_bytes, self.lse_offset, self.flag_offset, self.epoch)
         L.da_combine_peers(self.world, self.rank, self.bases, self.slot_bytes, self.lse_offset, self.flag_offset,
                            self.epoch, self.batch, self.h_q, self.d,
                            L.DA_F32 if out.dtype == torch.float32 else L.DA_BF16, out, lse)

@@ -383,6 +383,32 @@ def test_peer_exchange_validation(L):
     assert comb(out=A2 + 8) == L.DA_ERR_ALIGNMENT
 
 
+def test_forward_peer_validation(L):
+    # da_forward_peer: the peer-layout and counter checks, then da_forward's, all before any CUDA call
+    A2 = 1 << 22
+    plan = L.da_plan_make(1, 8, 1, 512, 128, 1, 0, 148, "seq_aware", 0)
+    slot, lo, fo = 4128, 4096, 2 * 4128
+
+    def fwd(**kw):
+        a = dict(plan=plan, q=A2, k_cache=A2, v_cache=A2, l_cap=512, cache_seqlens=None, strides=None,
+                 softmax_scale=0.0, world=2, rank=0, peer_bases=A2, slot_bytes=slot, lse_offset=lo,
+                 flag_offset=fo, epoch=A2, counter=A2, workspace=A2, workspace_bytes=1 << 20, stream=0)
+        a.update(kw)
+        with pytest.raises(L.DecAttnError) as e:
+            L.da_forward_peer(**a)
+        return e.value.status
+    assert fwd(counter=None) == L.DA_ERR_INVALID_ARG
+    assert fwd(counter=A2 + 2) == L.DA_ERR_ALIGNMENT
+    assert fwd(epoch=None) == L.DA_ERR_INVALID_ARG
+    assert fwd(rank=2) == L.DA_ERR_INVALID_ARG
+    assert fwd(lse_offset=16) == L.DA_ERR_INVALID_ARG            # slot rows follow the plan's B x H_Q
+    assert fwd(q=None) == L.DA_ERR_INVALID_ARG
+    assert fwd(l_cap=100) == L.DA_ERR_INVALID_ARG
+    assert fwd(k_cache=A2 + 8) == L.DA_ERR_ALIGNMENT
+    wide = L.da_plan_make(1, 64, 8, 512, 128, 1, 0, 148, "seq_aware", 0)
+    assert fwd(plan=wide) == L.DA_ERR_INVALID_ARG                # 64 rows do not fit the 8-row slot
+
+
 def test_peer_layout():
     from paper_2604_00028_b200.dist import peer_layout
     for B, H, W in ((1, 64, 8), (3, 24, 2), (1, 8, 1), (128, 64, 64)):

@@ -33,11 +33,12 @@ def one_rank_group():
     dist.destroy_process_group()
 
 
+@pytest.mark.parametrize("fused", [True, False])
 @pytest.mark.parametrize("batch,h_q,h_kv,l_k", [(1, 64, 8, 4096), (2, 8, 1, 1500)])
-def test_peer_exchange_matches_oracle(one_rank_group, batch, h_q, h_kv, l_k):
+def test_peer_exchange_matches_oracle(one_rank_group, batch, h_q, h_kv, l_k, fused):
     from paper_2604_00028_b200.dist import PeerSeqShardedDecode
     inp = synth.make_inputs(batch, h_q, h_kv, l_k, seed=1600, device="cuda")
-    sd = PeerSeqShardedDecode(batch, h_q, h_kv, l_k, device="cuda")
+    sd = PeerSeqShardedDecode(batch, h_q, h_kv, l_k, device="cuda", fused=fused)
     assert sd.world == 1 and sd.l_local == l_k
     ref_o, ref_l = OA.decode_attention(*(synth.to_f64(inp[n]) for n in ("q", "k", "v", "seqlens")))
     out = torch.empty((batch, h_q, 128), dtype=torch.bfloat16, device="cuda")
@@ -60,3 +61,33 @@ def test_peer_exchange_matches_oracle(one_rank_group, batch, h_q, h_kv, l_k):
         torch.cuda.synchronize()
         assert_out_close(synth.to_f64(out), ref_o)
     assert int(sd.epoch.item()) == 3 + 2 * 4            # capture records, the two replays run
+    assert int(sd.counter.item()) == 0                  # da_forward_peer leaves its counter at zero
+
+
+@pytest.mark.parametrize("batch,h_q,h_kv,l_k,policy,mode", [
+    (1, 64, 8, 300, "seq_aware", 0),        # s = 1: the forward writes the slot rows, every CTA counts
+    (2, 8, 1, 1500, "seq_aware", 1),        # cluster combine: the row owners write and count
+    (1, 64, 8, 4096, "seq_aware", 2),       # workspace combine: the combine kernel writes and counts
+    (4, 16, 2, 3000, "dynamic", 2),         # dynamic: s_b = 1 rows from the forward, the rest combined
+])
+def test_forward_peer_every_combine_mode(one_rank_group, batch, h_q, h_kv, l_k, policy, mode):
+    # da_forward_peer: the writer of the final rows publishes (slot e & 1, epoch flags), whichever
+    # kernel that is; checked against the oracle over several epochs (both slots)
+    from paper_2604_00028_b200.dist import PeerSeqShardedDecode
+    inp = synth.make_inputs(batch, h_q, h_kv, l_k, seed=1610, device="cuda",
+                            variant="ragged" if policy == "dynamic" else "normal")
+    sd = PeerSeqShardedDecode(batch, h_q, h_kv, l_k, device="cuda", policy=policy, fused=True)
+    assert sd.plan.combine_mode == mode
+    ref_o, ref_l = OA.decode_attention(*(synth.to_f64(inp[n]) for n in ("q", "k", "v", "seqlens")))
+    out = torch.empty((batch, h_q, 128), dtype=torch.float32, device="cuda")
+    lse = torch.empty((batch, h_q), dtype=torch.float32, device="cuda")
+    for e in range(1, 5):
+        out.zero_()
+        sd.step(inp["q"], inp["k"], inp["v"], inp["seqlens"], out, lse)
+        torch.cuda.synchronize()
+        assert_out_close(synth.to_f64(out), ref_o)
+        assert_lse_close(synth.to_f64(lse), ref_l)
+        assert int(sd.epoch.item()) == e and int(sd.counter.item()) == 0
+    # the partial of the last step sits in slot 4 & 1 = 0 of the exchange buffer, flag 0 holds 4
+    flags = sd.buf.view(torch.int32)[sd.flag_offset // 4: sd.flag_offset // 4 + 1]
+    assert int(flags.item()) == 4
