@@ -438,7 +438,10 @@ def main():
     ap.add_argument("--no-extras", action="store_true", help="skip the A/B and streaming extras")
     ap.add_argument("--ab-rounds", type=int, default=21)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
-    ap.add_argument("--exchange", default="p2p", choices=["nccl", "p2p"],
+    ap.add_argument("--seq-shard", action="store_true",
+                    help="long_context: take the sequence-sharded path (exchange included) even at N = 1 "
+                         "(a one-rank group; checks the sharded step on one GPU)")
+    ap.add_argument("--exchange", default="p2p", choices=["nccl", "p2p", "p2p-split"],
                     help="long_context with N > 1: the exchange over peer memory (default: da_peer_signal + "
                          "da_combine_peers over torch symmetric memory) or an NCCL all-gather + da_combine")
     ap.add_argument("--policy", default="seq_aware_sm",
@@ -461,6 +464,15 @@ def main():
     # waits on another rank's, and the ranks share the GPU, so the number is not a bench value)
     backend = os.environ.get("DECATTN_BENCH_BACKEND", "nccl")
     gpu_index = 0 if os.environ.get("DECATTN_BENCH_ONE_GPU") == "1" else local_rank
+    if world == 1 and args.seq_shard and args.workload == "long_context":
+        import socket
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        if "MASTER_PORT" not in os.environ:
+            with socket.socket() as sk:
+                sk.bind(("127.0.0.1", 0))
+                os.environ["MASTER_PORT"] = str(sk.getsockname()[1])
+        torch.cuda.set_device(gpu_index)
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", gpu_index))
     if world > 1:
         torch.cuda.set_device(gpu_index)
         if backend == "nccl":
@@ -494,30 +506,43 @@ def main():
         return float(t.item())
 
     cfg = WORKLOADS[args.workload]
-    long_sharded = args.workload == "long_context" and world > 1
+    long_sharded = args.workload == "long_context" and (world > 1 or args.seq_shard)
     if long_sharded:
         from paper_2604_00028_b200.dist import PeerSeqShardedDecode, SeqShardedDecode
-        cls = PeerSeqShardedDecode if args.exchange == "p2p" else SeqShardedDecode
-        sd = cls(cfg["batch"], cfg["h_q"], cfg["h_kv"], cfg["l_k"], HEAD_DIM, device=dev, policy=args.policy)
+        p2p = args.exchange.startswith("p2p")
+        if p2p:
+            sd = PeerSeqShardedDecode(cfg["batch"], cfg["h_q"], cfg["h_kv"], cfg["l_k"], HEAD_DIM, device=dev,
+                                      policy=args.policy, fused=args.exchange == "p2p")
+        else:
+            sd = SeqShardedDecode(cfg["batch"], cfg["h_q"], cfg["h_kv"], cfg["l_k"], HEAD_DIM, device=dev,
+                                  policy=args.policy)
         local_cfg = dict(cfg, l_k=sd.l_local)
         inp = synth.make_inputs(cfg["batch"], cfg["h_q"], cfg["h_kv"], sd.l_local, device=dev, seed=1000 + rank)
+        # rotate through shard copies totalling > 2x L2 (a shard of 8 ranks is 67 MB < L2)
+        shard_bytes = inp["k"].numel() * inp["k"].element_size() * 2
+        nkv = 1 if shard_bytes >= 2 * l2 else -(-2 * l2 // shard_bytes) + 1
+        ks = [inp["k"]] + [inp["k"].clone() for _ in range(nkv - 1)]
+        vs = [inp["v"]] + [inp["v"].clone() for _ in range(nkv - 1)]
         out = torch.empty((cfg["batch"], cfg["h_q"], HEAD_DIM), dtype=torch.bfloat16, device=dev)
         lse = torch.empty((cfg["batch"], cfg["h_q"]), dtype=torch.float32, device=dev)
         plan = sd.plan
         with torch.cuda.stream(stream):
-            for _ in range(args.warmup):
-                sd.step(inp["q"], inp["k"], inp["v"], None, out, lse)
+            for i in range(args.warmup):
+                sd.step(inp["q"], ks[i % nkv], vs[i % nkv], None, out, lse)
         torch.cuda.synchronize()
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g, stream=stream):
-            for _ in range(args.steps):
-                sd.step(inp["q"], inp["k"], inp["v"], None, out, lse)
+            for i in range(args.steps):
+                sd.step(inp["q"], ks[i % nkv], vs[i % nkv], None, out, lse)
         step_bytes_total = alg_bytes(cfg["batch"], cfg["h_q"], cfg["h_kv"], cfg["l_k"])
-        kernels_per_step = (2 if plan.combine_mode == L.DA_COMBINE_KERNEL else 1) + (2 if args.exchange == "p2p" else 1)
+        # forward (+ workspace combine) + the exchange: fused publish -> pull-combine (1 launch),
+        # signal + pull-combine (2), NCCL all-gather (library) + da_combine (1)
+        kernels_per_step = (2 if plan.combine_mode == L.DA_COMBINE_KERNEL else 1) + (2 if args.exchange == "p2p-split" else 1)
         scaling = "strong"
-        l2_note = "sequence shard per rank > 2x L2 + 256 MiB L2 scrub before the timed replay"
-        parallelism = (f"seq-sharded sp{world} + peer-memory exchange (signal + pull-combine)" if args.exchange == "p2p"
-                       else f"seq-sharded sp{world} + NCCL all-gather + LSE combine")
+        l2_note = f"{nkv} rotating copies of the sequence shard (> 2x L2) + 256 MiB L2 scrub before the timed replay"
+        parallelism = {"p2p": f"seq-sharded sp{world} + peer-memory exchange (fused publish + pull-combine)",
+                       "p2p-split": f"seq-sharded sp{world} + peer-memory exchange (signal + pull-combine)",
+                       "nccl": f"seq-sharded sp{world} + NCCL all-gather + LSE combine"}[args.exchange]
     else:
         local_cfg = cfg
         w = Workload(cfg, dev, 1000 + rank, l2)
@@ -616,7 +641,9 @@ def main():
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "traffic": trec.get("dram_bytes_per_launch") if trec else None,
                      "kernel": "split_kv_fwd_kernel", "peak_source": peak_src,
-                     "note": "latency-bound config (2.1 MB per step); see roofline_streaming for the HBM-bound configs"},
+                     "note": ("latency-bound config (2.1 MB per step); see roofline_streaming for the HBM-bound configs"
+                              if alg_bytes(**local_cfg) < (64 << 20) else
+                              "HBM-bound config; achieved = algorithmic bytes of the step / step time")},
         "cpu_baseline": cpu_baseline(local_cfg, args.cpu_seconds) if world == 1 else None,
         "e2e": {"value": round(e2e_value, 3), "unit": "GB/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": round(e2e_ms_max / args.steps, 6)},
@@ -626,7 +653,7 @@ def main():
     }
     line.update(extras)
     print(json.dumps(line), flush=True)
-    if world > 1:
+    if dist.is_initialized():
         dist.destroy_process_group()
     return 0
 

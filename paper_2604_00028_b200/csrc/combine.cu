@@ -197,17 +197,20 @@ __global__ void __launch_bounds__(kCombineThreads)
     peer_combine_kernel(const uint64_t* peer_bases, int64_t slot_bytes, int64_t lse_offset, int64_t flag_offset,
                         const int32_t* epoch, int32_t world, int32_t rank, int32_t rows, int32_t out_f32,
                         void* out, float* lse_out) {
-  pdl_launch_dependents();
-  pdl_wait();
   constexpr int kWarps = kCombineThreads / 32;
   __shared__ float4 s_acc[kWarps][32];
   __shared__ float s_m[kWarps], s_l[kWarps];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int row = blockIdx.x;
+  // the pointer table is set up once, before any step: read it while the producer drains, so the
+  // step's dependent chain is epoch -> flags -> partials
+  const uint64_t own = peer_bases[rank];
+  const uint64_t first = warp < world ? peer_bases[warp] : 0;
+  pdl_launch_dependents();
+  pdl_wait();
   const uint32_t e = static_cast<uint32_t>(*epoch);
   if (threadIdx.x == 0) {
-    const uint32_t* flags =
-        reinterpret_cast<const uint32_t*>(peer_bases[rank] + static_cast<uint64_t>(flag_offset));
+    const uint32_t* flags = reinterpret_cast<const uint32_t*>(own + static_cast<uint64_t>(flag_offset));
     for (int q = 0; q < world; ++q)
       while (ld_acquire_sys_u32(flags + q) < e) {
       }
@@ -217,7 +220,7 @@ __global__ void __launch_bounds__(kCombineThreads)
   float m = kNegInf, Lw = 0.f;
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
   for (int i = warp; i < world; i += kWarps) {
-    const uint64_t base = peer_bases[i] + slot_off;
+    const uint64_t base = (i == warp ? first : peer_bases[i]) + slot_off;
     const float li = reinterpret_cast<const float*>(base + static_cast<uint64_t>(lse_offset))[row] * kLog2e;
     const float4 oi = reinterpret_cast<const float4*>(base)[static_cast<int64_t>(row) * (kHeadDim / 4) + lane];
     const float mb = fmaxf(m, li);
