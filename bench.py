@@ -389,10 +389,13 @@ def run_reference(args, rank, world):
 
 
 # ----------------------------------------------------------------------------------------------
-def e2e_measure(dec, L, cfg, dev, stream, steps, warmup, policy="seq_aware_sm"):
+def e2e_measure(dec, L, cfg, dev, stream, steps, warmup, policy="seq_aware_sm", depth=2):
     """Same metric through the C ABI with HOST buffers (da_forward_host): per step da_plan_make,
     then the H2D copies of q/K/V from pinned memory, the forward and the D2H copies of out + lse,
-    all enqueued on one stream inside the timed region (CUDA events around the K steps)."""
+    enqueued on one stream.  depth > 1 pipelines consecutive steps over `depth` streams (each with
+    its own device staging and host output buffer, as a serving loop with several requests in
+    flight would), so one step's forward and D2H overlap the next step's H2D.  CUDA events around
+    the K steps (every stream joined into the end event)."""
     b, hq, hkv, lk = cfg["batch"], cfg["h_q"], cfg["h_kv"], cfg["l_k"]
     inp = synth.make_inputs(b, hq, hkv, lk, seed=2000)
     hq_ = inp["q"].contiguous().pin_memory()
@@ -403,28 +406,38 @@ def e2e_measure(dec, L, cfg, dev, stream, steps, warmup, policy="seq_aware_sm"):
     kv[1].copy_(inp["v"])
     hk_, hv_ = kv[0], kv[1]
     ob = b * hq * HEAD_DIM * 2
-    ol = torch.empty(ob + 4 * b * hq, dtype=torch.uint8).pin_memory()
-    h_out = ol[:ob].view(torch.bfloat16).view(b, hq, HEAD_DIM)
-    h_lse = ol[ob:].view(torch.float32).view(b, hq)
+    outs = []
+    for _ in range(depth):
+        ol = torch.empty(ob + 4 * b * hq, dtype=torch.uint8).pin_memory()
+        outs.append((ol[:ob].view(torch.bfloat16).view(b, hq, HEAD_DIM), ol[ob:].view(torch.float32).view(b, hq)))
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
-    staging = dec.HostStaging(dev)
+    streams = [stream] + [torch.cuda.Stream(device=dev) for _ in range(depth - 1)]
+    stagings = [dec.HostStaging(dev) for _ in range(depth)]
 
-    def step():
+    def step(j):
         plan = L.da_plan_make(b, hq, hkv, lk, HEAD_DIM, 1, 0, sms, L.POLICIES[policy], 0)
-        dec.forward_host(plan, hq_, hk_, hv_, None, out=h_out, lse=h_lse, staging=staging, stream=stream)
+        h_out, h_lse = outs[j % depth]
+        dec.forward_host(plan, hq_, hk_, hv_, None, out=h_out, lse=h_lse, staging=stagings[j % depth],
+                         stream=streams[j % depth])
 
-    for _ in range(max(warmup, 1)):
-        step()
+    for j in range(max(warmup, depth)):
+        step(j)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(steps):
-        step()
-    e1.record(stream)
+    e0.record(streams[0])
+    for st in streams[1:]:
+        st.wait_event(e0)
+    for j in range(steps):
+        step(j)
+    for st in streams[1:]:
+        ev = torch.cuda.Event()
+        ev.record(st)
+        streams[0].wait_event(ev)
+    e1.record(streams[0])
     e1.synchronize()
     ms = e0.elapsed_time(e1)
     h2d = sum(t.numel() * t.element_size() for t in (hq_, hk_, hv_))
-    d2h = h_out.numel() * h_out.element_size() + h_lse.numel() * h_lse.element_size()
+    d2h = outs[0][0].numel() * outs[0][0].element_size() + outs[0][1].numel() * outs[0][1].element_size()
     return ms, h2d, d2h
 
 
@@ -591,9 +604,12 @@ def main():
     value = step_bytes_total * args.steps / (ms_max * 1e-3) / 1e9
 
     # ---- end to end through the public API with host buffers ----
-    e2e_ms, h2d, d2h = e2e_measure(dec, L, local_cfg, dev, stream, args.steps, args.warmup, args.policy)
+    e2e_ms, h2d, d2h = e2e_measure(dec, L, local_cfg, dev, stream, args.steps, args.warmup, args.policy, depth=2)
+    e2e_serial_ms, _, _ = e2e_measure(dec, L, local_cfg, dev, stream, args.steps, args.warmup, args.policy, depth=1)
     e2e_ms_max = max_over_ranks(e2e_ms)
-    e2e_value = (alg_bytes(**local_cfg) * (world if not long_sharded else 1)) * args.steps / (e2e_ms_max * 1e-3) / 1e9
+    e2e_serial_max = max_over_ranks(e2e_serial_ms)
+    e2e_scale = alg_bytes(**local_cfg) * (world if not long_sharded else 1) * args.steps / 1e9
+    e2e_value = e2e_scale / (e2e_ms_max * 1e-3)
 
     extras = {}
     if rank == 0 and world == 1 and not args.no_extras:
@@ -646,7 +662,10 @@ def main():
                               "HBM-bound config; achieved = algorithmic bytes of the step / step time")},
         "cpu_baseline": cpu_baseline(local_cfg, args.cpu_seconds) if world == 1 else None,
         "e2e": {"value": round(e2e_value, 3), "unit": "GB/s", "h2d_bytes_per_step": h2d,
-                "d2h_bytes_per_step": d2h, "ms_per_step": round(e2e_ms_max / args.steps, 6)},
+                "d2h_bytes_per_step": d2h, "ms_per_step": round(e2e_ms_max / args.steps, 6),
+                "pipeline_depth": 2, "serial_value": round(e2e_scale / (e2e_serial_max * 1e-3), 3),
+                "note": "da_forward_host per step (H2D of q/K/V from pinned memory, forward, D2H of out/lse); "
+                        "value: two steps in flight on two streams, serial_value: one stream"},
         "gpu_launches": args.steps * kernels_per_step,
         "clocks": clk.summary(),
         "device": {"name": props.name, "sms": num_sms, "l2_bytes": l2},
