@@ -25,3 +25,19 @@ def test_bench_two_ranks_batch_sharded():
     d = json.loads(lines[0])
     assert d["n_gpus"] == 2 and d["scaling"] == "weak" and d["config"]["global_batch"] == 2
     assert d["value"] > 0 and d["e2e"]["value"] > 0 and d["gpu_launches"] == 20
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("exchange,launches", [("p2p", 2), ("p2p-split", 3), ("nccl", 2)])
+def test_bench_sequence_sharded_step_one_rank(exchange, launches):
+    # the long-context sequence-sharded step (forward + exchange + combine) through bench.py on a
+    # one-rank group: the same code path the N-GPU run takes, every exchange flavour
+    cmd = [sys.executable, os.path.join(ROOT, "bench.py"), "--workload", "long_context", "--seq-shard",
+           "--exchange", exchange, "--steps", "5", "--warmup", "3", "--no-extras", "--cpu-seconds", "0.5"]
+    r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    assert d["scaling"] == "strong" and d["config"]["workload"] == "long_context"
+    assert d["value"] > 1000 and d["gpu_launches"] == 5 * launches
