@@ -66,6 +66,25 @@ def _kv_strides(q, k, v):
             v.stride(0), v.stride(1), v.stride(2))
 
 
+def _check_shapes(plan: L.da_plan, q, k, v, cache_seqlens=None, out=None, lse=None, paged=False):
+    """The tensors against the plan's shape (the C ABI takes bare pointers, so a mismatch would
+    read or write out of bounds): q [B, H_Q, d]; dense k / v [B, L_cap >= L_K, H_KV, d], paged
+    [num_pages, page_size, H_KV, d]; cache_seqlens [B]; out [B, H_Q, d]; lse [B, H_Q]."""
+    B, HQ, HKV, D = plan.batch, plan.h_q, plan.h_kv, plan.head_dim
+    if tuple(q.shape) != (B, HQ, D):
+        raise ValueError(f"q shape {tuple(q.shape)} != plan (batch, h_q, head_dim) {(B, HQ, D)}")
+    for name, t in (("k_cache", k), ("v_cache", v)):
+        if t.dim() != 4 or t.shape[2] != HKV or t.shape[3] != D or (not paged and (t.shape[0] != B or t.shape[1] < plan.l_k)):
+            raise ValueError(f"{name} shape {tuple(t.shape)} does not match the plan (batch {B}, l_k {plan.l_k}, "
+                             f"h_kv {HKV}, head_dim {D})")
+    if cache_seqlens is not None and tuple(cache_seqlens.shape) != (B,):
+        raise ValueError(f"cache_seqlens shape {tuple(cache_seqlens.shape)} != ({B},)")
+    if out is not None and tuple(out.shape) != (B, HQ, D):
+        raise ValueError(f"out shape {tuple(out.shape)} != {(B, HQ, D)}")
+    if lse is not None and tuple(lse.shape) != (B, HQ):
+        raise ValueError(f"lse shape {tuple(lse.shape)} != {(B, HQ)}")
+
+
 def workspace_for(plan: L.da_plan, device) -> torch.Tensor | None:
     if plan.combine_mode != L.DA_COMBINE_KERNEL:
         return None
@@ -81,6 +100,7 @@ def forward(plan: L.da_plan, q, k_cache, v_cache, cache_seqlens=None, *, out=Non
         raise ValueError("q, k_cache, v_cache must be bfloat16")
     if cache_seqlens is not None and cache_seqlens.dtype != torch.int32:
         raise ValueError("cache_seqlens must be int32")
+    _check_shapes(plan, q, k_cache, v_cache, cache_seqlens, out, lse)
     B, HQ, D = q.shape
     if out is None:
         out = torch.empty((B, HQ, D), dtype=out_dtype, device=q.device)
@@ -106,6 +126,7 @@ def forward_peer(plan: L.da_plan, q, k_cache, v_cache, cache_seqlens, world, ran
         raise ValueError("q, k_cache, v_cache must be bfloat16")
     if cache_seqlens is not None and cache_seqlens.dtype != torch.int32:
         raise ValueError("cache_seqlens must be int32")
+    _check_shapes(plan, q, k_cache, v_cache, cache_seqlens)
     if workspace is None:
         workspace = workspace_for(plan, q.device)
     ws_bytes = 0 if workspace is None else workspace.numel() * workspace.element_size()
@@ -121,6 +142,9 @@ def forward_paged(plan: L.da_plan, q, k_pages, v_pages, block_table, cache_seqle
     _check_cuda(q, k_pages, v_pages, block_table, cache_seqlens)
     if block_table.dtype != torch.int32 or block_table.dim() != 2 or block_table.stride(1) != 1:
         raise ValueError("block_table must be a row-major int32 [B, max_pages] tensor")
+    _check_shapes(plan, q, k_pages, v_pages, cache_seqlens, out, lse, paged=True)
+    if block_table.shape[0] != plan.batch:
+        raise ValueError(f"block_table rows {block_table.shape[0]} != batch {plan.batch}")
     B, HQ, D = q.shape
     if out is None:
         out = torch.empty((B, HQ, D), dtype=out_dtype, device=q.device)
@@ -164,6 +188,7 @@ def forward_host(plan: L.da_plan, q, k_cache, v_cache, cache_seqlens=None, *, ou
         raise ValueError("q, k_cache, v_cache must be bfloat16")
     if cache_seqlens is not None and cache_seqlens.dtype != torch.int32:
         raise ValueError("cache_seqlens must be int32")
+    _check_shapes(plan, q, k_cache, v_cache, cache_seqlens, out, lse)
     B, HQ, D = q.shape
     if out is None:
         out = torch.empty((B, HQ, D), dtype=out_dtype).pin_memory()

@@ -417,3 +417,23 @@ def test_peer_layout():
         assert slot >= lo + 4 * B * H and slot % 16 == 0
         assert fo >= 2 * slot and fo % 16 == 0
         assert tot >= fo + 4 * W and tot % 16 == 0
+
+
+def test_python_shape_checks_before_any_launch(L):
+    # the binding refuses tensors that do not match the plan (the C ABI takes bare pointers)
+    import torch
+    from paper_2604_00028_b200 import api
+    plan = L.da_plan_make(2, 16, 2, 300, 128, 1, 0, 148, "seq_aware", 0)
+    bf = torch.bfloat16
+    q, k, v = torch.zeros(2, 16, 128, dtype=bf), torch.zeros(2, 300, 2, 128, dtype=bf), torch.zeros(2, 300, 2, 128, dtype=bf)
+    api._check_shapes(plan, q, k, v, torch.zeros(2, dtype=torch.int32))              # consistent: passes
+    api._check_shapes(plan, q, torch.zeros(2, 512, 2, 128, dtype=bf), v)              # L_cap > L_K: fine
+    bad = [dict(q=torch.zeros(2, 8, 128, dtype=bf)), dict(k_cache=torch.zeros(2, 299, 2, 128, dtype=bf)),
+           dict(v_cache=torch.zeros(2, 300, 1, 128, dtype=bf)), dict(k_cache=torch.zeros(1, 300, 2, 128, dtype=bf)),
+           dict(cache_seqlens=torch.zeros(3, dtype=torch.int32)), dict(out=torch.zeros(2, 16, 64, dtype=bf)),
+           dict(lse=torch.zeros(16, dtype=torch.float32))]
+    for kw in bad:
+        a = dict(q=q, k_cache=k, v_cache=v, cache_seqlens=None, out=None, lse=None)
+        a.update(kw)
+        with pytest.raises(ValueError):
+            api.forward_host(plan, a["q"], a["k_cache"], a["v_cache"], a["cache_seqlens"], out=a["out"], lse=a["lse"])
