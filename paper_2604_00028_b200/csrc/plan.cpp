@@ -138,7 +138,7 @@ bool is_dynamic(const da_plan& p) { return p.policy == DA_POLICY_DYNAMIC && p.nu
 
 // Rows per CTA on the tensor-core path: mma_rows, except that 8-row CTAs for G > 8 need the
 // whole grid (B x H_KV x ceil(G / 8) x s CTAs) in one wave; past it 16-row CTAs stand.
-int64_t launch_rows(const da_plan& p) {
+static int64_t launch_rows(const da_plan& p) {
   const int64_t G = p.h_q / p.h_kv;
   int64_t rows = mma_rows(G, p.l_k);
   if (rows == 8 && G > 8 &&
