@@ -520,6 +520,7 @@ def main():
 
     cfg = WORKLOADS[args.workload]
     long_sharded = args.workload == "long_context" and (world > 1 or args.seq_shard)
+    batch_sharded = args.workload == "high_load" and world > 1
     if long_sharded:
         from paper_2604_00028_b200.dist import PeerSeqShardedDecode, SeqShardedDecode
         p2p = args.exchange.startswith("p2p")
@@ -557,9 +558,15 @@ def main():
                        "p2p-split": f"seq-sharded sp{world} + peer-memory exchange (signal + pull-combine)",
                        "nccl": f"seq-sharded sp{world} + NCCL all-gather + LSE combine"}[args.exchange]
     else:
+        # high-load at N > 1: the B = 128 batch is sharded across ranks (the north star's
+        # "sharded by batch x KV-head", total work fixed); other workloads run one replica per rank
         local_cfg = cfg
-        w = Workload(cfg, dev, 1000 + rank, l2)
-        plan = dec.make_plan(cfg["batch"], cfg["h_q"], cfg["h_kv"], cfg["l_k"], policy=args.policy)
+        if batch_sharded:
+            from paper_2604_00028_b200.dist import shard_range
+            b0, b1 = shard_range(cfg["batch"], rank, world)
+            local_cfg = dict(cfg, batch=b1 - b0)
+        w = Workload(local_cfg, dev, 1000 + rank, l2)
+        plan = dec.make_plan(local_cfg["batch"], cfg["h_q"], cfg["h_kv"], cfg["l_k"], policy=args.policy)
         with torch.cuda.stream(stream):
             ws = dec.workspace_for(plan, dev)
             for i in range(args.warmup):
@@ -567,11 +574,13 @@ def main():
                 dec.forward(plan, w.q, w.k[j], w.v[j], w.seqlens, out=w.out, lse=w.lse, workspace=ws)
         torch.cuda.synchronize()
         g = make_graph(dec, plan, w, args.steps, stream)
-        step_bytes_total = w.bytes * world
+        step_bytes_total = alg_bytes(**cfg) if batch_sharded else w.bytes * world
         kernels_per_step = 2 if plan.combine_mode == L.DA_COMBINE_KERNEL else 1
-        scaling = "weak"
+        scaling = "strong" if batch_sharded else "weak"
         l2_note = w.l2_note(l2)
-        parallelism = f"batch-sharded dp{world} (independent sequences, no collective)" if world > 1 else "single GPU"
+        parallelism = (f"batch-sharded dp{world} (B={cfg['batch']} split across ranks, no collective)" if batch_sharded
+                       else f"batch-sharded dp{world} (independent sequences, no collective)" if world > 1
+                       else "single GPU")
 
     # ---- the timed region: exactly K steps (one graph replay), barrier + sync both sides ----
     with ClockSampler(dev.index) as clk:
@@ -652,7 +661,7 @@ def main():
         "data": "synthetic (seeded N(0,1) bf16 q/K/V, uniform cache_seqlens = L_K)",
         "config": {"workload": args.workload, **cfg, "head_dim": HEAD_DIM, "policy": args.policy,
                    "num_splits": plan.num_splits, "combine_mode": plan.combine_mode,
-                   "global_batch": cfg["batch"] * (world if not long_sharded else 1),
+                   "global_batch": cfg["batch"] * (world if not (long_sharded or batch_sharded) else 1),
                    "parallelism": parallelism, "l2": l2_note, "graph": "K steps in one CUDA graph"},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "traffic": trec.get("dram_bytes_per_launch") if trec else None,

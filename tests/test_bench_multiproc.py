@@ -41,3 +41,19 @@ def test_bench_sequence_sharded_step_one_rank(exchange, launches):
     d = json.loads(lines[0])
     assert d["scaling"] == "strong" and d["config"]["workload"] == "long_context"
     assert d["value"] > 1000 and d["gpu_launches"] == 5 * launches
+
+
+@pytest.mark.gpu
+def test_bench_two_ranks_high_load_batch_split():
+    # high-load at N > 1 splits the B = 128 batch across ranks (strong scaling, no collective)
+    env = dict(os.environ, DECATTN_BENCH_BACKEND="gloo", DECATTN_BENCH_ONE_GPU="1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr", "127.0.0.1", "--master-port", "29519", os.path.join(ROOT, "bench.py"),
+           "--gpus", "2", "--workload", "high_load", "--steps", "3", "--warmup", "3"]
+    r = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["scaling"] == "strong" and d["config"]["global_batch"] == 128
+    assert d["value"] > 0 and d["gpu_launches"] == 3
