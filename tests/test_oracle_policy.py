@@ -296,12 +296,12 @@ def test_seq_aware_sm_structure():
         assert P.num_splits(1, 8 * hkv, hkv, 512, B200_SMS, 0, "seq_aware_sm")[0] >= 3
 
 
-def _measured_grid():
+def _measured_grid(tag="r01h"):
     import csv
     import os
     root = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles")
     grid = {}
-    for name in ("r01h_ugrid.csv", "r01h_ugrid2.csv", "r01h_ugrid3.csv"):
+    for name in (f"{tag}_ugrid.csv", f"{tag}_ugrid2.csv", f"{tag}_ugrid3.csv"):
         with open(os.path.join(root, name)) as fh:
             for r in csv.DictReader(fh):
                 key = (int(r.get("batch", 1)), int(r["h_kv"]), int(r["l_k"]))
@@ -332,12 +332,14 @@ def test_seq_aware_sm_calibration_lowhead():
             assert t[g] / t[s] >= 1.2, (b, hkv, lk, s)
 
 
-def test_seq_aware_sm_calibration():
+@pytest.mark.parametrize("tag", ["r01h", "r01j"])
+def test_seq_aware_sm_calibration(tag):
     """C-ext-1's constants against the B200 measurements they were calibrated on
-    (profiles/r01h_ugrid*.csv, forced-s latencies of the current kernel, G = 8): the pick is
-    within 6 % of the best measured split (an unmeasured pick lies between two measured
-    neighbours) and never slower than the guarded pick beyond the 2 % A/B noise of these grids."""
-    grid = _measured_grid()
+    (profiles/r01h_ugrid*.csv, forced-s latencies, G = 8) and against the same grids re-measured
+    on the final round-1 kernel (r01j): the pick is within 6 % of the best measured split (an
+    unmeasured pick lies between two measured neighbours) and never slower than the guarded pick
+    beyond the 2 % A/B noise of these grids."""
+    grid = _measured_grid(tag)
     assert len(grid) >= 60
     for (b, hkv, lk), t in grid.items():
         s, _ = P.num_splits(b, 8 * hkv, hkv, lk, B200_SMS, 0, "seq_aware_sm")
