@@ -30,3 +30,7 @@ def test_parity_subset_under_debug_asserts():
                         "-m", "gpu", "-x", "-q", "-k", sel], cwd=ROOT, env=env, capture_output=True,
                        text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+    # the fused peer publish instantiations (da_forward_peer) and the peer exchange kernels
+    r = subprocess.run([sys.executable, "-m", "pytest", os.path.join(ROOT, "tests", "test_gpu_peer_exchange.py"),
+                        "-m", "gpu", "-x", "-q"], cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
