@@ -182,10 +182,10 @@ __global__ void __launch_bounds__(256)
   for (int i = threadIdx.x; i < rows; i += blockDim.x) dl[i] = lse_local != nullptr ? lse_local[i] : kNegInf;
   __syncthreads();
   if (threadIdx.x != 0) return;
-  fence_acq_rel_sys();
+  fence_acq_rel_sys();                // + the strong stores below: one release pattern per flag
   for (int q = 0; q < world; ++q) {
     uint32_t* flags = reinterpret_cast<uint32_t*>(peer_bases[q] + static_cast<uint64_t>(flag_offset));
-    st_release_sys_u32(flags + rank, e);
+    st_relaxed_sys_u32(flags + rank, e);
   }
   *epoch = static_cast<int32_t>(e);
 }

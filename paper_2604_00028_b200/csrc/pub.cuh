@@ -31,9 +31,9 @@ static __device__ __noinline__ void pub_arrive(const uint64_t* bases, int32_t* e
   ptx::fence_acq_rel_sys();                         // every writer's rows before the flags
   const uint32_t e = static_cast<uint32_t>(*reinterpret_cast<volatile int32_t*>(epoch)) + 1u;
   *reinterpret_cast<volatile uint32_t*>(count) = 0u;
-  for (int q = 0; q < world; ++q) {
+  for (int q = 0; q < world; ++q) {   // fence above + strong stores = one release pattern per flag
     uint32_t* flags = reinterpret_cast<uint32_t*>(bases[q] + static_cast<uint64_t>(flag_offset));
-    ptx::st_release_sys_u32(flags + rank, e);
+    ptx::st_relaxed_sys_u32(flags + rank, e);
   }
   *reinterpret_cast<volatile int32_t*>(epoch) = static_cast<int32_t>(e);
 }
