@@ -190,7 +190,7 @@ __global__ void __launch_bounds__(256)
   *epoch = static_cast<int32_t>(e);
 }
 
-// One CTA (4 warps) per (b, h) row: thread 0 acquires every rank's flag at this step's epoch, then
+// One CTA (4 warps) per (b, h) row: warp 0 acquires every rank's flag at this step's epoch, then
 // the row's P partials are read from the peers' buffers (NVLink loads, coherent: no __ldg) and
 // merged exactly like lse_combine_kernel (per-warp online max, warp-level rescale merge).
 __global__ void __launch_bounds__(kCombineThreads)
@@ -209,9 +209,9 @@ __global__ void __launch_bounds__(kCombineThreads)
   pdl_launch_dependents();
   pdl_wait();
   const uint32_t e = static_cast<uint32_t>(*epoch);
-  if (threadIdx.x == 0) {
+  if (warp == 0) {   // lane q polls rank q's flag (q, q + 32): the P acquires overlap
     const uint32_t* flags = reinterpret_cast<const uint32_t*>(own + static_cast<uint64_t>(flag_offset));
-    for (int q = 0; q < world; ++q)
+    for (int q = lane; q < world; q += 32)
       while (ld_acquire_sys_u32(flags + q) < e) {
       }
   }
