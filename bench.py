@@ -551,10 +551,14 @@ def main():
         step_bytes_total = alg_bytes(cfg["batch"], cfg["h_q"], cfg["h_kv"], cfg["l_k"])
         # forward (+ workspace combine) + the exchange: fused publish -> pull-combine (1 launch),
         # signal + pull-combine (2), NCCL all-gather (library) + da_combine (1)
-        kernels_per_step = (2 if plan.combine_mode == L.DA_COMBINE_KERNEL else 1) + (2 if args.exchange == "p2p-split" else 1)
+        one_kernel = p2p and getattr(sd, "one_kernel", False)
+        kernels_per_step = ((2 if plan.combine_mode == L.DA_COMBINE_KERNEL else 1)
+                            + (0 if one_kernel else 2 if args.exchange == "p2p-split" else 1))
         scaling = "strong"
         l2_note = f"{nkv} rotating copies of the sequence shard (> 2x L2) + 256 MiB L2 scrub before the timed replay"
-        parallelism = {"p2p": f"seq-sharded sp{world} + peer-memory exchange (fused publish + pull-combine)",
+        parallelism = {"p2p": (f"seq-sharded sp{world}, one kernel per step: forward + peer-memory publish + cross-rank "
+                               f"LSE combine" if one_kernel else
+                               f"seq-sharded sp{world} + peer-memory exchange (fused publish + pull-combine)"),
                        "p2p-split": f"seq-sharded sp{world} + peer-memory exchange (signal + pull-combine)",
                        "nccl": f"seq-sharded sp{world} + NCCL all-gather + LSE combine"}[args.exchange]
     else:

@@ -45,7 +45,7 @@
 extern "C" {
 #endif
 
-#define DA_ABI_VERSION 4
+#define DA_ABI_VERSION 5
 
 #if defined(__GNUC__)
 #define DA_API __attribute__((visibility("default")))
@@ -383,6 +383,25 @@ DA_API da_status da_forward_peer(const da_plan* plan, const void* q, const void*
                                  const uint64_t* peer_bases, int64_t slot_bytes, int64_t lse_offset,
                                  int64_t flag_offset, int32_t* epoch, uint32_t* counter, void* workspace,
                                  int64_t workspace_bytes, void* cuda_stream);
+
+/*
+ * da_forward_peer_combine - the whole sequence-sharded step in ONE kernel: da_forward_peer, then
+ * every CTA waits (acquire, system scope) until all `world` flags of this rank's buffer reach the
+ * step's epoch and LSE-merges, across the world partials read from the ranks' buffers (NVLink
+ * loads), the rows it wrote, into out (out_dtype [B, H_Q, d]) and lse (fp32 [B, H_Q], or NULL):
+ * the exchange and the combine of da_combine_peers fused into the forward.
+ * Plans with combine_mode NONE or CLUSTER whose grid is one wave (grid_x * grid_y * grid_z <=
+ * usable_sms; the CTAs spin, so the whole grid must be resident: an otherwise idle GPU);
+ * DA_ERR_UNSUPPORTED otherwise (use da_forward_peer + da_combine_peers).  No workspace.
+ * Arguments and errors otherwise as da_forward_peer and da_combine_peers.
+ */
+DA_API da_status da_forward_peer_combine(const da_plan* plan, const void* q, const void* k_cache,
+                                         const void* v_cache, int32_t l_cap, const int32_t* cache_seqlens,
+                                         const int64_t* strides, float softmax_scale, int32_t world,
+                                         int32_t rank, const uint64_t* peer_bases, int64_t slot_bytes,
+                                         int64_t lse_offset, int64_t flag_offset, int32_t* epoch,
+                                         uint32_t* counter, int32_t out_dtype, void* out, float* lse,
+                                         void* cuda_stream);
 
 /* Static, NUL-terminated description of a status code (never NULL). */
 DA_API const char* da_status_string(int32_t status);

@@ -28,7 +28,7 @@ DA_OK, DA_ERR_INVALID_ARG, DA_ERR_UNSUPPORTED, DA_ERR_ALIGNMENT, DA_ERR_WORKSPAC
 DA_BF16, DA_F32 = 0, 1
 DA_COMBINE_NONE, DA_COMBINE_CLUSTER, DA_COMBINE_KERNEL = range(3)
 DA_PATH_SCALAR, DA_PATH_MMA = 0, 1
-DA_ABI_VERSION = 4
+DA_ABI_VERSION = 5
 
 POLICIES = {"guarded": DA_POLICY_GUARDED, "seq_aware": DA_POLICY_SEQ_AWARE, "fixed": DA_POLICY_FIXED,
             "evolved": DA_POLICY_EVOLVED, "seq_aware_sm": DA_POLICY_SEQ_AWARE_SM, "dynamic": DA_POLICY_DYNAMIC}
@@ -90,6 +90,9 @@ def _load() -> ctypes.CDLL:
     lib.da_forward_peer.argtypes = [ctypes.POINTER(da_plan), vp, vp, vp, i32, vp, vp, f32, i32, i32, vp, i64, i64,
                                     i64, vp, vp, vp, i64, vp]
     lib.da_forward_peer.restype = i32
+    lib.da_forward_peer_combine.argtypes = [ctypes.POINTER(da_plan), vp, vp, vp, i32, vp, vp, f32, i32, i32, vp,
+                                            i64, i64, i64, vp, vp, i32, vp, vp, vp]
+    lib.da_forward_peer_combine.restype = i32
     lib.da_combine.argtypes = [i32, i32, i32, i32, vp, i64, vp, i64, i32, vp, vp, vp]
     lib.da_combine.restype = i32
     lib.da_status_string.argtypes = [i32]
@@ -105,7 +108,7 @@ LIB = _load()
 
 EXPORTED = ("da_plan_make", "da_plan_make_varlen", "da_plan_set_combine", "da_forward", "da_forward_paged",
             "da_forward_host_bytes", "da_forward_host", "da_combine", "da_peer_signal", "da_combine_peers",
-            "da_forward_peer", "da_status_string", "da_abi_version")
+            "da_forward_peer", "da_forward_peer_combine", "da_status_string", "da_abi_version")
 
 
 def da_status_string(status: int) -> str:
@@ -244,6 +247,20 @@ def da_forward_peer(plan: da_plan, q, k_cache, v_cache, l_cap, cache_seqlens, st
                              _ptr(workspace), int(workspace_bytes), _stream_handle(stream))
     if st != DA_OK:
         raise DecAttnError(st, "da_forward_peer")
+
+
+def da_forward_peer_combine(plan: da_plan, q, k_cache, v_cache, l_cap, cache_seqlens, strides, softmax_scale, world,
+                            rank, peer_bases, slot_bytes, lse_offset, flag_offset, epoch, counter, out_dtype, out, lse,
+                            stream=None) -> None:
+    sarr = None
+    if strides is not None:
+        sarr = (ctypes.c_int64 * 8)(*[int(x) for x in strides])
+    st = LIB.da_forward_peer_combine(ctypes.byref(plan), _ptr(q), _ptr(k_cache), _ptr(v_cache), int(l_cap),
+                                     _ptr(cache_seqlens), sarr, float(softmax_scale), int(world), int(rank),
+                                     _ptr(peer_bases), int(slot_bytes), int(lse_offset), int(flag_offset), _ptr(epoch),
+                                     _ptr(counter), int(out_dtype), _ptr(out), _ptr(lse), _stream_handle(stream))
+    if st != DA_OK:
+        raise DecAttnError(st, "da_forward_peer_combine")
 
 
 def da_combine(num_splits, batch, h_q, head_dim, o_partial, o_split_stride, lse_partial,

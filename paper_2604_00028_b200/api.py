@@ -135,6 +135,35 @@ def forward_peer(plan: L.da_plan, q, k_cache, v_cache, cache_seqlens, world, ran
                       workspace, ws_bytes, stream)
 
 
+def one_kernel_exchange_ok(plan: L.da_plan) -> bool:
+    """da_forward_peer_combine's condition: a NONE / CLUSTER plan whose grid is one wave."""
+    return (plan.combine_mode != L.DA_COMBINE_KERNEL
+            and plan.grid_x * plan.grid_y * plan.grid_z <= plan.usable_sms)
+
+
+def forward_peer_combine(plan: L.da_plan, q, k_cache, v_cache, cache_seqlens, world, rank, peer_bases, slot_bytes,
+                         lse_offset, flag_offset, epoch, counter, *, out=None, lse=None, softmax_scale=0.0,
+                         out_dtype=torch.bfloat16, stream=None):
+    """The sequence-sharded step in one kernel via da_forward_peer_combine: the forward publishes
+    this rank's partial, waits for every rank's, and LSE-merges them into (out, lse)."""
+    _check_cuda(q, k_cache, v_cache, cache_seqlens, peer_bases, epoch, counter, out, lse)
+    if q.dtype != torch.bfloat16 or k_cache.dtype != torch.bfloat16 or v_cache.dtype != torch.bfloat16:
+        raise ValueError("q, k_cache, v_cache must be bfloat16")
+    if cache_seqlens is not None and cache_seqlens.dtype != torch.int32:
+        raise ValueError("cache_seqlens must be int32")
+    _check_shapes(plan, q, k_cache, v_cache, cache_seqlens, out, lse)
+    B, HQ, D = q.shape
+    if out is None:
+        out = torch.empty((B, HQ, D), dtype=out_dtype, device=q.device)
+    if lse is None:
+        lse = torch.empty((B, HQ), dtype=torch.float32, device=q.device)
+    dt = L.DA_F32 if out.dtype == torch.float32 else L.DA_BF16
+    L.da_forward_peer_combine(plan, q, k_cache, v_cache, k_cache.shape[1], cache_seqlens,
+                              _kv_strides(q, k_cache, v_cache), softmax_scale, world, rank, peer_bases, slot_bytes,
+                              lse_offset, flag_offset, epoch, counter, dt, out, lse, stream)
+    return out, lse
+
+
 def forward_paged(plan: L.da_plan, q, k_pages, v_pages, block_table, cache_seqlens=None, *, out=None,
                   lse=None, workspace=None, softmax_scale=0.0, out_dtype=torch.bfloat16, stream=None):
     """Decode attention over a paged cache via da_forward_paged.  k/v_pages [num_pages, page_size,

@@ -414,6 +414,42 @@ extern "C" da_status da_forward_peer(const da_plan* plan, const void* q, const v
                       nullptr, workspace, workspace_bytes, cuda_stream, PagedArgs{}, &pub);
 }
 
+extern "C" da_status da_forward_peer_combine(const da_plan* plan, const void* q, const void* k_cache,
+                                             const void* v_cache, int32_t l_cap, const int32_t* cache_seqlens,
+                                             const int64_t* strides, float softmax_scale, int32_t world,
+                                             int32_t rank, const uint64_t* peer_bases, int64_t slot_bytes,
+                                             int64_t lse_offset, int64_t flag_offset, int32_t* epoch,
+                                             uint32_t* counter, int32_t out_dtype, void* out, float* lse,
+                                             void* cuda_stream) {
+  if (plan == nullptr) return DA_ERR_INVALID_ARG;
+  int64_t rows = 0;
+  da_status st = check_peer_layout(world, rank, peer_bases, epoch, plan->batch, plan->h_q, plan->head_dim,
+                                   slot_bytes, lse_offset, flag_offset, &rows);
+  if (st != DA_OK) return st;
+  if (counter == nullptr || out == nullptr || (out_dtype != DA_BF16 && out_dtype != DA_F32)) return DA_ERR_INVALID_ARG;
+  if ((reinterpret_cast<uintptr_t>(counter) & 3u) != 0 || !aligned16(out) ||
+      (lse != nullptr && (reinterpret_cast<uintptr_t>(lse) & 3u) != 0))
+    return DA_ERR_ALIGNMENT;
+  // the CTAs spin on the ranks' flags after writing their rows: the whole grid must be resident
+  // (one CTA per SM: the forward's shared memory), and no workspace combine kernel may follow
+  const int64_t ctas = int64_t(plan->grid_x) * plan->grid_y * plan->grid_z;
+  if (plan->combine_mode == DA_COMBINE_KERNEL || ctas > plan->usable_sms) return DA_ERR_UNSUPPORTED;
+  PubParams pub{};
+  pub.bases = peer_bases;
+  pub.epoch = epoch;
+  pub.count = counter;
+  pub.slot_bytes = slot_bytes;
+  pub.lse_offset = lse_offset;
+  pub.flag_offset = flag_offset;
+  pub.world = world;
+  pub.rank = rank;
+  pub.out = out;
+  pub.lse = lse;
+  pub.out_f32 = out_dtype == DA_F32;
+  return forward_impl(plan, q, k_cache, v_cache, l_cap, cache_seqlens, strides, softmax_scale, DA_F32, nullptr,
+                      nullptr, nullptr, 0, cuda_stream, PagedArgs{}, &pub);
+}
+
 extern "C" da_status da_combine_peers(int32_t world, int32_t rank, const uint64_t* peer_bases, int64_t slot_bytes,
                                       int64_t lse_offset, int64_t flag_offset, const int32_t* epoch, int32_t batch,
                                       int32_t h_q, int32_t head_dim, int32_t out_dtype, void* out, float* lse,

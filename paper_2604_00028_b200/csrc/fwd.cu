@@ -380,7 +380,7 @@ __device__ __noinline__ int4 dyn_schedule(const FwdParams& p, uint32_t slot, boo
 // rows (MMA path); kCombine: da_combine_mode; NS: ring stages; NW: consumer warps
 // (NS a multiple of NW: warp w owns stages w, w + NW, ... and consumes them in order).
 // ---------------------------------------------------------------------------
-template <int kPath, int kNB, int kCombine, int NS, int NW, bool kDyn, bool kPub>
+template <int kPath, int kNB, int kCombine, int NS, int NW, bool kDyn, int kPub>
 __global__ void __launch_bounds__(threads_for(NW, helpers_for(kCombine)), 1)
     split_kv_fwd_kernel(const __grid_constant__ CUtensorMap tmap_k,
                         const __grid_constant__ CUtensorMap tmap_v, const FwdParams p) {
@@ -756,7 +756,9 @@ __global__ void __launch_bounds__(threads_for(NW, helpers_for(kCombine)), 1)
   // final rows: out / lse, or (kPub, da_forward_peer) this step's slot of the exchange buffer
   void* o_dst = p.out;
   float* l_dst = p.lse;
-  if constexpr (kPub) {
+  uint32_t e_pub = 0;
+  if constexpr (kPub != 0) {
+    e_pub = pub_epoch(p.pub);
     const uint64_t sb = pub_slot(p.pub);
     o_dst = reinterpret_cast<void*>(sb);
     l_dst = reinterpret_cast<float*>(sb + static_cast<uint64_t>(p.pub.lse_offset));
@@ -848,9 +850,22 @@ __global__ void __launch_bounds__(threads_for(NW, helpers_for(kCombine)), 1)
     }
   }
   if (threadIdx.x == 0) TRACE(47);
-  if constexpr (kPub && kCombine != DA_COMBINE_KERNEL) {   // this kernel wrote the final rows
+  if constexpr (kPub != 0 && kCombine != DA_COMBINE_KERNEL) {   // this kernel wrote the final rows
     __syncthreads();
     if (threadIdx.x == 0) pub_arrive(p.pub);
+    if constexpr (kPub == 2) {
+      // da_forward_peer_combine: every rank's partial of the rows this CTA wrote, LSE-merged here
+      // (the cross-GPU combine fused into the forward; the grid is one wave, so spinning is safe)
+      if (warp == 0) pub_wait_all(p.pub, e_pub, lane);
+      __syncthreads();
+      const int s = kCluster ? s_cl : 1;
+      for (int t = threadIdx.x; t < rows_per_owner * 32; t += kT) {
+        const int rl = t >> 5, d4 = t & 31;
+        const int g = static_cast<int>(rank) + rl * s;
+        if (g >= rows_valid) break;
+        pub_merge_row(p.pub, e_pub, static_cast<size_t>(b) * p.h_q + hq0 + g, d4);
+      }
+    }
   }
 #ifdef DECATTN_TRACE
   __syncthreads();
@@ -862,7 +877,7 @@ __global__ void __launch_bounds__(threads_for(NW, helpers_for(kCombine)), 1)
 #endif
 }
 
-template <int kPath, int kNB, int kCombine, bool kDyn = false, bool kPub = false>
+template <int kPath, int kNB, int kCombine, bool kDyn = false, int kPub = 0>
 cudaError_t launch_impl(const da_plan& plan, const CUtensorMap& tk, const CUtensorMap& tv,
                         const FwdParams& p, cudaStream_t stream) {
   constexpr bool kCluster = kCombine == DA_COMBINE_CLUSTER;
@@ -914,17 +929,20 @@ cudaError_t dispatch_combine(const da_plan& plan, const CUtensorMap& tk, const C
                              const FwdParams& p, cudaStream_t stream) {
   // kPub (da_forward_peer) instantiations only where the forward writes final rows; with the
   // workspace combine the combine kernel publishes and the forward is the plain one
-  const bool pub = p.pub.bases != nullptr;
+  // (kPub = 2: publish + the in-kernel cross-rank combine, one-wave NONE / CLUSTER plans)
+  const int pub = p.pub.bases == nullptr ? 0 : (p.pub.out != nullptr ? 2 : 1);
   switch (plan.combine_mode) {
     case DA_COMBINE_NONE:
-      if (pub) return launch_impl<kPath, kNB, DA_COMBINE_NONE, false, true>(plan, tk, tv, p, stream);
+      if (pub == 2) return launch_impl<kPath, kNB, DA_COMBINE_NONE, false, 2>(plan, tk, tv, p, stream);
+      if (pub == 1) return launch_impl<kPath, kNB, DA_COMBINE_NONE, false, 1>(plan, tk, tv, p, stream);
       return launch_impl<kPath, kNB, DA_COMBINE_NONE>(plan, tk, tv, p, stream);
     case DA_COMBINE_CLUSTER:
-      if (pub) return launch_impl<kPath, kNB, DA_COMBINE_CLUSTER, false, true>(plan, tk, tv, p, stream);
+      if (pub == 2) return launch_impl<kPath, kNB, DA_COMBINE_CLUSTER, false, 2>(plan, tk, tv, p, stream);
+      if (pub == 1) return launch_impl<kPath, kNB, DA_COMBINE_CLUSTER, false, 1>(plan, tk, tv, p, stream);
       return launch_impl<kPath, kNB, DA_COMBINE_CLUSTER>(plan, tk, tv, p, stream);
     default:
       if (is_dynamic(plan)) {   // s_b = 1 rows are final rows written by the forward
-        if (pub) return launch_impl<kPath, kNB, DA_COMBINE_KERNEL, true, true>(plan, tk, tv, p, stream);
+        if (pub) return launch_impl<kPath, kNB, DA_COMBINE_KERNEL, true, 1>(plan, tk, tv, p, stream);
         return launch_impl<kPath, kNB, DA_COMBINE_KERNEL, true>(plan, tk, tv, p, stream);
       }
       return launch_impl<kPath, kNB, DA_COMBINE_KERNEL>(plan, tk, tv, p, stream);

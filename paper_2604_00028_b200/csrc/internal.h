@@ -22,6 +22,11 @@ struct PubParams {
   int64_t slot_bytes, lse_offset, flag_offset;
   int32_t world, rank;
   int32_t writers;          // CTAs of the writing launch
+  // da_forward_peer_combine (one-wave NONE / CLUSTER forwards): after publishing, every CTA waits
+  // for all ranks' flags and LSE-merges the rows it wrote across the ranks into out / lse
+  void* out;                // final [B, H_Q, d] bf16 or fp32
+  float* lse;               // final [B, H_Q] or nullptr
+  int32_t out_f32;
 };
 
 struct FwdParams {

@@ -163,16 +163,18 @@ def peer_layout(batch: int, h_q: int, head_dim: int, world: int):
 
 
 class PeerSeqShardedDecode:
-    """Long-context mode with the exchange over peer memory.  fused (default): da_forward_peer (the
-    kernel that produces the local partial writes it into slot epoch & 1 of this rank's symmetric
-    buffer and its last CTA releases the epoch into every peer's flag slot) -> da_combine_peers
-    (acquire every flag, read the partials from the peers' buffers, LSE-merge): two launches per
-    step.  fused=False: forward into a local fp32 partial -> da_peer_signal (copy + release) ->
+    """Long-context mode with the exchange over peer memory.  fused (default): when the plan's grid
+    is one wave (NONE / CLUSTER combine), da_forward_peer_combine runs the whole step in ONE kernel
+    (publish the partial into slot epoch & 1 of this rank's symmetric buffer, release the epoch to
+    every rank from the last CTA, wait for every rank's flag, LSE-merge the ranks' partials of the
+    rows each CTA wrote); otherwise da_forward_peer (publish) -> da_combine_peers (acquire every
+    flag, read the partials from the peers' buffers, LSE-merge).  one_kernel=False forces the
+    latter.  fused=False: forward into a local fp32 partial -> da_peer_signal (copy + release) ->
     da_combine_peers.  No NCCL call on the step; every call can be captured in a CUDA graph
     (monotonic epochs)."""
 
     def __init__(self, batch: int, h_q: int, h_kv: int, l_k_total: int, head_dim: int = 128, *,
-                 group=None, policy="seq_aware", device=None, fused: bool = True):
+                 group=None, policy="seq_aware", device=None, fused: bool = True, one_kernel: bool = True):
         import torch.distributed._symmetric_memory as symm
 
         from . import api
@@ -197,6 +199,7 @@ class PeerSeqShardedDecode:
         self.fused = fused
         self.counter = torch.zeros(1, dtype=torch.int32, device=self.device)   # da_forward_peer: writer CTAs
         self.plan = api.make_plan(batch, h_q, h_kv, self.l_local, head_dim, True, 0, None, policy)
+        self.one_kernel = fused and one_kernel and api.one_kernel_exchange_ok(self.plan)
         self._ws = api.workspace_for(self.plan, self.device)
         self.o_local = torch.empty((batch, h_q, head_dim), dtype=torch.float32, device=self.device)
         self.lse_local = torch.empty((batch, h_q), dtype=torch.float32, device=self.device)
@@ -205,6 +208,10 @@ class PeerSeqShardedDecode:
         """One decode step: local partial (published to the peers) -> pull-combine.  Returns (out, lse)."""
         from . import _lib as L
         from . import api
+        if self.one_kernel:
+            return api.forward_peer_combine(self.plan, q, k_local, v_local, seqlens_local, self.world, self.rank,
+                                            self.bases, self.slot_bytes, self.lse_offset, self.flag_offset,
+                                            self.epoch, self.counter, out=out, lse=lse)
         if self.fused:
             api.forward_peer(self.plan, q, k_local, v_local, seqlens_local, self.world, self.rank, self.bases,
                              self.slot_bytes, self.lse_offset, self.flag_offset, self.epoch, self.counter,

@@ -2,6 +2,7 @@
 per-rank shard of the long-context config at P = 2, 4, 8 (B = 1, H_Q = 64, H_KV = 8,
 L_K = 131072 / P), CUDA-graph replay, KV rotated past L2:
   fwd    the forward alone (fp32 partial into a local buffer)
+  one    da_forward_peer_combine (1 launch: publish + wait + cross-rank combine in the forward)
   fused  da_forward_peer -> da_combine_peers (2 launches)
   split  forward -> da_peer_signal -> da_combine_peers (3 launches)"""
 import os
@@ -55,23 +56,23 @@ def main():
         out = torch.empty((1, 64, 128), dtype=torch.bfloat16, device="cuda")
         lse = torch.empty((1, 64), dtype=torch.float32, device="cuda")
         o32 = torch.empty((1, 64, 128), dtype=torch.float32, device="cuda")
-        res = {"fwd": [], "fused": [], "split": []}
+        res = {"fwd": [], "one": [], "fused": [], "split": []}
         plan = None
         for _ in range(2):
-            sd = {f: PeerSeqShardedDecode(1, 64, 8, lk, device="cuda", fused=f, policy="seq_aware_sm")
-                  for f in (True, False)}
-            plan = sd[True].plan
+            sd = {f: PeerSeqShardedDecode(1, 64, 8, lk, device="cuda", fused=f != "split", one_kernel=f == "one",
+                                          policy="seq_aware_sm")
+                  for f in ("one", "fused", "split")}
+            plan = sd["fused"].plan
             ws = dec.workspace_for(plan, torch.device("cuda"))
             res["fwd"].append(graph_us(lambda i: dec.forward(plan, inp["q"], ks[i], vs[i], None, out=o32, lse=lse,
                                                              workspace=ws, out_dtype=torch.float32), nbuf))
-            res["fused"].append(graph_us(lambda i: sd[True].step(inp["q"], ks[i], vs[i], None, out, lse), nbuf))
-            res["split"].append(graph_us(lambda i: sd[False].step(inp["q"], ks[i], vs[i], None, out, lse), nbuf))
+            for f in ("one", "fused", "split"):
+                res[f].append(graph_us(lambda i, f=f: sd[f].step(inp["q"], ks[i], vs[i], None, out, lse), nbuf))
             del sd
         r = {k: min(v) for k, v in res.items()}
-        gbs = 4 * lk * 8 * 128 / (r["fused"] * 1e3)
         print(f"P={P} shard L_K={lk} s={plan.num_splits} mode={plan.combine_mode}: fwd {r['fwd']:.2f} us, "
-              f"fused step {r['fused']:.2f} us ({gbs:.0f} GB/s), split step {r['split']:.2f} us "
-              f"(split / fused {r['split'] / r['fused']:.3f}x)", flush=True)
+              f"one-kernel step {r['one']:.2f} us, fused (2 launches) {r['fused']:.2f} us, split (3 launches) "
+              f"{r['split']:.2f} us", flush=True)
     dist.destroy_process_group()
 
 

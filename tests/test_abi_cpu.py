@@ -437,3 +437,32 @@ def test_python_shape_checks_before_any_launch(L):
         a.update(kw)
         with pytest.raises(ValueError):
             api.forward_host(plan, a["q"], a["k_cache"], a["v_cache"], a["cache_seqlens"], out=a["out"], lse=a["lse"])
+
+
+def test_forward_peer_combine_validation(L):
+    # da_forward_peer_combine: one-wave NONE / CLUSTER plans only, checked before any CUDA call
+    A2 = 1 << 22
+    slot, lo, fo = 4128, 4096, 2 * 4128
+
+    def fwd(plan, **kw):
+        a = dict(plan=plan, q=A2, k_cache=A2, v_cache=A2, l_cap=plan.l_k, cache_seqlens=None, strides=None,
+                 softmax_scale=0.0, world=2, rank=0, peer_bases=A2, slot_bytes=slot, lse_offset=lo, flag_offset=fo,
+                 epoch=A2, counter=A2, out_dtype=L.DA_BF16, out=A2, lse=A2, stream=0)
+        a.update(kw)
+        with pytest.raises(L.DecAttnError) as e:
+            L.da_forward_peer_combine(**a)
+        return e.value.status
+    cluster = L.da_plan_make(1, 8, 1, 1500, 128, 1, 0, 148, "seq_aware", 0)
+    assert cluster.combine_mode == L.DA_COMBINE_CLUSTER
+    assert fwd(cluster, out=None) == L.DA_ERR_INVALID_ARG
+    assert fwd(cluster, out_dtype=7) == L.DA_ERR_INVALID_ARG
+    assert fwd(cluster, counter=None) == L.DA_ERR_INVALID_ARG
+    assert fwd(cluster, out=A2 + 8) == L.DA_ERR_ALIGNMENT
+    assert fwd(cluster, lse=A2 + 2) == L.DA_ERR_ALIGNMENT
+    ws = L.da_plan_make(1, 8, 1, 4096, 128, 1, 0, 148, "guarded", 0)          # s = 28: workspace combine
+    assert ws.combine_mode == L.DA_COMBINE_KERNEL and fwd(ws) == L.DA_ERR_UNSUPPORTED
+    big = L.da_plan_make(64, 8, 1, 300, 128, 1, 0, 148, "guarded", 0)         # 64 CTAs... one wave: allowed
+    wide = L.da_plan_make(256, 8, 1, 300, 128, 1, 0, 148, "guarded", 0)       # 256 CTAs > 148 SMs
+    assert big.grid_x * big.grid_y * big.grid_z <= 148
+    assert fwd(wide, slot_bytes=256 * 8 * 516 + 16, lse_offset=256 * 8 * 512,
+               flag_offset=2 * (256 * 8 * 516 + 16)) == L.DA_ERR_UNSUPPORTED

@@ -28,7 +28,7 @@ def test_bench_two_ranks_batch_sharded():
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("exchange,launches", [("p2p", 2), ("p2p-split", 3), ("nccl", 2)])
+@pytest.mark.parametrize("exchange,launches", [("p2p", 1), ("p2p-split", 3), ("nccl", 2)])
 def test_bench_sequence_sharded_step_one_rank(exchange, launches):
     # the long-context sequence-sharded step (forward + exchange + combine) through bench.py on a
     # one-rank group: the same code path the N-GPU run takes, every exchange flavour

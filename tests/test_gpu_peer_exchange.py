@@ -64,20 +64,24 @@ def test_peer_exchange_matches_oracle(one_rank_group, batch, h_q, h_kv, l_k, fus
     assert int(sd.counter.item()) == 0                  # da_forward_peer leaves its counter at zero
 
 
+@pytest.mark.parametrize("one_kernel", [True, False])
 @pytest.mark.parametrize("batch,h_q,h_kv,l_k,policy,mode", [
     (1, 64, 8, 300, "seq_aware", 0),        # s = 1: the forward writes the slot rows, every CTA counts
     (2, 8, 1, 1500, "seq_aware", 1),        # cluster combine: the row owners write and count
+    (3, 24, 3, 300, "seq_aware", 0),        # G = 8, several sequences: one wave of s = 1 CTAs
     (1, 64, 8, 4096, "seq_aware", 2),       # workspace combine: the combine kernel writes and counts
     (4, 16, 2, 3000, "dynamic", 2),         # dynamic: s_b = 1 rows from the forward, the rest combined
 ])
-def test_forward_peer_every_combine_mode(one_rank_group, batch, h_q, h_kv, l_k, policy, mode):
+def test_forward_peer_every_combine_mode(one_rank_group, batch, h_q, h_kv, l_k, policy, mode, one_kernel):
     # da_forward_peer: the writer of the final rows publishes (slot e & 1, epoch flags), whichever
-    # kernel that is; checked against the oracle over several epochs (both slots)
+    # kernel that is; da_forward_peer_combine (one-wave NONE / CLUSTER plans) also merges the ranks'
+    # partials inside the forward.  Checked against the oracle over several epochs (both slots).
     from paper_2604_00028_b200.dist import PeerSeqShardedDecode
     inp = synth.make_inputs(batch, h_q, h_kv, l_k, seed=1610, device="cuda",
                             variant="ragged" if policy == "dynamic" else "normal")
-    sd = PeerSeqShardedDecode(batch, h_q, h_kv, l_k, device="cuda", policy=policy, fused=True)
+    sd = PeerSeqShardedDecode(batch, h_q, h_kv, l_k, device="cuda", policy=policy, fused=True, one_kernel=one_kernel)
     assert sd.plan.combine_mode == mode
+    assert sd.one_kernel == (one_kernel and mode != 2)
     ref_o, ref_l = OA.decode_attention(*(synth.to_f64(inp[n]) for n in ("q", "k", "v", "seqlens")))
     out = torch.empty((batch, h_q, 128), dtype=torch.float32, device="cuda")
     lse = torch.empty((batch, h_q), dtype=torch.float32, device="cuda")
