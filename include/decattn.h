@@ -385,23 +385,31 @@ DA_API da_status da_forward_peer(const da_plan* plan, const void* q, const void*
                                  int64_t workspace_bytes, void* cuda_stream);
 
 /*
- * da_forward_peer_combine - the whole sequence-sharded step in ONE kernel: da_forward_peer, then
- * every CTA waits (acquire, system scope) until all `world` flags of this rank's buffer reach the
- * step's epoch and LSE-merges, across the world partials read from the ranks' buffers (NVLink
- * loads), the rows it wrote, into out (out_dtype [B, H_Q, d]) and lse (fp32 [B, H_Q], or NULL):
- * the exchange and the combine of da_combine_peers fused into the forward.
+ * da_forward_peer_combine - the whole sequence-sharded step in ONE kernel.  e = *epoch + 1.  Every
+ * CTA of the forward writes its final fp32 rows (o, then lse) into LL slot e & 1 of this rank's
+ * exchange buffer as self-validating 8-byte words ((e << 32) | fp32 bits, one system-scope relaxed
+ * store each: no fence, no flag), then polls the same words of every rank's slot (NVLink loads for
+ * peers) until they carry e and LSE-merges (C-comb) the world partials of its rows into out
+ * (out_dtype [B, H_Q, d]) and lse (fp32 [B, H_Q], or NULL); the last CTA to have read the epoch
+ * (device counter) advances *epoch.  The exchange and the combine fused into the forward
+ * (DESIGN.md §6).
+ *   ll_offset, ll_slot_bytes: the two LL slots (uint64 [B * H_Q][129] each, ll_slot_bytes >=
+ *     8 * 129 * B * H_Q, both multiples of 16) inside every rank's exchange buffer (same layout on
+ *     every rank, zero before the first step); a rank reuses slot e & 1 at step e + 2 only (the
+ *     stream order then guarantees every peer has read it).
+ *   counter: device uint32 owned by this rank, zero before the first step (left zero after each).
  * Plans with combine_mode NONE or CLUSTER whose grid is one wave (grid_x * grid_y * grid_z <=
  * usable_sms; the CTAs spin, so the whole grid must be resident: an otherwise idle GPU);
  * DA_ERR_UNSUPPORTED otherwise (use da_forward_peer + da_combine_peers).  No workspace.
- * Arguments and errors otherwise as da_forward_peer and da_combine_peers.
+ * Errors: as da_forward; DA_ERR_INVALID_ARG for world / rank / NULL pointers / a short LL slot,
+ * DA_ERR_ALIGNMENT for misaligned offsets, counter, epoch, out or lse.
  */
 DA_API da_status da_forward_peer_combine(const da_plan* plan, const void* q, const void* k_cache,
                                          const void* v_cache, int32_t l_cap, const int32_t* cache_seqlens,
                                          const int64_t* strides, float softmax_scale, int32_t world,
-                                         int32_t rank, const uint64_t* peer_bases, int64_t slot_bytes,
-                                         int64_t lse_offset, int64_t flag_offset, int32_t* epoch,
-                                         uint32_t* counter, int32_t out_dtype, void* out, float* lse,
-                                         void* cuda_stream);
+                                         int32_t rank, const uint64_t* peer_bases, int64_t ll_offset,
+                                         int64_t ll_slot_bytes, int32_t* epoch, uint32_t* counter,
+                                         int32_t out_dtype, void* out, float* lse, void* cuda_stream);
 
 /* Static, NUL-terminated description of a status code (never NULL). */
 DA_API const char* da_status_string(int32_t status);

@@ -141,8 +141,8 @@ def one_kernel_exchange_ok(plan: L.da_plan) -> bool:
             and plan.grid_x * plan.grid_y * plan.grid_z <= plan.usable_sms)
 
 
-def forward_peer_combine(plan: L.da_plan, q, k_cache, v_cache, cache_seqlens, world, rank, peer_bases, slot_bytes,
-                         lse_offset, flag_offset, epoch, counter, *, out=None, lse=None, softmax_scale=0.0,
+def forward_peer_combine(plan: L.da_plan, q, k_cache, v_cache, cache_seqlens, world, rank, peer_bases, ll_offset,
+                         ll_slot_bytes, epoch, counter, *, out=None, lse=None, softmax_scale=0.0,
                          out_dtype=torch.bfloat16, stream=None):
     """The sequence-sharded step in one kernel via da_forward_peer_combine: the forward publishes
     this rank's partial, waits for every rank's, and LSE-merges them into (out, lse)."""
@@ -159,8 +159,8 @@ def forward_peer_combine(plan: L.da_plan, q, k_cache, v_cache, cache_seqlens, wo
         lse = torch.empty((B, HQ), dtype=torch.float32, device=q.device)
     dt = L.DA_F32 if out.dtype == torch.float32 else L.DA_BF16
     L.da_forward_peer_combine(plan, q, k_cache, v_cache, k_cache.shape[1], cache_seqlens,
-                              _kv_strides(q, k_cache, v_cache), softmax_scale, world, rank, peer_bases, slot_bytes,
-                              lse_offset, flag_offset, epoch, counter, dt, out, lse, stream)
+                              _kv_strides(q, k_cache, v_cache), softmax_scale, world, rank, peer_bases, ll_offset,
+                              ll_slot_bytes, epoch, counter, dt, out, lse, stream)
     return out, lse
 
 

@@ -417,17 +417,17 @@ extern "C" da_status da_forward_peer(const da_plan* plan, const void* q, const v
 extern "C" da_status da_forward_peer_combine(const da_plan* plan, const void* q, const void* k_cache,
                                              const void* v_cache, int32_t l_cap, const int32_t* cache_seqlens,
                                              const int64_t* strides, float softmax_scale, int32_t world,
-                                             int32_t rank, const uint64_t* peer_bases, int64_t slot_bytes,
-                                             int64_t lse_offset, int64_t flag_offset, int32_t* epoch,
-                                             uint32_t* counter, int32_t out_dtype, void* out, float* lse,
-                                             void* cuda_stream) {
-  if (plan == nullptr) return DA_ERR_INVALID_ARG;
-  int64_t rows = 0;
-  da_status st = check_peer_layout(world, rank, peer_bases, epoch, plan->batch, plan->h_q, plan->head_dim,
-                                   slot_bytes, lse_offset, flag_offset, &rows);
-  if (st != DA_OK) return st;
-  if (counter == nullptr || out == nullptr || (out_dtype != DA_BF16 && out_dtype != DA_F32)) return DA_ERR_INVALID_ARG;
-  if ((reinterpret_cast<uintptr_t>(counter) & 3u) != 0 || !aligned16(out) ||
+                                             int32_t rank, const uint64_t* peer_bases, int64_t ll_offset,
+                                             int64_t ll_slot_bytes, int32_t* epoch, uint32_t* counter,
+                                             int32_t out_dtype, void* out, float* lse, void* cuda_stream) {
+  if (plan == nullptr || world < 1 || world > kMaxPeers || rank < 0 || rank >= world || peer_bases == nullptr ||
+      epoch == nullptr || counter == nullptr || out == nullptr || (out_dtype != DA_BF16 && out_dtype != DA_F32))
+    return DA_ERR_INVALID_ARG;
+  if (plan->head_dim != kHeadDim) return DA_ERR_UNSUPPORTED;
+  const int64_t rows = int64_t(plan->batch) * plan->h_q;
+  if (ll_offset < 0 || ll_slot_bytes < rows * 129 * 8) return DA_ERR_INVALID_ARG;
+  if ((ll_offset & 15) != 0 || (ll_slot_bytes & 15) != 0 || (reinterpret_cast<uintptr_t>(epoch) & 3u) != 0 ||
+      (reinterpret_cast<uintptr_t>(counter) & 3u) != 0 || !aligned16(out) ||
       (lse != nullptr && (reinterpret_cast<uintptr_t>(lse) & 3u) != 0))
     return DA_ERR_ALIGNMENT;
   // the CTAs spin on the ranks' flags after writing their rows: the whole grid must be resident
@@ -438,9 +438,8 @@ extern "C" da_status da_forward_peer_combine(const da_plan* plan, const void* q,
   pub.bases = peer_bases;
   pub.epoch = epoch;
   pub.count = counter;
-  pub.slot_bytes = slot_bytes;
-  pub.lse_offset = lse_offset;
-  pub.flag_offset = flag_offset;
+  pub.ll_offset = ll_offset;
+  pub.ll_slot_bytes = ll_slot_bytes;
   pub.world = world;
   pub.rank = rank;
   pub.out = out;

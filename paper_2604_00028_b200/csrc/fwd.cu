@@ -757,8 +757,8 @@ __global__ void __launch_bounds__(threads_for(NW, helpers_for(kCombine)), 1)
   void* o_dst = p.out;
   float* l_dst = p.lse;
   uint32_t e_pub = 0;
-  if constexpr (kPub != 0) {
-    e_pub = pub_epoch(p.pub);
+  if constexpr (kPub != 0) e_pub = pub_epoch(p.pub);
+  if constexpr (kPub == 1) {
     const uint64_t sb = pub_slot(p.pub);
     o_dst = reinterpret_cast<void*>(sb);
     l_dst = reinterpret_cast<float*>(sb + static_cast<uint64_t>(p.pub.lse_offset));
@@ -774,8 +774,12 @@ __global__ void __launch_bounds__(threads_for(NW, helpers_for(kCombine)), 1)
       const float lse_v = eL[it] > 0.f ? (eM[it] + lg2(eL[it])) * kLn2 : kNegInf;
       const size_t row = static_cast<size_t>(b) * p.h_q + hq0 + g;
       if (kCombine == DA_COMBINE_NONE || (kDyn && dyn_single)) {   // kDyn, s_b = 1: the final row
-        store_out(p, o_dst, row, d4, v);
-        if (d4 == 0 && l_dst != nullptr) l_dst[row] = lse_v;
+        if constexpr (kPub == 2) {
+          pub_ll_store(p.pub, e_pub, row, d4, v, lse_v);
+        } else {
+          store_out(p, o_dst, row, d4, v);
+          if (d4 == 0 && l_dst != nullptr) l_dst[row] = lse_v;
+        }
       } else {  // DA_COMBINE_KERNEL: normalised partial o_i, lse_i (C-part); kDyn: slot-major rows
         const size_t prow = kDyn ? static_cast<size_t>(dslot) * p.h_q + hq0 + g
                                  : static_cast<size_t>(split) * p.batch * p.h_q + row;
@@ -844,27 +848,33 @@ __global__ void __launch_bounds__(threads_for(NW, helpers_for(kCombine)), 1)
       if (t == 0) TRACE(45);
       const float inv = Lsum > 0.f ? __frcp_rn(Lsum) : 0.f;
       const size_t row = static_cast<size_t>(b) * p.h_q + hq0 + g;
-      store_out(p, o_dst, row, d4, make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv));
-      if (d4 == 0 && l_dst != nullptr) l_dst[row] = Lsum > 0.f ? (M + lg2(Lsum)) * kLn2 : kNegInf;
+      if constexpr (kPub == 2) {
+        pub_ll_store(p.pub, e_pub, row, d4, make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv),
+                     Lsum > 0.f ? (M + lg2(Lsum)) * kLn2 : kNegInf);
+      } else {
+        store_out(p, o_dst, row, d4, make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv));
+        if (d4 == 0 && l_dst != nullptr) l_dst[row] = Lsum > 0.f ? (M + lg2(Lsum)) * kLn2 : kNegInf;
+      }
       if (t == 0) TRACE(46);
     }
   }
   if (threadIdx.x == 0) TRACE(47);
-  if constexpr (kPub != 0 && kCombine != DA_COMBINE_KERNEL) {   // this kernel wrote the final rows
+  if constexpr (kPub == 1 && kCombine != DA_COMBINE_KERNEL) {   // this kernel wrote the final rows
     __syncthreads();
     if (threadIdx.x == 0) pub_arrive(p.pub);
-    if constexpr (kPub == 2) {
-      // da_forward_peer_combine: every rank's partial of the rows this CTA wrote, LSE-merged here
-      // (the cross-GPU combine fused into the forward; the grid is one wave, so spinning is safe)
-      if (warp == 0) pub_wait_all(p.pub, e_pub, lane);
-      __syncthreads();
-      const int s = kCluster ? s_cl : 1;
-      for (int t = threadIdx.x; t < rows_per_owner * 32; t += kT) {
-        const int rl = t >> 5, d4 = t & 31;
-        const int g = static_cast<int>(rank) + rl * s;
-        if (g >= rows_valid) break;
-        pub_merge_row(p.pub, e_pub, static_cast<size_t>(b) * p.h_q + hq0 + g, d4);
-      }
+  }
+  if constexpr (kPub == 2) {
+    // da_forward_peer_combine: the rows this CTA wrote as LL words, polled back from every rank and
+    // LSE-merged here (the cross-GPU combine fused into the forward; the grid is one wave, so the
+    // spinning is safe); the epoch advances once every CTA has read it
+    __syncthreads();
+    if (threadIdx.x == 0) pub_count_advance(p.pub, e_pub);
+    const int s = kCluster ? s_cl : 1;
+    for (int t = threadIdx.x; t < rows_per_owner * 32; t += kT) {
+      const int rl = t >> 5, d4 = t & 31;
+      const int g = static_cast<int>(rank) + rl * s;
+      if (g >= rows_valid) break;
+      pub_ll_merge_row(p.pub, e_pub, static_cast<size_t>(b) * p.h_q + hq0 + g, d4);
     }
   }
 #ifdef DECATTN_TRACE

@@ -22,8 +22,10 @@ struct PubParams {
   int64_t slot_bytes, lse_offset, flag_offset;
   int32_t world, rank;
   int32_t writers;          // CTAs of the writing launch
-  // da_forward_peer_combine (one-wave NONE / CLUSTER forwards): after publishing, every CTA waits
-  // for all ranks' flags and LSE-merges the rows it wrote across the ranks into out / lse
+  // da_forward_peer_combine (one-wave NONE / CLUSTER forwards): every CTA writes its rows as
+  // self-validating 8-byte words (epoch << 32 | fp32 bits; no fence, no flag) into LL slot e & 1,
+  // polls the same words of every rank and LSE-merges them into out / lse
+  int64_t ll_offset, ll_slot_bytes;   // two LL slots [B H_Q][129] uint64 at ll_offset
   void* out;                // final [B, H_Q, d] bf16 or fp32
   float* lse;               // final [B, H_Q] or nullptr
   int32_t out_f32;

@@ -42,38 +42,56 @@ static __device__ __forceinline__ void pub_arrive(const PubParams& pb) {
   pub_arrive(pb.bases, pb.epoch, pb.count, pb.flag_offset, pb.world, pb.rank, pb.writers);
 }
 
-// The epoch this step publishes (e = *epoch + 1), read before the CTA counts itself.
-static __device__ __forceinline__ uint32_t pub_epoch(const PubParams& pb) {
-  return static_cast<uint32_t>(*reinterpret_cast<const volatile int32_t*>(pb.epoch)) + 1u;
-}
+// ---- da_forward_peer_combine: LL (low-latency) words, data and epoch in one 8-byte store ----
+constexpr int kLLRowWords = 129;                  // 128 o floats + lse per row
 
-// Warp 0 of the CTA (lane q polls rank q's flag) waits until every rank has published epoch e.
-// Spinning is safe only when every CTA of this grid is resident (the host checks one wave).
-static __device__ __forceinline__ void pub_wait_all(const PubParams& pb, uint32_t e, int lane) {
-  const uint32_t* flags = reinterpret_cast<const uint32_t*>(pb.bases[pb.rank] + static_cast<uint64_t>(pb.flag_offset));
-  for (int q = lane; q < pb.world; q += 32)
-    while (ptx::ld_acquire_sys_u32(flags + q) < e) {
-    }
+static __device__ __forceinline__ uint64_t* pub_ll_row(const PubParams& pb, int q, uint32_t e, size_t row) {
+  return reinterpret_cast<uint64_t*>(pb.bases[q] + static_cast<uint64_t>(pb.ll_offset) +
+                                     static_cast<uint64_t>(pb.ll_slot_bytes) * (e & 1u)) + row * kLLRowWords;
 }
-
-// LSE merge (C-comb) of row `row`, float4 column d4, across the world partials of slot e & 1
-// (o fp32 at slot + row * 512, lse at slot + lse_offset + row * 4), read from the ranks' buffers
-// (NVLink loads for peers); writes the final out / lse.
-static __device__ __forceinline__ void pub_merge_row(const PubParams& pb, uint32_t e, size_t row, int d4) {
-  const uint64_t slot_off = static_cast<uint64_t>(pb.slot_bytes) * (e & 1u);
+static __device__ __forceinline__ void st_ll(uint64_t* p, uint32_t e, float v) {
+  const uint64_t w = (static_cast<uint64_t>(e) << 32) | __float_as_uint(v);
+  asm volatile("st.relaxed.sys.global.b64 [%0], %1;" ::"l"(p), "l"(w) : "memory");
+}
+static __device__ __forceinline__ uint64_t ld_ll(const uint64_t* p) {
+  uint64_t w;
+  asm volatile("ld.relaxed.sys.global.b64 %0, [%1];" : "=l"(w) : "l"(p) : "memory");
+  return w;
+}
+// Row `row`, float4 column d4 (and the lse when d4 == 0) of this rank's partial, as LL words.
+static __device__ __forceinline__ void pub_ll_store(const PubParams& pb, uint32_t e, size_t row, int d4, float4 v,
+                                                    float lse) {
+  uint64_t* w = pub_ll_row(pb, pb.rank, e, row) + 4 * d4;
+  st_ll(w, e, v.x);
+  st_ll(w + 1, e, v.y);
+  st_ll(w + 2, e, v.z);
+  st_ll(w + 3, e, v.w);
+  if (d4 == 0) st_ll(pub_ll_row(pb, pb.rank, e, row) + 128, e, lse);
+}
+// Every rank's (o, lse) words of row / d4, polled until they carry epoch e (each word validates
+// itself: no flag, no fence), LSE-merged (C-comb) into the final out / lse.
+static __device__ __forceinline__ void pub_ll_merge_row(const PubParams& pb, uint32_t e, size_t row, int d4) {
   constexpr float kLog2e = 1.4426950408889634f;
   float m = -__builtin_huge_valf(), L = 0.f;
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
   for (int q = 0; q < pb.world; ++q) {
-    const uint64_t base = pb.bases[q] + slot_off;
-    const float li = reinterpret_cast<const float*>(base + static_cast<uint64_t>(pb.lse_offset))[row] * kLog2e;
-    const float4 oi = reinterpret_cast<const float4*>(base)[row * 32 + d4];
+    const uint64_t* rw = pub_ll_row(pb, q, e, row);
+    uint64_t w[5];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) w[i] = ld_ll(rw + 4 * d4 + i);
+    w[4] = ld_ll(rw + 128);
+#pragma unroll
+    for (int i = 0; i < 5; ++i)
+      while (static_cast<uint32_t>(w[i] >> 32) != e) w[i] = ld_ll(i < 4 ? rw + 4 * d4 + i : rw + 128);
+    const float li = __uint_as_float(static_cast<uint32_t>(w[4])) * kLog2e;
+    const float4 oi = make_float4(__uint_as_float(static_cast<uint32_t>(w[0])), __uint_as_float(static_cast<uint32_t>(w[1])),
+                                  __uint_as_float(static_cast<uint32_t>(w[2])), __uint_as_float(static_cast<uint32_t>(w[3])));
     const float mb = fmaxf(m, li);
     if (mb == -__builtin_huge_valf()) continue;           // every partial so far empty
-    const float r = ptx::ex2(m - mb), w = ptx::ex2(li - mb);
-    L = fmaf(L, r, w);
-    acc = make_float4(fmaf(acc.x, r, w * oi.x), fmaf(acc.y, r, w * oi.y), fmaf(acc.z, r, w * oi.z),
-                      fmaf(acc.w, r, w * oi.w));
+    const float r = ptx::ex2(m - mb), wt = ptx::ex2(li - mb);
+    L = fmaf(L, r, wt);
+    acc = make_float4(fmaf(acc.x, r, wt * oi.x), fmaf(acc.y, r, wt * oi.y), fmaf(acc.z, r, wt * oi.z),
+                      fmaf(acc.w, r, wt * oi.w));
     m = mb;
   }
   const float inv = L > 0.f ? __frcp_rn(L) : 0.f;
@@ -87,6 +105,19 @@ static __device__ __forceinline__ void pub_merge_row(const PubParams& pb, uint32
     reinterpret_cast<uint2*>(pb.out)[row * 32 + d4] = w2;
   }
   if (d4 == 0 && pb.lse != nullptr) pb.lse[row] = L > 0.f ? (m + ptx::lg2(L)) * (1.f / kLog2e) : -__builtin_huge_valf();
+}
+// One thread per CTA, after the CTA read the epoch: the last of the grid's CTAs advances it (the
+// next step's kernel reads it after griddepcontrol.wait) and resets the count.
+static __device__ __forceinline__ void pub_count_advance(const PubParams& pb, uint32_t e) {
+  const uint32_t prev = atomicAdd(pb.count, 1u);
+  if (prev + 1u != static_cast<uint32_t>(pb.writers)) return;
+  *reinterpret_cast<volatile uint32_t*>(pb.count) = 0u;
+  *reinterpret_cast<volatile int32_t*>(pb.epoch) = static_cast<int32_t>(e);
+}
+
+// The epoch this step publishes (e = *epoch + 1), read before the CTA counts itself.
+static __device__ __forceinline__ uint32_t pub_epoch(const PubParams& pb) {
+  return static_cast<uint32_t>(*reinterpret_cast<const volatile int32_t*>(pb.epoch)) + 1u;
 }
 
 }  // namespace decattn

@@ -150,16 +150,19 @@ def _align16(n: int) -> int:
 
 
 def peer_layout(batch: int, h_q: int, head_dim: int, world: int):
-    """Byte layout of one rank's exchange buffer (include/decattn.h, da_combine_peers): two slots of
-    slot_bytes, each [0, lse_offset) o fp32 [B, H_Q, d] and [lse_offset, ...) lse fp32 [B, H_Q];
-    then one uint32 flag per rank at flag_offset.  Returns (slot_bytes, lse_offset, flag_offset,
-    total_bytes), all 16-byte aligned."""
+    """Byte layout of one rank's exchange buffer (include/decattn.h): two slots of slot_bytes, each
+    [0, lse_offset) o fp32 [B, H_Q, d] and [lse_offset, ...) lse fp32 [B, H_Q]; one uint32 flag per
+    rank at flag_offset (da_forward_peer / da_peer_signal / da_combine_peers); two LL slots of
+    ll_slot_bytes, uint64 [B H_Q][d + 1], at ll_offset (da_forward_peer_combine).  Returns
+    (slot_bytes, lse_offset, flag_offset, ll_offset, ll_slot_bytes, total_bytes), 16-byte aligned."""
     if min(batch, h_q, head_dim, world) < 1:
         raise ValueError("bad peer layout arguments")
     lse_offset = _align16(batch * h_q * head_dim * 4)
     slot_bytes = _align16(lse_offset + batch * h_q * 4)
     flag_offset = 2 * slot_bytes
-    return slot_bytes, lse_offset, flag_offset, flag_offset + _align16(4 * world)
+    ll_offset = flag_offset + _align16(4 * world)
+    ll_slot_bytes = _align16(8 * (head_dim + 1) * batch * h_q)
+    return slot_bytes, lse_offset, flag_offset, ll_offset, ll_slot_bytes, ll_offset + 2 * ll_slot_bytes
 
 
 class PeerSeqShardedDecode:
@@ -187,7 +190,8 @@ class PeerSeqShardedDecode:
         if self.l_local < 1:
             raise ValueError("every rank needs at least one token of the sequence")
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
-        self.slot_bytes, self.lse_offset, self.flag_offset, total = peer_layout(batch, h_q, head_dim, self.world)
+        self.slot_bytes, self.lse_offset, self.flag_offset, self.ll_offset, self.ll_slot_bytes, total = \
+            peer_layout(batch, h_q, head_dim, self.world)
         self.buf = symm.empty((total // 4,), dtype=torch.float32, device=self.device)
         pg = group if group is not None else dist.group.WORLD
         self.hdl = symm.rendezvous(self.buf, pg.group_name)
@@ -210,8 +214,8 @@ class PeerSeqShardedDecode:
         from . import api
         if self.one_kernel:
             return api.forward_peer_combine(self.plan, q, k_local, v_local, seqlens_local, self.world, self.rank,
-                                            self.bases, self.slot_bytes, self.lse_offset, self.flag_offset,
-                                            self.epoch, self.counter, out=out, lse=lse)
+                                            self.bases, self.ll_offset, self.ll_slot_bytes, self.epoch, self.counter,
+                                            out=out, lse=lse)
         if self.fused:
             api.forward_peer(self.plan, q, k_local, v_local, seqlens_local, self.world, self.rank, self.bases,
                              self.slot_bytes, self.lse_offset, self.flag_offset, self.epoch, self.counter,

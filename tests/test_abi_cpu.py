@@ -412,11 +412,12 @@ def test_forward_peer_validation(L):
 def test_peer_layout():
     from paper_2604_00028_b200.dist import peer_layout
     for B, H, W in ((1, 64, 8), (3, 24, 2), (1, 8, 1), (128, 64, 64)):
-        slot, lo, fo, tot = peer_layout(B, H, 128, W)
+        slot, lo, fo, llo, lls, tot = peer_layout(B, H, 128, W)
         assert lo >= B * H * 128 * 4 and lo % 16 == 0
         assert slot >= lo + 4 * B * H and slot % 16 == 0
         assert fo >= 2 * slot and fo % 16 == 0
-        assert tot >= fo + 4 * W and tot % 16 == 0
+        assert llo >= fo + 4 * W and llo % 16 == 0 and lls >= 8 * 129 * B * H and lls % 16 == 0
+        assert tot >= llo + 2 * lls and tot % 16 == 0
 
 
 def test_python_shape_checks_before_any_launch(L):
@@ -445,8 +446,9 @@ def test_forward_peer_combine_validation(L):
     slot, lo, fo = 4128, 4096, 2 * 4128
 
     def fwd(plan, **kw):
+        rows = plan.batch * plan.h_q
         a = dict(plan=plan, q=A2, k_cache=A2, v_cache=A2, l_cap=plan.l_k, cache_seqlens=None, strides=None,
-                 softmax_scale=0.0, world=2, rank=0, peer_bases=A2, slot_bytes=slot, lse_offset=lo, flag_offset=fo,
+                 softmax_scale=0.0, world=2, rank=0, peer_bases=A2, ll_offset=fo + 16, ll_slot_bytes=8 * 129 * rows + 16,
                  epoch=A2, counter=A2, out_dtype=L.DA_BF16, out=A2, lse=A2, stream=0)
         a.update(kw)
         with pytest.raises(L.DecAttnError) as e:
@@ -457,6 +459,9 @@ def test_forward_peer_combine_validation(L):
     assert fwd(cluster, out=None) == L.DA_ERR_INVALID_ARG
     assert fwd(cluster, out_dtype=7) == L.DA_ERR_INVALID_ARG
     assert fwd(cluster, counter=None) == L.DA_ERR_INVALID_ARG
+    assert fwd(cluster, ll_slot_bytes=8 * 129 * 8 - 16) == L.DA_ERR_INVALID_ARG    # slot shorter than 8 rows
+    assert fwd(cluster, ll_offset=fo + 8) == L.DA_ERR_ALIGNMENT
+    assert fwd(cluster, world=0) == L.DA_ERR_INVALID_ARG
     assert fwd(cluster, out=A2 + 8) == L.DA_ERR_ALIGNMENT
     assert fwd(cluster, lse=A2 + 2) == L.DA_ERR_ALIGNMENT
     ws = L.da_plan_make(1, 8, 1, 4096, 128, 1, 0, 148, "guarded", 0)          # s = 28: workspace combine
@@ -464,5 +469,4 @@ def test_forward_peer_combine_validation(L):
     big = L.da_plan_make(64, 8, 1, 300, 128, 1, 0, 148, "guarded", 0)         # 64 CTAs... one wave: allowed
     wide = L.da_plan_make(256, 8, 1, 300, 128, 1, 0, 148, "guarded", 0)       # 256 CTAs > 148 SMs
     assert big.grid_x * big.grid_y * big.grid_z <= 148
-    assert fwd(wide, slot_bytes=256 * 8 * 516 + 16, lse_offset=256 * 8 * 512,
-               flag_offset=2 * (256 * 8 * 516 + 16)) == L.DA_ERR_UNSUPPORTED
+    assert fwd(wide) == L.DA_ERR_UNSUPPORTED

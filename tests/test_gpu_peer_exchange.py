@@ -92,6 +92,10 @@ def test_forward_peer_every_combine_mode(one_rank_group, batch, h_q, h_kv, l_k, 
         assert_out_close(synth.to_f64(out), ref_o)
         assert_lse_close(synth.to_f64(lse), ref_l)
         assert int(sd.epoch.item()) == e and int(sd.counter.item()) == 0
-    # the partial of the last step sits in slot 4 & 1 = 0 of the exchange buffer, flag 0 holds 4
-    flags = sd.buf.view(torch.int32)[sd.flag_offset // 4: sd.flag_offset // 4 + 1]
-    assert int(flags.item()) == 4
+    if sd.one_kernel:   # the LL words of the last step (slot 4 & 1 = 0) carry epoch 4
+        words = sd.buf.view(torch.int64)[sd.ll_offset // 8: (sd.ll_offset + sd.ll_slot_bytes) // 8]
+        rows = batch * h_q
+        assert bool(((words[: rows * 129] >> 32) == 4).all())
+    else:               # the partial of the last step sits in slot 0 of the exchange buffer, flag 0 holds 4
+        flags = sd.buf.view(torch.int32)[sd.flag_offset // 4: sd.flag_offset // 4 + 1]
+        assert int(flags.item()) == 4
