@@ -1,7 +1,10 @@
-// Fused peer publish (da_forward_peer): the kernel that produces a rank's final
-// (o, lse) rows writes them straight into its exchange slot and the last CTA releases the step's
-// epoch to every rank, so no separate signal kernel or copy sits between the forward and the
-// cross-GPU combine.
+// Cross-GPU exchange from inside the producing kernel.
+//   da_forward_peer: the kernel that produces a rank's final (o, lse) rows writes them straight
+//     into its exchange slot and the last CTA releases the step's epoch to every rank (one
+//     system fence), so no separate signal kernel or copy sits before da_combine_peers.
+//   da_forward_peer_combine: every CTA writes its rows as LL words (value and epoch in one 8-byte
+//     store), polls the same words of every rank and LSE-merges them: the whole step in one
+//     kernel, with no fence and no flag on its critical path.
 #pragma once
 
 #include <cstdint>
