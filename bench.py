@@ -454,6 +454,10 @@ def main():
     ap.add_argument("--seq-shard", action="store_true",
                     help="long_context: take the sequence-sharded path (exchange included) even at N = 1 "
                          "(a one-rank group; checks the sharded step on one GPU)")
+    ap.add_argument("--shard-heads", action="store_true",
+                    help="N > 1, latency / throughput workloads: split the KV heads (and their query heads) "
+                         "across the ranks - the tensor-parallel mapping, e.g. Llama-70B over 8 GPUs = the TP-8 "
+                         "slice per rank; strong scaling, no collective")
     ap.add_argument("--exchange", default="p2p", choices=["nccl", "p2p", "p2p-split"],
                     help="long_context with N > 1: the exchange over peer memory (default: da_peer_signal + "
                          "da_combine_peers over torch symmetric memory) or an NCCL all-gather + da_combine")
@@ -520,7 +524,8 @@ def main():
 
     cfg = WORKLOADS[args.workload]
     long_sharded = args.workload == "long_context" and (world > 1 or args.seq_shard)
-    batch_sharded = args.workload == "high_load" and world > 1
+    batch_sharded = args.workload == "high_load" and world > 1 and not args.shard_heads
+    head_sharded = args.shard_heads and world > 1 and not long_sharded
     if long_sharded:
         from paper_2604_00028_b200.dist import PeerSeqShardedDecode, SeqShardedDecode
         p2p = args.exchange.startswith("p2p")
@@ -569,8 +574,12 @@ def main():
             from paper_2604_00028_b200.dist import shard_range
             b0, b1 = shard_range(cfg["batch"], rank, world)
             local_cfg = dict(cfg, batch=b1 - b0)
+        elif head_sharded:
+            from paper_2604_00028_b200.dist import head_shard
+            (k0, k1), (h0, h1) = head_shard(cfg["h_q"], cfg["h_kv"], rank, world)
+            local_cfg = dict(cfg, h_q=h1 - h0, h_kv=k1 - k0)
         w = Workload(local_cfg, dev, 1000 + rank, l2)
-        plan = dec.make_plan(local_cfg["batch"], cfg["h_q"], cfg["h_kv"], cfg["l_k"], policy=args.policy)
+        plan = dec.make_plan(local_cfg["batch"], local_cfg["h_q"], local_cfg["h_kv"], cfg["l_k"], policy=args.policy)
         with torch.cuda.stream(stream):
             ws = dec.workspace_for(plan, dev)
             for i in range(args.warmup):
@@ -578,11 +587,12 @@ def main():
                 dec.forward(plan, w.q, w.k[j], w.v[j], w.seqlens, out=w.out, lse=w.lse, workspace=ws)
         torch.cuda.synchronize()
         g = make_graph(dec, plan, w, args.steps, stream)
-        step_bytes_total = alg_bytes(**cfg) if batch_sharded else w.bytes * world
+        step_bytes_total = alg_bytes(**cfg) if (batch_sharded or head_sharded) else w.bytes * world
         kernels_per_step = 2 if plan.combine_mode == L.DA_COMBINE_KERNEL else 1
-        scaling = "strong" if batch_sharded else "weak"
+        scaling = "strong" if (batch_sharded or head_sharded) else "weak"
         l2_note = w.l2_note(l2)
         parallelism = (f"batch-sharded dp{world} (B={cfg['batch']} split across ranks, no collective)" if batch_sharded
+                       else f"head-sharded tp{world} (H_KV={cfg['h_kv']} split across ranks, no collective)" if head_sharded
                        else f"batch-sharded dp{world} (independent sequences, no collective)" if world > 1
                        else "single GPU")
 
@@ -665,7 +675,7 @@ def main():
         "data": "synthetic (seeded N(0,1) bf16 q/K/V, uniform cache_seqlens = L_K)",
         "config": {"workload": args.workload, **cfg, "head_dim": HEAD_DIM, "policy": args.policy,
                    "num_splits": plan.num_splits, "combine_mode": plan.combine_mode,
-                   "global_batch": cfg["batch"] * (world if not (long_sharded or batch_sharded) else 1),
+                   "global_batch": cfg["batch"] * (world if not (long_sharded or batch_sharded or head_sharded) else 1),
                    "parallelism": parallelism, "l2": l2_note, "graph": "K steps in one CUDA graph"},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "traffic": trec.get("dram_bytes_per_launch") if trec else None,

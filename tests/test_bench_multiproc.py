@@ -57,3 +57,19 @@ def test_bench_two_ranks_high_load_batch_split():
     d = json.loads(lines[0])
     assert d["n_gpus"] == 2 and d["scaling"] == "strong" and d["config"]["global_batch"] == 128
     assert d["value"] > 0 and d["gpu_launches"] == 3
+
+
+@pytest.mark.gpu
+def test_bench_two_ranks_head_sharded():
+    # Llama-70B with the KV heads split across ranks (the tensor-parallel mapping): strong scaling
+    env = dict(os.environ, DECATTN_BENCH_BACKEND="gloo", DECATTN_BENCH_ONE_GPU="1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr", "127.0.0.1", "--master-port", "29521", os.path.join(ROOT, "bench.py"),
+           "--gpus", "2", "--shard-heads", "--steps", "20", "--warmup", "3"]
+    r = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    assert d["scaling"] == "strong" and d["config"]["global_batch"] == 1 and "head-sharded" in d["config"]["parallelism"]
+    assert d["value"] > 0 and d["gpu_launches"] == 20
