@@ -36,6 +36,11 @@
 //                          second launch, no cluster-wide barrier on exit;
 //               KERNEL   : normalised fp32 partials + lse go to the
 //                          workspace for lse_combine_kernel (combine.cu).
+//   kPub (sequence-sharded steps, pub.cuh): 1 = the final rows go to this
+//               rank's exchange slot and the last CTA releases the epoch
+//               (da_forward_peer); 2 = the rows go out as LL words, every CTA
+//               polls the same words of every rank and LSE-merges them into
+//               the final out / lse (da_forward_peer_combine: one kernel).
 // Programmatic dependent launch: the prologue overlaps the previous kernel's
 // tail; griddepcontrol.wait precedes the first global read.  Scores are kept in
 // the log2 domain; lse is returned in natural log (C-amb-10).
