@@ -385,8 +385,10 @@ DA_API da_status da_forward_peer(const da_plan* plan, const void* q, const void*
                                  int64_t workspace_bytes, void* cuda_stream);
 
 /*
- * da_forward_peer_combine - the whole sequence-sharded step in ONE kernel.  e = *epoch + 1.  Every
- * CTA of the forward writes its final fp32 rows (o, then lse) into LL slot e & 1 of this rank's
+ * da_forward_peer_combine - the whole sequence-sharded step with the exchange inside the kernel
+ * that produces the final rows (the forward for NONE / CLUSTER plans: ONE kernel per step; the
+ * combine kernel for static workspace plans).  e = *epoch + 1.  Every CTA of that kernel writes
+ * its final fp32 rows (o, then lse) into LL slot e & 1 of this rank's
  * exchange buffer as self-validating 8-byte words ((e << 32) | fp32 bits, one system-scope relaxed
  * store each: no fence, no flag), then polls the same words of every rank's slot (NVLink loads for
  * peers) until they carry e and LSE-merges (C-comb) the world partials of its rows into out
@@ -398,9 +400,11 @@ DA_API da_status da_forward_peer(const da_plan* plan, const void* q, const void*
  *     every rank, zero before the first step); a rank reuses slot e & 1 at step e + 2 only (the
  *     stream order then guarantees every peer has read it).
  *   counter: device uint32 owned by this rank, zero before the first step (left zero after each).
- * Plans with combine_mode NONE or CLUSTER whose grid is one wave (grid_x * grid_y * grid_z <=
- * usable_sms; the CTAs spin, so the whole grid must be resident: an otherwise idle GPU);
- * DA_ERR_UNSUPPORTED otherwise (use da_forward_peer + da_combine_peers).  No workspace.
+ * The CTAs spin, so the writing grid must be resident (an otherwise idle GPU): NONE / CLUSTER
+ * plans whose forward grid is one wave (grid_x * grid_y * grid_z <= usable_sms), or static
+ * DA_COMBINE_KERNEL plans with B * H_Q <= 8 usable_sms (workspace, workspace_bytes as da_forward);
+ * DA_ERR_UNSUPPORTED otherwise, and for DA_POLICY_DYNAMIC plans with per-sequence split counts
+ * (use da_forward_peer + da_combine_peers).
  * Errors: as da_forward; DA_ERR_INVALID_ARG for world / rank / NULL pointers / a short LL slot,
  * DA_ERR_ALIGNMENT for misaligned offsets, counter, epoch, out or lse.
  */
@@ -409,7 +413,8 @@ DA_API da_status da_forward_peer_combine(const da_plan* plan, const void* q, con
                                          const int64_t* strides, float softmax_scale, int32_t world,
                                          int32_t rank, const uint64_t* peer_bases, int64_t ll_offset,
                                          int64_t ll_slot_bytes, int32_t* epoch, uint32_t* counter,
-                                         int32_t out_dtype, void* out, float* lse, void* cuda_stream);
+                                         int32_t out_dtype, void* out, float* lse, void* workspace,
+                                         int64_t workspace_bytes, void* cuda_stream);
 
 /* Static, NUL-terminated description of a status code (never NULL). */
 DA_API const char* da_status_string(int32_t status);

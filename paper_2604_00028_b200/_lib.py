@@ -91,7 +91,7 @@ def _load() -> ctypes.CDLL:
                                     i64, vp, vp, vp, i64, vp]
     lib.da_forward_peer.restype = i32
     lib.da_forward_peer_combine.argtypes = [ctypes.POINTER(da_plan), vp, vp, vp, i32, vp, vp, f32, i32, i32, vp,
-                                            i64, i64, vp, vp, i32, vp, vp, vp]
+                                            i64, i64, vp, vp, i32, vp, vp, vp, i64, vp]
     lib.da_forward_peer_combine.restype = i32
     lib.da_combine.argtypes = [i32, i32, i32, i32, vp, i64, vp, i64, i32, vp, vp, vp]
     lib.da_combine.restype = i32
@@ -251,14 +251,15 @@ def da_forward_peer(plan: da_plan, q, k_cache, v_cache, l_cap, cache_seqlens, st
 
 def da_forward_peer_combine(plan: da_plan, q, k_cache, v_cache, l_cap, cache_seqlens, strides, softmax_scale, world,
                             rank, peer_bases, ll_offset, ll_slot_bytes, epoch, counter, out_dtype, out, lse,
-                            stream=None) -> None:
+                            workspace=None, workspace_bytes=0, stream=None) -> None:
     sarr = None
     if strides is not None:
         sarr = (ctypes.c_int64 * 8)(*[int(x) for x in strides])
     st = LIB.da_forward_peer_combine(ctypes.byref(plan), _ptr(q), _ptr(k_cache), _ptr(v_cache), int(l_cap),
                                      _ptr(cache_seqlens), sarr, float(softmax_scale), int(world), int(rank),
                                      _ptr(peer_bases), int(ll_offset), int(ll_slot_bytes), _ptr(epoch), _ptr(counter),
-                                     int(out_dtype), _ptr(out), _ptr(lse), _stream_handle(stream))
+                                     int(out_dtype), _ptr(out), _ptr(lse), _ptr(workspace), int(workspace_bytes),
+                                     _stream_handle(stream))
     if st != DA_OK:
         raise DecAttnError(st, "da_forward_peer_combine")
 

@@ -136,13 +136,17 @@ def forward_peer(plan: L.da_plan, q, k_cache, v_cache, cache_seqlens, world, ran
 
 
 def one_kernel_exchange_ok(plan: L.da_plan) -> bool:
-    """da_forward_peer_combine's condition: a NONE / CLUSTER plan whose grid is one wave."""
-    return (plan.combine_mode != L.DA_COMBINE_KERNEL
-            and plan.grid_x * plan.grid_y * plan.grid_z <= plan.usable_sms)
+    """da_forward_peer_combine's condition: the kernel that writes the final rows can keep its whole
+    grid resident - a NONE / CLUSTER forward of one wave, or the combine kernel of a static
+    workspace plan (one small CTA per row, at most 8 per SM)."""
+    if plan.combine_mode == L.DA_COMBINE_KERNEL:
+        dynamic = plan.policy == L.POLICIES["dynamic"] and plan.num_splits > 1
+        return not dynamic and plan.batch * plan.h_q <= 8 * plan.usable_sms
+    return plan.grid_x * plan.grid_y * plan.grid_z <= plan.usable_sms
 
 
 def forward_peer_combine(plan: L.da_plan, q, k_cache, v_cache, cache_seqlens, world, rank, peer_bases, ll_offset,
-                         ll_slot_bytes, epoch, counter, *, out=None, lse=None, softmax_scale=0.0,
+                         ll_slot_bytes, epoch, counter, *, out=None, lse=None, workspace=None, softmax_scale=0.0,
                          out_dtype=torch.bfloat16, stream=None):
     """The sequence-sharded step in one kernel via da_forward_peer_combine: the forward publishes
     this rank's partial, waits for every rank's, and LSE-merges them into (out, lse)."""
@@ -158,9 +162,12 @@ def forward_peer_combine(plan: L.da_plan, q, k_cache, v_cache, cache_seqlens, wo
     if lse is None:
         lse = torch.empty((B, HQ), dtype=torch.float32, device=q.device)
     dt = L.DA_F32 if out.dtype == torch.float32 else L.DA_BF16
+    if workspace is None:
+        workspace = workspace_for(plan, q.device)
+    ws_bytes = 0 if workspace is None else workspace.numel() * workspace.element_size()
     L.da_forward_peer_combine(plan, q, k_cache, v_cache, k_cache.shape[1], cache_seqlens,
                               _kv_strides(q, k_cache, v_cache), softmax_scale, world, rank, peer_bases, ll_offset,
-                              ll_slot_bytes, epoch, counter, dt, out, lse, stream)
+                              ll_slot_bytes, epoch, counter, dt, out, lse, workspace, ws_bytes, stream)
     return out, lse
 
 

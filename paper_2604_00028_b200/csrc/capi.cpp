@@ -197,7 +197,7 @@ da_status forward_impl(const da_plan* plan, const void* q, const void* k_cache, 
   p.dyn_tiles = plan->h_kv * plan->num_m_blocks;
   p.dyn_u = plan->usable_sms;
   p.ws_meta = ws_meta;
-  if (pub != nullptr) {
+  if (pub != nullptr && !(pub->out != nullptr && plan->combine_mode == DA_COMBINE_KERNEL)) {
     p.pub = *pub;     // NONE / CLUSTER: every CTA of the forward writes final rows and counts
     p.pub.writers = plan->grid_x * plan->grid_y * plan->grid_z;
   }
@@ -419,7 +419,8 @@ extern "C" da_status da_forward_peer_combine(const da_plan* plan, const void* q,
                                              const int64_t* strides, float softmax_scale, int32_t world,
                                              int32_t rank, const uint64_t* peer_bases, int64_t ll_offset,
                                              int64_t ll_slot_bytes, int32_t* epoch, uint32_t* counter,
-                                             int32_t out_dtype, void* out, float* lse, void* cuda_stream) {
+                                             int32_t out_dtype, void* out, float* lse, void* workspace,
+                                             int64_t workspace_bytes, void* cuda_stream) {
   if (plan == nullptr || world < 1 || world > kMaxPeers || rank < 0 || rank >= world || peer_bases == nullptr ||
       epoch == nullptr || counter == nullptr || out == nullptr || (out_dtype != DA_BF16 && out_dtype != DA_F32))
     return DA_ERR_INVALID_ARG;
@@ -430,10 +431,13 @@ extern "C" da_status da_forward_peer_combine(const da_plan* plan, const void* q,
       (reinterpret_cast<uintptr_t>(counter) & 3u) != 0 || !aligned16(out) ||
       (lse != nullptr && (reinterpret_cast<uintptr_t>(lse) & 3u) != 0))
     return DA_ERR_ALIGNMENT;
-  // the CTAs spin on the ranks' flags after writing their rows: the whole grid must be resident
-  // (one CTA per SM: the forward's shared memory), and no workspace combine kernel may follow
+  // the CTAs that write the final rows spin on the ranks' words: their whole grid must be
+  // resident - the forward (one CTA per SM: its shared memory) for NONE / CLUSTER plans, the
+  // combine kernel (one small CTA per row, many per SM) for static workspace plans
   const int64_t ctas = int64_t(plan->grid_x) * plan->grid_y * plan->grid_z;
-  if (plan->combine_mode == DA_COMBINE_KERNEL || ctas > plan->usable_sms) return DA_ERR_UNSUPPORTED;
+  if (plan->combine_mode == DA_COMBINE_KERNEL ? (is_dynamic(*plan) || rows > 8LL * plan->usable_sms)
+                                              : ctas > plan->usable_sms)
+    return DA_ERR_UNSUPPORTED;
   PubParams pub{};
   pub.bases = peer_bases;
   pub.epoch = epoch;
@@ -446,7 +450,7 @@ extern "C" da_status da_forward_peer_combine(const da_plan* plan, const void* q,
   pub.lse = lse;
   pub.out_f32 = out_dtype == DA_F32;
   return forward_impl(plan, q, k_cache, v_cache, l_cap, cache_seqlens, strides, softmax_scale, DA_F32, nullptr,
-                      nullptr, nullptr, 0, cuda_stream, PagedArgs{}, &pub);
+                      nullptr, workspace, workspace_bytes, cuda_stream, PagedArgs{}, &pub);
 }
 
 extern "C" da_status da_combine_peers(int32_t world, int32_t rank, const uint64_t* peer_bases, int64_t slot_bytes,

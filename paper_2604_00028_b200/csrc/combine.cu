@@ -135,6 +135,18 @@ __global__ void __launch_bounds__(kCombineThreads)
   const float inv = L > 0.f ? __frcp_rn(L) : 0.f;
   sum = make_float4(sum.x * inv, sum.y * inv, sum.z * inv, sum.w * inv);
   const float lse = empty ? kNegInf : (M + lg2(L)) * (1.f / kLog2e);
+  if (p.pub.out != nullptr) {
+    // da_forward_peer_combine: this row of this rank's partial goes out as LL words, the same words
+    // of every rank are polled back and LSE-merged into the final row (the cross-rank combine in
+    // the kernel that produces the row; the grid is co-resident, so the spinning is safe)
+    const uint32_t e = pub_epoch(p.pub);
+    pub_ll_store(p.pub, e, static_cast<size_t>(row), lane, sum, lse);
+    __syncwarp();
+    if (lane == 0) pub_count_advance(p.pub, e);
+    pub_ll_merge_row(p.pub, e, static_cast<size_t>(row), lane);
+    CTRACE(2);
+    return;
+  }
   // final rows: out / lse, or this step's slot of the exchange buffer (da_forward_peer)
   void* o_dst = p.out;
   float* l_dst = p.lse;

@@ -215,7 +215,7 @@ class PeerSeqShardedDecode:
         if self.one_kernel:
             return api.forward_peer_combine(self.plan, q, k_local, v_local, seqlens_local, self.world, self.rank,
                                             self.bases, self.ll_offset, self.ll_slot_bytes, self.epoch, self.counter,
-                                            out=out, lse=lse)
+                                            out=out, lse=lse, workspace=self._ws)
         if self.fused:
             api.forward_peer(self.plan, q, k_local, v_local, seqlens_local, self.world, self.rank, self.bases,
                              self.slot_bytes, self.lse_offset, self.flag_offset, self.epoch, self.counter,

@@ -60,7 +60,7 @@ def main():
         plan = None
         for _ in range(2):
             sd = {f: PeerSeqShardedDecode(1, 64, 8, lk, device="cuda", fused=f != "split", one_kernel=f == "one",
-                                          policy="seq_aware_sm")
+                                          policy=os.environ.get("PROBE_POLICY", "seq_aware_sm"))
                   for f in ("one", "fused", "split")}
             plan = sd["fused"].plan
             ws = dec.workspace_for(plan, torch.device("cuda"))

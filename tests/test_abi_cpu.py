@@ -449,7 +449,8 @@ def test_forward_peer_combine_validation(L):
         rows = plan.batch * plan.h_q
         a = dict(plan=plan, q=A2, k_cache=A2, v_cache=A2, l_cap=plan.l_k, cache_seqlens=None, strides=None,
                  softmax_scale=0.0, world=2, rank=0, peer_bases=A2, ll_offset=fo + 16, ll_slot_bytes=8 * 129 * rows + 16,
-                 epoch=A2, counter=A2, out_dtype=L.DA_BF16, out=A2, lse=A2, stream=0)
+                 epoch=A2, counter=A2, out_dtype=L.DA_BF16, out=A2, lse=A2, workspace=None, workspace_bytes=0,
+                 stream=0)
         a.update(kw)
         with pytest.raises(L.DecAttnError) as e:
             L.da_forward_peer_combine(**a)
@@ -465,7 +466,9 @@ def test_forward_peer_combine_validation(L):
     assert fwd(cluster, out=A2 + 8) == L.DA_ERR_ALIGNMENT
     assert fwd(cluster, lse=A2 + 2) == L.DA_ERR_ALIGNMENT
     ws = L.da_plan_make(1, 8, 1, 4096, 128, 1, 0, 148, "guarded", 0)          # s = 28: workspace combine
-    assert ws.combine_mode == L.DA_COMBINE_KERNEL and fwd(ws) == L.DA_ERR_UNSUPPORTED
+    assert ws.combine_mode == L.DA_COMBINE_KERNEL and fwd(ws) == L.DA_ERR_WORKSPACE   # allowed, needs one
+    dyn = L.da_plan_make(4, 16, 2, 3000, 128, 1, 0, 148, "dynamic", 0)
+    assert dyn.combine_mode == L.DA_COMBINE_KERNEL and fwd(dyn) == L.DA_ERR_UNSUPPORTED
     big = L.da_plan_make(64, 8, 1, 300, 128, 1, 0, 148, "guarded", 0)         # 64 CTAs... one wave: allowed
     wide = L.da_plan_make(256, 8, 1, 300, 128, 1, 0, 148, "guarded", 0)       # 256 CTAs > 148 SMs
     assert big.grid_x * big.grid_y * big.grid_z <= 148

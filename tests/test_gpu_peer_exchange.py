@@ -74,14 +74,15 @@ def test_peer_exchange_matches_oracle(one_rank_group, batch, h_q, h_kv, l_k, fus
 ])
 def test_forward_peer_every_combine_mode(one_rank_group, batch, h_q, h_kv, l_k, policy, mode, one_kernel):
     # da_forward_peer: the writer of the final rows publishes (slot e & 1, epoch flags), whichever
-    # kernel that is; da_forward_peer_combine (one-wave NONE / CLUSTER plans) also merges the ranks'
-    # partials inside the forward.  Checked against the oracle over several epochs (both slots).
+    # kernel that is; da_forward_peer_combine (static plans) exchanges LL words and merges the ranks'
+    # partials inside that kernel (the forward for NONE / CLUSTER, the combine kernel for workspace
+    # plans).  Checked against the oracle over several epochs (both slots).
     from paper_2604_00028_b200.dist import PeerSeqShardedDecode
     inp = synth.make_inputs(batch, h_q, h_kv, l_k, seed=1610, device="cuda",
                             variant="ragged" if policy == "dynamic" else "normal")
     sd = PeerSeqShardedDecode(batch, h_q, h_kv, l_k, device="cuda", policy=policy, fused=True, one_kernel=one_kernel)
     assert sd.plan.combine_mode == mode
-    assert sd.one_kernel == (one_kernel and mode != 2)
+    assert sd.one_kernel == (one_kernel and policy != "dynamic")   # LL exchange in the final-row kernel
     ref_o, ref_l = OA.decode_attention(*(synth.to_f64(inp[n]) for n in ("q", "k", "v", "seqlens")))
     out = torch.empty((batch, h_q, 128), dtype=torch.float32, device="cuda")
     lse = torch.empty((batch, h_q), dtype=torch.float32, device="cuda")
