@@ -78,8 +78,9 @@ def test_forward_peer_every_combine_mode(one_rank_group, batch, h_q, h_kv, l_k, 
     # partials inside that kernel (the forward for NONE / CLUSTER, the combine kernel for workspace
     # plans).  Checked against the oracle over several epochs (both slots).
     from paper_2604_00028_b200.dist import PeerSeqShardedDecode
+    # ragged lengths everywhere: an empty sequence (lse = -inf partials) and a single-key one
     inp = synth.make_inputs(batch, h_q, h_kv, l_k, seed=1610, device="cuda",
-                            variant="ragged" if policy == "dynamic" else "normal")
+                            variant="ragged" if (policy == "dynamic" or batch >= 2) else "normal")
     sd = PeerSeqShardedDecode(batch, h_q, h_kv, l_k, device="cuda", policy=policy, fused=True, one_kernel=one_kernel)
     assert sd.plan.combine_mode == mode
     assert sd.one_kernel == (one_kernel and policy != "dynamic")   # LL exchange in the final-row kernel
