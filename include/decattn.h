@@ -402,9 +402,9 @@ DA_API da_status da_forward_peer(const da_plan* plan, const void* q, const void*
  *   counter: device uint32 owned by this rank, zero before the first step (left zero after each).
  * The CTAs spin, so the writing grid must be resident (an otherwise idle GPU): NONE / CLUSTER
  * plans whose forward grid is one wave (grid_x * grid_y * grid_z <= usable_sms), or static
- * DA_COMBINE_KERNEL plans with B * H_Q <= 8 usable_sms (workspace, workspace_bytes as da_forward);
- * DA_ERR_UNSUPPORTED otherwise, and for DA_POLICY_DYNAMIC plans with per-sequence split counts
- * (use da_forward_peer + da_combine_peers).
+ * DA_COMBINE_KERNEL plans (static or DA_POLICY_DYNAMIC, whose single-split rows then also pass
+ * through the combine kernel) with B * H_Q <= 8 usable_sms (workspace, workspace_bytes as
+ * da_forward); DA_ERR_UNSUPPORTED otherwise (use da_forward_peer + da_combine_peers).
  * Errors: as da_forward; DA_ERR_INVALID_ARG for world / rank / NULL pointers / a short LL slot,
  * DA_ERR_ALIGNMENT for misaligned offsets, counter, epoch, out or lse.
  */

@@ -137,11 +137,10 @@ def forward_peer(plan: L.da_plan, q, k_cache, v_cache, cache_seqlens, world, ran
 
 def one_kernel_exchange_ok(plan: L.da_plan) -> bool:
     """da_forward_peer_combine's condition: the kernel that writes the final rows can keep its whole
-    grid resident - a NONE / CLUSTER forward of one wave, or the combine kernel of a static
-    workspace plan (one small CTA per row, at most 8 per SM)."""
+    grid resident - a NONE / CLUSTER forward of one wave, or the combine kernel of a workspace plan
+    (one small CTA per row, at most 8 per SM)."""
     if plan.combine_mode == L.DA_COMBINE_KERNEL:
-        dynamic = plan.policy == L.POLICIES["dynamic"] and plan.num_splits > 1
-        return not dynamic and plan.batch * plan.h_q <= 8 * plan.usable_sms
+        return plan.batch * plan.h_q <= 8 * plan.usable_sms
     return plan.grid_x * plan.grid_y * plan.grid_z <= plan.usable_sms
 
 

@@ -197,6 +197,8 @@ da_status forward_impl(const da_plan* plan, const void* q, const void* k_cache, 
   p.dyn_tiles = plan->h_kv * plan->num_m_blocks;
   p.dyn_u = plan->usable_sms;
   p.ws_meta = ws_meta;
+  // LL exchange of a dynamic plan: every row, s_b = 1 included, is finished by the combine kernel
+  p.dyn_via_combine = (pub != nullptr && pub->out != nullptr && dyn) ? 1 : 0;
   if (pub != nullptr && !(pub->out != nullptr && plan->combine_mode == DA_COMBINE_KERNEL)) {
     p.pub = *pub;     // NONE / CLUSTER: every CTA of the forward writes final rows and counts
     p.pub.writers = plan->grid_x * plan->grid_y * plan->grid_z;
@@ -435,8 +437,7 @@ extern "C" da_status da_forward_peer_combine(const da_plan* plan, const void* q,
   // resident - the forward (one CTA per SM: its shared memory) for NONE / CLUSTER plans, the
   // combine kernel (one small CTA per row, many per SM) for static workspace plans
   const int64_t ctas = int64_t(plan->grid_x) * plan->grid_y * plan->grid_z;
-  if (plan->combine_mode == DA_COMBINE_KERNEL ? (is_dynamic(*plan) || rows > 8LL * plan->usable_sms)
-                                              : ctas > plan->usable_sms)
+  if (plan->combine_mode == DA_COMBINE_KERNEL ? rows > 8LL * plan->usable_sms : ctas > plan->usable_sms)
     return DA_ERR_UNSUPPORTED;
   PubParams pub{};
   pub.bases = peer_bases;

@@ -62,10 +62,10 @@ __global__ void __launch_bounds__(kCombineThreads)
     const int b = row / p.h_q, h = row - b * p.h_q;
     prow = static_cast<int64_t>(__ldg(p.meta + b)) * p.h_q + h;
     s = __ldg(p.meta + p.batch + b);
-    if (s == 1) {                      // one split: the forward wrote this row's out / lse itself
+    if (s == 1 && p.pub.out == nullptr) {   // one split: the forward wrote this row's out / lse itself
       if (p.pub.bases != nullptr && threadIdx.x == 0) pub_arrive(p.pub);
       return;
-    }
+    }                                  // (LL exchange: the forward left it in the workspace, merged below)
   }
   DA_DASSERT(row < p.rows && s >= 1);
   const float* lse_in = p.lse_in + prow;

@@ -778,7 +778,7 @@ __global__ void __launch_bounds__(threads_for(NW, helpers_for(kCombine)), 1)
       const float4 v = make_float4(eO[it].x * inv, eO[it].y * inv, eO[it].z * inv, eO[it].w * inv);
       const float lse_v = eL[it] > 0.f ? (eM[it] + lg2(eL[it])) * kLn2 : kNegInf;
       const size_t row = static_cast<size_t>(b) * p.h_q + hq0 + g;
-      if (kCombine == DA_COMBINE_NONE || (kDyn && dyn_single)) {   // kDyn, s_b = 1: the final row
+      if (kCombine == DA_COMBINE_NONE || (kDyn && dyn_single && !p.dyn_via_combine)) {   // kDyn, s_b = 1: the final row
         if constexpr (kPub == 2) {
           pub_ll_store(p.pub, e_pub, row, d4, v, lse_v);
         } else {

@@ -59,6 +59,7 @@ struct FwdParams {
   int32_t dyn_tiles;            // T_b = H_KV * num_m_blocks
   int32_t dyn_u;                // usable SMs U
   int32_t* ws_meta;             // [2, B] int32 (first slot, split count) or nullptr
+  int32_t dyn_via_combine;      // kDyn: s_b = 1 rows also go through the combine kernel (LL exchange)
   PubParams pub;                // fused peer publish (NONE / CLUSTER: this kernel writes the rows)
 };
 

@@ -468,7 +468,7 @@ def test_forward_peer_combine_validation(L):
     ws = L.da_plan_make(1, 8, 1, 4096, 128, 1, 0, 148, "guarded", 0)          # s = 28: workspace combine
     assert ws.combine_mode == L.DA_COMBINE_KERNEL and fwd(ws) == L.DA_ERR_WORKSPACE   # allowed, needs one
     dyn = L.da_plan_make(4, 16, 2, 3000, 128, 1, 0, 148, "dynamic", 0)
-    assert dyn.combine_mode == L.DA_COMBINE_KERNEL and fwd(dyn) == L.DA_ERR_UNSUPPORTED
+    assert dyn.combine_mode == L.DA_COMBINE_KERNEL and fwd(dyn) == L.DA_ERR_WORKSPACE     # allowed, needs one
     big = L.da_plan_make(64, 8, 1, 300, 128, 1, 0, 148, "guarded", 0)         # 64 CTAs... one wave: allowed
     wide = L.da_plan_make(256, 8, 1, 300, 128, 1, 0, 148, "guarded", 0)       # 256 CTAs > 148 SMs
     assert big.grid_x * big.grid_y * big.grid_z <= 148
