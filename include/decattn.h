@@ -387,21 +387,21 @@ DA_API da_status da_forward_peer(const da_plan* plan, const void* q, const void*
 /*
  * da_forward_peer_combine - the whole sequence-sharded step with the exchange inside the kernel
  * that produces the final rows (the forward for NONE / CLUSTER plans: ONE kernel per step; the
- * combine kernel for static workspace plans).  e = *epoch + 1.  Every CTA of that kernel writes
- * its final fp32 rows (o, then lse) into LL slot e & 1 of this rank's
- * exchange buffer as self-validating 8-byte words ((e << 32) | fp32 bits, one system-scope relaxed
+ * combine kernel for workspace plans).  e = *epoch + 1.  Every CTA of that kernel writes its
+ * final fp32 rows (o, then lse) into LL slot e & 1 of this rank's exchange buffer as
+ * self-validating 8-byte words ((e << 32) | fp32 bits, one system-scope relaxed
  * store each: no fence, no flag), then polls the same words of every rank's slot (NVLink loads for
  * peers) until they carry e and LSE-merges (C-comb) the world partials of its rows into out
  * (out_dtype [B, H_Q, d]) and lse (fp32 [B, H_Q], or NULL); the last CTA to have read the epoch
- * (device counter) advances *epoch.  The exchange and the combine fused into the forward
- * (DESIGN.md §6).
+ * (device counter) advances *epoch.  The exchange and the combine fused into the kernel that
+ * finishes the rows.
  *   ll_offset, ll_slot_bytes: the two LL slots (uint64 [B * H_Q][129] each, ll_slot_bytes >=
  *     8 * 129 * B * H_Q, both multiples of 16) inside every rank's exchange buffer (same layout on
  *     every rank, zero before the first step); a rank reuses slot e & 1 at step e + 2 only (the
  *     stream order then guarantees every peer has read it).
  *   counter: device uint32 owned by this rank, zero before the first step (left zero after each).
  * The CTAs spin, so the writing grid must be resident (an otherwise idle GPU): NONE / CLUSTER
- * plans whose forward grid is one wave (grid_x * grid_y * grid_z <= usable_sms), or static
+ * plans whose forward grid is one wave (grid_x * grid_y * grid_z <= usable_sms), or
  * DA_COMBINE_KERNEL plans (static or DA_POLICY_DYNAMIC, whose single-split rows then also pass
  * through the combine kernel) with B * H_Q <= 8 usable_sms (workspace, workspace_bytes as
  * da_forward); DA_ERR_UNSUPPORTED otherwise (use da_forward_peer + da_combine_peers).
