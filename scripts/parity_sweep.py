@@ -1,0 +1,47 @@
+"""Randomised GPU parity sweep against the fp64 oracle (development tool; the pinned cases live in
+tests/test_gpu_parity.py): random (B, H_KV, G, L_K, policy, combine, variant, pack_gqa) draws,
+every output element and lse checked with the test tolerances (DESIGN.md C-amb-14).
+
+    python scripts/parity_sweep.py [n_cases] [seed]
+"""
+import os
+import random
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import torch  # noqa: E402
+
+import paper_2604_00028_b200 as dec  # noqa: E402
+import synth  # noqa: E402
+from oracle import attention as OA  # noqa: E402
+from tests.helpers import assert_lse_close, assert_out_close  # noqa: E402
+
+if __name__ == "__main__":
+    n = int(sys.argv[1]) if len(sys.argv) > 1 else 200
+    rng = random.Random(int(sys.argv[2]) if len(sys.argv) > 2 else 7)
+    fails = 0
+    for i in range(n):
+        hkv = rng.choice([1, 1, 2, 3, 4, 8])
+        G = rng.choice([1, 2, 4, 5, 8, 8, 12, 16, 24, 64])
+        b = rng.choice([1, 1, 2, 3, 5, 8])
+        lk = rng.choice([1, 7, 63, 64, 65, 100, 300, 511, 512, 513, 1000, 2048, 3000, 4097, 6000])
+        policy = rng.choice(["guarded", "seq_aware", "seq_aware_sm", "evolved", "dynamic", "fixed"])
+        forced = rng.randint(1, 40) if policy == "fixed" else 0
+        variant = rng.choice(["normal", "peaked", "ragged"])
+        pack = rng.random() < 0.85
+        l_cap = lk + rng.choice([0, 0, 64, 129])
+        try:
+            inp = synth.make_inputs(b, G * hkv, hkv, lk, l_cap=l_cap, seed=5000 + i, variant=variant, device="cuda")
+            plan = dec.make_plan(b, G * hkv, hkv, lk, pack_gqa=pack, policy=policy, forced_splits=forced)
+            out, lse = dec.forward(plan, inp["q"], inp["k"], inp["v"], inp["seqlens"],
+                                   out_dtype=rng.choice([torch.bfloat16, torch.float32]))
+            torch.cuda.synchronize()
+            ref_o, ref_l = OA.decode_attention(*(synth.to_f64(inp[k]) for k in ("q", "k", "v", "seqlens")))
+            assert_out_close(synth.to_f64(out), ref_o)
+            assert_lse_close(synth.to_f64(lse), ref_l)
+        except Exception as e:   # noqa: BLE001 - report and continue the sweep
+            fails += 1
+            print(f"FAIL case {i}: B={b} H_KV={hkv} G={G} L={lk} cap={l_cap} {policy} s={forced} {variant} "
+                  f"pack={pack}: {e}", flush=True)
+    print(f"{n} cases, {fails} failures", flush=True)
