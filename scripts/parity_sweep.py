@@ -34,8 +34,22 @@ if __name__ == "__main__":
         try:
             inp = synth.make_inputs(b, G * hkv, hkv, lk, l_cap=l_cap, seed=5000 + i, variant=variant, device="cuda")
             plan = dec.make_plan(b, G * hkv, hkv, lk, pack_gqa=pack, policy=policy, forced_splits=forced)
-            out, lse = dec.forward(plan, inp["q"], inp["k"], inp["v"], inp["seqlens"],
-                                   out_dtype=rng.choice([torch.bfloat16, torch.float32]))
+            odt = rng.choice([torch.bfloat16, torch.float32])
+            if rng.random() < 0.25 and policy != "dynamic":   # paged: the same cache in a shuffled page pool
+                ps = rng.choice([64, 128, 256])
+                npg = -(-l_cap // ps)
+                k = torch.zeros((b, npg * ps, hkv, 128), dtype=torch.bfloat16, device="cuda")
+                v = torch.zeros_like(k)
+                k[:, :l_cap], v[:, :l_cap] = inp["k"], inp["v"]
+                perm = torch.randperm(b * npg, device="cuda")
+                kp = torch.empty((b * npg, ps, hkv, 128), dtype=torch.bfloat16, device="cuda")
+                vp = torch.empty_like(kp)
+                kp[perm] = k.reshape(b * npg, ps, hkv, 128)
+                vp[perm] = v.reshape(b * npg, ps, hkv, 128)
+                table = perm.view(b, npg).to(torch.int32).contiguous()
+                out, lse = dec.forward_paged(plan, inp["q"], kp, vp, table, inp["seqlens"], out_dtype=odt)
+            else:
+                out, lse = dec.forward(plan, inp["q"], inp["k"], inp["v"], inp["seqlens"], out_dtype=odt)
             torch.cuda.synchronize()
             ref_o, ref_l = OA.decode_attention(*(synth.to_f64(inp[k]) for k in ("q", "k", "v", "seqlens")))
             assert_out_close(synth.to_f64(out), ref_o)
