@@ -342,10 +342,26 @@ def cpu_baseline(cfg, budget_s=10.0):
             break
     step_s = dt / n
     b = alg_bytes(scfg["batch"], scfg["h_q"], scfg["h_kv"], scfg["l_k"])
+    # the same oracle with its BLAS limited to one thread (all cores plus a 1-thread
+    # figure), on a shorter budget
+    single = None
+    try:
+        from threadpoolctl import threadpool_limits
+        with threadpool_limits(limits=1):
+            n1, t1 = 0, time.perf_counter()
+            while True:
+                OA.decode_attention(q, k, v, s)
+                n1 += 1
+                d1 = time.perf_counter() - t1
+                if d1 >= max(0.5, budget_s / 5) or n1 >= 100000:
+                    break
+        single = round(b / (d1 / n1) / 1e9, 6)
+    except Exception:
+        pass
     what = "full steps of the workload" if scfg == cfg else f"sample steps (batch {scfg['batch']}, L_K {scfg['l_k']})"
     return {"value": round(b / step_s / 1e9, 6), "unit": "GB/s", "cores": int(cores), "kind": "oracle",
             "sample": f"{n} {what} in {dt:.1f} s (fp64 NumPy oracle.attention.decode_attention)",
-            "ms_per_step": round(step_s * 1e3, 4),
+            "ms_per_step": round(step_s * 1e3, 4), "single_thread_value": single,
             "host_cpus": len(os.sched_getaffinity(0))}
 
 
