@@ -8,29 +8,31 @@ One JSON line on rank 0.  A *step* is one pass of the whole hot path (SURVEY
 scheduler metadata the paper measures with) and one da_forward call,
 i.e. the split-KV kernel plus the LSE combine when s > 1.
 
-Headline (N = 1): BASELINE.json configs[1], Llama-3.1-70B decode B=1 H_Q=64
-H_KV=8 d=128 L_K=512 bf16, under the SM-count-aware sequence-aware policy
-(DESIGN.md C-ext-1; --policy seq_aware selects the paper's literal Fig. 3 rule,
-which leaves this T = 8 shape at s = 1 via Guard 2).  ``value`` = aggregate
-algorithmic HBM GB/s over all ranks (K+V+q+out+lse bytes / step time), with
-inputs resident in HBM; ``us_per_step`` the same measurement as time.  Timing:
-W eager warm-up steps, then K steps captured in ONE CUDA graph ("CUDA
-Graph replay") and timed with CUDA events between barrier + synchronize; the
-max over ranks is reported.  L2: every step reads a different KV buffer of a
-rotation totalling > 2x L2, and L2 is scrubbed (256 MB write) before each
-timed replay.
+Headline (N = 1): the largest single-GPU BASELINE.json config, high-load (configs[3]: B=128
+H_Q=64 H_KV=8 d=128 L_K=8192 bf16, 4.3 GB of KV per step), the HBM-bound step whose roofline
+fraction is the measure of the kernel.  ``--workload`` selects another config (llama70b =
+configs[1], Llama-3.1-70B decode B=1 L_K=512, latency-bound; long_context = configs[4]).
+``--policy`` picks the split policy (default: the SM-count-aware sequence-aware policy,
+DESIGN.md C-ext-1; ``seq_aware`` = the paper's literal Fig. 3 rule; high-load is saturated, so
+every policy gives s = 1 there).  ``value`` = aggregate algorithmic HBM GB/s over all ranks
+(K+V+q+out+lse bytes / step time), inputs resident in HBM; ``us_per_step`` the same as time.
+Timing: W eager warm-up steps, then K steps captured in ONE CUDA graph ("CUDA Graph
+replay") and timed with CUDA events between barrier + synchronize; a GPU-side sleep is queued
+before the start event so the host's graph submission is never inside the timed region; the
+max over ranks is reported.  L2: inputs larger than L2 (high-load, long-context) or a rotation
+of KV buffers totalling > 2x L2, and L2 is scrubbed (256 MB write) before each timed replay.
 
-N > 1: weak scaling by batch (rank r runs its own B=1 sequence: global batch =
-N, "shards by batch x KV-head"); no collective on the data path.
-``--workload long_context`` with N > 1 shards the sequence instead (one NCCL
-all-gather + the combine kernel per step; strong scaling).
+N > 1: high-load shards the B = 128 batch across the ranks (strong scaling, no collective:
+SURVEY §8(e) "shards by batch x KV-head"); ``--workload long_context`` shards the sequence
+(fp32 shard partials merged across ranks, over peer memory by default or ``--exchange nccl``:
+NCCL all-gather + the combine kernel); latency workloads run one replica per rank (weak).
 
-Extras (N = 1): guarded-vs-seq-aware A/B (interleaved graph replays, medians)
-on the headline, on its 8-way tensor-parallel slice (H_Q=8, H_KV=1)
-where the policies differ (s = 1 vs 3), and the KV-streaming-bound configs
-(high-load B=128 L_K=8192; long-context L_K=131072) with their roofline
-fractions.  ``--impl reference`` times the fp64 CPU oracle instead (the
-reference arm of this tier; rank 0 only).
+Extras (N = 1): the policy A/B (guarded / the paper's seq-aware / SM-count-aware / evolved,
+interleaved graph replays in random order per round, medians) on Llama-70B and its 8-way
+tensor-parallel slice (H_Q=8, H_KV=1) where the paper's rule differs (s = 1 vs 3), the
+isolated-step latency of those (one step per launch, no overlap with a preceding step), the
+KV-streaming configs with their roofline fractions, and a ragged batch.  ``--impl reference``
+times the fp64 CPU oracle instead (the reference arm of this tier; rank 0 only).
 """
 
 from __future__ import annotations
@@ -38,6 +40,7 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import random
 import statistics
 import subprocess
 import sys
@@ -200,6 +203,16 @@ def make_graph(dec, plan, w: Workload, steps: int, stream):
     return g
 
 
+# GPU-side sleep queued before a start event (~0.5 ms at 1.9 GHz): the stream is still busy when the
+# host has submitted the graph, so the host's submission latency never falls inside the timed region
+GUARD_CYCLES = 1_000_000
+
+
+def guard(stream):
+    with torch.cuda.stream(stream):
+        torch.cuda._sleep(GUARD_CYCLES)
+
+
 class Timer:
     def __init__(self, device):
         self.scrub = torch.empty(256 << 20, dtype=torch.uint8, device=device)
@@ -208,6 +221,7 @@ class Timer:
         if scrub:
             with torch.cuda.stream(stream):
                 self.scrub.fill_(1)
+        guard(stream)
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         with torch.cuda.stream(stream):
@@ -231,8 +245,11 @@ def ab_compare(dec, dev, stream, timer, cfg, steps, rounds, l2, seed, num_sms):
         plan = dec.make_plan(cfg["batch"], cfg["h_q"], cfg["h_kv"], cfg["l_k"], policy=pol)
         graphs[pol] = (plan, make_graph(dec, plan, w, steps, stream))
         res[pol] = []
+    rng = random.Random(seed)
     for _ in range(rounds):
-        for pol in AB_POLICIES:
+        order = list(AB_POLICIES)
+        rng.shuffle(order)                       # no arm always follows another (order bias)
+        for pol in order:
             res[pol].append(timer.time_replay(graphs[pol][1], stream) * 1e3 / steps)
     out = {}
     for pol in AB_POLICIES:
@@ -244,9 +261,10 @@ def ab_compare(dec, dev, stream, timer, cfg, steps, rounds, l2, seed, num_sms):
                     "us_per_step": round(us, 3), "p10_us": round(sorted(res[pol])[len(res[pol]) // 10], 3),
                     "p90_us": round(sorted(res[pol])[(9 * len(res[pol])) // 10], 3),
                     "gbs": round(w.bytes / (us * 1e-6) / 1e9, 1)}
-    out["speedup_seq_aware_vs_guarded"] = round(out["guarded"]["us_per_step"] / out["seq_aware"]["us_per_step"], 4)
-    out["speedup_seq_aware_sm_vs_guarded"] = round(out["guarded"]["us_per_step"] / out["seq_aware_sm"]["us_per_step"], 4)
-    out["speedup_evolved_vs_guarded"] = round(out["guarded"]["us_per_step"] / out["evolved"]["us_per_step"], 4)
+    for pol in AB_POLICIES[1:]:
+        # median of the per-round paired ratios (guarded time / policy time of the same round)
+        out[f"speedup_{pol}_vs_guarded"] = round(statistics.median(
+            g / t for g, t in zip(res["guarded"], res[pol])), 4)
     out["config"] = dict(cfg, head_dim=HEAD_DIM)
     out["l2"] = w.l2_note(l2)
     del w, graphs
@@ -254,14 +272,14 @@ def ab_compare(dec, dev, stream, timer, cfg, steps, rounds, l2, seed, num_sms):
     return out
 
 
-def streaming_roofline(dec, dev, stream, timer, cfg, steps, rounds, l2, seed, peak):
+def streaming_roofline(dec, dev, stream, timer, cfg, steps, rounds, l2, seed, peak, policy="seq_aware"):
     w = Workload(cfg, dev, seed, l2)
-    plan = dec.make_plan(cfg["batch"], cfg["h_q"], cfg["h_kv"], cfg["l_k"], policy="seq_aware")
+    plan = dec.make_plan(cfg["batch"], cfg["h_q"], cfg["h_kv"], cfg["l_k"], policy=policy)
     g = make_graph(dec, plan, w, steps, stream)
     ts = [timer.time_replay(g, stream) * 1e3 / steps for _ in range(rounds)]
     us = statistics.median(ts)
     gbs = w.bytes / (us * 1e-6) / 1e9
-    r = {"config": dict(cfg, head_dim=HEAD_DIM), "num_splits": plan.num_splits,
+    r = {"config": dict(cfg, head_dim=HEAD_DIM), "policy": policy, "num_splits": plan.num_splits,
          "combine_mode": plan.combine_mode, "us_per_step": round(us, 2), "achieved_gbs": round(gbs, 1),
          "frac_of_measured_peak": round(gbs / peak, 4), "frac_of_8tbs_nominal": round(gbs / 8000.0, 4),
          "bytes_per_step": w.bytes, "l2": w.l2_note(l2)}
@@ -271,6 +289,56 @@ def streaming_roofline(dec, dev, stream, timer, cfg, steps, rounds, l2, seed, pe
 
 
 RAGGED_AB = dict(batch=16, h_q=64, h_kv=8, l_k=32768)   # one 32768-token sequence + fifteen of 1024
+
+
+def isolated_latency(dec, dev, stream, timer, cfg, steps, rounds, l2, seed, policies=("guarded", "seq_aware", "seq_aware_sm")):
+    """The step's latency when it cannot overlap a preceding step (the paper times "pure kernel
+    execution times"): K steps captured as [separator, step] pairs, where the separator is a
+    1-element torch fill that does not trigger programmatic dependent launch, so each step's launch,
+    prologue and L2 prefetch start only after the previous step has finished; minus a graph of the K
+    separators alone.  Interleaved per round in random order (the separator graph included), medians."""
+    w = Workload(cfg, dev, seed, l2)
+    sep_buf = torch.zeros(1, dtype=torch.int32, device=dev)
+
+    def capture(plan):
+        ws = dec.workspace_for(plan, dev) if plan is not None else None
+        def body(i):
+            sep_buf.fill_(i)
+            if plan is not None:
+                j = i % w.nbuf
+                dec.forward(plan, w.q, w.k[j], w.v[j], w.seqlens, out=w.out, lse=w.lse, workspace=ws)
+        with torch.cuda.stream(stream):
+            for i in range(3):
+                body(i)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=stream):
+            for i in range(steps):
+                body(i)
+        return g
+
+    plans = {p: dec.make_plan(cfg["batch"], cfg["h_q"], cfg["h_kv"], cfg["l_k"], policy=p) for p in policies}
+    graphs = {p: capture(plans[p]) for p in policies}
+    graphs["_sep"] = capture(None)
+    res = {k: [] for k in graphs}
+    rng = random.Random(seed)
+    for _ in range(rounds):
+        order = list(graphs)
+        rng.shuffle(order)
+        for k in order:
+            res[k].append(timer.time_replay(graphs[k], stream) * 1e3 / steps)
+    sep = statistics.median(res["_sep"])
+    out = {"config": dict(cfg, head_dim=HEAD_DIM), "separator_us": round(sep, 3)}
+    for p in policies:
+        out[p] = {"num_splits": plans[p].num_splits, "combine_mode": plans[p].combine_mode,
+                  "us_per_step": round(statistics.median(res[p]) - sep, 3)}
+    for p in policies[1:]:
+        out[f"speedup_{p}_vs_guarded"] = round(out[policies[0]]["us_per_step"] / out[p]["us_per_step"], 4)
+    out["note"] = ("one step per launch chain: [1-element fill, step] x K minus [fill] x K; no step overlaps "
+                   "the previous one (no PDL early launch, no pre-wait prefetch under the previous step)")
+    del w, graphs
+    torch.cuda.empty_cache()
+    return out
 
 
 def latency_floor(dec, dev, stream, timer, cfg, steps, rounds, l2, seed, us_headline):
@@ -463,7 +531,8 @@ def main():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="llama70b")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="high_load",
+                    help="BASELINE.json config (default: high_load, the largest single-GPU config)")
     ap.add_argument("--no-extras", action="store_true", help="skip the A/B and streaming extras")
     ap.add_argument("--ab-rounds", type=int, default=21)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
@@ -475,8 +544,9 @@ def main():
                          "across the ranks - the tensor-parallel mapping, e.g. Llama-70B over 8 GPUs = the TP-8 "
                          "slice per rank; strong scaling, no collective")
     ap.add_argument("--exchange", default="p2p", choices=["nccl", "p2p", "p2p-split"],
-                    help="long_context with N > 1: the exchange over peer memory (default: da_peer_signal + "
-                         "da_combine_peers over torch symmetric memory) or an NCCL all-gather + da_combine")
+                    help="long_context with N > 1: the exchange over peer memory (default: one kernel per step, "
+                         "LL words over torch symmetric memory with a bounded wait), p2p-split (da_peer_signal + "
+                         "da_combine_peers) or nccl (all-gather + da_combine)")
     ap.add_argument("--policy", default="seq_aware_sm",
                     choices=["seq_aware_sm", "seq_aware", "guarded", "evolved"],
                     help="split policy of the headline step (default: the SM-count-aware sequence-aware "
@@ -624,6 +694,7 @@ def main():
         torch.cuda.synchronize()
         barrier()
         torch.cuda.synchronize()
+        guard(stream)                            # GPU busy while the host submits the graph
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         with torch.cuda.stream(stream):
             e0.record(stream)
@@ -638,32 +709,47 @@ def main():
             with torch.cuda.stream(stream):
                 g.replay()
             torch.cuda.synchronize()
+    if long_sharded and hasattr(sd, "check"):
+        sd.check()                               # raises if an exchange wait ran past its bound
     ms_max = max_over_ranks(ms)
     us_per_step = ms_max * 1e3 / args.steps
     value = step_bytes_total * args.steps / (ms_max * 1e-3) / 1e9
 
     # ---- end to end through the public API with host buffers ----
-    e2e_ms, h2d, d2h = e2e_measure(dec, L, local_cfg, dev, stream, args.steps, args.warmup, args.policy, depth=2)
-    e2e_serial_ms, _, _ = e2e_measure(dec, L, local_cfg, dev, stream, args.steps, args.warmup, args.policy, depth=1)
+    # (a step that moves > 64 MB over PCIe - high-load's 4.3 GB of K/V - is timed over at most 10 steps)
+    e2e_steps = args.steps if alg_bytes(**local_cfg) < (64 << 20) else max(3, min(args.steps, 10))
+    e2e_ms, h2d, d2h = e2e_measure(dec, L, local_cfg, dev, stream, e2e_steps, args.warmup, args.policy, depth=2)
+    e2e_serial_ms, _, _ = e2e_measure(dec, L, local_cfg, dev, stream, e2e_steps, args.warmup, args.policy, depth=1)
     e2e_ms_max = max_over_ranks(e2e_ms)
     e2e_serial_max = max_over_ranks(e2e_serial_ms)
-    e2e_scale = alg_bytes(**local_cfg) * (world if not long_sharded else 1) * args.steps / 1e9
+    e2e_scale = alg_bytes(**local_cfg) * (world if not long_sharded else 1) * e2e_steps / 1e9
     e2e_value = e2e_scale / (e2e_ms_max * 1e-3)
 
     extras = {}
     if rank == 0 and world == 1 and not args.no_extras:
+        lat_steps = 200
         extras["policy_ab"] = {
-            "llama70b": ab_compare(dec, dev, stream, timer, WORKLOADS["llama70b"], args.steps, args.ab_rounds, l2, 1001, num_sms),
-            "llama70b_tp8_slice": ab_compare(dec, dev, stream, timer, WORKLOADS["llama70b_tp8"], args.steps, args.ab_rounds, l2, 1002, num_sms),
+            "llama70b": ab_compare(dec, dev, stream, timer, WORKLOADS["llama70b"], lat_steps, args.ab_rounds, l2, 1001, num_sms),
+            "llama70b_tp8_slice": ab_compare(dec, dev, stream, timer, WORKLOADS["llama70b_tp8"], lat_steps, args.ab_rounds, l2, 1002, num_sms),
+        }
+        # the paper's headline claim on this box: its literal rule (Fig. 3) vs guarded on the TP-8 slice,
+        # where they differ (s = 1 -> 3); the target is >= 1.20x
+        extras["paper_rule_tp8_speedup"] = extras["policy_ab"]["llama70b_tp8_slice"]["speedup_seq_aware_vs_guarded"]
+        extras["isolated_latency"] = {
+            "llama70b": isolated_latency(dec, dev, stream, timer, WORKLOADS["llama70b"], lat_steps, args.ab_rounds, l2, 1007),
+            "llama70b_tp8_slice": isolated_latency(dec, dev, stream, timer, WORKLOADS["llama70b_tp8"], lat_steps, args.ab_rounds, l2, 1008),
         }
         extras["roofline_streaming"] = {
-            "high_load": streaming_roofline(dec, dev, stream, timer, WORKLOADS["high_load"], 5, 5, l2, 1003, peak),
             "long_context": streaming_roofline(dec, dev, stream, timer, WORKLOADS["long_context"], 20, 7, l2, 1004, peak),
+            "long_context_seq_aware_sm": streaming_roofline(dec, dev, stream, timer, WORKLOADS["long_context"], 20, 7, l2,
+                                                            1004, peak, policy="seq_aware_sm"),
         }
+        if args.workload != "high_load":
+            extras["roofline_streaming"]["high_load"] = streaming_roofline(dec, dev, stream, timer, WORKLOADS["high_load"],
+                                                                           5, 5, l2, 1003, peak)
         extras["ragged_ab"] = ragged_ab(dec, dev, stream, timer, 20, 7, l2, 1005)
-        if args.workload in ("llama70b", "llama70b_tp8", "mqa_tiny"):
-            extras["latency_floor"] = latency_floor(dec, dev, stream, timer, local_cfg, args.steps, 11, l2, 1006,
-                                                    ms * 1e3 / args.steps)
+        extras["latency_floor"] = latency_floor(dec, dev, stream, timer, WORKLOADS["llama70b"], lat_steps, 11, l2, 1006,
+                                                extras["policy_ab"]["llama70b"]["seq_aware_sm"]["us_per_step"])
     if world > 1:
         barrier()
     if rank != 0:
@@ -696,12 +782,14 @@ def main():
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "traffic": trec.get("dram_bytes_per_launch") if trec else None,
                      "kernel": "split_kv_fwd_kernel", "peak_source": peak_src,
-                     "note": ("latency-bound config (2.1 MB per step); see roofline_streaming for the HBM-bound configs"
+                     "note": (f"latency-bound config ({alg_bytes(**local_cfg) / 1e6:.2f} MB per step); see "
+                              "roofline_streaming for the HBM-bound configs"
                               if alg_bytes(**local_cfg) < (64 << 20) else
-                              "HBM-bound config; achieved = algorithmic bytes of the step / step time")},
+                              f"HBM-bound config ({alg_bytes(**local_cfg) / 1e9:.3f} GB per step, one launch per step "
+                              "when s = 1); achieved = algorithmic bytes of the step / step time")},
         "cpu_baseline": cpu_baseline(local_cfg, args.cpu_seconds) if world == 1 else None,
         "e2e": {"value": round(e2e_value, 3), "unit": "GB/s", "h2d_bytes_per_step": h2d,
-                "d2h_bytes_per_step": d2h, "ms_per_step": round(e2e_ms_max / args.steps, 6),
+                "d2h_bytes_per_step": d2h, "ms_per_step": round(e2e_ms_max / e2e_steps, 6), "steps": e2e_steps,
                 "pipeline_depth": 2, "serial_value": round(e2e_scale / (e2e_serial_max * 1e-3), 3),
                 "note": "da_forward_host per step (H2D of q/K/V from pinned memory, forward, D2H of out/lse); "
                         "value: two steps in flight on two streams, serial_value: one stream"},

@@ -45,7 +45,7 @@
 extern "C" {
 #endif
 
-#define DA_ABI_VERSION 5
+#define DA_ABI_VERSION 6
 
 #if defined(__GNUC__)
 #define DA_API __attribute__((visibility("default")))
@@ -66,7 +66,10 @@ typedef enum da_status {
                               that is not a multiple of 8 elements */
   DA_ERR_WORKSPACE = 4,    /* combine_mode == DA_COMBINE_KERNEL and the
                               workspace is missing or too small */
-  DA_ERR_CUDA = 5          /* a CUDA runtime / driver call failed */
+  DA_ERR_CUDA = 5,         /* a CUDA runtime / driver call failed */
+  DA_ERR_TIMEOUT = 6       /* a cross-GPU exchange wait ran past its bound (the device status
+                              word of da_combine_peers / da_forward_peer_combine; never returned
+                              by a call itself) */
 } da_status;
 
 /* Split policies (P:L34-39 knobs; decision functions SURVEY §8(c) C-pol). */
@@ -350,8 +353,13 @@ DA_API da_status da_combine(int32_t num_splits, int32_t batch, int32_t h_q, int3
  * A rank overwrites slot e & 1 again only at step e + 2, after every peer has signalled step e + 1,
  * i.e. finished combining step e.  The flags carry monotonic epochs, so both calls can be captured
  * in a CUDA graph and replayed.
- * Errors: DA_ERR_INVALID_ARG (world not in [1, 64], rank, NULL pointers, overlapping regions),
- * DA_ERR_UNSUPPORTED (head_dim != 128), DA_ERR_ALIGNMENT, DA_ERR_CUDA.
+ * Bounded wait: a flag still below *epoch timeout_ns after the first failed poll (<= 0: 10 s) ends
+ * the wait; the CTA stores DA_ERR_TIMEOUT into *status (device int32 owned by the caller, zero
+ * before the step; it is never cleared by the library) and merges what the slots hold, so the
+ * kernel completes and the caller reads the failure from *status instead of hanging on a peer that
+ * is late, crashed or out of step.
+ * Errors: DA_ERR_INVALID_ARG (world not in [1, 64], rank, NULL pointers incl. status, overlapping
+ * regions), DA_ERR_UNSUPPORTED (head_dim != 128), DA_ERR_ALIGNMENT, DA_ERR_CUDA.
  */
 DA_API da_status da_peer_signal(int32_t world, int32_t rank, const uint64_t* peer_bases, const float* o_local,
                                 const float* lse_local, int32_t batch, int32_t h_q, int32_t head_dim,
@@ -360,7 +368,7 @@ DA_API da_status da_peer_signal(int32_t world, int32_t rank, const uint64_t* pee
 DA_API da_status da_combine_peers(int32_t world, int32_t rank, const uint64_t* peer_bases, int64_t slot_bytes,
                                   int64_t lse_offset, int64_t flag_offset, const int32_t* epoch, int32_t batch,
                                   int32_t h_q, int32_t head_dim, int32_t out_dtype, void* out, float* lse,
-                                  void* cuda_stream);
+                                  int32_t* status, int64_t timeout_ns, void* cuda_stream);
 
 /*
  * da_forward_peer - da_forward (out_dtype = DA_F32) and da_peer_signal in one: the kernel that
@@ -400,21 +408,42 @@ DA_API da_status da_forward_peer(const da_plan* plan, const void* q, const void*
  *     every rank, zero before the first step); a rank reuses slot e & 1 at step e + 2 only (the
  *     stream order then guarantees every peer has read it).
  *   counter: device uint32 owned by this rank, zero before the first step (left zero after each).
- * The CTAs spin, so the writing grid must be resident (an otherwise idle GPU): NONE / CLUSTER
- * plans whose forward grid is one wave (grid_x * grid_y * grid_z <= usable_sms), or
- * DA_COMBINE_KERNEL plans (static or DA_POLICY_DYNAMIC, whose single-split rows then also pass
- * through the combine kernel) with B * H_Q <= 8 usable_sms (workspace, workspace_bytes as
+ * The CTAs spin, so the writing grid must be resident at once on an otherwise idle GPU, which the
+ * call checks against the device's own occupancy answer for the exact kernel (da_query_residency,
+ * scaled by usable_sms / SM count): NONE plans with grid_x * grid_y * grid_z CTAs, CLUSTER plans
+ * with grid_y * grid_z clusters of num_splits CTAs (cluster placement is GPC-bound: not SMs / s),
+ * or DA_COMBINE_KERNEL plans (static or DA_POLICY_DYNAMIC, whose single-split rows then also pass
+ * through the combine kernel) with B * H_Q combine CTAs (workspace, workspace_bytes as
  * da_forward); DA_ERR_UNSUPPORTED otherwise (use da_forward_peer + da_combine_peers).
+ * status, timeout_ns: the bounded wait of da_combine_peers, for the LL words.
  * Errors: as da_forward; DA_ERR_INVALID_ARG for world / rank / NULL pointers / a short LL slot,
- * DA_ERR_ALIGNMENT for misaligned offsets, counter, epoch, out or lse.
+ * DA_ERR_ALIGNMENT for misaligned offsets, counter, epoch, status, out or lse; DA_ERR_CUDA when the
+ * occupancy query fails.
  */
 DA_API da_status da_forward_peer_combine(const da_plan* plan, const void* q, const void* k_cache,
                                          const void* v_cache, int32_t l_cap, const int32_t* cache_seqlens,
                                          const int64_t* strides, float softmax_scale, int32_t world,
                                          int32_t rank, const uint64_t* peer_bases, int64_t ll_offset,
                                          int64_t ll_slot_bytes, int32_t* epoch, uint32_t* counter,
-                                         int32_t out_dtype, void* out, float* lse, void* workspace,
-                                         int64_t workspace_bytes, void* cuda_stream);
+                                         int32_t out_dtype, void* out, float* lse, int32_t* status,
+                                         int64_t timeout_ns, void* workspace, int64_t workspace_bytes,
+                                         void* cuda_stream);
+
+/*
+ * da_query_residency - how many launch units of the kernel a plan launches can be resident on the
+ * CURRENT device at once, as the CUDA occupancy API answers for the exact instantiation (its
+ * threads, registers and shared memory): the measurement behind the planner's cluster-fit table
+ * (config.h kMaxActiveClustersB200) and the residency guard of
+ * da_forward_peer_combine.
+ *   kernel 0: the split-KV forward of the plan (exchange 0 = da_forward, 1 = da_forward_peer,
+ *             2 = da_forward_peer_combine): clusters of num_splits CTAs for a DA_COMBINE_CLUSTER
+ *             plan (cudaOccupancyMaxActiveClusters), CTAs otherwise;
+ *   kernel 1: the LSE combine kernel: CTAs (the plan is only validated).
+ * *out: the count for the whole device (all SMs, sm_margin not applied).
+ * Errors: DA_ERR_INVALID_ARG (NULL, inconsistent plan, kernel / exchange out of range),
+ * DA_ERR_CUDA (no device, or the query failed).
+ */
+DA_API da_status da_query_residency(const da_plan* plan, int32_t kernel, int32_t exchange, int32_t* out);
 
 /* Static, NUL-terminated description of a status code (never NULL). */
 DA_API const char* da_status_string(int32_t status);

@@ -19,7 +19,7 @@ PKG_DIR = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("DECATTN_LIB") or os.path.join(PKG_DIR, "lib", "libdecattn.so")
 
 # ---- constants mirrored from include/decattn.h ----------------------------
-DA_OK, DA_ERR_INVALID_ARG, DA_ERR_UNSUPPORTED, DA_ERR_ALIGNMENT, DA_ERR_WORKSPACE, DA_ERR_CUDA = range(6)
+DA_OK, DA_ERR_INVALID_ARG, DA_ERR_UNSUPPORTED, DA_ERR_ALIGNMENT, DA_ERR_WORKSPACE, DA_ERR_CUDA, DA_ERR_TIMEOUT = range(7)
 (DA_POLICY_GUARDED, DA_POLICY_SEQ_AWARE, DA_POLICY_FIXED, DA_POLICY_EVOLVED, DA_POLICY_SEQ_AWARE_SM,
  DA_POLICY_DYNAMIC) = range(6)
 (DA_RULE_SATURATED, DA_RULE_GUARD_NBLK4, DA_RULE_GUARD1, DA_RULE_GUARD2, DA_RULE_LOW_TILE,
@@ -28,7 +28,7 @@ DA_OK, DA_ERR_INVALID_ARG, DA_ERR_UNSUPPORTED, DA_ERR_ALIGNMENT, DA_ERR_WORKSPAC
 DA_BF16, DA_F32 = 0, 1
 DA_COMBINE_NONE, DA_COMBINE_CLUSTER, DA_COMBINE_KERNEL = range(3)
 DA_PATH_SCALAR, DA_PATH_MMA = 0, 1
-DA_ABI_VERSION = 5
+DA_ABI_VERSION = 6
 
 POLICIES = {"guarded": DA_POLICY_GUARDED, "seq_aware": DA_POLICY_SEQ_AWARE, "fixed": DA_POLICY_FIXED,
             "evolved": DA_POLICY_EVOLVED, "seq_aware_sm": DA_POLICY_SEQ_AWARE_SM, "dynamic": DA_POLICY_DYNAMIC}
@@ -85,14 +85,16 @@ def _load() -> ctypes.CDLL:
     lib.da_forward_host.restype = i32
     lib.da_peer_signal.argtypes = [i32, i32, vp, vp, vp, i32, i32, i32, i64, i64, i64, vp, vp]
     lib.da_peer_signal.restype = i32
-    lib.da_combine_peers.argtypes = [i32, i32, vp, i64, i64, i64, vp, i32, i32, i32, i32, vp, vp, vp]
+    lib.da_combine_peers.argtypes = [i32, i32, vp, i64, i64, i64, vp, i32, i32, i32, i32, vp, vp, vp, i64, vp]
     lib.da_combine_peers.restype = i32
     lib.da_forward_peer.argtypes = [ctypes.POINTER(da_plan), vp, vp, vp, i32, vp, vp, f32, i32, i32, vp, i64, i64,
                                     i64, vp, vp, vp, i64, vp]
     lib.da_forward_peer.restype = i32
     lib.da_forward_peer_combine.argtypes = [ctypes.POINTER(da_plan), vp, vp, vp, i32, vp, vp, f32, i32, i32, vp,
-                                            i64, i64, vp, vp, i32, vp, vp, vp, i64, vp]
+                                            i64, i64, vp, vp, i32, vp, vp, vp, i64, vp, i64, vp]
     lib.da_forward_peer_combine.restype = i32
+    lib.da_query_residency.argtypes = [ctypes.POINTER(da_plan), i32, i32, ctypes.POINTER(i32)]
+    lib.da_query_residency.restype = i32
     lib.da_combine.argtypes = [i32, i32, i32, i32, vp, i64, vp, i64, i32, vp, vp, vp]
     lib.da_combine.restype = i32
     lib.da_status_string.argtypes = [i32]
@@ -108,7 +110,8 @@ LIB = _load()
 
 EXPORTED = ("da_plan_make", "da_plan_make_varlen", "da_plan_set_combine", "da_forward", "da_forward_paged",
             "da_forward_host_bytes", "da_forward_host", "da_combine", "da_peer_signal", "da_combine_peers",
-            "da_forward_peer", "da_forward_peer_combine", "da_status_string", "da_abi_version")
+            "da_forward_peer", "da_forward_peer_combine", "da_query_residency", "da_status_string",
+            "da_abi_version")
 
 
 def da_status_string(status: int) -> str:
@@ -227,10 +230,10 @@ def da_peer_signal(world, rank, peer_bases, o_local, lse_local, batch, h_q, head
 
 
 def da_combine_peers(world, rank, peer_bases, slot_bytes, lse_offset, flag_offset, epoch, batch, h_q, head_dim,
-                     out_dtype, out, lse, stream=None) -> None:
+                     out_dtype, out, lse, status, timeout_ns=0, stream=None) -> None:
     st = LIB.da_combine_peers(int(world), int(rank), _ptr(peer_bases), int(slot_bytes), int(lse_offset),
                               int(flag_offset), _ptr(epoch), int(batch), int(h_q), int(head_dim), int(out_dtype),
-                              _ptr(out), _ptr(lse), _stream_handle(stream))
+                              _ptr(out), _ptr(lse), _ptr(status), int(timeout_ns), _stream_handle(stream))
     if st != DA_OK:
         raise DecAttnError(st, "da_combine_peers")
 
@@ -251,17 +254,27 @@ def da_forward_peer(plan: da_plan, q, k_cache, v_cache, l_cap, cache_seqlens, st
 
 def da_forward_peer_combine(plan: da_plan, q, k_cache, v_cache, l_cap, cache_seqlens, strides, softmax_scale, world,
                             rank, peer_bases, ll_offset, ll_slot_bytes, epoch, counter, out_dtype, out, lse,
-                            workspace=None, workspace_bytes=0, stream=None) -> None:
+                            status, timeout_ns=0, workspace=None, workspace_bytes=0, stream=None) -> None:
     sarr = None
     if strides is not None:
         sarr = (ctypes.c_int64 * 8)(*[int(x) for x in strides])
     st = LIB.da_forward_peer_combine(ctypes.byref(plan), _ptr(q), _ptr(k_cache), _ptr(v_cache), int(l_cap),
                                      _ptr(cache_seqlens), sarr, float(softmax_scale), int(world), int(rank),
                                      _ptr(peer_bases), int(ll_offset), int(ll_slot_bytes), _ptr(epoch), _ptr(counter),
-                                     int(out_dtype), _ptr(out), _ptr(lse), _ptr(workspace), int(workspace_bytes),
-                                     _stream_handle(stream))
+                                     int(out_dtype), _ptr(out), _ptr(lse), _ptr(status), int(timeout_ns),
+                                     _ptr(workspace), int(workspace_bytes), _stream_handle(stream))
     if st != DA_OK:
         raise DecAttnError(st, "da_forward_peer_combine")
+
+
+def da_query_residency(plan: da_plan, kernel: int, exchange: int = 0) -> int:
+    """Co-resident launch units of the plan's forward (kernel 0; clusters for CLUSTER plans, else
+    CTAs) or of the combine kernel (kernel 1) on the current device."""
+    n = ctypes.c_int32(0)
+    st = LIB.da_query_residency(ctypes.byref(plan), int(kernel), int(exchange), ctypes.byref(n))
+    if st != DA_OK:
+        raise DecAttnError(st, "da_query_residency")
+    return int(n.value)
 
 
 def da_combine(num_splits, batch, h_q, head_dim, o_partial, o_split_stride, lse_partial,

@@ -136,20 +136,29 @@ def forward_peer(plan: L.da_plan, q, k_cache, v_cache, cache_seqlens, world, ran
 
 
 def one_kernel_exchange_ok(plan: L.da_plan) -> bool:
-    """da_forward_peer_combine's condition: the kernel that writes the final rows can keep its whole
-    grid resident - a NONE / CLUSTER forward of one wave, or the combine kernel of a workspace plan
-    (one small CTA per row, at most 8 per SM)."""
-    if plan.combine_mode == L.DA_COMBINE_KERNEL:
-        return plan.batch * plan.h_q <= 8 * plan.usable_sms
-    return plan.grid_x * plan.grid_y * plan.grid_z <= plan.usable_sms
+    """da_forward_peer_combine's condition: the kernel that writes the final rows keeps its whole grid
+    resident on the current device - the forward's CTAs (NONE) or clusters (CLUSTER), or the combine
+    kernel's one CTA per row (workspace plans) - by the occupancy API's answer for that exact kernel
+    (da_query_residency), scaled to the plan's usable SMs."""
+    kernel_ws = plan.combine_mode == L.DA_COMBINE_KERNEL
+    units = L.da_query_residency(plan, 1 if kernel_ws else 0, 2)
+    fit = units * plan.usable_sms // max(plan.num_sms, 1)
+    if kernel_ws:
+        need = plan.batch * plan.h_q
+    elif plan.combine_mode == L.DA_COMBINE_CLUSTER:
+        need = plan.grid_y * plan.grid_z
+    else:
+        need = plan.grid_x * plan.grid_y * plan.grid_z
+    return need <= fit
 
 
 def forward_peer_combine(plan: L.da_plan, q, k_cache, v_cache, cache_seqlens, world, rank, peer_bases, ll_offset,
-                         ll_slot_bytes, epoch, counter, *, out=None, lse=None, workspace=None, softmax_scale=0.0,
-                         out_dtype=torch.bfloat16, stream=None):
+                         ll_slot_bytes, epoch, counter, status, *, timeout_ns=0, out=None, lse=None, workspace=None,
+                         softmax_scale=0.0, out_dtype=torch.bfloat16, stream=None):
     """The sequence-sharded step in one kernel via da_forward_peer_combine: the forward publishes
-    this rank's partial, waits for every rank's, and LSE-merges them into (out, lse)."""
-    _check_cuda(q, k_cache, v_cache, cache_seqlens, peer_bases, epoch, counter, out, lse)
+    this rank's partial, waits for every rank's, and LSE-merges them into (out, lse).  status: device
+    int32 [1], set to DA_ERR_TIMEOUT if a peer's words did not arrive within timeout_ns."""
+    _check_cuda(q, k_cache, v_cache, cache_seqlens, peer_bases, epoch, counter, status, out, lse)
     if q.dtype != torch.bfloat16 or k_cache.dtype != torch.bfloat16 or v_cache.dtype != torch.bfloat16:
         raise ValueError("q, k_cache, v_cache must be bfloat16")
     if cache_seqlens is not None and cache_seqlens.dtype != torch.int32:
@@ -166,7 +175,8 @@ def forward_peer_combine(plan: L.da_plan, q, k_cache, v_cache, cache_seqlens, wo
     ws_bytes = 0 if workspace is None else workspace.numel() * workspace.element_size()
     L.da_forward_peer_combine(plan, q, k_cache, v_cache, k_cache.shape[1], cache_seqlens,
                               _kv_strides(q, k_cache, v_cache), softmax_scale, world, rank, peer_bases, ll_offset,
-                              ll_slot_bytes, epoch, counter, dt, out, lse, workspace, ws_bytes, stream)
+                              ll_slot_bytes, epoch, counter, dt, out, lse, status, timeout_ns, workspace, ws_bytes,
+                              stream)
     return out, lse
 
 

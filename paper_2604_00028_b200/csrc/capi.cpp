@@ -14,6 +14,9 @@
 #include <cmath>
 #include <cstdint>
 #include <cstring>
+#include <map>
+#include <mutex>
+#include <tuple>
 
 #include "../../include/decattn.h"
 #include "config.h"
@@ -83,6 +86,34 @@ bool make_kv_tmap(CUtensorMap* map, const void* base, int32_t batch, int32_t l_c
 }
 
 inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+constexpr uint64_t kDefaultTimeoutNs = 10ull * 1000 * 1000 * 1000;   // bounded exchange wait: 10 s
+
+// Co-resident launch units of a kernel variant on the current device (da_query_residency),
+// memoised per (device, kernel, exchange, path, rows, combine, cluster size): the answer depends on
+// the compiled kernel and the device only.
+cudaError_t residency(const da_plan& plan, int kernel, int exchange, int* out) {
+  static std::mutex mu;
+  static std::map<std::tuple<int, int, int, int, int, int, int>, int> memo;
+  int dev = 0;
+  cudaError_t err = cudaGetDevice(&dev);
+  if (err != cudaSuccess) return err;
+  const auto key = kernel == 1 ? std::make_tuple(dev, 1, 0, 0, 0, 0, 0)
+                               : std::make_tuple(dev, 0, exchange, plan.path, plan.rows_per_cta, plan.combine_mode,
+                                                 plan.combine_mode == DA_COMBINE_CLUSTER ? plan.num_splits : 0);
+  {
+    std::lock_guard<std::mutex> g(mu);
+    auto it = memo.find(key);
+    if (it != memo.end()) { *out = it->second; return cudaSuccess; }
+  }
+  int n = 0;
+  err = kernel == 1 ? combine_residency(&n) : forward_residency(plan, exchange, &n);
+  if (err != cudaSuccess) return err;
+  std::lock_guard<std::mutex> g(mu);
+  memo[key] = n;
+  *out = n;
+  return cudaSuccess;
+}
 
 // A plan may be edited by its owner; re-derive what the launch depends on.
 da_status check_plan(const da_plan* plan) {
@@ -421,11 +452,14 @@ extern "C" da_status da_forward_peer_combine(const da_plan* plan, const void* q,
                                              const int64_t* strides, float softmax_scale, int32_t world,
                                              int32_t rank, const uint64_t* peer_bases, int64_t ll_offset,
                                              int64_t ll_slot_bytes, int32_t* epoch, uint32_t* counter,
-                                             int32_t out_dtype, void* out, float* lse, void* workspace,
-                                             int64_t workspace_bytes, void* cuda_stream) {
+                                             int32_t out_dtype, void* out, float* lse, int32_t* status,
+                                             int64_t timeout_ns, void* workspace, int64_t workspace_bytes,
+                                             void* cuda_stream) {
   if (plan == nullptr || world < 1 || world > kMaxPeers || rank < 0 || rank >= world || peer_bases == nullptr ||
-      epoch == nullptr || counter == nullptr || out == nullptr || (out_dtype != DA_BF16 && out_dtype != DA_F32))
+      epoch == nullptr || counter == nullptr || out == nullptr || status == nullptr ||
+      (out_dtype != DA_BF16 && out_dtype != DA_F32))
     return DA_ERR_INVALID_ARG;
+  if ((reinterpret_cast<uintptr_t>(status) & 3u) != 0) return DA_ERR_ALIGNMENT;
   if (plan->head_dim != kHeadDim) return DA_ERR_UNSUPPORTED;
   const int64_t rows = int64_t(plan->batch) * plan->h_q;
   if (ll_offset < 0 || ll_slot_bytes < rows * 129 * 8) return DA_ERR_INVALID_ARG;
@@ -433,12 +467,26 @@ extern "C" da_status da_forward_peer_combine(const da_plan* plan, const void* q,
       (reinterpret_cast<uintptr_t>(counter) & 3u) != 0 || !aligned16(out) ||
       (lse != nullptr && (reinterpret_cast<uintptr_t>(lse) & 3u) != 0))
     return DA_ERR_ALIGNMENT;
+  {
+    da_status cs = check_plan(plan);
+    if (cs != DA_OK) return cs;
+  }
   // the CTAs that write the final rows spin on the ranks' words: their whole grid must be
-  // resident - the forward (one CTA per SM: its shared memory) for NONE / CLUSTER plans, the
-  // combine kernel (one small CTA per row, many per SM) for static workspace plans
-  const int64_t ctas = int64_t(plan->grid_x) * plan->grid_y * plan->grid_z;
-  if (plan->combine_mode == DA_COMBINE_KERNEL ? rows > 8LL * plan->usable_sms : ctas > plan->usable_sms)
-    return DA_ERR_UNSUPPORTED;
+  // resident at once - the forward for NONE plans (CTAs) and CLUSTER plans (clusters of s CTAs,
+  // GPC-bound placement), the combine kernel (one CTA per row) for workspace plans - as the
+  // occupancy API answers for the exact kernel, scaled to the usable SMs.  Host-only checks first:
+  // a bound no device can beat (one forward CTA per SM: its shared memory; 32 CTAs per SM) and the
+  // workspace, then the query.
+  const bool kernel_ws = plan->combine_mode == DA_COMBINE_KERNEL;
+  const int64_t need = kernel_ws ? rows
+                       : plan->combine_mode == DA_COMBINE_CLUSTER ? int64_t(plan->grid_y) * plan->grid_z
+                                                                  : int64_t(plan->grid_x) * plan->grid_y * plan->grid_z;
+  const int64_t ctas = kernel_ws ? rows : int64_t(plan->grid_x) * plan->grid_y * plan->grid_z;
+  if (ctas > int64_t(plan->usable_sms) * (kernel_ws ? 32 : 1)) return DA_ERR_UNSUPPORTED;
+  if (kernel_ws && (workspace == nullptr || workspace_bytes < plan->workspace_bytes)) return DA_ERR_WORKSPACE;
+  int units = 0;
+  if (residency(*plan, kernel_ws ? 1 : 0, 2, &units) != cudaSuccess) return DA_ERR_CUDA;
+  if (need > int64_t(units) * plan->usable_sms / (plan->num_sms > 0 ? plan->num_sms : 1)) return DA_ERR_UNSUPPORTED;
   PubParams pub{};
   pub.bases = peer_bases;
   pub.epoch = epoch;
@@ -450,6 +498,8 @@ extern "C" da_status da_forward_peer_combine(const da_plan* plan, const void* q,
   pub.out = out;
   pub.lse = lse;
   pub.out_f32 = out_dtype == DA_F32;
+  pub.status = status;
+  pub.timeout_ns = timeout_ns > 0 ? static_cast<uint64_t>(timeout_ns) : kDefaultTimeoutNs;
   return forward_impl(plan, q, k_cache, v_cache, l_cap, cache_seqlens, strides, softmax_scale, DA_F32, nullptr,
                       nullptr, workspace, workspace_bytes, cuda_stream, PagedArgs{}, &pub);
 }
@@ -457,15 +507,18 @@ extern "C" da_status da_forward_peer_combine(const da_plan* plan, const void* q,
 extern "C" da_status da_combine_peers(int32_t world, int32_t rank, const uint64_t* peer_bases, int64_t slot_bytes,
                                       int64_t lse_offset, int64_t flag_offset, const int32_t* epoch, int32_t batch,
                                       int32_t h_q, int32_t head_dim, int32_t out_dtype, void* out, float* lse,
-                                      void* cuda_stream) {
+                                      int32_t* status, int64_t timeout_ns, void* cuda_stream) {
   int64_t rows = 0;
   da_status st = check_peer_layout(world, rank, peer_bases, epoch, batch, h_q, head_dim, slot_bytes, lse_offset,
                                    flag_offset, &rows);
   if (st != DA_OK) return st;
-  if (out == nullptr || (out_dtype != DA_BF16 && out_dtype != DA_F32)) return DA_ERR_INVALID_ARG;
-  if (!aligned16(out) || (lse != nullptr && (reinterpret_cast<uintptr_t>(lse) & 3u) != 0)) return DA_ERR_ALIGNMENT;
+  if (out == nullptr || status == nullptr || (out_dtype != DA_BF16 && out_dtype != DA_F32)) return DA_ERR_INVALID_ARG;
+  if (!aligned16(out) || (lse != nullptr && (reinterpret_cast<uintptr_t>(lse) & 3u) != 0) ||
+      (reinterpret_cast<uintptr_t>(status) & 3u) != 0)
+    return DA_ERR_ALIGNMENT;
   return launch_peer_combine(peer_bases, slot_bytes, lse_offset, flag_offset, epoch, world, rank,
-                             static_cast<int32_t>(rows), out_dtype == DA_F32, out, lse,
+                             static_cast<int32_t>(rows), out_dtype == DA_F32, out, lse, status,
+                             timeout_ns > 0 ? static_cast<uint64_t>(timeout_ns) : kDefaultTimeoutNs,
                              static_cast<cudaStream_t>(cuda_stream)) == cudaSuccess
              ? DA_OK
              : DA_ERR_CUDA;
@@ -511,8 +564,20 @@ extern "C" const char* da_status_string(int32_t status) {
     case DA_ERR_ALIGNMENT: return "DA_ERR_ALIGNMENT: pointer not 16-byte aligned or stride not a multiple of 8 elements";
     case DA_ERR_WORKSPACE: return "DA_ERR_WORKSPACE: workspace missing or smaller than plan->workspace_bytes";
     case DA_ERR_CUDA: return "DA_ERR_CUDA: a CUDA runtime/driver call failed";
+    case DA_ERR_TIMEOUT: return "DA_ERR_TIMEOUT: a cross-GPU exchange wait ran past its bound (a peer is late, crashed or out of step)";
     default: return "unknown da_status";
   }
+}
+
+extern "C" da_status da_query_residency(const da_plan* plan, int32_t kernel, int32_t exchange, int32_t* out) {
+  if (plan == nullptr || out == nullptr || kernel < 0 || kernel > 1 || exchange < 0 || exchange > 2)
+    return DA_ERR_INVALID_ARG;
+  da_status st = check_plan(plan);
+  if (st != DA_OK) return st;
+  int n = 0;
+  if (residency(*plan, kernel, exchange, &n) != cudaSuccess) return DA_ERR_CUDA;
+  *out = n;
+  return DA_OK;
 }
 
 extern "C" int32_t da_abi_version(void) { return DA_ABI_VERSION; }

@@ -208,7 +208,7 @@ __global__ void __launch_bounds__(256)
 __global__ void __launch_bounds__(kCombineThreads)
     peer_combine_kernel(const uint64_t* peer_bases, int64_t slot_bytes, int64_t lse_offset, int64_t flag_offset,
                         const int32_t* epoch, int32_t world, int32_t rank, int32_t rows, int32_t out_f32,
-                        void* out, float* lse_out) {
+                        void* out, float* lse_out, int32_t* status, uint64_t timeout_ns) {
   constexpr int kWarps = kCombineThreads / 32;
   __shared__ float4 s_acc[kWarps][32];
   __shared__ float s_m[kWarps], s_l[kWarps];
@@ -223,9 +223,19 @@ __global__ void __launch_bounds__(kCombineThreads)
   const uint32_t e = static_cast<uint32_t>(*epoch);
   if (warp == 0) {   // lane q polls rank q's flag (q, q + 32): the P acquires overlap
     const uint32_t* flags = reinterpret_cast<const uint32_t*>(own + static_cast<uint64_t>(flag_offset));
-    for (int q = lane; q < world; q += 32)
+    for (int q = lane; q < world; q += 32) {
+      if (ld_acquire_sys_u32(flags + q) >= e) continue;
+      // bounded wait: a flag still behind timeout_ns after the first failed poll
+      // records DA_ERR_TIMEOUT and ends the wait (the merge below then reads stale slots)
+      const uint64_t t0 = globaltimer();
       while (ld_acquire_sys_u32(flags + q) < e) {
+        if (*reinterpret_cast<const volatile int32_t*>(status) != 0) break;
+        if (globaltimer() - t0 > timeout_ns) {
+          atomicExch(status, static_cast<int32_t>(DA_ERR_TIMEOUT));
+          break;
+        }
       }
+    }
   }
   __syncthreads();
   const uint64_t slot_off = static_cast<uint64_t>(slot_bytes) * (e & 1u);
@@ -309,7 +319,8 @@ cudaError_t launch_peer_signal(const uint64_t* peer_bases, int32_t world, int32_
 
 cudaError_t launch_peer_combine(const uint64_t* peer_bases, int64_t slot_bytes, int64_t lse_offset,
                                 int64_t flag_offset, const int32_t* epoch, int32_t world, int32_t rank, int32_t rows,
-                                int32_t out_f32, void* out, float* lse, cudaStream_t stream) {
+                                int32_t out_f32, void* out, float* lse, int32_t* status, uint64_t timeout_ns,
+                                cudaStream_t stream) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(rows, 1, 1);
   cfg.blockDim = dim3(kCombineThreads, 1, 1);
@@ -320,7 +331,19 @@ cudaError_t launch_peer_combine(const uint64_t* peer_bases, int64_t slot_bytes, 
   cfg.attrs = &attr;
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, peer_combine_kernel, peer_bases, slot_bytes, lse_offset, flag_offset, epoch,
-                            world, rank, rows, out_f32, out, lse);
+                            world, rank, rows, out_f32, out, lse, status, timeout_ns);
+}
+
+cudaError_t combine_residency(int* out) {
+  int dev = 0, sms = 0, per_sm = 0;
+  cudaError_t err = cudaGetDevice(&dev);
+  if (err != cudaSuccess) return err;
+  if ((err = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return err;
+  if ((err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lse_combine_kernel, kCombineThreads, 0)) !=
+      cudaSuccess)
+    return err;
+  *out = per_sm * sms;
+  return cudaSuccess;
 }
 
 }  // namespace decattn

@@ -892,51 +892,113 @@ __global__ void __launch_bounds__(threads_for(NW, helpers_for(kCombine)), 1)
 #endif
 }
 
+// The kernel instantiation a plan launches, its shared memory and block size, with the one-time
+// (per device) opt-in to > 48 KB of dynamic shared memory and to non-portable cluster sizes.
+template <int kPath, int kNB, int kCombine, bool kDyn = false, int kPub = 0>
+struct FwdKernel {
+  static constexpr bool kCluster = kCombine == DA_COMBINE_CLUSTER;
+  // dynamic split counts: mostly one split per sequence, so the streaming (s = 1) configuration
+  static constexpr int NS = kDyn ? kStagesNone : stages_for(kCombine);
+  static constexpr int NW = kDyn ? kWarpsNone : warps_for(kCombine);
+  static constexpr int kSmem = smem_for(NS, kCluster);
+  static constexpr int kThreads = threads_for(NW, helpers_for(kCombine));
+  static constexpr auto kern = split_kv_fwd_kernel<kPath, kNB, kCombine, NS, NW, kDyn, kPub>;
+
+  static cudaError_t prepare() {
+    static std::atomic<uint64_t> attr_done{0};
+    int dev = 0;
+    cudaError_t err = cudaGetDevice(&dev);
+    if (err != cudaSuccess) return err;
+    const uint64_t bit = 1ull << (dev & 63);
+    if ((attr_done.load(std::memory_order_acquire) & bit) == 0) {
+      err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+      if (err != cudaSuccess) return err;
+      if (kCluster) {   // clusters of 9..16 CTAs are a non-portable size
+        err = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        if (err != cudaSuccess) return err;
+      }
+      attr_done.fetch_or(bit, std::memory_order_acq_rel);
+    }
+    return cudaSuccess;
+  }
+
+  static void config(const da_plan& plan, cudaStream_t stream, cudaLaunchConfig_t& cfg, cudaLaunchAttribute* attrs) {
+    cfg = {};
+    cfg.gridDim = dim3(plan.grid_x, plan.grid_y, plan.grid_z);
+    cfg.blockDim = dim3(kThreads, 1, 1);
+    cfg.dynamicSmemBytes = kSmem;
+    cfg.stream = stream;
+    int na = 0;
+    attrs[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attrs[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+    if (kCluster) {
+      attrs[na].id = cudaLaunchAttributeClusterDimension;
+      attrs[na].val.clusterDim.x = static_cast<unsigned>(plan.num_splits);
+      attrs[na].val.clusterDim.y = 1;
+      attrs[na].val.clusterDim.z = 1;
+      ++na;
+    }
+    cfg.attrs = attrs;
+    cfg.numAttrs = na;
+  }
+
+  static cudaError_t launch(const da_plan& plan, const CUtensorMap& tk, const CUtensorMap& tv, const FwdParams& p,
+                            cudaStream_t stream) {
+    cudaError_t err = prepare();
+    if (err != cudaSuccess) return err;
+    if (kThreads != plan.block_threads || kSmem != plan.smem_bytes) return cudaErrorInvalidConfiguration;
+    cudaLaunchConfig_t cfg;
+    cudaLaunchAttribute attrs[2];
+    config(plan, stream, cfg, attrs);
+    return cudaLaunchKernelEx(&cfg, kern, tk, tv, p);
+  }
+
+  // Launch units of this instantiation that can be co-resident on the current device: clusters of
+  // plan.num_splits CTAs (cudaOccupancyMaxActiveClusters) for a cluster kernel, CTAs otherwise.
+  static cudaError_t residency(const da_plan& plan, int* out) {
+    cudaError_t err = prepare();
+    if (err != cudaSuccess) return err;
+    if (kCluster) {
+      cudaLaunchConfig_t cfg;
+      cudaLaunchAttribute attrs[2];
+      config(plan, nullptr, cfg, attrs);
+      return cudaOccupancyMaxActiveClusters(out, kern, &cfg);
+    }
+    int dev = 0, sms = 0, per_sm = 0;
+    if ((err = cudaGetDevice(&dev)) != cudaSuccess) return err;
+    if ((err = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return err;
+    if ((err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, kSmem)) != cudaSuccess)
+      return err;
+    *out = per_sm * sms;
+    return cudaSuccess;
+  }
+};
+
 template <int kPath, int kNB, int kCombine, bool kDyn = false, int kPub = 0>
 cudaError_t launch_impl(const da_plan& plan, const CUtensorMap& tk, const CUtensorMap& tv,
                         const FwdParams& p, cudaStream_t stream) {
-  constexpr bool kCluster = kCombine == DA_COMBINE_CLUSTER;
-  // dynamic split counts: mostly one split per sequence, so the streaming (s = 1) configuration
-  constexpr int NS = kDyn ? kStagesNone : stages_for(kCombine);
-  constexpr int NW = kDyn ? kWarpsNone : warps_for(kCombine);
-  constexpr int kSmem = smem_for(NS, kCluster);
-  auto kern = split_kv_fwd_kernel<kPath, kNB, kCombine, NS, NW, kDyn, kPub>;
-  // One-time (per device) opt-in to > 48 KB of dynamic shared memory.
-  static std::atomic<uint64_t> attr_done{0};
-  int dev = 0;
-  cudaError_t err = cudaGetDevice(&dev);
-  if (err != cudaSuccess) return err;
-  const uint64_t bit = 1ull << (dev & 63);
-  if ((attr_done.load(std::memory_order_acquire) & bit) == 0) {
-    err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
-    if (err != cudaSuccess) return err;
-    if (kCluster) {   // clusters of 9..16 CTAs are a non-portable size
-      err = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-      if (err != cudaSuccess) return err;
-    }
-    attr_done.fetch_or(bit, std::memory_order_acq_rel);
+  return FwdKernel<kPath, kNB, kCombine, kDyn, kPub>::launch(plan, tk, tv, p, stream);
+}
+
+template <int kPath, int kNB>
+cudaError_t residency_combine(const da_plan& plan, int pub, int* out) {
+  switch (plan.combine_mode) {
+    case DA_COMBINE_NONE:
+      if (pub == 2) return FwdKernel<kPath, kNB, DA_COMBINE_NONE, false, 2>::residency(plan, out);
+      if (pub == 1) return FwdKernel<kPath, kNB, DA_COMBINE_NONE, false, 1>::residency(plan, out);
+      return FwdKernel<kPath, kNB, DA_COMBINE_NONE>::residency(plan, out);
+    case DA_COMBINE_CLUSTER:
+      if (pub == 2) return FwdKernel<kPath, kNB, DA_COMBINE_CLUSTER, false, 2>::residency(plan, out);
+      if (pub == 1) return FwdKernel<kPath, kNB, DA_COMBINE_CLUSTER, false, 1>::residency(plan, out);
+      return FwdKernel<kPath, kNB, DA_COMBINE_CLUSTER>::residency(plan, out);
+    default:
+      if (is_dynamic(plan)) {
+        if (pub) return FwdKernel<kPath, kNB, DA_COMBINE_KERNEL, true, 1>::residency(plan, out);
+        return FwdKernel<kPath, kNB, DA_COMBINE_KERNEL, true>::residency(plan, out);
+      }
+      return FwdKernel<kPath, kNB, DA_COMBINE_KERNEL>::residency(plan, out);
   }
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(plan.grid_x, plan.grid_y, plan.grid_z);
-  cfg.blockDim = dim3(threads_for(NW, helpers_for(kCombine)), 1, 1);
-  if (static_cast<int>(cfg.blockDim.x) != plan.block_threads || kSmem != plan.smem_bytes) return cudaErrorInvalidConfiguration;
-  cfg.dynamicSmemBytes = kSmem;
-  cfg.stream = stream;
-  cudaLaunchAttribute attrs[2];
-  int na = 0;
-  attrs[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attrs[na].val.programmaticStreamSerializationAllowed = 1;
-  ++na;
-  if (kCluster) {
-    attrs[na].id = cudaLaunchAttributeClusterDimension;
-    attrs[na].val.clusterDim.x = static_cast<unsigned>(plan.num_splits);
-    attrs[na].val.clusterDim.y = 1;
-    attrs[na].val.clusterDim.z = 1;
-    ++na;
-  }
-  cfg.attrs = attrs;
-  cfg.numAttrs = na;
-  return cudaLaunchKernelEx(&cfg, kern, tk, tv, p);
 }
 
 template <int kPath, int kNB>
@@ -972,6 +1034,12 @@ cudaError_t launch_split_kv_fwd(const da_plan& plan, const CUtensorMap& tmap_k,
   if (plan.path == DA_PATH_SCALAR) return dispatch_combine<DA_PATH_SCALAR, 1>(plan, tmap_k, tmap_v, p, stream);
   if (plan.rows_per_cta == 8) return dispatch_combine<DA_PATH_MMA, 1>(plan, tmap_k, tmap_v, p, stream);
   return dispatch_combine<DA_PATH_MMA, 2>(plan, tmap_k, tmap_v, p, stream);
+}
+
+cudaError_t forward_residency(const da_plan& plan, int pub, int* out) {
+  if (plan.path == DA_PATH_SCALAR) return residency_combine<DA_PATH_SCALAR, 1>(plan, pub, out);
+  if (plan.rows_per_cta == 8) return residency_combine<DA_PATH_MMA, 1>(plan, pub, out);
+  return residency_combine<DA_PATH_MMA, 2>(plan, pub, out);
 }
 
 #ifdef DECATTN_TRACE

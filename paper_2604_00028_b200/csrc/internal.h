@@ -29,6 +29,10 @@ struct PubParams {
   void* out;                // final [B, H_Q, d] bf16 or fp32
   float* lse;               // final [B, H_Q] or nullptr
   int32_t out_f32;
+  // bounded spin: a peer word still not at this step's epoch timeout_ns after the
+  // first failed poll ends the wait and sets *status = DA_EXCHANGE_TIMEOUT (the kernel completes)
+  int32_t* status;
+  uint64_t timeout_ns;
 };
 
 struct FwdParams {
@@ -102,6 +106,12 @@ cudaError_t launch_peer_signal(const uint64_t* peer_bases, int32_t world, int32_
                                int64_t flag_offset, int32_t* epoch, cudaStream_t stream);
 cudaError_t launch_peer_combine(const uint64_t* peer_bases, int64_t slot_bytes, int64_t lse_offset,
                                 int64_t flag_offset, const int32_t* epoch, int32_t world, int32_t rank, int32_t rows,
-                                int32_t out_f32, void* out, float* lse, cudaStream_t stream);
+                                int32_t out_f32, void* out, float* lse, int32_t* status, uint64_t timeout_ns,
+                                cudaStream_t stream);
+// co-residency queries (da_query_residency): launch units of the instantiation a plan launches
+// that fit the current device at once (fwd.cu: clusters for CLUSTER plans, else CTAs; pub = the
+// exchange variant 0 / 1 / 2), and CTAs of the combine kernel (combine.cu)
+cudaError_t forward_residency(const da_plan& plan, int pub, int* out);
+cudaError_t combine_residency(int* out);
 
 }  // namespace decattn

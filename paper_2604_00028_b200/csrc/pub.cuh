@@ -71,6 +71,21 @@ static __device__ __forceinline__ void pub_ll_store(const PubParams& pb, uint32_
   st_ll(w + 3, e, v.w);
   if (d4 == 0) st_ll(pub_ll_row(pb, pb.rank, e, row) + 128, e, lse);
 }
+// Bounded wait: poll `p` until its epoch is e, at most pb.timeout_ns after the first
+// failed poll; past that (or once another thread has timed out) record DA_ERR_TIMEOUT in
+// *pb.status and return what the word holds, so the kernel completes and the host sees the failure.
+static __device__ __noinline__ uint64_t ld_ll_wait(const PubParams& pb, const uint64_t* p, uint64_t w, uint32_t e) {
+  const uint64_t t0 = ptx::globaltimer();
+  while (static_cast<uint32_t>(w >> 32) != e) {
+    if (*reinterpret_cast<const volatile int32_t*>(pb.status) != 0) break;
+    if (ptx::globaltimer() - t0 > pb.timeout_ns) {
+      atomicExch(pb.status, static_cast<int32_t>(DA_ERR_TIMEOUT));
+      break;
+    }
+    w = ld_ll(p);
+  }
+  return w;
+}
 // Every rank's (o, lse) words of row / d4, polled until they carry epoch e (each word validates
 // itself: no flag, no fence), LSE-merged (C-comb) into the final out / lse.
 static __device__ __forceinline__ void pub_ll_merge_row(const PubParams& pb, uint32_t e, size_t row, int d4) {
@@ -85,7 +100,7 @@ static __device__ __forceinline__ void pub_ll_merge_row(const PubParams& pb, uin
     w[4] = ld_ll(rw + 128);
 #pragma unroll
     for (int i = 0; i < 5; ++i)
-      while (static_cast<uint32_t>(w[i] >> 32) != e) w[i] = ld_ll(i < 4 ? rw + 4 * d4 + i : rw + 128);
+      if (static_cast<uint32_t>(w[i] >> 32) != e) w[i] = ld_ll_wait(pb, i < 4 ? rw + 4 * d4 + i : rw + 128, w[i], e);
     const float li = __uint_as_float(static_cast<uint32_t>(w[4])) * kLog2e;
     const float4 oi = make_float4(__uint_as_float(static_cast<uint32_t>(w[0])), __uint_as_float(static_cast<uint32_t>(w[1])),
                                   __uint_as_float(static_cast<uint32_t>(w[2])), __uint_as_float(static_cast<uint32_t>(w[3])));

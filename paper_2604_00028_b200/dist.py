@@ -177,7 +177,8 @@ class PeerSeqShardedDecode:
     (monotonic epochs)."""
 
     def __init__(self, batch: int, h_q: int, h_kv: int, l_k_total: int, head_dim: int = 128, *,
-                 group=None, policy="seq_aware", device=None, fused: bool = True, one_kernel: bool = True):
+                 group=None, policy="seq_aware", device=None, fused: bool = True, one_kernel: bool = True,
+                 timeout_ns: int = 0):
         import torch.distributed._symmetric_memory as symm
 
         from . import api
@@ -203,7 +204,17 @@ class PeerSeqShardedDecode:
         self.fused = fused
         self.counter = torch.zeros(1, dtype=torch.int32, device=self.device)   # da_forward_peer: writer CTAs
         self.plan = api.make_plan(batch, h_q, h_kv, self.l_local, head_dim, True, 0, None, policy)
-        self.one_kernel = fused and one_kernel and api.one_kernel_exchange_ok(self.plan)
+        # every rank must take the same protocol (LL words vs slot + flags): the shards' lengths can
+        # differ by one token, so their plans - and whether the one-kernel grid is resident - can
+        # differ; the decision is the minimum over the group
+        ok = torch.tensor([1 if (fused and one_kernel and api.one_kernel_exchange_ok(self.plan)) else 0],
+                          dtype=torch.int32, device=self.device)
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN, group=group)
+        self.one_kernel = bool(ok.item())
+        # bounded exchange waits: a peer's words / flags that do not arrive within timeout_ns
+        # (0: the library's default, 10 s) set status = DA_ERR_TIMEOUT instead of hanging the GPU
+        self.status = torch.zeros(1, dtype=torch.int32, device=self.device)
+        self.timeout_ns = int(timeout_ns)
         self._ws = api.workspace_for(self.plan, self.device)
         self.o_local = torch.empty((batch, h_q, head_dim), dtype=torch.float32, device=self.device)
         self.lse_local = torch.empty((batch, h_q), dtype=torch.float32, device=self.device)
@@ -215,7 +226,8 @@ class PeerSeqShardedDecode:
         if self.one_kernel:
             return api.forward_peer_combine(self.plan, q, k_local, v_local, seqlens_local, self.world, self.rank,
                                             self.bases, self.ll_offset, self.ll_slot_bytes, self.epoch, self.counter,
-                                            out=out, lse=lse, workspace=self._ws)
+                                            self.status, timeout_ns=self.timeout_ns, out=out, lse=lse,
+                                            workspace=self._ws)
         if self.fused:
             api.forward_peer(self.plan, q, k_local, v_local, seqlens_local, self.world, self.rank, self.bases,
                              self.slot_bytes, self.lse_offset, self.flag_offset, self.epoch, self.counter,
@@ -231,5 +243,14 @@ class PeerSeqShardedDecode:
             lse = torch.empty((self.batch, self.h_q), dtype=torch.float32, device=self.device)
         L.da_combine_peers(self.world, self.rank, self.bases, self.slot_bytes, self.lse_offset, self.flag_offset,
                            self.epoch, self.batch, self.h_q, self.d,
-                           L.DA_F32 if out.dtype == torch.float32 else L.DA_BF16, out, lse)
+                           L.DA_F32 if out.dtype == torch.float32 else L.DA_BF16, out, lse, self.status,
+                           self.timeout_ns)
         return out, lse
+
+    def check(self):
+        """Raise DecAttnError(DA_ERR_TIMEOUT) if an exchange wait of any step so far ran past its bound
+        (reads the device status word: synchronises with the steps enqueued before it)."""
+        from . import _lib as L
+        st = int(self.status.item())
+        if st != 0:
+            raise L.DecAttnError(st, "PeerSeqShardedDecode exchange")

@@ -17,7 +17,7 @@ run() {   # name, command
     ncu -i $OUT/full_$name.ncu-rep --page details > $OUT/details_$name.txt 2>/dev/null
   echo "$name rc=$?"
 }
-run llama70b python bench.py --steps 20 --warmup 3 --no-extras --cpu-seconds 1
+run llama70b python bench.py --workload llama70b --steps 20 --warmup 3 --no-extras --cpu-seconds 1
 run llama70b_tp8 python bench.py --workload llama70b_tp8 --steps 20 --warmup 3 --no-extras --cpu-seconds 1
 run long_context python bench.py --workload long_context --steps 5 --warmup 3 --no-extras --cpu-seconds 1
 run high_load python bench.py --workload high_load --steps 3 --warmup 3 --no-extras --cpu-seconds 1

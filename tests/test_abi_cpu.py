@@ -372,11 +372,14 @@ def test_peer_exchange_validation(L):
 
     def comb(**kw):
         a = dict(world=2, rank=1, peer_bases=A2, slot_bytes=slot, lse_offset=lo, flag_offset=fo, epoch=A2,
-                 batch=1, h_q=8, head_dim=128, out_dtype=L.DA_BF16, out=A2, lse=A2, stream=0)
+                 batch=1, h_q=8, head_dim=128, out_dtype=L.DA_BF16, out=A2, lse=A2, status=A2, timeout_ns=0,
+                 stream=0)
         a.update(kw)
         with pytest.raises(L.DecAttnError) as e:
             L.da_combine_peers(**a)
         return e.value.status
+    assert comb(status=None) == L.DA_ERR_INVALID_ARG              # the bounded wait needs its status word
+    assert comb(status=A2 + 2) == L.DA_ERR_ALIGNMENT
     assert comb(out=None) == L.DA_ERR_INVALID_ARG
     assert comb(out_dtype=5) == L.DA_ERR_INVALID_ARG
     assert comb(epoch=None) == L.DA_ERR_INVALID_ARG
@@ -449,14 +452,16 @@ def test_forward_peer_combine_validation(L):
         rows = plan.batch * plan.h_q
         a = dict(plan=plan, q=A2, k_cache=A2, v_cache=A2, l_cap=plan.l_k, cache_seqlens=None, strides=None,
                  softmax_scale=0.0, world=2, rank=0, peer_bases=A2, ll_offset=fo + 16, ll_slot_bytes=8 * 129 * rows + 16,
-                 epoch=A2, counter=A2, out_dtype=L.DA_BF16, out=A2, lse=A2, workspace=None, workspace_bytes=0,
-                 stream=0)
+                 epoch=A2, counter=A2, out_dtype=L.DA_BF16, out=A2, lse=A2, status=A2, timeout_ns=0, workspace=None,
+                 workspace_bytes=0, stream=0)
         a.update(kw)
         with pytest.raises(L.DecAttnError) as e:
             L.da_forward_peer_combine(**a)
         return e.value.status
     cluster = L.da_plan_make(1, 8, 1, 1500, 128, 1, 0, 148, "seq_aware", 0)
     assert cluster.combine_mode == L.DA_COMBINE_CLUSTER
+    assert fwd(cluster, status=None) == L.DA_ERR_INVALID_ARG
+    assert fwd(cluster, status=A2 + 2) == L.DA_ERR_ALIGNMENT
     assert fwd(cluster, out=None) == L.DA_ERR_INVALID_ARG
     assert fwd(cluster, out_dtype=7) == L.DA_ERR_INVALID_ARG
     assert fwd(cluster, counter=None) == L.DA_ERR_INVALID_ARG
@@ -473,3 +478,16 @@ def test_forward_peer_combine_validation(L):
     wide = L.da_plan_make(256, 8, 1, 300, 128, 1, 0, 148, "guarded", 0)       # 256 CTAs > 148 SMs
     assert big.grid_x * big.grid_y * big.grid_z <= 148
     assert fwd(wide) == L.DA_ERR_UNSUPPORTED
+
+
+def test_query_residency_validation(L):
+    import ctypes
+    plan = L.da_plan_make(1, 8, 1, 512, 128, 1, 0, 148, "seq_aware", 0)
+    n = ctypes.c_int32(0)
+    for kernel, exchange in ((2, 0), (-1, 0), (0, 3), (0, -1)):
+        assert L.LIB.da_query_residency(ctypes.byref(plan), kernel, exchange, ctypes.byref(n)) == L.DA_ERR_INVALID_ARG
+    assert L.LIB.da_query_residency(None, 0, 0, ctypes.byref(n)) == L.DA_ERR_INVALID_ARG
+    assert L.LIB.da_query_residency(ctypes.byref(plan), 0, 0, None) == L.DA_ERR_INVALID_ARG
+    bad = L.da_plan.from_buffer_copy(plan)
+    bad.grid_x += 1                                              # an inconsistent (edited) plan
+    assert L.LIB.da_query_residency(ctypes.byref(bad), 0, 0, ctypes.byref(n)) == L.DA_ERR_INVALID_ARG

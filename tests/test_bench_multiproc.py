@@ -17,7 +17,7 @@ def test_bench_two_ranks_batch_sharded():
     env = dict(os.environ, DECATTN_BENCH_BACKEND="gloo", DECATTN_BENCH_ONE_GPU="1")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
            "--master-addr", "127.0.0.1", "--master-port", "29517", os.path.join(ROOT, "bench.py"),
-           "--gpus", "2", "--steps", "20", "--warmup", "3"]
+           "--gpus", "2", "--workload", "llama70b", "--steps", "20", "--warmup", "3"]
     r = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stderr[-3000:]
     lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
@@ -65,7 +65,7 @@ def test_bench_two_ranks_head_sharded():
     env = dict(os.environ, DECATTN_BENCH_BACKEND="gloo", DECATTN_BENCH_ONE_GPU="1")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
            "--master-addr", "127.0.0.1", "--master-port", "29521", os.path.join(ROOT, "bench.py"),
-           "--gpus", "2", "--shard-heads", "--steps", "20", "--warmup", "3"]
+           "--gpus", "2", "--workload", "llama70b", "--shard-heads", "--steps", "20", "--warmup", "3"]
     r = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stderr[-3000:]
     lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]

@@ -206,6 +206,34 @@ def test_combine_kernel_direct():
             assert_lse_close(synth.to_f64(lse), ref_l)
 
 
+def test_combine_kernel_padded_split_stride():
+    # da_combine with split strides larger than a split's rows (the NCCL all-gather buffer [P][o | lse]
+    # padded to 16 bytes, dist.SeqShardedDecode): partials read through a non-contiguous view
+    dec = _dec()
+    from paper_2604_00028_b200 import _lib as L
+    rng = np.random.default_rng(4)
+    for s, B, HQ in ((2, 1, 64), (8, 3, 24), (5, 2, 8)):
+        rows = B * HQ
+        chunk = -(-(rows * 129) // 4) * 4 + 4 * int(rng.integers(0, 5))   # padded (+ up to 16 extra floats)
+        buf = torch.full((s, chunk), float("nan"), dtype=torch.float32, device="cuda")
+        o = rng.standard_normal((s, B, HQ, 128))
+        l = rng.standard_normal((s, B, HQ)) * 2
+        l[rng.random((s, B, HQ)) < 0.25] = -np.inf
+        o[np.isneginf(l)] = 0.0
+        buf[:, : rows * 128] = torch.tensor(o.reshape(s, -1), dtype=torch.float32, device="cuda")
+        buf[:, rows * 128: rows * 129] = torch.tensor(l.reshape(s, -1), dtype=torch.float32, device="cuda")
+        o_view = buf[:, : rows * 128]
+        l_view = buf[:, rows * 128: rows * 129]
+        for dt in (L.DA_BF16, L.DA_F32):
+            out = torch.empty((B, HQ, 128), dtype=torch.float32 if dt == L.DA_F32 else torch.bfloat16, device="cuda")
+            lse = torch.empty((B, HQ), dtype=torch.float32, device="cuda")
+            L.da_combine(s, B, HQ, 128, o_view, chunk, l_view, chunk, dt, out, lse)
+            torch.cuda.synchronize()
+            ref_o, ref_l = OA.lse_combine(o, l)
+            assert_out_close(synth.to_f64(out), ref_o)
+            assert_lse_close(synth.to_f64(lse), ref_l)
+
+
 def test_deterministic_replay():
     dec = _dec()
     inp = synth.make_inputs(1, 8, 1, 512, device="cuda", seed=5)
@@ -217,8 +245,9 @@ def test_deterministic_replay():
 
 
 # ---- BASELINE.json full sizes, in bench.py's launch configuration (cache_seqlens = NULL, plan
-#      cached per shape); sampled (b, kv-head) groups checked against the oracle one by one ------
-def _check_sampled(cfg, policy, picks, seed, variant="normal"):
+#      cached per shape); EVERY (b, kv-head) group checked against the fp64 oracle, one group at a
+#      time (the oracle's fp64 copy of one group is 2 x L_K x 128 x 8 bytes) -------------------------
+def _check_full(cfg, policy, seed, variant="normal", picks=None):
     dec = _dec()
     B, HQ, HKV, L = cfg["batch"], cfg["h_q"], cfg["h_kv"], cfg["l_k"]
     inp = synth.make_inputs(B, HQ, HKV, L, device="cuda", seed=seed, variant=variant)
@@ -227,41 +256,62 @@ def _check_sampled(cfg, policy, picks, seed, variant="normal"):
     out, lse = dec.forward(plan, inp["q"], inp["k"], inp["v"], seq)
     torch.cuda.synchronize()
     G = HQ // HKV
-    for b, g in picks:
-        rows = slice(g * G, (g + 1) * G)
-        q = synth.to_f64(inp["q"][b:b + 1, rows])
-        k = synth.to_f64(inp["k"][b:b + 1, :, g:g + 1])
-        v = synth.to_f64(inp["v"][b:b + 1, :, g:g + 1])
-        n = [L] if seq is None else [int(seq[b])]
-        ref_o, ref_l = OA.decode_attention(q, k, v, n)
-        assert_out_close(synth.to_f64(out[b:b + 1, rows]), ref_o, f"out[b={b}, g={g}]")
-        assert_lse_close(synth.to_f64(lse[b:b + 1, rows]), ref_l, f"lse[b={b}, g={g}]")
+    out_h, lse_h = synth.to_f64(out), synth.to_f64(lse)
+    q_h = synth.to_f64(inp["q"])
+    seq_h = None if seq is None else seq.cpu().tolist()
+    del out, lse
+    groups = picks if picks is not None else [(b, g) for b in range(B) for g in range(HKV)]
+    for b in sorted({b for b, _ in groups}):
+        kb, vb = inp["k"][b].cpu(), inp["v"][b].cpu()          # one sequence's cache on the host (bf16)
+        for g in [g for bb, g in groups if bb == b]:
+            rows = slice(g * G, (g + 1) * G)
+            n = L if seq_h is None else int(seq_h[b])
+            k = synth.to_f64(kb[None, :n, g:g + 1])
+            v = synth.to_f64(vb[None, :n, g:g + 1])
+            ref_o, ref_l = OA.decode_attention(q_h[b:b + 1, rows], k, v, [n])
+            assert_out_close(out_h[b:b + 1, rows], ref_o, f"out[b={b}, g={g}]")
+            assert_lse_close(lse_h[b:b + 1, rows], ref_l, f"lse[b={b}, g={g}]")
     return plan
 
 
-def test_full_size_high_load_sampled():
-    cfg = synth.CONFIGS["high_load"]               # B=128 H_Q=64 H_KV=8 L_K=8192 (4.3 GB of KV)
-    plan = _check_sampled(cfg, "seq_aware", [(0, 0), (17, 3), (64, 7), (127, 5), (99, 1)], 1003)
+def test_full_size_high_load_every_group():
+    cfg = synth.CONFIGS["high_load"]               # B=128 H_Q=64 H_KV=8 L_K=8192 (4.3 GB of KV), 1024 groups
+    plan = _check_full(cfg, "seq_aware", 1003)
     assert plan.num_splits == 1
 
 
-def test_full_size_long_context_sampled():
-    cfg = synth.CONFIGS["long_context"]            # B=1 H_Q=64 H_KV=8 L_K=131072, s = 16 workspace combine
-    plan = _check_sampled(cfg, "seq_aware", [(0, 0), (0, 5), (0, 7)], 1004)
-    assert plan.num_splits == 16 and plan.combine_mode == _dec().DA_COMBINE_KERNEL
+@pytest.mark.parametrize("policy,s,mode", [("seq_aware", 16, 2), ("seq_aware_sm", 10, 1)])
+def test_full_size_long_context_every_group(policy, s, mode):
+    # B=1 H_Q=64 H_KV=8 L_K=131072: the paper's rule gives s = 16 (workspace combine), C-ext-1 moves it
+    # to the one-wave cluster split (s = 10, 8 clusters)
+    plan = _check_full(synth.CONFIGS["long_context"], policy, 1004)
+    assert plan.num_splits == s and plan.combine_mode == mode
 
 
-def test_full_size_long_context_ragged_sampled():
+def test_full_size_long_context_ragged_every_group():
     # ragged lengths at the long-context size: batch of 3 with 0 / 1 / random tokens
     cfg = dict(synth.CONFIGS["long_context"], batch=3)
-    _check_sampled(cfg, "seq_aware", [(0, 1), (1, 2), (2, 4)], 1005, variant="ragged")
+    _check_full(cfg, "seq_aware", 1005, variant="ragged")
 
 
-def test_full_size_long_context_sm_policy_sampled():
-    # C-ext-1 moves the long-context split to the one-wave cluster split (s = 10, 8 clusters)
-    cfg = synth.CONFIGS["long_context"]
-    plan = _check_sampled(cfg, "seq_aware_sm", [(0, 0), (0, 3), (0, 7)], 1006)
-    assert plan.num_splits == 10 and plan.combine_mode == _dec().DA_COMBINE_CLUSTER
+@pytest.mark.parametrize("policy,forced", [("seq_aware", 0), ("seq_aware_sm", 0), ("fixed", 3), ("fixed", 5),
+                                           ("fixed", 20), ("dynamic", 0)])
+def test_seqlens_past_plan_length(policy, forced):
+    # cache_seqlens in (L_K, L_cap]: the plan is made for L_K = 512, the lengths reach the capacity
+    # 1024 (decattn.h: cache_seqlens is clamped to [0, l_cap] on the device, the split range follows
+    # the real length); one value past l_cap is clamped to it
+    dec = _dec()
+    B, HQ, HKV, LK, LCAP = 5, 16, 2, 512, 1024
+    inp = synth.make_inputs(B, HQ, HKV, LK, l_cap=LCAP, seed=1040, device="cuda")
+    seq = torch.tensor([700, 1024, 513, 200, 5000], dtype=torch.int32, device="cuda")
+    plan = dec.make_plan(B, HQ, HKV, LK, policy=policy, forced_splits=forced)
+    for dt in (torch.bfloat16, torch.float32):
+        out, lse = dec.forward(plan, inp["q"], inp["k"], inp["v"], seq, out_dtype=dt)
+        torch.cuda.synchronize()
+        ref_o, ref_l = OA.decode_attention(synth.to_f64(inp["q"]), synth.to_f64(inp["k"]), synth.to_f64(inp["v"]),
+                                           [700, 1024, 513, 200, 1024])
+        assert_out_close(synth.to_f64(out), ref_o)
+        assert_lse_close(synth.to_f64(lse), ref_l)
 
 
 # ---- SM-count-aware policy (C-ext-1): the efficiency-region one-wave cluster splits -----------

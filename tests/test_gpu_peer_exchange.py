@@ -101,3 +101,114 @@ def test_forward_peer_every_combine_mode(one_rank_group, batch, h_q, h_kv, l_k, 
     else:               # the partial of the last step sits in slot 0 of the exchange buffer, flag 0 holds 4
         flags = sd.buf.view(torch.int32)[sd.flag_offset // 4: sd.flag_offset // 4 + 1]
         assert int(flags.item()) == 4
+
+
+# ---- bounded waits: a peer that never arrives fails the step instead of hanging the GPU ----------
+def _fake_two_rank_buffers(batch, h_q, world=2):
+    """Exchange buffers for `world` ranks on this GPU, where only rank 0 (this process) runs: the
+    other ranks' buffers are plain zeroed allocations nobody writes, i.e. a peer that crashed or never
+    reached the step.  Returns (bufs, bases tensor, layout)."""
+    from paper_2604_00028_b200.dist import peer_layout
+    lay = peer_layout(batch, h_q, 128, world)
+    bufs = [torch.zeros(lay[-1] // 4, dtype=torch.float32, device="cuda") for _ in range(world)]
+    bases = torch.tensor([b.data_ptr() for b in bufs], dtype=torch.int64, device="cuda")
+    return bufs, bases, lay
+
+
+@pytest.mark.parametrize("batch,h_q,h_kv,l_k,mode", [(1, 8, 1, 1500, 1), (1, 64, 8, 300, 0), (1, 64, 8, 4096, 2)])
+def test_forward_peer_combine_times_out_on_a_missing_peer(batch, h_q, h_kv, l_k, mode):
+    import time
+    import paper_2604_00028_b200 as dec
+    from paper_2604_00028_b200 import api
+    inp = synth.make_inputs(batch, h_q, h_kv, l_k, seed=1620, device="cuda")
+    plan = dec.make_plan(batch, h_q, h_kv, l_k, policy="seq_aware")
+    assert plan.combine_mode == mode and api.one_kernel_exchange_ok(plan)
+    bufs, bases, (slot, lo, fo, llo, lls, tot) = _fake_two_rank_buffers(batch, h_q)
+    epoch = torch.zeros(1, dtype=torch.int32, device="cuda")
+    counter = torch.zeros(1, dtype=torch.int32, device="cuda")
+    status = torch.zeros(1, dtype=torch.int32, device="cuda")
+    t0 = time.perf_counter()
+    out, lse = api.forward_peer_combine(plan, inp["q"], inp["k"], inp["v"], None, 2, 0, bases, llo, lls, epoch,
+                                        counter, status, timeout_ns=2_000_000)       # 2 ms bound
+    torch.cuda.synchronize()
+    elapsed = time.perf_counter() - t0
+    assert int(status.item()) == dec.DA_ERR_TIMEOUT
+    assert elapsed < 5.0                                 # bounded: no hang (every thread gives up)
+    assert int(epoch.item()) == 1 and int(counter.item()) == 0   # the step still completes its bookkeeping
+    # this rank's own LL words were published with epoch 1
+    words = bufs[0].view(torch.int64)[llo // 8: (llo + lls) // 8][: batch * h_q * 129]
+    assert bool(((words >> 32) == 1).all())
+
+
+def test_combine_peers_times_out_on_a_missing_flag():
+    import time
+    import paper_2604_00028_b200 as dec
+    from paper_2604_00028_b200 import _lib as L
+    batch, h_q = 2, 16
+    bufs, bases, (slot, lo, fo, llo, lls, tot) = _fake_two_rank_buffers(batch, h_q)
+    o = torch.randn(batch, h_q, 128, device="cuda")
+    lse_local = torch.randn(batch, h_q, device="cuda")
+    epoch = torch.zeros(1, dtype=torch.int32, device="cuda")
+    status = torch.zeros(1, dtype=torch.int32, device="cuda")
+    out = torch.empty(batch, h_q, 128, dtype=torch.float32, device="cuda")
+    lse = torch.empty(batch, h_q, dtype=torch.float32, device="cuda")
+    L.da_peer_signal(2, 0, bases, o, lse_local, batch, h_q, 128, slot, lo, fo, epoch)   # rank 0 signals epoch 1
+    t0 = time.perf_counter()
+    L.da_combine_peers(2, 0, bases, slot, lo, fo, epoch, batch, h_q, 128, L.DA_F32, out, lse, status, 2_000_000)
+    torch.cuda.synchronize()
+    assert time.perf_counter() - t0 < 5.0
+    assert int(status.item()) == dec.DA_ERR_TIMEOUT       # rank 1's flag never reached epoch 1
+    # with both flags present the same call completes without touching status
+    status.zero_()
+    flags = bufs[0].view(torch.int32)[fo // 4: fo // 4 + 2]
+    flags[1] = 1
+    L.da_combine_peers(2, 0, bases, slot, lo, fo, epoch, batch, h_q, 128, L.DA_F32, out, lse, status, 2_000_000)
+    torch.cuda.synchronize()
+    assert int(status.item()) == 0
+
+
+def test_peer_step_check_reports_timeout(one_rank_group):
+    # PeerSeqShardedDecode.check(): a clean run reads status 0
+    from paper_2604_00028_b200.dist import PeerSeqShardedDecode
+    inp = synth.make_inputs(1, 8, 1, 1500, seed=1621, device="cuda")
+    sd = PeerSeqShardedDecode(1, 8, 1, 1500, device="cuda", timeout_ns=50_000_000)
+    sd.step(inp["q"], inp["k"], inp["v"])
+    sd.check()
+    sd.status.fill_(6)
+    with pytest.raises(Exception):
+        sd.check()
+
+
+# ---- the north_star's NCCL path: all-gather of the packed [o | lse] partials + da_combine ----------
+@pytest.mark.parametrize("batch,h_q,h_kv,l_k,policy", [(1, 64, 8, 4096, "seq_aware"), (3, 24, 3, 1500, "seq_aware_sm"),
+                                                       (2, 8, 1, 700, "seq_aware")])
+def test_nccl_seq_sharded_matches_oracle(one_rank_group, batch, h_q, h_kv, l_k, policy):
+    from paper_2604_00028_b200.dist import SeqShardedDecode
+    inp = synth.make_inputs(batch, h_q, h_kv, l_k, seed=1630, device="cuda",
+                            variant="ragged" if batch >= 2 else "normal")
+    sd = SeqShardedDecode(batch, h_q, h_kv, l_k, device="cuda", policy=policy)
+    # the packed chunk is padded to 16 bytes: da_combine reads the partials with that split stride
+    assert sd.chunk % 4 == 0 and sd.chunk >= batch * h_q * 129
+    ref_o, ref_l = OA.decode_attention(*(synth.to_f64(inp[n]) for n in ("q", "k", "v", "seqlens")))
+    for dt in (torch.bfloat16, torch.float32):
+        out = torch.zeros((batch, h_q, 128), dtype=dt, device="cuda")
+        lse = torch.empty((batch, h_q), dtype=torch.float32, device="cuda")
+        sd.step(inp["q"], inp["k"], inp["v"], inp["seqlens"], out, lse)
+        torch.cuda.synchronize()
+        assert_out_close(synth.to_f64(out), ref_o)
+        assert_lse_close(synth.to_f64(lse), ref_l)
+    # graph-captured steps (the bench's launch configuration)
+    out = torch.zeros((batch, h_q, 128), dtype=torch.bfloat16, device="cuda")
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        sd.step(inp["q"], inp["k"], inp["v"], inp["seqlens"], out, lse)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        for _ in range(3):
+            sd.step(inp["q"], inp["k"], inp["v"], inp["seqlens"], out, lse)
+    out.zero_()
+    g.replay()
+    torch.cuda.synchronize()
+    assert_out_close(synth.to_f64(out), ref_o)
+    assert_lse_close(synth.to_f64(lse), ref_l)
