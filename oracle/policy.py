@@ -86,9 +86,25 @@ SM_MID_T = 8          # efficiency region, <= 64 units (latency regime): at most
 SM_MID_UNITS = 64
 SM_CLUSTER_CAP = 12   # at most 12 otherwise (clusters of 13..16 measured slower than 12)
 # Clusters of s CTAs (one per split, s = 1..16) that are co-resident in one wave on a 148-SM
-# B200 with the cluster-combine kernel configuration (cudaOccupancyMaxActiveClusters,
-# scripts/microbench_cluster16.cu); index 0 unused, index 1 = one CTA per SM.  Scaled by U / 148.
-CLUSTER_FIT_B200 = (0, 148, 74, 45, 33, 26, 22, 15, 15, 15, 11, 7, 7, 7, 7, 7, 7)
+# B200 with the cluster-combine kernel configuration: a HARDWARE MEASUREMENT, not a paper value -
+# the CUDA occupancy API's answer for the exact cluster kernels, recorded by
+# scripts/measure_residency.py in profiles/cluster_fit_b200.json (the one source: this module loads
+# it, tests/test_abi_cpu.py checks the planner's copy in config.h against it, and
+# tests/test_gpu_residency.py checks both against the live device).  Index 0 unused, index 1 = one
+# CTA per SM.  Scaled by U / 148.
+def _load_cluster_fit():
+    import json
+    import os
+    path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles",
+                        "cluster_fit_b200.json")
+    with open(path) as f:
+        rec = json.load(f)
+    if rec["sms"] != 148 or len(rec["max_active_clusters"]) != 17:
+        raise ValueError("profiles/cluster_fit_b200.json is not a 148-SM B200 record")
+    return tuple(int(x) for x in rec["max_active_clusters"])
+
+
+CLUSTER_FIT_B200 = _load_cluster_fit()
 CLUSTER_MAX_SPLITS = 16
 # Per-batch dynamic split counts (the scheduler-metadata role of P:L125):
 DYN_MAX_SPLITS = 128  # per-sequence cap (the efficiency loop's candidate cap, C-amb-2)
@@ -179,7 +195,9 @@ def seq_aware_splits(geo: dict):
 
 
 def rows_per_cta(G: int, l_k: int) -> int:
-    """Query rows one CTA of the tensor-core path computes: 8, or 16 for G > 8 on
+    """BUILDER SPECIFICATION (C-ext-1's launch geometry), not a reading of the paper: the paper has
+    no B200 kernel.  Pinned by its hand-checked cases in tests/test_oracle_policy.py.
+    Query rows one CTA of the tensor-core path computes: 8, or 16 for G > 8 on
     long sequences (> 64 units).  Short sequences with G > 8 run two 8-row CTAs per 16 rows: the
     16-row kernel is twice the MMA work per warp and past the instruction cache, which costs
     the latency regime 25-40 % (scripts/probe_g16b.py), while on streaming lengths the 8-row split
@@ -188,7 +206,8 @@ def rows_per_cta(G: int, l_k: int) -> int:
 
 
 def launch_rows(batch: int, G: int, h_kv: int, l_k: int, s: int, U: int) -> int:
-    """Rows per CTA the plan launches with s splits: rows_per_cta(G, L_K), except
+    """BUILDER SPECIFICATION (launch geometry of the B200 kernel), not a reading of the paper.
+    Rows per CTA the plan launches with s splits: rows_per_cta(G, L_K), except
     that 8-row CTAs for G > 8 need their whole grid, Batch x H_KV x ceil(G / 8) x s CTAs, in one
     wave of U SMs -- past it, the doubled CTA count costs a second wave and 16-row CTAs stand."""
     rows = rows_per_cta(G, l_k)
@@ -198,7 +217,9 @@ def launch_rows(batch: int, G: int, h_kv: int, l_k: int, s: int, U: int) -> int:
 
 
 def cluster_fit_splits(T: int, U: int) -> int:
-    """Largest s in 1..16 whose T clusters of s CTAs are co-resident in one wave:
+    """BUILDER SPECIFICATION (C-ext-1), not a reading of the paper; the table is a hardware
+    measurement (CLUSTER_FIT_B200, loaded from profiles/cluster_fit_b200.json).
+    Largest s in 1..16 whose T clusters of s CTAs are co-resident in one wave:
     T <= floor(CLUSTER_FIT_B200[s] * U / 148); s = 1 (one CTA per tile) always qualifies."""
     best = 1
     for s in range(2, CLUSTER_MAX_SPLITS + 1):
@@ -208,7 +229,11 @@ def cluster_fit_splits(T: int, U: int) -> int:
 
 
 def seq_aware_sm_splits(geo: dict, l_k: int):
-    """C-ext-1, in this order (n_u = ceil(L_K / 64) units; T_k = Batch x H_KV x ceil(G / rows),
+    """BUILDER SPECIFICATION (C-ext-1, the SM-count-aware generalisation the paper leaves to future
+    work), not a reading of the paper: its constants are B200 calibrations.
+    Pinned by structure (tests/test_oracle_policy.py::test_seq_aware_sm_structure) and against the
+    measurements it was calibrated on; the paper pins only that it splits where Fig. 3 splits.
+    C-ext-1, in this order (n_u = ceil(L_K / 64) units; T_k = Batch x H_KV x ceil(G / rows),
     rows = rows_per_cta(G, L_K), the CTA groups the kernel launches per split (= T for G <= 8);
     f = cluster_fit_splits(T_k, U); c = 8 if T_k <= 4 else 4):
       saturated (5T >= 4U)                      -> 1                      (unchanged FA3 guard)
@@ -250,20 +275,24 @@ def seq_aware_sm_splits(geo: dict, l_k: int):
 
 
 def dynamic_cap(l_k: int) -> int:
-    """DA_POLICY_DYNAMIC's per-sequence split cap: no more splits than 64-token units of the
+    """BUILDER SPECIFICATION (C-ext-2), not a reading of the paper.
+    DA_POLICY_DYNAMIC's per-sequence split cap: no more splits than 64-token units of the
     longest sequence, and at most DYN_MAX_SPLITS."""
     return max(1, min(DYN_MAX_SPLITS, ceil_div(l_k, SPLIT_UNIT)))
 
 
 def dynamic_slots(batch: int, tiles_per_batch: int, U: int, s_cap: int) -> int:
-    """Slots (split CTAs per head group) a dynamic launch provides: enough for any lengths,
+    """BUILDER SPECIFICATION (C-ext-2), not a reading of the paper.
+    Slots (split CTAs per head group) a dynamic launch provides: enough for any lengths,
     because s_b <= n_u_b / W, or s_b = 1 where that rounds to 0, so sum_b s_b <=
     sum_b n_u_b / W + batch <= U / tiles_per_batch + batch."""
     return min(batch * s_cap, ceil_div(U, tiles_per_batch) + batch)
 
 
 def dynamic_schedule(seqlens, tiles_per_batch: int, U: int, s_cap: int):
-    """Per-batch split counts for one ragged batch, in this order:
+    """BUILDER SPECIFICATION (C-ext-2: the paper names the scheduler-metadata role, not a
+    rule), not a reading of the paper; invariants and hand-computed cases pinned.
+    Per-batch split counts for one ragged batch, in this order:
       n_u_b = ceil(n_b / 64)                      (units of each sequence, n_b already clamped)
       W     = max(1, ceil(sum_b n_u_b * tiles_per_batch / U))   (units per CTA for one wave)
       s_b   = min(s_cap, max(1, floor(n_u_b / W)))
@@ -284,7 +313,8 @@ def dynamic_schedule(seqlens, tiles_per_batch: int, U: int, s_cap: int):
 
 
 def varlen_policy(batch: int, h_q: int, h_kv: int, l_cap: int, num_sms: int, sm_margin: int, seqlens):
-    """C-ext-3, the plan for a ragged batch whose lengths are known on the host (the
+    """BUILDER SPECIFICATION (C-ext-3), not a reading of the paper.
+    C-ext-3, the plan for a ragged batch whose lengths are known on the host (the
     scheduler-metadata path of P:L125): the static SM-count-aware plan (C-ext-1) for the cache
     capacity, unless its longest split would hold more than twice the balanced per-CTA work W
     of dynamic_schedule and at least VARLEN_MIN_UNITS units (below that the step is latency-bound

@@ -82,9 +82,11 @@ constexpr int kMaxPeers = 64;          // da_peer_signal / da_combine_peers: ran
 // receives them from all s ranks (itself included): at most max_{s<=16} s ceil(16/s) = 30 rows (s = 15).
 constexpr int kSlotRowFloats = kHeadDim + 4;
 constexpr int kMaxSlotRows = 30;
-// Co-resident clusters of s CTAs (one CTA per SM, the cluster kernel's ~209 KB of shared memory)
-// measured on B200 (148 SMs) with cudaOccupancyMaxActiveClusters (scripts/microbench_cluster16.cu).
-// Cluster placement is GPC-bound, hence not simply 148 / s.  Index: s (0, 1 unused).
+// Co-resident clusters of s CTAs (one CTA per SM, the cluster kernel's ~221 KB of shared memory)
+// measured on B200 (148 SMs): the CUDA occupancy API's answer for these exact kernels
+// (da_query_residency), recorded by scripts/measure_residency.py in profiles/cluster_fit_b200.json;
+// tests/test_abi_cpu.py checks this copy against that record and tests/test_gpu_residency.py both
+// against the device.  Cluster placement is GPC-bound, hence not simply 148 / s.  Index: s.
 constexpr int kMaxActiveClustersB200[17] = {0, 148, 74, 45, 33, 26, 22, 15, 15, 15, 11, 7, 7, 7, 7, 7, 7};
 DA_HD constexpr int threads_for(int warps, int helpers = 0) { return (warps + 1 + helpers) * 32; }   // + TMA producer
 DA_HD constexpr int smem_for(int stages, bool cluster) {

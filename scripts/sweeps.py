@@ -32,25 +32,57 @@ OUT = os.environ.get("SWEEP_OUT", os.path.join(ROOT, "profiles"))
 D = 128
 
 
-def timed_graphs(cfg, plans, steps, rounds, seed):
-    """Interleaved replays of one CUDA graph per plan over the same rotating KV buffers."""
+def plan_key(p):
+    """Two plans with equal keys launch identical kernels with identical grids."""
+    return (p.path, p.rows_per_cta, p.combine_mode, p.num_splits, p.grid_x, p.grid_y, p.grid_z, p.policy == 5)
+
+
+def timed_graphs(cfg, plans, steps, rounds, seed, control=False, raw=False):
+    """Interleaved replays of one CUDA graph per DISTINCT plan over the same rotating KV buffers
+    (identical plans share one graph, so they measure identically by construction), in a
+    random order every round (no arm always follows another), each replay preceded by the L2 scrub
+    and a GPU-side sleep that keeps the host's graph submission out of the timed region
+    (bench.Timer).  control=True adds a second, separately captured graph of plans[0]: its ratio to
+    plans[0] is the harness's own noise.  Returns (median, p10, p90) per plan (+ the control), and
+    with raw=True also the per-round times (for paired ratios)."""
+    import random
     dev = torch.device("cuda", 0)
     l2 = torch.cuda.get_device_properties(0).L2_cache_size
     w = bench.Workload(cfg, dev, seed, l2, max_rot_bytes=200 << 20)
     stream = torch.cuda.Stream()
     timer = bench.Timer(dev)
-    graphs = [bench.make_graph(dec, p, w, steps, stream) for p in plans]
-    res = [[] for _ in plans]
+    keys, graphs = [], []
+    idx = []
+    for p in plans:
+        k = plan_key(p)
+        if k not in keys:
+            keys.append(k)
+            graphs.append(bench.make_graph(dec, p, w, steps, stream))
+        idx.append(keys.index(k))
+    if control:
+        graphs.append(bench.make_graph(dec, plans[0], w, steps, stream))
+        idx.append(len(graphs) - 1)
+    res = [[] for _ in graphs]
+    rng = random.Random(seed)
     for _ in range(rounds):
-        for i, g in enumerate(graphs):
-            res[i].append(timer.time_replay(g, stream) * 1e3 / steps)
+        order = list(range(len(graphs)))
+        rng.shuffle(order)
+        for i in order:
+            res[i].append(timer.time_replay(graphs[i], stream) * 1e3 / steps)
     del graphs, w, timer
     torch.cuda.empty_cache()
     out = []
-    for r in res:
-        r = sorted(r)
+    for i in idx:
+        r = sorted(res[i])
         out.append((statistics.median(r), r[len(r) // 10], r[(9 * len(r)) // 10]))
+    if raw:
+        return out, [res[i] for i in idx]
     return out
+
+
+def paired_speedup(base_rounds, rounds_):
+    """Median over rounds of base time / arm time (both measured in the same round)."""
+    return statistics.median(b / t for b, t in zip(base_rounds, rounds_))
 
 
 def steps_for(cfg):
@@ -77,6 +109,51 @@ def ab_row(cfg, rounds=15, seed=7):
                          speedup=round(tg / t, 4), regression=int(tg / t < 0.99 and not same),
                          same_plan=same, p10_us=round(p10, 3), p90_us=round(p90, 3), combine_mode=plan.combine_mode))
     return rows
+
+
+REG_POLICIES = ("guarded", "seq_aware", "seq_aware_sm", "evolved")
+REG_FIELDS = ["batch", "l_q", "l_k", "h_q", "h_kv", "d", "nblk", "total_mblocks", "policy", "num_splits",
+              "combine_mode", "latency_us", "baseline_us", "speedup", "regression", "same_plan", "p10_us", "p90_us",
+              "control_ratio"]
+
+
+def regress_policies(rounds=15):
+    """The paper's 160-config matrix for every shipped policy against guarded: speedup =
+    median of per-round paired ratios; same_plan = 1 where the policy's plan equals guarded's (one
+    shared graph: 1.0 by construction); control_ratio = guarded vs a second capture of guarded's plan
+    (the harness noise of that config); regression = differing plan and speedup < 0.99."""
+    rows = []
+    for b in (1, 2, 4, 8):
+        for lk in (128, 256, 384, 512, 1024, 2048, 4096, 8192):
+            for hkv in (1, 2, 4, 8, 32):
+                cfg = dict(batch=b, h_q=8 * hkv, h_kv=hkv, l_k=lk)
+                plans = [dec.make_plan(b, 8 * hkv, hkv, lk, policy=p) for p in REG_POLICIES]
+                (times, raw) = timed_graphs(cfg, plans, steps_for(cfg), rounds, 7, control=True, raw=True)
+                ctrl = paired_speedup(raw[0], raw[-1])
+                line = []
+                for pol, plan, (t, p10, p90), r in zip(REG_POLICIES, plans, times, raw):
+                    same = int(plan_key(plan) == plan_key(plans[0]))
+                    sp = 1.0 if same else paired_speedup(raw[0], r)
+                    rows.append(dict(batch=b, l_q=1, l_k=lk, h_q=8 * hkv, h_kv=hkv, d=D, nblk=plan.num_n_blocks,
+                                     total_mblocks=plan.total_mblocks, policy=pol, num_splits=plan.num_splits,
+                                     combine_mode=plan.combine_mode, latency_us=round(t, 3),
+                                     baseline_us=round(times[0][0], 3), speedup=round(sp, 4),
+                                     regression=int(sp < 0.99 and not same), same_plan=same, p10_us=round(p10, 3),
+                                     p90_us=round(p90, 3), control_ratio=round(ctrl, 4)))
+                    line.append(f"{pol} s={plan.num_splits}{'' if same else f' {sp:.3f}x'}")
+                print(f"B={b} L_K={lk:5d} H_KV={hkv:2d}: guarded {times[0][0]:8.2f} us  " + "  ".join(line[1:]) +
+                      f"  (control {ctrl:.3f})", flush=True)
+    write("regression_policies", rows, REG_FIELDS)
+    for pol in REG_POLICIES[1:]:
+        pr = [r for r in rows if r["policy"] == pol]
+        diff = [r for r in pr if not r["same_plan"]]
+        worst = min(diff, key=lambda r: r["speedup"]) if diff else None
+        print(f"{pol}: {len(diff)} of 160 configs with a plan different from guarded; regressions (< 0.99x): "
+              f"{sum(r['regression'] for r in pr)}" +
+              (f"; min {worst['speedup']:.3f}x at B={worst['batch']} L_K={worst['l_k']} H_KV={worst['h_kv']}"
+               if worst else ""))
+    ctrl = [r["control_ratio"] for r in rows if r["policy"] == "guarded"]
+    print(f"control (guarded vs a second capture of its plan): {min(ctrl):.4f} .. {max(ctrl):.4f}")
 
 
 def write(name, rows, fields=FIELDS):
@@ -359,3 +436,7 @@ def lowhead():
 
 if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "lowhead":
     lowhead()
+
+
+if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "regress_policies":
+    regress_policies()

@@ -53,8 +53,23 @@ def _expected_launch(b, hq, hkv, lk, pack, s, U):
 
 
 # cluster combine when every cluster of the launch is co-resident in one wave
-# (B200 table of cudaOccupancyMaxActiveClusters at the cluster kernel's shared memory).
-_FIT = [0, 148, 74, 45, 33, 26, 22, 15, 15, 15, 11, 7, 7, 7, 7, 7, 7]
+# (the measured B200 record of cudaOccupancyMaxActiveClusters for the cluster kernels, loaded by the
+# oracle from profiles/cluster_fit_b200.json).
+_FIT = list(OP.CLUSTER_FIT_B200)
+
+
+def test_cluster_fit_table_single_source():
+    # the planner's compiled-in copy (config.h kMaxActiveClustersB200) equals the measured record
+    import json
+    with open(os.path.join(ROOT, "paper_2604_00028_b200", "csrc", "config.h")) as f:
+        src = f.read()
+    m = re.search(r"kMaxActiveClustersB200\[17\]\s*=\s*\{([^}]*)\}", src)
+    table = [int(x) for x in m.group(1).split(",")]
+    with open(os.path.join(ROOT, "profiles", "cluster_fit_b200.json")) as f:
+        rec = json.load(f)
+    assert rec["device"].startswith("NVIDIA B200") and rec["sms"] == 148 and rec["variants_agree"]
+    assert table[1:] == rec["max_active_clusters"][1:]
+    assert list(OP.CLUSTER_FIT_B200) == rec["max_active_clusters"]
 
 
 def _expected_combine(b, hq, hkv, lk, pack, sms, s, U):

@@ -135,8 +135,8 @@ def test_forward_peer_combine_times_out_on_a_missing_peer(batch, h_q, h_kv, l_k,
     assert int(status.item()) == dec.DA_ERR_TIMEOUT
     assert elapsed < 5.0                                 # bounded: no hang (every thread gives up)
     assert int(epoch.item()) == 1 and int(counter.item()) == 0   # the step still completes its bookkeeping
-    # this rank's own LL words were published with epoch 1
-    words = bufs[0].view(torch.int64)[llo // 8: (llo + lls) // 8][: batch * h_q * 129]
+    # this rank's own LL words were published with epoch 1, in LL slot 1 & 1 = 1
+    words = bufs[0].view(torch.int64)[(llo + lls) // 8: (llo + 2 * lls) // 8][: batch * h_q * 129]
     assert bool(((words >> 32) == 1).all())
 
 
