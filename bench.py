@@ -200,6 +200,7 @@ def make_graph(dec, plan, w: Workload, steps: int, stream):
     with torch.cuda.stream(stream):
         g.replay()
     torch.cuda.synchronize()
+    g.keepalive = ws          # the graph reads the workspace: it must outlive the graph
     return g
 
 

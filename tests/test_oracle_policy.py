@@ -331,14 +331,18 @@ def _measured_grid(tag="r01h"):
     return grid
 
 
-def test_seq_aware_sm_calibration_lowhead():
-    """The 48 shapes of BASELINE configs[2] (profiles/r01i_lowhead.csv: guarded, the paper's rule and
-    the SM-count-aware pick, interleaved): every current pick was measured and is never > 2 %
-    behind guarded; at L_K = 512 it beats guarded by >= 1.2x for every T <= 32."""
+@pytest.mark.parametrize("tag,bound", [("r01i", 1.02), ("r02a", 1.01)])
+def test_seq_aware_sm_calibration_lowhead(tag, bound):
+    """The 48 shapes of BASELINE configs[2] (profiles/<tag>_lowhead.csv: guarded, the paper's rule and
+    the SM-count-aware pick, interleaved): every current pick was measured and is never more than
+    1 % behind guarded - the paper's no-regression bar (>= 0.99x) - on the round-2 harness
+    (r02a: identical plans share one graph, random arm order, host submission outside the timed
+    region), 2 % on the round-1 harness (r01i, whose same-plan noise was ~2-4 %); at L_K = 512 it
+    beats guarded by >= 1.2x for every T <= 32."""
     import csv
     import os
     path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles",
-                        "r01i_lowhead.csv")
+                        f"{tag}_lowhead.csv")
     meas = {}
     with open(path) as fh:
         for r in csv.DictReader(fh):
@@ -349,18 +353,19 @@ def test_seq_aware_sm_calibration_lowhead():
         s, _ = P.num_splits(b, 8 * hkv, hkv, lk, B200_SMS, 0, "seq_aware_sm")
         g, _ = P.num_splits(b, 8 * hkv, hkv, lk, B200_SMS, 0, "guarded")
         assert s in t and g in t, (b, hkv, lk, s)
-        assert t[s] <= 1.02 * t[g], (b, hkv, lk, s, g)
+        assert t[s] <= bound * t[g], (b, hkv, lk, s, g)
         if lk == 512 and b * hkv <= 32:
             assert t[g] / t[s] >= 1.2, (b, hkv, lk, s)
 
 
-@pytest.mark.parametrize("tag", ["r01h", "r01j"])
-def test_seq_aware_sm_calibration(tag):
+@pytest.mark.parametrize("tag,bound", [("r01h", 1.02), ("r01j", 1.02), ("r02a", 1.01)])
+def test_seq_aware_sm_calibration(tag, bound):
     """C-ext-1's constants against the B200 measurements they were calibrated on
-    (profiles/r01h_ugrid*.csv, forced-s latencies, G = 8) and against the same grids re-measured
-    on the final round-1 kernel (r01j): the pick is within 6 % of the best measured split (an
-    unmeasured pick lies between two measured neighbours) and never slower than the guarded pick
-    beyond the 2 % A/B noise of these grids."""
+    (profiles/r01h_ugrid*.csv, forced-s latencies, G = 8), against the same grids re-measured
+    on the final round-1 kernel (r01j) and on the round-2 harness (r02a): the pick is within 6 % of
+    the best measured split (an unmeasured pick lies between two measured neighbours) and never
+    slower than the guarded pick by more than the paper's no-regression bar, 1 % (>= 0.99x,
+    P:L179), on the r02a grids; 2 % on the round-1 grids, whose harness noise was ~2-4 %."""
     grid = _measured_grid(tag)
     assert len(grid) >= 60
     for (b, hkv, lk), t in grid.items():
@@ -373,7 +378,7 @@ def test_seq_aware_sm_calibration(tag):
             ts = t[s]
         assert ts <= 1.06 * min(t.values()), (b, hkv, lk, s)
         if g in t:
-            assert ts <= 1.02 * t[g], (b, hkv, lk, s, g)
+            assert ts <= bound * t[g], (b, hkv, lk, s, g)
 
 
 # ---- per-batch dynamic split counts (C-ext-2) -----------------------------------
