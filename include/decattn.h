@@ -416,6 +416,13 @@ DA_API da_status da_forward_peer(const da_plan* plan, const void* q, const void*
  * through the combine kernel) with B * H_Q combine CTAs (workspace, workspace_bytes as
  * da_forward); DA_ERR_UNSUPPORTED otherwise (use da_forward_peer + da_combine_peers).
  * status, timeout_ns: the bounded wait of da_combine_peers, for the LL words.
+ * rank = -1 (testing the multi-rank protocol on ONE GPU, where separate launches cannot be made to
+ *   wait on one another): one launch runs every rank's grid along z (NONE / CLUSTER plans only,
+ *   DA_ERR_UNSUPPORTED otherwise; the residency check covers all world grids).  Then k_cache /
+ *   v_cache hold the world shards stacked along the batch dimension ([world * B, l_cap, H_KV, d],
+ *   rank r's sequence b at cache batch r * B + b), cache_seqlens is [world * B] (or NULL), epoch
+ *   and counter are arrays [world], out is [world, B, H_Q, d] and lse [world, B, H_Q] (or NULL):
+ *   emulated rank r publishes into peer_bases[r], polls every rank's words and writes out[r].
  * Errors: as da_forward; DA_ERR_INVALID_ARG for world / rank / NULL pointers / a short LL slot,
  * DA_ERR_ALIGNMENT for misaligned offsets, counter, epoch, status, out or lse; DA_ERR_CUDA when the
  * occupancy query fails.

@@ -195,7 +195,9 @@ da_status forward_impl(const da_plan* plan, const void* q, const void* k_cache, 
   }
 
   CUtensorMap tk, tv;
-  const int32_t major = paged ? pg.num_pages : plan->batch;
+  // multi-rank emulation (da_forward_peer_combine, rank = -1): the cache holds every rank's shard
+  const int32_t emul = (pub != nullptr && pub->emulate) ? pub->world : 1;
+  const int32_t major = paged ? pg.num_pages : plan->batch * emul;
   const int32_t rows = paged ? pg.page_size : l_cap;
   if (!make_kv_tmap(&tk, k_cache, major, rows, plan->h_kv, sd[2], sd[3], sd[4]) ||
       !make_kv_tmap(&tv, v_cache, major, rows, plan->h_kv, sd[5], sd[6], sd[7]))
@@ -236,7 +238,10 @@ da_status forward_impl(const da_plan* plan, const void* q, const void* k_cache, 
   }
 
   cudaStream_t stream = static_cast<cudaStream_t>(cuda_stream);
-  if (launch_split_kv_fwd(*plan, tk, tv, p, stream) != cudaSuccess) return DA_ERR_CUDA;
+  da_plan lp = *plan;
+  lp.grid_z *= emul;                            // every emulated rank's grid in one launch
+  if (lp.grid_z > 65535) return DA_ERR_UNSUPPORTED;
+  if (launch_split_kv_fwd(lp, tk, tv, p, stream) != cudaSuccess) return DA_ERR_CUDA;
   if (plan->combine_mode == DA_COMBINE_KERNEL) {
     CombineParams c{};
     c.o = ws_o;
@@ -455,10 +460,12 @@ extern "C" da_status da_forward_peer_combine(const da_plan* plan, const void* q,
                                              int32_t out_dtype, void* out, float* lse, int32_t* status,
                                              int64_t timeout_ns, void* workspace, int64_t workspace_bytes,
                                              void* cuda_stream) {
-  if (plan == nullptr || world < 1 || world > kMaxPeers || rank < 0 || rank >= world || peer_bases == nullptr ||
+  // rank = -1: emulate all `world` ranks in this one launch (tests on one GPU; include/decattn.h)
+  if (plan == nullptr || world < 1 || world > kMaxPeers || rank < -1 || rank >= world || peer_bases == nullptr ||
       epoch == nullptr || counter == nullptr || out == nullptr || status == nullptr ||
       (out_dtype != DA_BF16 && out_dtype != DA_F32))
     return DA_ERR_INVALID_ARG;
+  const bool emulate = rank < 0;
   if ((reinterpret_cast<uintptr_t>(status) & 3u) != 0) return DA_ERR_ALIGNMENT;
   if (plan->head_dim != kHeadDim) return DA_ERR_UNSUPPORTED;
   const int64_t rows = int64_t(plan->batch) * plan->h_q;
@@ -478,10 +485,12 @@ extern "C" da_status da_forward_peer_combine(const da_plan* plan, const void* q,
   // a bound no device can beat (one forward CTA per SM: its shared memory; 32 CTAs per SM) and the
   // workspace, then the query.
   const bool kernel_ws = plan->combine_mode == DA_COMBINE_KERNEL;
-  const int64_t need = kernel_ws ? rows
+  if (emulate && kernel_ws) return DA_ERR_UNSUPPORTED;   // emulation: one-kernel (NONE / CLUSTER) plans only
+  const int64_t ranks_here = emulate ? world : 1;
+  const int64_t need = ranks_here * (kernel_ws ? rows
                        : plan->combine_mode == DA_COMBINE_CLUSTER ? int64_t(plan->grid_y) * plan->grid_z
-                                                                  : int64_t(plan->grid_x) * plan->grid_y * plan->grid_z;
-  const int64_t ctas = kernel_ws ? rows : int64_t(plan->grid_x) * plan->grid_y * plan->grid_z;
+                                                                  : int64_t(plan->grid_x) * plan->grid_y * plan->grid_z);
+  const int64_t ctas = ranks_here * (kernel_ws ? rows : int64_t(plan->grid_x) * plan->grid_y * plan->grid_z);
   if (ctas > int64_t(plan->usable_sms) * (kernel_ws ? 32 : 1)) return DA_ERR_UNSUPPORTED;
   if (kernel_ws && (workspace == nullptr || workspace_bytes < plan->workspace_bytes)) return DA_ERR_WORKSPACE;
   int units = 0;
@@ -494,7 +503,8 @@ extern "C" da_status da_forward_peer_combine(const da_plan* plan, const void* q,
   pub.ll_offset = ll_offset;
   pub.ll_slot_bytes = ll_slot_bytes;
   pub.world = world;
-  pub.rank = rank;
+  pub.rank = emulate ? 0 : rank;
+  pub.emulate = emulate ? 1 : 0;
   pub.out = out;
   pub.lse = lse;
   pub.out_f32 = out_dtype == DA_F32;

@@ -417,6 +417,16 @@ __global__ void __launch_bounds__(threads_for(NW, helpers_for(kCombine)), 1)
   const int grp = kDyn ? blockIdx.x : blockIdx.y;
   const uint32_t dslot = kDyn ? blockIdx.y : 0u;
   int split = blockIdx.x, b = blockIdx.z;       // kDyn: assigned from the schedule below
+  // batch index of the K / V cache and cache_seqlens: b, except under multi-rank emulation
+  // (kPub == 2, tests on one GPU), where z spans every rank's batch and the rank's shard sits at
+  // cache batch z while q / out use b = z mod B
+  int bkv = blockIdx.z, erank = 0;
+  if constexpr (kPub == 2) {
+    if (p.pub.emulate) {
+      erank = blockIdx.z / p.batch;
+      b = blockIdx.z - erank * p.batch;
+    }
+  }
   bool dyn_single = false;                       // kDyn: this sequence has one split (s_b = 1)
   int kvh, hq0, rows_valid;
   if constexpr (kPath == DA_PATH_MMA) {
@@ -462,7 +472,7 @@ __global__ void __launch_bounds__(threads_for(NW, helpers_for(kCombine)), 1)
     prefetch_tmap(&tmap_v);
     // the lengths are read right after griddepcontrol.wait: pull their line into L2 now (a
     // prefetch never returns data, so it cannot observe a stale value)
-    if (!kDyn && p.seqlens != nullptr) prefetch_l2(p.seqlens + b);
+    if (!kDyn && p.seqlens != nullptr) prefetch_l2(p.seqlens + bkv);
   }
   if (kDyn && warp == NW && p.seqlens != nullptr && lane * 32 < p.batch)
     prefetch_l2(p.seqlens + lane * 32);          // the first 1024 lengths, one 128-byte line per lane
@@ -502,8 +512,8 @@ __global__ void __launch_bounds__(threads_for(NW, helpers_for(kCombine)), 1)
     if (DECATTN_SPECULATE || p.seqlens == nullptr) {
       if (warp == NW && lane == 0 && n_tiles >= 1 && n_tiles <= 2 * NS && p.block_table == nullptr) {
         const int np = min(n_tiles, NS);
-        for (int i = 0; i < np; ++i) tma_prefetch_5d(&tmap_k, 0, t0 + i * kTileN, 0, kvh, b);
-        for (int i = 0; i < np; ++i) tma_prefetch_5d(&tmap_v, 0, t0 + i * kTileN, 0, kvh, b);
+        for (int i = 0; i < np; ++i) tma_prefetch_5d(&tmap_k, 0, t0 + i * kTileN, 0, kvh, bkv);
+        for (int i = 0; i < np; ++i) tma_prefetch_5d(&tmap_v, 0, t0 + i * kTileN, 0, kvh, bkv);
       }
     }
   }
@@ -541,7 +551,7 @@ __global__ void __launch_bounds__(threads_for(NW, helpers_for(kCombine)), 1)
     t_end = min(static_cast<int>(u1) * kTileN, r.w);
     n_tiles = static_cast<int>(u1 - u0);
   } else if (p.seqlens != nullptr) {
-    split_range(min(max(__ldg(p.seqlens + b), 0), p.l_cap), split, p.num_splits, p.s_magic, t0, t_end, n_tiles);
+    split_range(min(max(__ldg(p.seqlens + bkv), 0), p.l_cap), split, p.num_splits, p.s_magic, t0, t_end, n_tiles);
   }
 
   if (warp == NW) {
@@ -553,13 +563,13 @@ __global__ void __launch_bounds__(threads_for(NW, helpers_for(kCombine)), 1)
         for (int i = 0; i < n_tiles; ++i) {
           const uint32_t fb = smem_u32(&full_bar[i]);
           mbar_arrive_expect_tx(fb, kStageBytes / 2);
-          tma_load_5d(sbase + i * kStageBytes, &tmap_k, fb, 0, t0 + i * kTileN, 0, kvh, b);
+          tma_load_5d(sbase + i * kStageBytes, &tmap_k, fb, 0, t0 + i * kTileN, 0, kvh, bkv);
           if (i < 8) TRACE(2 + i);
         }
         for (int i = 0; i < n_tiles; ++i) {
           const uint32_t fvb = smem_u32(&fullv_bar[i]);
           mbar_arrive_expect_tx(fvb, kStageBytes / 2);
-          tma_load_5d(sbase + i * kStageBytes + 2 * kHalfBytes, &tmap_v, fvb, 0, t0 + i * kTileN, 0, kvh, b);
+          tma_load_5d(sbase + i * kStageBytes + 2 * kHalfBytes, &tmap_v, fvb, 0, t0 + i * kTileN, 0, kvh, bkv);
         }
       } else if (p.block_table == nullptr) {
         for (int i = 0; i < n_tiles; ++i) {
@@ -571,8 +581,8 @@ __global__ void __launch_bounds__(threads_for(NW, helpers_for(kCombine)), 1)
           mbar_arrive_expect_tx(fvb, kStageBytes / 2);
           const uint32_t dst = sbase + st * kStageBytes;
           const int t = t0 + i * kTileN;
-          tma_load_5d(dst, &tmap_k, fb, 0, t, 0, kvh, b);                   // K: both 64-dim halves
-          tma_load_5d(dst + 2 * kHalfBytes, &tmap_v, fvb, 0, t, 0, kvh, b);  // V
+          tma_load_5d(dst, &tmap_k, fb, 0, t, 0, kvh, bkv);                   // K: both 64-dim halves
+          tma_load_5d(dst + 2 * kHalfBytes, &tmap_v, fvb, 0, t, 0, kvh, bkv);  // V
           if (i < 8) TRACE(2 + i);
         }
       } else {
@@ -762,7 +772,8 @@ __global__ void __launch_bounds__(threads_for(NW, helpers_for(kCombine)), 1)
   void* o_dst = p.out;
   float* l_dst = p.lse;
   uint32_t e_pub = 0;
-  if constexpr (kPub != 0) e_pub = pub_epoch(p.pub);
+  if constexpr (kPub == 1) e_pub = pub_epoch(p.pub);
+  if constexpr (kPub == 2) e_pub = pub_epoch(pub_rank_view(p.pub, erank, static_cast<size_t>(p.batch) * p.h_q));
   if constexpr (kPub == 1) {
     const uint64_t sb = pub_slot(p.pub);
     o_dst = reinterpret_cast<void*>(sb);
@@ -780,7 +791,7 @@ __global__ void __launch_bounds__(threads_for(NW, helpers_for(kCombine)), 1)
       const size_t row = static_cast<size_t>(b) * p.h_q + hq0 + g;
       if (kCombine == DA_COMBINE_NONE || (kDyn && dyn_single && !p.dyn_via_combine)) {   // kDyn, s_b = 1: the final row
         if constexpr (kPub == 2) {
-          pub_ll_store(p.pub, e_pub, row, d4, v, lse_v);
+          pub_ll_store(pub_rank_view(p.pub, erank, static_cast<size_t>(p.batch) * p.h_q), e_pub, row, d4, v, lse_v);
         } else {
           store_out(p, o_dst, row, d4, v);
           if (d4 == 0 && l_dst != nullptr) l_dst[row] = lse_v;
@@ -854,7 +865,8 @@ __global__ void __launch_bounds__(threads_for(NW, helpers_for(kCombine)), 1)
       const float inv = Lsum > 0.f ? __frcp_rn(Lsum) : 0.f;
       const size_t row = static_cast<size_t>(b) * p.h_q + hq0 + g;
       if constexpr (kPub == 2) {
-        pub_ll_store(p.pub, e_pub, row, d4, make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv),
+        pub_ll_store(pub_rank_view(p.pub, erank, static_cast<size_t>(p.batch) * p.h_q), e_pub, row, d4,
+                     make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv),
                      Lsum > 0.f ? (M + lg2(Lsum)) * kLn2 : kNegInf);
       } else {
         store_out(p, o_dst, row, d4, make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv));
@@ -873,13 +885,14 @@ __global__ void __launch_bounds__(threads_for(NW, helpers_for(kCombine)), 1)
     // LSE-merged here (the cross-GPU combine fused into the forward; the grid is one wave, so the
     // spinning is safe); the epoch advances once every CTA has read it
     __syncthreads();
-    if (threadIdx.x == 0) pub_count_advance(p.pub, e_pub);
+    const PubParams pbr = pub_rank_view(p.pub, erank, static_cast<size_t>(p.batch) * p.h_q);
+    if (threadIdx.x == 0) pub_count_advance(pbr, e_pub);
     const int s = kCluster ? s_cl : 1;
     for (int t = threadIdx.x; t < rows_per_owner * 32; t += kT) {
       const int rl = t >> 5, d4 = t & 31;
       const int g = static_cast<int>(rank) + rl * s;
       if (g >= rows_valid) break;
-      pub_ll_merge_row(p.pub, e_pub, static_cast<size_t>(b) * p.h_q + hq0 + g, d4);
+      pub_ll_merge_row(pbr, e_pub, static_cast<size_t>(b) * p.h_q + hq0 + g, d4);
     }
   }
 #ifdef DECATTN_TRACE

@@ -33,6 +33,10 @@ struct PubParams {
   // first failed poll ends the wait and sets *status = DA_EXCHANGE_TIMEOUT (the kernel completes)
   int32_t* status;
   uint64_t timeout_ns;
+  // multi-rank emulation (da_forward_peer_combine with rank = -1; tests on one GPU): the launch
+  // holds all `world` ranks' grids along z (rank r's CTAs at z in [r B, (r + 1) B), its K / V shard
+  // at cache batches r B ..), and rank r has its own epoch[r], count[r], out[r] and lse[r]
+  int32_t emulate;
 };
 
 struct FwdParams {

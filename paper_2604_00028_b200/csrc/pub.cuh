@@ -133,6 +133,21 @@ static __device__ __forceinline__ void pub_count_advance(const PubParams& pb, ui
   *reinterpret_cast<volatile int32_t*>(pb.epoch) = static_cast<int32_t>(e);
 }
 
+// The exchange parameters of the rank this CTA acts for: the caller's rank, or under multi-rank
+// emulation (PubParams::emulate) rank `erank` with its own epoch, count, output and lse
+// (`rows` = B H_Q rows per rank).
+static __device__ __forceinline__ PubParams pub_rank_view(const PubParams& pb, int erank, size_t rows) {
+  PubParams v = pb;
+  if (pb.emulate) {
+    v.rank = erank;
+    v.epoch = pb.epoch + erank;
+    v.count = pb.count + erank;
+    v.out = static_cast<char*>(pb.out) + rows * static_cast<size_t>(erank) * 128 * (pb.out_f32 ? 4 : 2);
+    if (pb.lse != nullptr) v.lse = pb.lse + rows * static_cast<size_t>(erank);
+  }
+  return v;
+}
+
 // The epoch this step publishes (e = *epoch + 1), read before the CTA counts itself.
 static __device__ __forceinline__ uint32_t pub_epoch(const PubParams& pb) {
   return static_cast<uint32_t>(*reinterpret_cast<const volatile int32_t*>(pb.epoch)) + 1u;

@@ -15,7 +15,8 @@ sys.path.insert(0, ROOT)
 import synth  # noqa: E402
 
 CONFIGS = {"llama70b": synth.CONFIGS["llama70b"], "llama70b_tp8": synth.CONFIGS["llama70b_tp8"],
-           "long_context": synth.CONFIGS["long_context"], "high_load": synth.CONFIGS["high_load"]}
+           "long_context": synth.CONFIGS["long_context"], "long_context_sm": synth.CONFIGS["long_context"],
+           "high_load": synth.CONFIGS["high_load"]}
 
 
 def alg_bytes(c, d=128):

@@ -17,8 +17,11 @@ run() {   # name, command
     ncu -i $OUT/full_$name.ncu-rep --page details > $OUT/details_$name.txt 2>/dev/null
   echo "$name rc=$?"
 }
+# the headline (bench.py defaults: high_load, seq_aware_sm = s 1), the latency configs, and both
+# long-context plans the bench's roofline_streaming times (the paper's rule s = 16 workspace, C-ext-1 s = 10)
+run high_load python bench.py --steps 3 --warmup 3 --no-extras --cpu-seconds 1
 run llama70b python bench.py --workload llama70b --steps 20 --warmup 3 --no-extras --cpu-seconds 1
 run llama70b_tp8 python bench.py --workload llama70b_tp8 --steps 20 --warmup 3 --no-extras --cpu-seconds 1
-run long_context python bench.py --workload long_context --steps 5 --warmup 3 --no-extras --cpu-seconds 1
-run high_load python bench.py --workload high_load --steps 3 --warmup 3 --no-extras --cpu-seconds 1
+run long_context python bench.py --workload long_context --policy seq_aware --steps 5 --warmup 3 --no-extras --cpu-seconds 1
+run long_context_sm python bench.py --workload long_context --steps 5 --warmup 3 --no-extras --cpu-seconds 1
 ls -la $OUT

@@ -7,6 +7,7 @@ Slots (globaltimer ns): 0 entry, 1 after griddepcontrol.wait, 2+i TMA issued til
 """
 import ctypes
 import os
+import statistics
 import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -75,6 +76,12 @@ def trace(b, hq, hkv, lk, policy, forced=0, steps=50, combine=None):
         if r[60] and r[61] and r[30] > r[0]:
             parts.append(f"clk={(int(r[61]) - int(r[60])) / (int(r[30]) - int(r[0])) * 1e3:.0f}MHz")
         print(f"  cta{c}: " + " ".join(parts))
+    # spread over every traced CTA (first 64): when each started streaming and when each finished
+    def spread(j):
+        v = [int(r[j]) - t0 for r in rows if r[j]]
+        return (min(v), statistics.median(v), max(v)) if v else None
+    print(f"  spread over {len(rows)} CTAs (min / median / max ns): pdl_wait={spread(1)} first_ready={spread(10)} "
+          f"epi={spread(26)} end={spread(30)}")
     if plan.combine_mode == L.DA_COMBINE_KERNEL and hasattr(L.LIB, "da_trace_fetch_combine"):
         cb = (ctypes.c_ulonglong * (64 * 4))()
         L.LIB.da_trace_fetch_combine(ctypes.addressof(cb), 64 * 4)
@@ -91,6 +98,12 @@ if __name__ == "__main__":
     if which == "latency":
         trace(1, 8, 1, 512, "seq_aware_sm")
         trace(1, 64, 8, 512, "seq_aware_sm")
+    elif which == "long":
+        os.environ.setdefault("TRACE_NBUF", "1")
+        trace(1, 64, 8, 131072, "seq_aware_sm", steps=10)
+        trace(1, 64, 8, 131072, "seq_aware", steps=10)
+        trace(1, 64, 8, 131072, "fixed", 18, steps=10, combine=2)
+        trace(1, 8, 1, 131072, "fixed", 64, steps=10, combine=2)
     elif which == "kernel":
         trace(1, 8, 1, 768, "fixed", 16, combine=1)
         trace(1, 8, 1, 768, "fixed", 16, combine=2)

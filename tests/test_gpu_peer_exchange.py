@@ -212,3 +212,71 @@ def test_nccl_seq_sharded_matches_oracle(one_rank_group, batch, h_q, h_kv, l_k, 
     torch.cuda.synchronize()
     assert_out_close(synth.to_f64(out), ref_o)
     assert_lse_close(synth.to_f64(lse), ref_l)
+
+
+# ---- the multi-rank LL protocol with world > 1, emulated in ONE launch on one GPU --------------------
+# (separate launches that spin on each other's words are not guaranteed to be co-scheduled on one GPU:
+#  da_forward_peer_combine with rank = -1 runs every rank's grid in a single launch instead)
+@pytest.mark.parametrize("world,batch,h_q,h_kv,l_total,policy", [
+    (2, 2, 64, 8, 1024, "guarded"),        # s = 1 NONE plans, ragged lengths (an empty and a 1-token sequence)
+    (4, 1, 8, 1, 4096, "seq_aware_sm"),    # cluster plans: the owner CTAs of each rank exchange
+    (8, 1, 64, 8, 4095, "seq_aware"),      # world 8, shards of 511 / 512 tokens (lengths per rank)
+    (3, 3, 24, 3, 1500, "seq_aware_sm"),
+])
+def test_emulated_ranks_one_kernel_exchange(world, batch, h_q, h_kv, l_total, policy):
+    import paper_2604_00028_b200 as dec
+    from paper_2604_00028_b200 import _lib as L
+    from paper_2604_00028_b200.dist import peer_layout, shard_range
+    inp = synth.make_inputs(batch, h_q, h_kv, l_total, seed=1640, device="cuda",
+                            variant="ragged" if batch >= 2 else "normal")
+    ref_o, ref_l = OA.decode_attention(*(synth.to_f64(inp[n]) for n in ("q", "k", "v", "seqlens")))
+    shards = [shard_range(l_total, r, world) for r in range(world)]
+    l_cap = max(t1 - t0 for t0, t1 in shards)
+    k = torch.full((world * batch, l_cap, h_kv, 128), float("nan"), dtype=torch.bfloat16, device="cuda")
+    v = torch.full_like(k, float("nan"))
+    lens = torch.zeros(world * batch, dtype=torch.int32)
+    for r, (t0, t1) in enumerate(shards):
+        k[r * batch:(r + 1) * batch, : t1 - t0] = inp["k"][:, t0:t1]
+        v[r * batch:(r + 1) * batch, : t1 - t0] = inp["v"][:, t0:t1]
+        for b in range(batch):
+            lens[r * batch + b] = min(max(int(inp["seqlens"][b]) - t0, 0), t1 - t0)
+    lens = lens.to("cuda")
+    plan = dec.make_plan(batch, h_q, h_kv, l_cap, policy=policy)
+    assert plan.combine_mode in (0, 1)
+    lay = peer_layout(batch, h_q, 128, world)
+    slot, lo, fo, llo, lls, tot = lay
+    bufs = [torch.zeros(tot // 4, dtype=torch.float32, device="cuda") for _ in range(world)]
+    bases = torch.tensor([x.data_ptr() for x in bufs], dtype=torch.int64, device="cuda")
+    epoch = torch.zeros(world, dtype=torch.int32, device="cuda")
+    counter = torch.zeros(world, dtype=torch.int32, device="cuda")
+    status = torch.zeros(1, dtype=torch.int32, device="cuda")
+    out = torch.empty((world, batch, h_q, 128), dtype=torch.float32, device="cuda")
+    lse = torch.empty((world, batch, h_q), dtype=torch.float32, device="cuda")
+    strides = (inp["q"].stride(0), inp["q"].stride(1), k.stride(0), k.stride(1), k.stride(2),
+               v.stride(0), v.stride(1), v.stride(2))
+    for e in range(1, 6):                                 # both LL slots, several epochs
+        out.zero_()
+        L.da_forward_peer_combine(plan, inp["q"], k, v, l_cap, lens, strides, 0.0, world, -1, bases, llo, lls,
+                                  epoch, counter, L.DA_F32, out, lse, status, 2_000_000_000)
+        torch.cuda.synchronize()
+        assert int(status.item()) == 0
+        for r in range(world):                            # every emulated rank holds the full result
+            assert_out_close(synth.to_f64(out[r]), ref_o, f"rank {r} out")
+            assert_lse_close(synth.to_f64(lse[r]), ref_l, f"rank {r} lse")
+        assert epoch.tolist() == [e] * world and counter.tolist() == [0] * world
+
+
+def test_emulation_validation():
+    import paper_2604_00028_b200 as dec
+    from paper_2604_00028_b200 import _lib as L
+    plan = dec.make_plan(1, 64, 8, 131072, policy="seq_aware")           # s = 16: workspace combine
+    x = torch.zeros(4, dtype=torch.int64, device="cuda")
+    with pytest.raises(L.DecAttnError) as e:
+        L.da_forward_peer_combine(plan, x, x, x, 131072, None, None, 0.0, 2, -1, x, 0, 8 * 129 * 64, x, x, L.DA_F32,
+                                  x, x, x, 0, x, 1 << 30)
+    assert e.value.status == L.DA_ERR_UNSUPPORTED
+    big = dec.make_plan(1, 64, 8, 1024, policy="guarded")                 # s = 7 clusters: 8 per rank
+    with pytest.raises(L.DecAttnError) as e:
+        L.da_forward_peer_combine(big, x, x, x, 1024, None, None, 0.0, 8, -1, x, 0, 8 * 129 * 64, x, x, L.DA_F32,
+                                  x, x, x, 0)
+    assert e.value.status == L.DA_ERR_UNSUPPORTED                        # 8 ranks x 8 clusters do not fit
