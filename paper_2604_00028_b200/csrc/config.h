@@ -75,6 +75,23 @@ DA_HD constexpr int helpers_for(int combine_mode) { return combine_mode == 1 ? D
 #ifndef DECATTN_SPECULATE
 #define DECATTN_SPECULATE 1   // prefetch the plan-length range also when cache_seqlens is given
 #endif
+// Tail balancing of cluster plans: when every split holds >= kBalMinTiles tiles, each
+// CTA streams the first (1 - 1/kBalTailDiv) of its range and the last 1/kBalTailDiv of every range is
+// pooled in chunks of kBalChunk tiles, handed out by a ticket counter in rank 0's shared memory, so
+// CTAs on faster SMs take more of the pool and the cluster's CTAs end together.
+#ifndef DECATTN_BAL_MIN_TILES
+#define DECATTN_BAL_MIN_TILES 32
+#endif
+#ifndef DECATTN_BAL_TAIL_DIV
+#define DECATTN_BAL_TAIL_DIV 4
+#endif
+#ifndef DECATTN_BAL_CHUNK
+#define DECATTN_BAL_CHUNK 4
+#endif
+constexpr int kBalMinTiles = DECATTN_BAL_MIN_TILES, kBalTailDiv = DECATTN_BAL_TAIL_DIV, kBalChunk = DECATTN_BAL_CHUNK;
+#ifndef DECATTN_PREFETCH_LONG
+#define DECATTN_PREFETCH_LONG 1   // the pre-wait L2 prefetch of the first ring tiles also for long splits
+#endif
 constexpr int kMaxPageSize = 1 << 18;     // da_forward_paged: tiles per page < 2^13 (exact magic division)
 constexpr int kMaxClusterSplits = 16;
 constexpr int kMaxPeers = 64;          // da_peer_signal / da_combine_peers: ranks of one exchange  // cluster combine up to 16 CTAs (non-portable size, B200)

@@ -400,6 +400,12 @@ __global__ void __launch_bounds__(threads_for(NW, helpers_for(kCombine)), 1)
   __shared__ __align__(8) uint64_t fullv_bar[NS];   // V of the stage has landed (QK^T need not wait)
   __shared__ __align__(8) uint64_t empty_bar[NS];
   __shared__ __align__(8) uint64_t push_bar;              // CLUSTER: pushes of the rows this CTA owns
+  // tail balancing (cluster plans with long splits): the tile each ring stage holds, written by the
+  // producer before it arms the stage (-1: no more tiles for the warp that owns the stage), and the
+  // cluster's ticket counter for the pooled tail chunks (rank 0's copy is the one used)
+  constexpr bool kBalCapable = kCluster && !kDyn && kPub == 0;
+  __shared__ int stage_tile[kBalCapable ? NS : 1];
+  __shared__ uint32_t bal_next;
 
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t sbase = (raw + 1023u) & ~1023u;
@@ -457,6 +463,7 @@ __global__ void __launch_bounds__(threads_for(NW, helpers_for(kCombine)), 1)
       mbar_init(smem_u32(&fullv_bar[i]), 1);
       mbar_init(smem_u32(&empty_bar[i]), 1);
     }
+    if constexpr (kBalCapable) bal_next = 0u;
     if constexpr (kCluster) {
       // expect s pushes (every rank, this one included) of (O row, m, l) for every valid row
       // this rank owns, counted in st.async bytes
@@ -505,12 +512,13 @@ __global__ void __launch_bounds__(threads_for(NW, helpers_for(kCombine)), 1)
         if (++k == tpp) { k = 0; ++j; }
       }
     }
-    // short splits (<= 2 NS tiles: the latency regime): pull the tiles the ring loads first into L2
-    // while the previous kernel drains; L2 is the point of coherence, so the loads after
-    // griddepcontrol.wait still see the preceding kernel's writes (Llama 3.57 -> 3.12 us).  A wrong
-    // guess only costs DRAM reads.
+    // pull the tiles the ring loads first into L2 while the previous kernel drains; L2 is the point
+    // of coherence, so the loads after griddepcontrol.wait still see the preceding kernel's writes
+    // (latency regime: Llama 3.57 -> 3.12 us; streaming splits: the DRAM idles less between
+    // kernels).  A wrong guess only costs DRAM reads.
     if (DECATTN_SPECULATE || p.seqlens == nullptr) {
-      if (warp == NW && lane == 0 && n_tiles >= 1 && n_tiles <= 2 * NS && p.block_table == nullptr) {
+      if (warp == NW && lane == 0 && n_tiles >= 1 && (DECATTN_PREFETCH_LONG || n_tiles <= 2 * NS) &&
+          p.block_table == nullptr) {
         const int np = min(n_tiles, NS);
         for (int i = 0; i < np; ++i) tma_prefetch_5d(&tmap_k, 0, t0 + i * kTileN, 0, kvh, bkv);
         for (int i = 0; i < np; ++i) tma_prefetch_5d(&tmap_v, 0, t0 + i * kTileN, 0, kvh, bkv);
@@ -553,11 +561,66 @@ __global__ void __launch_bounds__(threads_for(NW, helpers_for(kCombine)), 1)
   } else if (p.seqlens != nullptr) {
     split_range(min(max(__ldg(p.seqlens + bkv), 0), p.l_cap), split, p.num_splits, p.s_magic, t0, t_end, n_tiles);
   }
+  // tail balancing (kBalCapable): every split of this sequence holds >= kBalMinTiles tiles (uniform
+  // over the cluster: one sequence, one length); n_seq = the sequence's length
+  bool bal = false;
+  int n_seq = 0, tail_chunks = 0;
+  if constexpr (kBalCapable) {
+    n_seq = min(max(p.seqlens != nullptr ? __ldg(p.seqlens + bkv) : p.l_default, 0), p.l_cap);
+    const int nu = (n_seq + kTileN - 1) / kTileN;
+    bal = p.block_table == nullptr && nu >= kBalMinTiles * p.num_splits;
+    tail_chunks = nu / p.num_splits / kBalTailDiv / kBalChunk;   // pooled chunks per split (>= 2)
+  }
 
   if (warp == NW) {
     // ================= TMA producer =================
+    if constexpr (kBalCapable) {
+      if (bal) cluster_wait();       // rank 0's ticket counter is initialised (the epilogue skips it)
+    }
     if (lane == 0) {
-      if (p.block_table == nullptr && n_tiles <= NS) {
+      if (kBalCapable && bal) {
+        // the head of this split's range, [t0, t_end - pooled tail), then pooled tail chunks: ticket j
+        // is chunk k = j mod tc of split i = j / tc's tail, the tickets fetched one chunk ahead; a
+        // ticket past the pool ends the CTA's share
+        const int tc = tail_chunks, s_ = p.num_splits, nu = (n_seq + kTileN - 1) / kTileN;
+        const int q = nu / s_, r = nu - q * s_;
+        const int head_end = n_tiles - tc * kBalChunk;      // tiles of the head
+        const uint32_t tkt = mapa(smem_u32(&bal_next), 0);
+        int i = 0;
+        auto issue = [&](int tile) {
+          const int st = i % NS;
+          if (i >= NS) mbar_wait(smem_u32(&empty_bar[st]), ((i / NS) - 1) & 1);
+          stage_tile[st] = tile;
+          const uint32_t fb = smem_u32(&full_bar[st]), fvb = smem_u32(&fullv_bar[st]);
+          mbar_arrive_expect_tx(fb, kStageBytes / 2);
+          mbar_arrive_expect_tx(fvb, kStageBytes / 2);
+          const uint32_t dst = sbase + st * kStageBytes;
+          tma_load_5d(dst, &tmap_k, fb, 0, tile * kTileN, 0, kvh, bkv);
+          tma_load_5d(dst + 2 * kHalfBytes, &tmap_v, fvb, 0, tile * kTileN, 0, kvh, bkv);
+          if (i < 8) TRACE(2 + i);
+          ++i;
+        };
+        const int tile0 = t0 / kTileN;
+        for (int t = 0; t < head_end; ++t) issue(tile0 + t);
+        const uint32_t pool = static_cast<uint32_t>(s_ * tc);
+        uint32_t jn = atom_add_cluster(tkt, 1u);
+        while (jn < pool) {
+          const int j = static_cast<int>(jn);
+          jn = atom_add_cluster(tkt, 1u);                    // the next ticket, in flight
+          const int si = j / tc, k = j - si * tc;
+          const int u1 = (si + 1) * q + ((si + 1) * r) / s_;  // end of split si's range (split_range)
+          const int c0 = u1 - (tc - k) * kBalChunk;
+          for (int c = 0; c < kBalChunk; ++c) issue(c0 + c);
+        }
+        // every consumer warp's next stage says "no more tiles"
+        for (int w = 0; w < NW; ++w) {
+          const int st = i % NS;
+          if (i >= NS) mbar_wait(smem_u32(&empty_bar[st]), ((i / NS) - 1) & 1);
+          stage_tile[st] = -1;
+          mbar_arrive(smem_u32(&full_bar[st]));
+          ++i;
+        }
+      } else if (p.block_table == nullptr && n_tiles <= NS) {
         // latency regime (every tile has its own stage): all K boxes first, then all V boxes, so
         // every consumer starts QK^T one V box earlier than in tile order
         for (int i = 0; i < n_tiles; ++i) {
@@ -654,13 +717,20 @@ __global__ void __launch_bounds__(threads_for(NW, helpers_for(kCombine)), 1)
 #pragma unroll
       for (int nb = 0; nb < kNB; ++nb) m[nb][0] = m[nb][1] = kNegInf, l[nb][0] = l[nb][1] = 0.f;
 
-      for (int i = warp; i < n_tiles; i += NW) {
+      for (int i = warp; bal || i < n_tiles; i += NW) {
         const int st = i % NS;
         const uint32_t sK = sbase + st * kStageBytes;
         const uint32_t sV = sK + 2 * kHalfBytes;
         mbar_wait(smem_u32(&full_bar[st]), (i / NS) & 1);      // K: QK^T and the softmax start now
         if (lane == 0 && i < 8) TRACE(10 + i);
-        const int valid = min(kTileN, t_end - (t0 + i * kTileN));
+        int valid;
+        if (kBalCapable && bal) {
+          const int tile = *reinterpret_cast<volatile int*>(&stage_tile[st]);
+          if (tile < 0) break;                                  // no more tiles for this warp
+          valid = min(kTileN, n_seq - tile * kTileN);
+        } else {
+          valid = min(kTileN, t_end - (t0 + i * kTileN));
+        }
         mma_tile<kNB>(sK, sV, valid, qf, o, m, l, p.scale_log2, lane, smem_u32(&fullv_bar[st]), (i / NS) & 1);
         __syncwarp();
         if (lane == 0) mbar_arrive(smem_u32(&empty_bar[st]));
@@ -678,13 +748,14 @@ __global__ void __launch_bounds__(threads_for(NW, helpers_for(kCombine)), 1)
           l[nb][c] = v;
         }
       asm volatile("bar.sync 0;" ::: "memory");   // (A) every tile consumed: the ring is free
-      if (warp < n_tiles && lane < 4) {
+      // (tail balancing: every warp writes; one that took no tile holds m = -inf, l = 0, O = 0)
+      if ((bal || warp < n_tiles) && lane < 4) {
 #pragma unroll
         for (int nb = 0; nb < kNB; ++nb)
 #pragma unroll
           for (int c = 0; c < 2; ++c) epi_ml[warp * 16 + nb * 8 + 2 * lane + c] = make_float2(m[nb][c], l[nb][c]);
       }
-      if (warp < n_tiles) {
+      if (bal || warp < n_tiles) {
 #pragma unroll
         for (int i = 0; i < 8; ++i)
 #pragma unroll
@@ -703,12 +774,19 @@ __global__ void __launch_bounds__(threads_for(NW, helpers_for(kCombine)), 1)
       for (int c = 0; c < 16; ++c) qv[c] = __ldg(q4 + c);
       float o[4] = {0.f, 0.f, 0.f, 0.f};
       float m = kNegInf, l = 0.f;
-      for (int i = warp; i < n_tiles; i += NW) {
+      for (int i = warp; bal || i < n_tiles; i += NW) {
         const int st = i % NS;
         const uint32_t sK = sbase + st * kStageBytes;
         mbar_wait(smem_u32(&full_bar[st]), (i / NS) & 1);
+        int valid;
+        if (kBalCapable && bal) {
+          const int tile = *reinterpret_cast<volatile int*>(&stage_tile[st]);
+          if (tile < 0) break;
+          valid = min(kTileN, n_seq - tile * kTileN);
+        } else {
+          valid = min(kTileN, t_end - (t0 + i * kTileN));
+        }
         mbar_wait(smem_u32(&fullv_bar[st]), (i / NS) & 1);
-        const int valid = min(kTileN, t_end - (t0 + i * kTileN));
         scalar_tile(sK, sK + 2 * kHalfBytes, valid, qv, o, m, l, p.scale_log2, lane);
         __syncwarp();
         if (lane == 0) mbar_arrive(smem_u32(&empty_bar[st]));
@@ -716,7 +794,7 @@ __global__ void __launch_bounds__(threads_for(NW, helpers_for(kCombine)), 1)
 #pragma unroll
       for (int off = 16; off > 0; off >>= 1) l += __shfl_xor_sync(0xffffffffu, l, off);
       asm volatile("bar.sync 0;" ::: "memory");   // (A)
-      if (warp < n_tiles) {
+      if (bal || warp < n_tiles) {
         if (lane == 0) epi_ml[warp * 16] = make_float2(m, l);
         *reinterpret_cast<float4*>(&epi_o[(warp * 16) * kEpiStride + 4 * lane]) =
             make_float4(o[0], o[1], o[2], o[3]);
@@ -730,7 +808,7 @@ __global__ void __launch_bounds__(threads_for(NW, helpers_for(kCombine)), 1)
   // Element e = (row g = e / 32, float4 column d4 = e % 32) of the CTA's [R x 128] result.
   // Only the n_active = min(NW, n_tiles) warps that received tiles wrote a partial; the
   // passes are branch-free (predicated loads), so the loads of all passes issue back to back.
-  const int n_active = min(NW, n_tiles);
+  const int n_active = bal ? NW : min(NW, n_tiles);
   float eM[kIters], eL[kIters];
   float4 eO[kIters];
 #pragma unroll
@@ -810,7 +888,8 @@ __global__ void __launch_bounds__(threads_for(NW, helpers_for(kCombine)), 1)
     // Row g belongs to rank g mod s.  Non-owned rows are pushed into the owner's slot with
     // st.async (bytes counted on the owner's push barrier; no fence, no cluster barrier on the
     // exit path); owned rows wait for the s - 1 pushes, merge, and are written out.
-    cluster_wait();                                 // every peer's push barrier is initialised
+    if (!(bal && warp == NW)) cluster_wait();       // every peer's push barrier is initialised
+                                                    // (a balancing producer warp waited already)
     const int s = s_cl;
 #pragma unroll
     for (int it = 0; it < kIters; ++it) {

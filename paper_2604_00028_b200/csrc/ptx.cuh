@@ -154,6 +154,12 @@ __device__ __forceinline__ void st_async_v2(uint32_t addr, float a, float b, uin
                "f"(a), "f"(b), "r"(remote_bar)
                : "memory");
 }
+// Atomic add on a (possibly remote) shared::cluster address; returns the old value.
+__device__ __forceinline__ uint32_t atom_add_cluster(uint32_t addr, uint32_t v) {
+  uint32_t r;
+  asm volatile("atom.shared::cluster.add.u32 %0, [%1], %2;" : "=r"(r) : "r"(addr), "r"(v) : "memory");
+  return r;
+}
 __device__ __forceinline__ void cluster_arrive_relaxed() {
   asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
 }

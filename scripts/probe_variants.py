@@ -1,0 +1,33 @@
+"""Build-variant A/B (development tool): the same shapes under the product library and the
+variants in paper_2604_00028_b200/lib/variants/libdecattn_<name>.so (DECATTN_LIB), in
+interleaved rounds.
+
+    python scripts/probe_variants.py name1 name2 ...      (on the GPU box)"""
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+if __name__ == "__main__":
+    if len(sys.argv) > 1 and sys.argv[1] == "one":
+        sys.path.insert(0, os.path.join(ROOT, "scripts"))
+        from probe_timing import bench
+        bench(1, 64, 8, 131072, "fixed", 10, combine=1, steps=20, reps=7)
+        bench(1, 64, 8, 131072, "fixed", 16, combine=2, steps=20, reps=7)
+        bench(1, 64, 8, 131072, "fixed", 18, combine=2, steps=20, reps=7)
+        bench(4, 32, 4, 65536, "seq_aware", steps=20, reps=7)
+        bench(1, 8, 1, 131072, "guarded", steps=40, reps=7)
+        bench(128, 64, 8, 8192, "seq_aware", steps=5, reps=5)
+        bench(1, 64, 8, 512, "seq_aware_sm", steps=200, reps=7)
+        bench(1, 8, 1, 512, "seq_aware", steps=200, reps=7)
+        bench(1, 64, 8, 2048, "seq_aware", steps=200, reps=7)
+        sys.exit(0)
+    names = [""] + sys.argv[1:]
+    for rnd in range(2):
+        for v in names:
+            lib = os.path.join(ROOT, "paper_2604_00028_b200", "lib",
+                               *(["variants", f"libdecattn_{v}.so"] if v else ["libdecattn.so"]))
+            env = dict(os.environ, DECATTN_LIB=lib)
+            r = subprocess.run([sys.executable, __file__, "one"], env=env, capture_output=True, text=True)
+            print(f"== round {rnd} {v or 'product'}\n{r.stdout}{r.stderr[-2000:] if r.returncode else ''}", flush=True)

@@ -94,6 +94,25 @@ def test_cluster_combine(s):
     run_and_check(2, 8, 1, 1000, policy="fixed", forced=s, combine_mode=1, seed=11)
 
 
+# ---- tail balancing of cluster plans: splits of >= 32 tiles stream the head of their
+#      range and share the pooled tails through a ticket counter in rank 0's shared memory ----------
+@pytest.mark.parametrize("batch,h_q,h_kv,l_k,s,pack,variant", [
+    (1, 8, 1, 16384, 8, True, "normal"),      # 32 tiles per split: the smallest balanced split
+    (1, 8, 1, 16448, 8, True, "normal"),      # a ragged last tile (16448 = 257 tiles)
+    (4, 16, 2, 20000, 5, True, "ragged"),     # balanced and static clusters in one launch
+    (2, 16, 2, 20000, 7, True, "peaked"),
+    (1, 32, 2, 40000, 9, True, "normal"),     # 16-row CTAs
+    (2, 4, 2, 9000, 4, False, "ragged"),      # scalar path
+    (1, 64, 8, 131072, 10, True, "normal"),   # the long-context C-ext-1 plan
+])
+def test_cluster_tail_balancing(batch, h_q, h_kv, l_k, s, pack, variant):
+    dec = _dec()
+    for _ in range(2):        # the tickets live in shared memory: nothing carries over between calls
+        plan, _, _ = run_and_check(batch, h_q, h_kv, l_k, policy="fixed", forced=s, combine_mode=1,
+                                   pack_gqa=pack, variant=variant, seed=31)
+        assert plan.combine_mode == dec.DA_COMBINE_CLUSTER
+
+
 @pytest.mark.parametrize("s", [5, 11, 15, 16])
 def test_cluster_combine_16_rows(s):
     # G = 16 query rows per CTA (L_K > 64 units): the largest push-slot use (s ceil(16 / s) rows
