@@ -76,8 +76,11 @@ __device__ __forceinline__ unsigned long long gtime() {
 }
 __device__ __forceinline__ int trace_cta() { return (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x; }
 #define TRACE(slot) do { const int c_ = trace_cta(); if (c_ < 64) g_trace[c_ * 64 + (slot)] = gtime(); } while (0)
+// timestamp once the value v has been produced (the compare waits for it)
+#define TRACE_DEP(slot, v, on) do { if ((on) && __float_as_uint(v) != 0x7fc0beefu) TRACE(slot); } while (0)
 #else
 #define TRACE(slot) do { } while (0)
+#define TRACE_DEP(slot, v, on) do { } while (0)
 #endif
 constexpr int kHalfBytes = kTileN * 128;     // one 64-token x 64-dim box: 8 KB
 constexpr int kEpiStride = kHeadDim + 4;     // fp32 row stride of epilogue buffers (bank spread)
@@ -91,8 +94,9 @@ template <int NB>
 __device__ __forceinline__ void mma_tile(uint32_t sK, uint32_t sV, int valid,
                                          const uint32_t (&qf)[8][NB][2], float (&o)[8][NB][4],
                                          float (&m)[NB][2], float (&l)[NB][2], float scale_log2,
-                                         int lane, uint32_t vbar, uint32_t vparity) {
+                                         int lane, uint32_t vbar, uint32_t vparity, bool tr = false) {
   const uint32_t sw = static_cast<uint32_t>(lane & 7);
+  tr = tr && lane == 0;                                    // trace builds: time the steps of this tile
   // ---- S^T[token, g] = sum_d K[token, d] Q[g, d]  (4 token blocks x NB g-blocks)
   float s[4][NB][4];
 #pragma unroll
@@ -119,6 +123,7 @@ __device__ __forceinline__ void mma_tile(uint32_t sK, uint32_t sV, int valid,
     }
   }
 
+  TRACE_DEP(32, s[0][0][0] + s[3][NB - 1][3], tr);       // QK^T done
   // ---- online softmax over the tile's tokens, per query row g (a5)
   // C layout: s[j][nb][c] holds token 16j + (lane >> 2) + 8*(c >> 1), g = 8nb + 2(lane & 3) + (c & 1).
   float mx[NB][2];
@@ -179,9 +184,11 @@ __device__ __forceinline__ void mma_tile(uint32_t sK, uint32_t sV, int valid,
       pl[j][nb][1] = movmatrix_trans(pack_bf16(p[2] - bf16lo(h23), p[3] - bf16hi(h23)));
     }
 
+  TRACE_DEP(33, __uint_as_float(pl[3][NB - 1][1] ^ pb[0][0][0]), tr);   // softmax + P done
   // ---- V: wait for its half of the stage (it lands while QK^T and the softmax run); rows past
   // the range may hold anything (even NaN): zero them so the P = 0 rows stay 0
   mbar_wait(vbar, vparity);
+  if (tr) TRACE(34);                                       // V landed
   if (valid < kTileN) {
     for (int idx = lane; idx < (kTileN - valid) * 16; idx += 32) {
       const int r = valid + (idx >> 4);
@@ -212,6 +219,7 @@ __device__ __forceinline__ void mma_tile(uint32_t sK, uint32_t sV, int valid,
       }
     }
   }
+  TRACE_DEP(35, o[0][0][0] + o[7][NB - 1][3], tr);        // PV done
 }
 
 // ---------------------------------------------------------------------------
@@ -731,7 +739,7 @@ __global__ void __launch_bounds__(threads_for(NW, helpers_for(kCombine)), 1)
         } else {
           valid = min(kTileN, t_end - (t0 + i * kTileN));
         }
-        mma_tile<kNB>(sK, sV, valid, qf, o, m, l, p.scale_log2, lane, smem_u32(&fullv_bar[st]), (i / NS) & 1);
+        mma_tile<kNB>(sK, sV, valid, qf, o, m, l, p.scale_log2, lane, smem_u32(&fullv_bar[st]), (i / NS) & 1, i == 0);
         __syncwarp();
         if (lane == 0) mbar_arrive(smem_u32(&empty_bar[st]));
         if (lane == 0 && i < 8) TRACE(18 + i);

@@ -2,7 +2,7 @@
 variants in paper_2604_00028_b200/lib/variants/libdecattn_<name>.so (DECATTN_LIB), in
 interleaved rounds.
 
-    python scripts/probe_variants.py name1 name2 ...      (on the GPU box)"""
+    python scripts/probe_variants.py [--set=latency] name1 name2 ...      (on the GPU box)"""
 import os
 import subprocess
 import sys
@@ -10,6 +10,21 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 if __name__ == "__main__":
+    if len(sys.argv) > 2 and sys.argv[1] == "one" and sys.argv[2] == "latency":
+        sys.path.insert(0, os.path.join(ROOT, "scripts"))
+        from probe_timing import bench
+        for pol in ("guarded", "seq_aware", "seq_aware_sm", "evolved"):
+            bench(1, 64, 8, 512, pol, steps=200, reps=7)
+            bench(1, 8, 1, 512, pol, steps=200, reps=7)
+        for lk in (128, 256, 384):
+            bench(1, 8, 1, lk, "guarded", steps=200, reps=7)
+        bench(1, 16, 1, 512, "seq_aware_sm", steps=200, reps=7)
+        bench(1, 128, 8, 512, "seq_aware_sm", steps=200, reps=7)
+        bench(2, 16, 2, 1024, "seq_aware_sm", steps=200, reps=7)
+        bench(1, 64, 8, 2048, "seq_aware_sm", steps=200, reps=7)
+        bench(1, 8, 1, 4096, "seq_aware_sm", steps=200, reps=7)
+        bench(1, 64, 8, 512, "seq_aware", pack=False, steps=200, reps=7)
+        sys.exit(0)
     if len(sys.argv) > 1 and sys.argv[1] == "one":
         sys.path.insert(0, os.path.join(ROOT, "scripts"))
         from probe_timing import bench
@@ -23,11 +38,15 @@ if __name__ == "__main__":
         bench(1, 8, 1, 512, "seq_aware", steps=200, reps=7)
         bench(1, 64, 8, 2048, "seq_aware", steps=200, reps=7)
         sys.exit(0)
-    names = [""] + sys.argv[1:]
+    args = sys.argv[1:]
+    which = []
+    if args and args[0].startswith("--set="):
+        which, args = [args[0][6:]], args[1:]
+    names = [""] + args
     for rnd in range(2):
         for v in names:
             lib = os.path.join(ROOT, "paper_2604_00028_b200", "lib",
                                *(["variants", f"libdecattn_{v}.so"] if v else ["libdecattn.so"]))
             env = dict(os.environ, DECATTN_LIB=lib)
-            r = subprocess.run([sys.executable, __file__, "one"], env=env, capture_output=True, text=True)
+            r = subprocess.run([sys.executable, __file__, "one"] + which, env=env, capture_output=True, text=True)
             print(f"== round {rnd} {v or 'product'}\n{r.stdout}{r.stderr[-2000:] if r.returncode else ''}", flush=True)

@@ -2,7 +2,8 @@
 
 DECATTN_LIB=paper_2604_00028_b200/lib/variants/libdecattn_trace.so python scripts/trace_timeline.py
 Slots (globaltimer ns): 0 entry, 1 after griddepcontrol.wait, 2+i TMA issued tile i,
-10+i tile i landed (consumer), 18+i tile i computed, 26 epilogue start, 27 merge done,
+10+i tile i landed (consumer), 18+i tile i computed, 32-35 tile 0's QK^T / softmax / V landed /
+PV results available, 26 epilogue start, 27 merge done,
 29 rank-0 push wait done, 30 CTA end, 63 previous step's end stamp.
 """
 import ctypes
@@ -59,7 +60,8 @@ def trace(b, hq, hkv, lk, policy, forced=0, steps=50, combine=None):
     t0 = min(r[63] for r in rows if r[63]) if any(r[63] for r in rows) else min(r[0] for r in rows)
     print(f"\n== B={b} HQ={hq} HKV={hkv} L={lk} {policy} s={plan.num_splits} comb={plan.combine_mode}: "
           f"{us:.2f} us/step (graph); times in ns after the previous step's end stamp")
-    names = {0: "entry", 1: "pdl_wait", 26: "epi", 27: "merged", 29: "push_in", 30: "end"}
+    names = {0: "entry", 1: "pdl_wait", 26: "epi", 27: "merged", 29: "push_in", 30: "end",
+             32: "t0_qk", 33: "t0_p", 34: "t0_v", 35: "t0_pv"}
     for c, r in enumerate(rows[:8]):
         parts = []
         for j in (0, 1):
@@ -70,7 +72,7 @@ def trace(b, hq, hkv, lk, policy, forced=0, steps=50, combine=None):
         parts.append(f"issue={iss}")
         parts.append(f"ready={rdy}")
         parts.append(f"done={dn}")
-        for j in (26, 40, 41, 42, 27, 29, 44, 45, 46, 47, 30):
+        for j in (32, 33, 34, 35, 26, 40, 41, 42, 27, 29, 44, 45, 46, 47, 30):
             if r[j]:
                 parts.append(f"{names.get(j, j)}={int(r[j]) - t0}")
         if r[60] and r[61] and r[30] > r[0]:
