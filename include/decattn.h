@@ -45,7 +45,7 @@
 extern "C" {
 #endif
 
-#define DA_ABI_VERSION 6
+#define DA_ABI_VERSION 7
 
 #if defined(__GNUC__)
 #define DA_API __attribute__((visibility("default")))
@@ -179,6 +179,16 @@ typedef struct da_plan {
                               DA_POLICY_DYNAMIC: grid_y * h_q * (head_dim + 1)
                               * 4 + 8 * batch (partials per slot, then the
                               schedule: first slot and split count per b)  */
+  int32_t seq_offset;      /* (in, da_plan_set_seq_offset; 0 from da_plan_make)
+                              tokens of every sequence that precede this cache:
+                              cache_seqlens hold whole-sequence lengths and
+                              batch b attends to tokens [0, seqlens[b] -
+                              seq_offset) of this cache (clamped to
+                              [0, l_cap]) - the shard of a sequence-sharded
+                              KV cache that starts at token seq_offset
+                              (DESIGN.md §6).  Not applied when cache_seqlens
+                              is NULL (then every sequence has plan->l_k).  */
+  int32_t reserved_;       /* 0 (keeps the struct 8-byte aligned)            */
 } da_plan;
 
 /*
@@ -224,6 +234,16 @@ DA_API da_status da_plan_make_varlen(int32_t batch, int32_t h_q, int32_t h_kv, i
  * KERNEL s >= 2.  Errors: DA_ERR_INVALID_ARG.
  */
 DA_API da_status da_plan_set_combine(da_plan* plan, int32_t combine_mode);
+
+/*
+ * da_plan_set_seq_offset - make the plan one sequence shard's: cache_seqlens passed to the
+ * forwards are then whole-sequence lengths and the cache holds tokens [seq_offset, seq_offset +
+ * l_cap) of each sequence (the kernel attends to min(max(seqlens[b] - seq_offset, 0), l_cap)
+ * of them).  Sequence sharding across GPUs (north_star: "only long-context configs
+ * shard the sequence") without a per-step length kernel.  seq_offset >= 0, else
+ * DA_ERR_INVALID_ARG.  Pure host code.
+ */
+DA_API da_status da_plan_set_seq_offset(da_plan* plan, int32_t seq_offset);
 
 /*
  * da_forward - decode attention for one step (L_Q = 1), asynchronously on

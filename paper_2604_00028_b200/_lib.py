@@ -28,7 +28,7 @@ DA_OK, DA_ERR_INVALID_ARG, DA_ERR_UNSUPPORTED, DA_ERR_ALIGNMENT, DA_ERR_WORKSPAC
 DA_BF16, DA_F32 = 0, 1
 DA_COMBINE_NONE, DA_COMBINE_CLUSTER, DA_COMBINE_KERNEL = range(3)
 DA_PATH_SCALAR, DA_PATH_MMA = 0, 1
-DA_ABI_VERSION = 6
+DA_ABI_VERSION = 7
 
 POLICIES = {"guarded": DA_POLICY_GUARDED, "seq_aware": DA_POLICY_SEQ_AWARE, "fixed": DA_POLICY_FIXED,
             "evolved": DA_POLICY_EVOLVED, "seq_aware_sm": DA_POLICY_SEQ_AWARE_SM, "dynamic": DA_POLICY_DYNAMIC}
@@ -45,7 +45,8 @@ class da_plan(ctypes.Structure):
         "policy", "forced_splits", "usable_sms", "block_n", "num_n_blocks", "num_m_blocks",
         "total_mblocks", "num_splits", "nonempty_splits", "rule", "split_unit", "path",
         "rows_per_cta", "combine_mode", "grid_x", "grid_y", "grid_z", "block_threads",
-        "cluster_x", "smem_bytes")] + [("workspace_bytes", ctypes.c_int64)]
+        "cluster_x", "smem_bytes")] + [("workspace_bytes", ctypes.c_int64), ("seq_offset", ctypes.c_int32),
+                                      ("reserved_", ctypes.c_int32)]
 
     def as_dict(self) -> dict:
         return {name: getattr(self, name) for name, _ in self._fields_}
@@ -73,6 +74,8 @@ def _load() -> ctypes.CDLL:
     lib.da_plan_make_varlen.restype = i32
     lib.da_plan_set_combine.argtypes = [ctypes.POINTER(da_plan), i32]
     lib.da_plan_set_combine.restype = i32
+    lib.da_plan_set_seq_offset.argtypes = [ctypes.POINTER(da_plan), i32]
+    lib.da_plan_set_seq_offset.restype = i32
     lib.da_forward.argtypes = [ctypes.POINTER(da_plan), vp, vp, vp, i32, vp, vp, f32, i32, vp, vp,
                                vp, i64, vp]
     lib.da_forward.restype = i32
@@ -108,7 +111,7 @@ def _load() -> ctypes.CDLL:
 
 LIB = _load()
 
-EXPORTED = ("da_plan_make", "da_plan_make_varlen", "da_plan_set_combine", "da_forward", "da_forward_paged",
+EXPORTED = ("da_plan_make", "da_plan_make_varlen", "da_plan_set_combine", "da_plan_set_seq_offset", "da_forward", "da_forward_paged",
             "da_forward_host_bytes", "da_forward_host", "da_combine", "da_peer_signal", "da_combine_peers",
             "da_forward_peer", "da_forward_peer_combine", "da_query_residency", "da_status_string",
             "da_abi_version")
@@ -147,6 +150,13 @@ def da_plan_make_varlen(batch, h_q, h_kv, l_cap, head_dim, pack_gqa, sm_margin, 
     if st != DA_OK:
         raise DecAttnError(st, "da_plan_make_varlen")
     return p
+
+
+def da_plan_set_seq_offset(plan: da_plan, seq_offset: int) -> da_plan:
+    st = LIB.da_plan_set_seq_offset(ctypes.byref(plan), int(seq_offset))
+    if st != DA_OK:
+        raise DecAttnError(st, "da_plan_set_seq_offset")
+    return plan
 
 
 def da_plan_set_combine(plan: da_plan, combine_mode: int) -> da_plan:

@@ -123,6 +123,7 @@ da_status check_plan(const da_plan* plan) {
   if (plan->num_splits < 1 || plan->num_splits > kMaxForcedSplits) return DA_ERR_INVALID_ARG;
   if (plan->pack_gqa != 0 && plan->pack_gqa != 1) return DA_ERR_INVALID_ARG;
   if (!combine_mode_valid(plan->combine_mode, plan->num_splits)) return DA_ERR_INVALID_ARG;
+  if (plan->seq_offset < 0 || plan->reserved_ != 0) return DA_ERR_INVALID_ARG;
   da_plan chk = *plan;
   derive_launch(&chk);
   if (chk.path != plan->path || chk.rows_per_cta != plan->rows_per_cta ||
@@ -208,6 +209,7 @@ da_status forward_impl(const da_plan* plan, const void* q, const void* k_cache, 
   p.q_sb = sd[0];
   p.q_sh = sd[1];
   p.seqlens = cache_seqlens;
+  p.seq_offset = plan->seq_offset;
   p.l_default = plan->l_k;
   p.l_cap = l_cap;
   p.num_splits = plan->num_splits;

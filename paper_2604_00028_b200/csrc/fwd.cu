@@ -324,7 +324,7 @@ __device__ __forceinline__ void split_range(int n, int split, int s, uint64_t s_
 constexpr int kDynScratch = kStageBytes / 4;   // sequences whose unit count is cached in shared memory
 
 __device__ __forceinline__ int dyn_len(const FwdParams& p, int b) {
-  return min(max(p.seqlens != nullptr ? __ldg(p.seqlens + b) : p.l_default, 0), p.l_cap);
+  return min(max(p.seqlens != nullptr ? (max(__ldg(p.seqlens + b), 0) - p.seq_offset) : p.l_default, 0), p.l_cap);
 }
 
 __device__ __noinline__ int4 dyn_schedule(const FwdParams& p, uint32_t slot, bool record, int lane,
@@ -557,6 +557,7 @@ __global__ void __launch_bounds__(threads_for(NW, helpers_for(kCombine)), 1)
     const int4 r = sched;
     if (r.x < 0) return;                          // unused slot (the launch provides an upper bound)
     b = r.x;
+    bkv = b;                                      // the sequence's cache batch and length index
     split = r.y;
     dyn_single = r.z == 1;
     // split r.y of r.z over n = r.w tokens; (split + 1) n_u < 2^32 since r.z <= 128, n_u < 2^25
@@ -567,14 +568,14 @@ __global__ void __launch_bounds__(threads_for(NW, helpers_for(kCombine)), 1)
     t_end = min(static_cast<int>(u1) * kTileN, r.w);
     n_tiles = static_cast<int>(u1 - u0);
   } else if (p.seqlens != nullptr) {
-    split_range(min(max(__ldg(p.seqlens + bkv), 0), p.l_cap), split, p.num_splits, p.s_magic, t0, t_end, n_tiles);
+    split_range(min(max((max(__ldg(p.seqlens + bkv), 0) - p.seq_offset), 0), p.l_cap), split, p.num_splits, p.s_magic, t0, t_end, n_tiles);
   }
   // tail balancing (kBalCapable): every split of this sequence holds >= kBalMinTiles tiles (uniform
   // over the cluster: one sequence, one length); n_seq = the sequence's length
   bool bal = false;
   int n_seq = 0, tail_chunks = 0;
   if constexpr (kBalCapable) {
-    n_seq = min(max(p.seqlens != nullptr ? __ldg(p.seqlens + bkv) : p.l_default, 0), p.l_cap);
+    n_seq = min(max(p.seqlens != nullptr ? (max(__ldg(p.seqlens + bkv), 0) - p.seq_offset) : p.l_default, 0), p.l_cap);
     const int nu = (n_seq + kTileN - 1) / kTileN;
     bal = p.block_table == nullptr && nu >= kBalMinTiles * p.num_splits;
     tail_chunks = nu / p.num_splits / kBalTailDiv / kBalChunk;   // pooled chunks per split (>= 2)

@@ -42,7 +42,8 @@ struct PubParams {
 struct FwdParams {
   const uint16_t* q;        // bf16 [B, H_Q, d]
   int64_t q_sb, q_sh;       // strides in elements
-  const int32_t* seqlens;   // device int32 [B] or nullptr
+  const int32_t* seqlens;   // device int32 [B] or nullptr: whole-sequence lengths
+  int32_t seq_offset;       // tokens before this cache (sequence shard): n_b = seqlens[b] - seq_offset
   int32_t l_default;        // length used when seqlens == nullptr (plan->l_k)
   int32_t l_cap;            // cache capacity (clamp bound)
   int32_t num_splits;       // s

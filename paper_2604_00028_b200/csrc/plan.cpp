@@ -282,6 +282,12 @@ extern "C" da_status da_plan_make_varlen(int32_t batch, int32_t h_q, int32_t h_k
   return DA_OK;
 }
 
+extern "C" da_status da_plan_set_seq_offset(da_plan* plan, int32_t seq_offset) {
+  if (plan == nullptr || seq_offset < 0) return DA_ERR_INVALID_ARG;
+  plan->seq_offset = seq_offset;
+  return DA_OK;
+}
+
 extern "C" da_status da_plan_set_combine(da_plan* plan, int32_t combine_mode) {
   if (plan == nullptr) return DA_ERR_INVALID_ARG;
   if (!combine_mode_valid(combine_mode, plan->num_splits)) return DA_ERR_INVALID_ARG;

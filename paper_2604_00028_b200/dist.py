@@ -52,7 +52,8 @@ def head_shard(h_q: int, h_kv: int, rank: int, world: int):
 
 
 def local_seqlens(seqlens_global: torch.Tensor, t0: int, l_local: int) -> torch.Tensor:
-    """Tokens of each sequence that fall in this rank's shard [t0, t0 + l_local)."""
+    """Tokens of each sequence that fall in this rank's shard [t0, t0 + l_local) (host reference of
+    what the kernel derives from the plan's seq_offset; injected local attentions use it)."""
     return (seqlens_global.to(torch.int64) - t0).clamp_(0, l_local).to(torch.int32)
 
 
@@ -77,7 +78,8 @@ class SeqShardedDecode:
     """Long-context mode: sequence-sharded KV cache + all-gather + LSE combine.
 
     ``local_attention(q, k, v, seqlens, o_out, lse_out)`` must write this rank's
-    fp32 partial into the given views; ``combine(o_parts, lse_parts, out, lse)``
+    fp32 partial into the given views (``seqlens``: whole-sequence lengths or None; the shard
+    holds tokens [t0, t0 + l_local)); ``combine(o_parts, lse_parts, out, lse)``
     merges P partials ([P, B, H_Q, d] / [P, B, H_Q] views of the gather
     buffer).  Both default to the CUDA path.
     """
@@ -101,7 +103,10 @@ class SeqShardedDecode:
         self.plan = None
         if local_attention is None or combine is None:
             from . import api
-            self.plan = api.make_plan(batch, h_q, h_kv, self.l_local, head_dim, True, 0, None, policy)
+            # seq_offset = t0: cache_seqlens stay whole-sequence lengths, the kernel takes this shard's
+            # part of each (no per-step length arithmetic on the host or in extra launches)
+            self.plan = api.make_plan(batch, h_q, h_kv, self.l_local, head_dim, True, 0, None, policy,
+                                      seq_offset=self.t0)
             self._ws = api.workspace_for(self.plan, self.device)
         self._local = local_attention or self._cuda_local
         self._combine = combine or self._cuda_combine
@@ -132,9 +137,10 @@ class SeqShardedDecode:
         L.da_combine(self.world, self.batch, self.h_q, self.d, o_parts, self.chunk, lse_parts,
                      self.chunk, L.DA_F32 if out.dtype == torch.float32 else L.DA_BF16, out, lse)
 
-    def step(self, q, k_local, v_local, seqlens_local=None, out=None, lse=None):
-        """One decode step: local partial -> all-gather -> combine.  Returns (out, lse)."""
-        self._local(q, k_local, v_local, seqlens_local, self._o_view(self.send), self._lse_view(self.send))
+    def step(self, q, k_local, v_local, cache_seqlens=None, out=None, lse=None):
+        """One decode step: local partial -> all-gather -> combine.  ``cache_seqlens``: whole-sequence
+        lengths (device int32 [B]) or None (every sequence l_k_total long).  Returns (out, lse)."""
+        self._local(q, k_local, v_local, cache_seqlens, self._o_view(self.send), self._lse_view(self.send))
         _all_gather_flat(self.recv, self.send, self.group)
         if out is None:
             out = torch.empty((self.batch, self.h_q, self.d), dtype=torch.bfloat16, device=self.device)
@@ -203,7 +209,8 @@ class PeerSeqShardedDecode:
         self.epoch = torch.zeros(1, dtype=torch.int32, device=self.device)
         self.fused = fused
         self.counter = torch.zeros(1, dtype=torch.int32, device=self.device)   # da_forward_peer: writer CTAs
-        self.plan = api.make_plan(batch, h_q, h_kv, self.l_local, head_dim, True, 0, None, policy)
+        self.plan = api.make_plan(batch, h_q, h_kv, self.l_local, head_dim, True, 0, None, policy,
+                                  seq_offset=self.t0)      # cache_seqlens: whole-sequence lengths
         # every rank must take the same protocol (LL words vs slot + flags): the shards' lengths can
         # differ by one token, so their plans - and whether the one-kernel grid is resident - can
         # differ; the decision is the minimum over the group
@@ -219,21 +226,22 @@ class PeerSeqShardedDecode:
         self.o_local = torch.empty((batch, h_q, head_dim), dtype=torch.float32, device=self.device)
         self.lse_local = torch.empty((batch, h_q), dtype=torch.float32, device=self.device)
 
-    def step(self, q, k_local, v_local, seqlens_local=None, out=None, lse=None):
-        """One decode step: local partial (published to the peers) -> pull-combine.  Returns (out, lse)."""
+    def step(self, q, k_local, v_local, cache_seqlens=None, out=None, lse=None):
+        """One decode step: local partial (published to the peers) -> pull-combine.  ``cache_seqlens``:
+        whole-sequence lengths (device int32 [B]) or None.  Returns (out, lse)."""
         from . import _lib as L
         from . import api
         if self.one_kernel:
-            return api.forward_peer_combine(self.plan, q, k_local, v_local, seqlens_local, self.world, self.rank,
+            return api.forward_peer_combine(self.plan, q, k_local, v_local, cache_seqlens, self.world, self.rank,
                                             self.bases, self.ll_offset, self.ll_slot_bytes, self.epoch, self.counter,
                                             self.status, timeout_ns=self.timeout_ns, out=out, lse=lse,
                                             workspace=self._ws)
         if self.fused:
-            api.forward_peer(self.plan, q, k_local, v_local, seqlens_local, self.world, self.rank, self.bases,
+            api.forward_peer(self.plan, q, k_local, v_local, cache_seqlens, self.world, self.rank, self.bases,
                              self.slot_bytes, self.lse_offset, self.flag_offset, self.epoch, self.counter,
                              workspace=self._ws)
         else:
-            api.forward(self.plan, q, k_local, v_local, seqlens_local, out=self.o_local, lse=self.lse_local,
+            api.forward(self.plan, q, k_local, v_local, cache_seqlens, out=self.o_local, lse=self.lse_local,
                         workspace=self._ws, out_dtype=torch.float32)
             L.da_peer_signal(self.world, self.rank, self.bases, self.o_local, self.lse_local, self.batch,
                              self.h_q, self.d, self.slot_bytes, self.lse_offset, self.flag_offset, self.epoch)

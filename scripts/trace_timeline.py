@@ -36,7 +36,7 @@ def trace(b, hq, hkv, lk, policy, forced=0, steps=50, combine=None):
     st = torch.cuda.Stream()
     with torch.cuda.stream(st):
         for i in range(3):
-            dec.forward(plan, w["q"], ks[i], vs[i], None, out=out, lse=lse, workspace=ws)
+            dec.forward(plan, w["q"], ks[i % nbuf], vs[i % nbuf], None, out=out, lse=lse, workspace=ws)
     torch.cuda.synchronize()
     g = torch.cuda.CUDAGraph()
     with torch.cuda.graph(g, stream=st):

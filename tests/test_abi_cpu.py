@@ -35,8 +35,9 @@ def test_library_exports_every_header_symbol(L):
 
 def test_plan_struct_layout(L):
     import ctypes
-    # 28 int32 fields + one int64 = 120 bytes (no padding before the int64 at offset 112)
-    assert ctypes.sizeof(L.da_plan) == 120
+    # 28 int32 fields + one int64 + two int32 = 128 bytes (no implicit padding)
+    assert ctypes.sizeof(L.da_plan) == 128
+    assert L.da_plan.workspace_bytes.offset == 112 and L.da_plan.seq_offset.offset == 120
     with open(os.path.join(ROOT, "include", "decattn.h")) as f:
         hdr = f.read()
     body = hdr[hdr.index("typedef struct da_plan"):hdr.index("} da_plan;")]
@@ -192,6 +193,24 @@ def test_plan_invalid_knobs(L):
     with pytest.raises(L.DecAttnError) as e:
         L.da_plan_make(1, 8, 1, 512, 64, 1, 0, 148, 1, 0)
     assert e.value.status == L.DA_ERR_UNSUPPORTED
+
+
+def test_set_seq_offset(L):
+    p = L.da_plan_make(2, 16, 2, 4096, 128, 1, 0, 148, "seq_aware", 0)
+    assert p.seq_offset == 0 and p.reserved_ == 0
+    q = L.da_plan.from_buffer_copy(p)
+    L.da_plan_set_seq_offset(q, 65536)
+    assert q.seq_offset == 65536
+    assert {f: getattr(q, f) for f, _ in q._fields_ if f != "seq_offset"} == \
+        {f: getattr(p, f) for f, _ in p._fields_ if f != "seq_offset"}      # the launch is unchanged
+    with pytest.raises(L.DecAttnError):
+        L.da_plan_set_seq_offset(q, -1)
+    bad = L.da_plan.from_buffer_copy(p)
+    bad.seq_offset = -5                              # hand-edited: rejected by the forwards' checks
+    assert _fwd(L, bad) == L.DA_ERR_INVALID_ARG
+    bad = L.da_plan.from_buffer_copy(p)
+    bad.reserved_ = 1
+    assert _fwd(L, bad) == L.DA_ERR_INVALID_ARG
 
 
 def test_set_combine_rules(L):

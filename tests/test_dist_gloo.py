@@ -49,6 +49,9 @@ def _worker(rank, world, port, B, HQ, HKV, L, seqlens, ret):
         q, k, v = (synth.to_f64(inp[n]) for n in ("q", "k", "v"))
 
         def local(qt, kt, vt, sl, o_out, lse_out):
+            # sl: whole-sequence lengths (the CUDA path takes the shard's part via the plan's
+            # seq_offset; this injected oracle does it on the host)
+            sl = local_seqlens(sl, sd.t0, sd.l_local)
             o, l = OA.decode_attention(q, synth.to_f64(kt), synth.to_f64(vt), sl.numpy())
             o_out.copy_(torch.from_numpy(o).float())
             lse_out.copy_(torch.from_numpy(l).float())
@@ -60,7 +63,7 @@ def _worker(rank, world, port, B, HQ, HKV, L, seqlens, ret):
 
         sd = SeqShardedDecode(B, HQ, HKV, L, 128, device="cpu", local_attention=local, combine=comb)
         kl, vl = inp["k"][:, sd.t0:sd.t0 + sd.l_local], inp["v"][:, sd.t0:sd.t0 + sd.l_local]
-        sl = local_seqlens(torch.tensor(seqlens, dtype=torch.int32), sd.t0, sd.l_local)
+        sl = torch.tensor(seqlens, dtype=torch.int32)
         out = torch.empty(B, HQ, 128, dtype=torch.float32)
         lse = torch.empty(B, HQ, dtype=torch.float32)
         sd.step(inp["q"], kl, vl, sl, out, lse)

@@ -511,3 +511,43 @@ def test_dynamic_splits_without_seqlens_and_paged():
     assert_out_close(synth.to_f64(out), ref_o)
     assert_lse_close(synth.to_f64(lse), ref_l)
     run_paged(6, 32, 4, 2500, 128, policy="dynamic")
+
+
+# ---- sequence shards (da_plan_set_seq_offset): cache_seqlens are whole-sequence lengths and the
+#      cache holds tokens [t0, t0 + L) of each sequence -------------------------------------------
+@pytest.mark.parametrize("batch,h_q,h_kv,l_local,t0,policy,forced,combine", [
+    (4, 16, 2, 700, 500, "seq_aware", 0, None),
+    (4, 16, 2, 700, 500, "fixed", 5, 1),
+    (4, 16, 2, 700, 500, "fixed", 20, 2),
+    (6, 32, 4, 3000, 2000, "dynamic", 0, None),
+    (3, 8, 1, 20000, 16384, "fixed", 5, 1),          # balanced cluster splits
+    (2, 8, 8, 300, 1000, "guarded", 0, None),       # scalar path
+])
+def test_seq_offset_shard(batch, h_q, h_kv, l_local, t0, policy, forced, combine):
+    dec = _dec()
+    from paper_2604_00028_b200.dist import local_seqlens
+    inp = synth.make_inputs(batch, h_q, h_kv, l_local, seed=1300, device="cuda")
+    g = torch.Generator(device="cpu").manual_seed(1301)
+    # whole-sequence lengths: before the shard, inside it, past it
+    glob = torch.randint(0, t0 + l_local + 300, (batch,), generator=g, dtype=torch.int32)
+    glob[0] = max(t0 - 1, 0)
+    glob[1] = t0 + l_local + 17
+    glob = glob.to("cuda")
+    plan = dec.make_plan(batch, h_q, h_kv, l_local, policy=policy, forced_splits=forced, combine_mode=combine,
+                         seq_offset=t0)
+    assert plan.seq_offset == t0
+    ws = dec.workspace_for(plan, inp["q"].device)
+    out, lse = dec.forward(plan, inp["q"], inp["k"], inp["v"], glob, workspace=ws)
+    torch.cuda.synchronize()
+    loc = local_seqlens(glob.cpu(), t0, l_local)
+    assert int(loc[0]) == 0 and int(loc[1]) == l_local
+    ref_o, ref_l = OA.decode_attention(*(synth.to_f64(t) for t in (inp["q"], inp["k"], inp["v"], loc)))
+    assert_out_close(synth.to_f64(out), ref_o)
+    assert_lse_close(synth.to_f64(lse), ref_l)
+    # without cache_seqlens the offset does not apply: every sequence is the plan's l_k long
+    out2, lse2 = dec.forward(plan, inp["q"], inp["k"], inp["v"], None, workspace=ws)
+    torch.cuda.synchronize()
+    ref_o, ref_l = OA.decode_attention(*(synth.to_f64(t) for t in (inp["q"], inp["k"], inp["v"])),
+                                       np.full(batch, l_local))
+    assert_out_close(synth.to_f64(out2), ref_o)
+    assert_lse_close(synth.to_f64(lse2), ref_l)
