@@ -25,6 +25,18 @@ if __name__ == "__main__":
         bench(1, 8, 1, 4096, "seq_aware_sm", steps=200, reps=7)
         bench(1, 64, 8, 512, "seq_aware", pack=False, steps=200, reps=7)
         sys.exit(0)
+    if len(sys.argv) > 2 and sys.argv[1] == "one" and sys.argv[2] == "wide":
+        # G > 8: 16-row CTAs (two 8-row MMA blocks per warp) on streaming and latency shapes
+        sys.path.insert(0, os.path.join(ROOT, "scripts"))
+        from probe_timing import bench
+        bench(64, 128, 8, 8192, "seq_aware", steps=5, reps=5)      # G = 16, saturated, 2.1 GB
+        bench(32, 128, 4, 16384, "seq_aware", steps=5, reps=5)     # G = 32, 2 m-blocks of 16 rows
+        bench(128, 64, 8, 8192, "seq_aware", steps=5, reps=5)      # G = 8 reference (high-load)
+        bench(1, 128, 8, 131072, "seq_aware_sm", steps=20, reps=5) # G = 16, long context
+        bench(1, 128, 8, 131072, "seq_aware", steps=20, reps=5)
+        bench(1, 16, 1, 512, "seq_aware_sm", steps=200, reps=7)
+        bench(1, 128, 8, 512, "seq_aware_sm", steps=200, reps=7)
+        sys.exit(0)
     if len(sys.argv) > 1 and sys.argv[1] == "one":
         sys.path.insert(0, os.path.join(ROOT, "scripts"))
         from probe_timing import bench
