@@ -140,8 +140,12 @@ typedef enum da_combine_mode {
 typedef enum da_path {
   DA_PATH_SCALAR = 0,  /* one query row per CTA (pack_gqa = 0, or G = 1):
                           fp32 FMA dot products + warp-shuffle softmax          */
-  DA_PATH_MMA = 1      /* pack_gqa with G >= 2: the G query rows of a KV head
-                          share each K/V tile; QK^T and PV on tensor cores     */
+  DA_PATH_MMA = 1,     /* pack_gqa with G >= 2: the G query rows of a KV head
+                          share each K/V tile; QK^T and PV on tensor cores
+                          (mma.sync, 8 or 16 rows per CTA)                     */
+  DA_PATH_TC = 2       /* pack_gqa with G >= 32 (MQA / wide GQA) and a static
+                          split count: 64 query rows per CTA on tcgen05 (TMEM
+                          accumulators); combine NONE (s == 1) or KERNEL     */
 } da_path;
 
 /*

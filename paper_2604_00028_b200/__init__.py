@@ -14,7 +14,7 @@ missing.
 
 from . import _lib  # noqa: F401  (raises ImportError if libdecattn.so is missing)
 from ._lib import (DA_BF16, DA_COMBINE_CLUSTER, DA_COMBINE_KERNEL, DA_COMBINE_NONE, DA_F32,  # noqa: F401
-                   DA_ERR_TIMEOUT, DA_PATH_MMA, DA_PATH_SCALAR, DA_POLICY_FIXED, DA_POLICY_GUARDED,
+                   DA_ERR_TIMEOUT, DA_PATH_MMA, DA_PATH_SCALAR, DA_PATH_TC, DA_POLICY_FIXED, DA_POLICY_GUARDED,
                    DA_POLICY_SEQ_AWARE, DecAttnError, da_abi_version, da_combine, da_combine_peers, da_forward,
                    da_forward_host, da_forward_host_bytes, da_forward_paged, da_forward_peer, da_peer_signal,
                    da_plan, da_plan_make, da_plan_make_varlen, da_plan_set_combine, da_plan_set_seq_offset, da_query_residency,

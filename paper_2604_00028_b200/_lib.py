@@ -27,7 +27,7 @@ DA_OK, DA_ERR_INVALID_ARG, DA_ERR_UNSUPPORTED, DA_ERR_ALIGNMENT, DA_ERR_WORKSPAC
  DA_RULE_SM_FIT, DA_RULE_DYNAMIC) = range(12)
 DA_BF16, DA_F32 = 0, 1
 DA_COMBINE_NONE, DA_COMBINE_CLUSTER, DA_COMBINE_KERNEL = range(3)
-DA_PATH_SCALAR, DA_PATH_MMA = 0, 1
+DA_PATH_SCALAR, DA_PATH_MMA, DA_PATH_TC = 0, 1, 2
 DA_ABI_VERSION = 7
 
 POLICIES = {"guarded": DA_POLICY_GUARDED, "seq_aware": DA_POLICY_SEQ_AWARE, "fixed": DA_POLICY_FIXED,

@@ -144,6 +144,8 @@ def one_kernel_exchange_ok(plan: L.da_plan) -> bool:
     kernel's one CTA per row (workspace plans) - by the occupancy API's answer for that exact kernel
     (da_query_residency), scaled to the plan's usable SMs."""
     kernel_ws = plan.combine_mode == L.DA_COMBINE_KERNEL
+    if plan.path == L.DA_PATH_TC and not kernel_ws:
+        return False                  # the tcgen05 forward does not publish (da_forward_peer* reject it)
     units = L.da_query_residency(plan, 1 if kernel_ws else 0, 2)
     fit = units * plan.usable_sms // max(plan.num_sms, 1)
     if kernel_ws:

@@ -5,7 +5,7 @@
 (run by path, or load it by path as __graft_entry__.build() does: importing it as a submodule
 of the package would import the package first, which loads the library it is meant to build)
 
-Sources: csrc/{plan.cpp, capi.cpp, fwd.cu, combine.cu}.  Output:
+Sources: csrc/{plan.cpp, capi.cpp, fwd.cu, fwd_tc.cu, combine.cu}.  Output:
 paper_2604_00028_b200/lib/libdecattn.so (git-ignored; travels to the GPU box
 with the gpurun snapshot).  cudart is linked statically, so the library
 loads on a machine without a GPU (the planner and the symbol checks run on
@@ -26,8 +26,8 @@ BUILD = os.path.join(PKG, "build")
 LIB = os.path.join(LIBDIR, "libdecattn.so")
 INCLUDE = os.path.join(os.path.dirname(PKG), "include")
 
-SOURCES = ["plan.cpp", "capi.cpp", "fwd.cu", "combine.cu"]
-HEADERS = ["config.h", "internal.h", "ptx.cuh", "pub.cuh"]
+SOURCES = ["plan.cpp", "capi.cpp", "fwd.cu", "fwd_tc.cu", "combine.cu"]
+HEADERS = ["config.h", "internal.h", "ptx.cuh", "pub.cuh", "tile_common.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-std=c++17", "-O3", "-lineinfo", "-Xcompiler", "-fPIC,-fvisibility=hidden",
           "-I", CSRC, "-I", INCLUDE]

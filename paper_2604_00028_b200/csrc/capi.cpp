@@ -159,6 +159,9 @@ da_status forward_impl(const da_plan* plan, const void* q, const void* k_cache, 
   if (out_dtype != DA_BF16 && out_dtype != DA_F32) return DA_ERR_INVALID_ARG;
   if (!(softmax_scale <= 0.f) && !std::isfinite(softmax_scale)) return DA_ERR_INVALID_ARG;
   const bool paged = pg.block_table != nullptr;
+  // the tcgen05 kernel does not publish into a peer exchange itself: with s == 1 the peer paths take
+  // da_forward + da_peer_signal instead (with s > 1 the combine kernel publishes, as for any plan)
+  if (pub != nullptr && plan->path == DA_PATH_TC && plan->combine_mode != DA_COMBINE_KERNEL) return DA_ERR_UNSUPPORTED;
 
   const int64_t B = plan->batch, HQ = plan->h_q, HKV = plan->h_kv, D = kHeadDim;
   const int64_t rows_per_major = paged ? pg.page_size : l_cap;   // tokens per batch entry / page
@@ -217,7 +220,7 @@ da_status forward_impl(const da_plan* plan, const void* q, const void* k_cache, 
   p.G = plan->h_q / plan->h_kv;
   p.h_q = plan->h_q;
   p.batch = plan->batch;
-  p.mblocks_per_head = plan->path == DA_PATH_MMA ? (p.G + plan->rows_per_cta - 1) / plan->rows_per_cta : 1;
+  p.mblocks_per_head = plan->path != DA_PATH_SCALAR ? (p.G + plan->rows_per_cta - 1) / plan->rows_per_cta : 1;
   const float scale = softmax_scale > 0.f ? softmax_scale : 1.0f / std::sqrt(float(D));
   p.scale_log2 = scale * 1.4426950408889634f;
   p.out = out;

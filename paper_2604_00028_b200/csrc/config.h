@@ -89,6 +89,22 @@ DA_HD constexpr int helpers_for(int combine_mode) { return combine_mode == 1 ? D
 #define DECATTN_BAL_CHUNK 4
 #endif
 constexpr int kBalMinTiles = DECATTN_BAL_MIN_TILES, kBalTailDiv = DECATTN_BAL_TAIL_DIV, kBalChunk = DECATTN_BAL_CHUNK;
+// tcgen05 path (fwd_tc.cu, DA_PATH_TC): pack_gqa with G >= kTcMinG; 64 query rows per CTA (the
+// MMA's M), 4 softmax warps + a TMA producer warp + an MMA warp, kTcStages ring stages (Q, S, P
+// and O live in TMEM).  Never a cluster combine.
+#ifndef DECATTN_TC_STAGES
+#define DECATTN_TC_STAGES 6
+#endif
+#ifndef DECATTN_TC_MIN_G
+#define DECATTN_TC_MIN_G 32
+#endif
+#ifndef DECATTN_TC_MIN_TILES
+#define DECATTN_TC_MIN_TILES 16   // 64-token tiles per split at the plan's length: streaming splits only
+#endif
+constexpr int kTcMinG = DECATTN_TC_MIN_G, kTcMinTiles = DECATTN_TC_MIN_TILES;
+constexpr int kTcRows = 64;
+constexpr int kTcThreadsCfg = 6 * 32;
+constexpr int kTcSmemCfg = DECATTN_TC_STAGES * kStageBytes + 1024;   // Q and P live in TMEM
 #ifndef DECATTN_PREFETCH_LONG
 #define DECATTN_PREFETCH_LONG 1   // the pre-wait L2 prefetch of the first ring tiles also for long splits
 #endif

@@ -55,6 +55,7 @@
 #include "internal.h"
 #include "ptx.cuh"
 #include "pub.cuh"
+#include "tile_common.cuh"
 
 namespace decattn {
 
@@ -62,8 +63,6 @@ using namespace ptx;
 
 namespace {
 
-constexpr float kNegInf = -__builtin_huge_valf();
-constexpr float kLn2 = 0.6931471805599453f;
 
 // ---- development timeline tracing (only in -DDECATTN_TRACE builds; no-op otherwise) ----
 #ifdef DECATTN_TRACE
@@ -82,7 +81,6 @@ __device__ __forceinline__ int trace_cta() { return (blockIdx.z * gridDim.y + bl
 #define TRACE(slot) do { } while (0)
 #define TRACE_DEP(slot, v, on) do { } while (0)
 #endif
-constexpr int kHalfBytes = kTileN * 128;     // one 64-token x 64-dim box: 8 KB
 constexpr int kEpiStride = kHeadDim + 4;     // fp32 row stride of epilogue buffers (bank spread)
 
 // ---------------------------------------------------------------------------
@@ -278,41 +276,6 @@ __device__ __forceinline__ void scalar_tile(uint32_t sK, uint32_t sV, int valid,
     o[2] = fmaf(pt, bf16lo(vv.y), o[2]);
     o[3] = fmaf(pt, bf16hi(vv.y), o[3]);
   }
-}
-
-__device__ __forceinline__ void store_out(const FwdParams& p, void* out, size_t row, int d4, float4 v) {
-  DA_DASSERT(row < static_cast<size_t>(p.batch) * p.h_q && d4 >= 0 && d4 < kHeadDim / 4);
-  if (p.out_f32) {
-    reinterpret_cast<float4*>(out)[row * (kHeadDim / 4) + d4] = v;
-  } else {
-    uint2 w;
-    w.x = pack_bf16(v.x, v.y);
-    w.y = pack_bf16(v.z, v.w);
-    reinterpret_cast<uint2*>(out)[row * (kHeadDim / 4) + d4] = w;
-  }
-}
-
-// floor(x / d) for a launch-invariant d given m = ceil(2^38 / d) (internal.h div_magic; exact
-// while x d < 2^38): a 32 x 64-bit multiply and a shift instead of an integer divide.
-__device__ __forceinline__ uint32_t udiv_magic(uint32_t x, uint64_t m) {
-  return static_cast<uint32_t>((static_cast<uint64_t>(x) * m) >> 38);
-}
-
-// Tokens [t0, t_end) of split `split` of s for a sequence of n tokens: units of kTileN
-// tokens, split i covering units [floor(i n_u / s), floor((i+1) n_u / s)) (C-pol item 6),
-// evaluated as i q + floor(i r / s) with n_u = q s + r so every quotient is exact (n_u < 2^25,
-// i r < 2^16, s <= 256).
-__device__ __forceinline__ void split_range(int n, int split, int s, uint64_t s_magic, int& t0, int& t_end,
-                                            int& n_tiles) {
-  const uint32_t nu = (static_cast<uint32_t>(n) + (kTileN - 1)) / kTileN;
-  const uint32_t q = udiv_magic(nu, s_magic);
-  const uint32_t r = nu - q * static_cast<uint32_t>(s);
-  const uint32_t i0 = static_cast<uint32_t>(split), i1 = i0 + 1;
-  const uint32_t u0 = i0 * q + udiv_magic(i0 * r, s_magic);
-  const uint32_t u1 = i1 * q + udiv_magic(i1 * r, s_magic);
-  t0 = static_cast<int>(u0) * kTileN;
-  t_end = min(static_cast<int>(u1) * kTileN, n);
-  n_tiles = static_cast<int>(u1 - u0);
 }
 
 // DA_POLICY_DYNAMIC (C-ext-2, oracle/policy.py dynamic_schedule): one warp derives the per-batch
@@ -1132,12 +1095,14 @@ cudaError_t dispatch_combine(const da_plan& plan, const CUtensorMap& tk, const C
 cudaError_t launch_split_kv_fwd(const da_plan& plan, const CUtensorMap& tmap_k,
                                 const CUtensorMap& tmap_v, const FwdParams& p,
                                 cudaStream_t stream) {
+  if (plan.path == DA_PATH_TC) return launch_split_kv_fwd_tc(plan, tmap_k, tmap_v, p, stream);
   if (plan.path == DA_PATH_SCALAR) return dispatch_combine<DA_PATH_SCALAR, 1>(plan, tmap_k, tmap_v, p, stream);
   if (plan.rows_per_cta == 8) return dispatch_combine<DA_PATH_MMA, 1>(plan, tmap_k, tmap_v, p, stream);
   return dispatch_combine<DA_PATH_MMA, 2>(plan, tmap_k, tmap_v, p, stream);
 }
 
 cudaError_t forward_residency(const da_plan& plan, int pub, int* out) {
+  if (plan.path == DA_PATH_TC) return forward_tc_residency(out);
   if (plan.path == DA_PATH_SCALAR) return residency_combine<DA_PATH_SCALAR, 1>(plan, pub, out);
   if (plan.rows_per_cta == 8) return residency_combine<DA_PATH_MMA, 1>(plan, pub, out);
   return residency_combine<DA_PATH_MMA, 2>(plan, pub, out);

@@ -98,6 +98,7 @@ struct CombineParams {
 // plan.cpp
 void derive_launch(da_plan* p);
 bool is_dynamic(const da_plan& p);
+bool tc_path(const da_plan& p);
 bool combine_mode_valid(int mode, int s);
 
 // fwd.cu
@@ -117,6 +118,10 @@ cudaError_t launch_peer_combine(const uint64_t* peer_bases, int64_t slot_bytes, 
 // that fit the current device at once (fwd.cu: clusters for CLUSTER plans, else CTAs; pub = the
 // exchange variant 0 / 1 / 2), and CTAs of the combine kernel (combine.cu)
 cudaError_t forward_residency(const da_plan& plan, int pub, int* out);
+// fwd_tc.cu (DA_PATH_TC)
+cudaError_t launch_split_kv_fwd_tc(const da_plan& plan, const CUtensorMap& tmap_k, const CUtensorMap& tmap_v,
+                                   const FwdParams& p, cudaStream_t stream);
+cudaError_t forward_tc_residency(int* out);
 cudaError_t combine_residency(int* out);
 
 }  // namespace decattn

@@ -147,6 +147,15 @@ static int64_t launch_rows(const da_plan& p) {
   return rows;
 }
 
+// pack_gqa plans with G >= kTcMinG, a static split count and streaming splits (>= kTcMinTiles tiles
+// each at the plan's length) run the tcgen05 kernel (fwd_tc.cu): 64 query rows per CTA, no cluster
+// combine.  Short splits stay on the mma.sync kernel, whose few-tile CTAs spread over 3-7 warps and
+// merge through clusters (MQA G = 64, L_K = 512 3.4 us there, 7.4 us on tcgen05).
+bool tc_path(const da_plan& p) {
+  return p.pack_gqa != 0 && p.h_q / p.h_kv >= kTcMinG && !is_dynamic(p) &&
+         ceil_div(static_cast<int64_t>(p.l_k), kSplitUnit) >= static_cast<int64_t>(kTcMinTiles) * p.num_splits;
+}
+
 // Launch geometry for a plan whose decision fields are set.  Shared by
 // da_plan_make, da_plan_set_combine and da_forward's consistency check.
 void derive_launch(da_plan* p) {
@@ -174,6 +183,14 @@ void derive_launch(da_plan* p) {
     p->block_threads = threads_for(kWarpsNone, 0);
     p->smem_bytes = smem_for(kStagesNone, false);
   }
+  if (tc_path(*p)) {      // tcgen05 kernel: the G query rows of a KV head in ceil(G / 64) CTAs
+    p->path = DA_PATH_TC;
+    p->rows_per_cta = kTcRows;
+    p->grid_y = p->h_kv * static_cast<int32_t>(ceil_div(G, kTcRows));
+    p->block_threads = kTcThreadsCfg;
+    p->smem_bytes = kTcSmemCfg;
+    p->cluster_x = 1;
+  }
   p->workspace_bytes = p->num_splits > 1
       ? static_cast<int64_t>(p->num_splits) * p->batch * p->h_q * (p->head_dim + 1) * 4
       : 0;
@@ -188,6 +205,7 @@ int default_combine_mode(const da_plan& p) {
   const int s = p.num_splits;
   if (s == 1) return DA_COMBINE_NONE;
   if (is_dynamic(p)) return DA_COMBINE_KERNEL;   // per-batch split counts: no uniform cluster shape
+  if (tc_path(p)) return DA_COMBINE_KERNEL;       // the tcgen05 kernel has no cluster combine
   if (s > kMaxClusterSplits) return DA_COMBINE_KERNEL;
   const int G = p.h_q / p.h_kv;
   const bool mma = p.pack_gqa != 0 && G >= 2;
@@ -292,6 +310,7 @@ extern "C" da_status da_plan_set_combine(da_plan* plan, int32_t combine_mode) {
   if (plan == nullptr) return DA_ERR_INVALID_ARG;
   if (!combine_mode_valid(combine_mode, plan->num_splits)) return DA_ERR_INVALID_ARG;
   if (is_dynamic(*plan) && combine_mode != DA_COMBINE_KERNEL) return DA_ERR_INVALID_ARG;
+  if (tc_path(*plan) && combine_mode == DA_COMBINE_CLUSTER) return DA_ERR_INVALID_ARG;
   plan->combine_mode = combine_mode;
   derive_launch(plan);
   return DA_OK;

@@ -207,10 +207,13 @@ class PeerSeqShardedDecode:
         dist.barrier(group)                                # every buffer zeroed before any signal
         self.bases = torch.tensor([int(x) for x in self.hdl.buffer_ptrs], dtype=torch.int64, device=self.device)
         self.epoch = torch.zeros(1, dtype=torch.int32, device=self.device)
-        self.fused = fused
         self.counter = torch.zeros(1, dtype=torch.int32, device=self.device)   # da_forward_peer: writer CTAs
         self.plan = api.make_plan(batch, h_q, h_kv, self.l_local, head_dim, True, 0, None, policy,
                                   seq_offset=self.t0)      # cache_seqlens: whole-sequence lengths
+        from . import _lib as L
+        if self.plan.path == L.DA_PATH_TC and self.plan.combine_mode != L.DA_COMBINE_KERNEL:
+            fused = False        # the tcgen05 forward (s = 1) does not publish: forward + da_peer_signal
+        self.fused = fused
         # every rank must take the same protocol (LL words vs slot + flags): the shards' lengths can
         # differ by one token, so their plans - and whether the one-kernel grid is resident - can
         # differ; the decision is the minimum over the group

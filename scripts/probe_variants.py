@@ -36,6 +36,27 @@ if __name__ == "__main__":
         bench(1, 128, 8, 131072, "seq_aware", steps=20, reps=5)
         bench(1, 16, 1, 512, "seq_aware_sm", steps=200, reps=7)
         bench(1, 128, 8, 512, "seq_aware_sm", steps=200, reps=7)
+        bench(128, 64, 1, 8192, "seq_aware", steps=10, reps=5)     # MQA, G = 64: 4 CTAs per KV head
+        bench(32, 64, 1, 32768, "seq_aware", steps=10, reps=5)
+        bench(128, 32, 1, 8192, "seq_aware", steps=10, reps=5)     # G = 32
+        bench(128, 16, 1, 8192, "seq_aware", steps=10, reps=5)     # G = 16
+        bench(128, 8, 1, 8192, "seq_aware", steps=10, reps=5)      # G = 8
+        bench(1, 64, 1, 131072, "seq_aware", steps=20, reps=5)     # MQA long context
+        sys.exit(0)
+    if len(sys.argv) > 2 and sys.argv[1] == "one" and sys.argv[2] == "mqa":
+        # wide query groups: the tcgen05 path (G >= 32) against the mma.sync path (variant notc)
+        sys.path.insert(0, os.path.join(ROOT, "scripts"))
+        from probe_timing import bench
+        bench(128, 64, 1, 8192, "seq_aware", steps=10, reps=5)
+        bench(32, 64, 1, 32768, "seq_aware", steps=10, reps=5)
+        bench(128, 32, 1, 8192, "seq_aware", steps=10, reps=5)
+        bench(64, 128, 2, 8192, "seq_aware", steps=10, reps=5)
+        bench(1, 64, 1, 131072, "seq_aware", steps=20, reps=5)
+        bench(1, 64, 1, 131072, "seq_aware_sm", steps=20, reps=5)
+        for pol in ("guarded", "seq_aware", "seq_aware_sm"):
+            bench(1, 64, 1, 512, pol, steps=200, reps=7)
+            bench(1, 32, 1, 512, pol, steps=200, reps=7)
+            bench(4, 64, 1, 2048, pol, steps=200, reps=7)
         sys.exit(0)
     if len(sys.argv) > 1 and sys.argv[1] == "one":
         sys.path.insert(0, os.path.join(ROOT, "scripts"))

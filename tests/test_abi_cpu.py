@@ -45,9 +45,11 @@ def test_plan_struct_layout(L):
     assert names == [n for n, _ in L.da_plan._fields_]
 
 
-def _expected_launch(b, hq, hkv, lk, pack, s, U):
+def _expected_launch(b, hq, hkv, lk, pack, s, U, dynamic=False):
     G = hq // hkv
     mma = bool(pack) and G >= 2
+    if mma and G >= 32 and not dynamic and -(-lk // 64) >= 16 * s:   # DA_PATH_TC (fwd_tc.cu): 64 rows per CTA
+        return 2, 64, (s, hkv * -(-G // 64), b)
     rows = OP.launch_rows(b, G, hkv, lk, s, U) if mma else 1
     gy = hkv * -(-G // rows) if mma else hq
     return (1 if mma else 0), rows, (s, gy, b)
@@ -76,7 +78,7 @@ def test_cluster_fit_table_single_source():
 def _expected_combine(b, hq, hkv, lk, pack, sms, s, U):
     if s == 1:
         return 0
-    if s > 16:
+    if s > 16 or (pack and hq // hkv >= 32 and -(-lk // 64) >= 16 * s):   # > 16 splits or the tcgen05 path
         return 2
     _, _, (_, gy, gz) = _expected_launch(b, hq, hkv, lk, pack, s, U)
     return 1 if gy * gz <= _FIT[s] * sms // 148 else 2
@@ -89,7 +91,7 @@ def _check_plan(L, b, hq, hkv, lk, pack, margin, sms, pol, forced=0):
     geo = OP.geometry(b, hq, hkv, lk, sms, margin)
     assert (p.num_n_blocks, p.num_m_blocks, p.total_mblocks, p.usable_sms) == (
         geo["nblk"], geo["num_m_blocks"], geo["T"], geo["U"])
-    path, rows, grid = _expected_launch(b, hq, hkv, lk, pack, s, geo["U"])
+    path, rows, grid = _expected_launch(b, hq, hkv, lk, pack, s, geo["U"], dynamic=pol == "dynamic" and s > 1)
     if pol == "dynamic" and s > 1:      # C-ext-2: split slots decided on the device, workspace combine
         slots = OP.dynamic_slots(b, hkv * geo["num_m_blocks"], geo["U"], s)
         grid = (grid[1], slots, 1)                      # head groups innermost, then split slots

@@ -129,7 +129,7 @@ def test_group_sizes_mma_path(h_q, h_kv):
     run_and_check(2, h_q, h_kv, 300, seed=21)
 
 
-@pytest.mark.parametrize("h_q,h_kv", [(32, 2), (24, 2), (64, 1), (12, 1)])
+@pytest.mark.parametrize("h_q,h_kv", [(32, 2), (24, 2), (16, 1), (12, 1)])
 def test_group_sizes_16_row_ctas(h_q, h_kv):
     # G > 8 beyond 64 units: 16 query rows per CTA, incl. ragged G = 12 / 24
     plan, _, _ = run_and_check(1, h_q, h_kv, 4500, seed=22, variant="ragged")
@@ -144,8 +144,12 @@ def test_many_query_rows_per_kv_head(batch, h_q, h_kv, l_k, policy):
     # eight 16-row CTAs per KV head on the MMA path
     plan, _, _ = run_and_check(batch, h_q, h_kv, l_k, policy=policy, variant="ragged", seed=1500)
     assert plan.num_m_blocks == 2
-    assert plan.rows_per_cta == OP.launch_rows(batch, h_q // h_kv, h_kv, l_k, plan.num_splits, plan.usable_sms)
-    assert plan.rows_per_cta == 16 or l_k <= 4096
+    if plan.path == 2:        # G >= 32 with >= 16 tiles per split: tcgen05, 64 rows, two CTAs per KV head
+        assert policy != "dynamic" and -(-l_k // 64) >= 16 * plan.num_splits
+        assert (plan.rows_per_cta, plan.grid_y) == (64, 2 * h_kv)
+    else:                     # short splits and the dynamic schedule: the mma.sync kernel
+        assert plan.rows_per_cta == OP.launch_rows(batch, h_q // h_kv, h_kv, l_k, plan.num_splits, plan.usable_sms)
+        assert plan.rows_per_cta == 16 or l_k <= 4096
 
 
 def test_large_batch_small_cache():
@@ -551,3 +555,92 @@ def test_seq_offset_shard(batch, h_q, h_kv, l_local, t0, policy, forced, combine
                                        np.full(batch, l_local))
     assert_out_close(synth.to_f64(out2), ref_o)
     assert_lse_close(synth.to_f64(lse2), ref_l)
+
+
+# ---- DA_PATH_TC: the tcgen05 kernel for G >= 32 (fwd_tc.cu): 64 query rows per CTA on TMEM ----
+@pytest.mark.parametrize("batch,h_q,h_kv,l_k,policy,forced,variant", [
+    (1, 64, 1, 1024, "fixed", 1, "normal"),          # MQA G = 64, one CTA per KV head, 16 tiles
+    (4, 64, 1, 3000, "fixed", 1, "ragged"),          # an empty and a one-token sequence
+    (4, 64, 1, 3000, "fixed", 2, "ragged"),          # + empty splits of the short sequences
+    (2, 32, 1, 5000, "fixed", 2, "peaked"),          # G = 32: rows 32-63 of the CTA are padding
+    (3, 96, 2, 2000, "fixed", 1, "ragged"),          # G = 48
+    (1, 128, 1, 9000, "fixed", 4, "normal"),         # G = 128: two 64-row CTAs per KV head
+    (2, 64, 1, 4500, "fixed", 4, "peaked"),          # workspace partials
+    (8, 64, 2, 1100, "fixed", 1, "normal"),          # a partial last tile (1100 = 17 x 64 + 12)
+    (1, 64, 1, 131072, "seq_aware", 0, "normal"),    # the paper's long context as MQA-64 (s = 109)
+])
+def test_tc_path_matches_oracle(batch, h_q, h_kv, l_k, policy, forced, variant):
+    dec = _dec()
+    plan, _, _ = run_and_check(batch, h_q, h_kv, l_k, policy=policy, forced=forced, variant=variant, seed=1700,
+                               check_partials=forced > 1)
+    assert (plan.path, plan.rows_per_cta, plan.cluster_x) == (dec.DA_PATH_TC, 64, 1)
+    assert plan.combine_mode == (dec.DA_COMBINE_NONE if plan.num_splits == 1 else dec.DA_COMBINE_KERNEL)
+
+
+@pytest.mark.parametrize("pack", [True])
+def test_tc_path_edges(pack):
+    # NaN past each sequence, l_cap > l_k, fp32 output, cache_seqlens past the plan's length
+    dec = _dec()
+    for kw in (dict(batch=3, l_k=1500, l_cap=1700, variant="ragged", nan_tail=True, forced=1),
+               dict(batch=2, l_k=1100, out_f32=True, forced=1),
+               dict(batch=2, l_k=3000, out_f32=True, forced=2, check_partials=True)):
+        b_ = kw.pop("batch")
+        plan, _, _ = run_and_check(b_, 64, 1, policy="fixed", seed=1701, **kw)
+        assert plan.path == dec.DA_PATH_TC
+    # short splits stay on the mma.sync kernel (and its cluster combine)
+    plan, _, _ = run_and_check(1, 64, 1, 512, policy="seq_aware_sm", seed=1704)
+    assert plan.path == dec.DA_PATH_MMA
+
+
+def test_tc_path_rescales_when_the_maximum_grows():
+    # scores that climb by ~16 (log2 units) every 64-token tile: the running reference moves and
+    # the O rows in TMEM are rescaled on every tile (the path that is rare on N(0, 1) inputs)
+    dec = _dec()
+    batch, h_q, h_kv, l_k = 2, 64, 1, 1024
+    g = torch.Generator(device="cpu").manual_seed(1710)
+    base = torch.randn(128, generator=g)
+    q = (base + 0.05 * torch.randn(batch, h_q, 128, generator=g)).to(torch.bfloat16)
+    ramp = torch.arange(l_k, dtype=torch.float32) / 64.0 * 1.3
+    k = (ramp[None, :, None, None] * base[None, None, None, :] / base.norm() * 11.3
+         + 0.3 * torch.randn(batch, l_k, h_kv, 128, generator=g)).to(torch.bfloat16)
+    v = torch.randn(batch, l_k, h_kv, 128, generator=g).to(torch.bfloat16)
+    seq = torch.tensor([l_k, 700], dtype=torch.int32)
+    plan = dec.make_plan(batch, h_q, h_kv, l_k, policy="fixed", forced_splits=1)   # one CTA: 16 tiles
+    assert plan.path == dec.DA_PATH_TC and plan.num_splits == 1
+    out, lse = dec.forward(plan, q.cuda(), k.cuda(), v.cuda(), seq.cuda())
+    torch.cuda.synchronize()
+    ref_o, ref_l = OA.decode_attention(*(synth.to_f64(t) for t in (q, k, v, seq)))
+    assert (np.diff(ref_l) != 0).any()
+    assert_out_close(synth.to_f64(out), ref_o)
+    assert_lse_close(synth.to_f64(lse), ref_l)
+
+
+def test_tc_path_paged_offset_and_graph():
+    dec = _dec()
+    assert run_paged(3, 64, 1, 2500, 128, policy="fixed", forced=1, seed=1720).path == dec.DA_PATH_TC
+    assert run_paged(2, 128, 2, 2600, 256, policy="fixed", forced=2, seed=1721).path == dec.DA_PATH_TC
+    # a sequence shard (seq_offset) and CUDA-graph replays of the tcgen05 kernel
+    batch, h_q, h_kv, l_local, t0 = 3, 64, 1, 2000, 777
+    from paper_2604_00028_b200.dist import local_seqlens
+    inp = synth.make_inputs(batch, h_q, h_kv, l_local, seed=1722, device="cuda")
+    glob = torch.tensor([100, t0 + l_local + 5, t0 + 900], dtype=torch.int32, device="cuda")
+    plan = dec.make_plan(batch, h_q, h_kv, l_local, policy="fixed", forced_splits=2, seq_offset=t0)
+    assert plan.path == dec.DA_PATH_TC
+    ws = dec.workspace_for(plan, inp["q"].device)
+    out = torch.empty((batch, h_q, 128), dtype=torch.bfloat16, device="cuda")
+    lse = torch.empty((batch, h_q), dtype=torch.float32, device="cuda")
+    st = torch.cuda.Stream()
+    with torch.cuda.stream(st):
+        dec.forward(plan, inp["q"], inp["k"], inp["v"], glob, out=out, lse=lse, workspace=ws)
+    torch.cuda.synchronize()
+    gr = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(gr, stream=st):
+        for _ in range(3):
+            dec.forward(plan, inp["q"], inp["k"], inp["v"], glob, out=out, lse=lse, workspace=ws)
+    out.zero_()
+    gr.replay()
+    torch.cuda.synchronize()
+    loc = local_seqlens(glob.cpu(), t0, l_local)
+    ref_o, ref_l = OA.decode_attention(*(synth.to_f64(t) for t in (inp["q"], inp["k"], inp["v"], loc)))
+    assert_out_close(synth.to_f64(out), ref_o)
+    assert_lse_close(synth.to_f64(lse), ref_l)
