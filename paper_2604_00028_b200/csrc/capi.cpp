@@ -69,15 +69,17 @@ bool one_allocation(const void* a, size_t bytes) {
 // the consumers' ldmatrix addressing expects.  Tokens past l_cap read as zero.
 // For a paged pool [num_pages, page_size, H_KV, d] the same map is built with (num_pages,
 // page_size, page stride) in place of (B, l_cap, batch stride).
+// box_halves: 2 = one box per 64-token tile (both 64-dim halves, the mma.sync kernels); 1 = one
+// box per tile and half (the tcgen05 kernel's [half][128 tokens][64 dims] stages)
 bool make_kv_tmap(CUtensorMap* map, const void* base, int32_t batch, int32_t l_cap, int32_t h_kv,
-                  int64_t sb, int64_t st, int64_t sh) {
+                  int64_t sb, int64_t st, int64_t sh, uint32_t box_halves = 2) {
   auto fn = encode_fn();
   if (fn == nullptr) return false;
   cuuint64_t dims[5] = {64, static_cast<cuuint64_t>(l_cap), 2, static_cast<cuuint64_t>(h_kv),
                         static_cast<cuuint64_t>(batch)};
   cuuint64_t strides[4] = {static_cast<cuuint64_t>(st) * 2, 128, static_cast<cuuint64_t>(sh) * 2,
                            static_cast<cuuint64_t>(sb) * 2};
-  cuuint32_t box[5] = {64, static_cast<cuuint32_t>(kTileN), 2, 1, 1};
+  cuuint32_t box[5] = {64, static_cast<cuuint32_t>(kTileN), box_halves, 1, 1};
   cuuint32_t estr[5] = {1, 1, 1, 1, 1};
   CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<void*>(base), dims, strides,
                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -203,8 +205,9 @@ da_status forward_impl(const da_plan* plan, const void* q, const void* k_cache, 
   const int32_t emul = (pub != nullptr && pub->emulate) ? pub->world : 1;
   const int32_t major = paged ? pg.num_pages : plan->batch * emul;
   const int32_t rows = paged ? pg.page_size : l_cap;
-  if (!make_kv_tmap(&tk, k_cache, major, rows, plan->h_kv, sd[2], sd[3], sd[4]) ||
-      !make_kv_tmap(&tv, v_cache, major, rows, plan->h_kv, sd[5], sd[6], sd[7]))
+  const uint32_t halves = plan->path == DA_PATH_TC ? 1u : 2u;
+  if (!make_kv_tmap(&tk, k_cache, major, rows, plan->h_kv, sd[2], sd[3], sd[4], halves) ||
+      !make_kv_tmap(&tv, v_cache, major, rows, plan->h_kv, sd[5], sd[6], sd[7], halves))
     return DA_ERR_CUDA;
 
   FwdParams p{};

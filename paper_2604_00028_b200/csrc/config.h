@@ -93,7 +93,7 @@ constexpr int kBalMinTiles = DECATTN_BAL_MIN_TILES, kBalTailDiv = DECATTN_BAL_TA
 // MMA's M), 4 softmax warps + a TMA producer warp + an MMA warp, kTcStages ring stages (Q, S, P
 // and O live in TMEM).  Never a cluster combine.
 #ifndef DECATTN_TC_STAGES
-#define DECATTN_TC_STAGES 6
+#define DECATTN_TC_STAGES 3
 #endif
 #ifndef DECATTN_TC_MIN_G
 #define DECATTN_TC_MIN_G 32
@@ -104,7 +104,7 @@ constexpr int kBalMinTiles = DECATTN_BAL_MIN_TILES, kBalTailDiv = DECATTN_BAL_TA
 constexpr int kTcMinG = DECATTN_TC_MIN_G, kTcMinTiles = DECATTN_TC_MIN_TILES;
 constexpr int kTcRows = 64;
 constexpr int kTcThreadsCfg = 6 * 32;
-constexpr int kTcSmemCfg = DECATTN_TC_STAGES * kStageBytes + 1024;   // Q and P live in TMEM
+constexpr int kTcSmemCfg = DECATTN_TC_STAGES * 2 * kStageBytes + 1024;   // 128-token stages; Q, S, P, O in TMEM
 #ifndef DECATTN_PREFETCH_LONG
 #define DECATTN_PREFETCH_LONG 1   // the pre-wait L2 prefetch of the first ring tiles also for long splits
 #endif

@@ -46,25 +46,33 @@ using namespace ptx;
 
 namespace {
 
-constexpr int kTcM = kTcRows;                    // query rows of a CTA (the MMA's M)
-constexpr int kTcStages = DECATTN_TC_STAGES;     // K / V ring stages (32 KB each)
+constexpr int kTcM = kTcRows;                    // query rows of a CTA (the S MMA's M)
+constexpr int kTcT = 2 * kTileN;                 // tokens per stage (the S MMA's N): two 64-token tiles
+constexpr int kTcStageBytes = 2 * kStageBytes;   // K [half][128 tokens][64 dims] + V: 64 KB
+constexpr int kTcStages = DECATTN_TC_STAGES;     // ring stages
 constexpr int kTcSoftmaxWarps = 4;
 constexpr int kTcThreads = (kTcSoftmaxWarps + 2) * 32;   // + TMA producer warp + MMA warp
 constexpr int kTcProducerWarp = kTcSoftmaxWarps, kTcMmaWarp = kTcSoftmaxWarps + 1;
-// TMEM columns (512 allocated): S double buffer, the O accumulator, Q and the P buffers as the A
-// operands of the MMAs (A from TMEM: two bf16 per 32-bit column, row r on the accumulator's lane)
+// TMEM columns (512 allocated): two S buffers (P is written over S once the softmax warps read it),
+// the O accumulator and Q (the S MMA's A operand, two bf16 per 32-bit column, row r on the
+// accumulator's lane).  The PV product runs at M = 128 with the P pair stacked along M: in warp
+// quadrant q, TMEM lanes 32 q + i hold P_hi and lanes 32 q + 16 + i hold P_lo of row 16 q + i
+// (i < 16), so the O rows on those lanes are the hi and lo parts of the row's output (summed in
+// the epilogue) and every lane a thread touches stays in its warp's quadrant: one pass over V at
+// M = 128, N = 128 instead of two passes at M = 64 (each at half the tensor rate).
 constexpr int kTcTmemCols = 512;
-constexpr uint32_t kTcColS = 0, kTcColO = 128, kTcColQ = 256, kTcColP = 320;   // P: [buf][32]
-// The PV product runs at M = 128 with the P pair stacked along M: in warp quadrant q, TMEM lanes
-// 32 q + i hold P_hi and lanes 32 q + 16 + i hold P_lo of row 16 q + i (i < 16), so the O
-// accumulator rows on those lanes are the hi and lo parts of the row's output (summed in the
-// epilogue) and every lane a thread touches stays in its warp's quadrant.  One pass over V (4 MMAs
-// at M = 128, N = 128) instead of two passes at M = 64 (8 MMAs, each at half the tensor rate).
-constexpr int kTcSmem = kTcStages * kStageBytes + 1024;
+constexpr uint32_t kTcColSP = 0, kTcColO = 2 * kTcT, kTcColQ = kTcColO + 128;
+constexpr int kTcSmem = kTcStages * kTcStageBytes + 1024;
 static_assert(kTcSmem <= 227 * 1024, "tcgen05 path shared memory");
 static_assert(kTcSmem == kTcSmemCfg && kTcThreads == kTcThreadsCfg, "the planner's launch fields (config.h)");
-static_assert(kTcColP + 2 * 32 <= kTcTmemCols, "TMEM columns");
+static_assert(kTcColQ + 64 <= kTcTmemCols, "TMEM columns");
 constexpr float kTcRescaleLog2 = 8.f;            // rescale O only when the maximum grows by > 2^8
+
+#ifdef DECATTN_TC_DBG_NOSM   // timing experiment only: no exponentials (wrong results)
+#define TC_EX2(x) (x)
+#else
+#define TC_EX2(x) ex2(x)
+#endif
 
 // development timeline tracing (-DDECATTN_TRACE builds): globaltimer ns of tiles 16..23 of the
 // first 64 CTAs: 0+k K TMA issued, 8+k S issued, 16+k S seen by softmax warp 0, 24+k P written,
@@ -210,12 +218,11 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   extern __shared__ uint8_t smem_raw[];
   __shared__ __align__(8) uint64_t full_bar[NS];    // K of the stage has landed
   __shared__ __align__(8) uint64_t fullv_bar[NS];   // V of the stage has landed
-  __shared__ __align__(8) uint64_t empty_bar[NS];   // PV of the stage's tile done (tcgen05.commit)
-  __shared__ __align__(8) uint64_t q_bar;           // Q is in shared memory (128 softmax threads)
-  __shared__ __align__(8) uint64_t s_full[2];       // S(i) in TMEM buffer i & 1 (commit)
-  __shared__ __align__(8) uint64_t s_free[2];       // the softmax warps read S buffer b (4 warps)
-  __shared__ __align__(8) uint64_t p_full[2];       // P buffer b written (4 warps)
-  __shared__ __align__(8) uint64_t pv_done[2];      // O += P(j) V(j) done for j & 1 == b (commit)
+  __shared__ __align__(8) uint64_t empty_bar[NS];   // PV of the stage done (tcgen05.commit)
+  __shared__ __align__(8) uint64_t q_bar;           // Q is in TMEM (128 softmax threads)
+  __shared__ __align__(8) uint64_t s_full[2];       // S(s) in TMEM buffer s & 1 (commit)
+  __shared__ __align__(8) uint64_t p_full[2];       // P(s) written over S(s) (4 warps)
+  __shared__ __align__(8) uint64_t pv_done[2];      // O += P(s) V(s) done for s & 1 == b (commit)
   __shared__ uint32_t tmem_base;
 
   const uint32_t raw = smem_u32(smem_raw);
@@ -238,13 +245,12 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     mbar_init(smem_u32(&q_bar), kTcSoftmaxWarps * 32);
     for (int i = 0; i < 2; ++i) {
       mbar_init(smem_u32(&s_full[i]), 1);
-      mbar_init(smem_u32(&s_free[i]), kTcSoftmaxWarps);
       mbar_init(smem_u32(&p_full[i]), kTcSoftmaxWarps);
       mbar_init(smem_u32(&pv_done[i]), 1);
     }
     fence_mbarrier_init();
   }
-  if (warp == kTcMmaWarp) {   // TMEM: S double buffer + O accumulator
+  if (warp == kTcMmaWarp) {   // TMEM: S / P double buffer, O accumulator, Q
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base)),
                  "r"(kTcTmemCols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -260,89 +266,104 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   const uint32_t tmem = tmem_base;
 
   // this split's range at the plan's length (exact without cache_seqlens; a guess for the L2
-  // prefetch otherwise, recomputed after the wait as in fwd.cu)
+  // prefetch otherwise, recomputed after the wait as in fwd.cu); tiles of 64 tokens, stages of two
   int t0 = 0, t_end = 0, n_tiles = 0;
   split_range(min(max(p.l_default, 0), p.l_cap), split, p.num_splits, p.s_magic, t0, t_end, n_tiles);
   if (p.block_table == nullptr && warp == kTcProducerWarp && lane == 0 && n_tiles >= 1) {
-    const int np = min(n_tiles, NS);
-    for (int i = 0; i < np; ++i) tma_prefetch_5d(&tmap_k, 0, t0 + i * kTileN, 0, kvh, b);
-    for (int i = 0; i < np; ++i) tma_prefetch_5d(&tmap_v, 0, t0 + i * kTileN, 0, kvh, b);
+    const int np = min(n_tiles, 2 * NS);
+    for (int i = 0; i < np; ++i)
+      for (int h = 0; h < 2; ++h) {
+        tma_prefetch_5d(&tmap_k, 0, t0 + i * kTileN, h, kvh, b);
+        tma_prefetch_5d(&tmap_v, 0, t0 + i * kTileN, h, kvh, b);
+      }
   }
   pdl_launch_dependents();
   pdl_wait();
   if (p.seqlens != nullptr)
     split_range(min(max(max(__ldg(p.seqlens + b), 0) - p.seq_offset, 0), p.l_cap), split, p.num_splits, p.s_magic,
                 t0, t_end, n_tiles);
+  const int n_st = (n_tiles + 1) >> 1;                 // 128-token stages
 
   if (warp == kTcProducerWarp) {
     // ================= TMA producer (dense or paged cache) =================
+    // a stage holds K then V of two 64-token tiles as [half][128 tokens][64 dims] (one 8 KB box per
+    // tile and half); the second tile of a split's last stage may be missing (not loaded: its
+    // tokens are masked and its V rows zeroed by the softmax warps)
     if (lane == 0) {
       const int32_t* bt = p.block_table != nullptr ? p.block_table + static_cast<int64_t>(b) * p.bt_stride : nullptr;
       const uint32_t tpp = p.page_size > 0 ? static_cast<uint32_t>(p.page_size / kTileN) : 1u;
       const uint32_t tile0 = static_cast<uint32_t>(t0 / kTileN);
       uint32_t cj = bt != nullptr ? udiv_magic(tile0, p.page_magic) : 0u, ck = tile0 - cj * tpp;
-      for (int i = 0; i < n_tiles; ++i) {
-        const int st = i % NS;
-        if (i >= NS) mbar_wait(smem_u32(&empty_bar[st]), ((i / NS) - 1) & 1);
+      for (int s = 0; s < n_st; ++s) {
+        const int st = s % NS;
+        if (s >= NS) mbar_wait(smem_u32(&empty_bar[st]), ((s / NS) - 1) & 1);
+        const int nsub = min(2, n_tiles - 2 * s);
         const uint32_t fb = smem_u32(&full_bar[st]), fvb = smem_u32(&fullv_bar[st]);
-        mbar_arrive_expect_tx(fb, kStageBytes / 2);
-        mbar_arrive_expect_tx(fvb, kStageBytes / 2);
-        const uint32_t dst = sbase + st * kStageBytes;
-        int major = b, tok = t0 + i * kTileN;
-        if (bt != nullptr) {   // paged: tile i in page block_table[b][t / page_size] at t % page_size
-          major = __ldg(bt + cj);
-          tok = static_cast<int>(ck) * kTileN;
-          if (++ck == tpp) { ck = 0; ++cj; }
+        mbar_arrive_expect_tx(fb, nsub * 2 * kHalfBytes);
+        mbar_arrive_expect_tx(fvb, nsub * 2 * kHalfBytes);
+        const uint32_t sK = sbase + st * kTcStageBytes, sV = sK + kTcStageBytes / 2;
+        for (int sub = 0; sub < nsub; ++sub) {
+          int major = b, tok = t0 + (2 * s + sub) * kTileN;
+          if (bt != nullptr) {   // paged: tile in page block_table[b][t / page_size] at t % page_size
+            major = __ldg(bt + cj);
+            tok = static_cast<int>(ck) * kTileN;
+            if (++ck == tpp) { ck = 0; ++cj; }
+          }
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            tma_load_5d(sK + h * (kTcStageBytes / 4) + sub * kHalfBytes, &tmap_k, fb, 0, tok, h, kvh, major);
+            tma_load_5d(sV + h * (kTcStageBytes / 4) + sub * kHalfBytes, &tmap_v, fvb, 0, tok, h, kvh, major);
+          }
         }
-        tma_load_5d(dst, &tmap_k, fb, 0, tok, 0, kvh, major);
-        tma_load_5d(dst + 2 * kHalfBytes, &tmap_v, fvb, 0, tok, 0, kvh, major);
-        TC_TRACE(0, i);
+        TC_TRACE(0, s);
       }
     }
   } else if (warp == kTcMmaWarp) {
     // ================= MMA issuer (one lane) =================
-    if (lane == 0 && n_tiles > 0) {
-      constexpr uint32_t id_s = tc_idesc(kTcM, kTileN, 0, 0);
-      constexpr uint32_t id_o = tc_idesc(2 * kTcM, kHeadDim, 0, 1);   // [P_hi; P_lo] stacked along M
+    if (lane == 0 && n_st > 0) {
+      constexpr uint32_t id_s = tc_idesc(kTcM, kTcT, 0, 0);             // S: M = 64, N = 128 tokens
+      constexpr uint32_t id_o = tc_idesc(2 * kTcM, kHeadDim, 0, 1);     // O: [P_hi; P_lo] stacked along M
       mbar_wait(smem_u32(&q_bar), 0);
-      auto issue_pv = [&](int j) {
-        const int st = j % NS, pb = j & 1;
-        mbar_wait(smem_u32(&p_full[pb]), (j >> 1) & 1);
-        mbar_wait(smem_u32(&fullv_bar[st]), (j / NS) & 1);
+      // S(s) = Q K(s)^T into TMEM buffer s & 1.  The buffer held P(s - 2), read by PV(s - 2), which
+      // was issued before: the tensor pipe executes in issue order
+      auto issue_s = [&](int s) {
+        const int st = s % NS, sb = s & 1;
+        mbar_wait(smem_u32(&full_bar[st]), (s / NS) & 1);
         tc_fence_after();
-        const uint32_t sV = sbase + st * kStageBytes + 2 * kHalfBytes;
-        const uint32_t pcol = tmem + kTcColP + pb * 32;
+        TC_TRACE(48, s);
+        const uint32_t sK = sbase + st * kTcStageBytes;
 #pragma unroll
-        for (int kk = 0; kk < 4; ++kk) {   // 16 tokens (8 packed columns, 16 V rows) per step
-          const uint64_t bv = tc_sdesc(sV + kk * 2048, 8 * 1024, 1024);
-          tc_mma_ts(tmem + kTcColO, pcol + kk * 8, bv, id_o, (j > 0 || kk > 0) ? 1u : 0u);
+        for (int kk = 0; kk < 8; ++kk) {   // 16 dims per step: K half kk / 4, +32 B per step in the row
+          const uint64_t bk = tc_sdesc(sK + (kk >> 2) * (kTcStageBytes / 4) + (kk & 3) * 32, 16, 1024);
+          tc_mma_ts(tmem + kTcColSP + sb * kTcT, tmem + kTcColQ + kk * 8, bk, id_s, kk > 0 ? 1u : 0u);
+        }
+        tc_commit(smem_u32(&s_full[sb]));
+        TC_TRACE(8, s);
+      };
+      // O += P(s) V(s), once the softmax warps wrote P(s) (over S(s)) and V(s) landed
+      auto issue_pv = [&](int s) {
+        const int st = s % NS, pb = s & 1;
+        mbar_wait(smem_u32(&p_full[pb]), (s >> 1) & 1);
+        mbar_wait(smem_u32(&fullv_bar[st]), (s / NS) & 1);
+        tc_fence_after();
+        TC_TRACE(56, s);
+        const uint32_t sV = sbase + st * kTcStageBytes + kTcStageBytes / 2;
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {   // 16 tokens (8 packed columns, 16 V rows) per step
+          const uint64_t bv = tc_sdesc(sV + kk * 2048, kTcStageBytes / 4, 1024);
+          tc_mma_ts(tmem + kTcColO, tmem + kTcColSP + pb * kTcT + kk * 8, bv, id_o, (s > 0 || kk > 0) ? 1u : 0u);
         }
         tc_commit(smem_u32(&pv_done[pb]));
         tc_commit(smem_u32(&empty_bar[st]));
-        TC_TRACE(32, j);
+        TC_TRACE(32, s);
       };
-      // S(i) = Q K(i)^T into TMEM buffer i & 1, once K(i) landed and the softmax warps read S(i - 2)
-      auto issue_s = [&](int i) {
-        const int st = i % NS, sb = i & 1;
-        mbar_wait(smem_u32(&full_bar[st]), (i / NS) & 1);
-        if (i >= 2) mbar_wait(smem_u32(&s_free[sb]), ((i - 2) >> 1) & 1);
-        tc_fence_after();
-        const uint32_t sK = sbase + st * kStageBytes;
-#pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {   // 16 dims per step: K box kk / 4, +32 B per step in the row
-          const uint64_t bk = tc_sdesc(sK + (kk >> 2) * kHalfBytes + (kk & 3) * 32, 16, 1024);
-          tc_mma_ts(tmem + kTcColS + sb * kTileN, tmem + kTcColQ + kk * 8, bk, id_s, kk > 0 ? 1u : 0u);
-        }
-        tc_commit(smem_u32(&s_full[sb]));
-        TC_TRACE(8, i);
-      };
-      // two S tiles ahead, then PV(j) and S(j + 2): the tensor pipe runs PV(j) and S(j + 2) while
-      // the softmax warps work on tile j + 1, whose S is already there
+      // two S stages ahead, then PV(s) and S(s + 2): the tensor pipe runs PV(s) and S(s + 2) while
+      // the softmax warps work on stage s + 1, whose S is already there
       issue_s(0);
-      if (n_tiles > 1) issue_s(1);
-      for (int j = 0; j < n_tiles; ++j) {
-        issue_pv(j);
-        if (j + 2 < n_tiles) issue_s(j + 2);
+      if (n_st > 1) issue_s(1);
+      for (int s = 0; s < n_st; ++s) {
+        issue_pv(s);
+        if (s + 2 < n_st) issue_s(s + 2);
       }
     }
   } else {
@@ -375,26 +396,25 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       mbar_arrive(smem_u32(&q_bar));
     }
     float mA = kNegInf, mB = kNegInf, lA = 0.f, lB = 0.f;   // reference maxima (log2 units), partial sums
-    for (int i = 0; i < n_tiles; ++i) {
-      const int sb = i & 1;
-      const int valid = min(kTileN, t_end - (t0 + i * kTileN));
-      mbar_wait(smem_u32(&s_full[sb]), (i >> 1) & 1);
+    for (int s = 0; s < n_st; ++s) {
+      const int sb = s & 1;
+      const uint32_t sp = tmem + lane_addr + kTcColSP + sb * kTcT;   // the S / P buffer of this stage
+      const int valid = min(kTcT, t_end - (t0 + s * kTcT));
+      mbar_wait(smem_u32(&s_full[sb]), (s >> 1) & 1);
       tc_fence_after();
-      if (threadIdx.x == 0) TC_TRACE(16, i);
-      float sv[32];
+      if (threadIdx.x == 0) TC_TRACE(16, s);
+      float sv[64];   // [half h][group g][4]: tokens 64 h + 8 g + 2 a (+1) of rows rA, rB
       {
-        uint32_t raw32[32];
-        tc_ld16x256<8>(tmem + lane_addr + kTcColS + sb * kTileN, raw32);
+        uint32_t r0[32], r1[32];
+        tc_ld16x256<8>(sp, r0);
+        tc_ld16x256<8>(sp + 64, r1);
         tc_wait_ld();
 #pragma unroll
-        for (int c = 0; c < 32; ++c) sv[c] = __uint_as_float(raw32[c]);
+        for (int c = 0; c < 32; ++c) sv[c] = __uint_as_float(r0[c]), sv[32 + c] = __uint_as_float(r1[c]);
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(smem_u32(&s_free[sb]));   // S buffer sb may take S(i + 2)
-      if (valid < kTileN) {                               // tokens past the range
+      if (valid < kTcT) {                                 // tokens past the range
 #pragma unroll
-        for (int g = 0; g < 8; ++g)
+        for (int g = 0; g < 16; ++g)
 #pragma unroll
           for (int c = 0; c < 2; ++c) {
             const bool ok = 8 * g + 2 * a4 + c < valid;
@@ -407,7 +427,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       float yA = fmaxf(fmaxf(sv[8], sv[9]), fmaxf(sv[12], sv[13]));
       float yB = fmaxf(fmaxf(sv[10], sv[11]), fmaxf(sv[14], sv[15]));
 #pragma unroll
-      for (int g = 4; g < 8; g += 2) {
+      for (int g = 4; g < 16; g += 2) {
         xA = fmaxf(xA, fmaxf(sv[4 * g], sv[4 * g + 1]));
         xB = fmaxf(xB, fmaxf(sv[4 * g + 2], sv[4 * g + 3]));
         yA = fmaxf(yA, fmaxf(sv[4 * g + 4], sv[4 * g + 5]));
@@ -420,17 +440,14 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       xA = fmaxf(xA, __shfl_xor_sync(0xffffffffu, xA, 2));
       xB = fmaxf(xB, __shfl_xor_sync(0xffffffffu, xB, 2));
       const float mxA = xA * p.scale_log2, mxB = xB * p.scale_log2;   // >= 1 valid token: finite
-      // the P buffer sb was read by PV(i - 2)
-      if (i >= 2) mbar_wait(smem_u32(&pv_done[sb]), ((i - 2) >> 1) & 1);
-      if (threadIdx.x == 0) TC_TRACE(40, i);
-      if (i == 0) mA = mxA, mB = mxB;                    // PV(0) starts O (accumulate = 0)
-      // the reference moves only when this tile's maximum exceeds it by more than 2^8: then the
-      // row's O (PV(0 .. i-1): wait for PV(i - 1)) and l are rescaled by exp2(m_old - m_new).  The
+      if (s == 0) mA = mxA, mB = mxB;                    // PV(0) starts O (accumulate = 0)
+      // the reference moves only when this stage's maximum exceeds it by more than 2^8: then the
+      // row's O (PV(0 .. s-1): wait for PV(s - 1)) and l are rescaled by exp2(m_old - m_new).  The
       // TMEM load / store is warp-collective: every lane takes part, factor 1 for unchanged rows
-      const bool resA = i > 0 && mxA > mA + kTcRescaleLog2, resB = i > 0 && mxB > mB + kTcRescaleLog2;
+      const bool resA = s > 0 && mxA > mA + kTcRescaleLog2, resB = s > 0 && mxB > mB + kTcRescaleLog2;
       if (__any_sync(0xffffffffu, resA || resB)) {
         const float alA = resA ? ex2(mA - mxA) : 1.f, alB = resB ? ex2(mB - mxB) : 1.f;
-        mbar_wait(smem_u32(&pv_done[(i - 1) & 1]), ((i - 1) >> 1) & 1);
+        mbar_wait(smem_u32(&pv_done[(s - 1) & 1]), ((s - 1) >> 1) & 1);
         tc_fence_after();
 #pragma unroll
         for (int h = 0; h < 4; ++h) {   // the hi lanes (h < 2) and lo lanes, O columns [64 (h & 1), + 64)
@@ -451,41 +468,46 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         if (resA) lA *= alA, mA = mxA;
         if (resB) lB *= alB, mB = mxB;
       }
-      // P = exp2(scale S - m) <= 2^8 as the pair P_hi + P_lo into the TMEM P buffer sb: u32 column
-      // j = tokens 2 j, 2 j + 1 = 4 g + a, 16x128b layout (the S layout's token pair of group g)
+      // P = exp2(scale S - m) <= 2^8 as the pair P_hi + P_lo, written over S(s): u32 column
+      // j = tokens 2 j, 2 j + 1 = 4 g + a (16x128b layout: the S layout's token pair of group g);
+      // P_hi on lanes 32 q + i, P_lo on lanes 32 q + 16 + i
       const float nA = -mA, nB = -mB;
-      uint32_t hw[16], lw[16];
       float sA0 = 0.f, sA1 = 0.f, sB0 = 0.f, sB1 = 0.f;
 #pragma unroll
-      for (int g = 0; g < 8; ++g) {
-        const float pa0 = ex2(fmaf(sv[4 * g], p.scale_log2, nA)), pa1 = ex2(fmaf(sv[4 * g + 1], p.scale_log2, nA));
-        const float pb0 = ex2(fmaf(sv[4 * g + 2], p.scale_log2, nB)), pb1 = ex2(fmaf(sv[4 * g + 3], p.scale_log2, nB));
-        if (g & 1) sA1 += pa0 + pa1, sB1 += pb0 + pb1;
-        else sA0 += pa0 + pa1, sB0 += pb0 + pb1;
-        hw[2 * g] = pack_bf16(pa0, pa1);
-        hw[2 * g + 1] = pack_bf16(pb0, pb1);
-        lw[2 * g] = pack_bf16(pa0 - bf16lo(hw[2 * g]), pa1 - bf16hi(hw[2 * g]));
-        lw[2 * g + 1] = pack_bf16(pb0 - bf16lo(hw[2 * g + 1]), pb1 - bf16hi(hw[2 * g + 1]));
+      for (int h = 0; h < 2; ++h) {
+        uint32_t hw[16], lw[16];
+#pragma unroll
+        for (int g8 = 0; g8 < 8; ++g8) {
+          const int g = 8 * h + g8;
+          const float pa0 = TC_EX2(fmaf(sv[4 * g], p.scale_log2, nA)), pa1 = TC_EX2(fmaf(sv[4 * g + 1], p.scale_log2, nA));
+          const float pb0 = TC_EX2(fmaf(sv[4 * g + 2], p.scale_log2, nB)), pb1 = TC_EX2(fmaf(sv[4 * g + 3], p.scale_log2, nB));
+          if (g8 & 1) sA1 += pa0 + pa1, sB1 += pb0 + pb1;
+          else sA0 += pa0 + pa1, sB0 += pb0 + pb1;
+          hw[2 * g8] = pack_bf16(pa0, pa1);
+          hw[2 * g8 + 1] = pack_bf16(pb0, pb1);
+          lw[2 * g8] = pack_bf16(pa0 - bf16lo(hw[2 * g8]), pa1 - bf16hi(hw[2 * g8]));
+          lw[2 * g8 + 1] = pack_bf16(pb0 - bf16lo(hw[2 * g8 + 1]), pb1 - bf16hi(hw[2 * g8 + 1]));
+        }
+        tc_st16x128_x8(sp + 32 * h, hw);
+        tc_st16x128_x8(sp + (16u << 16) + 32 * h, lw);
       }
       lA += sA0 + sA1;
       lB += sB0 + sB1;
-      tc_st16x128_x8(tmem + lane_addr + kTcColP + sb * 32, hw);                                  // lanes 32 q + i
-      tc_st16x128_x8(tmem + lane_addr + (16u << 16) + kTcColP + sb * 32, lw);                   // 32 q + 16 + i
-      if (valid < kTileN) {
-        // V rows past the range may hold anything (even NaN): zero them (P = 0 there, 0 x NaN = NaN)
-        const int st = i % NS;
-        mbar_wait(smem_u32(&fullv_bar[st]), (i / NS) & 1);
-        const uint32_t sV = sbase + st * kStageBytes + 2 * kHalfBytes;
-        for (int e = threadIdx.x; e < (kTileN - valid) * 16; e += kTcSoftmaxWarps * 32) {
+      if (valid < kTcT) {
+        // V rows past the range may hold anything (stale or NaN): zero them (P = 0 there)
+        const int st = s % NS;
+        mbar_wait(smem_u32(&fullv_bar[st]), (s / NS) & 1);
+        const uint32_t sV = sbase + st * kTcStageBytes + kTcStageBytes / 2;
+        for (int e = threadIdx.x; e < (kTcT - valid) * 16; e += kTcSoftmaxWarps * 32) {
           const int row = valid + (e >> 4), c = e & 15;
-          sts128(sV + (c >> 3) * kHalfBytes + sw128_chunk(row, c & 7), make_uint4(0, 0, 0, 0));
+          sts128(sV + (c >> 3) * (kTcStageBytes / 4) + sw128_chunk(row, c & 7), make_uint4(0, 0, 0, 0));
         }
         fence_proxy_async_smem();
       }
       tc_wait_st();
       tc_fence_before();
       __syncwarp();
-      if (threadIdx.x == 0) TC_TRACE(24, i);
+      if (threadIdx.x == 0) TC_TRACE(24, s);
       if (lane == 0) mbar_arrive(smem_u32(&p_full[sb]));
     }
     // ================= epilogue =================
@@ -494,8 +516,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     lA += __shfl_xor_sync(0xffffffffu, lA, 2);
     lB += __shfl_xor_sync(0xffffffffu, lB, 2);
     float invA = 0.f, invB = 0.f, lseA = kNegInf, lseB = kNegInf;
-    if (n_tiles > 0) {
-      mbar_wait(smem_u32(&pv_done[(n_tiles - 1) & 1]), ((n_tiles - 1) >> 1) & 1);
+    if (n_st > 0) {
+      mbar_wait(smem_u32(&pv_done[(n_st - 1) & 1]), ((n_st - 1) >> 1) & 1);
       tc_fence_after();
       invA = lA > 0.f ? __frcp_rn(lA) : 0.f;
       invB = lB > 0.f ? __frcp_rn(lB) : 0.f;
@@ -508,7 +530,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       uint32_t ov[32];
-      if (n_tiles > 0) {   // O = the hi lanes' part + the lo lanes' part
+      if (n_st > 0) {   // O = the hi lanes' part + the lo lanes' part
         uint32_t ol[32];
         tc_ld16x256<8>(tmem + lane_addr + kTcColO + 64 * h, ov);
         tc_ld16x256<8>(tmem + lane_addr + (16u << 16) + kTcColO + 64 * h, ol);

@@ -1,5 +1,5 @@
-"""Per-tile timeline of the tcgen05 kernel (DA_PATH_TC) from a -DDECATTN_TRACE build (development
-tool): tiles 16..23 of CTA 0, globaltimer ns relative to the K TMA issue of tile 16.
+"""Per-stage timeline of the tcgen05 kernel (DA_PATH_TC) from a -DDECATTN_TRACE build (development
+tool): 128-token stages 16..23 of CTAs 0 and 1, globaltimer ns relative to the K TMA issue of stage 16.
 
 DECATTN_LIB=paper_2604_00028_b200/lib/variants/libdecattn_trace.so python scripts/trace_tc.py"""
 import ctypes
@@ -26,14 +26,14 @@ def trace(b, hq, hkv, lk, policy="seq_aware", forced=0):
     torch.cuda.synchronize()
     buf = (ctypes.c_ulonglong * (64 * 64))()
     L.LIB.da_trace_fetch_tc(ctypes.addressof(buf), 64 * 64)
-    names = ["K_tma", "S_issue", "S_seen", "P_done", "PV_issue", "PVm2_seen"]
+    names = ["K_tma", "S_issue", "S_seen", "P_done", "PV_issue", "PVm2_seen", "S_start", "PV_start"]
     print(f"== B={b} HQ={hq} HKV={hkv} L={lk} s={plan.num_splits} path={plan.path}")
     for c in (0, 1):
         base = buf[c * 64 + 0]
         print(f" cta{c}")
         for k in range(8):
-            row = [int(buf[c * 64 + 8 * j + k]) - base if buf[c * 64 + 8 * j + k] else None for j in range(6)]
-            print("  tile", 16 + k, " ".join(f"{n}={v}" for n, v in zip(names, row)))
+            row = [int(buf[c * 64 + 8 * j + k]) - base if buf[c * 64 + 8 * j + k] else None for j in range(8)]
+            print("  stage", 16 + k, " ".join(f"{n}={v}" for n, v in zip(names, row)))
 
 
 if __name__ == "__main__":
