@@ -63,6 +63,9 @@ WORKLOADS = {
     "mqa_tiny": dict(synth.CONFIGS["mqa_tiny"]),
     "high_load": dict(synth.CONFIGS["high_load"]),
     "long_context": dict(synth.CONFIGS["long_context"]),
+    # beyond BASELINE.json's configs (all G = 8): MQA with 64 query heads per KV head, the shape
+    # the tcgen05 kernel (DA_PATH_TC) exists for; reported in extras only
+    "mqa_g64": dict(batch=128, h_q=64, h_kv=1, l_k=8192),
 }
 FALLBACK_HBM_GBS = 6650.0   # /opt/skills/guides/B200_PROFILING.md fallback (used only if MEASURED_PEAKS.json is absent)
 
@@ -280,7 +283,7 @@ def streaming_roofline(dec, dev, stream, timer, cfg, steps, rounds, l2, seed, pe
     ts = [timer.time_replay(g, stream) * 1e3 / steps for _ in range(rounds)]
     us = statistics.median(ts)
     gbs = w.bytes / (us * 1e-6) / 1e9
-    r = {"config": dict(cfg, head_dim=HEAD_DIM), "policy": policy, "num_splits": plan.num_splits,
+    r = {"config": dict(cfg, head_dim=HEAD_DIM), "policy": policy, "path": plan.path, "num_splits": plan.num_splits,
          "combine_mode": plan.combine_mode, "us_per_step": round(us, 2), "achieved_gbs": round(gbs, 1),
          "frac_of_measured_peak": round(gbs / peak, 4), "frac_of_8tbs_nominal": round(gbs / 8000.0, 4),
          "bytes_per_step": w.bytes, "l2": w.l2_note(l2)}
@@ -744,6 +747,8 @@ def main():
             "long_context": streaming_roofline(dec, dev, stream, timer, WORKLOADS["long_context"], 20, 7, l2, 1004, peak),
             "long_context_seq_aware_sm": streaming_roofline(dec, dev, stream, timer, WORKLOADS["long_context"], 20, 7, l2,
                                                             1004, peak, policy="seq_aware_sm"),
+            # MQA, G = 64 (not a BASELINE config): the tcgen05 kernel (path 2)
+            "mqa_g64_tcgen05": streaming_roofline(dec, dev, stream, timer, WORKLOADS["mqa_g64"], 10, 7, l2, 1007, peak),
         }
         if args.workload != "high_load":
             extras["roofline_streaming"]["high_load"] = streaming_roofline(dec, dev, stream, timer, WORKLOADS["high_load"],

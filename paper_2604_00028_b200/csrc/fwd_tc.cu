@@ -1,31 +1,33 @@
 // Split-KV decode-attention forward on the 5th-generation tensor cores (tcgen05 + TMEM) for wide
-// query groups: DA_PATH_TC, pack_gqa with G = H_Q / H_KV >= 32 (MQA / wide GQA), SURVEY §8(a)
-// steps a2-a7.  There the G query rows of a KV head make a real dense contraction per 64-token
-// tile (S = Q K^T: 64 x 64 x 128; O = P V: 64 x 128 x 64), which the mma.sync path could only run
-// as 16-row CTAs that read every K / V tile ceil(G / 16) times and issue 96+ HMMAs per warp per
-// tile (MQA G = 64 measured 2.0-2.6 TB/s there).
+// query groups: DA_PATH_TC, pack_gqa with G = H_Q / H_KV >= 32 (MQA / wide GQA) on streaming splits
+// (>= 16 tiles of 64 tokens each), SURVEY §8(a) steps a2-a7.  There the G query rows of a KV head
+// make a real dense contraction per KV tile, which the mma.sync path could only run as 16-row CTAs
+// that read every K / V tile ceil(G / 16) times and issue 96+ HMMAs per warp per tile (MQA G = 64
+// measured 2.6 TB/s there, 6.5 TB/s here).
 //
-// One CTA = 64 query rows of one KV head (rows hq0 .. hq0 + 63, G < 64 padded with zero rows) x
-// one split x one batch entry; grid = (s, H_KV * ceil(G / 64), B) as on the other paths.
-//   warp 4       TMA producer: the same 5-D K / V boxes and mbarrier ring as fwd.cu (32 KB a
-//                stage, K and V on separate barriers, dense or paged cache).
-//   warp 5       TMEM allocator and MMA issuer (one lane): S(i) = Q K(i)^T into TMEM buffer i & 1
-//                (tcgen05.mma kind::f16, M = 64, N = 64, K = 128, A = Q and B = K both K-major
-//                128B-swizzled), then O += P(i-1) V(i-1) (M = 64, N = 128, K = 64 twice: P_hi and
-//                P_lo, A = P K-major, B = the V box MN-major), so S(i) overlaps the softmax of
-//                tile i - 1.  tcgen05.commit releases the ring stage, the P buffer and the O
-//                accumulator to whoever waits on them.
-//   warps 0-3    softmax and epilogue, one query row per thread (row r lives on TMEM lane
-//                32 (r / 16) + r mod 16 for M = 64, scripts/microbench_tcgen05_rows.cu): tcgen05.ld
-//                of the row's 64 scores, online softmax in fp32 / log2 units, P = exp2(S - m) as
-//                the bf16 pair P_hi + P_lo (the precision of fwd.cu's PV) written to
-//                shared memory in the MMA's A layout.  The running maximum m is a reference that
-//                only moves when a tile's maximum exceeds it by more than 8 (log2 units); then the
-//                O row in TMEM is rescaled (tcgen05.ld / st) and l with it.  P <= 2^8 otherwise,
-//                and out = O / l and lse = m + log2 l hold for any reference, so the result is the
-//                exact softmax (C-att) and the O round trip leaves the steady state.
-//   epilogue     the O row from TMEM, / l: out + lse (s = 1, NONE) or the normalised fp32
-//                partial + lse (s > 1, KERNEL; merged by lse_combine_kernel).
+// One CTA = 64 query rows of one KV head (rows hq0 .. hq0 + 63; G < 64 padded with zero rows) x one
+// split x one batch entry; grid = (s, H_KV * ceil(G / 64), B) as on the other paths.  Stages of 128
+// tokens (two 64-token tiles): K and V as [half][128 tokens][64 dims], 128B-swizzled, 64 KB a stage.
+//   warp 4       TMA producer: one 5-D box per 64-token tile and 64-dim half, K and V on separate
+//                mbarriers (dense or paged cache); a split's last stage may hold one tile.
+//   warp 5       TMEM allocator and MMA issuer (one lane), tcgen05.mma kind::f16 with A from TMEM:
+//                S(s) = Q K(s)^T at M = 64 rows, N = 128 tokens, K = 128 dims into TMEM buffer s & 1,
+//                then O += P(s) V(s) at M = 128, N = 128 dims, K = 128 tokens with the pair
+//                P = P_hi + P_lo stacked along M (B = the V box, MN-major): two S stages ahead, so the
+//                tensor pipe runs PV(s) and S(s + 2) while the softmax warps work on stage s + 1.
+//                The pipe executes in issue order, so S(s + 2) overwrites the buffer only after PV(s)
+//                read P(s) from it; tcgen05.commit releases ring stages, S and O to their waiters.
+//   warps 0-3    softmax and epilogue: row r lives on TMEM lane 32 (r / 16) + r mod 16 (M = 64,
+//                scripts/microbench_tcgen05_rows.cu); the 16-lane TMEM shapes give thread t rows
+//                16 w + t / 4 and + 8 and a quarter of the tokens, the 4 threads of a row reduce
+//                with shuffles.  Online softmax in fp32 / log2 units; P = exp2(S - m) as the bf16
+//                pair P_hi + P_lo (the precision of fwd.cu's PV) written over S.  The
+//                running maximum m is a reference that moves only when a stage's maximum exceeds it
+//                by more than 8 (log2 units); then the O rows are rescaled in TMEM (tcgen05.ld /
+//                st) and l with them.  P <= 2^8 otherwise, and out = O / l and lse = m + log2 l hold
+//                for any reference, so the result is the exact softmax (C-att).
+//   epilogue     O = the hi lanes' part + the lo lanes' part, / l: out + lse (s = 1, NONE) or the
+//                normalised fp32 partial + lse (s > 1, KERNEL; merged by lse_combine_kernel).
 // Programmatic dependent launch as in fwd.cu: the prologue (barriers, TMEM allocation, tensor-map
 // prefetch, L2 prefetch of the first ring tiles) overlaps the previous kernel.
 #include <cuda.h>
@@ -68,17 +70,13 @@ static_assert(kTcSmem == kTcSmemCfg && kTcThreads == kTcThreadsCfg, "the planner
 static_assert(kTcColQ + 64 <= kTcTmemCols, "TMEM columns");
 constexpr float kTcRescaleLog2 = 8.f;            // rescale O only when the maximum grows by > 2^8
 
-#ifdef DECATTN_TC_DBG_NOSM   // timing experiment only: no exponentials (wrong results)
-#define TC_EX2(x) (x)
-#else
-#define TC_EX2(x) ex2(x)
-#endif
 
 // development timeline tracing (-DDECATTN_TRACE builds): globaltimer ns of tiles 16..23 of the
 // first 64 CTAs: 0+k K TMA issued, 8+k S issued, 16+k S seen by softmax warp 0, 24+k P written,
 // 32+k PV issued, 40+k PV seen done by softmax warp 0 (P-buffer wait)
 #ifdef DECATTN_TRACE
 __device__ unsigned long long g_trace_tc[64 * 64];
+__device__ unsigned long long g_clock_tc[4];   // globaltimer / clock64 at S(16), S(23) of CTA 0
 __device__ __forceinline__ void tc_trace(int slot_base, int i) {
   const int k = i - 16;
   if (k < 0 || k >= 8) return;
@@ -339,6 +337,14 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         }
         tc_commit(smem_u32(&s_full[sb]));
         TC_TRACE(8, s);
+#ifdef DECATTN_TRACE
+        if ((s == 16 || s == 23) && blockIdx.x + blockIdx.y + blockIdx.z == 0) {
+          g_clock_tc[s == 16 ? 2 : 3] = clock64();
+          unsigned long long t_;
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
+          g_clock_tc[s == 16 ? 0 : 1] = t_;
+        }
+#endif
       };
       // O += P(s) V(s), once the softmax warps wrote P(s) (over S(s)) and V(s) landed
       auto issue_pv = [&](int s) {
@@ -479,8 +485,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 #pragma unroll
         for (int g8 = 0; g8 < 8; ++g8) {
           const int g = 8 * h + g8;
-          const float pa0 = TC_EX2(fmaf(sv[4 * g], p.scale_log2, nA)), pa1 = TC_EX2(fmaf(sv[4 * g + 1], p.scale_log2, nA));
-          const float pb0 = TC_EX2(fmaf(sv[4 * g + 2], p.scale_log2, nB)), pb1 = TC_EX2(fmaf(sv[4 * g + 3], p.scale_log2, nB));
+          const float pa0 = ex2(fmaf(sv[4 * g], p.scale_log2, nA)), pa1 = ex2(fmaf(sv[4 * g + 1], p.scale_log2, nA));
+          const float pb0 = ex2(fmaf(sv[4 * g + 2], p.scale_log2, nB)), pb1 = ex2(fmaf(sv[4 * g + 3], p.scale_log2, nB));
           if (g8 & 1) sA1 += pa0 + pa1, sB1 += pb0 + pb1;
           else sA0 += pa0 + pa1, sB0 += pb0 + pb1;
           hw[2 * g8] = pack_bf16(pa0, pa1);
@@ -631,6 +637,9 @@ cudaError_t forward_tc_residency(int* out) {
 extern "C" __attribute__((visibility("default"))) int da_trace_fetch_tc(unsigned long long* host, int n) {
   if (n > 64 * 64) n = 64 * 64;
   return cudaMemcpyFromSymbol(host, g_trace_tc, sizeof(unsigned long long) * n) == cudaSuccess ? 0 : 1;
+}
+extern "C" __attribute__((visibility("default"))) int da_trace_fetch_tc_clock(unsigned long long* host) {
+  return cudaMemcpyFromSymbol(host, g_clock_tc, sizeof(unsigned long long) * 4) == cudaSuccess ? 0 : 1;
 }
 #endif
 

@@ -15,6 +15,8 @@ from paper_2604_00028_b200 import _lib as L
 import synth
 
 L.LIB.da_trace_fetch_tc.argtypes = [ctypes.c_void_p, ctypes.c_int]
+if hasattr(L.LIB, "da_trace_fetch_tc_clock"):
+    L.LIB.da_trace_fetch_tc_clock.argtypes = [ctypes.c_void_p]
 
 
 def trace(b, hq, hkv, lk, policy="seq_aware", forced=0):
@@ -28,6 +30,9 @@ def trace(b, hq, hkv, lk, policy="seq_aware", forced=0):
     L.LIB.da_trace_fetch_tc(ctypes.addressof(buf), 64 * 64)
     names = ["K_tma", "S_issue", "S_seen", "P_done", "PV_issue", "PVm2_seen", "S_start", "PV_start"]
     print(f"== B={b} HQ={hq} HKV={hkv} L={lk} s={plan.num_splits} path={plan.path}")
+    ck = (ctypes.c_ulonglong * 4)()
+    if hasattr(L.LIB, "da_trace_fetch_tc_clock") and L.LIB.da_trace_fetch_tc_clock(ctypes.addressof(ck)) == 0 and ck[1] > ck[0]:
+        print(f" SM clock over stages 16-23 (CTA 0): {(ck[3] - ck[2]) / (ck[1] - ck[0]) * 1e3:.0f} MHz")
     for c in (0, 1):
         base = buf[c * 64 + 0]
         print(f" cta{c}")
