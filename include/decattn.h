@@ -192,7 +192,9 @@ typedef struct da_plan {
                               KV cache that starts at token seq_offset
                               (DESIGN.md §6).  Not applied when cache_seqlens
                               is NULL (then every sequence has plan->l_k).  */
-  int32_t reserved_;       /* 0 (keeps the struct 8-byte aligned)            */
+  int32_t path_override;   /* (in, da_plan_set_path; 0 from da_plan_make) 0 =
+                              the planner's kernel choice, else the da_path
+                              forced: DA_PATH_MMA or DA_PATH_TC (A/B, tests) */
 } da_plan;
 
 /*
@@ -248,6 +250,16 @@ DA_API da_status da_plan_set_combine(da_plan* plan, int32_t combine_mode);
  * DA_ERR_INVALID_ARG.  Pure host code.
  */
 DA_API da_status da_plan_set_seq_offset(da_plan* plan, int32_t seq_offset);
+
+/*
+ * da_plan_set_path - force the kernel of a pack_gqa plan with G >= 2 and re-derive its launch
+ * fields: DA_PATH_MMA (mma.sync, 8 / 16 rows per CTA) or DA_PATH_TC (tcgen05, 64 rows per CTA; static
+ * split counts only, never a cluster combine: a CLUSTER plan becomes KERNEL); -1 restores the
+ * planner's choice.  The planner's own rule: DA_PATH_TC when G >= 32, every split
+ * holds >= 4 tiles of 64 tokens and the tcgen05 grid has >= U / 2 CTAs.  Errors: DA_ERR_INVALID_ARG
+ * (scalar plans, dynamic plans asked for DA_PATH_TC, unknown paths).  Pure host code.
+ */
+DA_API da_status da_plan_set_path(da_plan* plan, int32_t path);
 
 /*
  * da_forward - decode attention for one step (L_Q = 1), asynchronously on

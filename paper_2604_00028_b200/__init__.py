@@ -17,12 +17,12 @@ from ._lib import (DA_BF16, DA_COMBINE_CLUSTER, DA_COMBINE_KERNEL, DA_COMBINE_NO
                    DA_ERR_TIMEOUT, DA_PATH_MMA, DA_PATH_SCALAR, DA_PATH_TC, DA_POLICY_FIXED, DA_POLICY_GUARDED,
                    DA_POLICY_SEQ_AWARE, DecAttnError, da_abi_version, da_combine, da_combine_peers, da_forward,
                    da_forward_host, da_forward_host_bytes, da_forward_paged, da_forward_peer, da_peer_signal,
-                   da_plan, da_plan_make, da_plan_make_varlen, da_plan_set_combine, da_plan_set_seq_offset, da_query_residency,
+                   da_plan, da_plan_make, da_plan_make_varlen, da_plan_set_combine, da_plan_set_path, da_plan_set_seq_offset, da_query_residency,
                    da_status_string)
 from .api import (HostStaging, combine, decode_attention, forward, forward_host, forward_paged,  # noqa: F401
                   forward_peer, forward_peer_combine, make_plan, make_plan_varlen, workspace_for)
 
-__all__ = ["da_plan_make", "da_plan_make_varlen", "da_plan_set_combine", "da_plan_set_seq_offset", "da_forward", "da_forward_paged", "da_forward_host",
+__all__ = ["da_plan_make", "da_plan_make_varlen", "da_plan_set_combine", "da_plan_set_path", "da_plan_set_seq_offset", "da_forward", "da_forward_paged", "da_forward_host",
            "da_forward_host_bytes", "da_combine", "da_status_string", "da_abi_version", "make_plan", "forward",
            "forward_paged", "forward_host", "HostStaging", "combine", "decode_attention",
            "make_plan_varlen", "da_peer_signal", "da_combine_peers", "da_forward_peer", "forward_peer",

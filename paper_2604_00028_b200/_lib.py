@@ -46,7 +46,7 @@ class da_plan(ctypes.Structure):
         "total_mblocks", "num_splits", "nonempty_splits", "rule", "split_unit", "path",
         "rows_per_cta", "combine_mode", "grid_x", "grid_y", "grid_z", "block_threads",
         "cluster_x", "smem_bytes")] + [("workspace_bytes", ctypes.c_int64), ("seq_offset", ctypes.c_int32),
-                                      ("reserved_", ctypes.c_int32)]
+                                      ("path_override", ctypes.c_int32)]
 
     def as_dict(self) -> dict:
         return {name: getattr(self, name) for name, _ in self._fields_}
@@ -76,6 +76,8 @@ def _load() -> ctypes.CDLL:
     lib.da_plan_set_combine.restype = i32
     lib.da_plan_set_seq_offset.argtypes = [ctypes.POINTER(da_plan), i32]
     lib.da_plan_set_seq_offset.restype = i32
+    lib.da_plan_set_path.argtypes = [ctypes.POINTER(da_plan), i32]
+    lib.da_plan_set_path.restype = i32
     lib.da_forward.argtypes = [ctypes.POINTER(da_plan), vp, vp, vp, i32, vp, vp, f32, i32, vp, vp,
                                vp, i64, vp]
     lib.da_forward.restype = i32
@@ -111,7 +113,7 @@ def _load() -> ctypes.CDLL:
 
 LIB = _load()
 
-EXPORTED = ("da_plan_make", "da_plan_make_varlen", "da_plan_set_combine", "da_plan_set_seq_offset", "da_forward", "da_forward_paged",
+EXPORTED = ("da_plan_make", "da_plan_make_varlen", "da_plan_set_combine", "da_plan_set_seq_offset", "da_plan_set_path", "da_forward", "da_forward_paged",
             "da_forward_host_bytes", "da_forward_host", "da_combine", "da_peer_signal", "da_combine_peers",
             "da_forward_peer", "da_forward_peer_combine", "da_query_residency", "da_status_string",
             "da_abi_version")
@@ -150,6 +152,13 @@ def da_plan_make_varlen(batch, h_q, h_kv, l_cap, head_dim, pack_gqa, sm_margin, 
     if st != DA_OK:
         raise DecAttnError(st, "da_plan_make_varlen")
     return p
+
+
+def da_plan_set_path(plan: da_plan, path: int) -> da_plan:
+    st = LIB.da_plan_set_path(ctypes.byref(plan), int(path))
+    if st != DA_OK:
+        raise DecAttnError(st, "da_plan_set_path")
+    return plan
 
 
 def da_plan_set_seq_offset(plan: da_plan, seq_offset: int) -> da_plan:

@@ -32,8 +32,10 @@ def num_sms(device_index: int = 0) -> int:
 
 @functools.lru_cache(maxsize=4096)
 def _plan_cached(batch, h_q, h_kv, l_k, head_dim, pack_gqa, sm_margin, sms, policy, forced,
-                 combine_mode, seq_offset=0):
+                 combine_mode, seq_offset=0, path=None):
     p = L.da_plan_make(batch, h_q, h_kv, l_k, head_dim, pack_gqa, sm_margin, sms, policy, forced)
+    if path is not None:
+        L.da_plan_set_path(p, path)
     if combine_mode is not None and combine_mode != p.combine_mode:
         L.da_plan_set_combine(p, combine_mode)
     if seq_offset:
@@ -42,15 +44,17 @@ def _plan_cached(batch, h_q, h_kv, l_k, head_dim, pack_gqa, sm_margin, sms, poli
 
 
 def make_plan(batch, h_q, h_kv, l_k, head_dim=128, pack_gqa=True, sm_margin=0, num_sms_=None,
-              policy="seq_aware", forced_splits=0, combine_mode=None, seq_offset=0) -> L.da_plan:
+              policy="seq_aware", forced_splits=0, combine_mode=None, seq_offset=0, path=None) -> L.da_plan:
     """da_plan_make (+ da_plan_set_combine when combine_mode is given, + da_plan_set_seq_offset for
     the shard of a sequence-sharded cache that starts at token seq_offset: cache_seqlens are then
-    whole-sequence lengths).  The returned plan is shared through a cache: copy it before editing."""
+    whole-sequence lengths; + da_plan_set_path when path is given: DA_PATH_MMA / DA_PATH_TC).  The
+    returned plan is shared through a cache: copy it before editing."""
     if isinstance(policy, str):
         policy = L.POLICIES[policy]
     sms = num_sms_ if num_sms_ is not None else num_sms(torch.cuda.current_device())
     return _plan_cached(int(batch), int(h_q), int(h_kv), int(l_k), int(head_dim), int(bool(pack_gqa)),
-                        int(sm_margin), int(sms), int(policy), int(forced_splits), combine_mode, int(seq_offset))
+                        int(sm_margin), int(sms), int(policy), int(forced_splits), combine_mode, int(seq_offset),
+                        None if path is None else int(path))
 
 
 def make_plan_varlen(batch, h_q, h_kv, l_cap, host_seqlens, head_dim=128, pack_gqa=True, sm_margin=0,

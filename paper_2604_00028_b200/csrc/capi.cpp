@@ -125,7 +125,9 @@ da_status check_plan(const da_plan* plan) {
   if (plan->num_splits < 1 || plan->num_splits > kMaxForcedSplits) return DA_ERR_INVALID_ARG;
   if (plan->pack_gqa != 0 && plan->pack_gqa != 1) return DA_ERR_INVALID_ARG;
   if (!combine_mode_valid(plan->combine_mode, plan->num_splits)) return DA_ERR_INVALID_ARG;
-  if (plan->seq_offset < 0 || plan->reserved_ != 0) return DA_ERR_INVALID_ARG;
+  if (plan->seq_offset < 0) return DA_ERR_INVALID_ARG;
+  if (plan->path_override != 0 && plan->path_override != DA_PATH_MMA && plan->path_override != DA_PATH_TC)
+    return DA_ERR_INVALID_ARG;
   da_plan chk = *plan;
   derive_launch(&chk);
   if (chk.path != plan->path || chk.rows_per_cta != plan->rows_per_cta ||

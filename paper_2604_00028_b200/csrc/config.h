@@ -99,7 +99,7 @@ constexpr int kBalMinTiles = DECATTN_BAL_MIN_TILES, kBalTailDiv = DECATTN_BAL_TA
 #define DECATTN_TC_MIN_G 32
 #endif
 #ifndef DECATTN_TC_MIN_TILES
-#define DECATTN_TC_MIN_TILES 16   // 64-token tiles per split at the plan's length: streaming splits only
+#define DECATTN_TC_MIN_TILES 4    // 64-token tiles per split at the plan's length (and >= U / 2 CTAs)
 #endif
 constexpr int kTcMinG = DECATTN_TC_MIN_G, kTcMinTiles = DECATTN_TC_MIN_TILES;
 constexpr int kTcRows = 64;

@@ -147,13 +147,20 @@ static int64_t launch_rows(const da_plan& p) {
   return rows;
 }
 
-// pack_gqa plans with G >= kTcMinG, a static split count and streaming splits (>= kTcMinTiles tiles
-// each at the plan's length) run the tcgen05 kernel (fwd_tc.cu): 64 query rows per CTA, no cluster
-// combine.  Short splits stay on the mma.sync kernel, whose few-tile CTAs spread over 3-7 warps and
-// merge through clusters (MQA G = 64, L_K = 512 3.4 us there, 7.4 us on tcgen05).
+// pack_gqa plans with G >= kTcMinG and a static split count run the tcgen05 kernel (fwd_tc.cu: 64
+// query rows per CTA, no cluster combine) when every split holds >= kTcMinTiles tiles and its grid
+// has >= U / 2 CTAs; otherwise the mma.sync kernel (8 / 16-row CTAs: 4x the CTAs at G = 64, few-tile
+// CTAs spread over 3-7 warps and merged through clusters), which wins on short or few splits
+// (profiles/r02ze_mid.log).  da_plan_set_path overrides the choice.
 bool tc_path(const da_plan& p) {
-  return p.pack_gqa != 0 && p.h_q / p.h_kv >= kTcMinG && !is_dynamic(p) &&
-         ceil_div(static_cast<int64_t>(p.l_k), kSplitUnit) >= static_cast<int64_t>(kTcMinTiles) * p.num_splits;
+  const int64_t G = p.h_q / p.h_kv;
+  if (p.pack_gqa == 0 || G < 2 || is_dynamic(p)) return false;
+  if (p.path_override == DA_PATH_TC) return true;
+  if (p.path_override == DA_PATH_MMA) return false;
+  const int64_t ctas = static_cast<int64_t>(p.batch) * p.h_kv * ceil_div(G, kTcRows) * p.num_splits;
+  return G >= kTcMinG &&
+         ceil_div(static_cast<int64_t>(p.l_k), kSplitUnit) >= static_cast<int64_t>(kTcMinTiles) * p.num_splits &&
+         2 * ctas >= p.usable_sms;
 }
 
 // Launch geometry for a plan whose decision fields are set.  Shared by
@@ -303,6 +310,20 @@ extern "C" da_status da_plan_make_varlen(int32_t batch, int32_t h_q, int32_t h_k
 extern "C" da_status da_plan_set_seq_offset(da_plan* plan, int32_t seq_offset) {
   if (plan == nullptr || seq_offset < 0) return DA_ERR_INVALID_ARG;
   plan->seq_offset = seq_offset;
+  return DA_OK;
+}
+
+extern "C" da_status da_plan_set_path(da_plan* plan, int32_t path) {
+  if (plan == nullptr) return DA_ERR_INVALID_ARG;
+  const int32_t G = plan->h_kv > 0 ? plan->h_q / plan->h_kv : 0;
+  if (plan->pack_gqa == 0 || G < 2) return DA_ERR_INVALID_ARG;          // the scalar kernel only
+  if (path != -1 && path != DA_PATH_MMA && path != DA_PATH_TC) return DA_ERR_INVALID_ARG;
+  if (path == DA_PATH_TC && is_dynamic(*plan)) return DA_ERR_INVALID_ARG;
+  plan->path_override = path == -1 ? 0 : path;
+  if (tc_path(*plan) && plan->combine_mode == DA_COMBINE_CLUSTER) plan->combine_mode = DA_COMBINE_KERNEL;
+  if (!tc_path(*plan) && plan->combine_mode == DA_COMBINE_KERNEL && plan->num_splits <= kMaxClusterSplits)
+    plan->combine_mode = default_combine_mode(*plan);                 // the mma.sync kernel's own choice
+  derive_launch(plan);
   return DA_OK;
 }
 

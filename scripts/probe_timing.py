@@ -56,7 +56,7 @@ def bench(b, hq, hkv, lk, policy="seq_aware", forced=0, combine=None, steps=200,
     us = ts[len(ts) // 2]
     gbs = bytes_step(b, hq, hkv, lk) / (us * 1e-6) / 1e9
     print(f"B={b:4d} HQ={hq:3d} HKV={hkv:2d} L={lk:7d} pack={int(pack)} {policy:9s} s={plan.num_splits:3d} "
-          f"comb={plan.combine_mode} nbuf={nbuf:3d}: {us:9.2f} us/step  {gbs:8.1f} GB/s", flush=True)
+          f"comb={plan.combine_mode} path={plan.path} nbuf={nbuf:3d}: {us:9.2f} us/step  {gbs:8.1f} GB/s", flush=True)
     return us
 
 

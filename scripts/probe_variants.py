@@ -58,6 +58,15 @@ if __name__ == "__main__":
             bench(1, 32, 1, 512, pol, steps=200, reps=7)
             bench(4, 64, 1, 2048, pol, steps=200, reps=7)
         sys.exit(0)
+    if len(sys.argv) > 2 and sys.argv[1] == "one" and sys.argv[2] == "mqa_mid":
+        # MQA G = 64 mid-size shapes: where the tcgen05 / mma.sync boundary (kTcMinTiles) should sit
+        sys.path.insert(0, os.path.join(ROOT, "scripts"))
+        from probe_timing import bench
+        for shp in ((4, 64, 1, 8192), (8, 64, 1, 4096), (2, 64, 1, 32768), (16, 64, 1, 2048), (1, 64, 1, 16384),
+                    (1, 64, 1, 4096), (1, 64, 1, 1024), (32, 64, 1, 1024), (64, 64, 1, 2048)):
+            for pol in ("guarded", "seq_aware_sm"):
+                bench(*shp, pol, steps=50, reps=5)
+        sys.exit(0)
     if len(sys.argv) > 1 and sys.argv[1] == "one":
         sys.path.insert(0, os.path.join(ROOT, "scripts"))
         from probe_timing import bench

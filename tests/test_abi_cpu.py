@@ -45,10 +45,17 @@ def test_plan_struct_layout(L):
     assert names == [n for n, _ in L.da_plan._fields_]
 
 
+def _tc(b, hq, hkv, lk, pack, s, U, dynamic=False):
+    # the planner's kernel choice: tcgen05 for G >= 32 when every split holds >= 4
+    # tiles and the 64-row grid has >= U / 2 CTAs (static plans)
+    G = hq // hkv
+    return bool(pack) and G >= 32 and not dynamic and -(-lk // 64) >= 4 * s and 2 * b * hkv * -(-G // 64) * s >= U
+
+
 def _expected_launch(b, hq, hkv, lk, pack, s, U, dynamic=False):
     G = hq // hkv
     mma = bool(pack) and G >= 2
-    if mma and G >= 32 and not dynamic and -(-lk // 64) >= 16 * s:   # DA_PATH_TC (fwd_tc.cu): 64 rows per CTA
+    if _tc(b, hq, hkv, lk, pack, s, U, dynamic):   # DA_PATH_TC (fwd_tc.cu): 64 rows per CTA
         return 2, 64, (s, hkv * -(-G // 64), b)
     rows = OP.launch_rows(b, G, hkv, lk, s, U) if mma else 1
     gy = hkv * -(-G // rows) if mma else hq
@@ -78,7 +85,7 @@ def test_cluster_fit_table_single_source():
 def _expected_combine(b, hq, hkv, lk, pack, sms, s, U):
     if s == 1:
         return 0
-    if s > 16 or (pack and hq // hkv >= 32 and -(-lk // 64) >= 16 * s):   # > 16 splits or the tcgen05 path
+    if s > 16 or _tc(b, hq, hkv, lk, pack, s, U):   # > 16 splits or the tcgen05 path: no cluster combine
         return 2
     _, _, (_, gy, gz) = _expected_launch(b, hq, hkv, lk, pack, s, U)
     return 1 if gy * gz <= _FIT[s] * sms // 148 else 2
@@ -199,7 +206,7 @@ def test_plan_invalid_knobs(L):
 
 def test_set_seq_offset(L):
     p = L.da_plan_make(2, 16, 2, 4096, 128, 1, 0, 148, "seq_aware", 0)
-    assert p.seq_offset == 0 and p.reserved_ == 0
+    assert p.seq_offset == 0 and p.path_override == 0
     q = L.da_plan.from_buffer_copy(p)
     L.da_plan_set_seq_offset(q, 65536)
     assert q.seq_offset == 65536
@@ -211,8 +218,38 @@ def test_set_seq_offset(L):
     bad.seq_offset = -5                              # hand-edited: rejected by the forwards' checks
     assert _fwd(L, bad) == L.DA_ERR_INVALID_ARG
     bad = L.da_plan.from_buffer_copy(p)
-    bad.reserved_ = 1
+    bad.path_override = 5
     assert _fwd(L, bad) == L.DA_ERR_INVALID_ARG
+
+
+def test_set_path(L):
+    # MQA G = 64, B = 4, L = 8192 under guarded: s = 32, 4 tiles per split, 128 tcgen05 CTAs -> TC
+    p = L.da_plan_make(4, 64, 1, 8192, 128, 1, 0, 148, "guarded", 0)
+    assert (p.num_splits, p.path, p.rows_per_cta, p.grid_y, p.combine_mode) == (32, L.DA_PATH_TC, 64, 1, 2)
+    assert (p.block_threads, p.smem_bytes) == (192, 3 * 65536 + 1024)
+    q = L.da_plan.from_buffer_copy(p)
+    L.da_plan_set_path(q, L.DA_PATH_MMA)                      # the mma.sync kernel: 16-row CTAs
+    assert (q.path, q.rows_per_cta, q.grid_y, q.path_override) == (L.DA_PATH_MMA, 16, 4, L.DA_PATH_MMA)
+    L.da_plan_set_path(q, -1)                                 # back to the planner's choice
+    assert q.as_dict() == p.as_dict()
+    # a short TP-8 slice forced onto tcgen05 (G = 8 rows of the 64); its cluster combine becomes KERNEL
+    t = L.da_plan_make(1, 8, 1, 512, 128, 1, 0, 148, "seq_aware", 0)
+    assert (t.path, t.combine_mode) == (L.DA_PATH_MMA, L.DA_COMBINE_CLUSTER)
+    L.da_plan_set_path(t, L.DA_PATH_TC)
+    assert (t.path, t.rows_per_cta, t.combine_mode, t.cluster_x) == (L.DA_PATH_TC, 64, L.DA_COMBINE_KERNEL, 1)
+    L.da_plan_set_path(t, L.DA_PATH_MMA)
+    assert (t.path, t.combine_mode) == (L.DA_PATH_MMA, L.DA_COMBINE_CLUSTER)
+    with pytest.raises(L.DecAttnError):
+        L.da_plan_set_combine(L.da_plan_set_path(t, L.DA_PATH_TC), L.DA_COMBINE_CLUSTER)
+    for bad in (L.da_plan_make(1, 8, 8, 512, 128, 1, 0, 148, "guarded", 0),    # G = 1: scalar only
+                L.da_plan_make(1, 64, 1, 512, 128, 0, 0, 148, "guarded", 0)):   # pack_gqa = 0
+        with pytest.raises(L.DecAttnError):
+            L.da_plan_set_path(bad, L.DA_PATH_TC)
+    d = L.da_plan_make(4, 64, 1, 3000, 128, 1, 0, 148, "dynamic", 0)
+    with pytest.raises(L.DecAttnError):
+        L.da_plan_set_path(d, L.DA_PATH_TC)                   # the dynamic schedule is mma.sync only
+    with pytest.raises(L.DecAttnError):
+        L.da_plan_set_path(p, 7)
 
 
 def test_set_combine_rules(L):

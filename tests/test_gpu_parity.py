@@ -20,7 +20,7 @@ def _dec():
 
 def run_and_check(batch, h_q, h_kv, l_k, *, policy="seq_aware", forced=0, pack_gqa=True,
                   variant="normal", l_cap=None, seed=1000, combine_mode=None, out_f32=False,
-                  check_partials=False, nan_tail=False):
+                  check_partials=False, nan_tail=False, path=None):
     dec = _dec()
     inp = synth.make_inputs(batch, h_q, h_kv, l_k, l_cap=l_cap, seed=seed, variant=variant,
                             device="cuda")
@@ -31,7 +31,7 @@ def run_and_check(batch, h_q, h_kv, l_k, *, policy="seq_aware", forced=0, pack_g
             k[b, n:] = float("nan")
             v[b, n:] = float("nan")
     plan = dec.make_plan(batch, h_q, h_kv, l_k, pack_gqa=pack_gqa, policy=policy,
-                         forced_splits=forced, combine_mode=combine_mode)
+                         forced_splits=forced, combine_mode=combine_mode, path=path)
     sms = torch.cuda.get_device_properties(0).multi_processor_count
     # the planner's split count is the oracle's, bit for bit
     s_ref, rule_ref = OP.num_splits(batch, h_q, h_kv, l_k, sms, 0, policy, forced)
@@ -145,7 +145,7 @@ def test_many_query_rows_per_kv_head(batch, h_q, h_kv, l_k, policy):
     plan, _, _ = run_and_check(batch, h_q, h_kv, l_k, policy=policy, variant="ragged", seed=1500)
     assert plan.num_m_blocks == 2
     if plan.path == 2:        # G >= 32 with >= 16 tiles per split: tcgen05, 64 rows, two CTAs per KV head
-        assert policy != "dynamic" and -(-l_k // 64) >= 16 * plan.num_splits
+        assert policy != "dynamic" and -(-l_k // 64) >= 4 * plan.num_splits
         assert (plan.rows_per_cta, plan.grid_y) == (64, 2 * h_kv)
     else:                     # short splits and the dynamic schedule: the mma.sync kernel
         assert plan.rows_per_cta == OP.launch_rows(batch, h_q // h_kv, h_kv, l_k, plan.num_splits, plan.usable_sms)
@@ -349,7 +349,7 @@ def test_seq_aware_sm_fit(batch, h_q, h_kv, l_k, variant):
 
 # ---- paged KV cache (da_forward_paged) --------------------------------------
 def run_paged(batch, h_q, h_kv, l_k, page_size, *, policy="seq_aware", forced=0, pack=True, seed=90,
-              variant="ragged", combine_mode=None):
+              variant="ragged", combine_mode=None, path=None):
     dec = _dec()
     inp = synth.make_inputs(batch, h_q, h_kv, l_k, seed=seed, variant=variant, device="cuda")
     q, k, v, seq = inp["q"], inp["k"], inp["v"], inp["seqlens"]
@@ -371,7 +371,7 @@ def run_paged(batch, h_q, h_kv, l_k, page_size, *, policy="seq_aware", forced=0,
             vp[pg, : hi - lo] = v[b, lo:hi]
     table = table.to("cuda")
     plan = dec.make_plan(batch, h_q, h_kv, l_k, pack_gqa=pack, policy=policy, forced_splits=forced,
-                         combine_mode=combine_mode)
+                         combine_mode=combine_mode, path=path)
     out, lse = dec.forward_paged(plan, q, kp, vp, table, seq)
     torch.cuda.synchronize()
     ref_o, ref_l = OA.decode_attention(*(synth.to_f64(t) for t in (q, k, v, seq)))
@@ -568,11 +568,13 @@ def test_seq_offset_shard(batch, h_q, h_kv, l_local, t0, policy, forced, combine
     (2, 64, 1, 4500, "fixed", 4, "peaked"),          # workspace partials
     (8, 64, 2, 1100, "fixed", 1, "normal"),          # a partial last tile (1100 = 17 x 64 + 12)
     (1, 64, 1, 131072, "seq_aware", 0, "normal"),    # the paper's long context as MQA-64 (s = 109)
+    (2, 8, 1, 3000, "fixed", 2, "ragged"),           # G = 8 forced onto tcgen05: 56 padding rows
+    (1, 16, 2, 700, "fixed", 3, "peaked"),           # short splits (4 tiles) on tcgen05
 ])
 def test_tc_path_matches_oracle(batch, h_q, h_kv, l_k, policy, forced, variant):
     dec = _dec()
     plan, _, _ = run_and_check(batch, h_q, h_kv, l_k, policy=policy, forced=forced, variant=variant, seed=1700,
-                               check_partials=forced > 1)
+                               check_partials=forced > 1, path=dec.DA_PATH_TC)
     assert (plan.path, plan.rows_per_cta, plan.cluster_x) == (dec.DA_PATH_TC, 64, 1)
     assert plan.combine_mode == (dec.DA_COMBINE_NONE if plan.num_splits == 1 else dec.DA_COMBINE_KERNEL)
 
@@ -585,11 +587,14 @@ def test_tc_path_edges(pack):
                dict(batch=2, l_k=1100, out_f32=True, forced=1),
                dict(batch=2, l_k=3000, out_f32=True, forced=2, check_partials=True)):
         b_ = kw.pop("batch")
-        plan, _, _ = run_and_check(b_, 64, 1, policy="fixed", seed=1701, **kw)
+        plan, _, _ = run_and_check(b_, 64, 1, policy="fixed", seed=1701, path=dec.DA_PATH_TC, **kw)
         assert plan.path == dec.DA_PATH_TC
-    # short splits stay on the mma.sync kernel (and its cluster combine)
+    # the planner's choice: short / few splits stay on the mma.sync kernel (and its cluster combine),
+    # many CTAs with >= 4 tiles each take tcgen05
     plan, _, _ = run_and_check(1, 64, 1, 512, policy="seq_aware_sm", seed=1704)
     assert plan.path == dec.DA_PATH_MMA
+    plan, _, _ = run_and_check(80, 64, 1, 300, policy="guarded", seed=1705, variant="ragged")
+    assert (plan.num_splits, plan.path) == (1, dec.DA_PATH_TC)
 
 
 def test_tc_path_rescales_when_the_maximum_grows():
@@ -605,7 +610,7 @@ def test_tc_path_rescales_when_the_maximum_grows():
          + 0.3 * torch.randn(batch, l_k, h_kv, 128, generator=g)).to(torch.bfloat16)
     v = torch.randn(batch, l_k, h_kv, 128, generator=g).to(torch.bfloat16)
     seq = torch.tensor([l_k, 700], dtype=torch.int32)
-    plan = dec.make_plan(batch, h_q, h_kv, l_k, policy="fixed", forced_splits=1)   # one CTA: 16 tiles
+    plan = dec.make_plan(batch, h_q, h_kv, l_k, policy="fixed", forced_splits=1, path=2)   # one CTA: 16 tiles
     assert plan.path == dec.DA_PATH_TC and plan.num_splits == 1
     out, lse = dec.forward(plan, q.cuda(), k.cuda(), v.cuda(), seq.cuda())
     torch.cuda.synchronize()
@@ -617,14 +622,15 @@ def test_tc_path_rescales_when_the_maximum_grows():
 
 def test_tc_path_paged_offset_and_graph():
     dec = _dec()
-    assert run_paged(3, 64, 1, 2500, 128, policy="fixed", forced=1, seed=1720).path == dec.DA_PATH_TC
-    assert run_paged(2, 128, 2, 2600, 256, policy="fixed", forced=2, seed=1721).path == dec.DA_PATH_TC
+    assert run_paged(3, 64, 1, 2500, 128, policy="fixed", forced=1, seed=1720, path=2).path == dec.DA_PATH_TC
+    assert run_paged(2, 128, 2, 2600, 256, policy="fixed", forced=2, seed=1721, path=2).path == dec.DA_PATH_TC
+    assert run_paged(3, 64, 1, 2500, 64, policy="fixed", forced=1, seed=1723, path=2).path == dec.DA_PATH_TC
     # a sequence shard (seq_offset) and CUDA-graph replays of the tcgen05 kernel
     batch, h_q, h_kv, l_local, t0 = 3, 64, 1, 2000, 777
     from paper_2604_00028_b200.dist import local_seqlens
     inp = synth.make_inputs(batch, h_q, h_kv, l_local, seed=1722, device="cuda")
     glob = torch.tensor([100, t0 + l_local + 5, t0 + 900], dtype=torch.int32, device="cuda")
-    plan = dec.make_plan(batch, h_q, h_kv, l_local, policy="fixed", forced_splits=2, seq_offset=t0)
+    plan = dec.make_plan(batch, h_q, h_kv, l_local, policy="fixed", forced_splits=2, seq_offset=t0, path=2)
     assert plan.path == dec.DA_PATH_TC
     ws = dec.workspace_for(plan, inp["q"].device)
     out = torch.empty((batch, h_q, 128), dtype=torch.bfloat16, device="cuda")

@@ -103,6 +103,28 @@ def test_forward_peer_every_combine_mode(one_rank_group, batch, h_q, h_kv, l_k, 
         assert int(flags.item()) == 4
 
 
+@pytest.mark.parametrize("batch,h_q,h_kv,l_k,policy,mode", [
+    (80, 64, 1, 300, "guarded", 0),          # tcgen05, s = 1: the forward does not publish -> forward + signal
+    (4, 64, 1, 8192, "guarded", 2),          # tcgen05, s = 32: the combine kernel publishes / exchanges
+])
+def test_peer_exchange_tcgen05_plans(one_rank_group, batch, h_q, h_kv, l_k, policy, mode):
+    from paper_2604_00028_b200.dist import PeerSeqShardedDecode
+    inp = synth.make_inputs(batch, h_q, h_kv, l_k, seed=1650, device="cuda", variant="ragged")
+    sd = PeerSeqShardedDecode(batch, h_q, h_kv, l_k, device="cuda", policy=policy)
+    assert (sd.plan.path, sd.plan.combine_mode) == (2, mode)
+    assert sd.one_kernel == (mode == 2) and sd.fused == (mode == 2)
+    ref_o, ref_l = OA.decode_attention(*(synth.to_f64(inp[n]) for n in ("q", "k", "v", "seqlens")))
+    out = torch.empty((batch, h_q, 128), dtype=torch.float32, device="cuda")
+    lse = torch.empty((batch, h_q), dtype=torch.float32, device="cuda")
+    for e in range(1, 4):
+        out.zero_()
+        sd.step(inp["q"], inp["k"], inp["v"], inp["seqlens"], out, lse)
+        torch.cuda.synchronize()
+        assert_out_close(synth.to_f64(out), ref_o)
+        assert_lse_close(synth.to_f64(lse), ref_l)
+        assert int(sd.epoch.item()) == e
+
+
 # ---- bounded waits: a peer that never arrives fails the step instead of hanging the GPU ----------
 def _fake_two_rank_buffers(batch, h_q, world=2):
     """Exchange buffers for `world` ranks on this GPU, where only rank 0 (this process) runs: the
