@@ -167,11 +167,11 @@ typedef struct da_plan {
   int32_t path;            /* da_path                                          */
   int32_t rows_per_cta;    /* query rows one CTA computes: SCALAR 1; MMA 8,
                               or 16 when G > 8 and (n_u > 64 or the 8-row
-                              grid B H_KV ceil(G/8) s exceeds U)           */
+                              grid B H_KV ceil(G/8) s exceeds U); TC 64   */
   int32_t combine_mode;    /* da_combine_mode                                  */
   int32_t grid_x;          /* = num_splits; DA_POLICY_DYNAMIC: the head groups
                               (grid_y's static value)                        */
-  int32_t grid_y;          /* MMA: h_kv * ceil(G / rows_per_cta); SCALAR: h_q;
+  int32_t grid_y;          /* MMA / TC: h_kv * ceil(G / rows_per_cta); SCALAR: h_q;
                               DA_POLICY_DYNAMIC: split slots,
                               min(B * cap, ceil(U / T_b) + B)                */
   int32_t grid_z;          /* = batch; DA_POLICY_DYNAMIC: 1                    */
