@@ -105,6 +105,9 @@ constexpr int kTcMinG = DECATTN_TC_MIN_G, kTcMinTiles = DECATTN_TC_MIN_TILES;
 constexpr int kTcRows = 64;
 constexpr int kTcThreadsCfg = 6 * 32;
 constexpr int kTcSmemCfg = DECATTN_TC_STAGES * 2 * kStageBytes + 1024;   // 128-token stages; Q, S, P, O in TMEM
+#ifndef DECATTN_L2_PROMOTION
+#define DECATTN_L2_PROMOTION 3    // CU_TENSOR_MAP_L2_PROMOTION_L2_256B for the K / V tensor maps
+#endif
 #ifndef DECATTN_PREFETCH_LONG
 #define DECATTN_PREFETCH_LONG 1   // the pre-wait L2 prefetch of the first ring tiles also for long splits
 #endif

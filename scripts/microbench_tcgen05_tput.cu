@@ -147,6 +147,76 @@ __global__ void pattern(long long* out) {
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tm));
 }
 
+// the 128-token stage of fwd_tc.cu: S (M = 64, N = 128, K-major K halves 16 KB apart) + PV (M = 128,
+// N = 128, MN-major V with the 64-dim halves 16 KB apart, 8 steps of 16 tokens)
+template <int LBO_V>
+__global__ void pattern128(long long* out) {
+  extern __shared__ __align__(1024) uint8_t sm_raw[];
+  uint8_t* sm = (uint8_t*)(((uintptr_t)sm_raw + 1023) & ~(uintptr_t)1023);
+  __shared__ __align__(8) uint64_t bar, bar2;
+  __shared__ uint32_t tbase;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  for (int i = tid; i < 96 * 1024 / 16; i += blockDim.x) reinterpret_cast<uint4*>(sm)[i] = make_uint4(0, 0, 0, 0);
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar)));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar2)));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tbase)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tm = tbase;
+  if (tid == 0) {
+    constexpr uint32_t id_s = idesc(64, 128, 0, 0), id_o = idesc(128, 128, 0, 1);
+    const uint32_t sK = smem_u32(sm), sV = sK + 32768;
+    long long tS = 0, tP = 0;
+    const long long t0 = clock64();
+    for (int t = 0; t < 32; ++t) {
+      const long long a0 = clock64();
+      for (int kk = 0; kk < 8; ++kk)
+        mma_ts(tm + (t & 1) * 128, tm + 384 + kk * 8, sdesc(sK + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024), id_s);
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(&bar2)) : "memory");
+      const long long a1 = clock64();
+      for (int kk = 0; kk < 8; ++kk)
+        mma_ts(tm + 256, tm + (t & 1) * 128 + kk * 8, sdesc(sV + kk * 2048, LBO_V, 1024), id_o);
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(&bar2)) : "memory");
+      const long long a2 = clock64();
+      tS += a1 - a0;
+      tP += a2 - a1;
+    }
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(&bar)) : "memory");
+    asm volatile("{\n\t.reg .pred p;\n\tW: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n\t@!p bra W;\n\t}" ::"r"(smem_u32(&bar)) : "memory");
+    out[0] = clock64() - t0;
+    out[1] = tS;
+    out[2] = tP;
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tm));
+}
+
+template <int LBO_V>
+void run_pattern128() {
+  long long* d; cudaMalloc(&d, 24);
+  cudaFuncSetAttribute(pattern128<LBO_V>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+  long long best[3] = {1ll << 60, 0, 0};
+  for (int it = 0; it < 10; ++it) {
+    pattern128<LBO_V><<<1, 128, 100 * 1024>>>(d);
+    cudaDeviceSynchronize();
+    long long c[3]; cudaMemcpy(c, d, 24, cudaMemcpyDeviceToHost);
+    if (c[0] < best[0]) best[0] = c[0], best[1] = c[1], best[2] = c[2];
+  }
+  printf("128-token stage pattern (S 8 x M64 N128, PV 8 x M128 N128, V LBO %d): %.0f cycles per stage "
+         "(issue time S %.0f, PV %.0f; floor 8 x 65 + 8 x 66 = 1048)\n",
+         LBO_V, best[0] / 32.0, best[1] / 32.0, best[2] / 32.0);
+  cudaFree(d);
+}
+
 template <bool FENCE>
 void run_pattern() {
   long long* d; cudaMalloc(&d, 8);
@@ -194,6 +264,8 @@ int main(int argc, char** argv) {
   run<128, 128, true, true>("O = P V (B MN-major)");
   run<128, 256, true, false>("reference M128 N256 (B K-major)");
   run<64, 256, true, false>("reference M64 N256 (B K-major)");
+  run_pattern128<8192>();
+  run_pattern128<16384>();
   run_pattern<false>();
   run_pattern<true>();
   run<64, 64, true, false, 8>("S, commit after every 8");
