@@ -90,10 +90,13 @@ DA_HD constexpr int helpers_for(int combine_mode) { return combine_mode == 1 ? D
 #endif
 constexpr int kBalMinTiles = DECATTN_BAL_MIN_TILES, kBalTailDiv = DECATTN_BAL_TAIL_DIV, kBalChunk = DECATTN_BAL_CHUNK;
 // tcgen05 path (fwd_tc.cu, DA_PATH_TC): pack_gqa with G >= kTcMinG; 64 query rows per CTA (the
-// MMA's M), 4 softmax warps + a TMA producer warp + an MMA warp, kTcStages ring stages (Q, S, P
-// and O live in TMEM).  Never a cluster combine.
-#ifndef DECATTN_TC_STAGES
-#define DECATTN_TC_STAGES 3
+// MMA's M), 8 softmax warps + a TMA producer warp + an MMA warp, separate K and V rings of
+// 128-token slots (Q, S, P and O live in TMEM).  Never a cluster combine.
+#ifndef DECATTN_TC_KSLOTS
+#define DECATTN_TC_KSLOTS 2       // tcgen05 path: K ring slots of 128 tokens (32 KB)
+#endif
+#ifndef DECATTN_TC_VSLOTS
+#define DECATTN_TC_VSLOTS 5       // tcgen05 path: V ring slots of 128 tokens (32 KB)
 #endif
 #ifndef DECATTN_TC_MIN_G
 #define DECATTN_TC_MIN_G 32
@@ -103,8 +106,14 @@ constexpr int kBalMinTiles = DECATTN_BAL_MIN_TILES, kBalTailDiv = DECATTN_BAL_TA
 #endif
 constexpr int kTcMinG = DECATTN_TC_MIN_G, kTcMinTiles = DECATTN_TC_MIN_TILES;
 constexpr int kTcRows = 64;
-constexpr int kTcThreadsCfg = 6 * 32;
-constexpr int kTcSmemCfg = DECATTN_TC_STAGES * 2 * kStageBytes + 1024;   // 128-token stages; Q, S, P, O in TMEM
+#ifndef DECATTN_TC_QPREFETCH
+#define DECATTN_TC_QPREFETCH 1    // L2 prefetch of the CTA's Q rows at kernel entry
+#endif
+#ifndef DECATTN_TC_SMX_WARPS
+#define DECATTN_TC_SMX_WARPS 8    // softmax warps: 4 (one per TMEM lane quadrant) or 8 (two, token halves)
+#endif
+constexpr int kTcThreadsCfg = (DECATTN_TC_SMX_WARPS + 2) * 32;
+constexpr int kTcSmemCfg = (DECATTN_TC_KSLOTS + DECATTN_TC_VSLOTS) * kStageBytes + 1024;   // 128-token stages; Q, S, P, O in TMEM
 #ifndef DECATTN_L2_PROMOTION
 #define DECATTN_L2_PROMOTION 3    // CU_TENSOR_MAP_L2_PROMOTION_L2_256B for the K / V tensor maps
 #endif

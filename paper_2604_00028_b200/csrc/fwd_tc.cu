@@ -8,19 +8,20 @@
 // One CTA = 64 query rows of one KV head (rows hq0 .. hq0 + 63; G < 64 padded with zero rows) x one
 // split x one batch entry; grid = (s, H_KV * ceil(G / 64), B) as on the other paths.  Stages of 128
 // tokens (two 64-token tiles): K and V as [half][128 tokens][64 dims], 128B-swizzled, 64 KB a stage.
-//   warp 4       TMA producer: one 5-D box per 64-token tile and 64-dim half, K and V on separate
+//   warp 8       TMA producer: one 5-D box per 64-token tile and 64-dim half, K and V on separate
 //                mbarriers (dense or paged cache); a split's last stage may hold one tile.
-//   warp 5       TMEM allocator and MMA issuer (one lane), tcgen05.mma kind::f16 with A from TMEM:
+//   warp 9       TMEM allocator and MMA issuer (one lane), tcgen05.mma kind::f16 with A from TMEM:
 //                S(s) = Q K(s)^T at M = 64 rows, N = 128 tokens, K = 128 dims into TMEM buffer s & 1,
 //                then O += P(s) V(s) at M = 128, N = 128 dims, K = 128 tokens with the pair
 //                P = P_hi + P_lo stacked along M (B = the V box, MN-major): two S stages ahead, so the
 //                tensor pipe runs PV(s) and S(s + 2) while the softmax warps work on stage s + 1.
 //                The pipe executes in issue order, so S(s + 2) overwrites the buffer only after PV(s)
 //                read P(s) from it; tcgen05.commit releases ring stages, S and O to their waiters.
-//   warps 0-3    softmax and epilogue: row r lives on TMEM lane 32 (r / 16) + r mod 16 (M = 64,
+//   warps 0-7    softmax and epilogue: row r lives on TMEM lane 32 (r / 16) + r mod 16 (M = 64,
 //                scripts/microbench_tcgen05_rows.cu); the 16-lane TMEM shapes give thread t rows
-//                16 w + t / 4 and + 8 and a quarter of the tokens, the 4 threads of a row reduce
-//                with shuffles.  Online softmax in fp32 / log2 units; P = exp2(S - m) as the bf16
+//                16 q + t / 4 and + 8 (q = w mod 4), the 4 threads of a row reduce with shuffles,
+//                and warps q, q + 4 take the two 64-token halves of a stage (row maxima exchanged
+//                through shared memory).  (DECATTN_TC_SMX_WARPS = 4: warps 0-3 take both halves.)  Online softmax in fp32 / log2 units; P = exp2(S - m) as the bf16
 //                pair P_hi + P_lo (the precision of fwd.cu's PV) written over S.  The
 //                running maximum m is a reference that moves only when a stage's maximum exceeds it
 //                by more than 8 (log2 units); then the O rows are rescaled in TMEM (tcgen05.ld /
@@ -50,9 +51,13 @@ namespace {
 
 constexpr int kTcM = kTcRows;                    // query rows of a CTA (the S MMA's M)
 constexpr int kTcT = 2 * kTileN;                 // tokens per stage (the S MMA's N): two 64-token tiles
-constexpr int kTcStageBytes = 2 * kStageBytes;   // K [half][128 tokens][64 dims] + V: 64 KB
-constexpr int kTcStages = DECATTN_TC_STAGES;     // ring stages
-constexpr int kTcSoftmaxWarps = 4;
+constexpr int kTcSlotBytes = kStageBytes;        // K or V of a stage: [half][128 tokens][64 dims], 32 KB
+constexpr int kTcHalfStride = kTcSlotBytes / 2;  // the 64-dim halves of a slot
+constexpr int kTcKSlots = DECATTN_TC_KSLOTS;     // K ring (released when S(s) is computed)
+constexpr int kTcVSlots = DECATTN_TC_VSLOTS;     // V ring (released when PV(s) is done)
+constexpr int kTcSoftmaxWarps = DECATTN_TC_SMX_WARPS;
+constexpr int kTcHalvesPerWarp = 8 / kTcSoftmaxWarps;   // 64-token halves of a stage per softmax warp
+static_assert(kTcSoftmaxWarps == 4 || kTcSoftmaxWarps == 8, "one or two softmax warps per lane quadrant");
 constexpr int kTcThreads = (kTcSoftmaxWarps + 2) * 32;   // + TMA producer warp + MMA warp
 constexpr int kTcProducerWarp = kTcSoftmaxWarps, kTcMmaWarp = kTcSoftmaxWarps + 1;
 // TMEM columns (512 allocated): two S buffers (P is written over S once the softmax warps read it),
@@ -64,7 +69,7 @@ constexpr int kTcProducerWarp = kTcSoftmaxWarps, kTcMmaWarp = kTcSoftmaxWarps + 
 // M = 128, N = 128 instead of two passes at M = 64 (each at half the tensor rate).
 constexpr int kTcTmemCols = 512;
 constexpr uint32_t kTcColSP = 0, kTcColO = 2 * kTcT, kTcColQ = kTcColO + 128;
-constexpr int kTcSmem = kTcStages * kTcStageBytes + 1024;
+constexpr int kTcSmem = (kTcKSlots + kTcVSlots) * kTcSlotBytes + 1024;
 static_assert(kTcSmem <= 227 * 1024, "tcgen05 path shared memory");
 static_assert(kTcSmem == kTcSmemCfg && kTcThreads == kTcThreadsCfg, "the planner's launch fields (config.h)");
 static_assert(kTcColQ + 64 <= kTcTmemCols, "TMEM columns");
@@ -73,10 +78,25 @@ constexpr float kTcRescaleLog2 = 8.f;            // rescale O only when the maxi
 
 // development timeline tracing (-DDECATTN_TRACE builds): globaltimer ns of tiles 16..23 of the
 // first 64 CTAs: 0+k K TMA issued, 8+k S issued, 16+k S seen by softmax warp 0, 24+k P written,
-// 32+k PV issued, 40+k PV seen done by softmax warp 0 (P-buffer wait)
+// 32+k PV issued, 40+k P(s) seen complete by the MMA thread, 48+k S start, 56+k PV start
 #ifdef DECATTN_TRACE
 __device__ unsigned long long g_trace_tc[64 * 64];
 __device__ unsigned long long g_clock_tc[4];   // globaltimer / clock64 at S(16), S(23) of CTA 0
+__device__ unsigned long long g_cta_tc[8 * 1024];   // per CTA (first 1024): after the PDL wait, end, SM id,
+// entry, Q in TMEM (MMA thread), first S seen, last PV seen (softmax thread 0)
+__device__ __forceinline__ void tc_trace_cta(int slot) {
+  const int c = (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+  if (c >= 1024) return;
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  g_cta_tc[slot * 1024 + c] = t;
+  if (slot == 0) {
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    g_cta_tc[2 * 1024 + c] = smid;
+  }
+}
+#define TC_TRACE_CTA(slot) tc_trace_cta(slot)
 __device__ __forceinline__ void tc_trace(int slot_base, int i) {
   const int k = i - 16;
   if (k < 0 || k >= 8) return;
@@ -89,6 +109,31 @@ __device__ __forceinline__ void tc_trace(int slot_base, int i) {
 #define TC_TRACE(base, i) tc_trace(base, i)
 #else
 #define TC_TRACE(base, i) do { } while (0)
+#define TC_TRACE_CTA(slot) do { } while (0)
+#endif
+
+// development watchdog (-DDECATTN_TC_WATCHDOG builds): a wait that has not completed after 2 s
+// prints its barrier tag, stage and thread, then traps
+#ifdef DECATTN_TC_WATCHDOG
+}  // namespace
+}  // namespace decattn
+#include <cstdio>
+namespace decattn {
+namespace {
+__device__ __forceinline__ void tc_wait(uint32_t bar, uint32_t parity, int tag, int s) {
+  unsigned long long t0, t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  while (!mbar_try_wait(bar, parity)) {
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (t - t0 > 2000000000ull) {
+      printf("tc watchdog: tag %d stage %d parity %u thread %d block %d %d %d\n", tag, s, parity, (int)threadIdx.x,
+             (int)blockIdx.x, (int)blockIdx.y, (int)blockIdx.z);
+      asm volatile("trap;");
+    }
+  }
+}
+#else
+__device__ __forceinline__ void tc_wait(uint32_t bar, uint32_t parity, int, int) { mbar_wait(bar, parity); }
 #endif
 
 // ---- tcgen05 helpers --------------------------------------------------------------------------
@@ -212,18 +257,22 @@ __device__ __forceinline__ uint32_t sw128_chunk(int r, int c) {
 __global__ void __launch_bounds__(kTcThreads, 1)
     split_kv_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmap_k, const __grid_constant__ CUtensorMap tmap_v,
                            const FwdParams p, int kernel_combine) {
-  constexpr int NS = kTcStages;
+  constexpr int NK = kTcKSlots, NV = kTcVSlots;
   extern __shared__ uint8_t smem_raw[];
-  __shared__ __align__(8) uint64_t full_bar[NS];    // K of the stage has landed
-  __shared__ __align__(8) uint64_t fullv_bar[NS];   // V of the stage has landed
-  __shared__ __align__(8) uint64_t empty_bar[NS];   // PV of the stage done (tcgen05.commit)
+  __shared__ __align__(8) uint64_t fullk_bar[NK];   // K(s) has landed in slot s % NK
+  __shared__ __align__(8) uint64_t emptyk_bar[NK];  // S(s) done: slot free (tcgen05.commit)
+  __shared__ __align__(8) uint64_t fullv_bar[NV];   // V(s) has landed in slot s % NV
+  __shared__ __align__(8) uint64_t emptyv_bar[NV];  // PV(s) done: slot free (tcgen05.commit)
   __shared__ __align__(8) uint64_t q_bar;           // Q is in TMEM (128 softmax threads)
   __shared__ __align__(8) uint64_t s_full[2];       // S(s) in TMEM buffer s & 1 (commit)
   __shared__ __align__(8) uint64_t p_full[2];       // P(s) written over S(s) (4 warps)
   __shared__ __align__(8) uint64_t pv_done[2];      // O += P(s) V(s) done for s & 1 == b (commit)
   __shared__ uint32_t tmem_base;
+  __shared__ float red_x[2][2][kTcM];               // [stage parity][token half] row maxima (8 warps)
+  __shared__ float red_l[2][kTcM];                  // [token half] row sums (8 warps)
 
   const uint32_t raw = smem_u32(smem_raw);
+  if (threadIdx.x == 0) TC_TRACE_CTA(3);
   const uint32_t sbase = (raw + 1023u) & ~1023u;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
@@ -232,13 +281,23 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   const int rg = grp - kvh * p.mblocks_per_head;
   const int hq0 = kvh * p.G + rg * kTcM;
   const int rows_valid = min(kTcM, p.G - rg * kTcM);
+  // pull this CTA's Q rows (two 128-byte lines each) into L2 before anything else: the softmax
+  // warps read them right after griddepcontrol.wait, when the ring's first K / V loads of every
+  // CTA already queue at the DRAM (a prefetch returns no data, so it cannot observe a stale Q)
+  if (DECATTN_TC_QPREFETCH && threadIdx.x < 2 * kTcM && (threadIdx.x >> 1) < rows_valid)
+    prefetch_l2(p.q + static_cast<int64_t>(b) * p.q_sb + static_cast<int64_t>(hq0 + (threadIdx.x >> 1)) * p.q_sh +
+                (threadIdx.x & 1) * 64);
 
   if (threadIdx.x == 0) {
 #pragma unroll
-    for (int i = 0; i < NS; ++i) {
-      mbar_init(smem_u32(&full_bar[i]), 1);
+    for (int i = 0; i < NK; ++i) {
+      mbar_init(smem_u32(&fullk_bar[i]), 1);
+      mbar_init(smem_u32(&emptyk_bar[i]), 1);
+    }
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
       mbar_init(smem_u32(&fullv_bar[i]), 1);
-      mbar_init(smem_u32(&empty_bar[i]), 1);
+      mbar_init(smem_u32(&emptyv_bar[i]), 1);
     }
     mbar_init(smem_u32(&q_bar), kTcSoftmaxWarps * 32);
     for (int i = 0; i < 2; ++i) {
@@ -268,7 +327,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   int t0 = 0, t_end = 0, n_tiles = 0;
   split_range(min(max(p.l_default, 0), p.l_cap), split, p.num_splits, p.s_magic, t0, t_end, n_tiles);
   if (p.block_table == nullptr && warp == kTcProducerWarp && lane == 0 && n_tiles >= 1) {
-    const int np = min(n_tiles, 2 * NS);
+    const int np = min(n_tiles, 2 * NK);
     for (int i = 0; i < np; ++i)
       for (int h = 0; h < 2; ++h) {
         tma_prefetch_5d(&tmap_k, 0, t0 + i * kTileN, h, kvh, b);
@@ -281,6 +340,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     split_range(min(max(max(__ldg(p.seqlens + b), 0) - p.seq_offset, 0), p.l_cap), split, p.num_splits, p.s_magic,
                 t0, t_end, n_tiles);
   const int n_st = (n_tiles + 1) >> 1;                 // 128-token stages
+  if (threadIdx.x == 0) TC_TRACE_CTA(0);
 
   if (warp == kTcProducerWarp) {
     // ================= TMA producer (dense or paged cache) =================
@@ -291,29 +351,45 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       const int32_t* bt = p.block_table != nullptr ? p.block_table + static_cast<int64_t>(b) * p.bt_stride : nullptr;
       const uint32_t tpp = p.page_size > 0 ? static_cast<uint32_t>(p.page_size / kTileN) : 1u;
       const uint32_t tile0 = static_cast<uint32_t>(t0 / kTileN);
-      uint32_t cj = bt != nullptr ? udiv_magic(tile0, p.page_magic) : 0u, ck = tile0 - cj * tpp;
-      for (int s = 0; s < n_st; ++s) {
-        const int st = s % NS;
-        if (s >= NS) mbar_wait(smem_u32(&empty_bar[st]), ((s / NS) - 1) & 1);
+      // K and V of a stage go to their own rings in the order the tensor pipe needs them:
+      // K(0), K(1), then V(s), K(s + 2) (S runs two stages ahead of PV).  Each ring walks the
+      // split's tiles (and, paged, the block table) on its own
+      struct Walk {
+        uint32_t cj, ck;
+      };
+      Walk wk{bt != nullptr ? udiv_magic(tile0, p.page_magic) : 0u, 0u}, wv{0u, 0u};
+      wk.ck = tile0 - wk.cj * tpp;
+      wv = wk;
+      auto load = [&](const CUtensorMap* tm, Walk& w, uint32_t slot, uint32_t bar, int s) {
         const int nsub = min(2, n_tiles - 2 * s);
-        const uint32_t fb = smem_u32(&full_bar[st]), fvb = smem_u32(&fullv_bar[st]);
-        mbar_arrive_expect_tx(fb, nsub * 2 * kHalfBytes);
-        mbar_arrive_expect_tx(fvb, nsub * 2 * kHalfBytes);
-        const uint32_t sK = sbase + st * kTcStageBytes, sV = sK + kTcStageBytes / 2;
+        mbar_arrive_expect_tx(bar, nsub * 2 * kHalfBytes);
         for (int sub = 0; sub < nsub; ++sub) {
           int major = b, tok = t0 + (2 * s + sub) * kTileN;
           if (bt != nullptr) {   // paged: tile in page block_table[b][t / page_size] at t % page_size
-            major = __ldg(bt + cj);
-            tok = static_cast<int>(ck) * kTileN;
-            if (++ck == tpp) { ck = 0; ++cj; }
+            major = __ldg(bt + w.cj);
+            tok = static_cast<int>(w.ck) * kTileN;
+            if (++w.ck == tpp) { w.ck = 0; ++w.cj; }
           }
 #pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            tma_load_5d(sK + h * (kTcStageBytes / 4) + sub * kHalfBytes, &tmap_k, fb, 0, tok, h, kvh, major);
-            tma_load_5d(sV + h * (kTcStageBytes / 4) + sub * kHalfBytes, &tmap_v, fvb, 0, tok, h, kvh, major);
-          }
+          for (int h = 0; h < 2; ++h) tma_load_5d(slot + h * kTcHalfStride + sub * kHalfBytes, tm, bar, 0, tok, h, kvh, major);
         }
+      };
+      auto load_k = [&](int s) {
+        const int st = s % NK;
+        if (s >= NK) tc_wait(smem_u32(&emptyk_bar[st]), ((s / NK) - 1) & 1, 1, s);
+        load(&tmap_k, wk, sbase + st * kTcSlotBytes, smem_u32(&fullk_bar[st]), s);
         TC_TRACE(0, s);
+      };
+      auto load_v = [&](int s) {
+        const int st = s % NV;
+        if (s >= NV) tc_wait(smem_u32(&emptyv_bar[st]), ((s / NV) - 1) & 1, 2, s);
+        load(&tmap_v, wv, sbase + (NK + st) * kTcSlotBytes, smem_u32(&fullv_bar[st]), s);
+      };
+      if (n_st > 0) load_k(0);
+      if (n_st > 1) load_k(1);
+      for (int s = 0; s < n_st; ++s) {
+        load_v(s);
+        if (s + 2 < n_st) load_k(s + 2);
       }
     }
   } else if (warp == kTcMmaWarp) {
@@ -321,21 +397,23 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     if (lane == 0 && n_st > 0) {
       constexpr uint32_t id_s = tc_idesc(kTcM, kTcT, 0, 0);             // S: M = 64, N = 128 tokens
       constexpr uint32_t id_o = tc_idesc(2 * kTcM, kHeadDim, 0, 1);     // O: [P_hi; P_lo] stacked along M
-      mbar_wait(smem_u32(&q_bar), 0);
+      tc_wait(smem_u32(&q_bar), 0, 3, 0);
+      TC_TRACE_CTA(4);
       // S(s) = Q K(s)^T into TMEM buffer s & 1.  The buffer held P(s - 2), read by PV(s - 2), which
       // was issued before: the tensor pipe executes in issue order
       auto issue_s = [&](int s) {
-        const int st = s % NS, sb = s & 1;
-        mbar_wait(smem_u32(&full_bar[st]), (s / NS) & 1);
+        const int st = s % NK, sb = s & 1;
+        tc_wait(smem_u32(&fullk_bar[st]), (s / NK) & 1, 4, s);
         tc_fence_after();
         TC_TRACE(48, s);
-        const uint32_t sK = sbase + st * kTcStageBytes;
+        const uint32_t sK = sbase + st * kTcSlotBytes;
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {   // 16 dims per step: K half kk / 4, +32 B per step in the row
-          const uint64_t bk = tc_sdesc(sK + (kk >> 2) * (kTcStageBytes / 4) + (kk & 3) * 32, 16, 1024);
+          const uint64_t bk = tc_sdesc(sK + (kk >> 2) * kTcHalfStride + (kk & 3) * 32, 16, 1024);
           tc_mma_ts(tmem + kTcColSP + sb * kTcT, tmem + kTcColQ + kk * 8, bk, id_s, kk > 0 ? 1u : 0u);
         }
         tc_commit(smem_u32(&s_full[sb]));
+        tc_commit(smem_u32(&emptyk_bar[st]));
         TC_TRACE(8, s);
 #ifdef DECATTN_TRACE
         if ((s == 16 || s == 23) && blockIdx.x + blockIdx.y + blockIdx.z == 0) {
@@ -348,19 +426,20 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       };
       // O += P(s) V(s), once the softmax warps wrote P(s) (over S(s)) and V(s) landed
       auto issue_pv = [&](int s) {
-        const int st = s % NS, pb = s & 1;
-        mbar_wait(smem_u32(&p_full[pb]), (s >> 1) & 1);
-        mbar_wait(smem_u32(&fullv_bar[st]), (s / NS) & 1);
+        const int st = s % NV, pb = s & 1;
+        tc_wait(smem_u32(&p_full[pb]), (s >> 1) & 1, 5, s);
+        TC_TRACE(40, s);
+        tc_wait(smem_u32(&fullv_bar[st]), (s / NV) & 1, 6, s);
         tc_fence_after();
         TC_TRACE(56, s);
-        const uint32_t sV = sbase + st * kTcStageBytes + kTcStageBytes / 2;
+        const uint32_t sV = sbase + (NK + st) * kTcSlotBytes;
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {   // 16 tokens (8 packed columns, 16 V rows) per step
-          const uint64_t bv = tc_sdesc(sV + kk * 2048, kTcStageBytes / 4, 1024);
+          const uint64_t bv = tc_sdesc(sV + kk * 2048, kTcHalfStride, 1024);
           tc_mma_ts(tmem + kTcColO, tmem + kTcColSP + pb * kTcT + kk * 8, bv, id_o, (s > 0 || kk > 0) ? 1u : 0u);
         }
         tc_commit(smem_u32(&pv_done[pb]));
-        tc_commit(smem_u32(&empty_bar[st]));
+        tc_commit(smem_u32(&emptyv_bar[st]));
         TC_TRACE(32, s);
       };
       // two S stages ahead, then PV(s) and S(s + 2): the tensor pipe runs PV(s) and S(s + 2) while
@@ -374,56 +453,68 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     }
   } else {
     // ================= softmax + epilogue =================
-    // warp w reads TMEM lanes 32 w .. 32 w + 15 = rows 16 w .. 16 w + 15 (M = 64) with the 16-lane
-    // shapes: thread t holds rows rA = 16 w + t / 4 and rB = rA + 8, and of each 8-token group the
-    // tokens 2 a, 2 a + 1 (a = t % 4); the 4 threads of a row reduce with xor shuffles 1, 2
+    // warp w reads TMEM lanes 32 q .. 32 q + 15 (q = w mod 4) = rows 16 q .. 16 q + 15 (M = 64) with
+    // the 16-lane shapes: thread t holds rows rA = 16 q + t / 4 and rB = rA + 8, and of each 8-token
+    // group the tokens 2 a, 2 a + 1 (a = t % 4); the 4 threads of a row reduce with xor shuffles
+    // 1, 2.  With 8 softmax warps, warps q and q + 4 share the quadrant and split every stage's 128
+    // tokens (and O's 128 columns) into halves hh = w / 4: two warps per SM sub-partition hide each
+    // other's MUFU / conversion latency; the row maximum is exchanged through shared memory
+    // (named barrier 1 + q, 64 threads) and the row sums are added in the epilogue
+    const int q4 = warp & 3, hh = warp >> 2;
     const int a4 = lane & 3;
-    const int rA = 16 * warp + (lane >> 2), rB = rA + 8;
-    const uint32_t lane_addr = static_cast<uint32_t>(warp * 32) << 16;
+    const int rA = 16 * q4 + (lane >> 2), rB = rA + 8;
+    const uint32_t lane_addr = static_cast<uint32_t>(q4 * 32) << 16;
+    auto pair_sync = [&]() {
+      if (kTcSoftmaxWarps == 8) asm volatile("bar.sync %0, 64;" ::"r"(1 + q4) : "memory");
+    };
     // Q -> TMEM (the S MMA's A operand: u32 column j = dims 2 j, 2 j + 1), 16x128b layout: column
-    // 4 g + a of rows rA, rB; zero past G
+    // 4 g + a of rows rA, rB; zero past G.  Warp half hh writes dims [64 h, + 64) for its halves h
     {
       const uint32_t* qA = reinterpret_cast<const uint32_t*>(p.q + static_cast<int64_t>(b) * p.q_sb +
                                                               static_cast<int64_t>(hq0 + min(rA, rows_valid - 1)) * p.q_sh);
       const uint32_t* qB = reinterpret_cast<const uint32_t*>(p.q + static_cast<int64_t>(b) * p.q_sb +
                                                               static_cast<int64_t>(hq0 + min(rB, rows_valid - 1)) * p.q_sh);
-      uint32_t q0[16], q1[16];
 #pragma unroll
-      for (int g = 0; g < 8; ++g) {
-        q0[2 * g] = rA < rows_valid ? __ldg(qA + 4 * g + a4) : 0u;
-        q0[2 * g + 1] = rB < rows_valid ? __ldg(qB + 4 * g + a4) : 0u;
-        q1[2 * g] = rA < rows_valid ? __ldg(qA + 32 + 4 * g + a4) : 0u;
-        q1[2 * g + 1] = rB < rows_valid ? __ldg(qB + 32 + 4 * g + a4) : 0u;
+      for (int hi = 0; hi < kTcHalvesPerWarp; ++hi) {
+        const int h = hh * kTcHalvesPerWarp + hi;
+        uint32_t qv[16];
+#pragma unroll
+        for (int g = 0; g < 8; ++g) {
+          qv[2 * g] = rA < rows_valid ? __ldg(qA + 32 * h + 4 * g + a4) : 0u;
+          qv[2 * g + 1] = rB < rows_valid ? __ldg(qB + 32 * h + 4 * g + a4) : 0u;
+        }
+        tc_st16x128_x8(tmem + lane_addr + kTcColQ + 32 * h, qv);
       }
-      tc_st16x128_x8(tmem + lane_addr + kTcColQ, q0);
-      tc_st16x128_x8(tmem + lane_addr + kTcColQ + 32, q1);
       tc_wait_st();
       tc_fence_before();
       mbar_arrive(smem_u32(&q_bar));
     }
+    constexpr int NSV = 32 * kTcHalvesPerWarp;            // S values per thread and stage
     float mA = kNegInf, mB = kNegInf, lA = 0.f, lB = 0.f;   // reference maxima (log2 units), partial sums
     for (int s = 0; s < n_st; ++s) {
       const int sb = s & 1;
       const uint32_t sp = tmem + lane_addr + kTcColSP + sb * kTcT;   // the S / P buffer of this stage
       const int valid = min(kTcT, t_end - (t0 + s * kTcT));
-      mbar_wait(smem_u32(&s_full[sb]), (s >> 1) & 1);
+      tc_wait(smem_u32(&s_full[sb]), (s >> 1) & 1, 7, s);
       tc_fence_after();
       if (threadIdx.x == 0) TC_TRACE(16, s);
-      float sv[64];   // [half h][group g][4]: tokens 64 h + 8 g + 2 a (+1) of rows rA, rB
-      {
-        uint32_t r0[32], r1[32];
-        tc_ld16x256<8>(sp, r0);
-        tc_ld16x256<8>(sp + 64, r1);
+      if (threadIdx.x == 0 && s == 0) TC_TRACE_CTA(5);
+      float sv[NSV];   // [half hi][group g][4]: tokens 64 h + 8 g + 2 a (+1) of rows rA, rB
+#pragma unroll
+      for (int hi = 0; hi < kTcHalvesPerWarp; ++hi) {
+        uint32_t r0[32];
+        tc_ld16x256<8>(sp + 64 * (hh * kTcHalvesPerWarp + hi), r0);
         tc_wait_ld();
 #pragma unroll
-        for (int c = 0; c < 32; ++c) sv[c] = __uint_as_float(r0[c]), sv[32 + c] = __uint_as_float(r1[c]);
+        for (int c = 0; c < 32; ++c) sv[32 * hi + c] = __uint_as_float(r0[c]);
       }
-      if (valid < kTcT) {                                 // tokens past the range
+      const int tok0 = 64 * hh * kTcHalvesPerWarp;       // first token of this warp's values
+      if (valid < tok0 + NSV * 2) {                       // tokens past the range
 #pragma unroll
-        for (int g = 0; g < 16; ++g)
+        for (int g = 0; g < NSV / 4; ++g)
 #pragma unroll
           for (int c = 0; c < 2; ++c) {
-            const bool ok = 8 * g + 2 * a4 + c < valid;
+            const bool ok = tok0 + 8 * g + 2 * a4 + c < valid;
             sv[4 * g + c] = ok ? sv[4 * g + c] : kNegInf;
             sv[4 * g + 2 + c] = ok ? sv[4 * g + 2 + c] : kNegInf;
           }
@@ -433,7 +524,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       float yA = fmaxf(fmaxf(sv[8], sv[9]), fmaxf(sv[12], sv[13]));
       float yB = fmaxf(fmaxf(sv[10], sv[11]), fmaxf(sv[14], sv[15]));
 #pragma unroll
-      for (int g = 4; g < 16; g += 2) {
+      for (int g = 4; g < NSV / 4; g += 2) {
         xA = fmaxf(xA, fmaxf(sv[4 * g], sv[4 * g + 1]));
         xB = fmaxf(xB, fmaxf(sv[4 * g + 2], sv[4 * g + 3]));
         yA = fmaxf(yA, fmaxf(sv[4 * g + 4], sv[4 * g + 5]));
@@ -445,20 +536,29 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       xB = fmaxf(xB, __shfl_xor_sync(0xffffffffu, xB, 1));
       xA = fmaxf(xA, __shfl_xor_sync(0xffffffffu, xA, 2));
       xB = fmaxf(xB, __shfl_xor_sync(0xffffffffu, xB, 2));
+      if (kTcSoftmaxWarps == 8) {   // the other token half's maximum (parity-double-buffered slots)
+        if (a4 == 0) red_x[sb][hh][rA] = xA, red_x[sb][hh][rB] = xB;
+        pair_sync();
+        xA = fmaxf(xA, red_x[sb][hh ^ 1][rA]);
+        xB = fmaxf(xB, red_x[sb][hh ^ 1][rB]);
+      }
       const float mxA = xA * p.scale_log2, mxB = xB * p.scale_log2;   // >= 1 valid token: finite
       if (s == 0) mA = mxA, mB = mxB;                    // PV(0) starts O (accumulate = 0)
       // the reference moves only when this stage's maximum exceeds it by more than 2^8: then the
       // row's O (PV(0 .. s-1): wait for PV(s - 1)) and l are rescaled by exp2(m_old - m_new).  The
-      // TMEM load / store is warp-collective: every lane takes part, factor 1 for unchanged rows
+      // TMEM load / store is warp-collective: every lane takes part, factor 1 for unchanged rows.
+      // Both warps of a quadrant see the same maxima, so they take the same decision, each for its
+      // O columns
       const bool resA = s > 0 && mxA > mA + kTcRescaleLog2, resB = s > 0 && mxB > mB + kTcRescaleLog2;
       if (__any_sync(0xffffffffu, resA || resB)) {
         const float alA = resA ? ex2(mA - mxA) : 1.f, alB = resB ? ex2(mB - mxB) : 1.f;
         mbar_wait(smem_u32(&pv_done[(s - 1) & 1]), ((s - 1) >> 1) & 1);
         tc_fence_after();
 #pragma unroll
-        for (int h = 0; h < 4; ++h) {   // the hi lanes (h < 2) and lo lanes, O columns [64 (h & 1), + 64)
+        for (int i = 0; i < 2 * kTcHalvesPerWarp; ++i) {   // hi / lo lanes x this warp's O column halves
+          const int h = hh * kTcHalvesPerWarp + (i >> 1);
           uint32_t ov[32];
-          const uint32_t ta = tmem + lane_addr + (static_cast<uint32_t>(16 * (h >> 1)) << 16) + kTcColO + 64 * (h & 1);
+          const uint32_t ta = tmem + lane_addr + (static_cast<uint32_t>(16 * (i & 1)) << 16) + kTcColO + 64 * h;
           tc_ld16x256<8>(ta, ov);
           tc_wait_ld();
 #pragma unroll
@@ -480,11 +580,12 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       const float nA = -mA, nB = -mB;
       float sA0 = 0.f, sA1 = 0.f, sB0 = 0.f, sB1 = 0.f;
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
+      for (int hi = 0; hi < kTcHalvesPerWarp; ++hi) {
+        const int h = hh * kTcHalvesPerWarp + hi;
         uint32_t hw[16], lw[16];
 #pragma unroll
         for (int g8 = 0; g8 < 8; ++g8) {
-          const int g = 8 * h + g8;
+          const int g = 8 * hi + g8;
           const float pa0 = ex2(fmaf(sv[4 * g], p.scale_log2, nA)), pa1 = ex2(fmaf(sv[4 * g + 1], p.scale_log2, nA));
           const float pb0 = ex2(fmaf(sv[4 * g + 2], p.scale_log2, nB)), pb1 = ex2(fmaf(sv[4 * g + 3], p.scale_log2, nB));
           if (g8 & 1) sA1 += pa0 + pa1, sB1 += pb0 + pb1;
@@ -501,12 +602,12 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       lB += sB0 + sB1;
       if (valid < kTcT) {
         // V rows past the range may hold anything (stale or NaN): zero them (P = 0 there)
-        const int st = s % NS;
-        mbar_wait(smem_u32(&fullv_bar[st]), (s / NS) & 1);
-        const uint32_t sV = sbase + st * kTcStageBytes + kTcStageBytes / 2;
+        const int st = s % NV;
+        tc_wait(smem_u32(&fullv_bar[st]), (s / NV) & 1, 8, s);
+        const uint32_t sV = sbase + (NK + st) * kTcSlotBytes;
         for (int e = threadIdx.x; e < (kTcT - valid) * 16; e += kTcSoftmaxWarps * 32) {
           const int row = valid + (e >> 4), c = e & 15;
-          sts128(sV + (c >> 3) * (kTcStageBytes / 4) + sw128_chunk(row, c & 7), make_uint4(0, 0, 0, 0));
+          sts128(sV + (c >> 3) * kTcHalfStride + sw128_chunk(row, c & 7), make_uint4(0, 0, 0, 0));
         }
         fence_proxy_async_smem();
       }
@@ -521,9 +622,16 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     lB += __shfl_xor_sync(0xffffffffu, lB, 1);
     lA += __shfl_xor_sync(0xffffffffu, lA, 2);
     lB += __shfl_xor_sync(0xffffffffu, lB, 2);
+    if (kTcSoftmaxWarps == 8) {   // both token halves' sums (same reference maxima in both warps)
+      if (a4 == 0) red_l[hh][rA] = lA, red_l[hh][rB] = lB;
+      pair_sync();
+      lA += red_l[hh ^ 1][rA];
+      lB += red_l[hh ^ 1][rB];
+    }
     float invA = 0.f, invB = 0.f, lseA = kNegInf, lseB = kNegInf;
     if (n_st > 0) {
       mbar_wait(smem_u32(&pv_done[(n_st - 1) & 1]), ((n_st - 1) >> 1) & 1);
+      if (threadIdx.x == 0) TC_TRACE_CTA(6);
       tc_fence_after();
       invA = lA > 0.f ? __frcp_rn(lA) : 0.f;
       invB = lB > 0.f ? __frcp_rn(lB) : 0.f;
@@ -534,7 +642,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     const size_t prowA = static_cast<size_t>(split) * p.batch * p.h_q + rowA, prowB = prowA + 8;
     const bool wA = rA < rows_valid, wB = rB < rows_valid;
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
+    for (int hi = 0; hi < kTcHalvesPerWarp; ++hi) {
+      const int h = hh * kTcHalvesPerWarp + hi;
       uint32_t ov[32];
       if (n_st > 0) {   // O = the hi lanes' part + the lo lanes' part
         uint32_t ol[32];
@@ -564,7 +673,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         }
       }
     }
-    if (a4 == 0) {
+    if (a4 == 0 && hh == 0) {
       if (kernel_combine) {
         if (wA) p.ws_lse[prowA] = lseA;
         if (wB) p.ws_lse[prowB] = lseB;
@@ -576,6 +685,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   }
   tc_fence_before();
   __syncthreads();
+  if (threadIdx.x == 0) TC_TRACE_CTA(1);
   if (warp == kTcMmaWarp) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTcTmemCols));
@@ -637,6 +747,9 @@ cudaError_t forward_tc_residency(int* out) {
 extern "C" __attribute__((visibility("default"))) int da_trace_fetch_tc(unsigned long long* host, int n) {
   if (n > 64 * 64) n = 64 * 64;
   return cudaMemcpyFromSymbol(host, g_trace_tc, sizeof(unsigned long long) * n) == cudaSuccess ? 0 : 1;
+}
+extern "C" __attribute__((visibility("default"))) int da_trace_fetch_tc_cta(unsigned long long* host) {
+  return cudaMemcpyFromSymbol(host, g_cta_tc, sizeof(unsigned long long) * 8 * 1024) == cudaSuccess ? 0 : 1;
 }
 extern "C" __attribute__((visibility("default"))) int da_trace_fetch_tc_clock(unsigned long long* host) {
   return cudaMemcpyFromSymbol(host, g_clock_tc, sizeof(unsigned long long) * 4) == cudaSuccess ? 0 : 1;

@@ -19,20 +19,45 @@ if hasattr(L.LIB, "da_trace_fetch_tc_clock"):
     L.LIB.da_trace_fetch_tc_clock.argtypes = [ctypes.c_void_p]
 
 
-def trace(b, hq, hkv, lk, policy="seq_aware", forced=0):
+def trace(b, hq, hkv, lk, policy="seq_aware", forced=0, path=None):
     w = synth.make_inputs(b, hq, hkv, lk, device="cuda", seed=3)
-    plan = dec.make_plan(b, hq, hkv, lk, policy=policy, forced_splits=forced)
+    plan = dec.make_plan(b, hq, hkv, lk, policy=policy, forced_splits=forced, path=path)
     ws = dec.workspace_for(plan, w["q"].device)
     for _ in range(3):
         dec.forward(plan, w["q"], w["k"], w["v"], None, workspace=ws)
     torch.cuda.synchronize()
     buf = (ctypes.c_ulonglong * (64 * 64))()
     L.LIB.da_trace_fetch_tc(ctypes.addressof(buf), 64 * 64)
-    names = ["K_tma", "S_issue", "S_seen", "P_done", "PV_issue", "PVm2_seen", "S_start", "PV_start"]
+    names = ["K_tma", "S_issue", "S_seen", "P_done", "PV_issue", "P_seen_mma", "S_start", "PV_start"]
     print(f"== B={b} HQ={hq} HKV={hkv} L={lk} s={plan.num_splits} path={plan.path}")
     ck = (ctypes.c_ulonglong * 4)()
     if hasattr(L.LIB, "da_trace_fetch_tc_clock") and L.LIB.da_trace_fetch_tc_clock(ctypes.addressof(ck)) == 0 and ck[1] > ck[0]:
         print(f" SM clock over stages 16-23 (CTA 0): {(ck[3] - ck[2]) / (ck[1] - ck[0]) * 1e3:.0f} MHz")
+    if hasattr(L.LIB, "da_trace_fetch_tc_cta"):
+        L.LIB.da_trace_fetch_tc_cta.argtypes = [ctypes.c_void_p]
+        cb = (ctypes.c_ulonglong * (8 * 1024))()
+        L.LIB.da_trace_fetch_tc_cta(ctypes.addressof(cb))
+        n = min(1024, plan.grid_x * plan.grid_y * plan.grid_z)
+        st = [cb[i] for i in range(n)]
+        en = [cb[1024 + i] for i in range(n)]
+        t0 = min(st)
+        dur = sorted((e - s_) / 1e3 for s_, e in zip(st, en))
+        ends = sorted((e - t0) / 1e3 for e in en)
+        starts = sorted((s_ - t0) / 1e3 for s_ in st)
+        q = lambda a, f: a[min(len(a) - 1, int(f * len(a)))]
+        print(f" CTAs {n}: start us p0/p50/p100 {starts[0]:.2f}/{q(starts, .5):.2f}/{starts[-1]:.2f}; "
+              f"end {ends[0]:.2f}/{q(ends, .1):.2f}/{q(ends, .5):.2f}/{q(ends, .9):.2f}/{ends[-1]:.2f}; "
+              f"duration p0/p50/p100 {dur[0]:.2f}/{q(dur, .5):.2f}/{dur[-1]:.2f}")
+        med = lambda j: sorted((cb[j * 1024 + i] - cb[3 * 1024 + i]) / 1e3 for i in range(n) if cb[j * 1024 + i])
+        for j, nm in ((0, "PDL wait done"), (4, "Q in TMEM"), (5, "first S seen"), (6, "last PV seen"), (1, "end")):
+            m = med(j)
+            if m:
+                print(f"  from entry to {nm:14s} us p50 {q(m, .5):.2f} (p0 {m[0]:.2f}, p100 {m[-1]:.2f})")
+        order = sorted(range(n), key=lambda i: en[i])
+        print("  slowest CTAs (cta, sm, start, end):",
+              [(i, int(cb[2048 + i]), round((st[i] - t0) / 1e3, 2), round((en[i] - t0) / 1e3, 2)) for i in order[-6:]])
+        print("  fastest CTAs (cta, sm, start, end):",
+              [(i, int(cb[2048 + i]), round((st[i] - t0) / 1e3, 2), round((en[i] - t0) / 1e3, 2)) for i in order[:6]])
     for c in (0, 1):
         base = buf[c * 64 + 0]
         print(f" cta{c}")
@@ -42,5 +67,9 @@ def trace(b, hq, hkv, lk, policy="seq_aware", forced=0):
 
 
 if __name__ == "__main__":
+    trace(4, 64, 1, 8192, "guarded")
+    trace(1, 64, 1, 4096, "seq_aware_sm", path=2)
     trace(128, 64, 1, 8192)
+    trace(128, 32, 1, 8192)
+    trace(32, 64, 1, 32768)
     trace(1, 64, 1, 131072)

@@ -226,7 +226,7 @@ def test_set_path(L):
     # MQA G = 64, B = 4, L = 8192 under guarded: s = 32, 4 tiles per split, 128 tcgen05 CTAs -> TC
     p = L.da_plan_make(4, 64, 1, 8192, 128, 1, 0, 148, "guarded", 0)
     assert (p.num_splits, p.path, p.rows_per_cta, p.grid_y, p.combine_mode) == (32, L.DA_PATH_TC, 64, 1, 2)
-    assert (p.block_threads, p.smem_bytes) == (192, 3 * 65536 + 1024)
+    assert (p.block_threads, p.smem_bytes) == (320, 7 * 32768 + 1024)
     q = L.da_plan.from_buffer_copy(p)
     L.da_plan_set_path(q, L.DA_PATH_MMA)                      # the mma.sync kernel: 16-row CTAs
     assert (q.path, q.rows_per_cta, q.grid_y, q.path_override) == (L.DA_PATH_MMA, 16, 4, L.DA_PATH_MMA)
