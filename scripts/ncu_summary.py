@@ -16,7 +16,8 @@ import synth  # noqa: E402
 
 CONFIGS = {"llama70b": synth.CONFIGS["llama70b"], "llama70b_tp8": synth.CONFIGS["llama70b_tp8"],
            "long_context": synth.CONFIGS["long_context"], "long_context_sm": synth.CONFIGS["long_context"],
-           "high_load": synth.CONFIGS["high_load"]}
+           "high_load": synth.CONFIGS["high_load"],
+           "mqa_g64": {"batch": 128, "h_q": 64, "h_kv": 1, "l_k": 8192}}   # bench.py WORKLOADS["mqa_g64"]
 
 
 def alg_bytes(c, d=128):
@@ -63,12 +64,16 @@ def main():
             continue
         r = recs[0]
         kname = r["Kernel Name"][0]
-        short = kname[kname.find("split_kv_fwd_kernel"):kname.find("(")] if "(" in kname else kname
+        i0 = kname.find("split_kv_fwd")
+        short = kname[i0:kname.find("(")] if "(" in kname else kname[i0:]
         dur = num(r, "gpu__time_duration.sum")
         dram = (num(r, "dram__bytes_read.sum") or 0.0) + (num(r, "dram__bytes_write.sum") or 0.0)
         alg = alg_bytes(cfg)
         thr = num(r, "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed")
-        tens = num(r, "sm__inst_executed_pipe_tensor_subpipe_hmma.avg.pct_of_peak_sustained_active")
+        # tensor pipe busy cycles: HMMA (mma.sync) and tcgen05 (UTCHMMA) both count here
+        tens = num(r, "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active")
+        if tens is None:
+            tens = num(r, "sm__inst_executed_pipe_tensor_subpipe_hmma.avg.pct_of_peak_sustained_active")
         regs = r.get("launch__registers_per_thread", ("?", ""))[0]
         grid = r.get("launch__grid_size", ("?", ""))[0]
         block = r.get("launch__block_size", ("?", ""))[0]

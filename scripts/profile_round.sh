@@ -24,4 +24,5 @@ run llama70b python bench.py --workload llama70b --steps 20 --warmup 3 --no-extr
 run llama70b_tp8 python bench.py --workload llama70b_tp8 --steps 20 --warmup 3 --no-extras --cpu-seconds 1
 run long_context python bench.py --workload long_context --policy seq_aware --steps 5 --warmup 3 --no-extras --cpu-seconds 1
 run long_context_sm python bench.py --workload long_context --steps 5 --warmup 3 --no-extras --cpu-seconds 1
+run mqa_g64 python bench.py --workload mqa_g64 --steps 5 --warmup 3 --no-extras --cpu-seconds 1
 ls -la $OUT
