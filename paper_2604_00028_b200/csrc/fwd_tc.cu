@@ -58,8 +58,11 @@ constexpr int kTcVSlots = DECATTN_TC_VSLOTS;     // V ring (released when PV(s) 
 constexpr int kTcSoftmaxWarps = DECATTN_TC_SMX_WARPS;
 constexpr int kTcHalvesPerWarp = 8 / kTcSoftmaxWarps;   // 64-token halves of a stage per softmax warp
 static_assert(kTcSoftmaxWarps == 4 || kTcSoftmaxWarps == 8, "one or two softmax warps per lane quadrant");
-constexpr int kTcThreads = (kTcSoftmaxWarps + 2) * 32;   // + TMA producer warp + MMA warp
-constexpr int kTcProducerWarp = kTcSoftmaxWarps, kTcMmaWarp = kTcSoftmaxWarps + 1;
+constexpr bool kTcSplitProducer = DECATTN_TC_SPLIT_PRODUCER != 0;   // one TMA warp per ring
+constexpr int kTcThreads = (kTcSoftmaxWarps + 2 + (kTcSplitProducer ? 1 : 0)) * 32;   // + TMA warp(s) + MMA warp
+constexpr int kTcProducerWarp = kTcSoftmaxWarps;                          // K ring (and V without the split)
+constexpr int kTcProducerWarpV = kTcSplitProducer ? kTcSoftmaxWarps + 1 : kTcSoftmaxWarps;   // V ring
+constexpr int kTcMmaWarp = kTcProducerWarpV + 1;
 // TMEM columns (512 allocated): two S buffers (P is written over S once the softmax warps read it),
 // the O accumulator and Q (the S MMA's A operand, two bf16 per 32-bit column, row r on the
 // accumulator's lane).  The PV product runs at M = 128 with the P pair stacked along M: in warp
@@ -249,6 +252,25 @@ __device__ __forceinline__ void tc_st16x128_x8(uint32_t taddr, const uint32_t (&
 __device__ __forceinline__ void tc_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void tc_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
+// P = P_hi + P_lo for two values (x0 in the low half of each word).  DECATTN_TC_PAIR 0: both
+// rounded to nearest (cvt, the XU pipe); 1: P_hi = the top 16 bits of P (exact truncation, one
+// byte permute on the ALU), P_lo rounded; 2: both truncated (|error| < 2^-14 P, one-sided)
+__device__ __forceinline__ void tc_pair(float x0, float x1, uint32_t& hw, uint32_t& lw) {
+#if DECATTN_TC_PAIR == 0
+  hw = pack_bf16(x0, x1);
+  lw = pack_bf16(x0 - bf16lo(hw), x1 - bf16hi(hw));
+#else
+  const uint32_t u0 = __float_as_uint(x0), u1 = __float_as_uint(x1);
+  hw = __byte_perm(u0, u1, 0x7632);
+  const float r0 = x0 - __uint_as_float(u0 & 0xffff0000u), r1 = x1 - __uint_as_float(u1 & 0xffff0000u);
+#if DECATTN_TC_PAIR == 1
+  lw = pack_bf16(r0, r1);
+#else
+  lw = __byte_perm(__float_as_uint(r0), __float_as_uint(r1), 0x7632);
+#endif
+#endif
+}
+
 // byte offset of 16-byte chunk c (8 bf16) of row r in a 128B-swizzled box of 128-byte rows
 __device__ __forceinline__ uint32_t sw128_chunk(int r, int c) {
   return static_cast<uint32_t>(r * 128 + (((c ^ r) & 7) << 4));
@@ -342,8 +364,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   const int n_st = (n_tiles + 1) >> 1;                 // 128-token stages
   if (threadIdx.x == 0) TC_TRACE_CTA(0);
 
-  if (warp == kTcProducerWarp) {
-    // ================= TMA producer (dense or paged cache) =================
+  if (warp == kTcProducerWarp || warp == kTcProducerWarpV) {
+    // ================= TMA producer(s) (dense or paged cache) =================
     // a stage holds K then V of two 64-token tiles as [half][128 tokens][64 dims] (one 8 KB box per
     // tile and half); the second tile of a split's last stage may be missing (not loaded: its
     // tokens are masked and its V rows zeroed by the softmax warps)
@@ -385,11 +407,21 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         if (s >= NV) tc_wait(smem_u32(&emptyv_bar[st]), ((s / NV) - 1) & 1, 2, s);
         load(&tmap_v, wv, sbase + (NK + st) * kTcSlotBytes, smem_u32(&fullv_bar[st]), s);
       };
-      if (n_st > 0) load_k(0);
-      if (n_st > 1) load_k(1);
-      for (int s = 0; s < n_st; ++s) {
-        load_v(s);
-        if (s + 2 < n_st) load_k(s + 2);
+      if (kTcSplitProducer) {
+        // one warp per ring: each blocks only on its own ring's free slots, so a V load is issued
+        // the moment PV(s - NV) frees its slot, not after the K wait that precedes it in the
+        // single-lane order below (which left V(s) landing ~0.25 us after P(s), traced)
+        if (warp == kTcProducerWarp)
+          for (int s = 0; s < n_st; ++s) load_k(s);
+        else
+          for (int s = 0; s < n_st; ++s) load_v(s);
+      } else {
+        if (n_st > 0) load_k(0);
+        if (n_st > 1) load_k(1);
+        for (int s = 0; s < n_st; ++s) {
+          load_v(s);
+          if (s + 2 < n_st) load_k(s + 2);
+        }
       }
     }
   } else if (warp == kTcMmaWarp) {
@@ -405,7 +437,9 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         const int st = s % NK, sb = s & 1;
         tc_wait(smem_u32(&fullk_bar[st]), (s / NK) & 1, 4, s);
         tc_fence_after();
+#ifndef DECATTN_TRACE_VWAIT
         TC_TRACE(48, s);
+#endif
         const uint32_t sK = sbase + st * kTcSlotBytes;
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {   // 16 dims per step: K half kk / 4, +32 B per step in the row
@@ -430,6 +464,9 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         tc_wait(smem_u32(&p_full[pb]), (s >> 1) & 1, 5, s);
         TC_TRACE(40, s);
         tc_wait(smem_u32(&fullv_bar[st]), (s / NV) & 1, 6, s);
+#ifdef DECATTN_TRACE_VWAIT
+        TC_TRACE(48, s);   // development: V(s) seen, before the fence (slot of "S start")
+#endif
         tc_fence_after();
         TC_TRACE(56, s);
         const uint32_t sV = sbase + (NK + st) * kTcSlotBytes;
@@ -590,10 +627,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
           const float pb0 = ex2(fmaf(sv[4 * g + 2], p.scale_log2, nB)), pb1 = ex2(fmaf(sv[4 * g + 3], p.scale_log2, nB));
           if (g8 & 1) sA1 += pa0 + pa1, sB1 += pb0 + pb1;
           else sA0 += pa0 + pa1, sB0 += pb0 + pb1;
-          hw[2 * g8] = pack_bf16(pa0, pa1);
-          hw[2 * g8 + 1] = pack_bf16(pb0, pb1);
-          lw[2 * g8] = pack_bf16(pa0 - bf16lo(hw[2 * g8]), pa1 - bf16hi(hw[2 * g8]));
-          lw[2 * g8 + 1] = pack_bf16(pb0 - bf16lo(hw[2 * g8 + 1]), pb1 - bf16hi(hw[2 * g8 + 1]));
+          tc_pair(pa0, pa1, hw[2 * g8], lw[2 * g8]);
+          tc_pair(pb0, pb1, hw[2 * g8 + 1], lw[2 * g8 + 1]);
         }
         tc_st16x128_x8(sp + 32 * h, hw);
         tc_st16x128_x8(sp + (16u << 16) + 32 * h, lw);

@@ -67,6 +67,9 @@ def trace(b, hq, hkv, lk, policy="seq_aware", forced=0, path=None):
 
 
 if __name__ == "__main__":
+    if len(sys.argv) > 1 and sys.argv[1] == "mqa":
+        trace(128, 64, 1, 8192)
+        sys.exit(0)
     trace(4, 64, 1, 8192, "guarded")
     trace(1, 64, 1, 4096, "seq_aware_sm", path=2)
     trace(128, 64, 1, 8192)
