@@ -311,6 +311,13 @@ def test_full_size_long_context_every_group(policy, s, mode):
     assert plan.num_splits == s and plan.combine_mode == mode
 
 
+def test_full_size_mqa_tcgen05_every_group():
+    # bench.py's mqa_g64 workload (B=128 H_Q=64 H_KV=1 L_K=8192, 512 MiB of KV) in the plan the bench
+    # times: the tcgen05 kernel, one 64-row CTA per sequence, s = 1
+    plan = _check_full(dict(batch=128, h_q=64, h_kv=1, l_k=8192), "seq_aware", 1006)
+    assert plan.num_splits == 1 and plan.path == 2
+
+
 def test_full_size_long_context_ragged_every_group():
     # ragged lengths at the long-context size: batch of 3 with 0 / 1 / random tokens
     cfg = dict(synth.CONFIGS["long_context"], batch=3)
