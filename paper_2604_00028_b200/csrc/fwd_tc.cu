@@ -59,10 +59,12 @@ constexpr int kTcSoftmaxWarps = DECATTN_TC_SMX_WARPS;
 constexpr int kTcHalvesPerWarp = 8 / kTcSoftmaxWarps;   // 64-token halves of a stage per softmax warp
 static_assert(kTcSoftmaxWarps == 4 || kTcSoftmaxWarps == 8, "one or two softmax warps per lane quadrant");
 constexpr bool kTcSplitProducer = DECATTN_TC_SPLIT_PRODUCER != 0;   // one TMA warp per ring
-constexpr int kTcThreads = (kTcSoftmaxWarps + 2 + (kTcSplitProducer ? 1 : 0)) * 32;   // + TMA warp(s) + MMA warp
+constexpr bool kTcSplitMma = DECATTN_TC_SPLIT_MMA != 0;             // S and PV issued by two warps
+constexpr int kTcThreads = (kTcSoftmaxWarps + 2 + (kTcSplitProducer ? 1 : 0) + (kTcSplitMma ? 1 : 0)) * 32;
 constexpr int kTcProducerWarp = kTcSoftmaxWarps;                          // K ring (and V without the split)
 constexpr int kTcProducerWarpV = kTcSplitProducer ? kTcSoftmaxWarps + 1 : kTcSoftmaxWarps;   // V ring
-constexpr int kTcMmaWarp = kTcProducerWarpV + 1;
+constexpr int kTcMmaWarp = kTcProducerWarpV + 1;                        // TMEM owner, S (and PV) issuer
+constexpr int kTcMmaWarpPV = kTcSplitMma ? kTcMmaWarp + 1 : kTcMmaWarp;  // PV issuer
 // TMEM columns (512 allocated): two S buffers (P is written over S once the softmax warps read it),
 // the O accumulator and Q (the S MMA's A operand, two bf16 per 32-bit column, row r on the
 // accumulator's lane).  The PV product runs at M = 128 with the P pair stacked along M: in warp
@@ -110,9 +112,31 @@ __device__ __forceinline__ void tc_trace(int slot_base, int i) {
   g_trace_tc[c * 64 + slot_base + k] = t;
 }
 #define TC_TRACE(base, i) tc_trace(base, i)
+// softmax-internal stamps of warp 0 / lane 0 in CTA 0, stages 16..23 (slot j: 0 S loaded, 1 maximum
+// exchanged, 2 P computed, 3 P stored)
+__device__ unsigned long long g_trace_smx[4 * 8];
+__device__ unsigned long long g_trace_pw[16 * 8];   // P stored, per softmax warp (lane 0), CTA 0, stages 16..23
+#define TC_TRACE_PW(s)                                                                              \
+  do {                                                                                              \
+    if (lane == 0 && blockIdx.x + blockIdx.y + blockIdx.z == 0 && (s) >= 16 && (s) < 24) {          \
+      unsigned long long t_;                                                                        \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                                        \
+      g_trace_pw[warp * 8 + (s) - 16] = t_;                                                         \
+    }                                                                                               \
+  } while (0)
+#define TC_TRACE_SMX(j, s)                                                                        \
+  do {                                                                                            \
+    if (threadIdx.x == 0 && blockIdx.x + blockIdx.y + blockIdx.z == 0 && (s) >= 16 && (s) < 24) { \
+      unsigned long long t_;                                                                      \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                                      \
+      g_trace_smx[(j) * 8 + (s) - 16] = t_;                                                       \
+    }                                                                                             \
+  } while (0)
 #else
 #define TC_TRACE(base, i) do { } while (0)
 #define TC_TRACE_CTA(slot) do { } while (0)
+#define TC_TRACE_SMX(j, s) do { } while (0)
+#define TC_TRACE_PW(s) do { } while (0)
 #endif
 
 // development watchdog (-DDECATTN_TC_WATCHDOG builds): a wait that has not completed after 2 s
@@ -424,13 +448,15 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         }
       }
     }
-  } else if (warp == kTcMmaWarp) {
-    // ================= MMA issuer (one lane) =================
+  } else if (warp == kTcMmaWarp || warp == kTcMmaWarpPV) {
+    // ================= MMA issuer(s) (one lane each) =================
     if (lane == 0 && n_st > 0) {
       constexpr uint32_t id_s = tc_idesc(kTcM, kTcT, 0, 0);             // S: M = 64, N = 128 tokens
       constexpr uint32_t id_o = tc_idesc(2 * kTcM, kHeadDim, 0, 1);     // O: [P_hi; P_lo] stacked along M
-      tc_wait(smem_u32(&q_bar), 0, 3, 0);
-      TC_TRACE_CTA(4);
+      if (warp == kTcMmaWarp) {
+        tc_wait(smem_u32(&q_bar), 0, 3, 0);
+        TC_TRACE_CTA(4);
+      }
       // S(s) = Q K(s)^T into TMEM buffer s & 1.  The buffer held P(s - 2), read by PV(s - 2), which
       // was issued before: the tensor pipe executes in issue order
       auto issue_s = [&](int s) {
@@ -479,13 +505,31 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         tc_commit(smem_u32(&emptyv_bar[st]));
         TC_TRACE(32, s);
       };
-      // two S stages ahead, then PV(s) and S(s + 2): the tensor pipe runs PV(s) and S(s + 2) while
-      // the softmax warps work on stage s + 1, whose S is already there
-      issue_s(0);
-      if (n_st > 1) issue_s(1);
-      for (int s = 0; s < n_st; ++s) {
-        issue_pv(s);
-        if (s + 2 < n_st) issue_s(s + 2);
+      if (kTcSplitMma) {
+        // two issuers: a thread blocks in tcgen05.mma while the pipe's queue is full, so one thread
+        // issuing S(s + 2) cannot queue PV(s + 1) the moment P(s + 1) is ready.  S(s + 2) reuses the
+        // buffer PV(s) reads, so the S issuer waits for PV(s) to complete (not only to be issued);
+        // each issuer's commits track its own MMAs
+        if (warp == kTcMmaWarp) {
+          for (int s = 0; s < n_st; ++s) {
+            if (s >= 2) {
+              tc_wait(smem_u32(&pv_done[s & 1]), ((s - 2) >> 1) & 1, 9, s);
+              tc_fence_after();
+            }
+            issue_s(s);
+          }
+        } else {
+          for (int s = 0; s < n_st; ++s) issue_pv(s);
+        }
+      } else {
+        // two S stages ahead, then PV(s) and S(s + 2): the tensor pipe runs PV(s) and S(s + 2) while
+        // the softmax warps work on stage s + 1, whose S is already there
+        issue_s(0);
+        if (n_st > 1) issue_s(1);
+        for (int s = 0; s < n_st; ++s) {
+          issue_pv(s);
+          if (s + 2 < n_st) issue_s(s + 2);
+        }
       }
     }
   } else {
@@ -545,6 +589,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 #pragma unroll
         for (int c = 0; c < 32; ++c) sv[32 * hi + c] = __uint_as_float(r0[c]);
       }
+      TC_TRACE_SMX(0, s);
       const int tok0 = 64 * hh * kTcHalvesPerWarp;       // first token of this warp's values
       if (valid < tok0 + NSV * 2) {                       // tokens past the range
 #pragma unroll
@@ -579,6 +624,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         xA = fmaxf(xA, red_x[sb][hh ^ 1][rA]);
         xB = fmaxf(xB, red_x[sb][hh ^ 1][rB]);
       }
+      TC_TRACE_SMX(1, s);
       const float mxA = xA * p.scale_log2, mxB = xB * p.scale_log2;   // >= 1 valid token: finite
       if (s == 0) mA = mxA, mB = mxB;                    // PV(0) starts O (accumulate = 0)
       // the reference moves only when this stage's maximum exceeds it by more than 2^8: then the
@@ -623,8 +669,13 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 #pragma unroll
         for (int g8 = 0; g8 < 8; ++g8) {
           const int g = 8 * hi + g8;
+#if DECATTN_TC_EXP_WHATIF   // development timing experiment only: no exponential (wrong results)
+          const float pa0 = fmaf(sv[4 * g], p.scale_log2, nA), pa1 = fmaf(sv[4 * g + 1], p.scale_log2, nA);
+          const float pb0 = fmaf(sv[4 * g + 2], p.scale_log2, nB), pb1 = fmaf(sv[4 * g + 3], p.scale_log2, nB);
+#else
           const float pa0 = ex2(fmaf(sv[4 * g], p.scale_log2, nA)), pa1 = ex2(fmaf(sv[4 * g + 1], p.scale_log2, nA));
           const float pb0 = ex2(fmaf(sv[4 * g + 2], p.scale_log2, nB)), pb1 = ex2(fmaf(sv[4 * g + 3], p.scale_log2, nB));
+#endif
           if (g8 & 1) sA1 += pa0 + pa1, sB1 += pb0 + pb1;
           else sA0 += pa0 + pa1, sB0 += pb0 + pb1;
           tc_pair(pa0, pa1, hw[2 * g8], lw[2 * g8]);
@@ -635,6 +686,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       }
       lA += sA0 + sA1;
       lB += sB0 + sB1;
+      TC_TRACE_SMX(2, s);
       if (valid < kTcT) {
         // V rows past the range may hold anything (stale or NaN): zero them (P = 0 there)
         const int st = s % NV;
@@ -647,6 +699,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         fence_proxy_async_smem();
       }
       tc_wait_st();
+      TC_TRACE_SMX(3, s);
+      TC_TRACE_PW(s);
       tc_fence_before();
       __syncwarp();
       if (threadIdx.x == 0) TC_TRACE(24, s);
@@ -782,6 +836,12 @@ cudaError_t forward_tc_residency(int* out) {
 extern "C" __attribute__((visibility("default"))) int da_trace_fetch_tc(unsigned long long* host, int n) {
   if (n > 64 * 64) n = 64 * 64;
   return cudaMemcpyFromSymbol(host, g_trace_tc, sizeof(unsigned long long) * n) == cudaSuccess ? 0 : 1;
+}
+extern "C" __attribute__((visibility("default"))) int da_trace_fetch_tc_smx(unsigned long long* host) {
+  return cudaMemcpyFromSymbol(host, g_trace_smx, sizeof(unsigned long long) * 4 * 8) == cudaSuccess ? 0 : 1;
+}
+extern "C" __attribute__((visibility("default"))) int da_trace_fetch_tc_pw(unsigned long long* host) {
+  return cudaMemcpyFromSymbol(host, g_trace_pw, sizeof(unsigned long long) * 16 * 8) == cudaSuccess ? 0 : 1;
 }
 extern "C" __attribute__((visibility("default"))) int da_trace_fetch_tc_cta(unsigned long long* host) {
   return cudaMemcpyFromSymbol(host, g_cta_tc, sizeof(unsigned long long) * 8 * 1024) == cudaSuccess ? 0 : 1;

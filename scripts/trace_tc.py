@@ -58,8 +58,28 @@ def trace(b, hq, hkv, lk, policy="seq_aware", forced=0, path=None):
               [(i, int(cb[2048 + i]), round((st[i] - t0) / 1e3, 2), round((en[i] - t0) / 1e3, 2)) for i in order[-6:]])
         print("  fastest CTAs (cta, sm, start, end):",
               [(i, int(cb[2048 + i]), round((st[i] - t0) / 1e3, 2), round((en[i] - t0) / 1e3, 2)) for i in order[:6]])
+    smx = None
+    if hasattr(L.LIB, "da_trace_fetch_tc_smx"):
+        L.LIB.da_trace_fetch_tc_smx.argtypes = [ctypes.c_void_p]
+        sb = (ctypes.c_ulonglong * 32)()
+        if L.LIB.da_trace_fetch_tc_smx(ctypes.addressof(sb)) == 0:
+            smx = sb
+    pw = None
+    if hasattr(L.LIB, "da_trace_fetch_tc_pw"):
+        L.LIB.da_trace_fetch_tc_pw.argtypes = [ctypes.c_void_p]
+        pb = (ctypes.c_ulonglong * 128)()
+        if L.LIB.da_trace_fetch_tc_pw(ctypes.addressof(pb)) == 0:
+            pw = pb
     for c in (0, 1):
         base = buf[c * 64 + 0]
+        if c == 0 and pw is not None:
+            for k in range(8):
+                print("  P stored per softmax warp, stage", 16 + k, [int(pw[w * 8 + k]) - base if pw[w * 8 + k] else None
+                                                                      for w in range(16)])
+        if c == 0 and smx is not None:
+            for k in range(8):
+                print("  softmax warp 0 stage", 16 + k, " ".join(
+                    f"{n}={int(smx[j * 8 + k]) - base}" for j, n in enumerate(("S_loaded", "max_done", "P_computed", "P_stored"))))
         print(f" cta{c}")
         for k in range(8):
             row = [int(buf[c * 64 + 8 * j + k]) - base if buf[c * 64 + 8 * j + k] else None for j in range(8)]
