@@ -20,7 +20,7 @@ def bytes_step(b, hq, hkv, lk):
 
 
 def bench(b, hq, hkv, lk, policy="seq_aware", forced=0, combine=None, steps=200, reps=5, pack=True,
-          rotate=True):
+          rotate=True, path=None):
     kvb = 4 * b * lk * hkv * 128
     nbuf = max(1, min(256, -(-2 * L2 // kvb))) if rotate else 1
     ins = [synth.make_inputs(b, hq, hkv, lk, device="cuda", seed=i) for i in range(min(nbuf, 2))]
@@ -28,7 +28,7 @@ def bench(b, hq, hkv, lk, policy="seq_aware", forced=0, combine=None, steps=200,
     vs = [ins[i % len(ins)]["v"].clone() for i in range(nbuf)]
     q, seq = ins[0]["q"], ins[0]["seqlens"]
     plan = dec.make_plan(b, hq, hkv, lk, pack_gqa=pack, policy=policy, forced_splits=forced,
-                         combine_mode=combine)
+                         combine_mode=combine, path=path)
     ws = dec.workspace_for(plan, q.device)
     out = torch.empty_like(q)
     lse = torch.empty(b, hq, device="cuda")
