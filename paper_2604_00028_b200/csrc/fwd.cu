@@ -356,7 +356,7 @@ __device__ __noinline__ int4 dyn_schedule(const FwdParams& p, uint32_t slot, boo
 // rows (MMA path); kCombine: da_combine_mode; NS: ring stages; NW: consumer warps
 // (NS a multiple of NW: warp w owns stages w, w + NW, ... and consumes them in order).
 // ---------------------------------------------------------------------------
-template <int kPath, int kNB, int kCombine, int NS, int NW, bool kDyn, int kPub>
+template <int kPath, int kNB, int kCombine, int NS, int NW, bool kDyn, int kPub, bool kBal>
 __global__ void __launch_bounds__(threads_for(NW, helpers_for(kCombine)), 1)
     split_kv_fwd_kernel(const __grid_constant__ CUtensorMap tmap_k,
                         const __grid_constant__ CUtensorMap tmap_v, const FwdParams p) {
@@ -374,7 +374,9 @@ __global__ void __launch_bounds__(threads_for(NW, helpers_for(kCombine)), 1)
   // tail balancing (cluster plans with long splits): the tile each ring stage holds, written by the
   // producer before it arms the stage (-1: no more tiles for the warp that owns the stage), and the
   // cluster's ticket counter for the pooled tail chunks (rank 0's copy is the one used)
-  constexpr bool kBalCapable = kCluster && !kDyn && kPub == 0;
+  // (a separate instantiation, kBal: launched only when some sequence can be long enough, so the
+  // latency-regime cluster plans run without the balancing code - it cost them 5 %)
+  constexpr bool kBalCapable = kCluster && !kDyn && kPub == 0 && kBal;
   __shared__ int stage_tile[kBalCapable ? NS : 1];
   __shared__ uint32_t bal_next;
 
@@ -958,7 +960,7 @@ __global__ void __launch_bounds__(threads_for(NW, helpers_for(kCombine)), 1)
 
 // The kernel instantiation a plan launches, its shared memory and block size, with the one-time
 // (per device) opt-in to > 48 KB of dynamic shared memory and to non-portable cluster sizes.
-template <int kPath, int kNB, int kCombine, bool kDyn = false, int kPub = 0>
+template <int kPath, int kNB, int kCombine, bool kDyn = false, int kPub = 0, bool kBal = false>
 struct FwdKernel {
   static constexpr bool kCluster = kCombine == DA_COMBINE_CLUSTER;
   // dynamic split counts: mostly one split per sequence, so the streaming (s = 1) configuration
@@ -966,7 +968,7 @@ struct FwdKernel {
   static constexpr int NW = kDyn ? kWarpsNone : warps_for(kCombine);
   static constexpr int kSmem = smem_for(NS, kCluster);
   static constexpr int kThreads = threads_for(NW, helpers_for(kCombine));
-  static constexpr auto kern = split_kv_fwd_kernel<kPath, kNB, kCombine, NS, NW, kDyn, kPub>;
+  static constexpr auto kern = split_kv_fwd_kernel<kPath, kNB, kCombine, NS, NW, kDyn, kPub, kBal>;
 
   static cudaError_t prepare() {
     static std::atomic<uint64_t> attr_done{0};
@@ -1039,10 +1041,17 @@ struct FwdKernel {
   }
 };
 
-template <int kPath, int kNB, int kCombine, bool kDyn = false, int kPub = 0>
+template <int kPath, int kNB, int kCombine, bool kDyn = false, int kPub = 0, bool kBal = false>
 cudaError_t launch_impl(const da_plan& plan, const CUtensorMap& tk, const CUtensorMap& tv,
                         const FwdParams& p, cudaStream_t stream) {
-  return FwdKernel<kPath, kNB, kCombine, kDyn, kPub>::launch(plan, tk, tv, p, stream);
+  return FwdKernel<kPath, kNB, kCombine, kDyn, kPub, kBal>::launch(plan, tk, tv, p, stream);
+}
+
+// Tail balancing can engage in a cluster plan only when a sequence may span >= kBalMinTiles tiles
+// per split (dense cache): the cache capacity bounds every length
+inline bool balancing_possible(const da_plan& plan, const FwdParams& p) {
+  return p.block_table == nullptr &&
+         (static_cast<int64_t>(p.l_cap) + kTileN - 1) / kTileN >= static_cast<int64_t>(kBalMinTiles) * plan.num_splits;
 }
 
 template <int kPath, int kNB>
@@ -1080,6 +1089,7 @@ cudaError_t dispatch_combine(const da_plan& plan, const CUtensorMap& tk, const C
     case DA_COMBINE_CLUSTER:
       if (pub == 2) return launch_impl<kPath, kNB, DA_COMBINE_CLUSTER, false, 2>(plan, tk, tv, p, stream);
       if (pub == 1) return launch_impl<kPath, kNB, DA_COMBINE_CLUSTER, false, 1>(plan, tk, tv, p, stream);
+      if (balancing_possible(plan, p)) return launch_impl<kPath, kNB, DA_COMBINE_CLUSTER, false, 0, true>(plan, tk, tv, p, stream);
       return launch_impl<kPath, kNB, DA_COMBINE_CLUSTER>(plan, tk, tv, p, stream);
     default:
       if (is_dynamic(plan)) {   // s_b = 1 rows are final rows written by the forward
