@@ -356,7 +356,7 @@ __device__ __noinline__ int4 dyn_schedule(const FwdParams& p, uint32_t slot, boo
 // rows (MMA path); kCombine: da_combine_mode; NS: ring stages; NW: consumer warps
 // (NS a multiple of NW: warp w owns stages w, w + NW, ... and consumes them in order).
 // ---------------------------------------------------------------------------
-template <int kPath, int kNB, int kCombine, int NS, int NW, bool kDyn, int kPub, bool kBal>
+template <int kPath, int kNB, int kCombine, int NS, int NW, bool kDyn, int kPub, bool kBal, bool kPaged>
 __global__ void __launch_bounds__(threads_for(NW, helpers_for(kCombine)), 1)
     split_kv_fwd_kernel(const __grid_constant__ CUtensorMap tmap_k,
                         const __grid_constant__ CUtensorMap tmap_v, const FwdParams p) {
@@ -472,7 +472,7 @@ __global__ void __launch_bounds__(threads_for(NW, helpers_for(kCombine)), 1)
     // read here only steer L2 prefetches of the pages the ring loads first (a stale or torn entry
     // costs a useless prefetch; out-of-range pages are clipped by the tensor map); the producer
     // re-reads the table after the wait for the loads themselves
-    if (p.block_table != nullptr && warp == NW && lane == 0 && n_tiles >= 1 && n_tiles <= 2 * NS) {
+    if (kPaged && warp == NW && lane == 0 && n_tiles >= 1 && n_tiles <= 2 * NS) {
       const int32_t* bt = p.block_table + static_cast<int64_t>(b) * p.bt_stride;
       const uint32_t tpp = static_cast<uint32_t>(p.page_size / kTileN);
       const uint32_t tile0 = static_cast<uint32_t>(t0 / kTileN);
@@ -491,7 +491,7 @@ __global__ void __launch_bounds__(threads_for(NW, helpers_for(kCombine)), 1)
     // kernels).  A wrong guess only costs DRAM reads.
     if (DECATTN_SPECULATE || p.seqlens == nullptr) {
       if (warp == NW && lane == 0 && n_tiles >= 1 && (DECATTN_PREFETCH_LONG || n_tiles <= 2 * NS) &&
-          p.block_table == nullptr) {
+          !kPaged) {
         const int np = min(n_tiles, NS);
         for (int i = 0; i < np; ++i) tma_prefetch_5d(&tmap_k, 0, t0 + i * kTileN, 0, kvh, bkv);
         for (int i = 0; i < np; ++i) tma_prefetch_5d(&tmap_v, 0, t0 + i * kTileN, 0, kvh, bkv);
@@ -542,7 +542,7 @@ __global__ void __launch_bounds__(threads_for(NW, helpers_for(kCombine)), 1)
   if constexpr (kBalCapable) {
     n_seq = min(max(p.seqlens != nullptr ? (max(__ldg(p.seqlens + bkv), 0) - p.seq_offset) : p.l_default, 0), p.l_cap);
     const int nu = (n_seq + kTileN - 1) / kTileN;
-    bal = p.block_table == nullptr && nu >= kBalMinTiles * p.num_splits;
+    bal = !kPaged && nu >= kBalMinTiles * p.num_splits;
     tail_chunks = nu / p.num_splits / kBalTailDiv / kBalChunk;   // pooled chunks per split (>= 2)
   }
 
@@ -594,7 +594,7 @@ __global__ void __launch_bounds__(threads_for(NW, helpers_for(kCombine)), 1)
           mbar_arrive(smem_u32(&full_bar[st]));
           ++i;
         }
-      } else if (p.block_table == nullptr && n_tiles <= NS) {
+      } else if (!kPaged && n_tiles <= NS) {
         // latency regime (every tile has its own stage): all K boxes first, then all V boxes, so
         // every consumer starts QK^T one V box earlier than in tile order
         for (int i = 0; i < n_tiles; ++i) {
@@ -608,7 +608,7 @@ __global__ void __launch_bounds__(threads_for(NW, helpers_for(kCombine)), 1)
           mbar_arrive_expect_tx(fvb, kStageBytes / 2);
           tma_load_5d(sbase + i * kStageBytes + 2 * kHalfBytes, &tmap_v, fvb, 0, t0 + i * kTileN, 0, kvh, bkv);
         }
-      } else if (p.block_table == nullptr) {
+      } else if (!kPaged) {
         for (int i = 0; i < n_tiles; ++i) {
           const int st = i % NS;
           if (i >= NS) mbar_wait(smem_u32(&empty_bar[st]), ((i / NS) - 1) & 1);
@@ -960,7 +960,7 @@ __global__ void __launch_bounds__(threads_for(NW, helpers_for(kCombine)), 1)
 
 // The kernel instantiation a plan launches, its shared memory and block size, with the one-time
 // (per device) opt-in to > 48 KB of dynamic shared memory and to non-portable cluster sizes.
-template <int kPath, int kNB, int kCombine, bool kDyn = false, int kPub = 0, bool kBal = false>
+template <int kPath, int kNB, int kCombine, bool kDyn = false, int kPub = 0, bool kBal = false, bool kPaged = false>
 struct FwdKernel {
   static constexpr bool kCluster = kCombine == DA_COMBINE_CLUSTER;
   // dynamic split counts: mostly one split per sequence, so the streaming (s = 1) configuration
@@ -968,7 +968,7 @@ struct FwdKernel {
   static constexpr int NW = kDyn ? kWarpsNone : warps_for(kCombine);
   static constexpr int kSmem = smem_for(NS, kCluster);
   static constexpr int kThreads = threads_for(NW, helpers_for(kCombine));
-  static constexpr auto kern = split_kv_fwd_kernel<kPath, kNB, kCombine, NS, NW, kDyn, kPub, kBal>;
+  static constexpr auto kern = split_kv_fwd_kernel<kPath, kNB, kCombine, NS, NW, kDyn, kPub, kBal, kPaged>;
 
   static cudaError_t prepare() {
     static std::atomic<uint64_t> attr_done{0};
@@ -1044,7 +1044,11 @@ struct FwdKernel {
 template <int kPath, int kNB, int kCombine, bool kDyn = false, int kPub = 0, bool kBal = false>
 cudaError_t launch_impl(const da_plan& plan, const CUtensorMap& tk, const CUtensorMap& tv,
                         const FwdParams& p, cudaStream_t stream) {
-  return FwdKernel<kPath, kNB, kCombine, kDyn, kPub, kBal>::launch(plan, tk, tv, p, stream);
+  // paged and dense caches run separate instantiations (kPaged): the page walk's code stays out of
+  // the dense kernels, whose latency-bound launches pay for every instruction they fetch
+  if (p.block_table != nullptr)
+    return FwdKernel<kPath, kNB, kCombine, kDyn, kPub, false, true>::launch(plan, tk, tv, p, stream);
+  return FwdKernel<kPath, kNB, kCombine, kDyn, kPub, kBal, false>::launch(plan, tk, tv, p, stream);
 }
 
 // Tail balancing can engage in a cluster plan only when a sequence may span >= kBalMinTiles tiles
