@@ -15,7 +15,11 @@ run() {   # name, command
       > $OUT/ncu_full_$name.log 2>&1 && \
     ncu -i $OUT/full_$name.ncu-rep --page raw --csv > $OUT/raw_$name.csv 2>/dev/null && \
     ncu -i $OUT/full_$name.ncu-rep --page details > $OUT/details_$name.txt 2>/dev/null
-  echo "$name rc=$?"
+  local rc=$?
+  # the exported pages are what is kept; the report itself only with KEEP_REP=1 (gpurun copies
+  # back at most 64 MiB of gpurun_out/)
+  [ "${KEEP_REP:-0}" = "1" ] || rm -f $OUT/full_$name.ncu-rep
+  echo "$name rc=$rc"
 }
 # the headline (bench.py defaults: high_load, seq_aware_sm = s 1), the latency configs, and both
 # long-context plans the bench's roofline_streaming times (the paper's rule s = 16 workspace, C-ext-1 s = 10)
