@@ -226,6 +226,7 @@ da_status forward_impl(const da_plan* plan, const void* q, const void* k_cache, 
   p.h_q = plan->h_q;
   p.batch = plan->batch;
   p.mblocks_per_head = plan->path != DA_PATH_SCALAR ? (p.G + plan->rows_per_cta - 1) / plan->rows_per_cta : 1;
+  p.mb_magic = div_magic(static_cast<uint32_t>(p.mblocks_per_head));
   const float scale = softmax_scale > 0.f ? softmax_scale : 1.0f / std::sqrt(float(D));
   p.scale_log2 = scale * 1.4426950408889634f;
   p.out = out;

@@ -132,7 +132,7 @@ __global__ void __launch_bounds__(kCombineThreads)
       sum.w = fmaf(c, a.w, sum.w);
     }
   }
-  const float inv = L > 0.f ? __frcp_rn(L) : 0.f;
+  const float inv = L > 0.f ? ptx::rcp(L) : 0.f;
   sum = make_float4(sum.x * inv, sum.y * inv, sum.z * inv, sum.w * inv);
   const float lse = empty ? kNegInf : (M + lg2(L)) * (1.f / kLog2e);
   if (p.pub.out != nullptr) {
@@ -272,7 +272,7 @@ __global__ void __launch_bounds__(kCombineThreads)
       sum = make_float4(fmaf(c, a.x, sum.x), fmaf(c, a.y, sum.y), fmaf(c, a.z, sum.z), fmaf(c, a.w, sum.w));
     }
   }
-  const float inv = L > 0.f ? __frcp_rn(L) : 0.f;
+  const float inv = L > 0.f ? ptx::rcp(L) : 0.f;
   sum = make_float4(sum.x * inv, sum.y * inv, sum.z * inv, sum.w * inv);
   DA_DASSERT(row < rows);
   if (out_f32) {

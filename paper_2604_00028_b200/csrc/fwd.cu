@@ -409,7 +409,7 @@ __global__ void __launch_bounds__(threads_for(NW, helpers_for(kCombine)), 1)
   bool dyn_single = false;                       // kDyn: this sequence has one split (s_b = 1)
   int kvh, hq0, rows_valid;
   if constexpr (kPath == DA_PATH_MMA) {
-    kvh = grp / p.mblocks_per_head;
+    kvh = static_cast<int>(udiv_magic(static_cast<uint32_t>(grp), p.mb_magic));
     const int rg = grp - kvh * p.mblocks_per_head;
     hq0 = kvh * p.G + rg * R;
     rows_valid = min(R, p.G - rg * R);
@@ -837,7 +837,7 @@ __global__ void __launch_bounds__(threads_for(NW, helpers_for(kCombine)), 1)
       const int e = threadIdx.x + it * kT;
       const int g = e >> 5, d4 = e & 31;
       if (e >= R * 32 || g >= rows_valid) continue;
-      const float inv = eL[it] > 0.f ? __frcp_rn(eL[it]) : 0.f;
+      const float inv = eL[it] > 0.f ? rcp(eL[it]) : 0.f;
       const float4 v = make_float4(eO[it].x * inv, eO[it].y * inv, eO[it].z * inv, eO[it].w * inv);
       const float lse_v = eL[it] > 0.f ? (eM[it] + lg2(eL[it])) * kLn2 : kNegInf;
       const size_t row = static_cast<size_t>(b) * p.h_q + hq0 + g;
@@ -915,7 +915,7 @@ __global__ void __launch_bounds__(threads_for(NW, helpers_for(kCombine)), 1)
         }
       }
       if (t == 0) TRACE(45);
-      const float inv = Lsum > 0.f ? __frcp_rn(Lsum) : 0.f;
+      const float inv = Lsum > 0.f ? rcp(Lsum) : 0.f;
       const size_t row = static_cast<size_t>(b) * p.h_q + hq0 + g;
       if constexpr (kPub == 2) {
         pub_ll_store(pub_rank_view(p.pub, erank, static_cast<size_t>(p.batch) * p.h_q), e_pub, row, d4,

@@ -323,7 +323,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   const int grp = blockIdx.y, split = blockIdx.x, b = blockIdx.z;
-  const int kvh = grp / p.mblocks_per_head;
+  const int kvh = static_cast<int>(udiv_magic(static_cast<uint32_t>(grp), p.mb_magic));
   const int rg = grp - kvh * p.mblocks_per_head;
   const int hq0 = kvh * p.G + rg * kTcM;
   const int rows_valid = min(kTcM, p.G - rg * kTcM);
@@ -722,8 +722,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       mbar_wait(smem_u32(&pv_done[(n_st - 1) & 1]), ((n_st - 1) >> 1) & 1);
       if (threadIdx.x == 0) TC_TRACE_CTA(6);
       tc_fence_after();
-      invA = lA > 0.f ? __frcp_rn(lA) : 0.f;
-      invB = lB > 0.f ? __frcp_rn(lB) : 0.f;
+      invA = lA > 0.f ? rcp(lA) : 0.f;
+      invB = lB > 0.f ? rcp(lB) : 0.f;
       lseA = lA > 0.f ? (mA + lg2(lA)) * kLn2 : kNegInf;
       lseB = lB > 0.f ? (mB + lg2(lB)) * kLn2 : kNegInf;
     }

@@ -52,6 +52,7 @@ struct FwdParams {
   int32_t h_q;
   int32_t batch;
   int32_t mblocks_per_head; // MMA path: ceil(G / rows_per_cta); SCALAR: 1
+  uint64_t mb_magic;        // ceil(2^38 / mblocks_per_head) (udiv_magic: no integer divide on the device)
   float scale_log2;         // softmax_scale * log2(e)
   void* out;                // [B, H_Q, d] bf16 or f32
   int32_t out_f32;

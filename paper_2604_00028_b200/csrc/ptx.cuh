@@ -209,6 +209,14 @@ __device__ __forceinline__ float ex2(float x) {
   asm("ex2.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+// 1 / x by MUFU.RCP (<= 1 ulp): the normalisers here are >= 1 (the row's maximum contributes
+// exp2(0)), so the IEEE reciprocal's ~60-instruction special-case path (__frcp_rn) would only cost
+// instruction-cache space in the latency-bound kernels
+__device__ __forceinline__ float rcp(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
 __device__ __forceinline__ float lg2(float x) {
   float y;
   asm("lg2.approx.f32 %0, %1;" : "=f"(y) : "f"(x));

@@ -112,7 +112,7 @@ static __device__ __forceinline__ void pub_ll_merge_row(const PubParams& pb, uin
                       fmaf(acc.w, r, wt * oi.w));
     m = mb;
   }
-  const float inv = L > 0.f ? __frcp_rn(L) : 0.f;
+  const float inv = L > 0.f ? ptx::rcp(L) : 0.f;
   const float4 v = make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
   if (pb.out_f32) {
     reinterpret_cast<float4*>(pb.out)[row * 32 + d4] = v;
