@@ -430,7 +430,7 @@ __global__ void __launch_bounds__(threads_for(NW, helpers_for(kCombine)), 1)
   if (threadIdx.x == 0 && trace_cta() < 64) g_trace[trace_cta() * 64 + 60] = clock64();
 #endif
   if (threadIdx.x == 0) {
-#pragma unroll
+#pragma unroll 1
     for (int i = 0; i < NS; ++i) {
       mbar_init(smem_u32(&full_bar[i]), 1);
       mbar_init(smem_u32(&fullv_bar[i]), 1);
@@ -493,7 +493,11 @@ __global__ void __launch_bounds__(threads_for(NW, helpers_for(kCombine)), 1)
       if (warp == NW && lane == 0 && n_tiles >= 1 && (DECATTN_PREFETCH_LONG || n_tiles <= 2 * NS) &&
           !kPaged) {
         const int np = min(n_tiles, NS);
+        // (single-thread issue loops stay rolled here and below: the latency-bound launches pay
+        // for every instruction they fetch)
+#pragma unroll 1
         for (int i = 0; i < np; ++i) tma_prefetch_5d(&tmap_k, 0, t0 + i * kTileN, 0, kvh, bkv);
+#pragma unroll 1
         for (int i = 0; i < np; ++i) tma_prefetch_5d(&tmap_v, 0, t0 + i * kTileN, 0, kvh, bkv);
       }
     }
@@ -597,18 +601,21 @@ __global__ void __launch_bounds__(threads_for(NW, helpers_for(kCombine)), 1)
       } else if (!kPaged && n_tiles <= NS) {
         // latency regime (every tile has its own stage): all K boxes first, then all V boxes, so
         // every consumer starts QK^T one V box earlier than in tile order
+#pragma unroll 1
         for (int i = 0; i < n_tiles; ++i) {
           const uint32_t fb = smem_u32(&full_bar[i]);
           mbar_arrive_expect_tx(fb, kStageBytes / 2);
           tma_load_5d(sbase + i * kStageBytes, &tmap_k, fb, 0, t0 + i * kTileN, 0, kvh, bkv);
           if (i < 8) TRACE(2 + i);
         }
+#pragma unroll 1
         for (int i = 0; i < n_tiles; ++i) {
           const uint32_t fvb = smem_u32(&fullv_bar[i]);
           mbar_arrive_expect_tx(fvb, kStageBytes / 2);
           tma_load_5d(sbase + i * kStageBytes + 2 * kHalfBytes, &tmap_v, fvb, 0, t0 + i * kTileN, 0, kvh, bkv);
         }
       } else if (!kPaged) {
+#pragma unroll 1
         for (int i = 0; i < n_tiles; ++i) {
           const int st = i % NS;
           if (i >= NS) mbar_wait(smem_u32(&empty_bar[st]), ((i / NS) - 1) & 1);

@@ -20,7 +20,19 @@ bench(1, 8, 1, 512, 'guarded', steps=200, reps=7)
 bench(1, 64, 8, 512, 'guarded', steps=200, reps=7)
 """
 
+STREAM = """
+import sys
+sys.path.insert(0, 'scripts')
+from probe_timing import bench
+bench(128, 64, 8, 8192, 'seq_aware', steps=5, reps=5)
+bench(1, 64, 8, 131072, 'seq_aware_sm', steps=20, reps=7)
+bench(1, 64, 8, 131072, 'seq_aware', steps=20, reps=7)
+bench(4, 32, 4, 65536, 'seq_aware', steps=20, reps=7)
+"""
+
 if __name__ == "__main__":
+    if os.environ.get("AB_SET") == "stream":
+        CODE = STREAM
     trees = [ROOT] + [os.path.join(ROOT, t) for t in sys.argv[1:]]
     env = dict(os.environ)
     env.pop("DECATTN_LIB", None)
