@@ -30,9 +30,20 @@ bench(1, 64, 8, 131072, 'seq_aware', steps=20, reps=7)
 bench(4, 32, 4, 65536, 'seq_aware', steps=20, reps=7)
 """
 
+MQA = """
+import sys
+sys.path.insert(0, 'scripts')
+from probe_timing import bench
+for shp in ((4, 64, 1, 8192), (8, 64, 1, 4096), (2, 64, 1, 32768), (16, 64, 1, 2048), (32, 64, 1, 1024), (64, 64, 1, 2048)):
+    bench(*shp, 'guarded', steps=50, reps=5)
+bench(128, 64, 1, 8192, 'seq_aware', steps=10, reps=5)
+"""
+
 if __name__ == "__main__":
     if os.environ.get("AB_SET") == "stream":
         CODE = STREAM
+    if os.environ.get("AB_SET") == "mqa":
+        CODE = MQA
     trees = [ROOT] + [os.path.join(ROOT, t) for t in sys.argv[1:]]
     env = dict(os.environ)
     env.pop("DECATTN_LIB", None)
