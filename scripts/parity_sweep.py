@@ -2,7 +2,8 @@
 tests/test_gpu_parity.py): random (B, H_KV, G, L_K, policy, combine, variant, pack_gqa, paged,
 sequence-shard offset) draws, every output element and lse checked with the test tolerances
 (DESIGN.md C-amb-14).  Round 2 adds long lengths (tail-balanced cluster splits), explicit combine
-modes and da_plan_set_seq_offset shards (whole-sequence lengths in, the shard's part attended).
+modes and da_plan_set_seq_offset shards (whole-sequence lengths in, the shard's part attended),
+and plans forced onto the tcgen05 kernel.
 
     python scripts/parity_sweep.py [n_cases] [seed]
 """
@@ -41,8 +42,11 @@ if __name__ == "__main__":
             if policy == "fixed" and forced > 1 and rng.random() < 0.5:
                 comb = 1 if forced <= 16 and rng.random() < 0.6 else 2
             offset = rng.choice([0, 0, 0, 64, 1000, 77777])
+            # the tcgen05 kernel forced on a fifth of the packed static plans (any G >= 2; the
+            # planner alone picks it only for wide groups on long enough splits)
+            path = 2 if (pack and G >= 2 and policy != "dynamic" and comb != 1 and rng.random() < 0.2) else None
             plan = dec.make_plan(b, G * hkv, hkv, lk, pack_gqa=pack, policy=policy, forced_splits=forced,
-                                 combine_mode=comb, seq_offset=offset)
+                                 combine_mode=comb, seq_offset=offset, path=path)
             seq_arg = inp["seqlens"]
             if offset:                # a shard: whole-sequence lengths in; some end before the shard
                 seq_arg = inp["seqlens"] + offset
@@ -72,5 +76,5 @@ if __name__ == "__main__":
         except Exception as e:   # noqa: BLE001 - report and continue the sweep
             fails += 1
             print(f"FAIL case {i}: B={b} H_KV={hkv} G={G} L={lk} cap={l_cap} {policy} s={forced} {variant} "
-                  f"pack={pack} comb={comb} offset={offset}: {e}", flush=True)
+                  f"pack={pack} comb={comb} offset={offset} path={plan.path if 'plan' in dir() else '?'}: {e}", flush=True)
     print(f"{n} cases, {fails} failures", flush=True)
