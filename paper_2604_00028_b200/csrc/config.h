@@ -112,20 +112,7 @@ constexpr int kTcRows = 64;
 #ifndef DECATTN_TC_SMX_WARPS
 #define DECATTN_TC_SMX_WARPS 8    // softmax warps: 4 (one per TMEM lane quadrant) or 8 (two, token halves)
 #endif
-#ifndef DECATTN_TC_EXP_WHATIF
-#define DECATTN_TC_EXP_WHATIF 0   // development timing experiment (fwd_tc.cu); never 1 in a product build
-#endif
-#ifndef DECATTN_TC_PAIR
-#define DECATTN_TC_PAIR 0          // P_hi / P_lo conversion in the tcgen05 softmax (fwd_tc.cu tc_pair)
-#endif
-#ifndef DECATTN_TC_SPLIT_PRODUCER
-#define DECATTN_TC_SPLIT_PRODUCER 0   // 1: one TMA warp per ring (K, V); measured 1-5 % slower
-#endif
-#ifndef DECATTN_TC_SPLIT_MMA
-#define DECATTN_TC_SPLIT_MMA 0        // 1: S and PV MMAs issued by two warps
-#endif
-constexpr int kTcThreadsCfg =
-    (DECATTN_TC_SMX_WARPS + 2 + (DECATTN_TC_SPLIT_PRODUCER ? 1 : 0) + (DECATTN_TC_SPLIT_MMA ? 1 : 0)) * 32;
+constexpr int kTcThreadsCfg = (DECATTN_TC_SMX_WARPS + 2) * 32;
 constexpr int kTcSmemCfg = (DECATTN_TC_KSLOTS + DECATTN_TC_VSLOTS) * kStageBytes + 1024;   // 128-token stages; Q, S, P, O in TMEM
 #ifndef DECATTN_L2_PROMOTION
 #define DECATTN_L2_PROMOTION 3    // CU_TENSOR_MAP_L2_PROMOTION_L2_256B for the K / V tensor maps

@@ -58,13 +58,8 @@ constexpr int kTcVSlots = DECATTN_TC_VSLOTS;     // V ring (released when PV(s) 
 constexpr int kTcSoftmaxWarps = DECATTN_TC_SMX_WARPS;
 constexpr int kTcHalvesPerWarp = 8 / kTcSoftmaxWarps;   // 64-token halves of a stage per softmax warp
 static_assert(kTcSoftmaxWarps == 4 || kTcSoftmaxWarps == 8, "one or two softmax warps per lane quadrant");
-constexpr bool kTcSplitProducer = DECATTN_TC_SPLIT_PRODUCER != 0;   // one TMA warp per ring
-constexpr bool kTcSplitMma = DECATTN_TC_SPLIT_MMA != 0;             // S and PV issued by two warps
-constexpr int kTcThreads = (kTcSoftmaxWarps + 2 + (kTcSplitProducer ? 1 : 0) + (kTcSplitMma ? 1 : 0)) * 32;
-constexpr int kTcProducerWarp = kTcSoftmaxWarps;                          // K ring (and V without the split)
-constexpr int kTcProducerWarpV = kTcSplitProducer ? kTcSoftmaxWarps + 1 : kTcSoftmaxWarps;   // V ring
-constexpr int kTcMmaWarp = kTcProducerWarpV + 1;                        // TMEM owner, S (and PV) issuer
-constexpr int kTcMmaWarpPV = kTcSplitMma ? kTcMmaWarp + 1 : kTcMmaWarp;  // PV issuer
+constexpr int kTcThreads = (kTcSoftmaxWarps + 2) * 32;   // + TMA producer warp + MMA warp
+constexpr int kTcProducerWarp = kTcSoftmaxWarps, kTcMmaWarp = kTcSoftmaxWarps + 1;
 // TMEM columns (512 allocated): two S buffers (P is written over S once the softmax warps read it),
 // the O accumulator and Q (the S MMA's A operand, two bf16 per 32-bit column, row r on the
 // accumulator's lane).  The PV product runs at M = 128 with the P pair stacked along M: in warp
@@ -276,23 +271,11 @@ __device__ __forceinline__ void tc_st16x128_x8(uint32_t taddr, const uint32_t (&
 __device__ __forceinline__ void tc_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void tc_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
-// P = P_hi + P_lo for two values (x0 in the low half of each word).  DECATTN_TC_PAIR 0: both
-// rounded to nearest (cvt, the XU pipe); 1: P_hi = the top 16 bits of P (exact truncation, one
-// byte permute on the ALU), P_lo rounded; 2: both truncated (|error| < 2^-14 P, one-sided)
+// P = P_hi + P_lo for two values (x0 in the low half of each word), both rounded to nearest.
+// (Exact truncation by byte permutes instead of cvt measured no faster.)
 __device__ __forceinline__ void tc_pair(float x0, float x1, uint32_t& hw, uint32_t& lw) {
-#if DECATTN_TC_PAIR == 0
   hw = pack_bf16(x0, x1);
   lw = pack_bf16(x0 - bf16lo(hw), x1 - bf16hi(hw));
-#else
-  const uint32_t u0 = __float_as_uint(x0), u1 = __float_as_uint(x1);
-  hw = __byte_perm(u0, u1, 0x7632);
-  const float r0 = x0 - __uint_as_float(u0 & 0xffff0000u), r1 = x1 - __uint_as_float(u1 & 0xffff0000u);
-#if DECATTN_TC_PAIR == 1
-  lw = pack_bf16(r0, r1);
-#else
-  lw = __byte_perm(__float_as_uint(r0), __float_as_uint(r1), 0x7632);
-#endif
-#endif
 }
 
 // byte offset of 16-byte chunk c (8 bf16) of row r in a 128B-swizzled box of 128-byte rows
@@ -388,8 +371,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   const int n_st = (n_tiles + 1) >> 1;                 // 128-token stages
   if (threadIdx.x == 0) TC_TRACE_CTA(0);
 
-  if (warp == kTcProducerWarp || warp == kTcProducerWarpV) {
-    // ================= TMA producer(s) (dense or paged cache) =================
+  if (warp == kTcProducerWarp) {
+    // ================= TMA producer (dense or paged cache) =================
     // a stage holds K then V of two 64-token tiles as [half][128 tokens][64 dims] (one 8 KB box per
     // tile and half); the second tile of a split's last stage may be missing (not loaded: its
     // tokens are masked and its V rows zeroed by the softmax warps)
@@ -431,32 +414,20 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         if (s >= NV) tc_wait(smem_u32(&emptyv_bar[st]), ((s / NV) - 1) & 1, 2, s);
         load(&tmap_v, wv, sbase + (NK + st) * kTcSlotBytes, smem_u32(&fullv_bar[st]), s);
       };
-      if (kTcSplitProducer) {
-        // one warp per ring: each blocks only on its own ring's free slots, so a V load is issued
-        // the moment PV(s - NV) frees its slot, not after the K wait that precedes it in the
-        // single-lane order below (which left V(s) landing ~0.25 us after P(s), traced)
-        if (warp == kTcProducerWarp)
-          for (int s = 0; s < n_st; ++s) load_k(s);
-        else
-          for (int s = 0; s < n_st; ++s) load_v(s);
-      } else {
-        if (n_st > 0) load_k(0);
-        if (n_st > 1) load_k(1);
-        for (int s = 0; s < n_st; ++s) {
-          load_v(s);
-          if (s + 2 < n_st) load_k(s + 2);
-        }
+      if (n_st > 0) load_k(0);
+      if (n_st > 1) load_k(1);
+      for (int s = 0; s < n_st; ++s) {
+        load_v(s);
+        if (s + 2 < n_st) load_k(s + 2);
       }
     }
-  } else if (warp == kTcMmaWarp || warp == kTcMmaWarpPV) {
-    // ================= MMA issuer(s) (one lane each) =================
+  } else if (warp == kTcMmaWarp) {
+    // ================= MMA issuer (one lane) =================
     if (lane == 0 && n_st > 0) {
       constexpr uint32_t id_s = tc_idesc(kTcM, kTcT, 0, 0);             // S: M = 64, N = 128 tokens
       constexpr uint32_t id_o = tc_idesc(2 * kTcM, kHeadDim, 0, 1);     // O: [P_hi; P_lo] stacked along M
-      if (warp == kTcMmaWarp) {
-        tc_wait(smem_u32(&q_bar), 0, 3, 0);
-        TC_TRACE_CTA(4);
-      }
+      tc_wait(smem_u32(&q_bar), 0, 3, 0);
+      TC_TRACE_CTA(4);
       // S(s) = Q K(s)^T into TMEM buffer s & 1.  The buffer held P(s - 2), read by PV(s - 2), which
       // was issued before: the tensor pipe executes in issue order
       auto issue_s = [&](int s) {
@@ -505,31 +476,13 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         tc_commit(smem_u32(&emptyv_bar[st]));
         TC_TRACE(32, s);
       };
-      if (kTcSplitMma) {
-        // two issuers: a thread blocks in tcgen05.mma while the pipe's queue is full, so one thread
-        // issuing S(s + 2) cannot queue PV(s + 1) the moment P(s + 1) is ready.  S(s + 2) reuses the
-        // buffer PV(s) reads, so the S issuer waits for PV(s) to complete (not only to be issued);
-        // each issuer's commits track its own MMAs
-        if (warp == kTcMmaWarp) {
-          for (int s = 0; s < n_st; ++s) {
-            if (s >= 2) {
-              tc_wait(smem_u32(&pv_done[s & 1]), ((s - 2) >> 1) & 1, 9, s);
-              tc_fence_after();
-            }
-            issue_s(s);
-          }
-        } else {
-          for (int s = 0; s < n_st; ++s) issue_pv(s);
-        }
-      } else {
-        // two S stages ahead, then PV(s) and S(s + 2): the tensor pipe runs PV(s) and S(s + 2) while
-        // the softmax warps work on stage s + 1, whose S is already there
-        issue_s(0);
-        if (n_st > 1) issue_s(1);
-        for (int s = 0; s < n_st; ++s) {
-          issue_pv(s);
-          if (s + 2 < n_st) issue_s(s + 2);
-        }
+      // two S stages ahead, then PV(s) and S(s + 2): the tensor pipe runs PV(s) and S(s + 2) while
+      // the softmax warps work on stage s + 1, whose S is already there
+      issue_s(0);
+      if (n_st > 1) issue_s(1);
+      for (int s = 0; s < n_st; ++s) {
+        issue_pv(s);
+        if (s + 2 < n_st) issue_s(s + 2);
       }
     }
   } else {
@@ -669,13 +622,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 #pragma unroll
         for (int g8 = 0; g8 < 8; ++g8) {
           const int g = 8 * hi + g8;
-#if DECATTN_TC_EXP_WHATIF   // development timing experiment only: no exponential (wrong results)
-          const float pa0 = fmaf(sv[4 * g], p.scale_log2, nA), pa1 = fmaf(sv[4 * g + 1], p.scale_log2, nA);
-          const float pb0 = fmaf(sv[4 * g + 2], p.scale_log2, nB), pb1 = fmaf(sv[4 * g + 3], p.scale_log2, nB);
-#else
           const float pa0 = ex2(fmaf(sv[4 * g], p.scale_log2, nA)), pa1 = ex2(fmaf(sv[4 * g + 1], p.scale_log2, nA));
           const float pb0 = ex2(fmaf(sv[4 * g + 2], p.scale_log2, nB)), pb1 = ex2(fmaf(sv[4 * g + 3], p.scale_log2, nB));
-#endif
           if (g8 & 1) sA1 += pa0 + pa1, sB1 += pb0 + pb1;
           else sA0 += pa0 + pa1, sB0 += pb0 + pb1;
           tc_pair(pa0, pa1, hw[2 * g8], lw[2 * g8]);
