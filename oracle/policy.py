@@ -85,6 +85,17 @@ SM_STREAM_UNITS = 16  # efficiency region: cap to the one-wave cluster split whi
 SM_MID_T = 8          # efficiency region, <= 64 units (latency regime): at most 4 splits for T > 8,
 SM_MID_UNITS = 64
 SM_CLUSTER_CAP = 12   # at most 12 otherwise (clusters of 13..16 measured slower than 12)
+# wide query groups (round 2, profiles/r02zz4_wide_group_policy.log, 48 MQA shapes G = 32 / 64):
+# where the one-wave cluster fit leaves only a 2-CTA cluster split, the efficiency loop's split
+# runs on the tcgen05 kernel (64 query rows per CTA, workspace combine) and is faster, provided
+# each of its splits holds >= SM_TC_MIN_TILES 64-token tiles, its 64-row grid has >= U / 2 CTAs and
+# the sequence has >= SM_TC_UNITS units (B8 G64 L4096: 13.7 -> 9.9 us; B16 G32 L4096: 13.9 ->
+# 11.5 us; at 32 units, B16 G32 L2048, the 2-split mma.sync plan stays ahead)
+SM_TC_MIN_G = 32      # the tcgen05 kernel's group sizes (config.h kTcMinG)
+SM_TC_MIN_TILES = 4   # tiles per split it needs (config.h kTcMinTiles)
+SM_TC_ROWS = 64       # its query rows per CTA (config.h kTcRows)
+SM_TC_MAX_FIT = 2     # the cluster split it replaces: a 2-CTA cluster at most
+SM_TC_UNITS = 64
 # Clusters of s CTAs (one per split, s = 1..16) that are co-resident in one wave on a 148-SM
 # B200 with the cluster-combine kernel configuration: a HARDWARE MEASUREMENT, not a paper value -
 # the CUDA occupancy API's answer for the exact cluster kernels, recorded by
@@ -245,8 +256,11 @@ def seq_aware_sm_splits(geo: dict, l_k: int):
         e > f >= 2, 8-row CTAs and (n_u <= 16 f or 2 T_k f >= U) -> s = f
         else                                    -> e (streaming: returned as is)
         then, for short sequences (n_u <= 64): s = min(s, 4) if T_k > 8, and s = min(s, 12)
+        wide groups (round 2): G >= 32, s <= 2, n_u >= 64, n_u >= 4 e and
+          2 Batch H_KV ceil(G / 64) e >= U              -> e       (the tcgen05 kernel's split)
     The split count depends on the CTA groups T_k versus the usable SMs U through f, the largest
-    split whose clusters all fit one wave, not on a static L_K guard."""
+    split whose clusters all fit one wave, not on a static L_K guard.  The wide-group clause is a
+    launch-geometry statement about the packed layout (pack_gqa = 1, the default), like rows."""
     T, U, nblk = geo["T"], geo["U"], geo["nblk"]
     if saturated(T, U):
         return 1, RULE_SATURATED
@@ -271,6 +285,10 @@ def seq_aware_sm_splits(geo: dict, l_k: int):
         return e, RULE_EFF_LOOP
     if n_u <= SM_MID_UNITS:
         s = min(s, SM_MAX_SPLITS if Tk > SM_MID_T else SM_CLUSTER_CAP)
+    G = geo["G"]
+    if (G >= SM_TC_MIN_G and s <= SM_TC_MAX_FIT and n_u >= SM_TC_UNITS and n_u >= SM_TC_MIN_TILES * e
+            and 2 * (T // geo["num_m_blocks"]) * ceil_div(G, SM_TC_ROWS) * e >= U):
+        return e, RULE_EFF_LOOP
     return s, (RULE_EFF_LOOP if s == e else RULE_SM_FIT)
 
 

@@ -22,6 +22,9 @@ constexpr int kEvolvedSplits = 12, kEvolvedShortSplits = 16, kEvolvedShortLk = 2
 constexpr int kSmUnit = 64, kSmMinUnits = 5, kSmMinUnitsWide = 8, kSmWideT = 16, kSmMinSplits = 3;
 constexpr int kSmNarrowT = 4, kSmNarrowSplits = 8, kSmMaxSplits = 4;
 constexpr int kSmStreamUnits = 16, kSmMidT = 8, kSmMidUnits = 64, kSmClusterCap = 12;
+// wide groups: a <= 2-CTA cluster split gives way to the efficiency loop's split on the tcgen05
+// kernel (oracle/policy.py SM_TC_*; the kernel's own constants kTcMinG / kTcMinTiles / kTcRows)
+constexpr int kSmTcMaxFit = 2, kSmTcUnits = 64;
 constexpr int kDynMaxSplits = 128;   // DA_POLICY_DYNAMIC per-sequence cap (C-ext-2)
 constexpr int kVarlenMinUnits = 32;  // da_plan_make_varlen: dynamic only for splits >= 2048 tokens (C-ext-3)
 

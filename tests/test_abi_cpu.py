@@ -138,7 +138,8 @@ def test_plan_matches_oracle_wide_groups(L):
     # G > 8 at latency sizes: the policy's T_k and the launch's rows per CTA (8 within one wave
     # for <= 64 units, else 16) across the short / long boundary
     LKs = (64, 320, 512, 513, 1024, 2048, 4095, 4096, 4097, 4160, 4161, 8192, 65536)
-    for b, hkv, G in itertools.product((1, 2, 3, 8), (1, 2, 8), (12, 16, 32, 128)):
+    # (and G >= 32 where the one-wave cluster fit leaves a 2-CTA split: the tcgen05 clause, B = 16)
+    for b, hkv, G in itertools.product((1, 2, 3, 8, 16), (1, 2, 8), (12, 16, 32, 64, 128)):
         for lk in LKs:
             for pol in ("guarded", "seq_aware", "seq_aware_sm", "dynamic", "evolved"):
                 _check_plan(L, b, G * hkv, hkv, lk, 1, 0, 148, pol)

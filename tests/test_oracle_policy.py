@@ -318,6 +318,25 @@ def test_seq_aware_sm_structure():
         assert P.num_splits(1, 8 * hkv, hkv, 512, B200_SMS, 0, "seq_aware_sm")[0] >= 3
 
 
+def test_seq_aware_sm_wide_group_clause():
+    # C-ext-1's wide-group clause (round 2): where the one-wave cluster fit leaves a <= 2-CTA split
+    # for G >= 32, the efficiency loop's split runs on the tcgen05 kernel instead - the two
+    # measured wins of profiles/r02zz4_wide_group_policy.log ...
+    e = lambda b, hq, hkv, lk: P.efficiency_loop(P.geometry(b, hq, hkv, lk, B200_SMS, 0)["T"], B200_SMS,
+                                                  P.geometry(b, hq, hkv, lk, B200_SMS, 0)["nblk"])
+    assert P.num_splits(8, 64, 1, 4096, B200_SMS, 0, "seq_aware_sm") == (e(8, 64, 1, 4096), P.RULE_EFF_LOOP) == (16, 5)
+    assert P.num_splits(16, 32, 1, 4096, B200_SMS, 0, "seq_aware_sm") == (8, P.RULE_EFF_LOOP)
+    # ... and the shapes where the measured 2- / 4-split mma.sync plans stayed ahead keep them
+    assert P.num_splits(16, 32, 1, 2048, B200_SMS, 0, "seq_aware_sm") == (2, P.RULE_SM_FIT)   # 32 units
+    assert P.num_splits(8, 32, 1, 4096, B200_SMS, 0, "seq_aware_sm") == (4, P.RULE_SM_FIT)    # fit 4
+    # never for G < 32 (the mma.sync kernel's groups): G = 24 keeps its 2-CTA cluster split where
+    # G = 32 at the same shape takes the loop's 8
+    assert P.num_splits(16, 24, 1, 4096, B200_SMS, 0, "seq_aware_sm") == (2, P.RULE_SM_FIT)
+    # nor below 64 units (B8 G64 L2048 keeps s = 2), nor where the fit is > 2 (B4 G64 L4096: 4)
+    assert P.num_splits(8, 64, 1, 2048, B200_SMS, 0, "seq_aware_sm") == (2, P.RULE_SM_FIT)
+    assert P.num_splits(4, 64, 1, 4096, B200_SMS, 0, "seq_aware_sm") == (4, P.RULE_SM_FIT)
+
+
 def _measured_grid(tag="r01h"):
     import csv
     import os
