@@ -1058,11 +1058,13 @@ cudaError_t launch_impl(const da_plan& plan, const CUtensorMap& tk, const CUtens
   return FwdKernel<kPath, kNB, kCombine, kDyn, kPub, kBal, false>::launch(plan, tk, tv, p, stream);
 }
 
-// Tail balancing can engage in a cluster plan only when a sequence may span >= kBalMinTiles tiles
-// per split (dense cache): the cache capacity bounds every length
+// The balancing instantiation is launched when the plan's length gives every split >=
+// kBalMinTiles tiles (dense cache).  Either instantiation is exact for any length: the other one
+// only never balances, so a serving plan made for short sequences in a large cache keeps the lean
+// latency kernel even though its cache capacity would allow long ones
 inline bool balancing_possible(const da_plan& plan, const FwdParams& p) {
   return p.block_table == nullptr &&
-         (static_cast<int64_t>(p.l_cap) + kTileN - 1) / kTileN >= static_cast<int64_t>(kBalMinTiles) * plan.num_splits;
+         (static_cast<int64_t>(plan.l_k) + kTileN - 1) / kTileN >= static_cast<int64_t>(kBalMinTiles) * plan.num_splits;
 }
 
 template <int kPath, int kNB>
