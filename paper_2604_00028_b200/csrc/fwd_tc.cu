@@ -1,15 +1,16 @@
 // Split-KV decode-attention forward on the 5th-generation tensor cores (tcgen05 + TMEM) for wide
-// query groups: DA_PATH_TC, pack_gqa with G = H_Q / H_KV >= 32 (MQA / wide GQA) on streaming splits
-// (>= 16 tiles of 64 tokens each), SURVEY §8(a) steps a2-a7.  There the G query rows of a KV head
+// query groups: DA_PATH_TC, pack_gqa with G = H_Q / H_KV >= 32 (MQA / wide GQA) on splits of >= 4
+// tiles of 64 tokens with >= U / 2 CTAs (plan.cpp tc_path), SURVEY §8(a) steps a2-a7.  There the G query rows of a KV head
 // make a real dense contraction per KV tile, which the mma.sync path could only run as 16-row CTAs
 // that read every K / V tile ceil(G / 16) times and issue 96+ HMMAs per warp per tile (MQA G = 64
-// measured 2.6 TB/s there, 6.5 TB/s here).
+// measured 2.6 TB/s there, 6.6-6.8 TB/s here).
 //
 // One CTA = 64 query rows of one KV head (rows hq0 .. hq0 + 63; G < 64 padded with zero rows) x one
 // split x one batch entry; grid = (s, H_KV * ceil(G / 64), B) as on the other paths.  Stages of 128
-// tokens (two 64-token tiles): K and V as [half][128 tokens][64 dims], 128B-swizzled, 64 KB a stage.
-//   warp 8       TMA producer: one 5-D box per 64-token tile and 64-dim half, K and V on separate
-//                mbarriers (dense or paged cache); a split's last stage may hold one tile.
+// tokens (two 64-token tiles); K and V of a stage each [half][128 tokens][64 dims], 128B-swizzled,
+// 32 KB, in separate rings (2 K slots, freed when S(s) is computed; 5 V slots, freed when PV(s) is).
+//   warp 8       TMA producer: one 5-D box per 64-token tile and 64-dim half (dense or paged cache),
+//                issued K(0), K(1), then V(s), K(s + 2); a split's last stage may hold one tile.
 //   warp 9       TMEM allocator and MMA issuer (one lane), tcgen05.mma kind::f16 with A from TMEM:
 //                S(s) = Q K(s)^T at M = 64 rows, N = 128 tokens, K = 128 dims into TMEM buffer s & 1,
 //                then O += P(s) V(s) at M = 128, N = 128 dims, K = 128 tokens with the pair
@@ -21,7 +22,8 @@
 //                scripts/microbench_tcgen05_rows.cu); the 16-lane TMEM shapes give thread t rows
 //                16 q + t / 4 and + 8 (q = w mod 4), the 4 threads of a row reduce with shuffles,
 //                and warps q, q + 4 take the two 64-token halves of a stage (row maxima exchanged
-//                through shared memory).  (DECATTN_TC_SMX_WARPS = 4: warps 0-3 take both halves.)  Online softmax in fp32 / log2 units; P = exp2(S - m) as the bf16
+//                through shared memory; DECATTN_TC_SMX_WARPS = 4: warps 0-3 take both halves).
+//                Online softmax in fp32 / log2 units; P = exp2(S - m) as the bf16
 //                pair P_hi + P_lo (the precision of fwd.cu's PV) written over S.  The
 //                running maximum m is a reference that moves only when a stage's maximum exceeds it
 //                by more than 8 (log2 units); then the O rows are rescaled in TMEM (tcgen05.ld /
@@ -30,7 +32,7 @@
 //   epilogue     O = the hi lanes' part + the lo lanes' part, / l: out + lse (s = 1, NONE) or the
 //                normalised fp32 partial + lse (s > 1, KERNEL; merged by lse_combine_kernel).
 // Programmatic dependent launch as in fwd.cu: the prologue (barriers, TMEM allocation, tensor-map
-// prefetch, L2 prefetch of the first ring tiles) overlaps the previous kernel.
+// prefetch, L2 prefetch of the CTA's Q rows and of the first ring tiles) overlaps the previous kernel.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
