@@ -294,9 +294,9 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   __shared__ __align__(8) uint64_t emptyk_bar[NK];  // S(s) done: slot free (tcgen05.commit)
   __shared__ __align__(8) uint64_t fullv_bar[NV];   // V(s) has landed in slot s % NV
   __shared__ __align__(8) uint64_t emptyv_bar[NV];  // PV(s) done: slot free (tcgen05.commit)
-  __shared__ __align__(8) uint64_t q_bar;           // Q is in TMEM (128 softmax threads)
+  __shared__ __align__(8) uint64_t q_bar;           // Q is in TMEM (every softmax thread)
   __shared__ __align__(8) uint64_t s_full[2];       // S(s) in TMEM buffer s & 1 (commit)
-  __shared__ __align__(8) uint64_t p_full[2];       // P(s) written over S(s) (4 warps)
+  __shared__ __align__(8) uint64_t p_full[2];       // P(s) written over S(s) (every softmax warp)
   __shared__ __align__(8) uint64_t pv_done[2];      // O += P(s) V(s) done for s & 1 == b (commit)
   __shared__ uint32_t tmem_base;
   __shared__ float red_x[2][2][kTcM];               // [stage parity][token half] row maxima (8 warps)
