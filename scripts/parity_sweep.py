@@ -45,6 +45,9 @@ if __name__ == "__main__":
             # the tcgen05 kernel forced on a fifth of the packed static plans (any G >= 2; the
             # planner alone picks it only for wide groups on long enough splits)
             path = 2 if (pack and G >= 2 and policy != "dynamic" and comb != 1 and rng.random() < 0.2) else None
+            if comb == 1 and dec.make_plan(b, G * hkv, hkv, lk, pack_gqa=pack, policy=policy, forced_splits=forced,
+                                           path=path).path == dec.DA_PATH_TC:
+                comb = 2          # the tcgen05 kernel has no cluster combine (da_plan_set_combine rejects it)
             plan = dec.make_plan(b, G * hkv, hkv, lk, pack_gqa=pack, policy=policy, forced_splits=forced,
                                  combine_mode=comb, seq_offset=offset, path=path)
             seq_arg = inp["seqlens"]
