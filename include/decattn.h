@@ -143,7 +143,7 @@ typedef enum da_path {
   DA_PATH_MMA = 1,     /* pack_gqa with G >= 2: the G query rows of a KV head
                           share each K/V tile; QK^T and PV on tensor cores
                           (mma.sync, 8 or 16 rows per CTA)                     */
-  DA_PATH_TC = 2       /* pack_gqa with G >= 32 (MQA / wide GQA) and a static
+  DA_PATH_TC = 2       /* pack_gqa with G > 16 (MQA / wide GQA) and a static
                           split count: 64 query rows per CTA on tcgen05 (TMEM
                           accumulators); combine NONE (s == 1) or KERNEL     */
 } da_path;
@@ -255,7 +255,7 @@ DA_API da_status da_plan_set_seq_offset(da_plan* plan, int32_t seq_offset);
  * da_plan_set_path - force the kernel of a pack_gqa plan with G >= 2 and re-derive its launch
  * fields: DA_PATH_MMA (mma.sync, 8 / 16 rows per CTA) or DA_PATH_TC (tcgen05, 64 rows per CTA; static
  * split counts only, never a cluster combine: a CLUSTER plan becomes KERNEL); -1 restores the
- * planner's choice.  The planner's own rule: DA_PATH_TC when G >= 32, every split
+ * planner's choice.  The planner's own rule: DA_PATH_TC when G > 16, every split
  * holds >= 4 tiles of 64 tokens and the tcgen05 grid has >= U / 2 CTAs.  Errors: DA_ERR_INVALID_ARG
  * (scalar plans, dynamic plans asked for DA_PATH_TC, unknown paths).  Pure host code.
  */

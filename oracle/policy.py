@@ -91,7 +91,7 @@ SM_CLUSTER_CAP = 12   # at most 12 otherwise (clusters of 13..16 measured slower
 # each of its splits holds >= SM_TC_MIN_TILES 64-token tiles, its 64-row grid has >= U / 2 CTAs and
 # the sequence has >= SM_TC_UNITS units (B8 G64 L4096: 13.7 -> 9.9 us; B16 G32 L4096: 13.9 ->
 # 11.5 us; at 32 units, B16 G32 L2048, the 2-split mma.sync plan stays ahead)
-SM_TC_MIN_G = 32      # the tcgen05 kernel's group sizes (config.h kTcMinG)
+SM_TC_MIN_G = 32      # the clause's group sizes (calibrated on G = 32 / 64; config.h kSmTcMinG)
 SM_TC_MIN_TILES = 4   # tiles per split it needs (config.h kTcMinTiles)
 SM_TC_ROWS = 64       # its query rows per CTA (config.h kTcRows)
 SM_TC_MAX_FIT = 2     # the cluster split it replaces: a 2-CTA cluster at most

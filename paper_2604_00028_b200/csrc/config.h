@@ -24,7 +24,7 @@ constexpr int kSmNarrowT = 4, kSmNarrowSplits = 8, kSmMaxSplits = 4;
 constexpr int kSmStreamUnits = 16, kSmMidT = 8, kSmMidUnits = 64, kSmClusterCap = 12;
 // wide groups: a <= 2-CTA cluster split gives way to the efficiency loop's split on the tcgen05
 // kernel (oracle/policy.py SM_TC_*; the kernel's own constants kTcMinG / kTcMinTiles / kTcRows)
-constexpr int kSmTcMaxFit = 2, kSmTcUnits = 64;
+constexpr int kSmTcMinG = 32, kSmTcMaxFit = 2, kSmTcUnits = 64;   // (calibrated on G = 32 / 64)
 constexpr int kDynMaxSplits = 128;   // DA_POLICY_DYNAMIC per-sequence cap (C-ext-2)
 constexpr int kVarlenMinUnits = 32;  // da_plan_make_varlen: dynamic only for splits >= 2048 tokens (C-ext-3)
 
@@ -102,7 +102,7 @@ constexpr int kBalMinTiles = DECATTN_BAL_MIN_TILES, kBalTailDiv = DECATTN_BAL_TA
 #define DECATTN_TC_VSLOTS 5       // tcgen05 path: V ring slots of 128 tokens (32 KB)
 #endif
 #ifndef DECATTN_TC_MIN_G
-#define DECATTN_TC_MIN_G 32
+#define DECATTN_TC_MIN_G 17       // G > 16: the mma.sync kernel's 16-row CTAs would read K / V twice or more
 #endif
 #ifndef DECATTN_TC_MIN_TILES
 #define DECATTN_TC_MIN_TILES 4    // 64-token tiles per split at the plan's length (and >= U / 2 CTAs)

@@ -1,5 +1,5 @@
 // Split-KV decode-attention forward on the 5th-generation tensor cores (tcgen05 + TMEM) for wide
-// query groups: DA_PATH_TC, pack_gqa with G = H_Q / H_KV >= 32 (MQA / wide GQA) on splits of >= 4
+// query groups: DA_PATH_TC, pack_gqa with G = H_Q / H_KV > 16 (MQA / wide GQA) on splits of >= 4
 // tiles of 64 tokens with >= U / 2 CTAs (plan.cpp tc_path), SURVEY §8(a) steps a2-a7.  There the G query rows of a KV head
 // make a real dense contraction per KV tile, which the mma.sync path could only run as 16-row CTAs
 // that read every K / V tile ceil(G / 16) times and issue 96+ HMMAs per warp per tile (MQA G = 64

@@ -46,10 +46,10 @@ def test_plan_struct_layout(L):
 
 
 def _tc(b, hq, hkv, lk, pack, s, U, dynamic=False):
-    # the planner's kernel choice: tcgen05 for G >= 32 when every split holds >= 4
+    # the planner's kernel choice: tcgen05 for G > 16 when every split holds >= 4
     # tiles and the 64-row grid has >= U / 2 CTAs (static plans)
     G = hq // hkv
-    return bool(pack) and G >= 32 and not dynamic and -(-lk // 64) >= 4 * s and 2 * b * hkv * -(-G // 64) * s >= U
+    return bool(pack) and G >= 17 and not dynamic and -(-lk // 64) >= 4 * s and 2 * b * hkv * -(-G // 64) * s >= U
 
 
 def _expected_launch(b, hq, hkv, lk, pack, s, U, dynamic=False):
