@@ -1,9 +1,9 @@
 // Split-KV decode-attention forward on the 5th-generation tensor cores (tcgen05 + TMEM) for wide
 // query groups: DA_PATH_TC, pack_gqa with G = H_Q / H_KV > 16 (MQA / wide GQA) on splits of >= 4
-// tiles of 64 tokens with >= U / 2 CTAs (plan.cpp tc_path), SURVEY §8(a) steps a2-a7.  There the G query rows of a KV head
-// make a real dense contraction per KV tile, which the mma.sync path could only run as 16-row CTAs
-// that read every K / V tile ceil(G / 16) times and issue 96+ HMMAs per warp per tile (MQA G = 64
-// measured 2.6 TB/s there, 6.6-6.8 TB/s here).
+// tiles of 64 tokens with >= U / 2 CTAs (plan.cpp tc_path), SURVEY §8(a) steps a2-a7.  There the G
+// query rows of a KV head make a real dense contraction per KV tile, which the mma.sync path could
+// only run as 16-row CTAs that read every K / V tile ceil(G / 16) times and issue 96+ HMMAs per warp
+// per tile (MQA G = 64 measured 2.6 TB/s there, 6.6-6.8 TB/s here).
 //
 // One CTA = 64 query rows of one KV head (rows hq0 .. hq0 + 63; G < 64 padded with zero rows) x one
 // split x one batch entry; grid = (s, H_KV * ceil(G / 64), B) as on the other paths.  Stages of 128
