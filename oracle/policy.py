@@ -85,13 +85,14 @@ SM_STREAM_UNITS = 16  # efficiency region: cap to the one-wave cluster split whi
 SM_MID_T = 8          # efficiency region, <= 64 units (latency regime): at most 4 splits for T > 8,
 SM_MID_UNITS = 64
 SM_CLUSTER_CAP = 12   # at most 12 otherwise (clusters of 13..16 measured slower than 12)
-# wide query groups (round 2, profiles/r02zz4_wide_group_policy.log, 48 MQA shapes G = 32 / 64):
+# wide query groups (round 2, profiles/r02zz4_wide_group_policy.log, 48 MQA shapes G = 32 / 64, and
+# r02zz33_g17_31_policy.log, G = 20 / 24 / 28 at L_K = 4096, where the same B16 loss appears):
 # where the one-wave cluster fit leaves only a 2-CTA cluster split, the efficiency loop's split
 # runs on the tcgen05 kernel (64 query rows per CTA, workspace combine) and is faster, provided
 # each of its splits holds >= SM_TC_MIN_TILES 64-token tiles, its 64-row grid has >= U / 2 CTAs and
 # the sequence has >= SM_TC_UNITS units (B8 G64 L4096: 13.7 -> 9.9 us; B16 G32 L4096: 13.9 ->
 # 11.5 us; at 32 units, B16 G32 L2048, the 2-split mma.sync plan stays ahead)
-SM_TC_MIN_G = 32      # the clause's group sizes (calibrated on G = 32 / 64; config.h kSmTcMinG)
+SM_TC_MIN_G = 17      # the tcgen05 kernel's group sizes (config.h kTcMinG: G > 16)
 SM_TC_MIN_TILES = 4   # tiles per split it needs (config.h kTcMinTiles)
 SM_TC_ROWS = 64       # its query rows per CTA (config.h kTcRows)
 SM_TC_MAX_FIT = 2     # the cluster split it replaces: a 2-CTA cluster at most
@@ -256,7 +257,7 @@ def seq_aware_sm_splits(geo: dict, l_k: int):
         e > f >= 2, 8-row CTAs and (n_u <= 16 f or 2 T_k f >= U) -> s = f
         else                                    -> e (streaming: returned as is)
         then, for short sequences (n_u <= 64): s = min(s, 4) if T_k > 8, and s = min(s, 12)
-        wide groups (round 2): G >= 32, s <= 2, n_u >= 64, n_u >= 4 e and
+        wide groups (round 2): G > 16, s <= 2, n_u >= 64, n_u >= 4 e and
           2 Batch H_KV ceil(G / 64) e >= U              -> e       (the tcgen05 kernel's split)
     The split count depends on the CTA groups T_k versus the usable SMs U through f, the largest
     split whose clusters all fit one wave, not on a static L_K guard.  The wide-group clause is a

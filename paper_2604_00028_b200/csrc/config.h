@@ -24,7 +24,7 @@ constexpr int kSmNarrowT = 4, kSmNarrowSplits = 8, kSmMaxSplits = 4;
 constexpr int kSmStreamUnits = 16, kSmMidT = 8, kSmMidUnits = 64, kSmClusterCap = 12;
 // wide groups: a <= 2-CTA cluster split gives way to the efficiency loop's split on the tcgen05
 // kernel (oracle/policy.py SM_TC_*; the kernel's own constants kTcMinG / kTcMinTiles / kTcRows)
-constexpr int kSmTcMinG = 32, kSmTcMaxFit = 2, kSmTcUnits = 64;   // (calibrated on G = 32 / 64)
+constexpr int kSmTcMaxFit = 2, kSmTcUnits = 64;
 constexpr int kDynMaxSplits = 128;   // DA_POLICY_DYNAMIC per-sequence cap (C-ext-2)
 constexpr int kVarlenMinUnits = 32;  // da_plan_make_varlen: dynamic only for splits >= 2048 tokens (C-ext-3)
 

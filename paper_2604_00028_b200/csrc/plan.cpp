@@ -119,7 +119,7 @@ void decide(int64_t batch, int64_t l_k, int64_t T, int64_t U, int64_t nblk, int6
     }
     // wide groups: a <= 2-CTA cluster split gives way to the loop's split on the tcgen05 kernel
     // when that kernel's rule (tc_path) accepts it and the sequence has >= kSmTcUnits units
-    if (G >= kSmTcMinG && v <= kSmTcMaxFit && n_u >= kSmTcUnits && n_u >= static_cast<int64_t>(kTcMinTiles) * e &&
+    if (G >= kTcMinG && v <= kSmTcMaxFit && n_u >= kSmTcUnits && n_u >= static_cast<int64_t>(kTcMinTiles) * e &&
         2 * (T / mblocks) * ceil_div(G, static_cast<int64_t>(kTcRows)) * e >= U) {
       *s = static_cast<int>(e);
       *rule = DA_RULE_EFF_LOOP;

@@ -329,9 +329,12 @@ def test_seq_aware_sm_wide_group_clause():
     # ... and the shapes where the measured 2- / 4-split mma.sync plans stayed ahead keep them
     assert P.num_splits(16, 32, 1, 2048, B200_SMS, 0, "seq_aware_sm") == (2, P.RULE_SM_FIT)   # 32 units
     assert P.num_splits(8, 32, 1, 4096, B200_SMS, 0, "seq_aware_sm") == (4, P.RULE_SM_FIT)    # fit 4
-    # never for G < 32 (the mma.sync kernel's groups): G = 24 keeps its 2-CTA cluster split where
-    # G = 32 at the same shape takes the loop's 8
-    assert P.num_splits(16, 24, 1, 4096, B200_SMS, 0, "seq_aware_sm") == (2, P.RULE_SM_FIT)
+    # the same loss for 16 < G < 32 (profiles/r02zz33_g17_31_policy.log: B16 L4096 s = 2 mma.sync
+    # 13.6 us against the loop's s = 8 on tcgen05 11.0 us) ...
+    assert P.num_splits(16, 24, 1, 4096, B200_SMS, 0, "seq_aware_sm") == (8, P.RULE_EFF_LOOP)
+    assert P.num_splits(16, 20, 1, 4096, B200_SMS, 0, "seq_aware_sm") == (8, P.RULE_EFF_LOOP)
+    # ... never for G <= 16 (one 16-row mma.sync CTA per KV head: the tcgen05 kernel is not used)
+    assert P.num_splits(16, 16, 1, 4096, B200_SMS, 0, "seq_aware_sm") == (4, P.RULE_SM_FIT)
     # nor below 64 units (B8 G64 L2048 keeps s = 2), nor where the fit is > 2 (B4 G64 L4096: 4)
     assert P.num_splits(8, 64, 1, 2048, B200_SMS, 0, "seq_aware_sm") == (2, P.RULE_SM_FIT)
     assert P.num_splits(4, 64, 1, 4096, B200_SMS, 0, "seq_aware_sm") == (4, P.RULE_SM_FIT)
