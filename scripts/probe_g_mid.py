@@ -33,3 +33,14 @@ def grid():
 
 if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "grid":
     grid()
+
+
+if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "small":
+    # 8 < G <= 16: one 16-row mma.sync CTA per KV head on long splits (two 8-row CTAs on short ones)
+    for g, hkv in ((12, 1), (16, 1), (16, 2)):
+        for b in (4, 16, 64, 128):
+            for lk in (2048, 8192, 32768):
+                if b * hkv * lk * 512 > (1 << 30):
+                    continue
+                bench(b, g * hkv, hkv, lk, "seq_aware", steps=20, reps=5)
+                bench(b, g * hkv, hkv, lk, "seq_aware", steps=20, reps=5, path=2)
