@@ -604,6 +604,19 @@ def test_tc_path_edges(pack):
     assert (plan.num_splits, plan.path) == (1, dec.DA_PATH_TC)
 
 
+@pytest.mark.parametrize("batch,h_q,h_kv,l_k,policy,path", [
+    (16, 24, 1, 4096, "seq_aware_sm", 2),   # G = 24: C-ext-1's wide-group clause, s = 8 on tcgen05
+    (8, 40, 2, 8192, "guarded", 2),         # G = 20, two KV heads
+    (4, 28, 1, 16384, "seq_aware", 2),      # G = 28, s = 32
+    (16, 12, 1, 8192, "seq_aware", 1),      # G = 12 stays on mma.sync (one 16-row CTA per head)
+])
+def test_planner_picks_tcgen05_for_groups_above_16(batch, h_q, h_kv, l_k, policy, path):
+    # 16 < G < 32: the mma.sync kernel would read K / V twice (two 16-row CTAs per KV head), so the
+    # planner's own rule takes the tcgen05 kernel (kernel choice); ragged lengths
+    plan, _, _ = run_and_check(batch, h_q, h_kv, l_k, policy=policy, variant="ragged", seed=1720)
+    assert plan.path == path
+
+
 def test_tc_path_rescales_when_the_maximum_grows():
     # scores that climb by ~16 (log2 units) every 64-token tile: the running reference moves and
     # the O rows in TMEM are rescaled on every tile (the path that is rare on N(0, 1) inputs)
